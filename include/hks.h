@@ -1,0 +1,197 @@
+/*
+ * hks.h -- C ABI of libhks: CKKS hybrid key switching on NVIDIA B200 (sm_100a).
+ *
+ * The boundary follows the paper's statement of the problem (FIDESlib, arXiv 2507.04775,
+ * /root/reference/PAPER.md): a Context built once from (N, the Q chain, the special primes P,
+ * dnum) with all precomputation (§3.5), polynomials resident in GPU memory
+ * (§3.2), and the server-side key-switching steps of §3.6.3-§3.6.6.
+ * The operation list is SURVEY.md §8(b).
+ *
+ * Conventions (all entry points)
+ *   Buffers   Every polynomial buffer is caller-owned CUDA device memory on the context's device,
+ *             u64 little-endian, limb-major [limbs][N], residues canonical in [0, m) for the limb's
+ *             prime m.  The library never allocates on a hot-path call; the caller sizes the
+ *             workspace with hks_workspace_bytes().  evk buffers are borrowed for the call.
+ *   Forms     EVAL = bit-reversed evaluation order: x[j] = a(psi^(2*brv(j)+1)) (PAPER.md:341:
+ *             NTT output is bit-reversed, iNTT takes bit-reversed and returns natural order).
+ *             COEFF = natural coefficient order.  psi = the minimal primitive 2N-th root of unity
+ *             modulo each prime (SURVEY.md §8(c) reading 1; query it with hks_ctx_psi()).
+ *   Primes    Prime index space: 0..num_q-1 = q_0..q_L, num_q..num_q+num_p-1 = p_0..p_{K-1}.
+ *             Extended limb order at level l: Q_0..Q_l, P_0..P_{K-1}.  Key limb index of P_k is
+ *             L+1+k.  Digit j = chain limbs [j*alpha, min((j+1)*alpha, l+1)), alpha =
+ *             ceil((L+1)/dnum), beta(l) = ceil((l+1)/alpha) (§2.1).
+ *   Keys      evk layout [dnum][2][L+1+K][N]: evk[j][0] = b_j, evk[j][1] = a_j, EVAL.
+ *   Streams   Every compute call is enqueued on `stream` (a cudaStream_t passed as void*; NULL =
+ *             legacy default stream).  Argument errors return synchronously before any launch;
+ *             launch failures return HKS_ECUDA; asynchronous device faults surface on the
+ *             caller's next synchronisation.
+ *   Aliasing  In place is allowed only for hks_ntt_fwd / hks_ntt_inv.  All other outputs must not
+ *             overlap inputs (HKS_EINVAL when detectable from pointer ranges).
+ *   Errors    Status codes only; no exception crosses the ABI.  hks_last_error() returns a
+ *             thread-local description of the last non-OK status on the calling thread.
+ *   Threads   A context is immutable after creation and may be used concurrently from several
+ *             host threads / streams, each with its own workspace.
+ */
+#ifndef HKS_H
+#define HKS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hks_ctx hks_ctx;
+
+typedef enum {
+    HKS_OK = 0,
+    HKS_EINVAL = 1,     /* bad argument: NULL, size, level > L, aliasing, nlimbs = 0 ... */
+    HKS_ENOTPRIME = 2,  /* a modulus is not prime */
+    HKS_ENOTNTT = 3,    /* a modulus is not 1 mod 2N */
+    HKS_ERANGE = 4,     /* modulus >= 2^60, log_n outside [10, 17], dnum outside [1, L+1] */
+    HKS_EDUP = 5,       /* a modulus appears twice in q || p */
+    HKS_EKEY = 6,       /* evaluation key has fewer digits than beta(level) */
+    HKS_EGALOIS = 7,    /* Galois element even or >= 2N */
+    HKS_ECUDA = 8,      /* a CUDA runtime call or kernel launch failed */
+    HKS_ENOMEM = 9,     /* device table allocation failed at context creation */
+    HKS_EDEVICE = 10    /* host-only context (device < 0) used for compute, or wrong device */
+} hks_status;
+
+/* Operation selector for hks_workspace_bytes(). */
+typedef enum {
+    HKS_OP_MODUP = 0,           /* hks_modup */
+    HKS_OP_MODDOWN = 1,         /* hks_moddown */
+    HKS_OP_KEYSWITCH = 2,       /* hks_keyswitch */
+    HKS_OP_ROTATE_HOISTED = 3   /* hks_rotate_hoisted (count = nrot, not needed for sizing) */
+} hks_op;
+
+#define HKS_MAX_DIGITS 64
+
+typedef struct hks_info {
+    uint32_t log_n, n;          /* ring degree N = 2^log_n */
+    uint32_t num_q, num_p;      /* L+1 and K */
+    uint32_t dnum, alpha;       /* digits in the key, limbs per digit */
+    uint32_t level, beta;       /* the queried level and its active digit count */
+    uint32_t digit_lo[HKS_MAX_DIGITS], digit_hi[HKS_MAX_DIGITS];  /* digit j = [lo, hi) at `level` */
+    int32_t device;             /* CUDA device ordinal, -1 for a host-only context */
+} hks_info;
+
+/* Thread-local text for the last non-OK status returned on this thread ("" if none). */
+const char *hks_last_error(void);
+
+/* Context creation (§3.5 precomputation; SPEC.md:297-305 create_context).
+ *   log_n   10..17;  q[num_q] the chain q_0..q_L;  p[num_p] the special primes (K >= 1, any K:
+ *           SURVEY.md §8(c) reading 15b);  dnum in [1, num_q].
+ *   Every modulus must be prime, < 2^60, = 1 mod 2N, and all must be distinct.
+ *   device  CUDA ordinal that will own the tables; -1 builds a host-only context that supports
+ *           hks_ctx_query / hks_ctx_psi / hks_workspace_bytes only (compute calls: HKS_EDEVICE).
+ *   *out    receives the context (owned by the caller, release with hks_ctx_destroy).
+ * Builds, per prime: psi, forward/inverse twiddles with Shoup companions, N^-1; per (level,
+ * digit): the Eq. 1 ModUp constants; the ModDown constants; then uploads them (device >= 0). */
+hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t num_q, const uint64_t *p,
+                          uint32_t num_p, uint32_t dnum, int device, hks_ctx **out);
+
+/* Releases the context and its device tables.  NULL is ignored.  No call may be in flight. */
+void hks_ctx_destroy(hks_ctx *ctx);
+
+/* Structural query at `level` (0..L): N, L+1, K, dnum, alpha, beta(level), digit ranges. */
+hks_status hks_ctx_query(const hks_ctx *ctx, uint32_t level, hks_info *out);
+
+/* psi of prime `prime_idx` (the minimal primitive 2N-th root; SURVEY.md §8(c) reading 1). */
+hks_status hks_ctx_psi(const hks_ctx *ctx, uint32_t prime_idx, uint64_t *psi);
+
+/* Bytes of device workspace `op` needs at `level` (0 if the op needs none). */
+size_t hks_workspace_bytes(const hks_ctx *ctx, hks_op op, uint32_t level, uint32_t count);
+
+/* Batched forward negacyclic NTT, in place (§3.6.4).
+ *   x          [nlimbs][N] COEFF in, EVAL out (in place).
+ *   prime_idx  host array [nlimbs]: limb b is reduced modulo prime prime_idx[b].
+ * Output canonical.  Inputs must be canonical. */
+hks_status hks_ntt_fwd(const hks_ctx *ctx, uint64_t *x, const uint32_t *prime_idx, uint32_t nlimbs,
+                       void *stream);
+
+/* Batched inverse NTT, in place, including N^-1 (§3.6.4). */
+hks_status hks_ntt_inv(const hks_ctx *ctx, uint64_t *x, const uint32_t *prime_idx, uint32_t nlimbs,
+                       void *stream);
+
+/* Fast base conversion, Eq. 1 (§3.6.3):
+ *   out_t = [ sum_i [x_i * qhat_i^-1]_{q_i} * [qhat_i]_t ]_t ,  qhat_i = prod_{m in src, m != i} m
+ *   x       [nsrc][N] COEFF, limb i modulo prime src_idx[i];  out [ndst][N] COEFF.
+ *   src_idx / dst_idx are host arrays of prime indices; nsrc <= 16, ndst <= 128, src and dst
+ *   disjoint.  The result is the unique Eq. 1 value with canonical y_i (SURVEY.md reading 16). */
+hks_status hks_bconv(const hks_ctx *ctx, const uint64_t *x, const uint32_t *src_idx, uint32_t nsrc,
+                     const uint32_t *dst_idx, uint32_t ndst, uint64_t *out, void *stream);
+
+/* ModUp (§3.6.3): digit decomposition + BConv + NTT.
+ *   d    [l+1][N] EVAL at `level` = l.
+ *   ext  [beta][l+1+K][N] EVAL: ext[j][t] = d[t] for t in digit j, otherwise
+ *        NTT(BConv_{digit j -> t}(INTT(d[digit j]))).
+ *   ws   hks_workspace_bytes(ctx, HKS_OP_MODUP, level, 0) bytes of device memory. */
+hks_status hks_modup(const hks_ctx *ctx, const uint64_t *d, uint32_t level, uint64_t *ext, void *ws,
+                     void *stream);
+
+/* Evaluation-key inner product (§3.6.5 dot-product fusion):
+ *   acc[0][t] = sum_{j<beta} D_j[t] * b_j[key(t)],  acc[1][t] = sum_j D_j[t] * a_j[key(t)]  (mod t)
+ *   ext     [beta][l+1+K][N] EVAL (hks_modup output).  evk [dnum][2][L+1+K][N], dnum >= beta.
+ *   galois  1 for none; otherwise odd k < 2N and D_j is replaced by its automorphism pi_k
+ *           (EVAL permutation, hoisted order; SURVEY.md readings 14-15).
+ *   acc     [2][l+1+K][N] EVAL. */
+hks_status hks_ksk_inner_product(const hks_ctx *ctx, const uint64_t *ext, const uint64_t *evk,
+                                 uint32_t level, uint64_t galois, uint64_t *acc, void *stream);
+
+/* ModDown (§3.6.5 "P^-1(x - NTT(x'))"):
+ *   acc [l+1+K][N] EVAL -> out [l+1][N] EVAL,
+ *   out_i = (acc_i - NTT(BConv_{P -> q_i}(INTT(acc_P)))_i) * P^-1 mod q_i.
+ *   ws   hks_workspace_bytes(ctx, HKS_OP_MODDOWN, level, 0) bytes. */
+hks_status hks_moddown(const hks_ctx *ctx, const uint64_t *acc, uint32_t level, uint64_t *out, void *ws,
+                       void *stream);
+
+/* Hybrid KeySwitch of ct = (c0, c1) at `level`:
+ *   out0 = c0 + ModDown(acc0), out1 = ModDown(acc1), acc = KIP(ModUp(c1), evk).
+ *   Relinearisation of (d0, d1, d2): call with (c0, c1) = (0-or-d0, d2) and add d1 to out1.
+ *   c0 may be NULL (then out0 = ModDown(acc0)).  c0, c1, out0, out1: [l+1][N] EVAL.
+ *   evk [dnum][2][L+1+K][N]; dnum (the key's digit count) >= beta(level) is implied by the ctx.
+ *   ws   hks_workspace_bytes(ctx, HKS_OP_KEYSWITCH, level, 0) bytes. */
+hks_status hks_keyswitch(const hks_ctx *ctx, const uint64_t *c0, const uint64_t *c1, uint32_t level,
+                         const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws, void *stream);
+
+/* EVAL-form automorphism X -> X^galois on nlimbs limbs (prime-independent permutation,
+ * SPEC.md:244-252; SURVEY.md reading 15):  out[l][j] = in[l][j'], 2brv(j')+1 = k(2brv(j)+1) mod 2N.
+ * in != out required. */
+hks_status hks_automorph(const hks_ctx *ctx, const uint64_t *in, uint32_t nlimbs, uint64_t galois,
+                         uint64_t *out, void *stream);
+
+/* Hoisted rotations (§3.6.6): one ModUp of c1 shared by nrot rotations.
+ *   galois[r], evk[r], out0[r], out1[r]: host arrays of length nrot (device pointers inside).
+ *   out0[r] = pi_k(c0) + ModDown(acc0_r), out1[r] = ModDown(acc1_r), acc_r = KIP(ext, evk[r], k_r).
+ *   ws   hks_workspace_bytes(ctx, HKS_OP_ROTATE_HOISTED, level, nrot) bytes. */
+hks_status hks_rotate_hoisted(const hks_ctx *ctx, const uint64_t *c0, const uint64_t *c1, uint32_t level,
+                              uint32_t nrot, const uint64_t *galois, const uint64_t *const *evk,
+                              uint64_t *const *out0, uint64_t *const *out1, void *ws, void *stream);
+
+
+/* ---- diagnostics (bench.py evidence; not part of the key-switching math) ---------------------
+ * hks_launch_count: number of kernels this library has launched in this process (all contexts).
+ * hks_prof_enable(1): from now on every kernel launch is bracketed by a CUDA event pair recorded on
+ *   the launch's stream, tagged with its kernel class and its algorithmic bytes (limb words read and
+ *   written, excluding twiddle/constant tables).  hks_prof_enable(0) stops recording.
+ * hks_prof_read: synchronises the recorded events and returns, per kernel class, the launch count,
+ *   the summed device time (ms) and the summed algorithmic bytes; clears the record.  Returns the
+ *   number of classes written (<= max). */
+typedef struct hks_prof_entry {
+    char name[32];
+    uint64_t launches;
+    double total_ms;
+    double bytes;
+} hks_prof_entry;
+
+uint64_t hks_launch_count(void);
+hks_status hks_prof_enable(int on);
+int hks_prof_read(hks_prof_entry *out, int max);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HKS_H */

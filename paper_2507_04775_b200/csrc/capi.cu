@@ -1,0 +1,408 @@
+// capi.cu -- the extern "C" entry points of include/hks.h and the key-switching orchestration.
+//
+// KeySwitch at level l (§2.1, 287-322 §3.6.3, 343-352 §3.6.5):
+//   1. INTT(c1) with the Eq. 1 scale N^-1 [qhat_{j,i}]^-1 fused into the last pass   -> y (canonical)
+//   2. BConv per digit j: y[digit j] -> every other extended limb                    (COEFF)
+//   3. NTT of the beta(l+1+K) - (l+1) new limbs                                       (EVAL)
+//   4. key inner product (own-digit limbs read straight from c1, EVAL)               -> acc0, acc1
+//   5. ModDown of both: INTT(acc_P) with N^-1 [phat_k]^-1 fused, BConv P -> Q_l, NTT with the fused
+//      epilogue out = (acc - NTT(conv)) P^-1 (+ c0)
+// All launches go to the caller's stream; the workspace is caller-owned.
+#include <string.h>
+
+#include <algorithm>
+
+#include "internal.h"
+
+namespace {
+
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    ~DevGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+hks_status check_ctx(const hks_ctx *c) {
+    if (!c) HKS_FAIL(HKS_EINVAL, "NULL context");
+    if (c->device < 0) HKS_FAIL(HKS_EDEVICE, "host-only context cannot run device operations");
+    return HKS_OK;
+}
+
+bool overlap(const void *a, size_t na, const void *b, size_t nb) {
+    if (!a || !b || !na || !nb) return false;
+    const char *x = (const char *)a, *y = (const char *)b;
+    return x < y + nb && y < x + na;
+}
+
+size_t limb_bytes(const hks_ctx *c) { return (size_t)c->n * sizeof(u64); }
+
+// Launch BConv groups, batching up to BC_MAXG groups with equal nsrc per launch.
+hks_status run_bconv_groups(const hks_ctx *c, std::vector<BconvGroup> &groups, const u64 *in, u64 *out,
+                            cudaStream_t s) {
+    size_t i = 0;
+    while (i < groups.size()) {
+        BconvArgs a{};
+        a.in = in;
+        a.out = out;
+        a.pc = c->d_pc;
+        a.log_n = c->log_n;
+        a.prescale = 0;
+        u32 ns = groups[i].nsrc, k = 0;
+        while (i < groups.size() && k < BC_MAXG && groups[i].nsrc == ns) a.g[k++] = groups[i++];
+        a.ngroups = k;
+        hks_status st = launch_bconv(a, BC_MAXDST, s);
+        if (st != HKS_OK) return st;
+    }
+    return HKS_OK;
+}
+
+// groups converting src slots -> dst slots with a row-major matrix [nsrc][stride]; targets chunked by 64
+void add_groups(std::vector<BconvGroup> &out, u32 nsrc, const u16 *src_slot, const uint2 *mat, u32 stride,
+                const std::vector<u16> &dst_slot, const std::vector<u16> &dst_prime) {
+    for (size_t u0 = 0; u0 < dst_slot.size(); u0 += BC_MAXDST) {
+        BconvGroup g{};
+        g.nsrc = nsrc;
+        g.ndst = (u32)std::min<size_t>(BC_MAXDST, dst_slot.size() - u0);
+        g.mat_stride = stride;
+        g.mat = mat + u0;
+        for (u32 i = 0; i < nsrc; i++) g.src_slot[i] = src_slot[i];
+        for (u32 u = 0; u < g.ndst; u++) {
+            g.dst_slot[u] = dst_slot[u0 + u];
+            g.dst_prime[u] = dst_prime[u0 + u];
+        }
+        out.push_back(g);
+    }
+}
+
+// ModUp: d [l+1][N] EVAL -> ext slots (j * ne + t) for t outside digit j.  coef: [l+1][N] scratch.
+hks_status modup_core(const hks_ctx *c, const u64 *d, u32 level, u64 *ext, u64 *coef, cudaStream_t s) {
+    const u32 ne = c->ne(level), beta = c->beta(level);
+    LimbList L;
+    for (u32 i = 0; i <= level; i++) L.push(i, i, i);
+    hks_status st = run_ntt(c, NTT_INV, L, d, coef, c->d_mu_scale + c->mu_scale_off[level], level + 1, s);
+    if (st != HKS_OK) return st;
+    std::vector<BconvGroup> groups;
+    LimbList T;
+    for (u32 j = 0; j < beta; j++) {
+        u32 lo = c->digit_lo(j), hi = c->digit_hi(level, j);
+        u16 src[BC_MAXSRC];
+        for (u32 i = lo; i < hi; i++) src[i - lo] = (u16)i;
+        std::vector<u16> ds, dp;
+        for (u32 t = 0; t < ne; t++) {
+            if (t >= lo && t < hi) continue;
+            ds.push_back((u16)(j * ne + t));
+            dp.push_back((u16)c->ext_prime(level, t));
+            T.push(j * ne + t, j * ne + t, c->ext_prime(level, t));
+        }
+        add_groups(groups, hi - lo, src, c->d_mu_mat + c->mu_mat_off[(size_t)level * c->dnum + j],
+                   (u32)ds.size(), ds, dp);
+    }
+    st = run_bconv_groups(c, groups, coef, ext, s);
+    if (st != HKS_OK) return st;
+    return run_ntt(c, NTT_FWD, T, ext, ext, nullptr, 0, s);
+}
+
+// ModDown of npoly accumulators (acc poly p at slots p * ne + t) into out[p] (+ c0 on poly 0).
+// ws: y [npoly][K][N] then conv [npoly][l+1][N].
+hks_status moddown_core(const hks_ctx *c, const u64 *acc, u32 npoly, u32 level, u64 *const *outs, const u64 *c0,
+                        u64 galois, u64 *ws, cudaStream_t s) {
+    const u32 ne = c->ne(level), K = c->np;
+    u64 *y = ws, *conv = ws + (size_t)npoly * K * c->n;
+    LimbList L;
+    for (u32 p = 0; p < npoly; p++)
+        for (u32 k = 0; k < K; k++) L.push(p * ne + level + 1 + k, p * K + k, c->nq + k);
+    hks_status st = run_ntt(c, NTT_INV, L, acc, y, c->d_md_scale, K, s);
+    if (st != HKS_OK) return st;
+    std::vector<BconvGroup> groups;
+    std::vector<u16> dp(level + 1);
+    for (u32 i = 0; i <= level; i++) dp[i] = (u16)i;
+    for (u32 p = 0; p < npoly; p++) {
+        u16 src[BC_MAXSRC];
+        for (u32 k = 0; k < K; k++) src[k] = (u16)(p * K + k);
+        std::vector<u16> ds(level + 1);
+        for (u32 i = 0; i <= level; i++) ds[i] = (u16)(p * (level + 1) + i);
+        add_groups(groups, K, src, c->d_md_mat, c->nq, ds, dp);
+    }
+    st = run_bconv_groups(c, groups, y, conv, s);
+    if (st != HKS_OK) return st;
+    for (u32 p = 0; p < npoly; p++) {
+        LimbList M;
+        for (u32 i = 0; i <= level; i++) M.push(p * (level + 1) + i, i, i, p * ne + i, (p == 0 && c0) ? i : 0xffff);
+        st = run_ntt_moddown(c, M, conv, outs[p], acc, p == 0 ? c0 : nullptr, galois, s);
+        if (st != HKS_OK) return st;
+    }
+    return HKS_OK;
+}
+
+hks_status kip_core(const hks_ctx *c, const u64 *ext, const u64 *c1, const u64 *evk, u32 level, u64 galois,
+                    u64 *acc, cudaStream_t s) {
+    KipArgs a{};
+    a.ext = ext;
+    a.c1 = c1;
+    a.evk = evk;
+    a.acc = acc;
+    a.pc = c->d_pc;
+    a.galois = galois;
+    a.log_n = c->log_n;
+    a.level = level;
+    a.nq = c->nq;
+    a.np = c->np;
+    a.ne = c->ne(level);
+    a.nk = c->nq + c->np;
+    a.beta = c->beta(level);
+    a.alpha = c->alpha;
+    return launch_kip(a, s);
+}
+
+hks_status check_galois(const hks_ctx *c, u64 g) {
+    if ((g & 1) == 0 || g >= 2 * (u64)c->n) HKS_FAIL(HKS_EGALOIS, "galois element %llu must be odd and < 2N", (unsigned long long)g);
+    return HKS_OK;
+}
+
+}  // namespace
+
+extern "C" size_t hks_workspace_bytes(const hks_ctx *c, hks_op op, uint32_t level, uint32_t count) {
+    (void)count;
+    if (!c || level > c->L()) return 0;
+    const size_t lb = limb_bytes(c), l1 = level + 1, ne = c->ne(level), K = c->np, beta = c->beta(level);
+    switch (op) {
+        case HKS_OP_MODUP: return l1 * lb;
+        case HKS_OP_MODDOWN: return (K + l1) * lb;
+        case HKS_OP_KEYSWITCH:
+        case HKS_OP_ROTATE_HOISTED: return (l1 + beta * ne + 2 * ne + 2 * K + 2 * l1) * lb;
+    }
+    return 0;
+}
+
+extern "C" hks_status hks_ntt_fwd(const hks_ctx *c, uint64_t *x, const uint32_t *prime_idx, uint32_t nlimbs,
+                                  void *stream) {
+    hks_status st = check_ctx(c);
+    if (st != HKS_OK) return st;
+    if (!x || !prime_idx || nlimbs == 0) HKS_FAIL(HKS_EINVAL, "ntt_fwd: NULL buffer / empty batch");
+    if (nlimbs > 0xffff) HKS_FAIL(HKS_EINVAL, "ntt_fwd: batch too large");
+    LimbList L;
+    for (u32 b = 0; b < nlimbs; b++) {
+        if (prime_idx[b] >= c->primes.size()) HKS_FAIL(HKS_EINVAL, "ntt_fwd: prime index %u out of range", prime_idx[b]);
+        L.push(b, b, prime_idx[b]);
+    }
+    DevGuard g(c->device);
+    return run_ntt(c, NTT_FWD, L, x, x, nullptr, 0, (cudaStream_t)stream);
+}
+
+extern "C" hks_status hks_ntt_inv(const hks_ctx *c, uint64_t *x, const uint32_t *prime_idx, uint32_t nlimbs,
+                                  void *stream) {
+    hks_status st = check_ctx(c);
+    if (st != HKS_OK) return st;
+    if (!x || !prime_idx || nlimbs == 0) HKS_FAIL(HKS_EINVAL, "ntt_inv: NULL buffer / empty batch");
+    if (nlimbs > 0xffff) HKS_FAIL(HKS_EINVAL, "ntt_inv: batch too large");
+    LimbList L;
+    for (u32 b = 0; b < nlimbs; b++) {
+        if (prime_idx[b] >= c->primes.size()) HKS_FAIL(HKS_EINVAL, "ntt_inv: prime index %u out of range", prime_idx[b]);
+        L.push(b, b, prime_idx[b]);
+    }
+    DevGuard g(c->device);
+    return run_ntt(c, NTT_INV, L, x, x, nullptr, 0, (cudaStream_t)stream);
+}
+
+extern "C" hks_status hks_bconv(const hks_ctx *c, const uint64_t *x, const uint32_t *src_idx, uint32_t nsrc,
+                                const uint32_t *dst_idx, uint32_t ndst, uint64_t *out, void *stream) {
+    hks_status st = check_ctx(c);
+    if (st != HKS_OK) return st;
+    if (!x || !out || !src_idx || !dst_idx) HKS_FAIL(HKS_EINVAL, "bconv: NULL argument");
+    if (nsrc < 1 || nsrc > BC_MAXSRC || ndst < 1 || ndst > 2 * BC_MAXDST)
+        HKS_FAIL(HKS_EINVAL, "bconv: nsrc must be in [1,%d], ndst in [1,%d]", BC_MAXSRC, 2 * BC_MAXDST);
+    const size_t lb = limb_bytes(c);
+    if (overlap(x, nsrc * lb, out, ndst * lb)) HKS_FAIL(HKS_EINVAL, "bconv: out overlaps x");
+    const u32 nm = (u32)c->primes.size();
+    for (u32 i = 0; i < nsrc; i++) {
+        if (src_idx[i] >= nm) HKS_FAIL(HKS_EINVAL, "bconv: src prime index out of range");
+        for (u32 k = 0; k < i; k++)
+            if (src_idx[k] == src_idx[i]) HKS_FAIL(HKS_EINVAL, "bconv: repeated source prime");
+    }
+    for (u32 u = 0; u < ndst; u++) {
+        if (dst_idx[u] >= nm) HKS_FAIL(HKS_EINVAL, "bconv: dst prime index out of range");
+        for (u32 i = 0; i < nsrc; i++)
+            if (src_idx[i] == dst_idx[u]) HKS_FAIL(HKS_EINVAL, "bconv: source and target bases overlap");
+    }
+    typedef unsigned __int128 u128;
+    auto mm = [](u64 a, u64 b, u64 m) { return (u64)((u128)a * b % m); };
+    auto pw = [&](u64 a, u64 e, u64 m) { u64 r = 1; a %= m; for (; e; e >>= 1, a = mm(a, a, m)) if (e & 1) r = mm(r, a, m); return r; };
+    std::vector<uint2> mat((size_t)nsrc * ndst);
+    BconvGroup proto{};
+    for (u32 i = 0; i < nsrc; i++) {
+        u64 qi = c->primes[src_idx[i]], h = 1;
+        for (u32 k = 0; k < nsrc; k++)
+            if (k != i) h = mm(h, c->primes[src_idx[k]] % qi, qi);
+        u64 w = pw(h, qi - 2, qi);
+        proto.pre_w[i] = w;
+        proto.pre_wp[i] = (u64)(((u128)w << 64) / qi);
+        proto.src_slot[i] = (u16)i;
+        proto.src_prime[i] = (u16)src_idx[i];
+        for (u32 u = 0; u < ndst; u++) {
+            u64 t = c->primes[dst_idx[u]], v = 1;
+            for (u32 k = 0; k < nsrc; k++)
+                if (k != i) v = mm(v, c->primes[src_idx[k]] % t, t);
+            mat[(size_t)i * ndst + u] = make_uint2((u32)(v & 0x3fffffffu), (u32)(v >> 30));
+        }
+    }
+    DevGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    uint2 *dmat = nullptr;
+    HKS_CUDA(cudaMallocAsync((void **)&dmat, mat.size() * sizeof(uint2), s));
+    HKS_CUDA(cudaMemcpyAsync(dmat, mat.data(), mat.size() * sizeof(uint2), cudaMemcpyHostToDevice, s));
+    for (u32 u0 = 0; u0 < ndst; u0 += BC_MAXDST) {
+        BconvArgs a{};
+        a.in = x;
+        a.out = out;
+        a.pc = c->d_pc;
+        a.log_n = c->log_n;
+        a.prescale = 1;
+        a.ngroups = 1;
+        a.g[0] = proto;
+        a.g[0].nsrc = nsrc;
+        a.g[0].ndst = std::min<u32>(BC_MAXDST, ndst - u0);
+        a.g[0].mat = dmat + u0;
+        a.g[0].mat_stride = ndst;
+        for (u32 u = 0; u < a.g[0].ndst; u++) {
+            a.g[0].dst_slot[u] = (u16)(u0 + u);
+            a.g[0].dst_prime[u] = (u16)dst_idx[u0 + u];
+        }
+        st = launch_bconv(a, BC_MAXDST, s);
+        if (st != HKS_OK) break;
+    }
+    cudaFreeAsync(dmat, s);
+    return st;
+}
+
+extern "C" hks_status hks_modup(const hks_ctx *c, const uint64_t *d, uint32_t level, uint64_t *ext, void *ws,
+                                void *stream) {
+    hks_status st = check_ctx(c);
+    if (st != HKS_OK) return st;
+    if (!d || !ext || !ws) HKS_FAIL(HKS_EINVAL, "modup: NULL argument");
+    if (level > c->L()) HKS_FAIL(HKS_EINVAL, "modup: level %u > L", level);
+    const size_t lb = limb_bytes(c), ne = c->ne(level), beta = c->beta(level);
+    if (overlap(d, (level + 1) * lb, ext, beta * ne * lb) || overlap(ws, (level + 1) * lb, ext, beta * ne * lb) ||
+        overlap(ws, (level + 1) * lb, d, (level + 1) * lb))
+        HKS_FAIL(HKS_EINVAL, "modup: buffers overlap");
+    DevGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    st = modup_core(c, d, level, ext, (u64 *)ws, s);
+    if (st != HKS_OK) return st;
+    for (u32 j = 0; j < beta; j++) {
+        u32 lo = c->digit_lo(j), hi = c->digit_hi(level, j);
+        HKS_CUDA(cudaMemcpyAsync(ext + ((size_t)j * ne + lo) * c->n, d + (size_t)lo * c->n, (hi - lo) * lb,
+                                 cudaMemcpyDeviceToDevice, s));
+    }
+    return HKS_OK;
+}
+
+extern "C" hks_status hks_ksk_inner_product(const hks_ctx *c, const uint64_t *ext, const uint64_t *evk,
+                                            uint32_t level, uint64_t galois, uint64_t *acc, void *stream) {
+    hks_status st = check_ctx(c);
+    if (st != HKS_OK) return st;
+    if (!ext || !evk || !acc) HKS_FAIL(HKS_EINVAL, "ksk_inner_product: NULL argument");
+    if (level > c->L()) HKS_FAIL(HKS_EINVAL, "ksk_inner_product: level %u > L", level);
+    if (galois != 1 && (st = check_galois(c, galois)) != HKS_OK) return st;
+    const size_t lb = limb_bytes(c), ne = c->ne(level);
+    if (overlap(ext, c->beta(level) * ne * lb, acc, 2 * ne * lb) ||
+        overlap(evk, (size_t)c->dnum * 2 * (c->nq + c->np) * lb, acc, 2 * ne * lb))
+        HKS_FAIL(HKS_EINVAL, "ksk_inner_product: acc overlaps an input");
+    DevGuard g(c->device);
+    return kip_core(c, ext, nullptr, evk, level, galois, acc, (cudaStream_t)stream);
+}
+
+extern "C" hks_status hks_moddown(const hks_ctx *c, const uint64_t *acc, uint32_t level, uint64_t *out, void *ws,
+                                  void *stream) {
+    hks_status st = check_ctx(c);
+    if (st != HKS_OK) return st;
+    if (!acc || !out || !ws) HKS_FAIL(HKS_EINVAL, "moddown: NULL argument");
+    if (level > c->L()) HKS_FAIL(HKS_EINVAL, "moddown: level %u > L", level);
+    const size_t lb = limb_bytes(c), ne = c->ne(level), wsb = (c->np + level + 1) * lb;
+    if (overlap(acc, ne * lb, out, (level + 1) * lb) || overlap(ws, wsb, out, (level + 1) * lb) ||
+        overlap(ws, wsb, acc, ne * lb))
+        HKS_FAIL(HKS_EINVAL, "moddown: buffers overlap");
+    DevGuard g(c->device);
+    u64 *outs[1] = {out};
+    return moddown_core(c, acc, 1, level, outs, nullptr, 1, (u64 *)ws, (cudaStream_t)stream);
+}
+
+extern "C" hks_status hks_keyswitch(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, uint32_t level,
+                                    const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws, void *stream) {
+    hks_status st = check_ctx(c);
+    if (st != HKS_OK) return st;
+    if (!c1 || !evk || !out0 || !out1 || !ws) HKS_FAIL(HKS_EINVAL, "keyswitch: NULL argument");
+    if (level > c->L()) HKS_FAIL(HKS_EINVAL, "keyswitch: level %u > L", level);
+    if (c->beta(level) > c->dnum) HKS_FAIL(HKS_EKEY, "keyswitch: key has fewer digits than beta");
+    const size_t lb = limb_bytes(c), l1 = level + 1, ne = c->ne(level), beta = c->beta(level);
+    const size_t wsb = hks_workspace_bytes(c, HKS_OP_KEYSWITCH, level, 0);
+    const void *ins[3] = {c0, c1, evk};
+    size_t insz[3] = {l1 * lb, l1 * lb, (size_t)c->dnum * 2 * (c->nq + c->np) * lb};
+    void *outs_[3] = {out0, out1, ws};
+    size_t outsz[3] = {l1 * lb, l1 * lb, wsb};
+    for (int i = 0; i < 3; i++)
+        for (int o = 0; o < 3; o++)
+            if (overlap(ins[i], insz[i], outs_[o], outsz[o])) HKS_FAIL(HKS_EINVAL, "keyswitch: output overlaps an input");
+    if (overlap(out0, l1 * lb, out1, l1 * lb) || overlap(out0, l1 * lb, ws, wsb) || overlap(out1, l1 * lb, ws, wsb))
+        HKS_FAIL(HKS_EINVAL, "keyswitch: outputs overlap");
+    DevGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    u64 *coef = (u64 *)ws;
+    u64 *ext = coef + l1 * c->n;
+    u64 *acc = ext + beta * ne * c->n;
+    u64 *md = acc + 2 * ne * c->n;
+    if ((st = modup_core(c, c1, level, ext, coef, s)) != HKS_OK) return st;
+    if ((st = kip_core(c, ext, c1, evk, level, 1, acc, s)) != HKS_OK) return st;
+    u64 *outs[2] = {out0, out1};
+    return moddown_core(c, acc, 2, level, outs, c0, 1, md, s);
+}
+
+extern "C" hks_status hks_automorph(const hks_ctx *c, const uint64_t *in, uint32_t nlimbs, uint64_t galois,
+                                    uint64_t *out, void *stream) {
+    hks_status st = check_ctx(c);
+    if (st != HKS_OK) return st;
+    if (!in || !out || nlimbs == 0) HKS_FAIL(HKS_EINVAL, "automorph: NULL buffer / empty batch");
+    if ((st = check_galois(c, galois)) != HKS_OK) return st;
+    if (overlap(in, nlimbs * limb_bytes(c), out, nlimbs * limb_bytes(c))) HKS_FAIL(HKS_EINVAL, "automorph: in and out overlap");
+    DevGuard g(c->device);
+    return launch_automorph(in, out, nlimbs, c->log_n, galois, (cudaStream_t)stream);
+}
+
+extern "C" hks_status hks_rotate_hoisted(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, uint32_t level,
+                                         uint32_t nrot, const uint64_t *galois, const uint64_t *const *evk,
+                                         uint64_t *const *out0, uint64_t *const *out1, void *ws, void *stream) {
+    hks_status st = check_ctx(c);
+    if (st != HKS_OK) return st;
+    if (!c0 || !c1 || !ws || (nrot && (!galois || !evk || !out0 || !out1))) HKS_FAIL(HKS_EINVAL, "rotate_hoisted: NULL argument");
+    if (level > c->L()) HKS_FAIL(HKS_EINVAL, "rotate_hoisted: level %u > L", level);
+    if (nrot == 0) return HKS_OK;
+    const size_t lb = limb_bytes(c), l1 = level + 1, ne = c->ne(level), beta = c->beta(level);
+    const size_t wsb = hks_workspace_bytes(c, HKS_OP_ROTATE_HOISTED, level, nrot);
+    for (u32 r = 0; r < nrot; r++) {
+        if ((st = check_galois(c, galois[r])) != HKS_OK) return st;
+        if (!evk[r] || !out0[r] || !out1[r]) HKS_FAIL(HKS_EINVAL, "rotate_hoisted: NULL pointer in arrays");
+        if (overlap(out0[r], l1 * lb, c0, l1 * lb) || overlap(out0[r], l1 * lb, c1, l1 * lb) ||
+            overlap(out1[r], l1 * lb, c0, l1 * lb) || overlap(out1[r], l1 * lb, c1, l1 * lb) ||
+            overlap(out0[r], l1 * lb, ws, wsb) || overlap(out1[r], l1 * lb, ws, wsb) ||
+            overlap(out0[r], l1 * lb, out1[r], l1 * lb))
+            HKS_FAIL(HKS_EINVAL, "rotate_hoisted: output %u overlaps", r);
+    }
+    DevGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    u64 *coef = (u64 *)ws;
+    u64 *ext = coef + l1 * c->n;
+    u64 *acc = ext + beta * ne * c->n;
+    u64 *md = acc + 2 * ne * c->n;
+    if ((st = modup_core(c, c1, level, ext, coef, s)) != HKS_OK) return st;
+    for (u32 r = 0; r < nrot; r++) {
+        if ((st = kip_core(c, ext, c1, evk[r], level, galois[r], acc, s)) != HKS_OK) return st;
+        u64 *outs[2] = {out0[r], out1[r]};
+        if ((st = moddown_core(c, acc, 2, level, outs, c0, galois[r], md, s)) != HKS_OK) return st;
+    }
+    return HKS_OK;
+}

@@ -1,0 +1,321 @@
+// ctx.cu -- context creation: validation and one-time precomputation (§3.5).
+//
+// The library's own host number theory (independent of oracle/): Montgomery-free u128 arithmetic,
+// deterministic Miller-Rabin, the minimal primitive 2N-th root, bit-reversed twiddle tables with
+// Shoup companions, the Eq. 1 ModUp constants per (level, digit), and the ModDown constants.
+// Unlike the paper's singleton a context is an ordinary immutable handle; the
+// per-prime scalars every thread needs travel in kernel parameters / read-only loads instead of
+// a 64 KB __constant__ bank.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <thread>
+
+#include "internal.h"
+
+typedef unsigned __int128 u128;
+
+static thread_local char g_err[512] = "";
+
+void hks_set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+}
+
+extern "C" const char *hks_last_error(void) { return g_err; }
+
+namespace {
+
+u64 mul_mod(u64 a, u64 b, u64 m) { return (u64)((u128)a * b % m); }
+
+u64 pow_mod(u64 a, u64 e, u64 m) {
+    u64 r = 1 % m;
+    a %= m;
+    for (; e; e >>= 1, a = mul_mod(a, a, m))
+        if (e & 1) r = mul_mod(r, a, m);
+    return r;
+}
+
+u64 inv_mod(u64 a, u64 m) { return pow_mod(a, m - 2, m); }   // m prime
+
+bool is_prime64(u64 n) {
+    if (n < 2) return false;
+    static const u64 small[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+    for (u64 s : small)
+        if (n % s == 0) return n == s;
+    u64 d = n - 1;
+    int r = 0;
+    while (!(d & 1)) d >>= 1, r++;
+    for (u64 a : small) {
+        u64 x = pow_mod(a, d, n);
+        if (x == 1 || x == n - 1) continue;
+        bool comp = true;
+        for (int i = 1; i < r && comp; i++) {
+            x = mul_mod(x, x, n);
+            if (x == n - 1) comp = false;
+        }
+        if (comp) return false;
+    }
+    return true;
+}
+
+// SURVEY.md §8(c) reading 1: the smallest x with x^N = -1 (mod m).  Every such x is psi0^k, k odd.
+u64 minimal_psi(u64 m, u32 n) {
+    u64 psi0 = 0;
+    for (u64 g = 2;; g++) {
+        u64 c = pow_mod(g, (m - 1) / (2 * (u64)n), m);
+        if (pow_mod(c, n, m) == m - 1) { psi0 = c; break; }
+    }
+    u64 step = mul_mod(psi0, psi0, m), cur = psi0, best = psi0;
+    for (u32 k = 0; k < n; k++) {
+        best = std::min(best, cur);
+        cur = mul_mod(cur, step, m);
+    }
+    return best;
+}
+
+u64 shoup_of(u64 w, u64 m) { return (u64)(((u128)w << 64) / m); }
+
+ulonglong2 sh(u64 w, u64 m) { return make_ulonglong2(w, shoup_of(w, m)); }
+
+uint2 split(u64 v) { return make_uint2((u32)(v & 0x3fffffffu), (u32)(v >> 30)); }
+
+u32 bitrev(u32 x, u32 bits) {
+    u32 r = 0;
+    for (u32 i = 0; i < bits; i++) r |= ((x >> i) & 1u) << (bits - 1 - i);
+    return r;
+}
+
+template <typename T>
+hks_status upload(T **dptr, const std::vector<T> &h) {
+    if (h.empty()) { *dptr = nullptr; return HKS_OK; }
+    cudaError_t e = cudaMalloc((void **)dptr, h.size() * sizeof(T));
+    if (e != cudaSuccess) HKS_FAIL(HKS_ENOMEM, "cudaMalloc(%zu): %s", h.size() * sizeof(T), cudaGetErrorString(e));
+    e = cudaMemcpy(*dptr, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) HKS_FAIL(HKS_ECUDA, "cudaMemcpy: %s", cudaGetErrorString(e));
+    return HKS_OK;
+}
+
+void free_tables(hks_ctx *c) {
+    void *ptrs[] = {c->d_pc, c->d_tw_col_fwd, c->d_tw_row_fwd, c->d_tw_col_inv, c->d_tw_row_inv, c->d_ninv,
+                    c->d_mu_scale, c->d_mu_mat, c->d_md_scale, c->d_md_mat, c->d_pinv};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+}
+
+// Twiddle tables of one prime.  psi_brv[k] = psi^brv_logN(k) ("precomputing the
+// twiddle factors ... Shoup constants are also precomputed").  Column table = psi_brv[0..R);
+// row table of row r at heap index k = 2^s + i:  psi_brv[(R + r) 2^s + i].
+void twiddles(u64 m, u64 root, u32 log_n, u32 log_r, u32 log_c, ulonglong2 *col, ulonglong2 *row) {
+    const u32 n = 1u << log_n, R = 1u << log_r, C = 1u << log_c;
+    std::vector<u64> pw(n);
+    u64 x = 1;
+    for (u32 e = 0; e < n; e++) { pw[e] = x; x = mul_mod(x, root, m); }
+    auto psi_brv = [&](u32 k) { return pw[bitrev(k, log_n)]; };
+    for (u32 k = 0; k < R; k++) col[k] = sh(psi_brv(k), m);
+    for (u32 r = 0; r < R; r++) {
+        row[(size_t)r * C] = make_ulonglong2(0, 0);
+        for (u32 s = 0; (1u << s) < C; s++)
+            for (u32 i = 0; i < (1u << s); i++)
+                row[(size_t)r * C + (1u << s) + i] = sh(psi_brv(((R + r) << s) + i), m);
+    }
+}
+
+}  // namespace
+
+extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t num_q, const uint64_t *p,
+                                     uint32_t num_p, uint32_t dnum, int device, hks_ctx **out) {
+    if (!out || !q || !p) HKS_FAIL(HKS_EINVAL, "ctx_create: NULL argument");
+    *out = nullptr;
+    if (log_n < 10 || log_n > 17) HKS_FAIL(HKS_ERANGE, "ctx_create: log_n %u outside [10, 17]", log_n);
+    if (num_q < 1 || num_p < 1) HKS_FAIL(HKS_EINVAL, "ctx_create: need at least one q and one p");
+    if (dnum < 1 || dnum > num_q) HKS_FAIL(HKS_ERANGE, "ctx_create: dnum %u outside [1, %u]", dnum, num_q);
+    if (num_q + num_p > 1024) HKS_FAIL(HKS_ERANGE, "ctx_create: too many moduli");
+    const u32 alpha = (num_q + dnum - 1) / dnum;
+    if (alpha > BC_MAXSRC) HKS_FAIL(HKS_ERANGE, "ctx_create: alpha = ceil((L+1)/dnum) = %u > %d unsupported", alpha, BC_MAXSRC);
+    if (num_p > BC_MAXSRC) HKS_FAIL(HKS_ERANGE, "ctx_create: K = %u > %d unsupported", num_p, BC_MAXSRC);
+    const u32 n = 1u << log_n;
+    std::vector<u64> primes(q, q + num_q);
+    primes.insert(primes.end(), p, p + num_p);
+    for (size_t i = 0; i < primes.size(); i++) {
+        u64 m = primes[i];
+        if (m >= (1ull << 60)) HKS_FAIL(HKS_ERANGE, "ctx_create: modulus %zu = %llu >= 2^60", i, (unsigned long long)m);
+        if (!is_prime64(m)) HKS_FAIL(HKS_ENOTPRIME, "ctx_create: modulus %zu = %llu is not prime", i, (unsigned long long)m);
+        if ((m - 1) % (2 * (u64)n)) HKS_FAIL(HKS_ENOTNTT, "ctx_create: modulus %zu = %llu is not 1 mod 2N", i, (unsigned long long)m);
+        for (size_t j = 0; j < i; j++)
+            if (primes[j] == m) HKS_FAIL(HKS_EDUP, "ctx_create: modulus %llu repeated", (unsigned long long)m);
+    }
+    if (device >= 0) {
+        int cnt = 0;
+        if (cudaGetDeviceCount(&cnt) != cudaSuccess || device >= cnt)
+            HKS_FAIL(HKS_EDEVICE, "ctx_create: CUDA device %d not available", device);
+    }
+
+    hks_ctx *c = new hks_ctx();
+    c->log_n = log_n;
+    c->n = n;
+    c->log_r = (log_n + 1) / 2;
+    c->log_c = log_n / 2;
+    c->nq = num_q;
+    c->np = num_p;
+    c->dnum = dnum;
+    c->alpha = alpha;
+    c->device = device;
+    c->primes = primes;
+    const u32 nm = (u32)primes.size();
+    c->psi.resize(nm);
+    {
+        std::vector<std::thread> th;
+        u32 nt = std::max(1u, std::min(nm, std::thread::hardware_concurrency()));
+        for (u32 w = 0; w < nt; w++)
+            th.emplace_back([&, w] {
+                for (u32 i = w; i < nm; i += nt) c->psi[i] = minimal_psi(primes[i], n);
+            });
+        for (auto &t : th) t.join();
+    }
+    if (device < 0) { *out = c; return HKS_OK; }
+
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (cudaSetDevice(device) != cudaSuccess) { delete c; HKS_FAIL(HKS_EDEVICE, "ctx_create: cudaSetDevice(%d) failed", device); }
+
+    const u32 R = 1u << c->log_r, C = 1u << c->log_c, L = num_q - 1;
+    std::vector<PrimeConst> pc(nm);
+    std::vector<ulonglong2> ninv(nm);
+    for (u32 i = 0; i < nm; i++) {
+        u64 m = primes[i];
+        u64 r64 = (u64)(((u128)1 << 64) % m);
+        pc[i] = PrimeConst{m, r64, shoup_of(r64, m), (u64)(~0ull / m)};
+        ninv[i] = sh(inv_mod(n % m, m), m);
+    }
+    // one_p = floor(2^64 / m) = floor((2^64 - 1) / m) since m does not divide 2^64.
+    std::vector<ulonglong2> tcf((size_t)nm * R), trf((size_t)nm * n), tci((size_t)nm * R), tri((size_t)nm * n);
+    {
+        std::vector<std::thread> th;
+        u32 nt = std::max(1u, std::min(nm, std::thread::hardware_concurrency()));
+        for (u32 w = 0; w < nt; w++)
+            th.emplace_back([&, w] {
+                for (u32 i = w; i < nm; i += nt) {
+                    u64 m = primes[i];
+                    twiddles(m, c->psi[i], log_n, c->log_r, c->log_c, &tcf[(size_t)i * R], &trf[(size_t)i * n]);
+                    twiddles(m, inv_mod(c->psi[i], m), log_n, c->log_r, c->log_c, &tci[(size_t)i * R], &tri[(size_t)i * n]);
+                }
+            });
+        for (auto &t : th) t.join();
+    }
+
+    // ModUp constants (Eq. 1) per level l and digit j: scale N^-1 [qhat_{j,i}]^-1 mod q_i for the
+    // digit's active limbs, matrix [qhat_{j,i}]_t for targets t in (Q_l \ digit j) u P.
+    std::vector<ulonglong2> mu_scale;
+    std::vector<uint2> mu_mat;
+    c->mu_scale_off.resize(num_q);
+    c->mu_mat_off.assign((size_t)num_q * dnum, 0);
+    for (u32 lv = 0; lv <= L; lv++) {
+        c->mu_scale_off[lv] = mu_scale.size();
+        u32 beta = c->beta(lv);
+        for (u32 i = 0; i <= lv; i++) {
+            u32 j = i / alpha, lo = c->digit_lo(j), hi = c->digit_hi(lv, j);
+            u64 m = primes[i], h = 1;
+            for (u32 k = lo; k < hi; k++)
+                if (k != i) h = mul_mod(h, primes[k] % m, m);
+            mu_scale.push_back(sh(mul_mod(inv_mod(h, m), inv_mod(n % m, m), m), m));
+        }
+        for (u32 j = 0; j < beta; j++) {
+            c->mu_mat_off[(size_t)lv * dnum + j] = mu_mat.size();
+            u32 lo = c->digit_lo(j), hi = c->digit_hi(lv, j);
+            for (u32 i = lo; i < hi; i++)
+                for (u32 t = 0; t < c->ne(lv); t++) {
+                    if (t >= lo && t < hi) continue;
+                    u64 m = primes[c->ext_prime(lv, t)], h = 1;
+                    for (u32 k = lo; k < hi; k++)
+                        if (k != i) h = mul_mod(h, primes[k] % m, m);
+                    mu_mat.push_back(split(h));
+                }
+        }
+    }
+    // ModDown constants: scale N^-1 [phat_k]^-1 mod p_k, matrix [phat_k]_{q_i} [K][L+1], P^-1 mod q_i.
+    std::vector<ulonglong2> md_scale(num_p), pinv(num_q);
+    std::vector<uint2> md_mat((size_t)num_p * num_q);
+    for (u32 k = 0; k < num_p; k++) {
+        u64 m = p[k], h = 1;
+        for (u32 o = 0; o < num_p; o++)
+            if (o != k) h = mul_mod(h, p[o] % m, m);
+        md_scale[k] = sh(mul_mod(inv_mod(h, m), inv_mod(n % m, m), m), m);
+        for (u32 i = 0; i < num_q; i++) {
+            u64 qi = q[i], hv = 1;
+            for (u32 o = 0; o < num_p; o++)
+                if (o != k) hv = mul_mod(hv, p[o] % qi, qi);
+            md_mat[(size_t)k * num_q + i] = split(hv);
+        }
+    }
+    for (u32 i = 0; i < num_q; i++) {
+        u64 qi = q[i], P = 1;
+        for (u32 k = 0; k < num_p; k++) P = mul_mod(P, p[k] % qi, qi);
+        pinv[i] = sh(inv_mod(P, qi), qi);
+    }
+
+    hks_status st = HKS_OK;
+#define UP(dst, src) if (st == HKS_OK) st = upload(&c->dst, src)
+    UP(d_pc, pc);
+    UP(d_ninv, ninv);
+    UP(d_tw_col_fwd, tcf);
+    UP(d_tw_row_fwd, trf);
+    UP(d_tw_col_inv, tci);
+    UP(d_tw_row_inv, tri);
+    UP(d_mu_scale, mu_scale);
+    UP(d_mu_mat, mu_mat);
+    UP(d_md_scale, md_scale);
+    UP(d_md_mat, md_mat);
+    UP(d_pinv, pinv);
+#undef UP
+    cudaSetDevice(prev);
+    if (st != HKS_OK) {
+        free_tables(c);
+        delete c;
+        return st;
+    }
+    *out = c;
+    return HKS_OK;
+}
+
+extern "C" void hks_ctx_destroy(hks_ctx *c) {
+    if (!c) return;
+    if (c->device >= 0) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(c->device);
+        free_tables(c);
+        cudaSetDevice(prev);
+    }
+    delete c;
+}
+
+extern "C" hks_status hks_ctx_query(const hks_ctx *c, uint32_t level, hks_info *out) {
+    if (!c || !out) HKS_FAIL(HKS_EINVAL, "ctx_query: NULL argument");
+    if (level > c->L()) HKS_FAIL(HKS_EINVAL, "ctx_query: level %u > L = %u", level, c->L());
+    *out = hks_info{};
+    out->log_n = c->log_n;
+    out->n = c->n;
+    out->num_q = c->nq;
+    out->num_p = c->np;
+    out->dnum = c->dnum;
+    out->alpha = c->alpha;
+    out->level = level;
+    out->beta = c->beta(level);
+    for (u32 j = 0; j < out->beta && j < HKS_MAX_DIGITS; j++) {
+        out->digit_lo[j] = c->digit_lo(j);
+        out->digit_hi[j] = c->digit_hi(level, j);
+    }
+    out->device = c->device;
+    return HKS_OK;
+}
+
+extern "C" hks_status hks_ctx_psi(const hks_ctx *c, uint32_t prime_idx, uint64_t *psi) {
+    if (!c || !psi) HKS_FAIL(HKS_EINVAL, "ctx_psi: NULL argument");
+    if (prime_idx >= c->primes.size()) HKS_FAIL(HKS_EINVAL, "ctx_psi: prime index %u out of range", prime_idx);
+    *psi = c->psi[prime_idx];
+    return HKS_OK;
+}

@@ -1,0 +1,165 @@
+// internal.h -- context layout, kernel argument blocks and launcher declarations for libhks.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/hks.h"
+#include "modarith.cuh"
+
+typedef uint16_t u16;
+
+// ----------------------------------------------------------------------------------------------
+// Limb batches.  One kernel launch transforms up to HKS_MAXB limbs of N words; limb b reads slot
+// sin[b] of the input base pointer and writes slot sout[b] of the output base pointer (slot s =
+// words [s*N, (s+1)*N)), reduced modulo prime index prime[b].  The map travels in the kernel's
+// parameter space (warp-uniform, constant-bank broadcast: §3.5).
+#define HKS_MAXB 256
+
+struct LimbMap {
+    u16 sin[HKS_MAXB];
+    u16 sout[HKS_MAXB];
+    u16 prime[HKS_MAXB];
+    u16 sa[HKS_MAXB];   // epilogue operand slot (ModDown: acc limb)
+    u16 sb[HKS_MAXB];   // epilogue operand slot (ModDown: c0 limb), 0xffff = none
+};
+
+enum NttEpi : int {
+    EPI_LAZY = 0,      // first pass: store lazily reduced values
+    EPI_CANON = 1,     // last forward pass: canonical store
+    EPI_MODDOWN = 2,   // last forward pass: out = (a - x) * P^-1 [+ b]  (PAPER.md:350 ModDown fusion)
+    EPI_SCALE = 3      // last inverse pass: out = x * s (s = N^-1 or N^-1 * qhat^-1) canonical
+};
+
+struct NttArgs {
+    const u64 *in;
+    u64 *out;
+    const PrimeConst *pc;      // per prime
+    const ulonglong2 *tw;      // COLS: [nprimes][R] ; ROWS: [nprimes][R][C]   (w, w') pairs
+    const ulonglong2 *scale;   // EPI_SCALE: per-limb (w, w') = scale[b % scale_mod]; NULL -> ninv[prime]
+    const ulonglong2 *ninv;    // per prime N^-1
+    const u64 *ea;             // EPI_MODDOWN operand a base (acc)
+    const u64 *eb;             // EPI_MODDOWN operand b base (c0), may be NULL
+    const ulonglong2 *pinv;    // per prime P^-1 mod q (Shoup)
+    u64 galois;                // EPI_MODDOWN: b is read through the EVAL automorphism (1 = none)
+    u32 log_n, log_r, log_c;   // N = R * C; R = 2^log_r rows, C = 2^log_c columns (row length)
+    u32 tiles;                 // CTAs per limb
+    u32 scale_mod;
+    u32 nlimbs;
+    LimbMap map;
+};
+
+// ----------------------------------------------------------------------------------------------
+// Base conversion (Eq. 1).  A group converts nsrc canonical y_i limbs to up to BC_MAXDST targets.
+#define BC_MAXSRC 16
+#define BC_MAXDST 64
+#define BC_MAXG 4
+
+struct BconvGroup {
+    u32 nsrc, ndst, mat_stride;
+    const uint2 *mat;          // [nsrc][mat_stride] (lo30, hi30) of [qhat_i]_t, column u = target u
+    u16 src_slot[BC_MAXSRC];
+    u16 src_prime[BC_MAXSRC];
+    u64 pre_w[BC_MAXSRC];      // optional prescale y_i = x_i * pre_w (Shoup) -- generic hks_bconv
+    u64 pre_wp[BC_MAXSRC];
+    u16 dst_slot[BC_MAXDST];
+    u16 dst_prime[BC_MAXDST];
+};
+
+struct BconvArgs {
+    const u64 *in;
+    u64 *out;
+    const PrimeConst *pc;
+    u32 log_n;
+    u32 ngroups;
+    u32 prescale;              // 1: apply pre_w (inputs raw COEFF), 0: inputs are canonical y_i
+    BconvGroup g[BC_MAXG];
+};
+
+// ----------------------------------------------------------------------------------------------
+// Key inner product (dot-product fusion).
+struct KipArgs {
+    const u64 *ext;    // [beta][ne][N]
+    const u64 *c1;     // own-digit limbs read from here when non-NULL (KeySwitch), else from ext
+    const u64 *evk;    // [dnum][2][nk][N]
+    u64 *acc;          // [2][ne][N]
+    const PrimeConst *pc;
+    u64 galois;
+    u32 log_n, level, nq, np, ne, nk, beta, alpha;
+};
+
+// ----------------------------------------------------------------------------------------------
+struct hks_ctx {
+    u32 log_n, n, log_r, log_c, nq, np, dnum, alpha;
+    int device;
+    std::vector<u64> primes, psi;
+
+    // host mirrors of the small tables (offsets into the device arrays)
+    std::vector<size_t> mu_mat_off;     // [(L+1) * dnum]: matrix offset of (level, digit)
+    std::vector<size_t> mu_scale_off;   // [L+1]: scale offset of level (ℓ+1 entries)
+
+    // device tables (owned)
+    PrimeConst *d_pc = nullptr;
+    ulonglong2 *d_tw_col_fwd = nullptr, *d_tw_row_fwd = nullptr;
+    ulonglong2 *d_tw_col_inv = nullptr, *d_tw_row_inv = nullptr;
+    ulonglong2 *d_ninv = nullptr;
+    ulonglong2 *d_mu_scale = nullptr;   // ModUp: N^-1 * qhat_{j,i}^-1 mod q_i per (level, i)
+    uint2 *d_mu_mat = nullptr;          // ModUp: [qhat_{j,i}]_t split, per (level, digit)
+    ulonglong2 *d_md_scale = nullptr;   // ModDown: N^-1 * phat_k^-1 mod p_k  [K]
+    uint2 *d_md_mat = nullptr;          // ModDown: [phat_k]_{q_i} split  [K][L+1]
+    ulonglong2 *d_pinv = nullptr;       // P^-1 mod q_i  [L+1] (Shoup)
+
+    u32 L() const { return nq - 1; }
+    u32 beta(u32 level) const { return (level + 1 + alpha - 1) / alpha; }
+    u32 ne(u32 level) const { return level + 1 + np; }
+    u32 digit_lo(u32 j) const { return j * alpha; }
+    u32 digit_hi(u32 level, u32 j) const { u32 h = (j + 1) * alpha; return h < level + 1 ? h : level + 1; }
+    u32 ext_prime(u32 level, u32 t) const { return t <= level ? t : nq + (t - level - 1); }
+};
+
+// ----------------------------------------------------------------------------------------------
+// diagnostics (prof.cu): launch counter + optional per-launch event pair tagged with a kernel class
+enum KCls { K_NTT_FWD_COLS = 0, K_NTT_FWD_ROWS, K_NTT_FWD_ROWS_MODDOWN, K_NTT_INV_ROWS, K_NTT_INV_COLS, K_BCONV,
+            K_KIP, K_AUTOMORPH, K_NCLS };
+struct ProfScope {
+    int cls;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    ProfScope(int c, cudaStream_t st);
+    void done(double algorithmic_bytes);
+};
+
+// ----------------------------------------------------------------------------------------------
+// error plumbing
+void hks_set_error(const char *fmt, ...);
+#define HKS_FAIL(code, ...) do { hks_set_error(__VA_ARGS__); return code; } while (0)
+#define HKS_CUDA(call)                                                                    \
+    do {                                                                                  \
+        cudaError_t _e = (call);                                                          \
+        if (_e != cudaSuccess) HKS_FAIL(HKS_ECUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
+    } while (0)
+#define HKS_CHECK_LAUNCH() HKS_CUDA(cudaGetLastError())
+
+// ----------------------------------------------------------------------------------------------
+// launchers (ntt.cu, kernels.cu)
+enum NttDir { NTT_FWD = 0, NTT_INV = 1 };
+// pass 0 = first pass, pass 1 = second pass (forward: columns then rows; inverse: rows then columns)
+hks_status launch_ntt_pass(const hks_ctx *ctx, NttDir dir, int pass, int epi, NttArgs &a, cudaStream_t s);
+// full transform of a limb batch through both passes (in -> out, may alias), chunks > HKS_MAXB
+struct LimbList {
+    std::vector<u16> sin, sout, prime, sa, sb;
+    void push(u32 i, u32 o, u32 p, u32 a = 0, u32 b = 0xffff) {
+        sin.push_back((u16)i); sout.push_back((u16)o); prime.push_back((u16)p);
+        sa.push_back((u16)a); sb.push_back((u16)b);
+    }
+    size_t size() const { return sin.size(); }
+};
+hks_status run_ntt(const hks_ctx *ctx, NttDir dir, const LimbList &L, const u64 *in, u64 *out,
+                   const ulonglong2 *scale, u32 scale_mod, cudaStream_t s);
+hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 *out, const u64 *acc,
+                           const u64 *c0, u64 galois, cudaStream_t s);
+hks_status launch_bconv(const BconvArgs &a, u32 max_ndst, cudaStream_t s);
+hks_status launch_kip(const KipArgs &a, cudaStream_t s);
+hks_status launch_automorph(const u64 *in, u64 *out, u32 nlimbs, u32 log_n, u64 galois, cudaStream_t s);

@@ -1,0 +1,173 @@
+// kernels.cu -- base conversion (Eq. 1), evaluation-key inner product, EVAL automorphism.
+//
+// All three are cross-limb, same-coefficient passes (§3.6.1 dependency classes):
+// a thread owns two consecutive coefficients (16-byte vector loads/stores along the limb) and
+// loops over limbs.  They are integer-bound, not dense contractions, so no tensor cores: every
+// 60x60-bit product is four IMAD.WIDE.U32 on 30-bit halves accumulated carry-free in 64-bit
+// registers, reduced once per output (the paper's "128-bit accumulation, one reduction per
+// output").
+#include "internal.h"
+
+// ------------------------------------------------------------------------------------------------
+// Base conversion (§3.6.3, eq:conv):  out_t = [ sum_i y_i [qhat_i]_t ]_t.
+// grid.x: coefficient blocks (2 coefficients / thread), grid.y: group (digit or polynomial).
+template <int NSRC, bool PRESCALE>
+__global__ void __launch_bounds__(256) k_bconv(const __grid_constant__ BconvArgs A) {
+    const BconvGroup &G = A.g[blockIdx.y];
+    __shared__ uint2 smat[NSRC * BC_MAXDST];
+    __shared__ PrimeConst spc[BC_MAXDST];
+    const u32 ndst = G.ndst;
+    for (u32 idx = threadIdx.x; idx < NSRC * ndst; idx += blockDim.x) {
+        const u32 i = idx / ndst, u = idx - i * ndst;
+        smat[i * BC_MAXDST + u] = G.mat[(size_t)i * G.mat_stride + u];
+    }
+    for (u32 u = threadIdx.x; u < ndst; u += blockDim.x) spc[u] = A.pc[G.dst_prime[u]];
+    __syncthreads();
+
+    const size_t N = (size_t)1 << A.log_n;
+    const size_t x0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    if (x0 >= N) return;
+    u32 yl[NSRC][2], yh[NSRC][2];
+#pragma unroll
+    for (int i = 0; i < NSRC; i++) {
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(A.in + (size_t)G.src_slot[i] * N + x0);
+        u64 a = v.x, b = v.y;
+        if (PRESCALE) {
+            const u64 p = A.pc[G.src_prime[i]].p;
+            a = shoup(a, G.pre_w[i], G.pre_wp[i], p);
+            b = shoup(b, G.pre_w[i], G.pre_wp[i], p);
+        }
+        split30(a, yl[i][0], yh[i][0]);
+        split30(b, yl[i][1], yh[i][1]);
+    }
+    for (u32 u = 0; u < ndst; u++) {
+        Acc30 a0, a1;
+        acc_zero(a0);
+        acc_zero(a1);
+#pragma unroll
+        for (int i = 0; i < NSRC; i++) {
+            const uint2 m = smat[i * BC_MAXDST + u];
+            acc_mac(a0, yl[i][0], yh[i][0], m.x, m.y);
+            acc_mac(a1, yl[i][1], yh[i][1], m.x, m.y);
+        }
+        const PrimeConst pc = spc[u];
+        ulonglong2 o;
+        o.x = acc_reduce(a0, pc);
+        o.y = acc_reduce(a1, pc);
+        *reinterpret_cast<ulonglong2 *>(A.out + (size_t)G.dst_slot[u] * N + x0) = o;
+    }
+}
+
+template <int NSRC>
+static void bconv_go(const BconvArgs &a, cudaStream_t s) {
+    const u32 threads = 256;
+    const size_t N = (size_t)1 << a.log_n;
+    dim3 grid((u32)((N / 2 + threads - 1) / threads), a.ngroups);
+    ProfScope ps(K_BCONV, s);
+    if (a.prescale)
+        k_bconv<NSRC, true><<<grid, threads, 0, s>>>(a);
+    else
+        k_bconv<NSRC, false><<<grid, threads, 0, s>>>(a);
+    double words = 0;
+    for (u32 g = 0; g < a.ngroups; g++) words += a.g[g].nsrc + a.g[g].ndst;
+    ps.done(words * (double)N * 8.0);
+}
+
+hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
+    // all groups of one launch share nsrc (the caller groups them so)
+    switch (a.g[0].nsrc) {
+#define C(NS) case NS: bconv_go<NS>(a, s); break;
+        C(1) C(2) C(3) C(4) C(5) C(6) C(7) C(8) C(9) C(10) C(11) C(12) C(13) C(14) C(15) C(16)
+#undef C
+        default:
+            HKS_FAIL(HKS_EINVAL, "bconv: nsrc %u out of range", a.g[0].nsrc);
+    }
+    HKS_CHECK_LAUNCH();
+    return HKS_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Key inner product (§3.6.5 dot-product fusion):
+//   acc0[t] = sum_j D_j[t] * b_j[t],  acc1[t] = sum_j D_j[t] * a_j[t]   (mod t)
+// with D_j optionally read through the EVAL automorphism (hoisted rotation, reading 14).
+// grid.x: coefficient blocks, grid.y: extended limb t.
+__global__ void __launch_bounds__(256) k_kip(const __grid_constant__ KipArgs A) {
+    const size_t N = (size_t)1 << A.log_n;
+    const u32 t = blockIdx.y;
+    const size_t x0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    if (x0 >= N) return;
+    const u32 prime = t <= A.level ? t : A.nq + (t - A.level - 1);   // key limb index == prime index
+    const PrimeConst pc = A.pc[prime];
+    Acc30 a0[2], a1[2];
+    acc_zero(a0[0]); acc_zero(a0[1]);
+    acc_zero(a1[0]); acc_zero(a1[1]);
+    u32 s0 = 0, s1 = 1;
+    if (A.galois != 1) {
+        s0 = automorph_src((u32)x0, A.log_n, A.galois);
+        s1 = automorph_src((u32)x0 + 1, A.log_n, A.galois);
+    }
+    for (u32 j = 0; j < A.beta; j++) {
+        const bool own = A.c1 && t <= A.level && t / A.alpha == j;
+        const u64 *D = own ? A.c1 + (size_t)t * N : A.ext + ((size_t)j * A.ne + t) * N;
+        u64 d0, d1;
+        if (A.galois == 1) {
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(D + x0);
+            d0 = v.x;
+            d1 = v.y;
+        } else {
+            d0 = D[s0];
+            d1 = D[s1];
+        }
+        const ulonglong2 kb = *reinterpret_cast<const ulonglong2 *>(A.evk + (((size_t)j * 2 + 0) * A.nk + prime) * N + x0);
+        const ulonglong2 ka = *reinterpret_cast<const ulonglong2 *>(A.evk + (((size_t)j * 2 + 1) * A.nk + prime) * N + x0);
+        u32 dl, dh, ml, mh;
+        split30(d0, dl, dh);
+        split30(kb.x, ml, mh); acc_mac(a0[0], dl, dh, ml, mh);
+        split30(ka.x, ml, mh); acc_mac(a1[0], dl, dh, ml, mh);
+        split30(d1, dl, dh);
+        split30(kb.y, ml, mh); acc_mac(a0[1], dl, dh, ml, mh);
+        split30(ka.y, ml, mh); acc_mac(a1[1], dl, dh, ml, mh);
+    }
+    ulonglong2 o0, o1;
+    o0.x = acc_reduce(a0[0], pc);
+    o0.y = acc_reduce(a0[1], pc);
+    o1.x = acc_reduce(a1[0], pc);
+    o1.y = acc_reduce(a1[1], pc);
+    *reinterpret_cast<ulonglong2 *>(A.acc + (size_t)t * N + x0) = o0;
+    *reinterpret_cast<ulonglong2 *>(A.acc + ((size_t)A.ne + t) * N + x0) = o1;
+}
+
+hks_status launch_kip(const KipArgs &a, cudaStream_t s) {
+    const u32 threads = 256;
+    const size_t N = (size_t)1 << a.log_n;
+    dim3 grid((u32)((N / 2 + threads - 1) / threads), a.ne);
+    ProfScope ps(K_KIP, s);
+    k_kip<<<grid, threads, 0, s>>>(a);
+    HKS_CHECK_LAUNCH();
+    ps.done((3.0 * a.beta + 2.0) * a.ne * (double)N * 8.0);   // D_j + (b_j, a_j) read, acc0/acc1 written
+    return HKS_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// EVAL-form automorphism (SURVEY.md §8(c) reading 15): out[j] = in[j'].
+// The permutation maps aligned 2^b blocks onto aligned 2^b blocks, so a warp's gather stays
+// inside one 256-byte segment.
+__global__ void __launch_bounds__(256) k_automorph(const u64 *__restrict__ in, u64 *__restrict__ out,
+                                                  u32 log_n, u64 galois) {
+    const size_t N = (size_t)1 << log_n;
+    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t l = blockIdx.y;
+    if (j >= N) return;
+    out[l * N + j] = in[l * N + automorph_src(j, log_n, galois)];
+}
+
+hks_status launch_automorph(const u64 *in, u64 *out, u32 nlimbs, u32 log_n, u64 galois, cudaStream_t s) {
+    const u32 threads = 256;
+    const size_t N = (size_t)1 << log_n;
+    dim3 grid((u32)((N + threads - 1) / threads), nlimbs);
+    ProfScope ps(K_AUTOMORPH, s);
+    k_automorph<<<grid, threads, 0, s>>>(in, out, log_n, galois);
+    HKS_CHECK_LAUNCH();
+    ps.done(2.0 * nlimbs * (double)N * 8.0);
+    return HKS_OK;
+}

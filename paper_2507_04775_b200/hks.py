@@ -1,0 +1,231 @@
+"""Thin ctypes binding of libhks (include/hks.h).  Argument marshalling only: every step of the
+hot path runs in the library's CUDA kernels.  torch supplies device memory and streams.
+
+There is no CPU fallback: if libhks.so is missing or a call fails, this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhks.so")
+
+HKS_OK = 0
+STATUS = {0: "HKS_OK", 1: "HKS_EINVAL", 2: "HKS_ENOTPRIME", 3: "HKS_ENOTNTT", 4: "HKS_ERANGE", 5: "HKS_EDUP",
+          6: "HKS_EKEY", 7: "HKS_EGALOIS", 8: "HKS_ECUDA", 9: "HKS_ENOMEM", 10: "HKS_EDEVICE"}
+OP_MODUP, OP_MODDOWN, OP_KEYSWITCH, OP_ROTATE_HOISTED = 0, 1, 2, 3
+MAX_DIGITS = 64
+
+# every symbol include/hks.h declares (checked by tests/test_capi.py)
+EXPORTS = ("hks_last_error", "hks_ctx_create", "hks_ctx_destroy", "hks_ctx_query", "hks_ctx_psi",
+           "hks_workspace_bytes", "hks_ntt_fwd", "hks_ntt_inv", "hks_bconv", "hks_modup",
+           "hks_ksk_inner_product", "hks_moddown", "hks_keyswitch", "hks_automorph", "hks_rotate_hoisted",
+           "hks_launch_count", "hks_prof_enable", "hks_prof_read")
+
+
+class HksError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {detail}")
+        self.status = status
+
+
+class ProfEntry(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_uint64), ("total_ms", ctypes.c_double),
+                ("bytes", ctypes.c_double)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("log_n", ctypes.c_uint32), ("n", ctypes.c_uint32), ("num_q", ctypes.c_uint32),
+                ("num_p", ctypes.c_uint32), ("dnum", ctypes.c_uint32), ("alpha", ctypes.c_uint32),
+                ("level", ctypes.c_uint32), ("beta", ctypes.c_uint32),
+                ("digit_lo", ctypes.c_uint32 * MAX_DIGITS), ("digit_hi", ctypes.c_uint32 * MAX_DIGITS),
+                ("device", ctypes.c_int32)]
+
+
+_lib = None
+_vp = ctypes.c_void_p
+_u32 = ctypes.c_uint32
+_u64 = ctypes.c_uint64
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2507_04775_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        L.hks_last_error.restype = ctypes.c_char_p
+        L.hks_ctx_create.argtypes = [_u32, ctypes.POINTER(_u64), _u32, ctypes.POINTER(_u64), _u32, _u32,
+                                     ctypes.c_int, ctypes.POINTER(_vp)]
+        L.hks_ctx_destroy.argtypes = [_vp]
+        L.hks_ctx_destroy.restype = None
+        L.hks_ctx_query.argtypes = [_vp, _u32, ctypes.POINTER(Info)]
+        L.hks_ctx_psi.argtypes = [_vp, _u32, ctypes.POINTER(_u64)]
+        L.hks_workspace_bytes.argtypes = [_vp, ctypes.c_int, _u32, _u32]
+        L.hks_workspace_bytes.restype = ctypes.c_size_t
+        for f in ("hks_ntt_fwd", "hks_ntt_inv"):
+            getattr(L, f).argtypes = [_vp, _vp, ctypes.POINTER(_u32), _u32, _vp]
+        L.hks_bconv.argtypes = [_vp, _vp, ctypes.POINTER(_u32), _u32, ctypes.POINTER(_u32), _u32, _vp, _vp]
+        L.hks_modup.argtypes = [_vp, _vp, _u32, _vp, _vp, _vp]
+        L.hks_ksk_inner_product.argtypes = [_vp, _vp, _vp, _u32, _u64, _vp, _vp]
+        L.hks_moddown.argtypes = [_vp, _vp, _u32, _vp, _vp, _vp]
+        L.hks_keyswitch.argtypes = [_vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp]
+        L.hks_automorph.argtypes = [_vp, _vp, _u32, _u64, _vp, _vp]
+        L.hks_rotate_hoisted.argtypes = [_vp, _vp, _vp, _u32, _u32, ctypes.POINTER(_u64), ctypes.POINTER(_vp),
+                                         ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp]
+        L.hks_launch_count.restype = ctypes.c_uint64
+        L.hks_launch_count.argtypes = []
+        L.hks_prof_enable.argtypes = [ctypes.c_int]
+        L.hks_prof_read.argtypes = [ctypes.POINTER(ProfEntry), ctypes.c_int]
+        for f in EXPORTS[1:]:
+            if f not in ("hks_ctx_destroy", "hks_workspace_bytes", "hks_launch_count"):
+                getattr(L, f).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(st: int, where: str):
+    if st != HKS_OK:
+        raise HksError(st, where, lib().hks_last_error().decode())
+
+
+def _u32arr(seq: Sequence[int]):
+    return (_u32 * len(seq))(*[int(v) for v in seq])
+
+
+def _ptr(t) -> int:
+    """Device pointer of a torch tensor (or a raw int / None)."""
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class Context:
+    """hks_ctx handle: (N = 2^log_n, q chain, special primes p, dnum) on `device` (-1: host-only)."""
+
+    def __init__(self, log_n: int, q: Sequence[int], p: Sequence[int], dnum: int, device: int = 0):
+        qa = (_u64 * len(q))(*[int(v) for v in q])
+        pa = (_u64 * len(p))(*[int(v) for v in p])
+        h = _vp()
+        _check(lib().hks_ctx_create(log_n, qa, len(q), pa, len(p), dnum, device, ctypes.byref(h)), "hks_ctx_create")
+        self._h = h
+        self.log_n, self.n = log_n, 1 << log_n
+        self.q, self.p, self.dnum, self.device = tuple(q), tuple(p), dnum, device
+        self.nq, self.np = len(q), len(p)
+        self.alpha = -(-self.nq // dnum)
+
+    @classmethod
+    def from_config(cls, cfg, device: int = 0):
+        return cls(cfg.log_n, cfg.q, cfg.p, cfg.dnum, device)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hks_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def query(self, level: int) -> Info:
+        info = Info()
+        _check(lib().hks_ctx_query(self._h, level, ctypes.byref(info)), "hks_ctx_query")
+        return info
+
+    def psi(self, prime_idx: int) -> int:
+        v = _u64()
+        _check(lib().hks_ctx_psi(self._h, prime_idx, ctypes.byref(v)), "hks_ctx_psi")
+        return int(v.value)
+
+    def workspace_bytes(self, op: int, level: int, count: int = 0) -> int:
+        return int(lib().hks_workspace_bytes(self._h, op, level, count))
+
+    def beta(self, level: int) -> int:
+        return -(-(level + 1) // self.alpha)
+
+    def workspace(self, op: int, level: int, count: int = 0):
+        import torch
+        nbytes = self.workspace_bytes(op, level, count)
+        return torch.empty(max(nbytes // 8, 1), dtype=torch.uint64, device=f"cuda:{self.device}")
+
+
+def ntt_fwd(ctx: Context, x, prime_idx: Sequence[int], stream=None):
+    _check(lib().hks_ntt_fwd(ctx.handle, _ptr(x), _u32arr(prime_idx), len(prime_idx), _stream(stream)), "hks_ntt_fwd")
+
+
+def ntt_inv(ctx: Context, x, prime_idx: Sequence[int], stream=None):
+    _check(lib().hks_ntt_inv(ctx.handle, _ptr(x), _u32arr(prime_idx), len(prime_idx), _stream(stream)), "hks_ntt_inv")
+
+
+def bconv(ctx: Context, x, src_idx: Sequence[int], dst_idx: Sequence[int], out, stream=None):
+    _check(lib().hks_bconv(ctx.handle, _ptr(x), _u32arr(src_idx), len(src_idx), _u32arr(dst_idx), len(dst_idx),
+                           _ptr(out), _stream(stream)), "hks_bconv")
+
+
+def modup(ctx: Context, d, level: int, ext, ws, stream=None):
+    _check(lib().hks_modup(ctx.handle, _ptr(d), level, _ptr(ext), _ptr(ws), _stream(stream)), "hks_modup")
+
+
+def ksk_inner_product(ctx: Context, ext, evk, level: int, galois: int, acc, stream=None):
+    _check(lib().hks_ksk_inner_product(ctx.handle, _ptr(ext), _ptr(evk), level, galois, _ptr(acc), _stream(stream)),
+           "hks_ksk_inner_product")
+
+
+def moddown(ctx: Context, acc, level: int, out, ws, stream=None):
+    _check(lib().hks_moddown(ctx.handle, _ptr(acc), level, _ptr(out), _ptr(ws), _stream(stream)), "hks_moddown")
+
+
+def keyswitch(ctx: Context, c0, c1, level: int, evk, out0, out1, ws, stream=None):
+    _check(lib().hks_keyswitch(ctx.handle, _ptr(c0), _ptr(c1), level, _ptr(evk), _ptr(out0), _ptr(out1), _ptr(ws),
+                               _stream(stream)), "hks_keyswitch")
+
+
+def automorph(ctx: Context, x, nlimbs: int, galois: int, out, stream=None):
+    _check(lib().hks_automorph(ctx.handle, _ptr(x), nlimbs, galois, _ptr(out), _stream(stream)), "hks_automorph")
+
+
+def rotate_hoisted(ctx: Context, c0, c1, level: int, galois: Sequence[int], evks, outs0, outs1, ws, stream=None):
+    n = len(galois)
+    g = (_u64 * n)(*[int(v) for v in galois])
+    ek = (_vp * n)(*[_ptr(e) for e in evks])
+    o0 = (_vp * n)(*[_ptr(o) for o in outs0])
+    o1 = (_vp * n)(*[_ptr(o) for o in outs1])
+    _check(lib().hks_rotate_hoisted(ctx.handle, _ptr(c0), _ptr(c1), level, n, g, ek, o0, o1, _ptr(ws),
+                                    _stream(stream)), "hks_rotate_hoisted")
+
+
+def launch_count() -> int:
+    """Kernels libhks has launched in this process."""
+    return int(lib().hks_launch_count())
+
+
+def prof_enable(on: bool = True):
+    _check(lib().hks_prof_enable(1 if on else 0), "hks_prof_enable")
+
+
+def prof_read() -> dict:
+    """{kernel class: (launches, total_ms, algorithmic_bytes)} since the last read (synchronises)."""
+    arr = (ProfEntry * 16)()
+    k = lib().hks_prof_read(arr, 16)
+    return {arr[i].name.decode(): (int(arr[i].launches), float(arr[i].total_ms), float(arr[i].bytes))
+            for i in range(k)}

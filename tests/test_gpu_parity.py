@@ -1,0 +1,290 @@
+"""GPU parity: every hot-path step through the C ABI, bit-exact against the CPU oracle on the same
+seeded inputs (integer arithmetic -> the bar is bit-exact; BASELINE.json north_star).
+
+Sizes: small rings (several tiles, ragged digits, partial digits at lower levels) for every
+function, and the full BASELINE.json configurations (C1, C2 at N=2^16/L=29/dnum=3, C4 at
+N=2^17/L=35/dnum=4) in the same launch configuration bench.py times."""
+import numpy as np
+import pytest
+
+import hks_synth as S
+from helpers import Keys, empty_dev, encrypt_under, ks_bound, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+H = pytest.importorskip("paper_2507_04775_b200.hks")
+
+
+@pytest.fixture(autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+_CTX = {}
+
+
+def ctxs(orc, name):
+    if name not in _CTX:
+        cfg = S.config(name)
+        _CTX[name] = (cfg, H.Context.from_config(cfg, 0), orc.Ctx.from_config(cfg))
+    return _CTX[name]
+
+
+def edge_limbs(primes, n, g):
+    x = S.uniform_limbs(g, primes, n)
+    for b, p in enumerate(primes):
+        x[b, :8] = [0, 1, p - 1, p - 2, 2, 0, p - 1, 1]
+    return x
+
+
+# ------------------------------------------------------------------ NTT
+
+@pytest.mark.parametrize("log_n", [10, 11, 12, 13, 14, 15, 16, 17])
+def test_ntt_parity(orc, log_n):
+    primes = S.ntt_primes(log_n, 5, 60)
+    q, p = primes[1:], primes[:1]
+    ctx = H.Context(log_n, q, p, 1, 0)
+    o = orc.Ctx(log_n, q, p, 1)
+    g = S.rng(400 + log_n)
+    idx = [0, 1, 2, 3, 4, 2, 0]
+    x = edge_limbs([o.primes[i] for i in idx], o.n, g)
+    d = to_dev(x)
+    H.ntt_fwd(ctx, d, idx)
+    want = o.ntt(x, idx)
+    got = to_host(d)
+    assert (got == want).all()
+    H.ntt_inv(ctx, d, idx)
+    assert (to_host(d) == x).all()
+    y = to_dev(want)
+    H.ntt_inv(ctx, y, idx)
+    assert (to_host(y) == o.intt(want, idx)).all()
+
+
+def test_ntt_batch_invariance(orc):
+    cfg, ctx, o = ctxs(orc, "T16s")
+    g = S.rng(410)
+    idx = list(range(len(o.primes))) * 3
+    x = S.uniform_limbs(g, [o.primes[i] for i in idx], o.n)
+    d = to_dev(x)
+    H.ntt_fwd(ctx, d, idx)
+    whole = to_host(d)
+    for b in range(len(idx)):
+        e = to_dev(x[b:b + 1])
+        H.ntt_fwd(ctx, e, [idx[b]])
+        assert (to_host(e)[0] == whole[b]).all()
+
+
+def test_ntt_large_batch(orc):
+    # more limbs than one launch carries (HKS_MAXB = 256)
+    primes = S.ntt_primes(10, 3, 60)
+    ctx = H.Context(10, primes[1:], primes[:1], 1, 0)
+    o = orc.Ctx(10, primes[1:], primes[:1], 1)
+    g = S.rng(411)
+    idx = [i % 3 for i in range(300)]
+    x = S.uniform_limbs(g, [o.primes[i] for i in idx], o.n)
+    d = to_dev(x)
+    H.ntt_fwd(ctx, d, idx)
+    assert (to_host(d) == o.ntt(x, idx)).all()
+
+
+# ------------------------------------------------------------------ BConv, automorphism
+
+@pytest.mark.parametrize("name,src,dst", [("T12", [0, 1, 2], [3, 4, 5, 6, 7, 8, 9]),
+                                          ("C2", list(range(10)), list(range(10, 40))),
+                                          ("C2", list(range(30, 40)), list(range(30))),
+                                          ("T12", [5], [0, 1, 9])])
+def test_bconv_parity(orc, name, src, dst):
+    cfg, ctx, o = ctxs(orc, name)
+    g = S.rng(420)
+    x = edge_limbs([o.primes[i] for i in src], o.n, g)
+    out = empty_dev((len(dst), o.n))
+    H.bconv(ctx, to_dev(x), src, dst, out)
+    assert (to_host(out) == o.bconv(x, src, dst)).all()
+
+
+@pytest.mark.parametrize("name", ["T12", "C2"])
+def test_automorph_parity(orc, name):
+    cfg, ctx, o = ctxs(orc, name)
+    g = S.rng(430)
+    x = S.uniform_limbs(g, o.primes[:4], o.n)
+    for k in (S.galois_rot(1, cfg.log_n), S.galois_rot(7, cfg.log_n), S.GALOIS_CONJ(cfg.log_n)):
+        out = empty_dev((4, o.n))
+        H.automorph(ctx, to_dev(x), 4, k, out)
+        assert (to_host(out) == o.automorph(x, k)).all()
+
+
+# ------------------------------------------------------------------ ModUp, KIP, ModDown
+
+@pytest.mark.parametrize("name,level", [("T12", 6), ("T12", 3), ("T12", 0), ("C2", 29), ("C2", 20), ("C2", 9)])
+def test_modup_parity(orc, name, level):
+    cfg, ctx, o = ctxs(orc, name)
+    g = S.rng(440 + level)
+    d = edge_limbs(o.q[: level + 1], o.n, g)
+    beta = ctx.beta(level)
+    ne = level + 1 + o.np
+    ext = empty_dev((beta, ne, o.n))
+    ws = ctx.workspace(H.OP_MODUP, level)
+    H.modup(ctx, to_dev(d), level, ext, ws)
+    assert (to_host(ext) == o.modup(d, level)).all()
+
+
+@pytest.mark.parametrize("name,level,galois", [("T12", 6, 1), ("T12", 4, 5), ("C2", 29, 1), ("C2", 15, 25)])
+def test_kip_parity(orc, name, level, galois):
+    cfg, ctx, o = ctxs(orc, name)
+    g = S.rng(450 + level)
+    beta = ctx.beta(level)
+    eidx = o.ext_primes(level)
+    ext = np.stack([S.uniform_limbs(g, [o.primes[i] for i in eidx], o.n) for _ in range(beta)])
+    nk = o.nq + o.np
+    evk = np.stack([S.uniform_limbs(g, o.primes, o.n) for _ in range(2 * o.dnum)]).reshape(o.dnum, 2, nk, o.n)
+    acc = empty_dev((2, len(eidx), o.n))
+    H.ksk_inner_product(ctx, to_dev(ext), to_dev(evk), level, galois, acc)
+    assert (to_host(acc) == o.kip(ext, evk, level, galois)).all()
+
+
+@pytest.mark.parametrize("name,level", [("T12", 6), ("T12", 1), ("C2", 29), ("C2", 9), ("C2", 0)])
+def test_moddown_parity(orc, name, level):
+    cfg, ctx, o = ctxs(orc, name)
+    g = S.rng(460 + level)
+    eidx = o.ext_primes(level)
+    acc = edge_limbs([o.primes[i] for i in eidx], o.n, g)
+    out = empty_dev((level + 1, o.n))
+    ws = ctx.workspace(H.OP_MODDOWN, level)
+    H.moddown(ctx, to_dev(acc), level, out, ws)
+    assert (to_host(out) == o.moddown(acc, level)).all()
+
+
+# ------------------------------------------------------------------ KeySwitch end to end
+
+_KEYS = {}
+
+
+def relin_key(o, name):
+    if name not in _KEYS:
+        cfg = S.config(name)
+        k = Keys(o, cfg.seed)
+        _KEYS[name] = (k, k.relin())
+    return _KEYS[name]
+
+
+def run_ks(ctx, c0, c1, level, evk_dev):
+    out0 = empty_dev(c0.shape)
+    out1 = empty_dev(c1.shape)
+    ws = ctx.workspace(H.OP_KEYSWITCH, level)
+    H.keyswitch(ctx, to_dev(c0), to_dev(c1), level, evk_dev, out0, out1, ws)
+    return to_host(out0), to_host(out1)
+
+
+@pytest.mark.parametrize("name,levels", [("C1", [2]), ("C1p", [2, 1, 0]), ("T10", [4, 2]),
+                                         ("T12", [6, 5, 3, 0]), ("T16s", [5, 1]), ("T17s", [4])])
+def test_keyswitch_parity_small(orc, name, levels):
+    cfg, ctx, o = ctxs(orc, name)
+    keys, evk = relin_key(o, name)
+    evk_d = to_dev(evk)
+    s2 = o.mul(keys.s_eval, keys.s_eval, list(range(keys.nk)))
+    g = S.rng(cfg.seed + 7)
+    for level in levels:
+        m, c0, c1 = encrypt_under(o, g, s2, level, 20)
+        got0, got1 = run_ks(ctx, c0, c1, level, evk_d)
+        want0, want1 = o.keyswitch(c0, c1, evk, level)
+        assert (got0 == want0).all() and (got1 == want1).all(), level
+        dec = o.crt_centered(o.decrypt_coeff(got0, got1, keys.s_eval, level), level)
+        err = max(abs(a - int(b)) for a, b in zip(dec, m))
+        assert err <= ks_bound(o, level, keys.B_e, keys.h)
+
+
+@pytest.mark.parametrize("level", [29, 20, 19, 9, 0])
+def test_keyswitch_parity_c2(orc, level):
+    """BASELINE.json configs[1]: N=2^16, L=29, dnum=3, 60-bit primes; level sweep across digit drops."""
+    cfg, ctx, o = ctxs(orc, "C2")
+    keys, evk = relin_key(o, "C2")
+    g = S.rng(cfg.seed + 100 + level)
+    c0 = S.uniform_limbs(g, o.q[: level + 1], o.n)
+    c1 = edge_limbs(o.q[: level + 1], o.n, g)
+    got0, got1 = run_ks(ctx, c0, c1, level, to_dev(evk))
+    want0, want1 = o.keyswitch(c0, c1, evk, level)
+    assert (got0 == want0).all() and (got1 == want1).all()
+
+
+def test_keyswitch_c2_decrypts(orc):
+    cfg, ctx, o = ctxs(orc, "C2")
+    keys, evk = relin_key(o, "C2")
+    s2 = o.mul(keys.s_eval, keys.s_eval, list(range(keys.nk)))
+    m, c0, c1 = encrypt_under(o, S.rng(5), s2, 29, 20)
+    got0, got1 = run_ks(ctx, c0, c1, 29, to_dev(evk))
+    dec = o.crt_centered(o.decrypt_coeff(got0, got1, keys.s_eval, 29), 29)
+    assert max(abs(a - int(b)) for a, b in zip(dec, m)) <= ks_bound(o, 29, keys.B_e, keys.h)
+
+
+@pytest.mark.slow
+def test_keyswitch_parity_c4(orc):
+    """BASELINE.json configs[3] parameters: N=2^17, L=35, dnum=4 (single GPU, unsharded)."""
+    cfg, ctx, o = ctxs(orc, "C4")
+    g = S.rng(cfg.seed)
+    nk = o.nq + o.np
+    evk = np.stack([S.uniform_limbs(g, o.primes, o.n) for _ in range(2 * o.dnum)]).reshape(o.dnum, 2, nk, o.n)
+    for level in (35, 17):
+        c0 = S.uniform_limbs(g, o.q[: level + 1], o.n)
+        c1 = S.uniform_limbs(g, o.q[: level + 1], o.n)
+        got0, got1 = run_ks(ctx, c0, c1, level, to_dev(evk))
+        want0, want1 = o.keyswitch(c0, c1, evk, level)
+        assert (got0 == want0).all() and (got1 == want1).all(), level
+
+
+def test_keyswitch_c0_null_and_determinism(orc):
+    cfg, ctx, o = ctxs(orc, "T12")
+    keys, evk = relin_key(o, "T12")
+    g = S.rng(470)
+    level = 6
+    c1 = S.uniform_limbs(g, o.q[: level + 1], o.n)
+    z = np.zeros_like(c1)
+    evk_d = to_dev(evk)
+    out0, out1 = empty_dev(c1.shape), empty_dev(c1.shape)
+    ws = ctx.workspace(H.OP_KEYSWITCH, level)
+    H.keyswitch(ctx, None, to_dev(c1), level, evk_d, out0, out1, ws)
+    want0, want1 = o.keyswitch(z, c1, evk, level)
+    assert (to_host(out0) == want0).all() and (to_host(out1) == want1).all()
+    a0, a1 = run_ks(ctx, z, c1, level, evk_d)
+    b0, b1 = run_ks(ctx, z, c1, level, evk_d)
+    assert (a0 == b0).all() and (a1 == b1).all() and (a0 == want0).all()
+
+
+# ------------------------------------------------------------------ hoisted rotations
+
+@pytest.mark.parametrize("name,level,rots", [("T12", 6, [1, 2, 5]), ("C2", 29, [1, 3])])
+def test_rotate_hoisted_parity(orc, name, level, rots):
+    cfg, ctx, o = ctxs(orc, name)
+    keys = Keys(o, cfg.seed + 11)
+    ks = [S.galois_rot(r, cfg.log_n) for r in rots] + [S.GALOIS_CONJ(cfg.log_n)]
+    evks = [keys.rot(k) for k in ks]
+    g = S.rng(480)
+    m, c0, c1 = encrypt_under(o, g, keys.s_eval, level, 20)
+    outs0 = [empty_dev(c0.shape) for _ in ks]
+    outs1 = [empty_dev(c0.shape) for _ in ks]
+    ws = ctx.workspace(H.OP_ROTATE_HOISTED, level, len(ks))
+    evk_d = [to_dev(e) for e in evks]
+    H.rotate_hoisted(ctx, to_dev(c0), to_dev(c1), level, ks, evk_d, outs0, outs1, ws)
+    w0, w1 = o.rotate_hoisted(c0, c1, evks, level, ks)
+    for r in range(len(ks)):
+        assert (to_host(outs0[r]) == w0[r]).all() and (to_host(outs1[r]) == w1[r]).all(), r
+
+
+# ------------------------------------------------------------------ error behaviour
+
+def test_error_codes(orc):
+    cfg, ctx, o = ctxs(orc, "T12")
+    x = empty_dev((2, o.n))
+    with pytest.raises(H.HksError) as e:
+        H.automorph(ctx, x, 1, 4, x[1:])                     # even Galois element
+    assert e.value.status == 7
+    with pytest.raises(H.HksError) as e:
+        H.automorph(ctx, x, 2, 5, x[1:])                     # overlapping in/out
+    assert e.value.status == 1
+    with pytest.raises(H.HksError) as e:
+        H.ntt_fwd(ctx, x, [0, 99])                           # bad prime index
+    assert e.value.status == 1
+    with pytest.raises(H.HksError) as e:
+        H.modup(ctx, x, 7, x, x)                             # level > L
+    assert e.value.status == 1
