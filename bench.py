@@ -1,0 +1,524 @@
+#!/usr/bin/env python
+"""bench.py -- hybrid key switching on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+Default workload (BASELINE.json configs[1], `C2`): one relinearisation KeySwitch of one ciphertext at
+N=2^16, L=29 (30 Q limbs), K=10 special primes, dnum=3, 60-bit primes, level 29.  A step = one
+KeySwitch (all of SURVEY.md §8(a): INTT, ModUp BConv, NTT, key inner product, ModDown).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl hks|reference] [--config C2|C1|C4]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, ciphertexts sharded: weak scaling)
+
+Timing: W untimed steps, then K steps between barrier + synchronize, CUDA events on the launch
+stream, max over ranks.  L2: every step uses the next of `--sets` distinct (ciphertext, key) sets
+(total > 4x the 126 MB L2), so nothing is L2-resident from the previous step.
+Inputs are seeded synthetic residues (timing is data-independent; bit-exactness with real keys is
+the job of tests/test_gpu_parity.py).  `--impl reference` times the CPU oracle (oracle/) instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import hks_synth as S  # noqa: E402
+
+METRIC = "KeySwitch ops/s at N=2^16,L=29,dnum=3; NTT limbs/s; % HBM peak"
+HBM_FALLBACK_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="hks", choices=["hks", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--level", type=int, default=None)
+    ap.add_argument("--sets", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip e2e / NTT / profile legs (for ncu runs)")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def workload_desc(cfg, level):
+    base = f"N=2^{cfg.log_n}, L={cfg.L}, K={cfg.K}, dnum={cfg.dnum}"
+    if cfg.name == "C3":
+        return (f"C3: 8 ciphertexts x 8 hoisted rotation KeySwitches (r=1..8, Galois 5^r), {base}, level={level}, "
+                f"keys replicated, ciphertexts sharded over ranks")
+    if cfg.name == "C5":
+        return (f"C5: BOOT_SHAPE v1 (SURVEY.md 8(d)): CtS 3x(7 hoisted baby + 7 giant rotations) at l=29..27, "
+                f"conjugation at 26, 12 relin KS + rescale-shaped INTT/NTT at l=26..15, StC 3x14 at l=14..12 "
+                f"= 97 KeySwitches, {base}")
+    return f"{cfg.name}: one relinearisation KeySwitch per ciphertext, {base}, level={level}, primes<2^{cfg.bits}"
+
+
+# ---------------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock and clock-event reasons DURING the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, dev_index: int):
+        self.ok = False
+        self.samples, self.reasons = [], 0
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            h = None
+            try:
+                uuid = str(torch.cuda.get_device_properties(dev_index).uuid)
+                h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.h = h
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _loop(self):
+        nv = self.nv
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop:
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(get_r(self.h))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.stop = False
+            self.t = threading.Thread(target=self._loop, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop = True
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"error": getattr(self, "err", "nvml unavailable")}
+        s = sorted(self.samples)
+        med = s[len(s) // 2] if s else None
+        reasons = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(s)}
+
+
+# ---------------------------------------------------------------------------------------------- inputs
+def make_sets(cfg, level, nsets, dev, seed):
+    """Seeded uniform residues per limb, generated on the device (torch Philox, seed per rank)."""
+    import torch
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    n = cfg.n
+    primes = list(cfg.q) + list(cfg.p)
+    nk = len(primes)
+
+    def limbs(pr):
+        t = torch.empty((len(pr), n), dtype=torch.int64, device=dev)
+        for i, q in enumerate(pr):
+            t[i] = torch.randint(0, int(q), (n,), generator=g, device=dev, dtype=torch.int64)
+        return t
+
+    sets = []
+    for _ in range(nsets):
+        c0 = limbs(cfg.q[: level + 1])
+        c1 = limbs(cfg.q[: level + 1])
+        evk = torch.stack([limbs(primes) for _ in range(2 * cfg.dnum)]).reshape(cfg.dnum, 2, nk, n)
+        sets.append({"c0": c0, "c1": c1, "evk": evk,
+                     "out0": torch.empty_like(c0), "out1": torch.empty_like(c1)})
+    return sets
+
+
+# ---------------------------------------------------------------------------------------------- cpu
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_ks_timer(cfg, level, seed):
+    import numpy as np
+    import oracle
+    o = oracle.Ctx.from_config(cfg)
+    g = S.rng(seed)
+    nk = len(cfg.q) + len(cfg.p)
+    evk = np.stack([S.uniform_limbs(g, o.primes, o.n) for _ in range(2 * cfg.dnum)]).reshape(cfg.dnum, 2, nk, o.n)
+    c0 = S.uniform_limbs(g, cfg.q[: level + 1], o.n)
+    c1 = S.uniform_limbs(g, cfg.q[: level + 1], o.n)
+
+    def one():
+        t = time.perf_counter()
+        o.keyswitch(c0, c1, evk, level)
+        return time.perf_counter() - t
+    return one
+
+
+def cpu_baseline(cfg, level, budget_s=20.0):
+    one = oracle_ks_timer(cfg, level, 7)
+    ts = [one()]
+    while sum(ts) < budget_s * 0.5 and len(ts) < 10:
+        ts.append(one())
+    return {"value": len(ts) / sum(ts), "unit": "KeySwitch/s", "cores": cpu_cores(), "kind": "oracle",
+            "sample": f"{len(ts)} full KeySwitches of {cfg.name} at level {level} (oracle/oracle.c, %-on-u128, "
+                      f"OpenMP over limbs), {sum(ts):.1f} s"}
+
+
+def run_reference(args, cfg, level):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    one = oracle_ks_timer(cfg, level, 7)
+    budget = 150.0
+    t_w = one()                                   # first warm-up step also sizes the run
+    for _ in range(max(0, min(args.warmup, 3) - 1)):
+        one()
+    k = max(1, min(args.steps, int(budget / max(t_w, 1e-3))))
+    ts = [one() for _ in range(k)]
+    v = k / sum(ts)
+    line = {"metric": METRIC, "value": v, "unit": "KeySwitch/s", "n_gpus": args.gpus, "steps": k,
+            "warmup": min(args.warmup, 3), "ms_per_step": 1e3 * sum(ts) / k, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": workload_desc(cfg, level), "parallelism": "cpu oracle, rank 0 only"},
+            "cpu_baseline": {"value": v, "unit": "KeySwitch/s", "kind": "oracle", "cores": cpu_cores(),
+                             "sample": f"{k} full KeySwitches (steps capped at {budget:.0f} s of CPU time; "
+                                       f"requested {args.steps})"},
+            "e2e": {"value": v, "unit": "KeySwitch/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------- workloads
+class KSWorkload:
+    """C1 / C2 / C4 (unsharded): one relinearisation KeySwitch per step, rotating (ct, key) sets."""
+    unit = "KeySwitch/s"
+    scaling = "weak"
+
+    def __init__(self, H, ctx, cfg, level, nsets, dev, seed, sid):
+        self.H, self.ctx, self.cfg, self.level, self.sid = H, ctx, cfg, level, sid
+        self.sets = make_sets(cfg, level, nsets, dev, seed)
+        self.ws = ctx.workspace(H.OP_KEYSWITCH, level)
+        self.units = 1
+        self.nsets = nsets
+
+    def step(self, i):
+        s = self.sets[i % len(self.sets)]
+        self.H.keyswitch(self.ctx, s["c0"], s["c1"], self.level, s["evk"], s["out0"], s["out1"], self.ws, self.sid)
+
+    def alg_bytes(self):
+        c, l = self.cfg, self.level
+        return (4 * (l + 1) + 2 * c.beta(l) * (l + 1 + c.K)) * c.n * 8
+
+    def l2_note(self):
+        c, l = self.cfg, self.level
+        mb = self.nsets * (2 * c.dnum * (c.L + 1 + c.K) + 2 * (l + 1)) * c.n * 8 / 1e6
+        return f"{self.nsets} rotating (ct, key) sets, {mb:.0f} MB > 4x 126 MB L2"
+
+    # e2e: H2D of (c0, c1) from pinned host memory, KeySwitch, D2H of (out0, out1)
+    def e2e_setup(self):
+        self.hsets = [{k: self.sets[i][k].cpu().pin_memory() for k in ("c0", "c1")} for i in range(min(2, len(self.sets)))]
+        self.hout0 = torch_empty_pinned_like(self.sets[0]["out0"])
+        self.hout1 = torch_empty_pinned_like(self.sets[0]["out1"])
+        return 4 * 0 + 2 * (self.level + 1) * self.cfg.n * 8, 2 * (self.level + 1) * self.cfg.n * 8
+
+    def e2e_step(self, i):
+        s, h = self.sets[i % len(self.sets)], self.hsets[i % len(self.hsets)]
+        s["c0"].copy_(h["c0"], non_blocking=True)
+        s["c1"].copy_(h["c1"], non_blocking=True)
+        self.H.keyswitch(self.ctx, s["c0"], s["c1"], self.level, s["evk"], s["out0"], s["out1"], self.ws, self.sid)
+        self.hout0.copy_(s["out0"], non_blocking=True)
+        self.hout1.copy_(s["out1"], non_blocking=True)
+
+
+class C3Workload:
+    """C3: 8 ciphertexts x 8 hoisted rotations, ciphertexts sharded over ranks (keys replicated)."""
+    unit = "rotation-KeySwitch/s"
+    scaling = "strong"
+
+    def __init__(self, H, ctx, cfg, level, world, rank, dev, seed, sid):
+        import torch
+        self.H, self.ctx, self.cfg, self.level, self.sid = H, ctx, cfg, level, sid
+        nct_total, self.nrot = 8, 8
+        assert nct_total % world == 0, "C3 shards 8 ciphertexts: world size must divide 8"
+        self.nct = nct_total // world
+        self.galois = [S.galois_rot(r, cfg.log_n) for r in range(1, self.nrot + 1)]
+        keysets = make_sets(cfg, level, self.nrot, dev, seed)            # one key per rotation
+        self.evks = [k["evk"] for k in keysets]
+        cts = make_sets(cfg, level, self.nct, dev, seed + 7)
+        for k in keysets:
+            del k["c0"], k["c1"], k["out0"], k["out1"]
+        self.cts = [(c["c0"], c["c1"]) for c in cts]
+        shape = cts[0]["c0"].shape
+        self.out0 = [[torch.empty(shape, dtype=torch.int64, device=dev) for _ in range(self.nrot)] for _ in range(self.nct)]
+        self.out1 = [[torch.empty(shape, dtype=torch.int64, device=dev) for _ in range(self.nrot)] for _ in range(self.nct)]
+        self.ws = ctx.workspace(H.OP_ROTATE_HOISTED, level, self.nrot)
+        self.units = self.nct * self.nrot
+
+    def step(self, i):
+        for c in range(self.nct):
+            c0, c1 = self.cts[c]
+            self.H.rotate_hoisted(self.ctx, c0, c1, self.level, self.galois, self.evks, self.out0[c], self.out1[c],
+                                  self.ws, self.sid)
+
+    def alg_bytes(self):
+        c, l = self.cfg, self.level
+        key = 2 * c.beta(l) * (l + 1 + c.K) * c.n * 8
+        ct = 2 * (l + 1) * c.n * 8
+        return self.nrot * key + self.nct * ct + self.units * ct     # keys once, ct in, rotated cts out
+
+    def l2_note(self):
+        c = self.cfg
+        return f"8 rotation keys ({8 * 2 * c.dnum * (c.L + 1 + c.K) * c.n * 8 / 1e6:.0f} MB) > 4x 126 MB L2"
+
+
+class C5Workload:
+    """C5 = BOOT_SHAPE v1 on one ciphertext per rank (replicas)."""
+    unit = "sequences/s"
+    scaling = "weak"
+
+    def __init__(self, H, ctx, cfg, dev, seed, sid):
+        import torch
+        self.H, self.ctx, self.cfg, self.sid = H, ctx, cfg, sid
+        L = cfg.L
+        bs = [S.galois_rot(r, cfg.log_n) for r in range(1, 8)]              # baby steps 1..7
+        gs = [S.galois_rot(8 * r, cfg.log_n) for r in range(1, 8)]          # giant steps 8..56
+        self.baby, self.giant, self.conj = bs, gs, S.GALOIS_CONJ(cfg.log_n)
+        keys = make_sets(cfg, L, 16, dev, seed)
+        self.kb = [keys[i]["evk"] for i in range(7)]
+        self.kg = [keys[7 + i]["evk"] for i in range(7)]
+        self.krelin, self.kconj = keys[14]["evk"], keys[15]["evk"]
+        for k in keys:
+            del k["c0"], k["c1"], k["out0"], k["out1"]
+        ct = make_sets(cfg, L, 1, dev, seed + 3)[0]
+        self.c0, self.c1 = ct["c0"], ct["c1"]
+        shape = self.c0.shape
+        self.o0 = [torch.empty(shape, dtype=torch.int64, device=dev) for _ in range(7)]
+        self.o1 = [torch.empty(shape, dtype=torch.int64, device=dev) for _ in range(7)]
+        self.t0 = torch.empty(shape, dtype=torch.int64, device=dev)
+        self.t1 = torch.empty(shape, dtype=torch.int64, device=dev)
+        self.ws = ctx.workspace(H.OP_ROTATE_HOISTED, L, 7)
+        self.units = 1
+        self.ks_per_seq = 97
+
+    def _stage(self, level):
+        H, c, s = self.H, self.ctx, self.sid
+        a0, a1 = self.c0[: level + 1], self.c1[: level + 1]
+        H.rotate_hoisted(c, a0, a1, level, self.baby, self.kb, [o[: level + 1] for o in self.o0],
+                         [o[: level + 1] for o in self.o1], self.ws, s)                    # 7 hoisted baby steps
+        for g in range(7):                                                                 # 7 giant steps
+            H.rotate_hoisted(c, self.o0[g][: level + 1], self.o1[g][: level + 1], level, [self.giant[g]],
+                             [self.kg[g]], [self.t0[: level + 1]], [self.t1[: level + 1]], self.ws, s)
+
+    def step(self, i):
+        H, c, s, L = self.H, self.ctx, self.sid, self.cfg.L
+        for level in (L, L - 1, L - 2):                                                    # CoeffToSlot
+            self._stage(level)
+        lv = L - 3
+        H.rotate_hoisted(c, self.c0[: lv + 1], self.c1[: lv + 1], lv, [self.conj], [self.kconj],
+                         [self.t0[: lv + 1]], [self.t1[: lv + 1]], self.ws, s)             # conjugation
+        for level in range(L - 3, L - 15, -1):                                             # EvalMod stand-in
+            H.keyswitch(c, self.c0[: level + 1], self.c1[: level + 1], level, self.krelin, self.t0[: level + 1],
+                        self.t1[: level + 1], self.ws, s)
+            H.ntt_inv(c, self.t0[: level + 1], list(range(level + 1)), s)                    # rescale-shaped
+            H.ntt_fwd(c, self.t0[: level], list(range(level)), s)
+        for level in (L - 15, L - 16, L - 17):                                             # SlotToCoeff
+            self._stage(level)
+
+    def alg_bytes(self):
+        c = self.cfg
+        tot = 0
+        for l in [c.L, c.L - 1, c.L - 2] * 1 + [c.L - 15, c.L - 16, c.L - 17]:
+            tot += 14 * (4 * (l + 1) + 2 * c.beta(l) * (l + 1 + c.K)) * c.n * 8
+        for l in range(c.L - 3, c.L - 15, -1):
+            tot += (4 * (l + 1) + 2 * c.beta(l) * (l + 1 + c.K) + 4 * (l + 1)) * c.n * 8
+        return tot
+
+    def l2_note(self):
+        c = self.cfg
+        return f"16 keys ({16 * 2 * c.dnum * (c.L + 1 + c.K) * c.n * 8 / 1e9:.2f} GB) >> 126 MB L2"
+
+
+def torch_empty_pinned_like(t):
+    import torch
+    return torch.empty(t.shape, dtype=t.dtype, device="cpu").pin_memory()
+
+
+# ---------------------------------------------------------------------------------------------- main
+def main():
+    args = parse()
+    cfg = S.config(args.config)
+    level = cfg.L if args.level is None else args.level
+    if args.impl == "reference":
+        run_reference(args, cfg, level)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2507_04775_b200 import hks as H
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(dev))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world > 1:
+            t = torch.tensor([x], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return x
+
+    ctx = H.Context.from_config(cfg, local)
+    stream = torch.cuda.current_stream()
+    sid = stream.cuda_stream
+    seed = cfg.seed * 1000 + rank
+    if cfg.name == "C3":
+        wl = C3Workload(H, ctx, cfg, level, world, rank, dev, seed, sid)
+    elif cfg.name == "C5":
+        wl = C5Workload(H, ctx, cfg, dev, seed, sid)
+    else:
+        wl = KSWorkload(H, ctx, cfg, level, args.sets, dev, seed, sid)
+
+    for i in range(args.warmup):
+        wl.step(i)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = H.launch_count()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            wl.step(i)
+        ev1.record(stream)
+        ev1.synchronize()
+    launches = H.launch_count() - n0
+    torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    total_units = world * wl.units if wl.scaling == "weak" else 8 * wl.nrot if cfg.name == "C3" else wl.units
+    value = total_units * args.steps / (ms / 1e3)
+
+    hbm_peak, peak_src = peaks()
+    extra = {}
+    if not args.quick:
+        # ---- per-kernel breakdown: CUDA events recorded by libhks around each launch, same stream
+        H.prof_enable(True)
+        nprof = max(1, min(args.steps, 100 if cfg.name not in ("C3", "C5") else 5))
+        for i in range(nprof):
+            wl.step(i)
+        prof = H.prof_read()
+        H.prof_enable(False)
+        tot = sum(v[1] for v in prof.values())
+        kern = {k: {"launches_per_step": v[0] / nprof, "ms_per_step": v[1] / nprof, "share": v[1] / tot,
+                    "avg_launch_us": 1e3 * v[1] / v[0], "alg_bytes_per_launch": v[2] / v[0],
+                    "achieved_gbs": (v[2] / v[0]) / (1e-3 * v[1] / v[0]) / 1e9}
+                for k, v in prof.items()}
+        dom = max(kern, key=lambda k: kern[k]["share"])
+        d = kern[dom]
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            with open(tpath) as f:
+                traffic = json.load(f).get(cfg.name, {}).get(dom)
+        extra["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": d["achieved_gbs"], "peak": hbm_peak,
+                             "unit": "GB/s", "frac": d["achieved_gbs"] / hbm_peak, "traffic": traffic,
+                             "peak_source": peak_src, "share_of_step": d["share"]}
+        extra["kernels"] = kern
+        alg = wl.alg_bytes()
+        extra["step_hbm"] = {"alg_bytes": alg, "achieved_gbs": alg / (ms / args.steps * 1e-3) / 1e9,
+                             "frac": alg / (ms / args.steps * 1e-3) / 1e9 / hbm_peak}
+
+        # ---- NTT limbs/s: the ModUp NTT batch (beta(l+1+K) - (l+1) limbs), 4 buffers > L2
+        beta = cfg.beta(level)
+        nl = beta * (level + 1 + cfg.K) - (level + 1)
+        prim = list(range(len(cfg.q) + len(cfg.p)))
+        idx = [prim[i % len(prim)] for i in range(nl)]
+        bufs = [torch.randint(0, int(cfg.p[-1]), (nl, cfg.n), device=dev, dtype=torch.int64) for _ in range(4)]
+        for kind, fn in (("fwd", H.ntt_fwd), ("inv", H.ntt_inv)):
+            for i in range(3):
+                fn(ctx, bufs[i % 4], idx, sid)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            it = 40
+            e0.record(stream)
+            for i in range(it):
+                fn(ctx, bufs[i % 4], idx, sid)
+            e1.record(stream)
+            e1.synchronize()
+            t = e0.elapsed_time(e1) / it
+            extra[f"ntt_{kind}_limbs_per_s"] = nl / (t * 1e-3) * world
+            extra[f"ntt_{kind}_hbm_frac"] = 2 * nl * cfg.n * 8 / (t * 1e-3) / 1e9 / hbm_peak
+        del bufs
+
+        # ---- e2e: through the public API from pinned host buffers, H2D + op + D2H per step
+        if hasattr(wl, "e2e_setup"):
+            h2d, d2h = wl.e2e_setup()
+            e_steps = min(args.steps, 50)
+            for i in range(3):
+                wl.e2e_step(i)
+            torch.cuda.synchronize()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(e_steps):
+                wl.e2e_step(i)
+            e1.record(stream)
+            e1.synchronize()
+            et = max_over_ranks(e0.elapsed_time(e1))
+            extra["e2e"] = {"value": world * wl.units * e_steps / (et / 1e3), "unit": wl.unit,
+                            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e_steps}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": wl.unit, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": wl.scaling, "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "config": {"workload": workload_desc(cfg, level), "N": cfg.n, "L": cfg.L, "K": cfg.K,
+                           "dnum": cfg.dnum, "level": level,
+                           "parallelism": f"{'replicas' if cfg.name == 'C5' else 'ciphertexts sharded'} over {world} GPU(s)",
+                           "l2": wl.l2_note()},
+                "gpu_launches": launches, "clocks": clk.summary()}
+        if cfg.name == "C5":
+            line["keyswitch_per_s"] = value * wl.ks_per_seq
+        line.update(extra)
+        if "ntt_fwd_limbs_per_s" in extra:
+            line["ntt_limbs_per_s"] = extra["ntt_fwd_limbs_per_s"]
+        if world == 1 and not args.no_cpu_baseline and not args.quick and isinstance(wl, KSWorkload):
+            line["cpu_baseline"] = cpu_baseline(cfg, level)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -98,6 +98,10 @@ class Config:
     def beta(self, level: int) -> int:
         return -(-(level + 1) // self.alpha)
 
+    @property
+    def bits(self) -> int:
+        return max(max(self.q), max(self.p)).bit_length()
+
 
 def _mk(name, log_n, nq, np_, dnum, bits, seed, level=None):
     primes = ntt_primes(log_n, nq + np_, bits)

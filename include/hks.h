@@ -190,6 +190,42 @@ uint64_t hks_launch_count(void);
 hks_status hks_prof_enable(int on);
 int hks_prof_read(hks_prof_entry *out, int max);
 
+/* ---- limb-sharded KeySwitch (BASELINE.json configs[3]) ------------------
+ * `world` ranks (one per GPU) each own a contiguous, balanced slice of the chain limbs q_0..q_L and
+ * of the special limbs p_0..p_{K-1} (the paper's LimbPartition, §3.3, which the paper
+ * leaves "in development").  Base conversion needs every source limb of a coefficient, so a
+ * KeySwitch is three local phases around two all-gathers that the caller issues (NCCL over NVLink,
+ * torch.distributed.all_gather_into_tensor) on the same stream:
+ *   A  hks_shard_ks_modup_in    : ysend = INTT(c1_loc) * N^-1 [qhat]^-1          (COEFF, owned chain limbs)
+ *      all-gather #1            : yall[world][q_pad][N] <- ysend[q_pad][N]
+ *   B  hks_shard_ks_inner       : BConv to owned limbs + NTT + key inner product -> acc_loc;
+ *                                 ypsend = INTT(acc_loc[P]) * N^-1 [phat]^-1      (owned special limbs)
+ *      all-gather #2            : ypall[world][2][p_pad][N] <- ypsend[2][p_pad][N]
+ *   C  hks_shard_ks_moddown_out : BConv P -> owned chain limbs + NTT + (acc - .) P^-1 (+ c0)
+ * The result is bit-identical to hks_keyswitch restricted to the owned limbs.
+ * Local layouts: c0_loc, c1_loc, out0_loc, out1_loc [nq_act][N] (owned chain limbs <= level, in
+ * order); evk_loc [dnum][2][nkey][N] (owned chain limbs of the full chain, then owned special limbs);
+ * acc_loc [2][nq_act + (p_hi - p_lo)][N]. */
+typedef struct hks_shard_info {
+    uint32_t world, rank, level;
+    uint32_t q_lo, q_hi;     /* owned chain limbs [q_lo, q_hi) of q_0..q_L */
+    uint32_t p_lo, p_hi;     /* owned special limbs [p_lo, p_hi) of p_0..p_{K-1} */
+    uint32_t nq_act;         /* owned chain limbs active at `level` */
+    uint32_t q_pad, p_pad;   /* all-gather chunk sizes (limbs): max owned chain / special limbs */
+    uint32_t nkey;           /* owned key limbs = (q_hi - q_lo) + (p_hi - p_lo) */
+} hks_shard_info;
+
+hks_status hks_shard_query(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank, hks_shard_info *out);
+size_t hks_shard_workspace_bytes(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank);
+hks_status hks_shard_ks_modup_in(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
+                                 const uint64_t *c1_loc, uint64_t *ysend, void *stream);
+hks_status hks_shard_ks_inner(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
+                              const uint64_t *yall, const uint64_t *c1_loc, const uint64_t *evk_loc,
+                              uint64_t *acc_loc, uint64_t *ypsend, void *ws, void *stream);
+hks_status hks_shard_ks_moddown_out(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
+                                    const uint64_t *ypall, const uint64_t *acc_loc, const uint64_t *c0_loc,
+                                    uint64_t *out0_loc, uint64_t *out1_loc, void *ws, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,6 +53,7 @@ hks_status run_bconv_groups(const hks_ctx *c, std::vector<BconvGroup> &groups, c
         a.pc = c->d_pc;
         a.log_n = c->log_n;
         a.prescale = 0;
+        a.lazy_out = 1;   // internal conversions feed the forward NTT, which takes [0, 8p + 2^32)
         u32 ns = groups[i].nsrc, k = 0;
         while (i < groups.size() && k < BC_MAXG && groups[i].nsrc == ns) a.g[k++] = groups[i++];
         a.ngroups = k;
@@ -81,7 +82,10 @@ void add_groups(std::vector<BconvGroup> &out, u32 nsrc, const u16 *src_slot, con
 }
 
 // ModUp: d [l+1][N] EVAL -> ext slots (j * ne + t) for t outside digit j.  coef: [l+1][N] scratch.
-hks_status modup_core(const hks_ctx *c, const u64 *d, u32 level, u64 *ext, u64 *coef, cudaStream_t s) {
+// rows_pass = false stops after the column pass of the forward NTT (the KeySwitch fuses the row
+// pass with the key inner product).
+hks_status modup_core(const hks_ctx *c, const u64 *d, u32 level, u64 *ext, u64 *coef, cudaStream_t s,
+                      bool rows_pass = true) {
     const u32 ne = c->ne(level), beta = c->beta(level);
     LimbList L;
     for (u32 i = 0; i <= level; i++) L.push(i, i, i);
@@ -105,7 +109,40 @@ hks_status modup_core(const hks_ctx *c, const u64 *d, u32 level, u64 *ext, u64 *
     }
     st = run_bconv_groups(c, groups, coef, ext, s);
     if (st != HKS_OK) return st;
+    if (!rows_pass) return run_ntt_fwd_cols(c, T, ext, ext, s);
     return run_ntt(c, NTT_FWD, T, ext, ext, nullptr, 0, s);
+}
+
+// Fused row pass + key inner product for the KeySwitch (own-digit limbs read from c1, EVAL).
+hks_status ntt_kip_core(const hks_ctx *c, const u64 *ext, const u64 *c1, const u64 *evk, u32 level, u64 *acc,
+                        cudaStream_t s) {
+    const u32 ne = c->ne(level), beta = c->beta(level);
+    for (u32 u0 = 0; u0 < ne; u0 += FK_MAXU) {
+        FusedKipArgs a{};
+        a.ext = ext;
+        a.c1 = c1;
+        a.evk = evk;
+        a.acc = acc;
+        a.pc = c->d_pc;
+        a.tw = c->d_tw_row_fwd;
+        a.nu = std::min<u32>(FK_MAXU, ne - u0);
+        a.ndig = beta;
+        a.nkey = c->nq + c->np;
+        a.acc_stride = ne;
+        for (u32 u = 0; u < a.nu; u++) {
+            const u32 t = u0 + u, pr = c->ext_prime(level, t);
+            a.map.prime[u] = (u16)pr;
+            a.map.kslot[u] = (u16)pr;
+            a.map.aslot[u] = (u16)t;
+            for (u32 j = 0; j < beta; j++) {
+                const bool own = t <= level && t >= c->digit_lo(j) && t < c->digit_hi(level, j);
+                a.map.dsrc[u][j] = own ? (u16)(FK_DIRECT | t) : (u16)(j * ne + t);
+            }
+        }
+        hks_status st = launch_ntt_kip(c, a, s);
+        if (st != HKS_OK) return st;
+    }
+    return HKS_OK;
 }
 
 // ModDown of npoly accumulators (acc poly p at slots p * ne + t) into out[p] (+ c0 on poly 0).
@@ -356,8 +393,14 @@ extern "C" hks_status hks_keyswitch(const hks_ctx *c, const uint64_t *c0, const 
     u64 *ext = coef + l1 * c->n;
     u64 *acc = ext + beta * ne * c->n;
     u64 *md = acc + 2 * ne * c->n;
-    if ((st = modup_core(c, c1, level, ext, coef, s)) != HKS_OK) return st;
-    if ((st = kip_core(c, ext, c1, evk, level, 1, acc, s)) != HKS_OK) return st;
+    if (beta <= FK_MAXD) {
+        // INTT + BConv + NTT column pass, then the fused NTT row pass + key inner product
+        if ((st = modup_core(c, c1, level, ext, coef, s, false)) != HKS_OK) return st;
+        if ((st = ntt_kip_core(c, ext, c1, evk, level, acc, s)) != HKS_OK) return st;
+    } else {
+        if ((st = modup_core(c, c1, level, ext, coef, s)) != HKS_OK) return st;
+        if ((st = kip_core(c, ext, c1, evk, level, 1, acc, s)) != HKS_OK) return st;
+    }
     u64 *outs[2] = {out0, out1};
     return moddown_core(c, acc, 2, level, outs, c0, 1, md, s);
 }

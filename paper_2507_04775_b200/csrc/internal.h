@@ -75,6 +75,7 @@ struct BconvArgs {
     u32 log_n;
     u32 ngroups;
     u32 prescale;              // 1: apply pre_w (inputs raw COEFF), 0: inputs are canonical y_i
+    u32 lazy_out;              // 1: outputs in [0, 8t) (consumer: forward NTT), 0: canonical
     BconvGroup g[BC_MAXG];
 };
 
@@ -89,6 +90,35 @@ struct KipArgs {
     u64 galois;
     u32 log_n, level, nq, np, ne, nk, beta, alpha;
 };
+
+// ----------------------------------------------------------------------------------------------
+// Fused last forward NTT pass + key inner product (PAPER.md:351 HMult fusion part (ii): "the NTT
+// kernels generate NTT(x') * ksk"; PAPER.md:352 dot-product fusion).  Output limb u of a launch:
+// for every digit j, D_j = row pass of ext slot dsrc[u][j] (pass-1 output), or -- bit 15 set --
+// the already-EVAL limb c1[dsrc & 0x7fff] (own-digit limb); acc_p[aslot] = sum_j D_j * evk[j][p][kslot].
+#define FK_MAXU 64
+#define FK_MAXD 4
+#define FK_DIRECT 0x8000
+
+struct FusedKipMap {
+    u16 prime[FK_MAXU];
+    u16 kslot[FK_MAXU];
+    u16 aslot[FK_MAXU];
+    u16 dsrc[FK_MAXU][FK_MAXD];
+};
+
+struct FusedKipArgs {
+    const u64 *ext;
+    const u64 *c1;
+    const u64 *evk;     // [dnum][2][nkey][N]
+    u64 *acc;           // poly p, slot a at (p * acc_stride + a) * N
+    const PrimeConst *pc;
+    const ulonglong2 *tw;   // forward row twiddles [nprimes][R][C]
+    u32 log_n, log_r, log_c, tiles, nu, ndig, nkey, acc_stride;
+    FusedKipMap map;
+};
+
+hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s);
 
 // ----------------------------------------------------------------------------------------------
 struct hks_ctx {
@@ -122,7 +152,7 @@ struct hks_ctx {
 // ----------------------------------------------------------------------------------------------
 // diagnostics (prof.cu): launch counter + optional per-launch event pair tagged with a kernel class
 enum KCls { K_NTT_FWD_COLS = 0, K_NTT_FWD_ROWS, K_NTT_FWD_ROWS_MODDOWN, K_NTT_INV_ROWS, K_NTT_INV_COLS, K_BCONV,
-            K_KIP, K_AUTOMORPH, K_NCLS };
+            K_KIP, K_AUTOMORPH, K_NTT_ROWS_KIP, K_NCLS };
 struct ProfScope {
     int cls;
     cudaStream_t s;
@@ -158,6 +188,8 @@ struct LimbList {
 };
 hks_status run_ntt(const hks_ctx *ctx, NttDir dir, const LimbList &L, const u64 *in, u64 *out,
                    const ulonglong2 *scale, u32 scale_mod, cudaStream_t s);
+// first (column) pass of the forward NTT only; the row pass is fused elsewhere (launch_ntt_kip)
+hks_status run_ntt_fwd_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in, u64 *out, cudaStream_t s);
 hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 *out, const u64 *acc,
                            const u64 *c0, u64 galois, cudaStream_t s);
 hks_status launch_bconv(const BconvArgs &a, u32 max_ndst, cudaStream_t s);

@@ -11,17 +11,23 @@
 // ------------------------------------------------------------------------------------------------
 // Base conversion (§3.6.3, eq:conv):  out_t = [ sum_i y_i [qhat_i]_t ]_t.
 // grid.x: coefficient blocks (2 coefficients / thread), grid.y: group (digit or polynomial).
-template <int NSRC, bool PRESCALE>
+// grid.x: coefficient blocks (2 coefficients / thread), grid.y: group (digit or polynomial),
+// grid.z: chunk of BC_TCH targets.  LAZY: outputs in [0, 8t) for a consumer that accepts the lazy
+// range (the forward NTT); otherwise canonical.
+#define BC_TCH 10
+template <int NSRC, bool PRESCALE, bool LAZY>
 __global__ void __launch_bounds__(256) k_bconv(const __grid_constant__ BconvArgs A) {
     const BconvGroup &G = A.g[blockIdx.y];
-    __shared__ uint2 smat[NSRC * BC_MAXDST];
-    __shared__ PrimeConst spc[BC_MAXDST];
-    const u32 ndst = G.ndst;
-    for (u32 idx = threadIdx.x; idx < NSRC * ndst; idx += blockDim.x) {
-        const u32 i = idx / ndst, u = idx - i * ndst;
-        smat[i * BC_MAXDST + u] = G.mat[(size_t)i * G.mat_stride + u];
+    const u32 u0 = blockIdx.z * BC_TCH;
+    if (u0 >= G.ndst) return;
+    const u32 nt = min((u32)BC_TCH, G.ndst - u0);
+    __shared__ uint2 smat[NSRC * BC_TCH];
+    __shared__ PrimeConst spc[BC_TCH];
+    for (u32 idx = threadIdx.x; idx < NSRC * nt; idx += blockDim.x) {
+        const u32 i = idx / nt, u = idx - i * nt;
+        smat[i * BC_TCH + u] = G.mat[(size_t)i * G.mat_stride + u0 + u];
     }
-    for (u32 u = threadIdx.x; u < ndst; u += blockDim.x) spc[u] = A.pc[G.dst_prime[u]];
+    for (u32 u = threadIdx.x; u < nt; u += blockDim.x) spc[u] = A.pc[G.dst_prime[u0 + u]];
     __syncthreads();
 
     const size_t N = (size_t)1 << A.log_n;
@@ -40,21 +46,29 @@ __global__ void __launch_bounds__(256) k_bconv(const __grid_constant__ BconvArgs
         split30(a, yl[i][0], yh[i][0]);
         split30(b, yl[i][1], yh[i][1]);
     }
-    for (u32 u = 0; u < ndst; u++) {
+    for (u32 u = 0; u < nt; u++) {
         Acc30 a0, a1;
-        acc_zero(a0);
-        acc_zero(a1);
+        {
+            const uint2 m = smat[u];
+            acc_first(a0, yl[0][0], yh[0][0], m.x, m.y);
+            acc_first(a1, yl[0][1], yh[0][1], m.x, m.y);
+        }
 #pragma unroll
-        for (int i = 0; i < NSRC; i++) {
-            const uint2 m = smat[i * BC_MAXDST + u];
+        for (int i = 1; i < NSRC; i++) {
+            const uint2 m = smat[i * BC_TCH + u];
             acc_mac(a0, yl[i][0], yh[i][0], m.x, m.y);
             acc_mac(a1, yl[i][1], yh[i][1], m.x, m.y);
         }
         const PrimeConst pc = spc[u];
         ulonglong2 o;
-        o.x = acc_reduce(a0, pc);
-        o.y = acc_reduce(a1, pc);
-        *reinterpret_cast<ulonglong2 *>(A.out + (size_t)G.dst_slot[u] * N + x0) = o;
+        if (LAZY) {
+            o.x = acc_reduce_lazy(a0, pc);
+            o.y = acc_reduce_lazy(a1, pc);
+        } else {
+            o.x = acc_reduce(a0, pc);
+            o.y = acc_reduce(a1, pc);
+        }
+        *reinterpret_cast<ulonglong2 *>(A.out + (size_t)G.dst_slot[u0 + u] * N + x0) = o;
     }
 }
 
@@ -62,12 +76,16 @@ template <int NSRC>
 static void bconv_go(const BconvArgs &a, cudaStream_t s) {
     const u32 threads = 256;
     const size_t N = (size_t)1 << a.log_n;
-    dim3 grid((u32)((N / 2 + threads - 1) / threads), a.ngroups);
+    u32 maxdst = 0;
+    for (u32 g = 0; g < a.ngroups; g++) maxdst = max(maxdst, a.g[g].ndst);
+    dim3 grid((u32)((N / 2 + threads - 1) / threads), a.ngroups, (maxdst + BC_TCH - 1) / BC_TCH);
     ProfScope ps(K_BCONV, s);
     if (a.prescale)
-        k_bconv<NSRC, true><<<grid, threads, 0, s>>>(a);
+        k_bconv<NSRC, true, false><<<grid, threads, 0, s>>>(a);
+    else if (a.lazy_out)
+        k_bconv<NSRC, false, true><<<grid, threads, 0, s>>>(a);
     else
-        k_bconv<NSRC, false><<<grid, threads, 0, s>>>(a);
+        k_bconv<NSRC, false, false><<<grid, threads, 0, s>>>(a);
     double words = 0;
     for (u32 g = 0; g < a.ngroups; g++) words += a.g[g].nsrc + a.g[g].ndst;
     ps.done(words * (double)N * 8.0);

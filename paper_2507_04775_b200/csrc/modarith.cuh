@@ -44,17 +44,36 @@ struct Acc30 {
 
 HKS_DEV void acc_zero(Acc30 &a) { a.s0 = a.s1a = a.s1b = a.s2 = 0; }
 
-// a += y * m with y = (yh, yl), m = (mh, ml) 30-bit halves.  4 IMAD.WIDE.U32.
+// a += y * m with y = (yh, yl), m = (mh, ml) 30-bit halves.  4 IMAD.WIDE.U32 (PTX, so that the
+// compiler neither re-materialises the split nor routes the accumulators through extra adds).
+HKS_DEV void mad_wide(u64 &acc, u32 a, u32 b) { asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b)); }
+HKS_DEV u64 mul_wide(u32 a, u32 b) {
+    u64 r;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
+    return r;
+}
+
 HKS_DEV void acc_mac(Acc30 &a, u32 yl, u32 yh, u32 ml, u32 mh) {
-    a.s0 += (u64)yl * ml;
-    a.s1a += (u64)yl * mh;
-    a.s1b += (u64)yh * ml;
-    a.s2 += (u64)yh * mh;
+    mad_wide(a.s0, yl, ml);
+    mad_wide(a.s1a, yl, mh);
+    mad_wide(a.s1b, yh, ml);
+    mad_wide(a.s2, yh, mh);
+}
+
+// first term of a chain: a = y * m
+HKS_DEV void acc_first(Acc30 &a, u32 yl, u32 yh, u32 ml, u32 mh) {
+    a.s0 = mul_wide(yl, ml);
+    a.s1a = mul_wide(yl, mh);
+    a.s1b = mul_wide(yh, ml);
+    a.s2 = mul_wide(yh, mh);
 }
 
 HKS_DEV void split30(u64 y, u32 &lo, u32 &hi) {
-    lo = (u32)y & 0x3fffffffu;
-    hi = (u32)(y >> 30);
+    u32 l, h;
+    asm("{\n\t.reg .u32 a, b;\n\tmov.b64 {a, b}, %2;\n\tand.b32 %0, a, 0x3fffffff;\n\tshf.r.clamp.b32 %1, a, b, 30;\n\t}"
+        : "=r"(l), "=r"(h) : "l"(y));
+    lo = l;
+    hi = h;
 }
 
 // canonical X mod p for the accumulated 128-bit value (< 2^124, i.e. <= 16 terms of 60x60 bits).
@@ -67,6 +86,114 @@ HKS_DEV u64 acc_reduce(const Acc30 &a, const PrimeConst &c) {
     u64 r = shoup_lazy(hi, c.r64, c.r64p, c.p) + (lo - mulhi64(lo, c.one_p) * c.p);   // [0, 4p)
     r = csub(r, 2 * c.p);
     return csub(r, c.p);
+}
+
+// X mod p in [0, 8p) for the accumulated 128-bit value, with two approximate-quotient Shoup steps:
+// X = hi 2^64 + lo, X = hi (2^64 mod p) + lo (mod p).  (Defined after shoup_approx below.)
+HKS_DEV u64 acc_reduce_lazy(const Acc30 &a, const PrimeConst &c);
+
+// Per-prime constants of the lazy butterflies.
+struct NttMod {
+    u64 p, np;       // p and 2^64 - p
+    u64 two_p, four_p, eight_p;
+    u32 h4;          // (4p) >> 32: hi-word threshold of the one-instruction range test
+};
+
+HKS_DEV NttMod make_nttmod(u64 p) {
+    NttMod m;
+    m.p = p;
+    m.np = 0 - p;
+    m.two_p = 2 * p;
+    m.four_p = 4 * p;
+    m.eight_p = 8 * p;
+    m.h4 = (u32)((4 * p) >> 32);
+    return m;
+}
+
+// Shoup product with an approximate quotient: three 32x32 partial products of y * w' (the
+// low x low one dropped), so q is short by 0..2 and the result is y*w mod p in [0, 4p) for any
+// y < 2^64.  r = y*w - q*p is formed as y*w + q*(2^64 - p) mod 2^64.
+HKS_DEV u64 shoup_approx(u64 y, u64 w, u64 wp, u64 np) {
+#ifdef HKS_EXACT_SHOUP
+    return y * w + __umul64hi(y, wp) * np;      // [0, 2p)
+#elif !defined(HKS_C_SHOUP)
+    // 2 IMAD.HI + 3 IMAD.WIDE + 4 IMAD (28 FMA-pipe cycles per warp on sm_100); the 33-bit sum of
+    // the two high halves is a plain 64-bit add so that it lands on the ALU pipe.
+    u64 r;
+    asm("{\n\t"
+        ".reg .u32 yl, yh, wl, wh, pl, ph, nl, nh, t1, t3, ql, qh, rl, rh;\n\t"
+        ".reg .u64 a, b, mid, q, rr;\n\t"
+        "mov.b64 {yl, yh}, %1;\n\t"
+        "mov.b64 {wl, wh}, %2;\n\t"
+        "mov.b64 {pl, ph}, %3;\n\t"
+        "mov.b64 {nl, nh}, %4;\n\t"
+        "mul.hi.u32 t1, yh, pl;\n\t"
+        "mul.hi.u32 t3, yl, ph;\n\t"
+        "cvt.u64.u32 a, t1;\n\t"
+        "cvt.u64.u32 b, t3;\n\t"
+        "add.u64 mid, a, b;\n\t"
+        "mad.wide.u32 q, yh, ph, mid;\n\t"
+        "mov.b64 {ql, qh}, q;\n\t"
+        "mul.wide.u32 rr, yl, wl;\n\t"
+        "mad.wide.u32 rr, ql, nl, rr;\n\t"
+        "mov.b64 {rl, rh}, rr;\n\t"
+        "mad.lo.u32 rh, yh, wl, rh;\n\t"
+        "mad.lo.u32 rh, yl, wh, rh;\n\t"
+        "mad.lo.u32 rh, qh, nl, rh;\n\t"
+        "mad.lo.u32 rh, ql, nh, rh;\n\t"
+        "mov.b64 %0, {rl, rh};\n\t"
+        "}"
+        : "=l"(r) : "l"(y), "l"(w), "l"(wp), "l"(np));
+    return r;
+#else
+    const u32 yl = (u32)y, yh = (u32)(y >> 32), wl = (u32)wp, wh = (u32)(wp >> 32);
+    const u64 mid = (u64)__umulhi(yh, wl) + __umulhi(yl, wh);
+    const u64 q = (u64)yh * wh + mid;
+    return y * w + q * np;
+#endif
+}
+
+// x >= 4p (tested on the high word only) ? x - 4p : x.  For x < 8p + 2^32 the result is < 4p + 2^32.
+HKS_DEV u64 lazy_sub4p(u64 x, const NttMod &m) {
+    u64 r = x;
+    asm("{\n\t"
+        ".reg .pred p;\n\t"
+        ".reg .u32 xl, xh, fl, fh;\n\t"
+        "mov.b64 {xl, xh}, %0;\n\t"
+        "mov.b64 {fl, fh}, %2;\n\t"
+        "setp.gt.u32 p, xh, %1;\n\t"
+        "@p sub.cc.u32 xl, xl, fl;\n\t"
+        "@p subc.u32 xh, xh, fh;\n\t"
+        "mov.b64 %0, {xl, xh};\n\t"
+        "}"
+        : "+l"(r) : "r"(m.h4), "l"(m.four_p));
+    return r;
+}
+
+// Forward CT butterfly on the lazy range [0, 8p + 2^32):  X' = x + t, Y' = x - t + 4p with
+// x = X reduced below 4p + 2^32 and t = Y*w in [0, 4p).  Both outputs stay in [0, 8p + 2^32).
+HKS_DEV void ct_lazy(u64 &X, u64 &Y, u64 w, u64 wp, const NttMod &m) {
+    const u64 x = lazy_sub4p(X, m);
+    const u64 t = shoup_approx(Y, w, wp, m.np);
+    X = x + t;
+    Y = x - t + m.four_p;
+}
+
+// Inverse GS butterfly.  Inputs < 4p + c with c <= 2^(32+s) after s stages (c < 4p for every
+// supported N): X' = X + Y reduced by 4p on the high-word test (< 4p + 2c), Y' = (X - Y + 8p)*w in
+// [0, 4p).
+HKS_DEV void gs_lazy(u64 &X, u64 &Y, u64 w, u64 wp, const NttMod &m) {
+    const u64 x = X, y = Y;
+    X = lazy_sub4p(x + y, m);
+    Y = shoup_approx(x - y + m.eight_p, w, wp, m.np);
+}
+
+// canonical residue of x < 8p + 2^33
+HKS_DEV u64 canon8(u64 x, const NttMod &m) {
+    x = csub(x, m.four_p);
+    x = csub(x, m.two_p);
+    x = csub(x, m.p);
+    return csub(x, m.p);
 }
 
 // Forward Cooley-Tukey butterfly, Harvey lazy form: X, Y in [0, 4p) -> [0, 4p).
@@ -93,4 +220,13 @@ HKS_DEV u32 automorph_src(u32 j, u32 log_n, u64 galois) {
     u32 two_n_mask = (2u << log_n) - 1;
     u32 e = ((u32)galois * (2u * brev_bits(j, log_n) + 1u)) & two_n_mask;
     return brev_bits((e - 1u) >> 1, log_n);
+}
+
+HKS_DEV u64 acc_reduce_lazy(const Acc30 &a, const PrimeConst &c) {
+    u64 lo = a.s0, hi = 0, t;
+    t = a.s1a << 30; lo += t; hi += (lo < t); hi += a.s1a >> 34;
+    t = a.s1b << 30; lo += t; hi += (lo < t); hi += a.s1b >> 34;
+    t = a.s2 << 60;  lo += t; hi += (lo < t); hi += a.s2 >> 4;
+    const u64 np = 0 - c.p;
+    return shoup_approx(hi, c.r64, c.r64p, np) + shoup_approx(lo, 1, c.one_p, np);   // [0, 8p)
 }

@@ -20,36 +20,41 @@
 //     pass canonicalises and applies the fused epilogue (SCALE, MODDOWN; §3.6.5).
 #include "internal.h"
 
-template <int LOGN, int LOGE, int LOGNB, bool COLS, bool FWD, int EPI>
+// One pass over a limb batch.  LOGN = log2 of the sub-transform length n; LOGE = log2 of the
+// elements a thread holds (radix-2^LOGE rounds); LOGNB = log2 of the sub-transforms per CTA;
+// LOGC = log2 of the row length C (the column stride).  COLS: sub-transforms are columns (stride C);
+// else rows (contiguous).  Values between butterflies live in the lazy ranges of modarith.cuh.
+template <int LOGN, int LOGE, int LOGNB, int LOGC, bool COLS, bool FWD, int EPI>
 __global__ void __launch_bounds__((1 << LOGNB) << (LOGN - LOGE))
 k_ntt(const __grid_constant__ NttArgs A) {
     constexpr int n = 1 << LOGN;
     constexpr int E = 1 << LOGE;
     constexpr int NB = 1 << LOGNB;
+    constexpr int C = 1 << LOGC;
     constexpr int TPS = n >> LOGE;                    // threads per sub-transform
+    constexpr int NT = NB * TPS;                      // threads per CTA
     constexpr int NR = (LOGN + LOGE - 1) / LOGE;      // rounds
     constexpr int ROWPAD = n + (n >> LOGE);
+    constexpr int LOG_NLIMB = COLS ? (LOGN + LOGC) : 0;   // log2 N for the column pass
     extern __shared__ __align__(16) u64 sm[];
 
     const u32 b = blockIdx.x / A.tiles;
     const u32 tile = blockIdx.x - b * A.tiles;
     const u32 prime = A.map.prime[b];
-    const u32 log_n = A.log_n;
+    const u32 log_n = COLS ? (u32)LOG_NLIMB : A.log_n;
     const size_t N = (size_t)1 << log_n;
-    const u64 *__restrict__ src = A.in + (size_t)A.map.sin[b] * N;
-    u64 *__restrict__ dst = A.out + (size_t)A.map.sout[b] * N;
-    const u64 p = A.pc[prime].p;
-    const u64 two_p = 2 * p;
-    const u32 C = 1u << A.log_c;
+    const NttMod m = make_nttmod(A.pc[prime].p);
     const int tid = threadIdx.x;
     const int bsub = COLS ? (tid & (NB - 1)) : (tid >> (LOGN - LOGE));
     const int tu = COLS ? (tid >> LOGNB) : (tid & (TPS - 1));
-    const u32 gcol = COLS ? tile * NB + bsub : 0;
-    const u32 grow = COLS ? 0 : tile * NB + bsub;
+    // element j of this thread's sub-transform lives at src_sub[j * JS]
+    constexpr int JS = COLS ? C : 1;
+    const size_t sub_off = COLS ? (size_t)(tile * NB + bsub) : (size_t)(tile * NB + bsub) * n;
+    const u64 *__restrict__ src = A.in + (size_t)A.map.sin[b] * N + sub_off;
+    u64 *__restrict__ dst = A.out + (size_t)A.map.sout[b] * N + sub_off;
     const ulonglong2 *__restrict__ tw =
-        COLS ? A.tw + (size_t)prime * n : A.tw + (((size_t)prime << A.log_r) + grow) * n;
+        COLS ? A.tw + (size_t)prime * n : A.tw + (((size_t)prime << A.log_r) + tile * NB + bsub) * n;
 
-    auto gidx = [&](int k) -> size_t { return COLS ? (size_t)k * C + gcol : (size_t)grow * C + k; };
     auto saddr = [&](int k) -> int {
         return COLS ? (k + (k >> LOGE)) * NB + bsub : bsub * ROWPAD + k + (k >> LOGE);
     };
@@ -61,30 +66,34 @@ k_ntt(const __grid_constant__ NttArgs A) {
     const u64 *ea = nullptr, *eb = nullptr;
     if (EPI == EPI_MODDOWN) {
         pinv = A.pinv[prime];
-        ea = A.ea + (size_t)A.map.sa[b] * N;
+        ea = A.ea + (size_t)A.map.sa[b] * N + sub_off;
         eb = (A.eb && A.map.sb[b] != 0xffff) ? A.eb + (size_t)A.map.sb[b] * N : nullptr;
     }
-    auto epi = [&](u64 x, int k) -> u64 {
+    auto epi = [&](u64 x, int j) -> u64 {
         if (EPI == EPI_LAZY) return x;
-        if (EPI == EPI_SCALE) return shoup(x, sc.x, sc.y, p);
-        u64 y = csub(csub(x, two_p), p);
-        if (EPI == EPI_CANON) return y;
-        // EPI_MODDOWN: (a - y) * P^-1 [+ b]
-        const size_t xg = gidx(k);
-        u64 r = shoup(ea[xg] + p - y, pinv.x, pinv.y, p);
+        if (EPI == EPI_SCALE) return csub(csub(shoup_approx(x, sc.x, sc.y, m.np), m.two_p), m.p);
+        if (EPI == EPI_CANON) return canon8(x, m);
+        // EPI_MODDOWN: (a - x) * P^-1 [+ b], a canonical, x < 8p + 2^32
+        u64 r = shoup_approx(ea[(size_t)j * JS] + m.eight_p + m.p - x, pinv.x, pinv.y, m.np);
+        r = csub(csub(r, m.two_p), m.p);
         if (eb) {
-            const size_t xs = A.galois == 1 ? xg : (size_t)automorph_src((u32)xg, log_n, A.galois);
-            r = csub(r + eb[xs], p);
+            const u32 xg = (u32)(sub_off + (size_t)j * JS);
+            r = csub(r + eb[A.galois == 1 ? xg : automorph_src(xg, log_n, A.galois)], m.p);
         }
         return r;
     };
 
-    // inverse ROWS (first inverse pass) reads the tile through shared memory: per-thread elements
-    // of its first round are contiguous, so a direct load would not coalesce.
+    // inverse ROWS (first inverse pass) reads the tile through shared memory (per-thread elements
+    // of its first round are contiguous, so a direct load would not coalesce); loads are batched.
     if (!FWD && !COLS) {
-        for (int idx = tid; idx < NB * n; idx += NB * TPS) {
-            const int r = idx >> LOGN, k = idx & (n - 1);
-            sm[r * ROWPAD + k + (k >> LOGE)] = src[(size_t)(tile * NB + r) * C + k];
+        const u64 *__restrict__ tsrc = A.in + (size_t)A.map.sin[b] * N + (size_t)tile * NB * n;
+        u64 tmp[E];
+#pragma unroll
+        for (int q = 0; q < E; q++) tmp[q] = tsrc[tid + q * NT];
+#pragma unroll
+        for (int q = 0; q < E; q++) {
+            const int idx = tid + q * NT, r = idx >> LOGN, k = idx & (n - 1);
+            sm[r * ROWPAD + k + (k >> LOGE)] = tmp[q];
         }
         __syncthreads();
     }
@@ -110,28 +119,31 @@ k_ntt(const __grid_constant__ NttArgs A) {
 #pragma unroll
             for (int k = 0; k < Ee; k++) {
                 const int j = base + (k << lstride);
-                v[q * Ee + k] = from_global ? src[gidx(j)] : sm[saddr(j)];
+                v[q * Ee + k] = from_global ? src[(size_t)j * JS] : sm[saddr(j)];
             }
         }
-        // butterflies
+        // butterflies: twiddle of (stage half-size 2^ltg, element j) is tw[(n + j) >> (ltg + 1)],
+        // = tw[(n >> s) + (blk << (lBsz - s)) + ((k << lstride) >> s)] with s = ltg + 1.
 #pragma unroll
         for (int q = 0; q < UPT; q++) {
             const int uid = tu * UPT + q;
-            const int base = ((uid >> lstride) << lBsz) + (uid & ((1 << lstride) - 1));
+            const int blk = uid >> lstride;
+            const int base = (blk << lBsz) + (uid & ((1 << lstride) - 1));
+            (void)base;
 #pragma unroll
             for (int l = 0; l < e; l++) {
                 const int lt = FWD ? (e - 1 - l) : l;
                 const int t = 1 << lt;
-                const int ltg = lt + lstride;
+                const int sh = lt + lstride + 1;
+                const ulonglong2 *twb = tw + (n >> sh) + (blk << (lBsz - sh));
 #pragma unroll
                 for (int k = 0; k < Ee; k++) {
                     if (k & t) continue;
-                    const int j = base + (k << lstride);
-                    const ulonglong2 w = __ldg(&tw[(n + j) >> (ltg + 1)]);
+                    const ulonglong2 w = __ldg(twb + ((k << lstride) >> sh));
                     if (FWD)
-                        ct_bfly(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, p, two_p);
+                        ct_lazy(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, m);
                     else
-                        gs_bfly(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, p, two_p);
+                        gs_lazy(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, m);
                 }
             }
         }
@@ -146,7 +158,7 @@ k_ntt(const __grid_constant__ NttArgs A) {
 #pragma unroll
                 for (int k = 0; k < Ee; k++) {
                     const int j = base + (k << lstride);
-                    sm[saddr(j)] = last ? epi(v[q * Ee + k], j) : v[q * Ee + k];
+                    sm[saddr(j)] = v[q * Ee + k];
                 }
             }
         } else {
@@ -157,25 +169,56 @@ k_ntt(const __grid_constant__ NttArgs A) {
 #pragma unroll
                 for (int k = 0; k < Ee; k++) {
                     const int j = base + (k << lstride);
-                    dst[gidx(j)] = epi(v[q * Ee + k], j);
+                    dst[(size_t)j * JS] = epi(v[q * Ee + k], j);
                 }
             }
         }
     }
     if (FWD && !COLS) {
+        // forward ROWS (last forward pass): coalesced copy-out through shared memory, epilogue here.
+        // All global operands of the epilogue are loaded first so their latencies overlap.
         __syncthreads();
-        for (int idx = tid; idx < NB * n; idx += NB * TPS) {
-            const int r = idx >> LOGN, k = idx & (n - 1);
-            dst[(size_t)(tile * NB + r) * C + k] = sm[r * ROWPAD + k + (k >> LOGE)];
+        const size_t tbase = (size_t)tile * NB * n;
+        u64 *__restrict__ tdst = A.out + (size_t)A.map.sout[b] * N + tbase;
+        constexpr int CH = E < 8 ? E : 8;   // epilogue chunk: loads of a chunk are issued together
+#pragma unroll
+        for (int q0 = 0; q0 < E; q0 += CH) {
+            u64 av[CH], bv[CH];
+            if (EPI == EPI_MODDOWN) {
+                const u64 *__restrict__ tea = A.ea + (size_t)A.map.sa[b] * N + tbase;
+#pragma unroll
+                for (int q = 0; q < CH; q++) av[q] = tea[tid + (q0 + q) * NT];
+                if (eb) {
+#pragma unroll
+                    for (int q = 0; q < CH; q++) {
+                        const u32 xg = (u32)(tbase + tid + (q0 + q) * NT);
+                        bv[q] = eb[A.galois == 1 ? xg : automorph_src(xg, log_n, A.galois)];
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < CH; q++) {
+                const int idx = tid + (q0 + q) * NT, r = idx >> LOGN, k = idx & (n - 1);
+                u64 x = sm[r * ROWPAD + k + (k >> LOGE)];
+                if (EPI == EPI_CANON) {
+                    x = canon8(x, m);
+                } else if (EPI == EPI_MODDOWN) {
+                    u64 rr2 = shoup_approx(av[q] + m.eight_p + m.p - x, pinv.x, pinv.y, m.np);
+                    rr2 = csub(csub(rr2, m.two_p), m.p);
+                    if (eb) rr2 = csub(rr2 + bv[q], m.p);
+                    x = rr2;
+                }
+                tdst[idx] = x;
+            }
         }
     }
 }
 
-template <int LOGN, int LOGE, int LOGNB, bool COLS, bool FWD, int EPI>
+template <int LOGN, int LOGE, int LOGNB, int LOGC, bool COLS, bool FWD, int EPI>
 static hks_status go(NttArgs &a, cudaStream_t s) {
     constexpr int threads = (1 << LOGNB) << (LOGN - LOGE);
     constexpr size_t smem = (size_t)((1 << LOGN) + ((1 << LOGN) >> LOGE)) * (1 << LOGNB) * sizeof(u64);
-    auto kern = k_ntt<LOGN, LOGE, LOGNB, COLS, FWD, EPI>;
+    auto kern = k_ntt<LOGN, LOGE, LOGNB, LOGC, COLS, FWD, EPI>;
     if (smem > 48 * 1024) {
         static bool once = [&] {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -215,12 +258,12 @@ hks_status launch_ntt_pass(const hks_ctx *ctx, NttDir dir, int pass, int epi, Nt
     switch (ctx->log_n) {
 #define X(LN, LR, ER, BR, LC, EC, BC)                                                               \
     case LN:                                                                                        \
-        if (dir == NTT_FWD && cols) return go<LR, ER, BR, true, true, EPI_LAZY>(a, s);              \
-        if (dir == NTT_FWD && epi == EPI_CANON) return go<LC, EC, BC, false, true, EPI_CANON>(a, s); \
+        if (dir == NTT_FWD && cols) return go<LR, ER, BR, LC, true, true, EPI_LAZY>(a, s);          \
+        if (dir == NTT_FWD && epi == EPI_CANON) return go<LC, EC, BC, LC, false, true, EPI_CANON>(a, s); \
         if (dir == NTT_FWD && epi == EPI_MODDOWN)                                                   \
-            return go<LC, EC, BC, false, true, EPI_MODDOWN>(a, s);                                  \
-        if (dir == NTT_INV && !cols) return go<LC, EC, BC, false, false, EPI_LAZY>(a, s);           \
-        if (dir == NTT_INV && cols) return go<LR, ER, BR, true, false, EPI_SCALE>(a, s);            \
+            return go<LC, EC, BC, LC, false, true, EPI_MODDOWN>(a, s);                              \
+        if (dir == NTT_INV && !cols) return go<LC, EC, BC, LC, false, false, EPI_LAZY>(a, s);       \
+        if (dir == NTT_INV && cols) return go<LR, ER, BR, LC, true, false, EPI_SCALE>(a, s);        \
         break;
         NTT_SHAPES(X)
 #undef X
@@ -272,6 +315,23 @@ hks_status run_ntt(const hks_ctx *ctx, NttDir dir, const LimbList &L, const u64 
     return HKS_OK;
 }
 
+hks_status run_ntt_fwd_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in, u64 *out, cudaStream_t s) {
+    for (size_t off = 0; off < L.size(); off += HKS_MAXB) {
+        u32 cnt = (u32)((L.size() - off) < HKS_MAXB ? (L.size() - off) : HKS_MAXB);
+        NttArgs a{};
+        a.pc = ctx->d_pc;
+        a.ninv = ctx->d_ninv;
+        a.galois = 1;
+        fill_map(a, L, off, cnt, false);
+        a.in = in;
+        a.out = out;
+        a.tw = ctx->d_tw_col_fwd;
+        hks_status st = launch_ntt_pass(ctx, NTT_FWD, 0, EPI_LAZY, a, s);
+        if (st != HKS_OK) return st;
+    }
+    return HKS_OK;
+}
+
 hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 *out, const u64 *acc,
                            const u64 *c0, u64 galois, cudaStream_t s) {
     for (size_t off = 0; off < L.size(); off += HKS_MAXB) {
@@ -304,4 +364,198 @@ hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 
         if (st != HKS_OK) return st;
     }
     return HKS_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Fused forward row pass + key inner product.  CTA = NB rows of one output limb u.  Phase 1: for
+// every digit j whose D_j[u] still needs its row pass, run the row rounds into shared buffer j
+// (lazy values).  Phase 2: coalesced sweep over the tile, two coefficients per thread:
+// acc_p = sum_j canon(D_j) * evk_j[p] with the 30-bit-split IMAD.WIDE accumulation (one reduction
+// per output).  D never returns to HBM.
+template <int LOGN, int LOGE, int LOGNB, int NDIG>
+__global__ void __launch_bounds__(NDIG * ((1 << LOGNB) << (LOGN - LOGE)))
+k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
+    constexpr int n = 1 << LOGN;
+    constexpr int E = 1 << LOGE;
+    constexpr int NB = 1 << LOGNB;
+    constexpr int TPS = n >> LOGE;
+    constexpr int NTG = NB * TPS;                      // threads per digit group
+    constexpr int NT = NDIG * NTG;                     // threads per CTA
+    constexpr int NR = (LOGN + LOGE - 1) / LOGE;
+    constexpr int ROWPAD = n + (n >> LOGE);
+    constexpr int BUF = NB * ROWPAD;
+    extern __shared__ __align__(16) u64 sm[];
+
+    const u32 u = blockIdx.x / A.tiles;
+    const u32 tile = blockIdx.x - u * A.tiles;
+    const u32 prime = A.map.prime[u];
+    const size_t N = (size_t)1 << A.log_n;
+    const PrimeConst pc = A.pc[prime];
+    const NttMod m = make_nttmod(pc.p);
+    const int tid = threadIdx.x;
+    const size_t tbase = (size_t)tile * NB * n;
+
+    // phase 1: thread group j runs the row pass of digit j into shared buffer j (concurrently)
+    {
+        const int j = tid / NTG, gt = tid - j * NTG;
+        const int bsub = gt >> (LOGN - LOGE);
+        const int tu = gt & (TPS - 1);
+        const u16 ds = A.map.dsrc[u][j];
+        const bool work = !(ds & FK_DIRECT);
+        const ulonglong2 *__restrict__ tw = A.tw + (((size_t)prime << A.log_r) + tile * NB + bsub) * n;
+        u64 *smj = sm + j * BUF + bsub * ROWPAD;
+        const u64 *__restrict__ src = A.ext + (size_t)(ds & 0x7fff) * N + tbase + (size_t)bsub * n;
+        u64 v[E];
+#pragma unroll
+        for (int rr = 0; rr < NR; rr++) {
+            const int s0 = rr * LOGE;
+            const int e = (LOGN - s0) < LOGE ? (LOGN - s0) : LOGE;
+            const int Ee = 1 << e;
+            const int UPT = E >> e;
+            const int lstride = LOGN - s0 - e;
+            const int lBsz = lstride + e;
+            if (rr > 0) __syncthreads();
+            if (work) {
+#pragma unroll
+                for (int q = 0; q < UPT; q++) {
+                    const int uid = tu * UPT + q;
+                    const int base = ((uid >> lstride) << lBsz) + (uid & ((1 << lstride) - 1));
+#pragma unroll
+                    for (int k = 0; k < Ee; k++) {
+                        const int jj = base + (k << lstride);
+                        v[q * Ee + k] = rr == 0 ? src[jj] : smj[jj + (jj >> LOGE)];
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < UPT; q++) {
+                    const int uid = tu * UPT + q;
+                    const int blk = uid >> lstride;
+#pragma unroll
+                    for (int l = 0; l < e; l++) {
+                        const int lt = e - 1 - l;
+                        const int t = 1 << lt;
+                        const int sh = lt + lstride + 1;
+                        const ulonglong2 *twb = tw + (n >> sh) + (blk << (lBsz - sh));
+#pragma unroll
+                        for (int k = 0; k < Ee; k++) {
+                            if (k & t) continue;
+                            const ulonglong2 w = __ldg(twb + ((k << lstride) >> sh));
+                            ct_lazy(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, m);
+                        }
+                    }
+                }
+            }
+            if (rr > 0) __syncthreads();
+            if (work) {
+#pragma unroll
+                for (int q = 0; q < UPT; q++) {
+                    const int uid = tu * UPT + q;
+                    const int base = ((uid >> lstride) << lBsz) + (uid & ((1 << lstride) - 1));
+#pragma unroll
+                    for (int k = 0; k < Ee; k++) {
+                        const int jj = base + (k << lstride);
+                        smj[jj + (jj >> LOGE)] = v[q * Ee + k];
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+
+    // phase 2: acc_p = sum_j canon(D_j) * evk_j[p], two coefficients per thread per step; the loads
+    // of all digits are issued before the multiply-accumulates.
+    const size_t kst = (size_t)A.nkey * N;
+    const u64 *__restrict__ kbase = A.evk + (size_t)A.map.kslot[u] * N + tbase;
+    const u32 as = A.map.aslot[u];
+    for (int idx = 2 * tid; idx < NB * n; idx += 2 * NT) {
+        const int r = idx >> LOGN, k = idx & (n - 1);
+        ulonglong2 kb[NDIG], ka[NDIG], dv[NDIG];
+#pragma unroll
+        for (int j = 0; j < NDIG; j++) {
+            kb[j] = *reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j) * kst + idx);
+            ka[j] = *reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j + 1) * kst + idx);
+            const u16 ds = A.map.dsrc[u][j];
+            if (ds & FK_DIRECT) {
+                dv[j] = *reinterpret_cast<const ulonglong2 *>(A.c1 + (size_t)(ds & 0x7fff) * N + tbase + idx);
+            } else {
+                const u64 *smj = sm + j * BUF + r * ROWPAD + k + (k >> LOGE);
+                dv[j].x = canon8(smj[0], m);
+                dv[j].y = canon8(smj[1], m);
+            }
+        }
+        Acc30 a0[2], a1[2];
+        acc_zero(a0[0]); acc_zero(a0[1]); acc_zero(a1[0]); acc_zero(a1[1]);
+#pragma unroll
+        for (int j = 0; j < NDIG; j++) {
+            u32 dl, dh, ml, mh;
+            split30(dv[j].x, dl, dh);
+            split30(kb[j].x, ml, mh); acc_mac(a0[0], dl, dh, ml, mh);
+            split30(ka[j].x, ml, mh); acc_mac(a1[0], dl, dh, ml, mh);
+            split30(dv[j].y, dl, dh);
+            split30(kb[j].y, ml, mh); acc_mac(a0[1], dl, dh, ml, mh);
+            split30(ka[j].y, ml, mh); acc_mac(a1[1], dl, dh, ml, mh);
+        }
+        ulonglong2 o0, o1;
+        o0.x = acc_reduce(a0[0], pc);
+        o0.y = acc_reduce(a0[1], pc);
+        o1.x = acc_reduce(a1[0], pc);
+        o1.y = acc_reduce(a1[1], pc);
+        *reinterpret_cast<ulonglong2 *>(A.acc + (size_t)as * N + tbase + idx) = o0;
+        *reinterpret_cast<ulonglong2 *>(A.acc + ((size_t)A.acc_stride + as) * N + tbase + idx) = o1;
+    }
+}
+
+template <int LOGN, int LOGE, int LOGNB, int NDIG>
+static hks_status go_kip(FusedKipArgs &a, cudaStream_t s) {
+    constexpr int threads = NDIG * ((1 << LOGNB) << (LOGN - LOGE));
+    constexpr size_t smem = (size_t)NDIG * ((1 << LOGN) + ((1 << LOGN) >> LOGE)) * (1 << LOGNB) * sizeof(u64);
+    auto kern = k_ntt_kip<LOGN, LOGE, LOGNB, NDIG>;
+    if (smem > 48 * 1024) {
+        static bool once = [&] {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            return true;
+        }();
+        (void)once;
+    }
+    a.tiles = (1u << a.log_r) >> LOGNB;
+    ProfScope ps(K_NTT_ROWS_KIP, s);
+    kern<<<a.nu * a.tiles, threads, smem, s>>>(a);
+    HKS_CHECK_LAUNCH();
+    u32 nntt = 0, ndirect = 0;
+    for (u32 u = 0; u < a.nu; u++)
+        for (u32 j = 0; j < a.ndig; j++) (a.map.dsrc[u][j] & FK_DIRECT) ? ndirect++ : nntt++;
+    // algorithmic words: D read once (pass-1 output or c1), key 2 limbs per (u, j), acc 2 limbs per u
+    ps.done(((double)nntt + ndirect + 2.0 * a.nu * a.ndig + 2.0 * a.nu) * (double)(1ull << a.log_n) * 8.0);
+    return HKS_OK;
+}
+
+template <int LOGN, int LOGE, int LOGNB>
+static hks_status go_kip_d(FusedKipArgs &a, cudaStream_t s) {
+    switch (a.ndig) {
+        case 1: return go_kip<LOGN, LOGE, LOGNB, 1>(a, s);
+        case 2: return go_kip<LOGN, LOGE, LOGNB, 2>(a, s);
+        case 3: return go_kip<LOGN, LOGE, LOGNB, 3>(a, s);
+        case 4: return go_kip<LOGN, LOGE, LOGNB, 4>(a, s);
+        default: break;
+    }
+    HKS_FAIL(HKS_EINVAL, "ntt_kip: %u digits", a.ndig);
+}
+
+hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s) {
+    a.log_n = ctx->log_n;
+    a.log_r = ctx->log_r;
+    a.log_c = ctx->log_c;
+    if (a.ndig > FK_MAXD || a.nu > FK_MAXU) HKS_FAIL(HKS_EINVAL, "ntt_kip: %u digits / %u limbs per launch", a.ndig, a.nu);
+    switch (ctx->log_n) {
+        case 17: return go_kip_d<8, 4, 3>(a, s);
+        case 16: return go_kip_d<8, 4, 3>(a, s);
+        case 15: return go_kip_d<7, 4, 3>(a, s);
+        case 14: return go_kip_d<7, 4, 3>(a, s);
+        case 13: return go_kip_d<6, 3, 3>(a, s);
+        case 12: return go_kip_d<6, 3, 3>(a, s);
+        case 11: return go_kip_d<5, 3, 3>(a, s);
+        case 10: return go_kip_d<5, 3, 3>(a, s);
+        default: break;
+    }
+    HKS_FAIL(HKS_EINVAL, "ntt_kip: unsupported log_n %u", ctx->log_n);
 }

@@ -1,0 +1,253 @@
+// shard.cu -- limb-sharded KeySwitch phases (include/hks.h "limb-sharded KeySwitch").
+//
+// Ownership (full index space, independent of the level so keys are distributed once): chain limbs
+// q_0..q_L in `world` contiguous chunks, the first (L+1) mod world ranks one limb larger; special
+// limbs p_0..p_{K-1} in contiguous chunks, the LAST K mod world ranks one limb larger (they own fewer
+// chain limbs).  Every step reuses the single-GPU kernels with slot maps into the gathered buffers.
+#include <algorithm>
+
+#include "internal.h"
+
+namespace {
+
+struct Plan {
+    u32 world, rank, level;
+    u32 q_lo, q_hi, p_lo, p_hi, nq_act, q_pad, p_pad, nkey, np_own, n_own;
+    std::vector<u32> qlo_r, qhi_r, plo_r, phi_r;   // per rank
+    u32 q_owner(u32 i) const { for (u32 r = 0; r < world; r++) if (i < qhi_r[r]) return r; return world - 1; }
+    u32 p_owner(u32 k) const { for (u32 r = 0; r < world; r++) if (k < phi_r[r]) return r; return world - 1; }
+};
+
+void chunks(u32 total, u32 world, bool extra_last, std::vector<u32> &lo, std::vector<u32> &hi) {
+    lo.resize(world);
+    hi.resize(world);
+    const u32 base = total / world, rem = total % world;
+    u32 at = 0;
+    for (u32 r = 0; r < world; r++) {
+        const bool extra = extra_last ? (r >= world - rem) : (r < rem);
+        lo[r] = at;
+        at += base + (extra ? 1 : 0);
+        hi[r] = at;
+    }
+}
+
+hks_status make_plan(const hks_ctx *c, u32 level, u32 world, u32 rank, Plan &P) {
+    if (!c) HKS_FAIL(HKS_EINVAL, "shard: NULL context");
+    if (world < 1 || rank >= world) HKS_FAIL(HKS_EINVAL, "shard: rank %u / world %u", rank, world);
+    if (level > c->L()) HKS_FAIL(HKS_EINVAL, "shard: level %u > L", level);
+    if (world > c->nq) HKS_FAIL(HKS_EINVAL, "shard: world %u larger than the chain", world);
+    P.world = world; P.rank = rank; P.level = level;
+    chunks(c->nq, world, false, P.qlo_r, P.qhi_r);
+    chunks(c->np, world, true, P.plo_r, P.phi_r);
+    P.q_lo = P.qlo_r[rank]; P.q_hi = P.qhi_r[rank];
+    P.p_lo = P.plo_r[rank]; P.p_hi = P.phi_r[rank];
+    P.nq_act = P.q_lo >= level + 1 ? 0 : std::min(P.q_hi, level + 1) - P.q_lo;
+    P.q_pad = P.p_pad = 0;
+    for (u32 r = 0; r < world; r++) {
+        P.q_pad = std::max(P.q_pad, P.qhi_r[r] - P.qlo_r[r]);
+        P.p_pad = std::max(P.p_pad, P.phi_r[r] - P.plo_r[r]);
+    }
+    P.np_own = P.p_hi - P.p_lo;
+    P.nkey = (P.q_hi - P.q_lo) + P.np_own;
+    P.n_own = P.nq_act + P.np_own;
+    return HKS_OK;
+}
+
+hks_status dev_ctx(const hks_ctx *c) {
+    if (c->device < 0) HKS_FAIL(HKS_EDEVICE, "host-only context cannot run device operations");
+    return HKS_OK;
+}
+
+// BConv launch helper (same as capi.cu's, kept local)
+hks_status bconv_groups(const hks_ctx *c, std::vector<BconvGroup> &groups, const u64 *in, u64 *out, cudaStream_t s) {
+    size_t i = 0;
+    while (i < groups.size()) {
+        BconvArgs a{};
+        a.in = in;
+        a.out = out;
+        a.pc = c->d_pc;
+        a.log_n = c->log_n;
+        a.lazy_out = 1;
+        u32 ns = groups[i].nsrc, k = 0;
+        while (i < groups.size() && k < BC_MAXG && groups[i].nsrc == ns) a.g[k++] = groups[i++];
+        a.ngroups = k;
+        hks_status st = launch_bconv(a, BC_MAXDST, s);
+        if (st != HKS_OK) return st;
+    }
+    return HKS_OK;
+}
+
+void push_group(std::vector<BconvGroup> &out, u32 nsrc, const u16 *src_slot, const uint2 *mat, u32 stride,
+                const std::vector<u16> &ds, const std::vector<u16> &dp) {
+    for (size_t u0 = 0; u0 < ds.size(); u0 += BC_MAXDST) {
+        BconvGroup g{};
+        g.nsrc = nsrc;
+        g.ndst = (u32)std::min<size_t>(BC_MAXDST, ds.size() - u0);
+        g.mat_stride = stride;
+        g.mat = mat + u0;
+        for (u32 i = 0; i < nsrc; i++) g.src_slot[i] = src_slot[i];
+        for (u32 u = 0; u < g.ndst; u++) { g.dst_slot[u] = ds[u0 + u]; g.dst_prime[u] = dp[u0 + u]; }
+        out.push_back(g);
+    }
+}
+
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int dev) { cudaGetDevice(&prev); if (prev != dev) cudaSetDevice(dev); else prev = -1; }
+    ~DevGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+}  // namespace
+
+extern "C" hks_status hks_shard_query(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank, hks_shard_info *out) {
+    if (!out) HKS_FAIL(HKS_EINVAL, "shard_query: NULL out");
+    Plan P;
+    hks_status st = make_plan(c, level, world, rank, P);
+    if (st != HKS_OK) return st;
+    *out = hks_shard_info{P.world, P.rank, P.level, P.q_lo, P.q_hi, P.p_lo, P.p_hi, P.nq_act, P.q_pad, P.p_pad, P.nkey};
+    return HKS_OK;
+}
+
+extern "C" size_t hks_shard_workspace_bytes(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank) {
+    Plan P;
+    if (make_plan(c, level, world, rank, P) != HKS_OK) return 0;
+    return ((size_t)c->beta(level) * P.n_own + 2 * (size_t)P.nq_act) * c->n * sizeof(u64);
+}
+
+// Phase A: ysend[li] = INTT(c1_loc[li]) * N^-1 [qhat_{j,i}]^-1, i = q_lo + li (canonical COEFF).
+extern "C" hks_status hks_shard_ks_modup_in(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
+                                           const uint64_t *c1_loc, uint64_t *ysend, void *stream) {
+    Plan P;
+    hks_status st = make_plan(c, level, world, rank, P);
+    if (st != HKS_OK || (st = dev_ctx(c)) != HKS_OK) return st;
+    if (P.nq_act == 0) return HKS_OK;
+    if (!c1_loc || !ysend) HKS_FAIL(HKS_EINVAL, "shard_ks_modup_in: NULL buffer");
+    DevGuard g(c->device);
+    LimbList L;
+    for (u32 li = 0; li < P.nq_act; li++) L.push(li, li, P.q_lo + li);
+    return run_ntt(c, NTT_INV, L, c1_loc, ysend, c->d_mu_scale + c->mu_scale_off[level] + P.q_lo, P.nq_act,
+                   (cudaStream_t)stream);
+}
+
+// Phase B: D_j for owned limbs from the gathered y, fused NTT + key inner product, then
+// ypsend[p][kk] = INTT(acc_p[owned P_kk]) * N^-1 [phat_k]^-1.
+extern "C" hks_status hks_shard_ks_inner(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
+                                        const uint64_t *yall, const uint64_t *c1_loc, const uint64_t *evk_loc,
+                                        uint64_t *acc_loc, uint64_t *ypsend, void *ws, void *stream) {
+    Plan P;
+    hks_status st = make_plan(c, level, world, rank, P);
+    if (st != HKS_OK || (st = dev_ctx(c)) != HKS_OK) return st;
+    if (!yall || !evk_loc || !acc_loc || !ypsend || !ws || (P.nq_act && !c1_loc))
+        HKS_FAIL(HKS_EINVAL, "shard_ks_inner: NULL buffer");
+    const u32 beta = c->beta(level), ne = c->ne(level);
+    if (beta > FK_MAXD) HKS_FAIL(HKS_EINVAL, "shard_ks_inner: beta %u > %d", beta, FK_MAXD);
+    DevGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    u64 *ext = (u64 *)ws;
+    // owned extended limbs: chain t in [q_lo, q_lo + nq_act), then special P_k, k in [p_lo, p_hi)
+    std::vector<u32> own_t;
+    for (u32 li = 0; li < P.nq_act; li++) own_t.push_back(P.q_lo + li);
+    for (u32 k = P.p_lo; k < P.p_hi; k++) own_t.push_back(level + 1 + k);
+    // BConv per digit to the owned targets outside the digit; matrix columns of (level, digit) follow
+    // the target order t in [0, ne) \ digit, so owned targets map to column positions.
+    std::vector<BconvGroup> groups;
+    LimbList T;
+    for (u32 j = 0; j < beta; j++) {
+        const u32 lo = c->digit_lo(j), hi = c->digit_hi(level, j);
+        u16 src[BC_MAXSRC];
+        for (u32 i = lo; i < hi; i++) {
+            const u32 r = P.q_owner(i);
+            src[i - lo] = (u16)(r * P.q_pad + (i - P.qlo_r[r]));
+        }
+        const uint2 *mat = c->d_mu_mat + c->mu_mat_off[(size_t)level * c->dnum + j];
+        const u32 ntg = ne - (hi - lo);
+        // contiguous runs of column positions
+        std::vector<u16> ds, dp;
+        int run_col = -1;
+        auto flush = [&]() {
+            if (!ds.empty()) push_group(groups, hi - lo, src, mat + run_col, ntg, ds, dp);
+            ds.clear(); dp.clear(); run_col = -1;
+        };
+        int prev_col = -2;
+        for (u32 u = 0; u < own_t.size(); u++) {
+            const u32 t = own_t[u];
+            if (t >= lo && t < hi) continue;
+            const int col = (int)(t < lo ? t : t - (hi - lo));
+            if (col != prev_col + 1) { flush(); run_col = col; }
+            ds.push_back((u16)(j * P.n_own + u));
+            dp.push_back((u16)c->ext_prime(level, t));
+            T.push(j * P.n_own + u, j * P.n_own + u, c->ext_prime(level, t));
+            prev_col = col;
+        }
+        flush();
+    }
+    if ((st = bconv_groups(c, groups, yall, ext, s)) != HKS_OK) return st;
+    if (T.size() && (st = run_ntt_fwd_cols(c, T, ext, ext, s)) != HKS_OK) return st;
+    for (u32 u0 = 0; u0 < own_t.size(); u0 += FK_MAXU) {
+        FusedKipArgs a{};
+        a.ext = ext;
+        a.c1 = c1_loc;
+        a.evk = evk_loc;
+        a.acc = acc_loc;
+        a.pc = c->d_pc;
+        a.tw = c->d_tw_row_fwd;
+        a.nu = std::min<u32>(FK_MAXU, (u32)own_t.size() - u0);
+        a.ndig = beta;
+        a.nkey = P.nkey;
+        a.acc_stride = P.n_own;
+        for (u32 uu = 0; uu < a.nu; uu++) {
+            const u32 u = u0 + uu, t = own_t[u];
+            a.map.prime[uu] = (u16)c->ext_prime(level, t);
+            a.map.kslot[uu] = (u16)(t <= level ? t - P.q_lo : (P.q_hi - P.q_lo) + (t - level - 1 - P.p_lo));
+            a.map.aslot[uu] = (u16)u;
+            for (u32 j = 0; j < beta; j++) {
+                const bool own = t <= level && t >= c->digit_lo(j) && t < c->digit_hi(level, j);
+                a.map.dsrc[uu][j] = own ? (u16)(FK_DIRECT | (t - P.q_lo)) : (u16)(j * P.n_own + u);
+            }
+        }
+        if ((st = launch_ntt_kip(c, a, s)) != HKS_OK) return st;
+    }
+    if (P.np_own) {
+        LimbList L;
+        for (u32 p = 0; p < 2; p++)
+            for (u32 kk = 0; kk < P.np_own; kk++) L.push(p * P.n_own + P.nq_act + kk, p * P.p_pad + kk, c->nq + P.p_lo + kk);
+        // scale index b % np_own = kk
+        if ((st = run_ntt(c, NTT_INV, L, acc_loc, ypsend, c->d_md_scale + P.p_lo, P.np_own, s)) != HKS_OK) return st;
+    }
+    return HKS_OK;
+}
+
+// Phase C: conv_p = BConv_{P -> owned chain}(ypall_p); out_p = (acc_p - NTT(conv_p)) P^-1 (+ c0 on p = 0).
+extern "C" hks_status hks_shard_ks_moddown_out(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
+                                              const uint64_t *ypall, const uint64_t *acc_loc, const uint64_t *c0_loc,
+                                              uint64_t *out0_loc, uint64_t *out1_loc, void *ws, void *stream) {
+    Plan P;
+    hks_status st = make_plan(c, level, world, rank, P);
+    if (st != HKS_OK || (st = dev_ctx(c)) != HKS_OK) return st;
+    if (P.nq_act == 0) return HKS_OK;
+    if (!ypall || !acc_loc || !out0_loc || !out1_loc || !ws) HKS_FAIL(HKS_EINVAL, "shard_ks_moddown_out: NULL buffer");
+    DevGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const u32 beta = c->beta(level), K = c->np;
+    u64 *conv = (u64 *)ws + (size_t)beta * P.n_own * c->n;
+    std::vector<BconvGroup> groups;
+    for (u32 p = 0; p < 2; p++) {
+        u16 src[BC_MAXSRC];
+        for (u32 k = 0; k < K; k++) {
+            const u32 r = P.p_owner(k);
+            src[k] = (u16)(r * 2 * P.p_pad + p * P.p_pad + (k - P.plo_r[r]));
+        }
+        std::vector<u16> ds(P.nq_act), dp(P.nq_act);
+        for (u32 li = 0; li < P.nq_act; li++) { ds[li] = (u16)(p * P.nq_act + li); dp[li] = (u16)(P.q_lo + li); }
+        push_group(groups, K, src, c->d_md_mat + P.q_lo, c->nq, ds, dp);
+    }
+    if ((st = bconv_groups(c, groups, ypall, conv, s)) != HKS_OK) return st;
+    u64 *outs[2] = {out0_loc, out1_loc};
+    for (u32 p = 0; p < 2; p++) {
+        LimbList M;
+        for (u32 li = 0; li < P.nq_act; li++)
+            M.push(p * P.nq_act + li, li, P.q_lo + li, p * P.n_own + li, (p == 0 && c0_loc) ? li : 0xffff);
+        if ((st = run_ntt_moddown(c, M, conv, outs[p], acc_loc, p == 0 ? c0_loc : nullptr, 1, s)) != HKS_OK) return st;
+    }
+    return HKS_OK;
+}

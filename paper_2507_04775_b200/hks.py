@@ -22,7 +22,8 @@ MAX_DIGITS = 64
 EXPORTS = ("hks_last_error", "hks_ctx_create", "hks_ctx_destroy", "hks_ctx_query", "hks_ctx_psi",
            "hks_workspace_bytes", "hks_ntt_fwd", "hks_ntt_inv", "hks_bconv", "hks_modup",
            "hks_ksk_inner_product", "hks_moddown", "hks_keyswitch", "hks_automorph", "hks_rotate_hoisted",
-           "hks_launch_count", "hks_prof_enable", "hks_prof_read")
+           "hks_launch_count", "hks_prof_enable", "hks_prof_read", "hks_shard_query", "hks_shard_workspace_bytes",
+           "hks_shard_ks_modup_in", "hks_shard_ks_inner", "hks_shard_ks_moddown_out")
 
 
 class HksError(RuntimeError):
@@ -34,6 +35,11 @@ class HksError(RuntimeError):
 class ProfEntry(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_uint64), ("total_ms", ctypes.c_double),
                 ("bytes", ctypes.c_double)]
+
+
+class ShardInfo(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_uint32) for f in ("world", "rank", "level", "q_lo", "q_hi", "p_lo", "p_hi", "nq_act",
+                                                "q_pad", "p_pad", "nkey")]
 
 
 class Info(ctypes.Structure):
@@ -80,8 +86,14 @@ def lib() -> ctypes.CDLL:
         L.hks_launch_count.argtypes = []
         L.hks_prof_enable.argtypes = [ctypes.c_int]
         L.hks_prof_read.argtypes = [ctypes.POINTER(ProfEntry), ctypes.c_int]
+        L.hks_shard_query.argtypes = [_vp, _u32, _u32, _u32, ctypes.POINTER(ShardInfo)]
+        L.hks_shard_workspace_bytes.argtypes = [_vp, _u32, _u32, _u32]
+        L.hks_shard_workspace_bytes.restype = ctypes.c_size_t
+        L.hks_shard_ks_modup_in.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp]
+        L.hks_shard_ks_inner.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.hks_shard_ks_moddown_out.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         for f in EXPORTS[1:]:
-            if f not in ("hks_ctx_destroy", "hks_workspace_bytes", "hks_launch_count"):
+            if f not in ("hks_ctx_destroy", "hks_workspace_bytes", "hks_launch_count", "hks_shard_workspace_bytes"):
                 getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -229,3 +241,31 @@ def prof_read() -> dict:
     k = lib().hks_prof_read(arr, 16)
     return {arr[i].name.decode(): (int(arr[i].launches), float(arr[i].total_ms), float(arr[i].bytes))
             for i in range(k)}
+
+
+# ---- limb-sharded KeySwitch (C4): phases of include/hks.h; the all-gathers are the caller's
+def shard_query(ctx: Context, level: int, world: int, rank: int) -> ShardInfo:
+    info = ShardInfo()
+    _check(lib().hks_shard_query(ctx.handle, level, world, rank, ctypes.byref(info)), "hks_shard_query")
+    return info
+
+
+def shard_workspace_bytes(ctx: Context, level: int, world: int, rank: int) -> int:
+    return int(lib().hks_shard_workspace_bytes(ctx.handle, level, world, rank))
+
+
+def shard_ks_modup_in(ctx: Context, level, world, rank, c1_loc, ysend, stream=None):
+    _check(lib().hks_shard_ks_modup_in(ctx.handle, level, world, rank, _ptr(c1_loc), _ptr(ysend), _stream(stream)),
+           "hks_shard_ks_modup_in")
+
+
+def shard_ks_inner(ctx: Context, level, world, rank, yall, c1_loc, evk_loc, acc_loc, ypsend, ws, stream=None):
+    _check(lib().hks_shard_ks_inner(ctx.handle, level, world, rank, _ptr(yall), _ptr(c1_loc), _ptr(evk_loc),
+                                    _ptr(acc_loc), _ptr(ypsend), _ptr(ws), _stream(stream)), "hks_shard_ks_inner")
+
+
+def shard_ks_moddown_out(ctx: Context, level, world, rank, ypall, acc_loc, c0_loc, out0_loc, out1_loc, ws,
+                         stream=None):
+    _check(lib().hks_shard_ks_moddown_out(ctx.handle, level, world, rank, _ptr(ypall), _ptr(acc_loc), _ptr(c0_loc),
+                                          _ptr(out0_loc), _ptr(out1_loc), _ptr(ws), _stream(stream)),
+           "hks_shard_ks_moddown_out")

@@ -1,0 +1,92 @@
+"""Limb-sharded KeySwitch across ranks (BASELINE.json configs[3]).
+
+Each rank (one GPU) owns a contiguous slice of the chain limbs and of the special limbs
+(`hks_shard_query`).  A KeySwitch is three library phases around two all-gathers that this module
+issues with torch.distributed (NCCL over NVLink on the GPU box, gloo in CPU tests):
+
+    A  ysend  = INTT(c1_loc) scaled                       -> all_gather -> yall
+    B  acc    = KIP(NTT(BConv(yall)))  ; ypsend = INTT(acc_P)  -> all_gather -> ypall
+    C  out    = (acc - NTT(BConv(ypall))) P^-1 (+ c0)
+
+The collectives are ordinary NCCL all-gathers (`all_gather_into_tensor`, padded to equal chunks);
+the math runs in libhks.  `gather_fn` can be replaced (tests use a local concatenation to simulate
+several ranks on one device).
+"""
+from __future__ import annotations
+
+from . import hks as H
+
+
+class ShardPlan:
+    """Host-side view of the ownership plan of every rank (computed by libhks)."""
+
+    def __init__(self, ctx, level: int, world: int):
+        self.level, self.world = level, world
+        self.info = [H.shard_query(ctx, level, world, r) for r in range(world)]
+        self.q_pad = self.info[0].q_pad
+        self.p_pad = self.info[0].p_pad
+
+    def q_slot(self, i: int) -> int:
+        """Slot of chain limb i in the gathered y buffer [world][q_pad]."""
+        for r, s in enumerate(self.info):
+            if s.q_lo <= i < s.q_hi:
+                return r * self.q_pad + (i - s.q_lo)
+        raise IndexError(i)
+
+    def p_slot(self, k: int, poly: int) -> int:
+        """Slot of special limb k of polynomial `poly` in the gathered buffer [world][2][p_pad]."""
+        for r, s in enumerate(self.info):
+            if s.p_lo <= k < s.p_hi:
+                return r * 2 * self.p_pad + poly * self.p_pad + (k - s.p_lo)
+        raise IndexError(k)
+
+
+class ShardedKeySwitch:
+    """One rank's part of a limb-sharded KeySwitch at `level` (buffers allocated once)."""
+
+    def __init__(self, ctx, level: int, world: int, rank: int, device, gather_fn=None):
+        import torch
+        self.ctx, self.level, self.world, self.rank = ctx, level, world, rank
+        self.info = H.shard_query(ctx, level, world, rank)
+        n = ctx.n
+        s = self.info
+        self.ysend = torch.zeros((s.q_pad, n), dtype=torch.int64, device=device)
+        self.yall = torch.empty((world * s.q_pad, n), dtype=torch.int64, device=device)
+        self.ypsend = torch.zeros((2 * s.p_pad, n), dtype=torch.int64, device=device)
+        self.ypall = torch.empty((world * 2 * s.p_pad, n), dtype=torch.int64, device=device)
+        self.acc = torch.empty((2 * (s.nq_act + s.p_hi - s.p_lo), n), dtype=torch.int64, device=device)
+        self.ws = torch.empty((max(H.shard_workspace_bytes(ctx, level, world, rank) // 8, 1),), dtype=torch.int64,
+                              device=device)
+        self.gather = gather_fn or self._nccl_gather
+
+    @staticmethod
+    def _nccl_gather(out, inp):
+        import torch.distributed as dist
+        dist.all_gather_into_tensor(out, inp)
+
+    def phase_a(self, c1_loc, stream=None):
+        H.shard_ks_modup_in(self.ctx, self.level, self.world, self.rank, c1_loc, self.ysend, stream)
+
+    def phase_b(self, c1_loc, evk_loc, stream=None):
+        H.shard_ks_inner(self.ctx, self.level, self.world, self.rank, self.yall, c1_loc, evk_loc, self.acc,
+                         self.ypsend, self.ws, stream)
+
+    def phase_c(self, c0_loc, out0_loc, out1_loc, stream=None):
+        H.shard_ks_moddown_out(self.ctx, self.level, self.world, self.rank, self.ypall, self.acc, c0_loc, out0_loc,
+                               out1_loc, self.ws, stream)
+
+    def __call__(self, c0_loc, c1_loc, evk_loc, out0_loc, out1_loc, stream=None):
+        self.phase_a(c1_loc, stream)
+        self.gather(self.yall, self.ysend)
+        self.phase_b(c1_loc, evk_loc, stream)
+        self.gather(self.ypall, self.ypsend)
+        self.phase_c(c0_loc, out0_loc, out1_loc, stream)
+
+
+def slice_key(evk_full, info, num_q: int):
+    """A rank's owned key limbs [dnum][2][nkey][N] from a full key [dnum][2][L+1+K][N]: owned chain
+    limbs then owned special limbs (the evk_loc layout of include/hks.h)."""
+    import torch
+    q = evk_full[:, :, info.q_lo:info.q_hi]
+    p = evk_full[:, :, num_q + info.p_lo:num_q + info.p_hi]
+    return torch.cat([q, p], dim=2).contiguous()

@@ -1,0 +1,123 @@
+"""Limb-sharded KeySwitch.
+
+CPU (gloo, world_size 2): the ownership plan is a partition, and the all-gather layout the Python
+orchestrator produces matches the slots libhks reads (q_slot / p_slot).
+GPU: G simulated ranks on one device (all-gather = local concatenation) give results bit-identical
+to the unsharded hks_keyswitch (integer math is order-independent: SURVEY.md §4 item 5)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import hks_synth as S
+
+H = pytest.importorskip("paper_2507_04775_b200.hks")
+from paper_2507_04775_b200 import shard  # noqa: E402
+
+
+@pytest.mark.parametrize("name,level", [("C4", 35), ("C4", 20), ("C2", 29), ("T12", 6), ("T12", 2)])
+def test_plan_is_partition(name, level):
+    cfg = S.config(name)
+    ctx = H.Context.from_config(cfg, -1)
+    for world in (1, 2, 3, 4, 8):
+        if world > len(cfg.q):
+            continue
+        infos = [H.shard_query(ctx, level, world, r) for r in range(world)]
+        q_owned = [i for s in infos for i in range(s.q_lo, s.q_hi)]
+        p_owned = [k for s in infos for k in range(s.p_lo, s.p_hi)]
+        assert q_owned == list(range(len(cfg.q))) and p_owned == list(range(len(cfg.p)))
+        tot = [(s.q_hi - s.q_lo) + (s.p_hi - s.p_lo) for s in infos]
+        assert max(tot) - min(tot) <= 2
+        assert sum(s.nq_act for s in infos) == level + 1
+        assert all(s.q_pad == max(x.q_hi - x.q_lo for x in infos) for s in infos)
+
+
+def _gloo_worker(rank, world, port, name, level, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = S.config(name)
+        ctx = H.Context.from_config(cfg, -1)
+        plan = shard.ShardPlan(ctx, level, world)
+        me = plan.info[rank]
+        n = 8                                               # stand-in row length
+        ysend = torch.full((me.q_pad, n), -1, dtype=torch.int64)
+        for li in range(me.nq_act):
+            ysend[li] = me.q_lo + li                        # marker: global chain limb index
+        ypsend = torch.full((2 * me.p_pad, n), -1, dtype=torch.int64)
+        for poly in range(2):
+            for kk in range(me.p_hi - me.p_lo):
+                ypsend[poly * me.p_pad + kk] = 1000 * (poly + 1) + me.p_lo + kk
+        yall = torch.empty((world * me.q_pad, n), dtype=torch.int64)
+        ypall = torch.empty((world * 2 * me.p_pad, n), dtype=torch.int64)
+        dist.all_gather_into_tensor(yall, ysend)
+        dist.all_gather_into_tensor(ypall, ypsend)
+        ok = all(int(yall[plan.q_slot(i), 0]) == i for i in range(level + 1))
+        ok &= all(int(ypall[plan.p_slot(k, poly), 0]) == 1000 * (poly + 1) + k
+                  for k in range(len(cfg.p)) for poly in range(2))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,level", [("C4", 35), ("T12", 5)])
+def test_gloo_allgather_layout(name, level):
+    world = 2
+    ctxmp = mp.get_context("spawn")
+    q = ctxmp.Queue()
+    port = 29500 + (os.getpid() % 1000)
+    procs = [ctxmp.Process(target=_gloo_worker, args=(r, world, port, name, level, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
+
+
+# ------------------------------------------------------------------ GPU: simulated ranks
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,level,world", [("T12", 6, 2), ("T12", 4, 3), ("T16s", 5, 2), ("C2", 29, 4),
+                                              ("C4", 35, 8), ("C4", 35, 2), ("C4", 17, 4)])
+def test_sharded_keyswitch_matches_unsharded(name, level, world):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    dev = "cuda:0"
+    cfg = S.config(name)
+    ctx = H.Context.from_config(cfg, 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(cfg.seed)
+    n = cfg.n
+    primes = list(cfg.q) + list(cfg.p)
+
+    def limbs(pr):
+        return torch.stack([torch.randint(0, int(p), (n,), generator=g, device=dev, dtype=torch.int64) for p in pr])
+
+    c0, c1 = limbs(cfg.q[: level + 1]), limbs(cfg.q[: level + 1])
+    evk = torch.stack([limbs(primes) for _ in range(2 * cfg.dnum)]).reshape(cfg.dnum, 2, len(primes), n)
+    ref0, ref1 = torch.empty_like(c0), torch.empty_like(c1)
+    H.keyswitch(ctx, c0, c1, level, evk, ref0, ref1, ctx.workspace(H.OP_KEYSWITCH, level))
+
+    ranks = [shard.ShardedKeySwitch(ctx, level, world, r, dev, gather_fn=lambda o, i: None) for r in range(world)]
+    loc = []
+    for r, ks in enumerate(ranks):
+        s = ks.info
+        c0l, c1l = c0[s.q_lo:s.q_lo + s.nq_act].contiguous(), c1[s.q_lo:s.q_lo + s.nq_act].contiguous()
+        loc.append((c0l, c1l, shard.slice_key(evk, s, len(cfg.q)), torch.empty_like(c0l), torch.empty_like(c1l)))
+        ks.phase_a(c1l)
+    yall = torch.cat([ks.ysend for ks in ranks])
+    for r, ks in enumerate(ranks):
+        ks.yall.copy_(yall)
+        ks.phase_b(loc[r][1], loc[r][2])
+    ypall = torch.cat([ks.ypsend for ks in ranks])
+    for r, ks in enumerate(ranks):
+        ks.ypall.copy_(ypall)
+        c0l, c1l, _, o0, o1 = loc[r]
+        ks.phase_c(c0l, o0, o1)
+    got0 = torch.cat([l[3] for l in loc])
+    got1 = torch.cat([l[4] for l in loc])
+    torch.cuda.synchronize()
+    assert torch.equal(got0, ref0) and torch.equal(got1, ref1)
