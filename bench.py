@@ -55,6 +55,18 @@ def peaks():
     return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
 
 
+def mul_peak():
+    """Peak 32x32->64-bit integer multiplies/s (IMAD.WIDE / IMAD.HI, half-rate FMA-pipe ops), measured
+    by tools/int_probe.cu on this pool's B200 (profiles/int_probe.json, imad_hi); fallback: the
+    nominal 32 per SM per clock x 148 SMs x 1.965 GHz."""
+    path = os.path.join(ROOT, "profiles", "int_probe.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["imad_hi"]["ops_per_s"]), "measured (profiles/int_probe.json imad_hi)"
+    return 32 * 148 * 1.965e9, "nominal (32/clk/SM x 148 x 1.965 GHz)"
+
+
 def workload_desc(cfg, level):
     base = f"N=2^{cfg.log_n}, L={cfg.L}, K={cfg.K}, dnum={cfg.dnum}"
     if cfg.name == "C3":
@@ -237,20 +249,49 @@ class KSWorkload:
         mb = self.nsets * (2 * c.dnum * (c.L + 1 + c.K) + 2 * (l + 1)) * c.n * 8 / 1e6
         return f"{self.nsets} rotating (ct, key) sets, {mb:.0f} MB > 4x 126 MB L2"
 
-    # e2e: H2D of (c0, c1) from pinned host memory, KeySwitch, D2H of (out0, out1)
+    # e2e: every step copies its ciphertext (c0, c1) H2D from pinned host memory, runs the KeySwitch
+    # and copies (out0, out1) D2H.  Three streams pipeline step i's H2D, step i-1's KeySwitch and
+    # step i-2's D2H (PCIe is full duplex), with events ordering each step's three stages.
     def e2e_setup(self):
-        self.hsets = [{k: self.sets[i][k].cpu().pin_memory() for k in ("c0", "c1")} for i in range(min(2, len(self.sets)))]
-        self.hout0 = torch_empty_pinned_like(self.sets[0]["out0"])
-        self.hout1 = torch_empty_pinned_like(self.sets[0]["out1"])
-        return 4 * 0 + 2 * (self.level + 1) * self.cfg.n * 8, 2 * (self.level + 1) * self.cfg.n * 8
+        import torch
+        dev = self.sets[0]["c0"].device
+        self.NB = 3
+        self.hin = [{k: self.sets[i % len(self.sets)][k].cpu().pin_memory() for k in ("c0", "c1")}
+                    for i in range(2)]
+        self.din = [{k: torch.empty_like(self.sets[0][k]) for k in ("c0", "c1")} for _ in range(self.NB)]
+        self.dout = [{k: torch.empty_like(self.sets[0][k]) for k in ("out0", "out1")} for _ in range(self.NB)]
+        self.hout = [{k: torch_empty_pinned_like(self.sets[0][k]) for k in ("out0", "out1")} for _ in range(self.NB)]
+        self.s_in, self.s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        self.s_cmp = torch.cuda.current_stream(dev)
+        self.ev_in = [torch.cuda.Event() for _ in range(self.NB)]
+        self.ev_cmp = [torch.cuda.Event() for _ in range(self.NB)]
+        self.ev_out = [torch.cuda.Event() for _ in range(self.NB)]
+        io = 2 * (self.level + 1) * self.cfg.n * 8
+        return io, io
 
     def e2e_step(self, i):
-        s, h = self.sets[i % len(self.sets)], self.hsets[i % len(self.hsets)]
-        s["c0"].copy_(h["c0"], non_blocking=True)
-        s["c1"].copy_(h["c1"], non_blocking=True)
-        self.H.keyswitch(self.ctx, s["c0"], s["c1"], self.level, s["evk"], s["out0"], s["out1"], self.ws, self.sid)
-        self.hout0.copy_(s["out0"], non_blocking=True)
-        self.hout1.copy_(s["out1"], non_blocking=True)
+        import torch
+        b = i % self.NB
+        h, d, o, ho = self.hin[i % 2], self.din[b], self.dout[b], self.hout[b]
+        s = self.sets[i % len(self.sets)]
+        with torch.cuda.stream(self.s_in):
+            self.s_in.wait_event(self.ev_cmp[b])          # buffer b's previous KeySwitch has read it
+            d["c0"].copy_(h["c0"], non_blocking=True)
+            d["c1"].copy_(h["c1"], non_blocking=True)
+            self.ev_in[b].record(self.s_in)
+        self.s_cmp.wait_event(self.ev_in[b])
+        self.s_cmp.wait_event(self.ev_out[b])             # previous D2H of buffer b is done
+        self.H.keyswitch(self.ctx, d["c0"], d["c1"], self.level, s["evk"], o["out0"], o["out1"], self.ws,
+                         self.s_cmp.cuda_stream)
+        self.ev_cmp[b].record(self.s_cmp)
+        with torch.cuda.stream(self.s_out):
+            self.s_out.wait_event(self.ev_cmp[b])
+            ho["out0"].copy_(o["out0"], non_blocking=True)
+            ho["out1"].copy_(o["out1"], non_blocking=True)
+            self.ev_out[b].record(self.s_out)
+
+    def e2e_streams(self):
+        return self.s_in, self.s_out
 
 
 class C3Workload:
@@ -440,10 +481,16 @@ def main():
         prof = H.prof_read()
         H.prof_enable(False)
         tot = sum(v[1] for v in prof.values())
+        mpeak, mpeak_src = mul_peak()
         kern = {k: {"launches_per_step": v[0] / nprof, "ms_per_step": v[1] / nprof, "share": v[1] / tot,
                     "avg_launch_us": 1e3 * v[1] / v[0], "alg_bytes_per_launch": v[2] / v[0],
-                    "achieved_gbs": (v[2] / v[0]) / (1e-3 * v[1] / v[0]) / 1e9}
+                    "achieved_gbs": (v[2] / v[0]) / (1e-3 * v[1] / v[0]) / 1e9,
+                    "alg_muls_per_launch": v[3] / v[0],
+                    "achieved_tmul": (v[3] / v[0]) / (1e-3 * v[1] / v[0]) / 1e12}
                 for k, v in prof.items()}
+        for k in kern.values():
+            k["hbm_frac"] = k["achieved_gbs"] / hbm_peak
+            k["alu_frac"] = k["achieved_tmul"] * 1e12 / mpeak
         dom = max(kern, key=lambda k: kern[k]["share"])
         d = kern[dom]
         traffic = None
@@ -451,9 +498,14 @@ def main():
         if os.path.exists(tpath):
             with open(tpath) as f:
                 traffic = json.load(f).get(cfg.name, {}).get(dom)
-        extra["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": d["achieved_gbs"], "peak": hbm_peak,
-                             "unit": "GB/s", "frac": d["achieved_gbs"] / hbm_peak, "traffic": traffic,
-                             "peak_source": peak_src, "share_of_step": d["share"]}
+        hbm = {"kernel": dom, "bound": "hbm", "achieved": d["achieved_gbs"], "peak": hbm_peak, "unit": "GB/s",
+               "frac": d["hbm_frac"], "traffic": traffic, "peak_source": peak_src, "share_of_step": d["share"]}
+        alu = {"kernel": dom, "bound": "alu", "achieved": d["achieved_tmul"], "peak": mpeak / 1e12,
+               "unit": "T int-mul32x32/s", "frac": d["alu_frac"], "traffic": traffic, "peak_source": mpeak_src,
+               "share_of_step": d["share"],
+               "work": "algorithmic 32x32->64 partial products: 4 per exact 60x60-bit product, 7 per Shoup butterfly"}
+        # the binding roofline of the dominant kernel is the one it is closer to
+        extra["roofline"], extra["roofline_other"] = (alu, hbm) if d["alu_frac"] >= d["hbm_frac"] else (hbm, alu)
         extra["kernels"] = kern
         alg = wl.alg_bytes()
         extra["step_hbm"] = {"alg_bytes": alg, "achieved_gbs": alg / (ms / args.steps * 1e-3) / 1e9,
@@ -490,10 +542,12 @@ def main():
             torch.cuda.synchronize()
             barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
+            s_in, s_out = wl.e2e_streams()
+            e0.record(s_in)
             for i in range(e_steps):
                 wl.e2e_step(i)
-            e1.record(stream)
+            s_out.wait_stream(stream)
+            e1.record(s_out)
             e1.synchronize()
             et = max_over_ranks(e0.elapsed_time(e1))
             extra["e2e"] = {"value": world * wl.units * e_steps / (et / 1e3), "unit": wl.unit,

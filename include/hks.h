@@ -156,6 +156,14 @@ hks_status hks_moddown(const hks_ctx *ctx, const uint64_t *acc, uint32_t level, 
 hks_status hks_keyswitch(const hks_ctx *ctx, const uint64_t *c0, const uint64_t *c1, uint32_t level,
                          const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws, void *stream);
 
+/* Relinearisation of a tensor-product ciphertext (d0, d1, d2) at `level` (HMult's KeySwitch,
+ * PAPER.md:75 Table 1 HMult, PAPER.md:351 HMult fusion):  out0 = d0 + ModDown(acc0),
+ * out1 = d1 + ModDown(acc1), acc = KIP(ModUp(d2), evk).  Both additions are fused in the ModDown
+ * epilogue.  d0 may be NULL (treated as 0); d1 must not be NULL.  Layouts and ws as hks_keyswitch. */
+hks_status hks_relinearize(const hks_ctx *ctx, const uint64_t *d0, const uint64_t *d1, const uint64_t *d2,
+                           uint32_t level, const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws,
+                           void *stream);
+
 /* EVAL-form automorphism X -> X^galois on nlimbs limbs (prime-independent permutation,
  * SPEC.md:244-252; SURVEY.md reading 15):  out[l][j] = in[l][j'], 2brv(j')+1 = k(2brv(j)+1) mod 2N.
  * in != out required. */
@@ -177,13 +185,15 @@ hks_status hks_rotate_hoisted(const hks_ctx *ctx, const uint64_t *c0, const uint
  *   the launch's stream, tagged with its kernel class and its algorithmic bytes (limb words read and
  *   written, excluding twiddle/constant tables).  hks_prof_enable(0) stops recording.
  * hks_prof_read: synchronises the recorded events and returns, per kernel class, the launch count,
- *   the summed device time (ms) and the summed algorithmic bytes; clears the record.  Returns the
+ *   the summed device time (ms), algorithmic bytes and algorithmic multiplies; clears the record.  Returns the
  *   number of classes written (<= max). */
 typedef struct hks_prof_entry {
     char name[32];
     uint64_t launches;
     double total_ms;
-    double bytes;
+    double bytes;   /* algorithmic HBM bytes (limb words read + written) */
+    double muls;    /* algorithmic 32x32->64-bit integer partial products (4 per exact 60x60-bit
+                       product; 7 wide-equivalents per Shoup butterfly) */
 } hks_prof_entry;
 
 uint64_t hks_launch_count(void);

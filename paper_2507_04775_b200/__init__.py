@@ -5,7 +5,7 @@ sm_100a; ``hks`` is its argument-marshalling binding.  Nothing here imports ``or
 """
 from . import hks
 from .hks import (Context, HksError, automorph, bconv, keyswitch, ksk_inner_product, moddown, modup,
-                  ntt_fwd, ntt_inv, rotate_hoisted)
+                  ntt_fwd, ntt_inv, relinearize, rotate_hoisted)
 
 __all__ = ["hks", "Context", "HksError", "ntt_fwd", "ntt_inv", "bconv", "modup", "ksk_inner_product",
-           "moddown", "keyswitch", "automorph", "rotate_hoisted"]
+           "moddown", "keyswitch", "relinearize", "automorph", "rotate_hoisted"]

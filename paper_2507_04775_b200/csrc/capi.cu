@@ -65,13 +65,14 @@ hks_status run_bconv_groups(const hks_ctx *c, std::vector<BconvGroup> &groups, c
 
 // groups converting src slots -> dst slots with a row-major matrix [nsrc][stride]; targets chunked by 64
 void add_groups(std::vector<BconvGroup> &out, u32 nsrc, const u16 *src_slot, const uint2 *mat, u32 stride,
-                const std::vector<u16> &dst_slot, const std::vector<u16> &dst_prime) {
+                const std::vector<u16> &dst_slot, const std::vector<u16> &dst_prime, const double *matf = nullptr) {
     for (size_t u0 = 0; u0 < dst_slot.size(); u0 += BC_MAXDST) {
         BconvGroup g{};
         g.nsrc = nsrc;
         g.ndst = (u32)std::min<size_t>(BC_MAXDST, dst_slot.size() - u0);
         g.mat_stride = stride;
         g.mat = mat + u0;
+        g.matf = matf ? matf + 3 * u0 : nullptr;
         for (u32 i = 0; i < nsrc; i++) g.src_slot[i] = src_slot[i];
         for (u32 u = 0; u < g.ndst; u++) {
             g.dst_slot[u] = dst_slot[u0 + u];
@@ -104,8 +105,8 @@ hks_status modup_core(const hks_ctx *c, const u64 *d, u32 level, u64 *ext, u64 *
             dp.push_back((u16)c->ext_prime(level, t));
             T.push(j * ne + t, j * ne + t, c->ext_prime(level, t));
         }
-        add_groups(groups, hi - lo, src, c->d_mu_mat + c->mu_mat_off[(size_t)level * c->dnum + j],
-                   (u32)ds.size(), ds, dp);
+        const size_t off = c->mu_mat_off[(size_t)level * c->dnum + j];
+        add_groups(groups, hi - lo, src, c->d_mu_mat + off, (u32)ds.size(), ds, dp, c->d_mu_matf + 3 * off);
     }
     st = run_bconv_groups(c, groups, coef, ext, s);
     if (st != HKS_OK) return st;
@@ -145,10 +146,10 @@ hks_status ntt_kip_core(const hks_ctx *c, const u64 *ext, const u64 *c1, const u
     return HKS_OK;
 }
 
-// ModDown of npoly accumulators (acc poly p at slots p * ne + t) into out[p] (+ c0 on poly 0).
-// ws: y [npoly][K][N] then conv [npoly][l+1][N].
+// ModDown of npoly accumulators (acc poly p at slots p * ne + t) into out[p] (+ adds[p], read through
+// the automorphism `galois` for p = 0).  ws: y [npoly][K][N] then conv [npoly][l+1][N].
 hks_status moddown_core(const hks_ctx *c, const u64 *acc, u32 npoly, u32 level, u64 *const *outs, const u64 *c0,
-                        u64 galois, u64 *ws, cudaStream_t s) {
+                        u64 galois, u64 *ws, cudaStream_t s, const u64 *c1add = nullptr) {
     const u32 ne = c->ne(level), K = c->np;
     u64 *y = ws, *conv = ws + (size_t)npoly * K * c->n;
     LimbList L;
@@ -164,15 +165,28 @@ hks_status moddown_core(const hks_ctx *c, const u64 *acc, u32 npoly, u32 level, 
         for (u32 k = 0; k < K; k++) src[k] = (u16)(p * K + k);
         std::vector<u16> ds(level + 1);
         for (u32 i = 0; i <= level; i++) ds[i] = (u16)(p * (level + 1) + i);
-        add_groups(groups, K, src, c->d_md_mat, c->nq, ds, dp);
+        add_groups(groups, K, src, c->d_md_mat, c->nq, ds, dp, c->d_md_matf);
     }
     st = run_bconv_groups(c, groups, y, conv, s);
     if (st != HKS_OK) return st;
+    // both polynomials in one pair of launches: limbs [0, l+1) -> outs[0] (+ c0 through `galois`),
+    // limbs [l+1, 2(l+1)) -> outs[1] (+ c1add)
+    LimbList M;
     for (u32 p = 0; p < npoly; p++) {
-        LimbList M;
-        for (u32 i = 0; i <= level; i++) M.push(p * (level + 1) + i, i, i, p * ne + i, (p == 0 && c0) ? i : 0xffff);
-        st = run_ntt_moddown(c, M, conv, outs[p], acc, p == 0 ? c0 : nullptr, galois, s);
+        const u64 *add = p == 0 ? c0 : c1add;
+        for (u32 i = 0; i <= level; i++) M.push(p * (level + 1) + i, i, i, p * ne + i, add ? i : 0xffff);
+    }
+    if (npoly == 2 && M.size() <= HKS_MAXB) {
+        st = run_ntt_moddown(c, M, conv, outs[0], acc, c0, galois, s, level + 1, outs[1], c1add);
         if (st != HKS_OK) return st;
+    } else {
+        for (u32 p = 0; p < npoly; p++) {
+            LimbList Mp;
+            const u64 *add = p == 0 ? c0 : c1add;
+            for (u32 i = 0; i <= level; i++) Mp.push(p * (level + 1) + i, i, i, p * ne + i, add ? i : 0xffff);
+            st = run_ntt_moddown(c, Mp, conv, outs[p], acc, add, p == 0 ? galois : 1, s);
+            if (st != HKS_OK) return st;
+        }
     }
     return HKS_OK;
 }
@@ -369,8 +383,28 @@ extern "C" hks_status hks_moddown(const hks_ctx *c, const uint64_t *acc, uint32_
     return moddown_core(c, acc, 1, level, outs, nullptr, 1, (u64 *)ws, (cudaStream_t)stream);
 }
 
+static hks_status keyswitch_impl(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, const uint64_t *add1,
+                                  uint32_t level, const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws,
+                                  void *stream);
+
 extern "C" hks_status hks_keyswitch(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, uint32_t level,
                                     const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws, void *stream) {
+    return keyswitch_impl(c, c0, c1, nullptr, level, evk, out0, out1, ws, stream);
+}
+
+extern "C" hks_status hks_relinearize(const hks_ctx *c, const uint64_t *d0, const uint64_t *d1, const uint64_t *d2,
+                                      uint32_t level, const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws,
+                                      void *stream) {
+    if (!d1) HKS_FAIL(HKS_EINVAL, "relinearize: NULL d1");
+    if (c && level <= c->L() && (overlap(d1, (level + 1) * limb_bytes(c), out0, (level + 1) * limb_bytes(c)) ||
+                                 overlap(d1, (level + 1) * limb_bytes(c), out1, (level + 1) * limb_bytes(c))))
+        HKS_FAIL(HKS_EINVAL, "relinearize: d1 overlaps an output");
+    return keyswitch_impl(c, d0, d2, d1, level, evk, out0, out1, ws, stream);
+}
+
+static hks_status keyswitch_impl(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, const uint64_t *add1,
+                                  uint32_t level, const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws,
+                                  void *stream) {
     hks_status st = check_ctx(c);
     if (st != HKS_OK) return st;
     if (!c1 || !evk || !out0 || !out1 || !ws) HKS_FAIL(HKS_EINVAL, "keyswitch: NULL argument");
@@ -402,7 +436,7 @@ extern "C" hks_status hks_keyswitch(const hks_ctx *c, const uint64_t *c0, const 
         if ((st = kip_core(c, ext, c1, evk, level, 1, acc, s)) != HKS_OK) return st;
     }
     u64 *outs[2] = {out0, out1};
-    return moddown_core(c, acc, 2, level, outs, c0, 1, md, s);
+    return moddown_core(c, acc, 2, level, outs, c0, 1, md, s, add1);
 }
 
 extern "C" hks_status hks_automorph(const hks_ctx *c, const uint64_t *in, uint32_t nlimbs, uint64_t galois,

@@ -101,7 +101,7 @@ hks_status upload(T **dptr, const std::vector<T> &h) {
 
 void free_tables(hks_ctx *c) {
     void *ptrs[] = {c->d_pc, c->d_tw_col_fwd, c->d_tw_row_fwd, c->d_tw_col_inv, c->d_tw_row_inv, c->d_ninv,
-                    c->d_mu_scale, c->d_mu_mat, c->d_md_scale, c->d_md_mat, c->d_pinv};
+                    c->d_mu_scale, c->d_mu_mat, c->d_md_scale, c->d_md_mat, c->d_pinv, c->d_mu_matf, c->d_md_matf};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -257,6 +257,19 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
         pinv[i] = sh(inv_mod(P, qi), qi);
     }
 
+    // the same matrices as exact 20-bit limbs in doubles (FP64-pipe part of k_bconv_fp)
+    auto limbs20 = [](const std::vector<uint2> &m) {
+        std::vector<double> f(m.size() * 3);
+        for (size_t i = 0; i < m.size(); i++) {
+            const u64 v = (u64)m[i].x | ((u64)m[i].y << 30);
+            f[3 * i + 0] = (double)(v & 0xfffff);
+            f[3 * i + 1] = (double)((v >> 20) & 0xfffff);
+            f[3 * i + 2] = (double)(v >> 40);
+        }
+        return f;
+    };
+    std::vector<double> mu_matf = limbs20(mu_mat), md_matf = limbs20(md_mat);
+
     hks_status st = HKS_OK;
 #define UP(dst, src) if (st == HKS_OK) st = upload(&c->dst, src)
     UP(d_pc, pc);
@@ -270,6 +283,8 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     UP(d_md_scale, md_scale);
     UP(d_md_mat, md_mat);
     UP(d_pinv, pinv);
+    UP(d_mu_matf, mu_matf);
+    UP(d_md_matf, md_matf);
 #undef UP
     cudaSetDevice(prev);
     if (st != HKS_OK) {

@@ -44,6 +44,9 @@ struct NttArgs {
     const u64 *eb;             // EPI_MODDOWN operand b base (c0), may be NULL
     const ulonglong2 *pinv;    // per prime P^-1 mod q (Shoup)
     u64 galois;                // EPI_MODDOWN: b is read through the EVAL automorphism (1 = none)
+    u64 *out_b;                // limbs b >= nsplit write to out_b (second polynomial of a ModDown)
+    const u64 *eb_b;           // and add eb_b (NULL: none) without automorphism
+    u32 nsplit;                // 0xffffffff: single output
     u32 log_n, log_r, log_c;   // N = R * C; R = 2^log_r rows, C = 2^log_c columns (row length)
     u32 tiles;                 // CTAs per limb
     u32 scale_mod;
@@ -60,6 +63,7 @@ struct NttArgs {
 struct BconvGroup {
     u32 nsrc, ndst, mat_stride;
     const uint2 *mat;          // [nsrc][mat_stride] (lo30, hi30) of [qhat_i]_t, column u = target u
+    const double *matf;        // same entries as three exact 20-bit limbs [nsrc][mat_stride][3] (FP64 path) or NULL
     u16 src_slot[BC_MAXSRC];
     u16 src_prime[BC_MAXSRC];
     u64 pre_w[BC_MAXSRC];      // optional prescale y_i = x_i * pre_w (Shoup) -- generic hks_bconv
@@ -139,6 +143,8 @@ struct hks_ctx {
     uint2 *d_mu_mat = nullptr;          // ModUp: [qhat_{j,i}]_t split, per (level, digit)
     ulonglong2 *d_md_scale = nullptr;   // ModDown: N^-1 * phat_k^-1 mod p_k  [K]
     uint2 *d_md_mat = nullptr;          // ModDown: [phat_k]_{q_i} split  [K][L+1]
+    double *d_mu_matf = nullptr;        // ModUp matrices as 20-bit limbs in doubles (3 per entry)
+    double *d_md_matf = nullptr;        // ModDown matrix as 20-bit limbs in doubles
     ulonglong2 *d_pinv = nullptr;       // P^-1 mod q_i  [L+1] (Shoup)
 
     u32 L() const { return nq - 1; }
@@ -158,7 +164,9 @@ struct ProfScope {
     cudaStream_t s;
     cudaEvent_t a = nullptr;
     ProfScope(int c, cudaStream_t st);
-    void done(double algorithmic_bytes);
+    // algorithmic_muls: 32x32->64-bit partial products the launch needs (4 per exact 60x60-bit
+    // product; 7 wide-equivalents per Shoup butterfly: 3 for the quotient, 2 + 4/2 for the remainder)
+    void done(double algorithmic_bytes, double algorithmic_muls = 0);
 };
 
 // ----------------------------------------------------------------------------------------------
@@ -191,7 +199,8 @@ hks_status run_ntt(const hks_ctx *ctx, NttDir dir, const LimbList &L, const u64 
 // first (column) pass of the forward NTT only; the row pass is fused elsewhere (launch_ntt_kip)
 hks_status run_ntt_fwd_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in, u64 *out, cudaStream_t s);
 hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 *out, const u64 *acc,
-                           const u64 *c0, u64 galois, cudaStream_t s);
+                           const u64 *c0, u64 galois, cudaStream_t s, u32 nsplit = 0xffffffffu, u64 *out_b = nullptr,
+                           const u64 *eb_b = nullptr);
 hks_status launch_bconv(const BconvArgs &a, u32 max_ndst, cudaStream_t s);
 hks_status launch_kip(const KipArgs &a, cudaStream_t s);
 hks_status launch_automorph(const u64 *in, u64 *out, u32 nlimbs, u32 log_n, u64 galois, cudaStream_t s);

@@ -6,7 +6,20 @@
 // 60x60-bit product is four IMAD.WIDE.U32 on 30-bit halves accumulated carry-free in 64-bit
 // registers, reduced once per output (the paper's "128-bit accumulation, one reduction per
 // output").
+#include <stdlib.h>
+
 #include "internal.h"
+
+// HKS_BCONV_FP=1 enables the FP64-assisted base conversion (results are identical).  Off by default:
+// on B200 it measured slower (60 vs 52 us for the C2 ModUp conversion) because the 128-bit
+// recombination of the five FP64 limb sums makes it issue-bound (+48 % instructions); see DESIGN.md.
+static bool getenv_fp_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("HKS_BCONV_FP");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
 
 // ------------------------------------------------------------------------------------------------
 // Base conversion (§3.6.3, eq:conv):  out_t = [ sum_i y_i [qhat_i]_t ]_t.
@@ -72,6 +85,98 @@ __global__ void __launch_bounds__(256) k_bconv(const __grid_constant__ BconvArgs
     }
 }
 
+// FP64-assisted variant (B200: the FP64 pipe runs 64 DFMA/clk/SM and is otherwise idle here):
+// sources [0, NSRC - NFP) accumulate on the integer pipe (4 IMAD.WIDE per MAC), sources
+// [NSRC - NFP, NSRC) on the FP64 pipe (9 exact DFMA per MAC on 20-bit limbs), one coefficient per
+// thread; both partial sums are added as 128-bit integers before the single reduction.  The result
+// is the same integer X = sum_i y_i [qhat_i]_t, so the output is bit-identical to k_bconv.
+template <int NSRC, int NFP, bool LAZY>
+__global__ void __launch_bounds__(256) k_bconv_fp(const __grid_constant__ BconvArgs A) {
+    constexpr int NINT = NSRC - NFP;
+    const BconvGroup &G = A.g[blockIdx.y];
+    const u32 u0 = blockIdx.z * BC_TCH;
+    if (u0 >= G.ndst) return;
+    const u32 nt = min((u32)BC_TCH, G.ndst - u0);
+    __shared__ uint2 smat[(NINT > 0 ? NINT : 1) * BC_TCH];
+    __shared__ double smatf[NFP * BC_TCH * 3];
+    __shared__ PrimeConst spc[BC_TCH];
+    for (u32 idx = threadIdx.x; idx < NSRC * nt; idx += blockDim.x) {
+        const u32 i = idx / nt, u = idx - i * nt;
+        if ((int)i < NINT) {
+            smat[i * BC_TCH + u] = G.mat[(size_t)i * G.mat_stride + u0 + u];
+        } else {
+            const double *f = G.matf + ((size_t)i * G.mat_stride + u0 + u) * 3;
+            double *d = smatf + ((i - NINT) * BC_TCH + u) * 3;
+            d[0] = f[0];
+            d[1] = f[1];
+            d[2] = f[2];
+        }
+    }
+    for (u32 u = threadIdx.x; u < nt; u += blockDim.x) spc[u] = A.pc[G.dst_prime[u0 + u]];
+    __syncthreads();
+
+    const size_t N = (size_t)1 << A.log_n;
+    const size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= N) return;
+    u32 yl[NINT > 0 ? NINT : 1], yh[NINT > 0 ? NINT : 1];
+    double Y[NFP][3];
+#pragma unroll
+    for (int i = 0; i < NSRC; i++) {
+        const u64 v = A.in[(size_t)G.src_slot[i] * N + x];
+        if (i < NINT)
+            split30(v, yl[i], yh[i]);
+        else
+            split20d(v, Y[i - NINT][0], Y[i - NINT][1], Y[i - NINT][2]);
+    }
+    for (u32 u = 0; u < nt; u++) {
+        Acc30 a;
+        if (NINT > 0) {
+            const uint2 m = smat[u];
+            acc_first(a, yl[0], yh[0], m.x, m.y);
+#pragma unroll
+            for (int i = 1; i < NINT; i++) {
+                const uint2 mm = smat[i * BC_TCH + u];
+                acc_mac(a, yl[i], yh[i], mm.x, mm.y);
+            }
+        }
+        AccF f;
+        {
+            const double *m = smatf + u * 3;
+            accf_first(f, Y[0][0], Y[0][1], Y[0][2], m[0], m[1], m[2]);
+        }
+#pragma unroll
+        for (int i = 1; i < NFP; i++) {
+            const double *m = smatf + (i * BC_TCH + u) * 3;
+            accf_mac(f, Y[i][0], Y[i][1], Y[i][2], m[0], m[1], m[2]);
+        }
+        u64 lo = 0, hi = 0;
+        if (NINT > 0) acc_to128(a, lo, hi);
+        accf_add128(f, lo, hi);
+        const PrimeConst pc = spc[u];
+        A.out[(size_t)G.dst_slot[u0 + u] * N + x] = LAZY ? reduce128_lazy(lo, hi, pc) : reduce128(lo, hi, pc);
+    }
+}
+
+template <int NSRC, int NFP>
+static void bconv_fp_go(const BconvArgs &a, cudaStream_t s) {
+    const u32 threads = 256;
+    const size_t N = (size_t)1 << a.log_n;
+    u32 maxdst = 0;
+    for (u32 g = 0; g < a.ngroups; g++) maxdst = max(maxdst, a.g[g].ndst);
+    dim3 grid((u32)((N + threads - 1) / threads), a.ngroups, (maxdst + BC_TCH - 1) / BC_TCH);
+    ProfScope ps(K_BCONV, s);
+    if (a.lazy_out)
+        k_bconv_fp<NSRC, NFP, true><<<grid, threads, 0, s>>>(a);
+    else
+        k_bconv_fp<NSRC, NFP, false><<<grid, threads, 0, s>>>(a);
+    double words = 0, macs = 0;
+    for (u32 g = 0; g < a.ngroups; g++) {
+        words += a.g[g].nsrc + a.g[g].ndst;
+        macs += (double)a.g[g].nsrc * a.g[g].ndst;
+    }
+    ps.done(words * (double)N * 8.0, macs * (double)N * 4.0);
+}
+
 template <int NSRC>
 static void bconv_go(const BconvArgs &a, cudaStream_t s) {
     const u32 threads = 256;
@@ -86,13 +191,33 @@ static void bconv_go(const BconvArgs &a, cudaStream_t s) {
         k_bconv<NSRC, false, true><<<grid, threads, 0, s>>>(a);
     else
         k_bconv<NSRC, false, false><<<grid, threads, 0, s>>>(a);
-    double words = 0;
-    for (u32 g = 0; g < a.ngroups; g++) words += a.g[g].nsrc + a.g[g].ndst;
-    ps.done(words * (double)N * 8.0);
+    double words = 0, macs = 0;
+    for (u32 g = 0; g < a.ngroups; g++) {
+        words += a.g[g].nsrc + a.g[g].ndst;
+        macs += (double)a.g[g].nsrc * a.g[g].ndst;
+    }
+    ps.done(words * (double)N * 8.0, macs * (double)N * 4.0);
 }
 
 hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
     // all groups of one launch share nsrc (the caller groups them so)
+    if (!a.prescale && a.g[0].matf && getenv_fp_enabled()) {
+        // FP64-pipe share chosen so both pipes carry similar work: 16 NINT + 56 ~ 18 NFP + 10 cycles
+        switch (a.g[0].nsrc) {
+            case 6: bconv_fp_go<6, 3>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            case 7: bconv_fp_go<7, 4>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            case 8: bconv_fp_go<8, 4>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            case 9: bconv_fp_go<9, 5>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            case 10: bconv_fp_go<10, 6>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            case 11: bconv_fp_go<11, 6>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            case 12: bconv_fp_go<12, 7>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            case 13: bconv_fp_go<13, 7>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            case 14: bconv_fp_go<14, 8>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            case 15: bconv_fp_go<15, 8>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            case 16: bconv_fp_go<16, 9>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            default: break;
+        }
+    }
     switch (a.g[0].nsrc) {
 #define C(NS) case NS: bconv_go<NS>(a, s); break;
         C(1) C(2) C(3) C(4) C(5) C(6) C(7) C(8) C(9) C(10) C(11) C(12) C(13) C(14) C(15) C(16)
@@ -162,7 +287,8 @@ hks_status launch_kip(const KipArgs &a, cudaStream_t s) {
     ProfScope ps(K_KIP, s);
     k_kip<<<grid, threads, 0, s>>>(a);
     HKS_CHECK_LAUNCH();
-    ps.done((3.0 * a.beta + 2.0) * a.ne * (double)N * 8.0);   // D_j + (b_j, a_j) read, acc0/acc1 written
+    ps.done((3.0 * a.beta + 2.0) * a.ne * (double)N * 8.0,    // D_j + (b_j, a_j) read, acc0/acc1 written
+            (double)a.ne * a.beta * 2.0 * (double)N * 4.0);
     return HKS_OK;
 }
 

@@ -76,6 +76,65 @@ HKS_DEV void split30(u64 y, u32 &lo, u32 &hi) {
     hi = h;
 }
 
+// 128-bit value of an Acc30 accumulator:  s0 + (s1a + s1b) 2^30 + s2 2^60.
+HKS_DEV void acc_to128(const Acc30 &a, u64 &lo, u64 &hi) {
+    u64 t;
+    lo = a.s0;
+    hi = 0;
+    t = a.s1a << 30; lo += t; hi += (lo < t); hi += a.s1a >> 34;
+    t = a.s1b << 30; lo += t; hi += (lo < t); hi += a.s1b >> 34;
+    t = a.s2 << 60;  lo += t; hi += (lo < t); hi += a.s2 >> 4;
+}
+
+// ---- FP64-pipe partial dot products (k_bconv_fp): 60-bit operands as three exact 20-bit limbs in
+// doubles; every product < 2^40 and every partial sum < 2^46 is an integer below 2^53, so DFMA is
+// exact.  Five accumulators C_c = sum_{a+b=c} Y_a M_b give X = sum_c C_c 2^(20c).
+struct AccF {
+    double c[5];
+};
+
+HKS_DEV double exact_dbl(u32 v) {   // v < 2^52: 2^52 + v has v as its mantissa
+    return __longlong_as_double(0x4330000000000000ll | (long long)v) - 4503599627370496.0;
+}
+
+HKS_DEV void split20d(u64 y, double &y0, double &y1, double &y2) {
+    y0 = exact_dbl((u32)y & 0xfffffu);
+    y1 = exact_dbl((u32)(y >> 20) & 0xfffffu);
+    y2 = exact_dbl((u32)(y >> 40));
+}
+
+HKS_DEV void accf_first(AccF &A, double y0, double y1, double y2, double m0, double m1, double m2) {
+    A.c[0] = y0 * m0;
+    A.c[1] = fma(y1, m0, y0 * m1);
+    A.c[2] = fma(y2, m0, fma(y1, m1, y0 * m2));
+    A.c[3] = fma(y2, m1, y1 * m2);
+    A.c[4] = y2 * m2;
+}
+
+HKS_DEV void accf_mac(AccF &A, double y0, double y1, double y2, double m0, double m1, double m2) {
+    A.c[0] = fma(y0, m0, A.c[0]);
+    A.c[1] = fma(y1, m0, fma(y0, m1, A.c[1]));
+    A.c[2] = fma(y2, m0, fma(y1, m1, fma(y0, m2, A.c[2])));
+    A.c[3] = fma(y2, m1, fma(y1, m2, A.c[3]));
+    A.c[4] = fma(y2, m2, A.c[4]);
+}
+
+HKS_DEV u64 dbl_int(double c) {    // c integral in [0, 2^52)
+    return (u64)(__double_as_longlong(c + 4503599627370496.0) - 0x4330000000000000ll);
+}
+
+// (lo, hi) += sum_c C_c 2^(20c)
+HKS_DEV void accf_add128(const AccF &A, u64 &lo, u64 &hi) {
+    const u64 c0 = dbl_int(A.c[0]), c1 = dbl_int(A.c[1]), c2 = dbl_int(A.c[2]), c3 = dbl_int(A.c[3]),
+              c4 = dbl_int(A.c[4]);
+    u64 t;
+    t = c0;       lo += t; hi += (lo < t);
+    t = c1 << 20; lo += t; hi += (lo < t); hi += c1 >> 44;
+    t = c2 << 40; lo += t; hi += (lo < t); hi += c2 >> 24;
+    t = c3 << 60; lo += t; hi += (lo < t); hi += c3 >> 4;
+    hi += c4 << 16;
+}
+
 // canonical X mod p for the accumulated 128-bit value (< 2^124, i.e. <= 16 terms of 60x60 bits).
 HKS_DEV u64 acc_reduce(const Acc30 &a, const PrimeConst &c) {
     // lo/hi of s0 + (s1a << 30) + (s1b << 30) + (s2 << 60)
@@ -229,4 +288,16 @@ HKS_DEV u64 acc_reduce_lazy(const Acc30 &a, const PrimeConst &c) {
     t = a.s2 << 60;  lo += t; hi += (lo < t); hi += a.s2 >> 4;
     const u64 np = 0 - c.p;
     return shoup_approx(hi, c.r64, c.r64p, np) + shoup_approx(lo, 1, c.one_p, np);   // [0, 8p)
+}
+
+// X = hi 2^64 + lo (hi < 2^62) reduced to [0, 8p) with two approximate-quotient Shoup steps.
+HKS_DEV u64 reduce128_lazy(u64 lo, u64 hi, const PrimeConst &c) {
+    const u64 np = 0 - c.p;
+    return shoup_approx(hi, c.r64, c.r64p, np) + shoup_approx(lo, 1, c.one_p, np);
+}
+
+HKS_DEV u64 reduce128(u64 lo, u64 hi, const PrimeConst &c) {
+    u64 r = shoup_lazy(hi, c.r64, c.r64p, c.p) + (lo - mulhi64(lo, c.one_p) * c.p);   // [0, 4p)
+    r = csub(r, 2 * c.p);
+    return csub(r, c.p);
 }

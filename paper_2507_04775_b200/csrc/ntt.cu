@@ -24,8 +24,12 @@
 // elements a thread holds (radix-2^LOGE rounds); LOGNB = log2 of the sub-transforms per CTA;
 // LOGC = log2 of the row length C (the column stride).  COLS: sub-transforms are columns (stride C);
 // else rows (contiguous).  Values between butterflies live in the lazy ranges of modarith.cuh.
+#ifndef HKS_NTT_MINB
+#define HKS_NTT_MINB 4
+#endif
 template <int LOGN, int LOGE, int LOGNB, int LOGC, bool COLS, bool FWD, int EPI>
-__global__ void __launch_bounds__((1 << LOGNB) << (LOGN - LOGE))
+__global__ void __launch_bounds__((1 << LOGNB) << (LOGN - LOGE),
+                                  (((1 << LOGNB) << (LOGN - LOGE)) >= 512) ? 2 : HKS_NTT_MINB)
 k_ntt(const __grid_constant__ NttArgs A) {
     constexpr int n = 1 << LOGN;
     constexpr int E = 1 << LOGE;
@@ -50,8 +54,10 @@ k_ntt(const __grid_constant__ NttArgs A) {
     // element j of this thread's sub-transform lives at src_sub[j * JS]
     constexpr int JS = COLS ? C : 1;
     const size_t sub_off = COLS ? (size_t)(tile * NB + bsub) : (size_t)(tile * NB + bsub) * n;
+    const bool second = b >= A.nsplit;                 // second polynomial of a merged ModDown
+    u64 *const out_base = second ? A.out_b : A.out;
     const u64 *__restrict__ src = A.in + (size_t)A.map.sin[b] * N + sub_off;
-    u64 *__restrict__ dst = A.out + (size_t)A.map.sout[b] * N + sub_off;
+    u64 *__restrict__ dst = out_base + (size_t)A.map.sout[b] * N + sub_off;
     const ulonglong2 *__restrict__ tw =
         COLS ? A.tw + (size_t)prime * n : A.tw + (((size_t)prime << A.log_r) + tile * NB + bsub) * n;
 
@@ -67,8 +73,10 @@ k_ntt(const __grid_constant__ NttArgs A) {
     if (EPI == EPI_MODDOWN) {
         pinv = A.pinv[prime];
         ea = A.ea + (size_t)A.map.sa[b] * N + sub_off;
-        eb = (A.eb && A.map.sb[b] != 0xffff) ? A.eb + (size_t)A.map.sb[b] * N : nullptr;
+        const u64 *ebase = second ? A.eb_b : A.eb;
+        eb = (ebase && A.map.sb[b] != 0xffff) ? ebase + (size_t)A.map.sb[b] * N : nullptr;
     }
+    const u64 galois = second ? 1 : A.galois;
     auto epi = [&](u64 x, int j) -> u64 {
         if (EPI == EPI_LAZY) return x;
         if (EPI == EPI_SCALE) return csub(csub(shoup_approx(x, sc.x, sc.y, m.np), m.two_p), m.p);
@@ -78,7 +86,7 @@ k_ntt(const __grid_constant__ NttArgs A) {
         r = csub(csub(r, m.two_p), m.p);
         if (eb) {
             const u32 xg = (u32)(sub_off + (size_t)j * JS);
-            r = csub(r + eb[A.galois == 1 ? xg : automorph_src(xg, log_n, A.galois)], m.p);
+            r = csub(r + eb[galois == 1 ? xg : automorph_src(xg, log_n, galois)], m.p);
         }
         return r;
     };
@@ -179,7 +187,7 @@ k_ntt(const __grid_constant__ NttArgs A) {
         // All global operands of the epilogue are loaded first so their latencies overlap.
         __syncthreads();
         const size_t tbase = (size_t)tile * NB * n;
-        u64 *__restrict__ tdst = A.out + (size_t)A.map.sout[b] * N + tbase;
+        u64 *__restrict__ tdst = out_base + (size_t)A.map.sout[b] * N + tbase;
         constexpr int CH = E < 8 ? E : 8;   // epilogue chunk: loads of a chunk are issued together
 #pragma unroll
         for (int q0 = 0; q0 < E; q0 += CH) {
@@ -192,7 +200,7 @@ k_ntt(const __grid_constant__ NttArgs A) {
 #pragma unroll
                     for (int q = 0; q < CH; q++) {
                         const u32 xg = (u32)(tbase + tid + (q0 + q) * NT);
-                        bv[q] = eb[A.galois == 1 ? xg : automorph_src(xg, log_n, A.galois)];
+                        bv[q] = eb[galois == 1 ? xg : automorph_src(xg, log_n, galois)];
                     }
                 }
             }
@@ -235,42 +243,45 @@ static hks_status go(NttArgs &a, cudaStream_t s) {
     // algorithmic bytes: each limb read once and written once (+ ModDown operands acc, c0)
     double words = 2.0 * a.nlimbs;
     if (EPI == EPI_MODDOWN) words += a.nlimbs * (a.eb ? 2.0 : 1.0);
-    ps.done(words * (double)(1ull << a.log_n) * 8.0);
+    // butterflies of this pass: N/2 per stage, LOGN stages; +1 Shoup per element for SCALE/MODDOWN
+    const double nn = (double)(1ull << a.log_n);
+    double muls = a.nlimbs * (nn / 2.0) * LOGN * 7.0;
+    if (EPI == EPI_SCALE || EPI == EPI_MODDOWN) muls += a.nlimbs * nn * 7.0;
+    ps.done(words * nn * 8.0, muls);
     return HKS_OK;
 }
 
-// per ring size: sub-transform shapes for the column pass (length R) and the row pass (length C)
-#define NTT_SHAPES(X)                  \
-    X(17, 9, 4, 3, 8, 4, 4)            \
-    X(16, 8, 4, 4, 8, 4, 4)            \
-    X(15, 8, 4, 4, 7, 4, 4)            \
-    X(14, 7, 4, 4, 7, 4, 4)            \
-    X(13, 7, 4, 4, 6, 3, 4)            \
-    X(12, 6, 3, 4, 6, 3, 4)            \
-    X(11, 6, 3, 4, 5, 3, 4)            \
-    X(10, 5, 3, 4, 5, 3, 4)
+template <int LR, int ER, int BR, int LC, int EC, int BC>
+static hks_status dispatch(NttDir dir, bool cols, int epi, NttArgs &a, cudaStream_t s) {
+    if (dir == NTT_FWD && cols) return go<LR, ER, BR, LC, true, true, EPI_LAZY>(a, s);
+    if (dir == NTT_FWD && epi == EPI_CANON) return go<LC, EC, BC, LC, false, true, EPI_CANON>(a, s);
+    if (dir == NTT_FWD && epi == EPI_MODDOWN) return go<LC, EC, BC, LC, false, true, EPI_MODDOWN>(a, s);
+    if (dir == NTT_INV && !cols) return go<LC, EC, BC, LC, false, false, EPI_LAZY>(a, s);
+    if (dir == NTT_INV && cols) return go<LR, ER, BR, LC, true, false, EPI_SCALE>(a, s);
+    HKS_FAIL(HKS_EINVAL, "ntt: unsupported epilogue %d", epi);
+}
 
+// Per ring size: sub-transform shapes (log length, log elements per thread, log sub-transforms per
+// CTA) of the column pass (length R) and the row pass (length C).  Batches too small to fill two
+// waves of 256-thread CTAs use radix-8 rounds (E = 8, twice the warps per tile) at N = 2^16 / 2^17.
 hks_status launch_ntt_pass(const hks_ctx *ctx, NttDir dir, int pass, int epi, NttArgs &a, cudaStream_t s) {
     a.log_n = ctx->log_n;
     a.log_r = ctx->log_r;
     a.log_c = ctx->log_c;
     const bool cols = (dir == NTT_FWD) ? (pass == 0) : (pass == 1);
+    const bool small = a.nlimbs * 16u < 2u * 148u * 4u;
     switch (ctx->log_n) {
-#define X(LN, LR, ER, BR, LC, EC, BC)                                                               \
-    case LN:                                                                                        \
-        if (dir == NTT_FWD && cols) return go<LR, ER, BR, LC, true, true, EPI_LAZY>(a, s);          \
-        if (dir == NTT_FWD && epi == EPI_CANON) return go<LC, EC, BC, LC, false, true, EPI_CANON>(a, s); \
-        if (dir == NTT_FWD && epi == EPI_MODDOWN)                                                   \
-            return go<LC, EC, BC, LC, false, true, EPI_MODDOWN>(a, s);                              \
-        if (dir == NTT_INV && !cols) return go<LC, EC, BC, LC, false, false, EPI_LAZY>(a, s);       \
-        if (dir == NTT_INV && cols) return go<LR, ER, BR, LC, true, false, EPI_SCALE>(a, s);        \
-        break;
-        NTT_SHAPES(X)
-#undef X
-        default:
-            break;
+        case 17: return small ? dispatch<9, 3, 3, 8, 3, 4>(dir, cols, epi, a, s) : dispatch<9, 4, 3, 8, 4, 4>(dir, cols, epi, a, s);
+        case 16: return small ? dispatch<8, 3, 4, 8, 3, 4>(dir, cols, epi, a, s) : dispatch<8, 4, 4, 8, 4, 4>(dir, cols, epi, a, s);
+        case 15: return dispatch<8, 4, 4, 7, 4, 4>(dir, cols, epi, a, s);
+        case 14: return dispatch<7, 4, 4, 7, 4, 4>(dir, cols, epi, a, s);
+        case 13: return dispatch<7, 4, 4, 6, 3, 4>(dir, cols, epi, a, s);
+        case 12: return dispatch<6, 3, 4, 6, 3, 4>(dir, cols, epi, a, s);
+        case 11: return dispatch<6, 3, 4, 5, 3, 4>(dir, cols, epi, a, s);
+        case 10: return dispatch<5, 3, 4, 5, 3, 4>(dir, cols, epi, a, s);
+        default: break;
     }
-    HKS_FAIL(HKS_EINVAL, "ntt: unsupported log_n %u / epilogue %d", ctx->log_n, epi);
+    HKS_FAIL(HKS_EINVAL, "ntt: unsupported log_n %u", ctx->log_n);
 }
 
 static void fill_map(NttArgs &a, const LimbList &L, size_t off, u32 cnt, bool second_pass) {
@@ -292,6 +303,7 @@ hks_status run_ntt(const hks_ctx *ctx, NttDir dir, const LimbList &L, const u64 
         a.pc = ctx->d_pc;
         a.ninv = ctx->d_ninv;
         a.galois = 1;
+        a.nsplit = 0xffffffffu;
         // pass 0
         fill_map(a, L, off, cnt, false);
         a.in = in;
@@ -322,6 +334,7 @@ hks_status run_ntt_fwd_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in
         a.pc = ctx->d_pc;
         a.ninv = ctx->d_ninv;
         a.galois = 1;
+        a.nsplit = 0xffffffffu;
         fill_map(a, L, off, cnt, false);
         a.in = in;
         a.out = out;
@@ -333,7 +346,8 @@ hks_status run_ntt_fwd_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in
 }
 
 hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 *out, const u64 *acc,
-                           const u64 *c0, u64 galois, cudaStream_t s) {
+                           const u64 *c0, u64 galois, cudaStream_t s, u32 nsplit, u64 *out_b, const u64 *eb_b) {
+    if (nsplit != 0xffffffffu && L.size() > HKS_MAXB) HKS_FAIL(HKS_EINVAL, "moddown: merged batch too large");
     for (size_t off = 0; off < L.size(); off += HKS_MAXB) {
         u32 cnt = (u32)((L.size() - off) < HKS_MAXB ? (L.size() - off) : HKS_MAXB);
         NttArgs a{};
@@ -341,6 +355,7 @@ hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 
         a.ninv = ctx->d_ninv;
         a.pinv = ctx->d_pinv;
         a.galois = galois;
+        a.nsplit = 0xffffffffu;   // pass 0 stays in buf; only the epilogue pass splits
         // pass 0: columns, in place on buf (slots sin)
         for (u32 i = 0; i < cnt; i++) {
             a.map.sin[i] = L.sin[off + i];
@@ -353,8 +368,11 @@ hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 
         a.tw = ctx->d_tw_col_fwd;
         hks_status st = launch_ntt_pass(ctx, NTT_FWD, 0, EPI_LAZY, a, s);
         if (st != HKS_OK) return st;
-        // pass 1: rows, buf -> out with the ModDown epilogue
+        // pass 1: rows, buf -> out (limbs >= nsplit -> out_b) with the ModDown epilogue
         fill_map(a, L, off, cnt, false);
+        a.nsplit = nsplit;
+        a.out_b = out_b;
+        a.eb_b = eb_b;
         a.in = buf;
         a.out = out;
         a.ea = acc;
@@ -373,7 +391,8 @@ hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 
 // acc_p = sum_j canon(D_j) * evk_j[p] with the 30-bit-split IMAD.WIDE accumulation (one reduction
 // per output).  D never returns to HBM.
 template <int LOGN, int LOGE, int LOGNB, int NDIG>
-__global__ void __launch_bounds__(NDIG * ((1 << LOGNB) << (LOGN - LOGE)))
+__global__ void __launch_bounds__(NDIG * ((1 << LOGNB) << (LOGN - LOGE)),
+                                  (NDIG * ((1 << LOGNB) << (LOGN - LOGE))) >= 384 ? 2 : 3)
 k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
     constexpr int n = 1 << LOGN;
     constexpr int E = 1 << LOGE;
@@ -525,7 +544,9 @@ static hks_status go_kip(FusedKipArgs &a, cudaStream_t s) {
     for (u32 u = 0; u < a.nu; u++)
         for (u32 j = 0; j < a.ndig; j++) (a.map.dsrc[u][j] & FK_DIRECT) ? ndirect++ : nntt++;
     // algorithmic words: D read once (pass-1 output or c1), key 2 limbs per (u, j), acc 2 limbs per u
-    ps.done(((double)nntt + ndirect + 2.0 * a.nu * a.ndig + 2.0 * a.nu) * (double)(1ull << a.log_n) * 8.0);
+    const double nn = (double)(1ull << a.log_n);
+    const double muls = nntt * (nn / 2.0) * a.log_c * 7.0 + (double)a.nu * a.ndig * 2.0 * nn * 4.0;
+    ps.done(((double)nntt + ndirect + 2.0 * a.nu * a.ndig + 2.0 * a.nu) * nn * 8.0, muls);
     return HKS_OK;
 }
 
@@ -547,8 +568,8 @@ hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s) {
     a.log_c = ctx->log_c;
     if (a.ndig > FK_MAXD || a.nu > FK_MAXU) HKS_FAIL(HKS_EINVAL, "ntt_kip: %u digits / %u limbs per launch", a.ndig, a.nu);
     switch (ctx->log_n) {
-        case 17: return go_kip_d<8, 4, 3>(a, s);
-        case 16: return go_kip_d<8, 4, 3>(a, s);
+        case 17: return a.ndig > 3 ? go_kip_d<8, 4, 2>(a, s) : go_kip_d<8, 4, 3>(a, s);
+        case 16: return a.ndig > 3 ? go_kip_d<8, 4, 2>(a, s) : go_kip_d<8, 4, 3>(a, s);
         case 15: return go_kip_d<7, 4, 3>(a, s);
         case 14: return go_kip_d<7, 4, 3>(a, s);
         case 13: return go_kip_d<6, 3, 3>(a, s);

@@ -12,7 +12,7 @@ std::atomic<int> g_on{0};
 struct Rec {
     int cls;
     cudaEvent_t a, b;
-    double bytes;
+    double bytes, muls;
 };
 std::mutex g_mu;
 std::vector<Rec> g_recs;
@@ -40,13 +40,13 @@ ProfScope::ProfScope(int c, cudaStream_t st) : cls(c), s(st) {
     }
 }
 
-void ProfScope::done(double bytes) {
+void ProfScope::done(double bytes, double muls) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (!a) return;
     cudaEvent_t b = get_event();
     cudaEventRecord(b, s);
     std::lock_guard<std::mutex> l(g_mu);
-    g_recs.push_back(Rec{cls, a, b, bytes});
+    g_recs.push_back(Rec{cls, a, b, bytes, muls});
     a = nullptr;
 }
 
@@ -64,7 +64,7 @@ extern "C" int hks_prof_read(hks_prof_entry *out, int max) {
         recs.swap(g_recs);
     }
     uint64_t n[K_NCLS] = {0};
-    double ms[K_NCLS] = {0}, by[K_NCLS] = {0};
+    double ms[K_NCLS] = {0}, by[K_NCLS] = {0}, mu[K_NCLS] = {0};
     for (auto &r : recs) {
         float t = 0.f;
         cudaEventSynchronize(r.b);
@@ -72,6 +72,7 @@ extern "C" int hks_prof_read(hks_prof_entry *out, int max) {
         n[r.cls]++;
         ms[r.cls] += t;
         by[r.cls] += r.bytes;
+        mu[r.cls] += r.muls;
     }
     {
         std::lock_guard<std::mutex> l(g_mu);
@@ -88,6 +89,7 @@ extern "C" int hks_prof_read(hks_prof_entry *out, int max) {
         out[k].launches = n[c];
         out[k].total_ms = ms[c];
         out[k].bytes = by[c];
+        out[k].muls = mu[c];
         k++;
     }
     return k;

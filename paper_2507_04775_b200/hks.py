@@ -21,7 +21,8 @@ MAX_DIGITS = 64
 # every symbol include/hks.h declares (checked by tests/test_capi.py)
 EXPORTS = ("hks_last_error", "hks_ctx_create", "hks_ctx_destroy", "hks_ctx_query", "hks_ctx_psi",
            "hks_workspace_bytes", "hks_ntt_fwd", "hks_ntt_inv", "hks_bconv", "hks_modup",
-           "hks_ksk_inner_product", "hks_moddown", "hks_keyswitch", "hks_automorph", "hks_rotate_hoisted",
+           "hks_ksk_inner_product", "hks_moddown", "hks_keyswitch", "hks_relinearize", "hks_automorph",
+           "hks_rotate_hoisted",
            "hks_launch_count", "hks_prof_enable", "hks_prof_read", "hks_shard_query", "hks_shard_workspace_bytes",
            "hks_shard_ks_modup_in", "hks_shard_ks_inner", "hks_shard_ks_moddown_out")
 
@@ -34,7 +35,7 @@ class HksError(RuntimeError):
 
 class ProfEntry(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_uint64), ("total_ms", ctypes.c_double),
-                ("bytes", ctypes.c_double)]
+                ("bytes", ctypes.c_double), ("muls", ctypes.c_double)]
 
 
 class ShardInfo(ctypes.Structure):
@@ -80,6 +81,7 @@ def lib() -> ctypes.CDLL:
         L.hks_moddown.argtypes = [_vp, _vp, _u32, _vp, _vp, _vp]
         L.hks_keyswitch.argtypes = [_vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp]
         L.hks_automorph.argtypes = [_vp, _vp, _u32, _u64, _vp, _vp]
+        L.hks_relinearize.argtypes = [_vp, _vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp]
         L.hks_rotate_hoisted.argtypes = [_vp, _vp, _vp, _u32, _u32, ctypes.POINTER(_u64), ctypes.POINTER(_vp),
                                          ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp]
         L.hks_launch_count.restype = ctypes.c_uint64
@@ -212,6 +214,11 @@ def keyswitch(ctx: Context, c0, c1, level: int, evk, out0, out1, ws, stream=None
                                _stream(stream)), "hks_keyswitch")
 
 
+def relinearize(ctx: Context, d0, d1, d2, level: int, evk, out0, out1, ws, stream=None):
+    _check(lib().hks_relinearize(ctx.handle, _ptr(d0), _ptr(d1), _ptr(d2), level, _ptr(evk), _ptr(out0), _ptr(out1),
+                                 _ptr(ws), _stream(stream)), "hks_relinearize")
+
+
 def automorph(ctx: Context, x, nlimbs: int, galois: int, out, stream=None):
     _check(lib().hks_automorph(ctx.handle, _ptr(x), nlimbs, galois, _ptr(out), _stream(stream)), "hks_automorph")
 
@@ -236,11 +243,11 @@ def prof_enable(on: bool = True):
 
 
 def prof_read() -> dict:
-    """{kernel class: (launches, total_ms, algorithmic_bytes)} since the last read (synchronises)."""
+    """{kernel class: (launches, total_ms, algorithmic_bytes, algorithmic_muls)} since the last read."""
     arr = (ProfEntry * 16)()
     k = lib().hks_prof_read(arr, 16)
-    return {arr[i].name.decode(): (int(arr[i].launches), float(arr[i].total_ms), float(arr[i].bytes))
-            for i in range(k)}
+    return {arr[i].name.decode(): (int(arr[i].launches), float(arr[i].total_ms), float(arr[i].bytes),
+                                   float(arr[i].muls)) for i in range(k)}
 
 
 # ---- limb-sharded KeySwitch (C4): phases of include/hks.h; the all-gathers are the caller's

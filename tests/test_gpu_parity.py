@@ -288,3 +288,45 @@ def test_error_codes(orc):
     with pytest.raises(H.HksError) as e:
         H.modup(ctx, x, 7, x, x)                             # level > L
     assert e.value.status == 1
+
+
+@pytest.mark.parametrize("name,level", [("T12", 6), ("T12", 3), ("C2", 29), ("C2", 12)])
+def test_relinearize_parity(orc, name, level):
+    """HMult relinearisation: (d0, d1, d2) -> (d0 + ModDown(acc0), d1 + ModDown(acc1)); bit-exact with the
+    oracle's KeySwitch(d0, d2) plus d1, and Dec(out) = d0 + d1 s + d2 s^2 within the bound."""
+    cfg, ctx, o = ctxs(orc, name)
+    keys, evk = relin_key(o, name)
+    g = S.rng(cfg.seed + 31 + level)
+    qidx = list(range(level + 1))
+    d0, d1, d2 = (S.uniform_limbs(g, o.q[: level + 1], o.n) for _ in range(3))
+    out0, out1 = empty_dev(d0.shape), empty_dev(d0.shape)
+    ws = ctx.workspace(H.OP_KEYSWITCH, level)
+    H.relinearize(ctx, to_dev(d0), to_dev(d1), to_dev(d2), level, to_dev(evk), out0, out1, ws)
+    w0, w1 = o.keyswitch(d0, d2, evk, level)
+    w1 = o.add(w1, d1, qidx)
+    got0, got1 = to_host(out0), to_host(out1)
+    assert (got0 == w0).all() and (got1 == w1).all()
+    # decryption: out0 + out1 s == d0 + d1 s + d2 s^2 + e_ks
+    s_ev = keys.s_eval[: level + 1]
+    s2 = o.mul(s_ev, s_ev, qidx)
+    ref = o.intt(o.add(o.add(d0, o.mul(d1, s_ev, qidx), qidx), o.mul(d2, s2, qidx), qidx), qidx)
+    dec = o.decrypt_coeff(got0, got1, keys.s_eval, level)
+    diff = o.crt_centered(o.sub(dec, ref, qidx), level)
+    assert max(abs(v) for v in diff) <= ks_bound(o, level, keys.B_e, keys.h)
+
+
+def test_bconv_fp64_path_identical(orc):
+    """The FP64-assisted conversion (HKS_BCONV_FP=1) must produce the same KeySwitch bits."""
+    import subprocess, sys, os
+    code = ("import sys; sys.path.insert(0, 'tests'); sys.path.insert(0, '.');"
+            "import numpy as np, hks_synth as S, oracle; from helpers import *;"
+            "from paper_2507_04775_b200 import hks as H;"
+            "cfg=S.config('C2'); ctx=H.Context.from_config(cfg,0); o=oracle.Ctx.from_config(cfg); g=S.rng(9);"
+            "nk=o.nq+o.np; evk=np.stack([S.uniform_limbs(g,o.primes,o.n) for _ in range(2*o.dnum)]).reshape(o.dnum,2,nk,o.n);"
+            "c0=S.uniform_limbs(g,o.q,o.n); c1=S.uniform_limbs(g,o.q,o.n); a,b=empty_dev(c0.shape),empty_dev(c0.shape);"
+            "H.keyswitch(ctx,to_dev(c0),to_dev(c1),29,to_dev(evk),a,b,ctx.workspace(H.OP_KEYSWITCH,29));"
+            "w0,w1=o.keyswitch(c0,c1,evk,29); assert (to_host(a)==w0).all() and (to_host(b)==w1).all(); print('ok')")
+    env = dict(os.environ, HKS_BCONV_FP="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
