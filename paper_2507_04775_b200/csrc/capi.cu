@@ -115,47 +115,43 @@ hks_status modup_core(const hks_ctx *c, const u64 *d, u32 level, u64 *ext, u64 *
 }
 
 // Fused row pass + key inner product for the KeySwitch (own-digit limbs read from c1, EVAL).
+// y != NULL: P-limb tiles also run ModDown's first inverse-NTT pass and write it to y [2][K][N]
+// (needs beta >= 2: two thread groups for the two accumulators).
 hks_status ntt_kip_core(const hks_ctx *c, const u64 *ext, const u64 *c1, const u64 *evk, u32 level, u64 *acc,
-                        cudaStream_t s) {
+                        cudaStream_t s, u64 *y = nullptr) {
     const u32 ne = c->ne(level), beta = c->beta(level);
-    for (u32 u0 = 0; u0 < ne; u0 += FK_MAXU) {
-        FusedKipArgs a{};
-        a.ext = ext;
-        a.c1 = c1;
-        a.evk = evk;
-        a.acc = acc;
-        a.pc = c->d_pc;
-        a.tw = c->d_tw_row_fwd;
-        a.nu = std::min<u32>(FK_MAXU, ne - u0);
-        a.ndig = beta;
-        a.nkey = c->nq + c->np;
-        a.acc_stride = ne;
-        for (u32 u = 0; u < a.nu; u++) {
-            const u32 t = u0 + u, pr = c->ext_prime(level, t);
-            a.map.prime[u] = (u16)pr;
-            a.map.kslot[u] = (u16)pr;
-            a.map.aslot[u] = (u16)t;
-            for (u32 j = 0; j < beta; j++) {
-                const bool own = t <= level && t >= c->digit_lo(j) && t < c->digit_hi(level, j);
-                a.map.dsrc[u][j] = own ? (u16)(FK_DIRECT | t) : (u16)(j * ne + t);
-            }
+    std::vector<KipItem> items(ne);
+    for (u32 t = 0; t < ne; t++) {
+        KipItem &it = items[t];
+        it.prime = it.kslot = (u16)c->ext_prime(level, t);
+        it.aslot = (u16)t;
+        if (y && t > level) it.yslot = (u16)(t - level - 1);
+        for (u32 j = 0; j < beta; j++) {
+            const bool own = t <= level && t >= c->digit_lo(j) && t < c->digit_hi(level, j);
+            it.src[j] = own ? (u16)(FK_DIRECT | t) : (u16)(j * ne + t);
         }
-        hks_status st = launch_ntt_kip(c, a, s);
-        if (st != HKS_OK) return st;
     }
-    return HKS_OK;
+    return run_ntt_kip(c, items, beta, ext, c1, evk, acc, c->nq + c->np, ne, s, y, c->np);
 }
 
 // ModDown of npoly accumulators (acc poly p at slots p * ne + t) into out[p] (+ adds[p], read through
 // the automorphism `galois` for p = 0).  ws: y [npoly][K][N] then conv [npoly][l+1][N].
 hks_status moddown_core(const hks_ctx *c, const u64 *acc, u32 npoly, u32 level, u64 *const *outs, const u64 *c0,
-                        u64 galois, u64 *ws, cudaStream_t s, const u64 *c1add = nullptr) {
+                        u64 galois, u64 *ws, cudaStream_t s, const u64 *c1add = nullptr, bool y_rows_done = false) {
     const u32 ne = c->ne(level), K = c->np;
     u64 *y = ws, *conv = ws + (size_t)npoly * K * c->n;
-    LimbList L;
-    for (u32 p = 0; p < npoly; p++)
-        for (u32 k = 0; k < K; k++) L.push(p * ne + level + 1 + k, p * K + k, c->nq + k);
-    hks_status st = run_ntt(c, NTT_INV, L, acc, y, c->d_md_scale, K, s);
+    hks_status st;
+    if (y_rows_done) {          // the inverse row pass already ran inside k_ntt_kip (y holds it)
+        LimbList Y;
+        for (u32 p = 0; p < npoly; p++)
+            for (u32 k = 0; k < K; k++) Y.push(p * K + k, p * K + k, c->nq + k);
+        st = run_ntt_inv_cols(c, Y, y, y, c->d_md_scale, K, s);
+    } else {
+        LimbList L;
+        for (u32 p = 0; p < npoly; p++)
+            for (u32 k = 0; k < K; k++) L.push(p * ne + level + 1 + k, p * K + k, c->nq + k);
+        st = run_ntt(c, NTT_INV, L, acc, y, c->d_md_scale, K, s);
+    }
     if (st != HKS_OK) return st;
     std::vector<BconvGroup> groups;
     std::vector<u16> dp(level + 1);
@@ -427,16 +423,19 @@ static hks_status keyswitch_impl(const hks_ctx *c, const uint64_t *c0, const uin
     u64 *ext = coef + l1 * c->n;
     u64 *acc = ext + beta * ne * c->n;
     u64 *md = acc + 2 * ne * c->n;
-    if (beta <= FK_MAXD) {
-        // INTT + BConv + NTT column pass, then the fused NTT row pass + key inner product
+    const bool fused = beta <= FK_MAXD;
+    const bool ymode = fused && beta >= 2 && 2 * c->np <= HKS_MAXB;
+    if (fused) {
+        // INTT + BConv + NTT column pass, then the fused NTT row pass + key inner product (+ for the P
+        // limbs, ModDown's inverse row pass straight into the ModDown workspace)
         if ((st = modup_core(c, c1, level, ext, coef, s, false)) != HKS_OK) return st;
-        if ((st = ntt_kip_core(c, ext, c1, evk, level, acc, s)) != HKS_OK) return st;
+        if ((st = ntt_kip_core(c, ext, c1, evk, level, acc, s, ymode ? md : nullptr)) != HKS_OK) return st;
     } else {
         if ((st = modup_core(c, c1, level, ext, coef, s)) != HKS_OK) return st;
         if ((st = kip_core(c, ext, c1, evk, level, 1, acc, s)) != HKS_OK) return st;
     }
     u64 *outs[2] = {out0, out1};
-    return moddown_core(c, acc, 2, level, outs, c0, 1, md, s, add1);
+    return moddown_core(c, acc, 2, level, outs, c0, 1, md, s, add1, ymode);
 }
 
 extern "C" hks_status hks_automorph(const hks_ctx *c, const uint64_t *in, uint32_t nlimbs, uint64_t galois,

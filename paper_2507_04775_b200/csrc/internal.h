@@ -10,6 +10,7 @@
 #include "modarith.cuh"
 
 typedef uint16_t u16;
+typedef uint8_t u8;
 
 // ----------------------------------------------------------------------------------------------
 // Limb batches.  One kernel launch transforms up to HKS_MAXB limbs of N words; limb b reads slot
@@ -108,7 +109,10 @@ struct FusedKipMap {
     u16 prime[FK_MAXU];
     u16 kslot[FK_MAXU];
     u16 aslot[FK_MAXU];
-    u16 dsrc[FK_MAXU][FK_MAXD];
+    u16 dsrc[FK_MAXU][FK_MAXD];   // per term i: transformed terms first (i < ntr), then direct ones
+    u8 dig[FK_MAXU][FK_MAXD];     // key digit j of term i
+    u8 ntr[FK_MAXU];              // number of transformed terms of limb u (<= the launch's NTR)
+    u16 yslot[FK_MAXU];           // 0xffff, or: write INTT row pass of acc_p to y slot p * ystride + yslot
 };
 
 struct FusedKipArgs {
@@ -119,10 +123,26 @@ struct FusedKipArgs {
     const PrimeConst *pc;
     const ulonglong2 *tw;   // forward row twiddles [nprimes][R][C]
     u32 log_n, log_r, log_c, tiles, nu, ndig, nkey, acc_stride;
+    u32 ntr;                // thread groups = max transformed terms over the launch
+    u64 *y;                 // ModDown input buffer (y mode): first inverse-NTT pass of acc's P limbs
+    const ulonglong2 *tw_inv;   // inverse row twiddles [nprimes][R][C]
+    u32 ystride;
     FusedKipMap map;
 };
 
 hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s);
+
+// One output limb of the fused row pass + key product: its prime, key slot, acc slot, and per digit j
+// the source slot (ext pass-1 output, or FK_DIRECT | c1 slot for the own-digit limb).
+struct KipItem {
+    u16 prime, kslot, aslot;
+    u16 src[FK_MAXD];
+    u16 yslot = 0xffff;     // P limb whose acc goes straight into ModDown's inverse row pass
+};
+// Groups items by their number of transformed terms and launches k_ntt_kip per group.
+hks_status run_ntt_kip(const hks_ctx *ctx, const std::vector<KipItem> &items, u32 ndig, const u64 *ext,
+                       const u64 *c1, const u64 *evk, u64 *acc, u32 nkey, u32 acc_stride, cudaStream_t s,
+                       u64 *y = nullptr, u32 ystride = 0);
 
 // ----------------------------------------------------------------------------------------------
 struct hks_ctx {
@@ -196,6 +216,9 @@ struct LimbList {
 };
 hks_status run_ntt(const hks_ctx *ctx, NttDir dir, const LimbList &L, const u64 *in, u64 *out,
                    const ulonglong2 *scale, u32 scale_mod, cudaStream_t s);
+// second (column) pass of the inverse NTT only (the row pass was fused into k_ntt_kip)
+hks_status run_ntt_inv_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in, u64 *out, const ulonglong2 *scale,
+                            u32 scale_mod, cudaStream_t s);
 // first (column) pass of the forward NTT only; the row pass is fused elsewhere (launch_ntt_kip)
 hks_status run_ntt_fwd_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in, u64 *out, cudaStream_t s);
 hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 *out, const u64 *acc,

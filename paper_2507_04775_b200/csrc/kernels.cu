@@ -28,8 +28,8 @@ static bool getenv_fp_enabled() {
 // grid.z: chunk of BC_TCH targets.  LAZY: outputs in [0, 8t) for a consumer that accepts the lazy
 // range (the forward NTT); otherwise canonical.
 #define BC_TCH 10
-template <int NSRC, bool PRESCALE, bool LAZY>
-__global__ void __launch_bounds__(256) k_bconv(const __grid_constant__ BconvArgs A) {
+template <int NSRC, bool PRESCALE, bool LAZY, int CPT>
+__global__ void __launch_bounds__(256, CPT == 1 ? 5 : 3) k_bconv(const __grid_constant__ BconvArgs A) {
     const BconvGroup &G = A.g[blockIdx.y];
     const u32 u0 = blockIdx.z * BC_TCH;
     if (u0 >= G.ndst) return;
@@ -44,44 +44,50 @@ __global__ void __launch_bounds__(256) k_bconv(const __grid_constant__ BconvArgs
     __syncthreads();
 
     const size_t N = (size_t)1 << A.log_n;
-    const size_t x0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    const size_t x0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * CPT;
     if (x0 >= N) return;
-    u32 yl[NSRC][2], yh[NSRC][2];
+    u32 yl[NSRC][CPT], yh[NSRC][CPT];
 #pragma unroll
     for (int i = 0; i < NSRC; i++) {
-        const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(A.in + (size_t)G.src_slot[i] * N + x0);
-        u64 a = v.x, b = v.y;
-        if (PRESCALE) {
-            const u64 p = A.pc[G.src_prime[i]].p;
-            a = shoup(a, G.pre_w[i], G.pre_wp[i], p);
-            b = shoup(b, G.pre_w[i], G.pre_wp[i], p);
+        u64 v[CPT];
+        if (CPT == 2) {
+            const ulonglong2 t = *reinterpret_cast<const ulonglong2 *>(A.in + (size_t)G.src_slot[i] * N + x0);
+            v[0] = t.x;
+            v[CPT - 1] = t.y;
+        } else {
+            v[0] = A.in[(size_t)G.src_slot[i] * N + x0];
         }
-        split30(a, yl[i][0], yh[i][0]);
-        split30(b, yl[i][1], yh[i][1]);
+#pragma unroll
+        for (int c = 0; c < CPT; c++) {
+            if (PRESCALE) {
+                const u64 p = A.pc[G.src_prime[i]].p;
+                v[c] = shoup(v[c], G.pre_w[i], G.pre_wp[i], p);
+            }
+            split30(v[c], yl[i][c], yh[i][c]);
+        }
     }
     for (u32 u = 0; u < nt; u++) {
-        Acc30 a0, a1;
+        Acc30 a[CPT];
         {
             const uint2 m = smat[u];
-            acc_first(a0, yl[0][0], yh[0][0], m.x, m.y);
-            acc_first(a1, yl[0][1], yh[0][1], m.x, m.y);
+#pragma unroll
+            for (int c = 0; c < CPT; c++) acc_first(a[c], yl[0][c], yh[0][c], m.x, m.y);
         }
 #pragma unroll
         for (int i = 1; i < NSRC; i++) {
             const uint2 m = smat[i * BC_TCH + u];
-            acc_mac(a0, yl[i][0], yh[i][0], m.x, m.y);
-            acc_mac(a1, yl[i][1], yh[i][1], m.x, m.y);
+#pragma unroll
+            for (int c = 0; c < CPT; c++) acc_mac(a[c], yl[i][c], yh[i][c], m.x, m.y);
         }
         const PrimeConst pc = spc[u];
-        ulonglong2 o;
-        if (LAZY) {
-            o.x = acc_reduce_lazy(a0, pc);
-            o.y = acc_reduce_lazy(a1, pc);
-        } else {
-            o.x = acc_reduce(a0, pc);
-            o.y = acc_reduce(a1, pc);
-        }
-        *reinterpret_cast<ulonglong2 *>(A.out + (size_t)G.dst_slot[u0 + u] * N + x0) = o;
+        u64 o[CPT];
+#pragma unroll
+        for (int c = 0; c < CPT; c++) o[c] = LAZY ? acc_reduce_lazy(a[c], pc) : acc_reduce(a[c], pc);
+        u64 *dst = A.out + (size_t)G.dst_slot[u0 + u] * N + x0;
+        if (CPT == 2)
+            *reinterpret_cast<ulonglong2 *>(dst) = make_ulonglong2(o[0], o[CPT - 1]);
+        else
+            dst[0] = o[0];
     }
 }
 
@@ -177,20 +183,24 @@ static void bconv_fp_go(const BconvArgs &a, cudaStream_t s) {
     ps.done(words * (double)N * 8.0, macs * (double)N * 4.0);
 }
 
+#ifndef HKS_BCONV_CPT
+#define HKS_BCONV_CPT 1
+#endif
 template <int NSRC>
 static void bconv_go(const BconvArgs &a, cudaStream_t s) {
+    constexpr int CPT = HKS_BCONV_CPT;   // coefficients per thread
     const u32 threads = 256;
     const size_t N = (size_t)1 << a.log_n;
     u32 maxdst = 0;
     for (u32 g = 0; g < a.ngroups; g++) maxdst = max(maxdst, a.g[g].ndst);
-    dim3 grid((u32)((N / 2 + threads - 1) / threads), a.ngroups, (maxdst + BC_TCH - 1) / BC_TCH);
+    dim3 grid((u32)((N / CPT + threads - 1) / threads), a.ngroups, (maxdst + BC_TCH - 1) / BC_TCH);
     ProfScope ps(K_BCONV, s);
     if (a.prescale)
-        k_bconv<NSRC, true, false><<<grid, threads, 0, s>>>(a);
+        k_bconv<NSRC, true, false, CPT><<<grid, threads, 0, s>>>(a);
     else if (a.lazy_out)
-        k_bconv<NSRC, false, true><<<grid, threads, 0, s>>>(a);
+        k_bconv<NSRC, false, true, CPT><<<grid, threads, 0, s>>>(a);
     else
-        k_bconv<NSRC, false, false><<<grid, threads, 0, s>>>(a);
+        k_bconv<NSRC, false, false, CPT><<<grid, threads, 0, s>>>(a);
     double words = 0, macs = 0;
     for (u32 g = 0; g < a.ngroups; g++) {
         words += a.g[g].nsrc + a.g[g].ndst;

@@ -136,19 +136,11 @@ HKS_DEV void accf_add128(const AccF &A, u64 &lo, u64 &hi) {
 }
 
 // canonical X mod p for the accumulated 128-bit value (< 2^124, i.e. <= 16 terms of 60x60 bits).
-HKS_DEV u64 acc_reduce(const Acc30 &a, const PrimeConst &c) {
-    // lo/hi of s0 + (s1a << 30) + (s1b << 30) + (s2 << 60)
-    u64 lo = a.s0, hi = 0, t;
-    t = a.s1a << 30; lo += t; hi += (lo < t); hi += a.s1a >> 34;
-    t = a.s1b << 30; lo += t; hi += (lo < t); hi += a.s1b >> 34;
-    t = a.s2 << 60;  lo += t; hi += (lo < t); hi += a.s2 >> 4;
-    u64 r = shoup_lazy(hi, c.r64, c.r64p, c.p) + (lo - mulhi64(lo, c.one_p) * c.p);   // [0, 4p)
-    r = csub(r, 2 * c.p);
-    return csub(r, c.p);
-}
+// (Defined after shoup_approx below.)
+HKS_DEV u64 acc_reduce(const Acc30 &a, const PrimeConst &c);
 
-// X mod p in [0, 8p) for the accumulated 128-bit value, with two approximate-quotient Shoup steps:
-// X = hi 2^64 + lo, X = hi (2^64 mod p) + lo (mod p).  (Defined after shoup_approx below.)
+// X = hi 2^64 + lo (hi < 2^62) reduced to [0, 8p) with two approximate-quotient Shoup steps.
+// (Defined after shoup_approx below.)
 HKS_DEV u64 acc_reduce_lazy(const Acc30 &a, const PrimeConst &c);
 
 // Per-prime constants of the lazy butterflies.
@@ -281,23 +273,36 @@ HKS_DEV u32 automorph_src(u32 j, u32 log_n, u64 galois) {
     return brev_bits((e - 1u) >> 1, log_n);
 }
 
-HKS_DEV u64 acc_reduce_lazy(const Acc30 &a, const PrimeConst &c) {
-    u64 lo = a.s0, hi = 0, t;
-    t = a.s1a << 30; lo += t; hi += (lo < t); hi += a.s1a >> 34;
-    t = a.s1b << 30; lo += t; hi += (lo < t); hi += a.s1b >> 34;
-    t = a.s2 << 60;  lo += t; hi += (lo < t); hi += a.s2 >> 4;
-    const u64 np = 0 - c.p;
-    return shoup_approx(hi, c.r64, c.r64p, np) + shoup_approx(lo, 1, c.one_p, np);   // [0, 8p)
+
+// lo mod p in [0, 4p) for p > 2^32: one_p = floor(2^64/p) < 2^32, so the quotient estimate is one
+// 32x32 high product of lo's high word (short by at most 3), and lo - q p needs one IMAD.WIDE + IMAD.
+HKS_DEV u64 mod64_lazy(u64 lo, const PrimeConst &c) {
+    if (c.one_p >> 32) return shoup_approx(lo, 1, c.one_p, 0 - c.p);   // p < 2^32: generic path
+    const u32 q = __umulhi((u32)(lo >> 32), (u32)c.one_p);
+    return lo + (u64)q * (0 - c.p);
 }
 
-// X = hi 2^64 + lo (hi < 2^62) reduced to [0, 8p) with two approximate-quotient Shoup steps.
+// X = hi 2^64 + lo (hi < 2^62) reduced to [0, 8p): hi (2^64 mod p) by an approximate Shoup step,
+// lo by mod64_lazy.
 HKS_DEV u64 reduce128_lazy(u64 lo, u64 hi, const PrimeConst &c) {
-    const u64 np = 0 - c.p;
-    return shoup_approx(hi, c.r64, c.r64p, np) + shoup_approx(lo, 1, c.one_p, np);
+    return shoup_approx(hi, c.r64, c.r64p, 0 - c.p) + mod64_lazy(lo, c);
 }
 
 HKS_DEV u64 reduce128(u64 lo, u64 hi, const PrimeConst &c) {
-    u64 r = shoup_lazy(hi, c.r64, c.r64p, c.p) + (lo - mulhi64(lo, c.one_p) * c.p);   // [0, 4p)
+    u64 r = reduce128_lazy(lo, hi, c);   // [0, 8p)
+    r = csub(r, 4 * c.p);
     r = csub(r, 2 * c.p);
     return csub(r, c.p);
+}
+
+HKS_DEV u64 acc_reduce_lazy(const Acc30 &a, const PrimeConst &c) {
+    u64 lo, hi;
+    acc_to128(a, lo, hi);
+    return reduce128_lazy(lo, hi, c);
+}
+
+HKS_DEV u64 acc_reduce(const Acc30 &a, const PrimeConst &c) {
+    u64 lo, hi;
+    acc_to128(a, lo, hi);
+    return reduce128(lo, hi, c);
 }

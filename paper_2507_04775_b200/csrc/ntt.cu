@@ -18,6 +18,8 @@
 //     RTX 4090 trade-off), because on B200 the integer pipe, not L2, is scarce.
 //   * Butterflies are Harvey-lazy: forward values live in [0, 4p), inverse in [0, 2p); the last
 //     pass canonicalises and applies the fused epilogue (SCALE, MODDOWN; §3.6.5).
+#include <algorithm>
+
 #include "internal.h"
 
 // One pass over a limb batch.  LOGN = log2 of the sub-transform length n; LOGE = log2 of the
@@ -147,7 +149,12 @@ k_ntt(const __grid_constant__ NttArgs A) {
 #pragma unroll
                 for (int k = 0; k < Ee; k++) {
                     if (k & t) continue;
+#ifdef HKS_EXPERIMENT_CONST_TW
+                    const ulonglong2 w = make_ulonglong2(m.p - 3 - k, 0x123456789abcull + l);   // timing-only experiment
+                    (void)twb;
+#else
                     const ulonglong2 w = __ldg(twb + ((k << lstride) >> sh));
+#endif
                     if (FWD)
                         ct_lazy(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, m);
                     else
@@ -345,6 +352,23 @@ hks_status run_ntt_fwd_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in
     return HKS_OK;
 }
 
+hks_status run_ntt_inv_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in, u64 *out, const ulonglong2 *scale,
+                            u32 scale_mod, cudaStream_t s) {
+    if (L.size() > HKS_MAXB) HKS_FAIL(HKS_EINVAL, "ntt: scaled batch larger than one launch");
+    NttArgs a{};
+    a.pc = ctx->d_pc;
+    a.ninv = ctx->d_ninv;
+    a.galois = 1;
+    a.nsplit = 0xffffffffu;
+    fill_map(a, L, 0, (u32)L.size(), false);
+    a.in = in;
+    a.out = out;
+    a.tw = ctx->d_tw_col_inv;
+    a.scale = scale;
+    a.scale_mod = scale_mod ? scale_mod : 1;
+    return launch_ntt_pass(ctx, NTT_INV, 1, EPI_SCALE, a, s);
+}
+
 hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 *out, const u64 *acc,
                            const u64 *c0, u64 galois, cudaStream_t s, u32 nsplit, u64 *out_b, const u64 *eb_b) {
     if (nsplit != 0xffffffffu && L.size() > HKS_MAXB) HKS_FAIL(HKS_EINVAL, "moddown: merged batch too large");
@@ -390,16 +414,16 @@ hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 
 // (lazy values).  Phase 2: coalesced sweep over the tile, two coefficients per thread:
 // acc_p = sum_j canon(D_j) * evk_j[p] with the 30-bit-split IMAD.WIDE accumulation (one reduction
 // per output).  D never returns to HBM.
-template <int LOGN, int LOGE, int LOGNB, int NDIG>
-__global__ void __launch_bounds__(NDIG * ((1 << LOGNB) << (LOGN - LOGE)),
-                                  (NDIG * ((1 << LOGNB) << (LOGN - LOGE))) >= 384 ? 2 : 3)
+template <int LOGN, int LOGE, int LOGNB, int NTR, int NDIG>
+__global__ void __launch_bounds__(NTR * ((1 << LOGNB) << (LOGN - LOGE)),
+                                  (NTR * ((1 << LOGNB) << (LOGN - LOGE))) >= 384 ? 2 : 3)
 k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
     constexpr int n = 1 << LOGN;
     constexpr int E = 1 << LOGE;
     constexpr int NB = 1 << LOGNB;
     constexpr int TPS = n >> LOGE;
-    constexpr int NTG = NB * TPS;                      // threads per digit group
-    constexpr int NT = NDIG * NTG;                     // threads per CTA
+    constexpr int NTG = NB * TPS;                      // threads per term group
+    constexpr int NT = NTR * NTG;                      // threads per CTA
     constexpr int NR = (LOGN + LOGE - 1) / LOGE;
     constexpr int ROWPAD = n + (n >> LOGE);
     constexpr int BUF = NB * ROWPAD;
@@ -414,16 +438,15 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
     const int tid = threadIdx.x;
     const size_t tbase = (size_t)tile * NB * n;
 
-    // phase 1: thread group j runs the row pass of digit j into shared buffer j (concurrently)
+    // phase 1: thread group i runs the row pass of term i (< NTR) into shared buffer i, concurrently
     {
-        const int j = tid / NTG, gt = tid - j * NTG;
+        const int i = tid / NTG, gt = tid - i * NTG;
         const int bsub = gt >> (LOGN - LOGE);
         const int tu = gt & (TPS - 1);
-        const u16 ds = A.map.dsrc[u][j];
-        const bool work = !(ds & FK_DIRECT);
         const ulonglong2 *__restrict__ tw = A.tw + (((size_t)prime << A.log_r) + tile * NB + bsub) * n;
-        u64 *smj = sm + j * BUF + bsub * ROWPAD;
-        const u64 *__restrict__ src = A.ext + (size_t)(ds & 0x7fff) * N + tbase + (size_t)bsub * n;
+        u64 *smj = sm + i * BUF + bsub * ROWPAD;
+        const bool work = i < (int)A.map.ntr[u];                   // warp-uniform (groups are whole warps)
+        const u64 *__restrict__ src = A.ext + (size_t)(A.map.dsrc[u][i] & 0x7fff) * N + tbase + (size_t)bsub * n;
         u64 v[E];
 #pragma unroll
         for (int rr = 0; rr < NR; rr++) {
@@ -436,34 +459,128 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
             if (rr > 0) __syncthreads();
             if (work) {
 #pragma unroll
-                for (int q = 0; q < UPT; q++) {
-                    const int uid = tu * UPT + q;
-                    const int base = ((uid >> lstride) << lBsz) + (uid & ((1 << lstride) - 1));
+            for (int q = 0; q < UPT; q++) {
+                const int uid = tu * UPT + q;
+                const int base = ((uid >> lstride) << lBsz) + (uid & ((1 << lstride) - 1));
+#pragma unroll
+                for (int k = 0; k < Ee; k++) {
+                    const int jj = base + (k << lstride);
+                    v[q * Ee + k] = rr == 0 ? src[jj] : smj[jj + (jj >> LOGE)];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < UPT; q++) {
+                const int uid = tu * UPT + q;
+                const int blk = uid >> lstride;
+#pragma unroll
+                for (int l = 0; l < e; l++) {
+                    const int lt = e - 1 - l;
+                    const int t = 1 << lt;
+                    const int sh = lt + lstride + 1;
+                    const ulonglong2 *twb = tw + (n >> sh) + (blk << (lBsz - sh));
 #pragma unroll
                     for (int k = 0; k < Ee; k++) {
-                        const int jj = base + (k << lstride);
-                        v[q * Ee + k] = rr == 0 ? src[jj] : smj[jj + (jj >> LOGE)];
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < UPT; q++) {
-                    const int uid = tu * UPT + q;
-                    const int blk = uid >> lstride;
-#pragma unroll
-                    for (int l = 0; l < e; l++) {
-                        const int lt = e - 1 - l;
-                        const int t = 1 << lt;
-                        const int sh = lt + lstride + 1;
-                        const ulonglong2 *twb = tw + (n >> sh) + (blk << (lBsz - sh));
-#pragma unroll
-                        for (int k = 0; k < Ee; k++) {
-                            if (k & t) continue;
-                            const ulonglong2 w = __ldg(twb + ((k << lstride) >> sh));
-                            ct_lazy(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, m);
-                        }
+                        if (k & t) continue;
+                        const ulonglong2 w = __ldg(twb + ((k << lstride) >> sh));
+                        ct_lazy(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, m);
                     }
                 }
             }
+            }
+            if (rr > 0) __syncthreads();
+            if (work)
+#pragma unroll
+            for (int q = 0; q < UPT; q++) {
+                const int uid = tu * UPT + q;
+                const int base = ((uid >> lstride) << lBsz) + (uid & ((1 << lstride) - 1));
+#pragma unroll
+                for (int k = 0; k < Ee; k++) {
+                    const int jj = base + (k << lstride);
+                    smj[jj + (jj >> LOGE)] = v[q * Ee + k];
+                }
+            }
+        }
+    }
+    __syncthreads();
+
+    // phase 2: acc_p = sum_i canon(D_i) * evk_{dig(i)}[p], two coefficients per thread per step; the
+    // loads of all terms are issued before the multiply-accumulates.
+    const size_t kst = (size_t)A.nkey * N;
+    const u64 *__restrict__ kbase = A.evk + (size_t)A.map.kslot[u] * N + tbase;
+    const u32 as = A.map.aslot[u];
+    const u32 ys = A.map.yslot[u];
+    const bool ymode = ys != 0xffff && NTR >= 2;      // uniform per CTA
+    for (int idx = 2 * tid; idx < NB * n; idx += 2 * NT) {
+        const int r = idx >> LOGN, k = idx & (n - 1);
+        ulonglong2 kb[NDIG], ka[NDIG], dv[NDIG];
+#pragma unroll
+        for (int i = 0; i < NDIG; i++) {
+            const u32 j = A.map.dig[u][i];
+            kb[i] = *reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j) * kst + idx);
+            ka[i] = *reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j + 1) * kst + idx);
+            if (i >= (int)A.map.ntr[u]) {
+                dv[i] = *reinterpret_cast<const ulonglong2 *>(A.c1 + (size_t)(A.map.dsrc[u][i] & 0x7fff) * N + tbase + idx);
+            } else {
+                const u64 *smj = sm + i * BUF + r * ROWPAD + k + (k >> LOGE);
+                dv[i].x = canon8(smj[0], m);
+                dv[i].y = canon8(smj[1], m);
+            }
+        }
+        Acc30 a0[2], a1[2];
+#pragma unroll
+        for (int i = 0; i < NDIG; i++) {
+            u32 dl, dh, ml, mh;
+            split30(dv[i].x, dl, dh);
+            split30(kb[i].x, ml, mh);
+            if (i == 0) acc_first(a0[0], dl, dh, ml, mh); else acc_mac(a0[0], dl, dh, ml, mh);
+            split30(ka[i].x, ml, mh);
+            if (i == 0) acc_first(a1[0], dl, dh, ml, mh); else acc_mac(a1[0], dl, dh, ml, mh);
+            split30(dv[i].y, dl, dh);
+            split30(kb[i].y, ml, mh);
+            if (i == 0) acc_first(a0[1], dl, dh, ml, mh); else acc_mac(a0[1], dl, dh, ml, mh);
+            split30(ka[i].y, ml, mh);
+            if (i == 0) acc_first(a1[1], dl, dh, ml, mh); else acc_mac(a1[1], dl, dh, ml, mh);
+        }
+        ulonglong2 o0, o1;
+        o0.x = acc_reduce(a0[0], pc);
+        o0.y = acc_reduce(a0[1], pc);
+        o1.x = acc_reduce(a1[0], pc);
+        o1.y = acc_reduce(a1[1], pc);
+        if (ymode) {
+            // each thread overwrites only the positions it read its D values from: no race
+            u64 *s0 = sm + r * ROWPAD + k + (k >> LOGE);
+            s0[0] = o0.x;
+            s0[1] = o0.y;
+            s0[BUF] = o1.x;
+            s0[BUF + 1] = o1.y;
+        } else {
+            *reinterpret_cast<ulonglong2 *>(A.acc + (size_t)as * N + tbase + idx) = o0;
+            *reinterpret_cast<ulonglong2 *>(A.acc + ((size_t)A.acc_stride + as) * N + tbase + idx) = o1;
+        }
+    }
+    if (!ymode) return;
+
+    // phase 3 (P limbs): ModDown's first inverse-NTT pass (Gentleman-Sande row stages) on acc_0 / acc_1,
+    // thread groups 0 and 1, written to y; the column pass follows in run_ntt_inv_cols.
+    __syncthreads();
+    {
+        const int g = tid / NTG, gt = tid - g * NTG;
+        const bool work = g < 2;
+        const int bsub = gt >> (LOGN - LOGE);
+        const int tu = gt & (TPS - 1);
+        const ulonglong2 *__restrict__ tw = A.tw_inv + (((size_t)prime << A.log_r) + tile * NB + bsub) * n;
+        u64 *smj = sm + (work ? g : 0) * BUF + bsub * ROWPAD;
+        u64 *__restrict__ dst = A.y + ((size_t)(work ? g : 0) * A.ystride + ys) * N + tbase + (size_t)bsub * n;
+        u64 v[E];
+#pragma unroll
+        for (int rr = 0; rr < NR; rr++) {
+            const int s0 = rr * LOGE;
+            const int e = (LOGN - s0) < LOGE ? (LOGN - s0) : LOGE;
+            const int Ee = 1 << e;
+            const int UPT = E >> e;
+            const int lstride = s0;
+            const int lBsz = lstride + e;
+            const bool last = rr == NR - 1;
             if (rr > 0) __syncthreads();
             if (work) {
 #pragma unroll
@@ -473,62 +590,59 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
 #pragma unroll
                     for (int k = 0; k < Ee; k++) {
                         const int jj = base + (k << lstride);
-                        smj[jj + (jj >> LOGE)] = v[q * Ee + k];
+                        v[q * Ee + k] = smj[jj + (jj >> LOGE)];
                     }
+                }
+#pragma unroll
+                for (int q = 0; q < UPT; q++) {
+                    const int uid = tu * UPT + q;
+                    const int blk = uid >> lstride;
+#pragma unroll
+                    for (int l = 0; l < e; l++) {
+                        const int t = 1 << l;
+                        const int sh = l + lstride + 1;
+                        const ulonglong2 *twb = tw + (n >> sh) + (blk << (lBsz - sh));
+#pragma unroll
+                        for (int k = 0; k < Ee; k++) {
+                            if (k & t) continue;
+                            const ulonglong2 w = __ldg(twb + ((k << lstride) >> sh));
+                            gs_lazy(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, m);
+                        }
+                    }
+                }
+            }
+            if (!last) {
+                __syncthreads();
+                if (work) {
+#pragma unroll
+                    for (int q = 0; q < UPT; q++) {
+                        const int uid = tu * UPT + q;
+                        const int base = ((uid >> lstride) << lBsz) + (uid & ((1 << lstride) - 1));
+#pragma unroll
+                        for (int k = 0; k < Ee; k++) {
+                            const int jj = base + (k << lstride);
+                            smj[jj + (jj >> LOGE)] = v[q * Ee + k];
+                        }
+                    }
+                }
+            } else if (work) {
+#pragma unroll
+                for (int q = 0; q < UPT; q++) {
+                    const int uid = tu * UPT + q;
+                    const int base = ((uid >> lstride) << lBsz) + (uid & ((1 << lstride) - 1));
+#pragma unroll
+                    for (int k = 0; k < Ee; k++) dst[base + (k << lstride)] = v[q * Ee + k];
                 }
             }
         }
     }
-    __syncthreads();
-
-    // phase 2: acc_p = sum_j canon(D_j) * evk_j[p], two coefficients per thread per step; the loads
-    // of all digits are issued before the multiply-accumulates.
-    const size_t kst = (size_t)A.nkey * N;
-    const u64 *__restrict__ kbase = A.evk + (size_t)A.map.kslot[u] * N + tbase;
-    const u32 as = A.map.aslot[u];
-    for (int idx = 2 * tid; idx < NB * n; idx += 2 * NT) {
-        const int r = idx >> LOGN, k = idx & (n - 1);
-        ulonglong2 kb[NDIG], ka[NDIG], dv[NDIG];
-#pragma unroll
-        for (int j = 0; j < NDIG; j++) {
-            kb[j] = *reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j) * kst + idx);
-            ka[j] = *reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j + 1) * kst + idx);
-            const u16 ds = A.map.dsrc[u][j];
-            if (ds & FK_DIRECT) {
-                dv[j] = *reinterpret_cast<const ulonglong2 *>(A.c1 + (size_t)(ds & 0x7fff) * N + tbase + idx);
-            } else {
-                const u64 *smj = sm + j * BUF + r * ROWPAD + k + (k >> LOGE);
-                dv[j].x = canon8(smj[0], m);
-                dv[j].y = canon8(smj[1], m);
-            }
-        }
-        Acc30 a0[2], a1[2];
-        acc_zero(a0[0]); acc_zero(a0[1]); acc_zero(a1[0]); acc_zero(a1[1]);
-#pragma unroll
-        for (int j = 0; j < NDIG; j++) {
-            u32 dl, dh, ml, mh;
-            split30(dv[j].x, dl, dh);
-            split30(kb[j].x, ml, mh); acc_mac(a0[0], dl, dh, ml, mh);
-            split30(ka[j].x, ml, mh); acc_mac(a1[0], dl, dh, ml, mh);
-            split30(dv[j].y, dl, dh);
-            split30(kb[j].y, ml, mh); acc_mac(a0[1], dl, dh, ml, mh);
-            split30(ka[j].y, ml, mh); acc_mac(a1[1], dl, dh, ml, mh);
-        }
-        ulonglong2 o0, o1;
-        o0.x = acc_reduce(a0[0], pc);
-        o0.y = acc_reduce(a0[1], pc);
-        o1.x = acc_reduce(a1[0], pc);
-        o1.y = acc_reduce(a1[1], pc);
-        *reinterpret_cast<ulonglong2 *>(A.acc + (size_t)as * N + tbase + idx) = o0;
-        *reinterpret_cast<ulonglong2 *>(A.acc + ((size_t)A.acc_stride + as) * N + tbase + idx) = o1;
-    }
 }
 
-template <int LOGN, int LOGE, int LOGNB, int NDIG>
+template <int LOGN, int LOGE, int LOGNB, int NTR, int NDIG>
 static hks_status go_kip(FusedKipArgs &a, cudaStream_t s) {
-    constexpr int threads = NDIG * ((1 << LOGNB) << (LOGN - LOGE));
-    constexpr size_t smem = (size_t)NDIG * ((1 << LOGN) + ((1 << LOGN) >> LOGE)) * (1 << LOGNB) * sizeof(u64);
-    auto kern = k_ntt_kip<LOGN, LOGE, LOGNB, NDIG>;
+    constexpr int threads = NTR * ((1 << LOGNB) << (LOGN - LOGE));
+    constexpr size_t smem = (size_t)NTR * ((1 << LOGN) + ((1 << LOGN) >> LOGE)) * (1 << LOGNB) * sizeof(u64);
+    auto kern = k_ntt_kip<LOGN, LOGE, LOGNB, NTR, NDIG>;
     if (smem > 48 * 1024) {
         static bool once = [&] {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -540,36 +654,36 @@ static hks_status go_kip(FusedKipArgs &a, cudaStream_t s) {
     ProfScope ps(K_NTT_ROWS_KIP, s);
     kern<<<a.nu * a.tiles, threads, smem, s>>>(a);
     HKS_CHECK_LAUNCH();
-    u32 nntt = 0, ndirect = 0;
-    for (u32 u = 0; u < a.nu; u++)
-        for (u32 j = 0; j < a.ndig; j++) (a.map.dsrc[u][j] & FK_DIRECT) ? ndirect++ : nntt++;
     // algorithmic words: D read once (pass-1 output or c1), key 2 limbs per (u, j), acc 2 limbs per u
     const double nn = (double)(1ull << a.log_n);
-    const double muls = nntt * (nn / 2.0) * a.log_c * 7.0 + (double)a.nu * a.ndig * 2.0 * nn * 4.0;
-    ps.done(((double)nntt + ndirect + 2.0 * a.nu * a.ndig + 2.0 * a.nu) * nn * 8.0, muls);
+    double nntt = 0;
+    for (u32 u = 0; u < a.nu; u++) nntt += a.map.ntr[u];
+    const double ndirect = (double)a.nu * NDIG - nntt;
+    double ny = 0;
+    for (u32 u = 0; u < a.nu; u++) ny += (a.y && a.map.yslot[u] != 0xffff) ? 2.0 : 0.0;
+    const double muls = (nntt + ny) * (nn / 2.0) * a.log_c * 7.0 + (double)a.nu * NDIG * 2.0 * nn * 4.0;
+    ps.done((nntt + ndirect + 2.0 * a.nu * NDIG + 2.0 * a.nu) * nn * 8.0, muls);
     return HKS_OK;
 }
 
 template <int LOGN, int LOGE, int LOGNB>
 static hks_status go_kip_d(FusedKipArgs &a, cudaStream_t s) {
-    switch (a.ndig) {
-        case 1: return go_kip<LOGN, LOGE, LOGNB, 1>(a, s);
-        case 2: return go_kip<LOGN, LOGE, LOGNB, 2>(a, s);
-        case 3: return go_kip<LOGN, LOGE, LOGNB, 3>(a, s);
-        case 4: return go_kip<LOGN, LOGE, LOGNB, 4>(a, s);
-        default: break;
-    }
-    HKS_FAIL(HKS_EINVAL, "ntt_kip: %u digits", a.ndig);
+#define KC(T, D) if (a.ntr == T && a.ndig == D) return go_kip<LOGN, LOGE, LOGNB, T, D>(a, s);
+    KC(1, 1) KC(1, 2) KC(2, 2) KC(2, 3) KC(3, 3) KC(3, 4) KC(4, 4)
+#undef KC
+    if (a.ntr == 0) { a.ntr = 1; return go_kip_d<LOGN, LOGE, LOGNB>(a, s); }   // all-direct launch
+    HKS_FAIL(HKS_EINVAL, "ntt_kip: %u transformed of %u digits", a.ntr, a.ndig);
 }
 
 hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s) {
     a.log_n = ctx->log_n;
     a.log_r = ctx->log_r;
     a.log_c = ctx->log_c;
-    if (a.ndig > FK_MAXD || a.nu > FK_MAXU) HKS_FAIL(HKS_EINVAL, "ntt_kip: %u digits / %u limbs per launch", a.ndig, a.nu);
+    if (a.ndig > FK_MAXD || a.nu > FK_MAXU || a.ntr > a.ndig)
+        HKS_FAIL(HKS_EINVAL, "ntt_kip: %u digits (%u transformed) / %u limbs per launch", a.ndig, a.ntr, a.nu);
     switch (ctx->log_n) {
-        case 17: return a.ndig > 3 ? go_kip_d<8, 4, 2>(a, s) : go_kip_d<8, 4, 3>(a, s);
-        case 16: return a.ndig > 3 ? go_kip_d<8, 4, 2>(a, s) : go_kip_d<8, 4, 3>(a, s);
+        case 17: return a.ntr > 3 ? go_kip_d<8, 4, 2>(a, s) : go_kip_d<8, 4, 3>(a, s);
+        case 16: return a.ntr > 3 ? go_kip_d<8, 4, 2>(a, s) : go_kip_d<8, 4, 3>(a, s);
         case 15: return go_kip_d<7, 4, 3>(a, s);
         case 14: return go_kip_d<7, 4, 3>(a, s);
         case 13: return go_kip_d<6, 3, 3>(a, s);
@@ -579,4 +693,48 @@ hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s) {
         default: break;
     }
     HKS_FAIL(HKS_EINVAL, "ntt_kip: unsupported log_n %u", ctx->log_n);
+}
+
+hks_status run_ntt_kip(const hks_ctx *ctx, const std::vector<KipItem> &items, u32 ndig, const u64 *ext,
+                       const u64 *c1, const u64 *evk, u64 *acc, u32 nkey, u32 acc_stride, cudaStream_t s,
+                       u64 *y, u32 ystride) {
+    for (size_t u0 = 0; u0 < items.size(); u0 += FK_MAXU) {
+        FusedKipArgs a{};
+        a.ext = ext;
+        a.c1 = c1;
+        a.evk = evk;
+        a.acc = acc;
+        a.pc = ctx->d_pc;
+        a.tw = ctx->d_tw_row_fwd;
+        a.nu = (u32)std::min<size_t>(FK_MAXU, items.size() - u0);
+        a.ndig = ndig;
+        a.ntr = 0;
+        a.nkey = nkey;
+        a.acc_stride = acc_stride;
+        a.y = y;
+        a.ystride = ystride;
+        a.tw_inv = ctx->d_tw_row_inv;
+        for (u32 uu = 0; uu < a.nu; uu++) {
+            const KipItem &it = items[u0 + uu];
+            a.map.prime[uu] = it.prime;
+            a.map.kslot[uu] = it.kslot;
+            a.map.aslot[uu] = it.aslot;
+            a.map.yslot[uu] = y ? it.yslot : (u16)0xffff;
+            u32 i = 0, ntr = 0;
+            for (u32 pass = 0; pass < 2; pass++)          // transformed terms first, then direct
+                for (u32 j = 0; j < ndig; j++) {
+                    const bool direct = (it.src[j] & FK_DIRECT) != 0;
+                    if (direct != (pass == 1)) continue;
+                    a.map.dsrc[uu][i] = it.src[j];
+                    a.map.dig[uu][i] = (u8)j;
+                    i++;
+                    ntr += direct ? 0 : 1;
+                }
+            a.map.ntr[uu] = (u8)ntr;
+            a.ntr = std::max(a.ntr, ntr);
+        }
+        hks_status st = launch_ntt_kip(ctx, a, s);
+        if (st != HKS_OK) return st;
+    }
+    return HKS_OK;
 }

@@ -186,30 +186,19 @@ extern "C" hks_status hks_shard_ks_inner(const hks_ctx *c, uint32_t level, uint3
     }
     if ((st = bconv_groups(c, groups, yall, ext, s)) != HKS_OK) return st;
     if (T.size() && (st = run_ntt_fwd_cols(c, T, ext, ext, s)) != HKS_OK) return st;
-    for (u32 u0 = 0; u0 < own_t.size(); u0 += FK_MAXU) {
-        FusedKipArgs a{};
-        a.ext = ext;
-        a.c1 = c1_loc;
-        a.evk = evk_loc;
-        a.acc = acc_loc;
-        a.pc = c->d_pc;
-        a.tw = c->d_tw_row_fwd;
-        a.nu = std::min<u32>(FK_MAXU, (u32)own_t.size() - u0);
-        a.ndig = beta;
-        a.nkey = P.nkey;
-        a.acc_stride = P.n_own;
-        for (u32 uu = 0; uu < a.nu; uu++) {
-            const u32 u = u0 + uu, t = own_t[u];
-            a.map.prime[uu] = (u16)c->ext_prime(level, t);
-            a.map.kslot[uu] = (u16)(t <= level ? t - P.q_lo : (P.q_hi - P.q_lo) + (t - level - 1 - P.p_lo));
-            a.map.aslot[uu] = (u16)u;
-            for (u32 j = 0; j < beta; j++) {
-                const bool own = t <= level && t >= c->digit_lo(j) && t < c->digit_hi(level, j);
-                a.map.dsrc[uu][j] = own ? (u16)(FK_DIRECT | (t - P.q_lo)) : (u16)(j * P.n_own + u);
-            }
+    std::vector<KipItem> items(own_t.size());
+    for (u32 u = 0; u < own_t.size(); u++) {
+        const u32 t = own_t[u];
+        KipItem &it = items[u];
+        it.prime = (u16)c->ext_prime(level, t);
+        it.kslot = (u16)(t <= level ? t - P.q_lo : (P.q_hi - P.q_lo) + (t - level - 1 - P.p_lo));
+        it.aslot = (u16)u;
+        for (u32 j = 0; j < beta; j++) {
+            const bool own = t <= level && t >= c->digit_lo(j) && t < c->digit_hi(level, j);
+            it.src[j] = own ? (u16)(FK_DIRECT | (t - P.q_lo)) : (u16)(j * P.n_own + u);
         }
-        if ((st = launch_ntt_kip(c, a, s)) != HKS_OK) return st;
     }
+    if ((st = run_ntt_kip(c, items, beta, ext, c1_loc, evk_loc, acc_loc, P.nkey, P.n_own, s)) != HKS_OK) return st;
     if (P.np_own) {
         LimbList L;
         for (u32 p = 0; p < 2; p++)

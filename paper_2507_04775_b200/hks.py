@@ -10,7 +10,7 @@ import os
 from typing import Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhks.so")
+LIB_PATH = os.environ.get("HKS_LIB_PATH") or os.path.join(_HERE, "libhks.so")   # override: experiments only
 
 HKS_OK = 0
 STATUS = {0: "HKS_OK", 1: "HKS_EINVAL", 2: "HKS_ENOTPRIME", 3: "HKS_ENOTNTT", 4: "HKS_ERANGE", 5: "HKS_EDUP",

@@ -60,7 +60,7 @@ def summarise_rep(rep, name, config):
         u = units[hdr.index("dram__bytes_read.sum")]
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         tu = units[hdr.index("gpu__time_duration.sum")]
-        tscale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(tu, 1.0)
+        tscale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(tu, 1.0)
         t_us = metric(row, hdr, "gpu__time_duration.sum") * tscale
         stalls = sorted(((metric(row, hdr, h), h.replace("smsp__average_warps_issue_stalled_", "")
                           .replace("_per_issue_active.ratio", "")) for h in stall_keys), reverse=True)[:3]
@@ -114,7 +114,7 @@ def summarise_launches(path, name):
             continue
         unit = r[hdr.index("Metric Unit")]
         v = float(r[hdr.index("Metric Value")].replace(",", ""))
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0)
         cls = kernel_class(r[hdr.index("Kernel Name")].replace("void ", ""))
         agg[cls][0] += 1
         agg[cls][1] += v
