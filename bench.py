@@ -315,14 +315,18 @@ class C3Workload:
         shape = cts[0]["c0"].shape
         self.out0 = [[torch.empty(shape, dtype=torch.int64, device=dev) for _ in range(self.nrot)] for _ in range(self.nct)]
         self.out1 = [[torch.empty(shape, dtype=torch.int64, device=dev) for _ in range(self.nrot)] for _ in range(self.nct)]
-        self.ws = ctx.workspace(H.OP_ROTATE_HOISTED, level, self.nrot)
+        self.ws = H.rotate_hoisted_batch_workspace(ctx, self.nct, level)
         self.units = self.nct * self.nrot
+        self.c0s = [c[0] for c in self.cts]
+        self.c1s = [c[1] for c in self.cts]
+        self.flat0 = [o for c in range(self.nct) for o in self.out0[c]]
+        self.flat1 = [o for c in range(self.nct) for o in self.out1[c]]
 
     def step(self, i):
-        for c in range(self.nct):
-            c0, c1 = self.cts[c]
-            self.H.rotate_hoisted(self.ctx, c0, c1, self.level, self.galois, self.evks, self.out0[c], self.out1[c],
-                                  self.ws, self.sid)
+        # one hoisted ModUp per ciphertext; per rotation key one key product over all of the rank's
+        # ciphertexts (each key word loaded once) and one batched ModDown
+        self.H.rotate_hoisted_batch(self.ctx, self.c0s, self.c1s, self.level, self.galois, self.evks, self.flat0,
+                                    self.flat1, self.ws, self.sid)
 
     def alg_bytes(self):
         c, l = self.cfg, self.level

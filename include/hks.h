@@ -179,6 +179,16 @@ hks_status hks_rotate_hoisted(const hks_ctx *ctx, const uint64_t *c0, const uint
                               uint64_t *const *out0, uint64_t *const *out1, void *ws, void *stream);
 
 
+/* Hoisted rotations of nct <= 8 ciphertexts sharing the same nrot rotation keys (SURVEY.md §7 "key
+ * streaming": the key product loads every key word once for the whole batch).  c0[i], c1[i]:
+ * ciphertext i [l+1][N] EVAL; out0/out1[i * nrot + r] receive rotation r of ciphertext i (as in
+ * hks_rotate_hoisted).  beta(level) <= 4.  ws: hks_rotate_hoisted_batch_workspace_bytes(ctx, nct, level). */
+hks_status hks_rotate_hoisted_batch(const hks_ctx *ctx, uint32_t nct, const uint64_t *const *c0,
+                                    const uint64_t *const *c1, uint32_t level, uint32_t nrot,
+                                    const uint64_t *galois, const uint64_t *const *evk, uint64_t *const *out0,
+                                    uint64_t *const *out1, void *ws, void *stream);
+size_t hks_rotate_hoisted_batch_workspace_bytes(const hks_ctx *ctx, uint32_t nct, uint32_t level);
+
 /* ---- diagnostics (bench.py evidence; not part of the key-switching math) ---------------------
  * hks_launch_count: number of kernels this library has launched in this process (all contexts).
  * hks_prof_enable(1): from now on every kernel launch is bracketed by a CUDA event pair recorded on

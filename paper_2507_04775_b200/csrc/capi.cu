@@ -134,23 +134,24 @@ hks_status ntt_kip_core(const hks_ctx *c, const u64 *ext, const u64 *c1, const u
     return run_ntt_kip(c, items, beta, ext, c1, evk, acc, c->nq + c->np, ne, s, y, c->np);
 }
 
-// ModDown of npoly accumulators (acc poly p at slots p * ne + t) into out[p] (+ adds[p], read through
-// the automorphism `galois` for p = 0).  ws: y [npoly][K][N] then conv [npoly][l+1][N].
-hks_status moddown_core(const hks_ctx *c, const u64 *acc, u32 npoly, u32 level, u64 *const *outs, const u64 *c0,
-                        u64 galois, u64 *ws, cudaStream_t s, const u64 *c1add = nullptr, bool y_rows_done = false) {
+// ModDown of npoly accumulators (acc poly p at slots p * ne + t) into outs[p], + adds[p] read through
+// the automorphism gal[p].  ws: y [npoly][K][N] then conv [npoly][l+1][N].  y_rows_done: the inverse
+// row pass of the P limbs already ran inside k_ntt_kip (y holds it).
+hks_status moddown_core(const hks_ctx *c, const u64 *acc, u32 npoly, u32 level, u64 *const *outs,
+                        const u64 *const *adds, const u64 *gal, u64 *ws, cudaStream_t s, bool y_rows_done = false) {
     const u32 ne = c->ne(level), K = c->np;
     u64 *y = ws, *conv = ws + (size_t)npoly * K * c->n;
-    hks_status st;
-    if (y_rows_done) {          // the inverse row pass already ran inside k_ntt_kip (y holds it)
-        LimbList Y;
-        for (u32 p = 0; p < npoly; p++)
-            for (u32 k = 0; k < K; k++) Y.push(p * K + k, p * K + k, c->nq + k);
-        st = run_ntt_inv_cols(c, Y, y, y, c->d_md_scale, K, s);
-    } else {
+    hks_status st = HKS_OK;
+    // inverse NTT of the P limbs with N^-1 [phat_k]^-1 (one launch pair per HKS_MAXB limbs)
+    for (u32 p0 = 0; p0 < npoly && st == HKS_OK;) {
+        const u32 np = std::min<u32>(npoly - p0, HKS_MAXB / K);
         LimbList L;
-        for (u32 p = 0; p < npoly; p++)
-            for (u32 k = 0; k < K; k++) L.push(p * ne + level + 1 + k, p * K + k, c->nq + k);
-        st = run_ntt(c, NTT_INV, L, acc, y, c->d_md_scale, K, s);
+        for (u32 p = p0; p < p0 + np; p++)
+            for (u32 k = 0; k < K; k++)
+                L.push(y_rows_done ? p * K + k : p * ne + level + 1 + k, p * K + k, c->nq + k);
+        st = y_rows_done ? run_ntt_inv_cols(c, L, y, y, c->d_md_scale, K, s)
+                         : run_ntt(c, NTT_INV, L, acc, y, c->d_md_scale, K, s);
+        p0 += np;
     }
     if (st != HKS_OK) return st;
     std::vector<BconvGroup> groups;
@@ -165,26 +166,17 @@ hks_status moddown_core(const hks_ctx *c, const u64 *acc, u32 npoly, u32 level, 
     }
     st = run_bconv_groups(c, groups, y, conv, s);
     if (st != HKS_OK) return st;
-    // both polynomials in one pair of launches: limbs [0, l+1) -> outs[0] (+ c0 through `galois`),
-    // limbs [l+1, 2(l+1)) -> outs[1] (+ c1add)
     LimbList M;
+    std::vector<uint8_t> poly;
+    std::vector<MdOut> mo(npoly);
     for (u32 p = 0; p < npoly; p++) {
-        const u64 *add = p == 0 ? c0 : c1add;
-        for (u32 i = 0; i <= level; i++) M.push(p * (level + 1) + i, i, i, p * ne + i, add ? i : 0xffff);
-    }
-    if (npoly == 2 && M.size() <= HKS_MAXB) {
-        st = run_ntt_moddown(c, M, conv, outs[0], acc, c0, galois, s, level + 1, outs[1], c1add);
-        if (st != HKS_OK) return st;
-    } else {
-        for (u32 p = 0; p < npoly; p++) {
-            LimbList Mp;
-            const u64 *add = p == 0 ? c0 : c1add;
-            for (u32 i = 0; i <= level; i++) Mp.push(p * (level + 1) + i, i, i, p * ne + i, add ? i : 0xffff);
-            st = run_ntt_moddown(c, Mp, conv, outs[p], acc, add, p == 0 ? galois : 1, s);
-            if (st != HKS_OK) return st;
+        mo[p] = MdOut{outs[p], adds ? adds[p] : nullptr, gal ? gal[p] : 1};
+        for (u32 i = 0; i <= level; i++) {
+            M.push(p * (level + 1) + i, i, i, p * ne + i, mo[p].add ? i : 0xffff);
+            poly.push_back((uint8_t)p);
         }
     }
-    return HKS_OK;
+    return run_ntt_moddown(c, M, poly, mo, conv, acc, s);
 }
 
 hks_status kip_core(const hks_ctx *c, const u64 *ext, const u64 *c1, const u64 *evk, u32 level, u64 galois,
@@ -207,6 +199,13 @@ hks_status kip_core(const hks_ctx *c, const u64 *ext, const u64 *c1, const u64 *
     return launch_kip(a, s);
 }
 
+// rotations whose ModDowns are batched together: 2 RB polynomials must fit the 16-entry output
+// table of one ModDown epilogue launch and the K-limb INTT batches (HKS_MAXB limbs).
+size_t rot_batch(const hks_ctx *c, u32 level) {
+    (void)level;
+    return std::max<size_t>(1, std::min<size_t>(NTT_MAXO / 2, HKS_MAXB / (2 * c->np)));
+}
+
 hks_status check_galois(const hks_ctx *c, u64 g) {
     if ((g & 1) == 0 || g >= 2 * (u64)c->n) HKS_FAIL(HKS_EGALOIS, "galois element %llu must be odd and < 2N", (unsigned long long)g);
     return HKS_OK;
@@ -215,14 +214,16 @@ hks_status check_galois(const hks_ctx *c, u64 g) {
 }  // namespace
 
 extern "C" size_t hks_workspace_bytes(const hks_ctx *c, hks_op op, uint32_t level, uint32_t count) {
-    (void)count;
     if (!c || level > c->L()) return 0;
     const size_t lb = limb_bytes(c), l1 = level + 1, ne = c->ne(level), K = c->np, beta = c->beta(level);
     switch (op) {
         case HKS_OP_MODUP: return l1 * lb;
         case HKS_OP_MODDOWN: return (K + l1) * lb;
-        case HKS_OP_KEYSWITCH:
-        case HKS_OP_ROTATE_HOISTED: return (l1 + beta * ne + 2 * ne + 2 * K + 2 * l1) * lb;
+        case HKS_OP_KEYSWITCH: return (l1 + beta * ne + 2 * ne + 2 * K + 2 * l1) * lb;
+        case HKS_OP_ROTATE_HOISTED: {
+            const size_t rb = std::min<size_t>(count ? count : 1, rot_batch(c, level));
+            return (l1 + beta * ne + rb * (2 * ne + 2 * K + 2 * l1)) * lb;
+        }
     }
     return 0;
 }
@@ -376,7 +377,7 @@ extern "C" hks_status hks_moddown(const hks_ctx *c, const uint64_t *acc, uint32_
         HKS_FAIL(HKS_EINVAL, "moddown: buffers overlap");
     DevGuard g(c->device);
     u64 *outs[1] = {out};
-    return moddown_core(c, acc, 1, level, outs, nullptr, 1, (u64 *)ws, (cudaStream_t)stream);
+    return moddown_core(c, acc, 1, level, outs, nullptr, nullptr, (u64 *)ws, (cudaStream_t)stream);
 }
 
 static hks_status keyswitch_impl(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, const uint64_t *add1,
@@ -435,7 +436,8 @@ static hks_status keyswitch_impl(const hks_ctx *c, const uint64_t *c0, const uin
         if ((st = kip_core(c, ext, c1, evk, level, 1, acc, s)) != HKS_OK) return st;
     }
     u64 *outs[2] = {out0, out1};
-    return moddown_core(c, acc, 2, level, outs, c0, 1, md, s, add1, ymode);
+    const u64 *adds[2] = {c0, add1};
+    return moddown_core(c, acc, 2, level, outs, adds, nullptr, md, s, ymode);
 }
 
 extern "C" hks_status hks_automorph(const hks_ctx *c, const uint64_t *in, uint32_t nlimbs, uint64_t galois,
@@ -472,13 +474,99 @@ extern "C" hks_status hks_rotate_hoisted(const hks_ctx *c, const uint64_t *c0, c
     cudaStream_t s = (cudaStream_t)stream;
     u64 *coef = (u64 *)ws;
     u64 *ext = coef + l1 * c->n;
-    u64 *acc = ext + beta * ne * c->n;
-    u64 *md = acc + 2 * ne * c->n;
     if ((st = modup_core(c, c1, level, ext, coef, s)) != HKS_OK) return st;
-    for (u32 r = 0; r < nrot; r++) {
-        if ((st = kip_core(c, ext, c1, evk[r], level, galois[r], acc, s)) != HKS_OK) return st;
-        u64 *outs[2] = {out0[r], out1[r]};
-        if ((st = moddown_core(c, acc, 2, level, outs, c0, galois[r], md, s)) != HKS_OK) return st;
+    // rotations in groups of RB: RB key products (each with its automorphism gather) into RB
+    // accumulator pairs, then ONE ModDown over the 2 RB polynomials (large batches per launch)
+    const u32 RB = (u32)std::min<size_t>(nrot, rot_batch(c, level));
+    u64 *acc = ext + beta * ne * c->n;
+    u64 *md = acc + (size_t)RB * 2 * ne * c->n;
+    for (u32 r0 = 0; r0 < nrot; r0 += RB) {
+        const u32 nr = std::min(RB, nrot - r0);
+        std::vector<u64 *> outs(2 * nr);
+        std::vector<const u64 *> adds(2 * nr);
+        std::vector<u64> gal(2 * nr);
+        for (u32 r = 0; r < nr; r++) {
+            if ((st = kip_core(c, ext, c1, evk[r0 + r], level, galois[r0 + r], acc + (size_t)r * 2 * ne * c->n, s)) != HKS_OK)
+                return st;
+            outs[2 * r] = out0[r0 + r];
+            outs[2 * r + 1] = out1[r0 + r];
+            adds[2 * r] = c0;
+            adds[2 * r + 1] = nullptr;
+            gal[2 * r] = galois[r0 + r];
+            gal[2 * r + 1] = 1;
+        }
+        if ((st = moddown_core(c, acc, 2 * nr, level, outs.data(), adds.data(), gal.data(), md, s)) != HKS_OK) return st;
     }
     return HKS_OK;
+}
+
+extern "C" hks_status hks_rotate_hoisted_batch(const hks_ctx *c, uint32_t nct, const uint64_t *const *c0,
+                                               const uint64_t *const *c1, uint32_t level, uint32_t nrot,
+                                               const uint64_t *galois, const uint64_t *const *evk,
+                                               uint64_t *const *out0, uint64_t *const *out1, void *ws, void *stream) {
+    hks_status st = check_ctx(c);
+    if (st != HKS_OK) return st;
+    if (nct == 0 || nrot == 0) return HKS_OK;
+    if (!c0 || !c1 || !galois || !evk || !out0 || !out1 || !ws) HKS_FAIL(HKS_EINVAL, "rotate_hoisted_batch: NULL argument");
+    if (level > c->L()) HKS_FAIL(HKS_EINVAL, "rotate_hoisted_batch: level %u > L", level);
+    if (nct > KIP_MAXCT) HKS_FAIL(HKS_EINVAL, "rotate_hoisted_batch: at most %d ciphertexts per call", KIP_MAXCT);
+    const u32 beta = c->beta(level);
+    if (beta > 4) HKS_FAIL(HKS_EINVAL, "rotate_hoisted_batch: beta %u > 4", beta);
+    for (u32 r = 0; r < nrot; r++)
+        if ((st = check_galois(c, galois[r])) != HKS_OK) return st;
+    for (u32 i = 0; i < nct * nrot; i++)
+        if (!out0[i] || !out1[i]) HKS_FAIL(HKS_EINVAL, "rotate_hoisted_batch: NULL output");
+    for (u32 i = 0; i < nct; i++)
+        if (!c0[i] || !c1[i]) HKS_FAIL(HKS_EINVAL, "rotate_hoisted_batch: NULL input");
+    DevGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t N = c->n, l1 = level + 1, ne = c->ne(level), K = c->np;
+    u64 *base = (u64 *)ws;
+    u64 *coef = base;
+    u64 *exts = coef + l1 * N;                          // [nct][beta][ne]
+    u64 *accs = exts + (size_t)nct * beta * ne * N;     // [nct][2][ne]
+    u64 *md = accs + (size_t)nct * 2 * ne * N;          // ModDown workspace for 2 nct polynomials
+    for (u32 i = 0; i < nct; i++)
+        if ((st = modup_core(c, c1[i], level, exts + (size_t)i * beta * ne * N, coef, s)) != HKS_OK) return st;
+    for (u32 r = 0; r < nrot; r++) {
+        KipMultiArgs a{};
+        for (u32 i = 0; i < nct; i++) {
+            a.ext[i] = exts + (size_t)i * beta * ne * N;
+            a.c1[i] = c1[i];
+            a.acc[i] = accs + (size_t)i * 2 * ne * N;
+        }
+        a.evk = evk[r];
+        a.pc = c->d_pc;
+        a.galois = galois[r];
+        a.nct = nct;
+        a.log_n = c->log_n;
+        a.level = level;
+        a.nq = c->nq;
+        a.np = c->np;
+        a.ne = (u32)ne;
+        a.nk = c->nq + c->np;
+        a.beta = beta;
+        a.alpha = c->alpha;
+        if ((st = launch_kip_multi(a, s)) != HKS_OK) return st;
+        std::vector<u64 *> outs(2 * nct);
+        std::vector<const u64 *> adds(2 * nct);
+        std::vector<u64> gal(2 * nct);
+        for (u32 i = 0; i < nct; i++) {
+            outs[2 * i] = out0[(size_t)i * nrot + r];
+            outs[2 * i + 1] = out1[(size_t)i * nrot + r];
+            adds[2 * i] = c0[i];
+            adds[2 * i + 1] = nullptr;
+            gal[2 * i] = galois[r];
+            gal[2 * i + 1] = 1;
+        }
+        if ((st = moddown_core(c, accs, 2 * nct, level, outs.data(), adds.data(), gal.data(), md, s)) != HKS_OK) return st;
+    }
+    (void)K;
+    return HKS_OK;
+}
+
+extern "C" size_t hks_rotate_hoisted_batch_workspace_bytes(const hks_ctx *c, uint32_t nct, uint32_t level) {
+    if (!c || level > c->L() || nct == 0) return 0;
+    const size_t lb = limb_bytes(c), l1 = level + 1, ne = c->ne(level), K = c->np, beta = c->beta(level);
+    return (l1 + nct * (beta * ne + 2 * ne) + nct * (2 * K + 2 * l1)) * lb;
 }

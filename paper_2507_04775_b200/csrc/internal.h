@@ -25,7 +25,10 @@ struct LimbMap {
     u16 prime[HKS_MAXB];
     u16 sa[HKS_MAXB];   // epilogue operand slot (ModDown: acc limb)
     u16 sb[HKS_MAXB];   // epilogue operand slot (ModDown: c0 limb), 0xffff = none
+    uint8_t ob[HKS_MAXB];   // EPI_MODDOWN: output-table entry of limb b
 };
+
+#define NTT_MAXO 16         // output-table entries per ModDown launch
 
 enum NttEpi : int {
     EPI_LAZY = 0,      // first pass: store lazily reduced values
@@ -44,10 +47,11 @@ struct NttArgs {
     const u64 *ea;             // EPI_MODDOWN operand a base (acc)
     const u64 *eb;             // EPI_MODDOWN operand b base (c0), may be NULL
     const ulonglong2 *pinv;    // per prime P^-1 mod q (Shoup)
-    u64 galois;                // EPI_MODDOWN: b is read through the EVAL automorphism (1 = none)
-    u64 *out_b;                // limbs b >= nsplit write to out_b (second polynomial of a ModDown)
-    const u64 *eb_b;           // and add eb_b (NULL: none) without automorphism
-    u32 nsplit;                // 0xffffffff: single output
+    u64 galois;                // unused (kept for layout); see ogal
+    // EPI_MODDOWN output table: limb b writes outs[ob[b]] and adds adds[ob[b]] read through ogal[ob[b]]
+    u64 *outs[NTT_MAXO];
+    const u64 *adds[NTT_MAXO];
+    u64 ogal[NTT_MAXO];
     u32 log_n, log_r, log_c;   // N = R * C; R = 2^log_r rows, C = 2^log_c columns (row length)
     u32 tiles;                 // CTAs per limb
     u32 scale_mod;
@@ -59,7 +63,7 @@ struct NttArgs {
 // Base conversion (Eq. 1).  A group converts nsrc canonical y_i limbs to up to BC_MAXDST targets.
 #define BC_MAXSRC 16
 #define BC_MAXDST 64
-#define BC_MAXG 4
+#define BC_MAXG 16
 
 struct BconvGroup {
     u32 nsrc, ndst, mat_stride;
@@ -95,6 +99,20 @@ struct KipArgs {
     u64 galois;
     u32 log_n, level, nq, np, ne, nk, beta, alpha;
 };
+
+// Key inner product for several ciphertexts sharing one key (hoisted rotation batches): every key
+// word is loaded once and applied to all nct ciphertexts.
+#define KIP_MAXCT 8
+struct KipMultiArgs {
+    const u64 *ext[KIP_MAXCT];   // per ciphertext [beta][ne][N]
+    const u64 *c1[KIP_MAXCT];    // per ciphertext own-digit source (EVAL)
+    u64 *acc[KIP_MAXCT];         // per ciphertext [2][ne][N]
+    const u64 *evk;
+    const PrimeConst *pc;
+    u64 galois;
+    u32 nct, log_n, level, nq, np, ne, nk, beta, alpha;
+};
+hks_status launch_kip_multi(const KipMultiArgs &a, cudaStream_t s);
 
 // ----------------------------------------------------------------------------------------------
 // Fused last forward NTT pass + key inner product (PAPER.md:351 HMult fusion part (ii): "the NTT
@@ -221,9 +239,15 @@ hks_status run_ntt_inv_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in
                             u32 scale_mod, cudaStream_t s);
 // first (column) pass of the forward NTT only; the row pass is fused elsewhere (launch_ntt_kip)
 hks_status run_ntt_fwd_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in, u64 *out, cudaStream_t s);
-hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 *out, const u64 *acc,
-                           const u64 *c0, u64 galois, cudaStream_t s, u32 nsplit = 0xffffffffu, u64 *out_b = nullptr,
-                           const u64 *eb_b = nullptr);
+// ModDown's last NTT + epilogue for many polynomials at once: limb i of L belongs to polynomial
+// poly[i]; polynomial p writes outs[p] (+ adds[p] through the automorphism gal[p]).
+struct MdOut {
+    u64 *out;
+    const u64 *add;
+    u64 galois;
+};
+hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, const std::vector<uint8_t> &poly,
+                           const std::vector<MdOut> &outs, u64 *buf, const u64 *acc, cudaStream_t s);
 hks_status launch_bconv(const BconvArgs &a, u32 max_ndst, cudaStream_t s);
 hks_status launch_kip(const KipArgs &a, cudaStream_t s);
 hks_status launch_automorph(const u64 *in, u64 *out, u32 nlimbs, u32 log_n, u64 galois, cudaStream_t s);

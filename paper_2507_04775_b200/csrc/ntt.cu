@@ -56,8 +56,8 @@ k_ntt(const __grid_constant__ NttArgs A) {
     // element j of this thread's sub-transform lives at src_sub[j * JS]
     constexpr int JS = COLS ? C : 1;
     const size_t sub_off = COLS ? (size_t)(tile * NB + bsub) : (size_t)(tile * NB + bsub) * n;
-    const bool second = b >= A.nsplit;                 // second polynomial of a merged ModDown
-    u64 *const out_base = second ? A.out_b : A.out;
+    const u32 ob = EPI == EPI_MODDOWN ? A.map.ob[b] : 0;   // ModDown output-table entry
+    u64 *const out_base = EPI == EPI_MODDOWN ? A.outs[ob] : A.out;
     const u64 *__restrict__ src = A.in + (size_t)A.map.sin[b] * N + sub_off;
     u64 *__restrict__ dst = out_base + (size_t)A.map.sout[b] * N + sub_off;
     const ulonglong2 *__restrict__ tw =
@@ -75,10 +75,10 @@ k_ntt(const __grid_constant__ NttArgs A) {
     if (EPI == EPI_MODDOWN) {
         pinv = A.pinv[prime];
         ea = A.ea + (size_t)A.map.sa[b] * N + sub_off;
-        const u64 *ebase = second ? A.eb_b : A.eb;
+        const u64 *ebase = A.adds[ob];
         eb = (ebase && A.map.sb[b] != 0xffff) ? ebase + (size_t)A.map.sb[b] * N : nullptr;
     }
-    const u64 galois = second ? 1 : A.galois;
+    const u64 galois = EPI == EPI_MODDOWN ? A.ogal[ob] : 1;
     auto epi = [&](u64 x, int j) -> u64 {
         if (EPI == EPI_LAZY) return x;
         if (EPI == EPI_SCALE) return csub(csub(shoup_approx(x, sc.x, sc.y, m.np), m.two_p), m.p);
@@ -249,7 +249,8 @@ static hks_status go(NttArgs &a, cudaStream_t s) {
     HKS_CHECK_LAUNCH();
     // algorithmic bytes: each limb read once and written once (+ ModDown operands acc, c0)
     double words = 2.0 * a.nlimbs;
-    if (EPI == EPI_MODDOWN) words += a.nlimbs * (a.eb ? 2.0 : 1.0);
+    if (EPI == EPI_MODDOWN)
+        for (u32 i = 0; i < a.nlimbs; i++) words += (a.adds[a.map.ob[i]] && a.map.sb[i] != 0xffff) ? 2.0 : 1.0;
     // butterflies of this pass: N/2 per stage, LOGN stages; +1 Shoup per element for SCALE/MODDOWN
     const double nn = (double)(1ull << a.log_n);
     double muls = a.nlimbs * (nn / 2.0) * LOGN * 7.0;
@@ -298,6 +299,7 @@ static void fill_map(NttArgs &a, const LimbList &L, size_t off, u32 cnt, bool se
         a.map.prime[i] = L.prime[off + i];
         a.map.sa[i] = L.sa[off + i];
         a.map.sb[i] = L.sb[off + i];
+        a.map.ob[i] = 0;
     }
     a.nlimbs = cnt;
 }
@@ -310,7 +312,6 @@ hks_status run_ntt(const hks_ctx *ctx, NttDir dir, const LimbList &L, const u64 
         a.pc = ctx->d_pc;
         a.ninv = ctx->d_ninv;
         a.galois = 1;
-        a.nsplit = 0xffffffffu;
         // pass 0
         fill_map(a, L, off, cnt, false);
         a.in = in;
@@ -341,7 +342,6 @@ hks_status run_ntt_fwd_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in
         a.pc = ctx->d_pc;
         a.ninv = ctx->d_ninv;
         a.galois = 1;
-        a.nsplit = 0xffffffffu;
         fill_map(a, L, off, cnt, false);
         a.in = in;
         a.out = out;
@@ -359,7 +359,6 @@ hks_status run_ntt_inv_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in
     a.pc = ctx->d_pc;
     a.ninv = ctx->d_ninv;
     a.galois = 1;
-    a.nsplit = 0xffffffffu;
     fill_map(a, L, 0, (u32)L.size(), false);
     a.in = in;
     a.out = out;
@@ -369,17 +368,27 @@ hks_status run_ntt_inv_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in
     return launch_ntt_pass(ctx, NTT_INV, 1, EPI_SCALE, a, s);
 }
 
-hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 *out, const u64 *acc,
-                           const u64 *c0, u64 galois, cudaStream_t s, u32 nsplit, u64 *out_b, const u64 *eb_b) {
-    if (nsplit != 0xffffffffu && L.size() > HKS_MAXB) HKS_FAIL(HKS_EINVAL, "moddown: merged batch too large");
-    for (size_t off = 0; off < L.size(); off += HKS_MAXB) {
-        u32 cnt = (u32)((L.size() - off) < HKS_MAXB ? (L.size() - off) : HKS_MAXB);
+hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, const std::vector<uint8_t> &poly,
+                           const std::vector<MdOut> &outs, u64 *buf, const u64 *acc, cudaStream_t s) {
+    size_t off = 0;
+    while (off < L.size()) {
+        // one launch: at most HKS_MAXB limbs spanning at most NTT_MAXO polynomials
+        size_t end = off;
+        std::vector<uint8_t> seen;
+        while (end < L.size() && end - off < HKS_MAXB) {
+            const uint8_t p = poly[end];
+            if (std::find(seen.begin(), seen.end(), p) == seen.end()) {
+                if (seen.size() == NTT_MAXO) break;
+                seen.push_back(p);
+            }
+            end++;
+        }
+        const u32 cnt = (u32)(end - off);
         NttArgs a{};
         a.pc = ctx->d_pc;
         a.ninv = ctx->d_ninv;
         a.pinv = ctx->d_pinv;
-        a.galois = galois;
-        a.nsplit = 0xffffffffu;   // pass 0 stays in buf; only the epilogue pass splits
+        a.galois = 1;
         // pass 0: columns, in place on buf (slots sin)
         for (u32 i = 0; i < cnt; i++) {
             a.map.sin[i] = L.sin[off + i];
@@ -392,18 +401,21 @@ hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 
         a.tw = ctx->d_tw_col_fwd;
         hks_status st = launch_ntt_pass(ctx, NTT_FWD, 0, EPI_LAZY, a, s);
         if (st != HKS_OK) return st;
-        // pass 1: rows, buf -> out (limbs >= nsplit -> out_b) with the ModDown epilogue
+        // pass 1: rows, buf -> outs[...] with the ModDown epilogue
         fill_map(a, L, off, cnt, false);
-        a.nsplit = nsplit;
-        a.out_b = out_b;
-        a.eb_b = eb_b;
+        for (u32 k = 0; k < seen.size(); k++) {
+            a.outs[k] = outs[seen[k]].out;
+            a.adds[k] = outs[seen[k]].add;
+            a.ogal[k] = outs[seen[k]].galois;
+        }
+        for (u32 i = 0; i < cnt; i++)
+            a.map.ob[i] = (uint8_t)(std::find(seen.begin(), seen.end(), poly[off + i]) - seen.begin());
         a.in = buf;
-        a.out = out;
         a.ea = acc;
-        a.eb = c0;
         a.tw = ctx->d_tw_row_fwd;
         st = launch_ntt_pass(ctx, NTT_FWD, 1, EPI_MODDOWN, a, s);
         if (st != HKS_OK) return st;
+        off = end;
     }
     return HKS_OK;
 }
@@ -414,9 +426,12 @@ hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, u64 *buf, u64 
 // (lazy values).  Phase 2: coalesced sweep over the tile, two coefficients per thread:
 // acc_p = sum_j canon(D_j) * evk_j[p] with the 30-bit-split IMAD.WIDE accumulation (one reduction
 // per output).  D never returns to HBM.
+#ifndef HKS_KIP_MINB
+#define HKS_KIP_MINB 4
+#endif
 template <int LOGN, int LOGE, int LOGNB, int NTR, int NDIG>
 __global__ void __launch_bounds__(NTR * ((1 << LOGNB) << (LOGN - LOGE)),
-                                  (NTR * ((1 << LOGNB) << (LOGN - LOGE))) >= 384 ? 2 : 3)
+                                  (NTR * ((1 << LOGNB) << (LOGN - LOGE))) >= 384 ? 2 : HKS_KIP_MINB)
 k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
     constexpr int n = 1 << LOGN;
     constexpr int E = 1 << LOGE;
@@ -675,6 +690,9 @@ static hks_status go_kip_d(FusedKipArgs &a, cudaStream_t s) {
     HKS_FAIL(HKS_EINVAL, "ntt_kip: %u transformed of %u digits", a.ntr, a.ndig);
 }
 
+#ifndef HKS_KIP_LOGNB
+#define HKS_KIP_LOGNB 2   // 4 rows per CTA: more, smaller CTAs keep the three phases of co-resident CTAs staggered
+#endif
 hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s) {
     a.log_n = ctx->log_n;
     a.log_r = ctx->log_r;
@@ -682,8 +700,8 @@ hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s) {
     if (a.ndig > FK_MAXD || a.nu > FK_MAXU || a.ntr > a.ndig)
         HKS_FAIL(HKS_EINVAL, "ntt_kip: %u digits (%u transformed) / %u limbs per launch", a.ndig, a.ntr, a.nu);
     switch (ctx->log_n) {
-        case 17: return a.ntr > 3 ? go_kip_d<8, 4, 2>(a, s) : go_kip_d<8, 4, 3>(a, s);
-        case 16: return a.ntr > 3 ? go_kip_d<8, 4, 2>(a, s) : go_kip_d<8, 4, 3>(a, s);
+        case 17: return go_kip_d<8, 4, HKS_KIP_LOGNB>(a, s);
+        case 16: return go_kip_d<8, 4, HKS_KIP_LOGNB>(a, s);
         case 15: return go_kip_d<7, 4, 3>(a, s);
         case 14: return go_kip_d<7, 4, 3>(a, s);
         case 13: return go_kip_d<6, 3, 3>(a, s);

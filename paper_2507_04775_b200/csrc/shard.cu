@@ -235,10 +235,13 @@ extern "C" hks_status hks_shard_ks_moddown_out(const hks_ctx *c, uint32_t level,
     }
     if ((st = bconv_groups(c, groups, ypall, conv, s)) != HKS_OK) return st;
     LimbList M;
+    std::vector<uint8_t> poly;
     for (u32 p = 0; p < 2; p++)
-        for (u32 li = 0; li < P.nq_act; li++)
+        for (u32 li = 0; li < P.nq_act; li++) {
             M.push(p * P.nq_act + li, li, P.q_lo + li, p * P.n_own + li, (p == 0 && c0_loc) ? li : 0xffff);
-    if ((st = run_ntt_moddown(c, M, conv, out0_loc, acc_loc, c0_loc, 1, s, P.nq_act, out1_loc, nullptr)) != HKS_OK)
-        return st;
+            poly.push_back((uint8_t)p);
+        }
+    std::vector<MdOut> mo = {MdOut{out0_loc, c0_loc, 1}, MdOut{out1_loc, nullptr, 1}};
+    if ((st = run_ntt_moddown(c, M, poly, mo, conv, acc_loc, s)) != HKS_OK) return st;
     return HKS_OK;
 }

@@ -22,7 +22,7 @@ MAX_DIGITS = 64
 EXPORTS = ("hks_last_error", "hks_ctx_create", "hks_ctx_destroy", "hks_ctx_query", "hks_ctx_psi",
            "hks_workspace_bytes", "hks_ntt_fwd", "hks_ntt_inv", "hks_bconv", "hks_modup",
            "hks_ksk_inner_product", "hks_moddown", "hks_keyswitch", "hks_relinearize", "hks_automorph",
-           "hks_rotate_hoisted",
+           "hks_rotate_hoisted", "hks_rotate_hoisted_batch", "hks_rotate_hoisted_batch_workspace_bytes",
            "hks_launch_count", "hks_prof_enable", "hks_prof_read", "hks_shard_query", "hks_shard_workspace_bytes",
            "hks_shard_ks_modup_in", "hks_shard_ks_inner", "hks_shard_ks_moddown_out")
 
@@ -88,6 +88,11 @@ def lib() -> ctypes.CDLL:
         L.hks_launch_count.argtypes = []
         L.hks_prof_enable.argtypes = [ctypes.c_int]
         L.hks_prof_read.argtypes = [ctypes.POINTER(ProfEntry), ctypes.c_int]
+        L.hks_rotate_hoisted_batch.argtypes = [_vp, _u32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _u32, _u32,
+                                               ctypes.POINTER(_u64), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                               ctypes.POINTER(_vp), _vp, _vp]
+        L.hks_rotate_hoisted_batch_workspace_bytes.argtypes = [_vp, _u32, _u32]
+        L.hks_rotate_hoisted_batch_workspace_bytes.restype = ctypes.c_size_t
         L.hks_shard_query.argtypes = [_vp, _u32, _u32, _u32, ctypes.POINTER(ShardInfo)]
         L.hks_shard_workspace_bytes.argtypes = [_vp, _u32, _u32, _u32]
         L.hks_shard_workspace_bytes.restype = ctypes.c_size_t
@@ -95,7 +100,8 @@ def lib() -> ctypes.CDLL:
         L.hks_shard_ks_inner.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         L.hks_shard_ks_moddown_out.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         for f in EXPORTS[1:]:
-            if f not in ("hks_ctx_destroy", "hks_workspace_bytes", "hks_launch_count", "hks_shard_workspace_bytes"):
+            if f not in ("hks_ctx_destroy", "hks_workspace_bytes", "hks_launch_count", "hks_shard_workspace_bytes",
+                         "hks_rotate_hoisted_batch_workspace_bytes"):
                 getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -248,6 +254,26 @@ def prof_read() -> dict:
     k = lib().hks_prof_read(arr, 16)
     return {arr[i].name.decode(): (int(arr[i].launches), float(arr[i].total_ms), float(arr[i].bytes),
                                    float(arr[i].muls)) for i in range(k)}
+
+
+def rotate_hoisted_batch(ctx: Context, c0s, c1s, level: int, galois: Sequence[int], evks, outs0, outs1, ws,
+                         stream=None):
+    """outs0/outs1: flat lists, index ct * nrot + r."""
+    nct, n = len(c0s), len(galois)
+    g = (_u64 * n)(*[int(v) for v in galois])
+    a0 = (_vp * nct)(*[_ptr(x) for x in c0s])
+    a1 = (_vp * nct)(*[_ptr(x) for x in c1s])
+    ek = (_vp * n)(*[_ptr(e) for e in evks])
+    o0 = (_vp * (nct * n))(*[_ptr(o) for o in outs0])
+    o1 = (_vp * (nct * n))(*[_ptr(o) for o in outs1])
+    _check(lib().hks_rotate_hoisted_batch(ctx.handle, nct, a0, a1, level, n, g, ek, o0, o1, _ptr(ws), _stream(stream)),
+           "hks_rotate_hoisted_batch")
+
+
+def rotate_hoisted_batch_workspace(ctx: Context, nct: int, level: int):
+    import torch
+    nbytes = int(lib().hks_rotate_hoisted_batch_workspace_bytes(ctx.handle, nct, level))
+    return torch.empty(max(nbytes // 8, 1), dtype=torch.uint64, device=f"cuda:{ctx.device}")
 
 
 # ---- limb-sharded KeySwitch (C4): phases of include/hks.h; the all-gathers are the caller's

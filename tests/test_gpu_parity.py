@@ -253,7 +253,8 @@ def test_keyswitch_c0_null_and_determinism(orc):
 
 # ------------------------------------------------------------------ hoisted rotations
 
-@pytest.mark.parametrize("name,level,rots", [("T12", 6, [1, 2, 5]), ("C2", 29, [1, 3])])
+@pytest.mark.parametrize("name,level,rots", [("T12", 6, [1, 2, 5]), ("C2", 29, [1, 3]),
+                                             ("T12", 5, list(range(1, 11))), ("C2", 20, [1, 2, 3, 4, 5, 6, 7, 8, 9])])
 def test_rotate_hoisted_parity(orc, name, level, rots):
     cfg, ctx, o = ctxs(orc, name)
     keys = Keys(o, cfg.seed + 11)
@@ -330,3 +331,24 @@ def test_bconv_fp64_path_identical(orc):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("name,level,nct,rots", [("T12", 6, 3, [1, 2, 5]), ("C2", 29, 2, [1, 3, 8])])
+def test_rotate_hoisted_batch_parity(orc, name, level, nct, rots):
+    """Several ciphertexts sharing rotation keys (C3 shape): each output bit-equal to the hoisted oracle."""
+    cfg, ctx, o = ctxs(orc, name)
+    keys = Keys(o, cfg.seed + 13)
+    ks = [S.galois_rot(r, cfg.log_n) for r in rots]
+    evks = [keys.rot(k) for k in ks]
+    g = S.rng(490)
+    cts = [encrypt_under(o, g, keys.s_eval, level, 20)[1:] for _ in range(nct)]
+    nr = len(ks)
+    outs0 = [empty_dev(cts[0][0].shape) for _ in range(nct * nr)]
+    outs1 = [empty_dev(cts[0][0].shape) for _ in range(nct * nr)]
+    ws = H.rotate_hoisted_batch_workspace(ctx, nct, level)
+    H.rotate_hoisted_batch(ctx, [to_dev(c[0]) for c in cts], [to_dev(c[1]) for c in cts], level, ks,
+                           [to_dev(e) for e in evks], outs0, outs1, ws)
+    for i, (c0, c1) in enumerate(cts):
+        w0, w1 = o.rotate_hoisted(c0, c1, evks, level, ks)
+        for r in range(nr):
+            assert (to_host(outs0[i * nr + r]) == w0[r]).all() and (to_host(outs1[i * nr + r]) == w1[r]).all(), (i, r)
