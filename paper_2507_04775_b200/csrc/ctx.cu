@@ -101,7 +101,7 @@ hks_status upload(T **dptr, const std::vector<T> &h) {
 
 void free_tables(hks_ctx *c) {
     void *ptrs[] = {c->d_pc, c->d_tw_col_fwd, c->d_tw_row_fwd, c->d_tw_col_inv, c->d_tw_row_inv, c->d_ninv,
-                    c->d_mu_scale, c->d_mu_mat, c->d_md_scale, c->d_md_mat, c->d_pinv, c->d_mu_matf, c->d_md_matf};
+                    c->d_mu_scale, c->d_mu_mat, c->d_md_scale, c->d_md_mat, c->d_pinv, c->d_mu_matf, c->d_md_matf, c->d_mu_mats, c->d_md_mats};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -269,6 +269,12 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
         return f;
     };
     std::vector<double> mu_matf = limbs20(mu_mat), md_matf = limbs20(md_mat);
+    auto sums = [](const std::vector<uint2> &m) {
+        std::vector<u32> f(m.size());
+        for (size_t i = 0; i < m.size(); i++) f[i] = m[i].x + m[i].y;
+        return f;
+    };
+    std::vector<u32> mu_mats = sums(mu_mat), md_mats = sums(md_mat);
 
     hks_status st = HKS_OK;
 #define UP(dst, src) if (st == HKS_OK) st = upload(&c->dst, src)
@@ -285,6 +291,8 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     UP(d_pinv, pinv);
     UP(d_mu_matf, mu_matf);
     UP(d_md_matf, md_matf);
+    UP(d_mu_mats, mu_mats);
+    UP(d_md_mats, md_mats);
 #undef UP
     cudaSetDevice(prev);
     if (st != HKS_OK) {

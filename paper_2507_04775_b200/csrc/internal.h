@@ -69,6 +69,7 @@ struct BconvGroup {
     u32 nsrc, ndst, mat_stride;
     const uint2 *mat;          // [nsrc][mat_stride] (lo30, hi30) of [qhat_i]_t, column u = target u
     const double *matf;        // same entries as three exact 20-bit limbs [nsrc][mat_stride][3] (FP64 path) or NULL
+    const u32 *mats;           // (lo30 + hi30) of each entry [nsrc][mat_stride] (Karatsuba path) or NULL
     u16 src_slot[BC_MAXSRC];
     u16 src_prime[BC_MAXSRC];
     u64 pre_w[BC_MAXSRC];      // optional prescale y_i = x_i * pre_w (Shoup) -- generic hks_bconv
@@ -182,6 +183,8 @@ struct hks_ctx {
     ulonglong2 *d_md_scale = nullptr;   // ModDown: N^-1 * phat_k^-1 mod p_k  [K]
     uint2 *d_md_mat = nullptr;          // ModDown: [phat_k]_{q_i} split  [K][L+1]
     double *d_mu_matf = nullptr;        // ModUp matrices as 20-bit limbs in doubles (3 per entry)
+    u32 *d_mu_mats = nullptr;           // ModUp matrices: lo30 + hi30 per entry (Karatsuba middle term)
+    u32 *d_md_mats = nullptr;           // ModDown matrix: lo30 + hi30 per entry
     double *d_md_matf = nullptr;        // ModDown matrix as 20-bit limbs in doubles
     ulonglong2 *d_pinv = nullptr;       // P^-1 mod q_i  [L+1] (Shoup)
 

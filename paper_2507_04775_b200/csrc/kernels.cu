@@ -91,6 +91,76 @@ __global__ void __launch_bounds__(256, CPT == 1 ? 5 : 3) k_bconv(const __grid_co
     }
 }
 
+// Karatsuba variant (3 IMAD.WIDE per MAC instead of 4), one coefficient per thread, NSRC <= 12.
+template <int NSRC, bool LAZY>
+__global__ void __launch_bounds__(256, 3) k_bconv_kara(const __grid_constant__ BconvArgs A) {
+    const BconvGroup &G = A.g[blockIdx.y];
+    const u32 u0 = blockIdx.z * BC_TCH;
+    if (u0 >= G.ndst) return;
+    const u32 nt = min((u32)BC_TCH, G.ndst - u0);
+    __shared__ uint4 smat[NSRC * BC_TCH];
+    __shared__ PrimeConst spc[BC_TCH];
+    for (u32 idx = threadIdx.x; idx < NSRC * nt; idx += blockDim.x) {
+        const u32 i = idx / nt, u = idx - i * nt;
+        const uint2 m = G.mat[(size_t)i * G.mat_stride + u0 + u];
+        smat[i * BC_TCH + u] = make_uint4(m.x, m.y, G.mats[(size_t)i * G.mat_stride + u0 + u], 0);
+    }
+    for (u32 u = threadIdx.x; u < nt; u += blockDim.x) spc[u] = A.pc[G.dst_prime[u0 + u]];
+    __syncthreads();
+
+    const size_t N = (size_t)1 << A.log_n;
+    const size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= N) return;
+    u32 yl[NSRC], yh[NSRC];
+#pragma unroll
+    for (int i = 0; i < NSRC; i++) split30(A.in[(size_t)G.src_slot[i] * N + x], yl[i], yh[i]);
+    // two targets per iteration: their independent MAC/reduction chains interleave
+    for (u32 u = 0; u < nt; u += 2) {
+        const u32 v = (u + 1 < nt) ? u + 1 : u;
+        AccK a, b;
+#define KMAC(I) if (I < NSRC) { const uint4 m = smat[I * BC_TCH + u], mb = smat[I * BC_TCH + v]; \
+        const u32 ys = yl[I] + yh[I]; acck_mac<I>(a, yl[I], yh[I], ys, m.x, m.y, m.z); acck_mac<I>(b, yl[I], yh[I], ys, mb.x, mb.y, mb.z); }
+        KMAC(0) KMAC(1) KMAC(2) KMAC(3) KMAC(4) KMAC(5) KMAC(6) KMAC(7) KMAC(8) KMAC(9) KMAC(10) KMAC(11)
+#undef KMAC
+        u64 lo, hi, lob, hib;
+        acck_to128(a, NSRC, lo, hi);
+        acck_to128(b, NSRC, lob, hib);
+        const PrimeConst pc = spc[u], pcb = spc[v];
+        const u64 ra = LAZY ? reduce128_lazy(lo, hi, pc) : reduce128(lo, hi, pc);
+        const u64 rb = LAZY ? reduce128_lazy(lob, hib, pcb) : reduce128(lob, hib, pcb);
+        A.out[(size_t)G.dst_slot[u0 + u] * N + x] = ra;
+        if (v != u) A.out[(size_t)G.dst_slot[u0 + v] * N + x] = rb;
+    }
+}
+
+template <int NSRC>
+static void bconv_kara_go(const BconvArgs &a, cudaStream_t s) {
+    const u32 threads = 256;
+    const size_t N = (size_t)1 << a.log_n;
+    u32 maxdst = 0;
+    for (u32 g = 0; g < a.ngroups; g++) maxdst = max(maxdst, a.g[g].ndst);
+    dim3 grid((u32)((N + threads - 1) / threads), a.ngroups, (maxdst + BC_TCH - 1) / BC_TCH);
+    ProfScope ps(K_BCONV, s);
+    if (a.lazy_out)
+        k_bconv_kara<NSRC, true><<<grid, threads, 0, s>>>(a);
+    else
+        k_bconv_kara<NSRC, false><<<grid, threads, 0, s>>>(a);
+    double words = 0, macs = 0;
+    for (u32 g = 0; g < a.ngroups; g++) {
+        words += a.g[g].nsrc + a.g[g].ndst;
+        macs += (double)a.g[g].nsrc * a.g[g].ndst;
+    }
+    ps.done(words * (double)N * 8.0, macs * (double)N * 4.0);
+}
+
+static bool getenv_kara_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("HKS_BCONV_KARA");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // FP64-assisted variant (B200: the FP64 pipe runs 64 DFMA/clk/SM and is otherwise idle here):
 // sources [0, NSRC - NFP) accumulate on the integer pipe (4 IMAD.WIDE per MAC), sources
 // [NSRC - NFP, NSRC) on the FP64 pipe (9 exact DFMA per MAC on 20-bit limbs), one coefficient per
@@ -225,6 +295,14 @@ hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
             case 14: bconv_fp_go<14, 8>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
             case 15: bconv_fp_go<15, 8>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
             case 16: bconv_fp_go<16, 9>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            default: break;
+        }
+    }
+    if (!a.prescale && a.g[0].mats && getenv_kara_enabled()) {
+        switch (a.g[0].nsrc) {
+#define CK(NS) case NS: bconv_kara_go<NS>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            CK(2) CK(3) CK(4) CK(5) CK(6) CK(7) CK(8) CK(9) CK(10) CK(11) CK(12)
+#undef CK
             default: break;
         }
     }

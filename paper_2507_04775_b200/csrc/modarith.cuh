@@ -86,6 +86,45 @@ HKS_DEV void acc_to128(const Acc30 &a, u64 &lo, u64 &hi) {
     t = a.s2 << 60;  lo += t; hi += (lo < t); hi += a.s2 >> 4;
 }
 
+// ---- Karatsuba accumulation (3 IMAD.WIDE per MAC): y m = yl ml + ((yl+yh)(ml+mh) - yl ml - yh mh) 2^30
+// + yh mh 2^60.  (yl+yh), (ml+mh) < 2^31, so a middle product is < 2^62 and each of the three middle
+// accumulators (terms i = 0, 1, 2 mod 3) stays below 2^64 for up to 12 terms; s0, s2 < 16 * 2^60.
+struct AccK {
+    u64 s0, s2, m0, m1, m2;
+};
+
+template <int I>
+HKS_DEV void acck_mac(AccK &a, u32 yl, u32 yh, u32 ys, u32 ml, u32 mh, u32 ms) {
+    if (I == 0) {
+        a.s0 = mul_wide(yl, ml);
+        a.s2 = mul_wide(yh, mh);
+    } else {
+        mad_wide(a.s0, yl, ml);
+        mad_wide(a.s2, yh, mh);
+    }
+    if (I % 3 == 0) {
+        if (I == 0) a.m0 = mul_wide(ys, ms); else mad_wide(a.m0, ys, ms);
+    } else if (I % 3 == 1) {
+        if (I == 1) a.m1 = mul_wide(ys, ms); else mad_wide(a.m1, ys, ms);
+    } else {
+        if (I == 2) a.m2 = mul_wide(ys, ms); else mad_wide(a.m2, ys, ms);
+    }
+}
+
+// 128-bit value s0 + (m0 + m1 + m2 - s0 - s2) 2^30 + s2 2^60 for a chain of n terms
+HKS_DEV void acck_to128(const AccK &a, int n, u64 &lo, u64 &hi) {
+    // mid = m0 + m1 + m2 - s0 - s2  (< 2^66 as a 128-bit intermediate; the true value is < 2^65)
+    u64 mlo = a.m0, mhi = 0, t;
+    if (n > 1) { t = a.m1; mlo += t; mhi += (mlo < t); }
+    if (n > 2) { t = a.m2; mlo += t; mhi += (mlo < t); }
+    mhi -= (mlo < a.s0); mlo -= a.s0;
+    mhi -= (mlo < a.s2); mlo -= a.s2;
+    lo = a.s0;
+    hi = 0;
+    t = mlo << 30; lo += t; hi += (lo < t); hi += (mlo >> 34) | (mhi << 30);
+    t = a.s2 << 60; lo += t; hi += (lo < t); hi += a.s2 >> 4;
+}
+
 // ---- FP64-pipe partial dot products (k_bconv_fp): 60-bit operands as three exact 20-bit limbs in
 // doubles; every product < 2^40 and every partial sum < 2^46 is an integer below 2^53, so DFMA is
 // exact.  Five accumulators C_c = sum_{a+b=c} Y_a M_b give X = sum_c C_c 2^(20c).
