@@ -477,6 +477,19 @@ def main():
     hbm_peak, peak_src = peaks()
     extra = {}
     if not args.quick:
+        # ---- per-step distribution (SURVEY 8(d) timing protocol: median, p10, p90), own pass so
+        # the per-step events do not perturb the timed region above
+        nd = max(1, min(args.steps, 200))
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(nd + 1)]
+        evs[0].record(stream)
+        for i in range(nd):
+            wl.step(i)
+            evs[i + 1].record(stream)
+        evs[-1].synchronize()
+        per = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(nd))
+        q = lambda f: per[min(nd - 1, int(f * nd))]
+        extra["step_ms"] = {"p10": q(0.1), "median": q(0.5), "p90": q(0.9), "steps": nd}
+
         # ---- per-kernel breakdown: CUDA events recorded by libhks around each launch, same stream
         H.prof_enable(True)
         nprof = max(1, min(args.steps, 100 if cfg.name not in ("C3", "C5") else 5))
