@@ -75,6 +75,9 @@ def lib():
         L.or_rotate.argtypes = [_vp, _u64p, _u64p, ctypes.c_uint32, ctypes.c_uint64, _u64p, _u64p, _u64p]
         L.or_rotate_hoisted.argtypes = [_vp, _u64p, _u64p, ctypes.c_uint32, ctypes.c_uint32, _u64p,
                                         ctypes.POINTER(_u64p), ctypes.POINTER(_u64p), ctypes.POINTER(_u64p)]
+        L.or_tensor.argtypes = [_vp, _u64p, _u64p, _u64p, _u64p, ctypes.c_uint32, _u64p, _u64p, _u64p]
+        L.or_hmult.argtypes = [_vp, _u64p, _u64p, _u64p, _u64p, ctypes.c_uint32, _u64p, _u64p, _u64p]
+        L.or_rescale.argtypes = [_vp, _u64p, ctypes.c_uint32, _u64p]
         L.or_keygen_ks.argtypes = [_vp, _u64p, _u64p, _u64p, _i64p, _u64p]
         L.or_decrypt.argtypes = [_vp, _u64p, _u64p, ctypes.c_uint32, _u64p, _u64p]
         _lib = L
@@ -262,6 +265,29 @@ class Ctx:
         o1 = (_u64p * nrot)(*[_p64(o) for o in outs1])
         lib().or_rotate_hoisted(self._h, _p64(c0), _p64(c1), level, nrot, _p64(g), ek, o0, o1)
         return outs0, outs1
+
+    # ---- HMult front-end and Rescale (oracle.c: or_tensor, or_hmult, or_rescale)
+    def tensor(self, a0, a1, b0, b1, level: int):
+        a0, a1, b0, b1 = (np.ascontiguousarray(v, dtype=np.uint64) for v in (a0, a1, b0, b1))
+        d0, d1, d2 = np.empty_like(a0), np.empty_like(a0), np.empty_like(a0)
+        lib().or_tensor(self._h, _p64(a0), _p64(a1), _p64(b0), _p64(b1), level, _p64(d0), _p64(d1), _p64(d2))
+        return d0, d1, d2
+
+    def hmult(self, a0, a1, b0, b1, evk, level: int):
+        a0, a1, b0, b1 = (np.ascontiguousarray(v, dtype=np.uint64) for v in (a0, a1, b0, b1))
+        evk = np.ascontiguousarray(evk, dtype=np.uint64)
+        out0, out1 = np.empty_like(a0), np.empty_like(a0)
+        lib().or_hmult(self._h, _p64(a0), _p64(a1), _p64(b0), _p64(b1), level, _p64(evk), _p64(out0), _p64(out1))
+        return out0, out1
+
+    def rescale(self, x, level: int):
+        """One polynomial [l+1][N] EVAL at level l -> [l][N] EVAL at level l-1."""
+        assert level >= 1
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        assert x.shape == (level + 1, self.n)
+        out = np.empty((level, self.n), dtype=np.uint64)
+        lib().or_rescale(self._h, _p64(x), level, _p64(out))
+        return out
 
     # ---- client side (harness only)
     def secret_eval(self, s_coef: np.ndarray) -> np.ndarray:

@@ -488,6 +488,71 @@ void or_rotate(const or_ctx *c, const u64 *c0, const u64 *c1, u32 level, u64 gal
     free(r1);
 }
 
+/* ---------------------------------------------------------------- HMult front-end, Rescale */
+
+/* Tensor product of two ciphertexts in EVAL form (§3.6.5 HMult fusion lists its
+ * three outputs c0*c0', c0*c1' + c1*c0', c1*c1'; "tensor product (c0c0', c0c1'+c1c0',
+ * c1c1')"):  d0 = a0*b0, d1 = a0*b1 + a1*b0, d2 = a1*b1 (mod q_i), limbs 0..l. */
+void or_tensor(const or_ctx *c, const u64 *a0, const u64 *a1, const u64 *b0, const u64 *b1, u32 level,
+               u64 *d0, u64 *d1, u64 *d2) {
+    u32 n = c->n;
+    for (u32 i = 0; i <= level; i++) {
+        u64 q = c->m[i];
+        for (u32 x = 0; x < n; x++) {
+            size_t o = (size_t)i * n + x;
+            d0[o] = mulmod(a0[o], b0[o], q);
+            d1[o] = addmod(mulmod(a0[o], b1[o], q), mulmod(a1[o], b0[o], q), q);
+            d2[o] = mulmod(a1[o], b1[o], q);
+        }
+    }
+}
+
+/* HMult without rescale (Table 1 "HMult"): tensor product, then
+ * relinearisation of d2 by hybrid key switching with the relinearisation key:
+ *   out0 = d0 + ModDown(acc0), out1 = d1 + ModDown(acc1),  acc = KIP(ModUp(d2)). */
+void or_hmult(const or_ctx *c, const u64 *a0, const u64 *a1, const u64 *b0, const u64 *b1, u32 level,
+              const u64 *evk, u64 *out0, u64 *out1) {
+    size_t sz = (size_t)(level + 1) * c->n;
+    u64 *d0 = (u64 *)malloc(sizeof(u64) * sz), *d1 = (u64 *)malloc(sizeof(u64) * sz);
+    u64 *d2 = (u64 *)malloc(sizeof(u64) * sz), *t1 = (u64 *)malloc(sizeof(u64) * sz);
+    u32 *qidx = (u32 *)malloc(sizeof(u32) * (level + 1));
+    for (u32 i = 0; i <= level; i++) qidx[i] = i;
+    or_tensor(c, a0, a1, b0, b1, level, d0, d1, d2);
+    or_keyswitch(c, d0, d2, level, evk, out0, t1);
+    or_add(c, d1, t1, qidx, level + 1, out1);
+    free(d0); free(d1); free(d2); free(t1); free(qidx);
+}
+
+/* Rescale of one polynomial x [l+1][N] EVAL at level l >= 1 to level l-1 (Table 1
+ * "Rescale after multiplication"; §3.6.5 "q_l^{-1}(x^{(i)} - NTT(SwitchModulo(x^{(l)})))"):
+ *   t    = INTT_{q_l}(x_l)                                   (COEFF, [0, q_l))
+ *   s_i  = SwitchModulo(t) into q_i, centered: t if 2t < q_l, else t - q_l   (reading 15)
+ *   out_i = q_l^{-1} (x_i - NTT_{q_i}(s_i)) mod q_i,  i < l.
+ * Centered SwitchModulo makes the result the rounded quotient round(X / q_l) of the CRT value X. */
+void or_rescale(const or_ctx *c, const u64 *x, u32 level, u64 *out) {
+    u32 n = c->n;
+    u64 ql = c->m[level];
+    u64 *t = (u64 *)malloc(sizeof(u64) * n), *s = (u64 *)malloc(sizeof(u64) * n);
+    u32 li = level;
+    memcpy(t, x + (size_t)level * n, sizeof(u64) * n);
+    or_intt(c, t, &li, 1);
+    for (u32 i = 0; i < level; i++) {
+        u64 q = c->m[i];
+        for (u32 k = 0; k < n; k++) {
+            if ((u128)t[k] * 2 < ql) s[k] = t[k] % q;
+            else s[k] = submod(t[k] % q, ql % q, q); /* t - q_l (negative) mod q */
+        }
+        or_ntt(c, s, &i, 1);
+        u64 qinv = invmod(ql % q, q);
+        for (u32 k = 0; k < n; k++) {
+            size_t o = (size_t)i * n + k;
+            out[o] = mulmod(submod(x[o], s[k], q), qinv, q);
+        }
+    }
+    free(t);
+    free(s);
+}
+
 /* ---------------------------------------------------------------- client side (harness only) */
 
 /* Key-switching key generation (SURVEY.md §8(c) "oracle-side keygen", reading 10):
