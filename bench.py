@@ -550,6 +550,42 @@ def main():
             extra[f"ntt_{kind}_hbm_frac"] = 2 * nl * cfg.n * 8 / (t * 1e-3) / 1e9 / hbm_peak
         del bufs
 
+        # ---- NEXT-1 ops at this level (Table 3 "HMult" / "Rescale" rows): fused HMult
+        # (tensor + relinearisation) and Rescale of a 2-polynomial ciphertext, rotating the KS sets
+        if isinstance(wl, KSWorkload) and level >= 1:
+            ops = {}
+            sets = wl.sets
+            outs = [torch.empty_like(sets[0]["c0"]) for _ in range(2)]
+            wsh = ctx.workspace(H.OP_HMULT, level)
+            xs = [torch.stack([s["c0"], s["c1"]]) for s in sets]
+            rout = torch.empty((2, level, cfg.n), dtype=torch.int64, device=dev)
+            wsr = ctx.workspace(H.OP_RESCALE, level, 2)
+
+            def hm(i):
+                a, b = sets[i % len(sets)], sets[(i + 1) % len(sets)]
+                H.hmult(ctx, a["c0"], a["c1"], b["c0"], b["c1"], level, a["evk"], outs[0], outs[1], wsh, sid)
+
+            def rs(i):
+                H.rescale(ctx, xs[i % len(xs)], 2, level, rout, wsr, sid)
+
+            for name, fn, it, nbytes in (
+                    ("hmult", hm, 50, (6 * (level + 1) + 2 * cfg.beta(level) * (level + 1 + cfg.K)) * cfg.n * 8),
+                    ("rescale", rs, 200, (2 * (level + 1) + 2 * level) * cfg.n * 8)):
+                for i in range(3):
+                    fn(i)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for i in range(it):
+                    fn(i)
+                e1.record(stream)
+                e1.synchronize()
+                t = e0.elapsed_time(e1) / it
+                ops[name] = {"us": 1e3 * t, "per_s": 1e3 / t, "alg_bytes": nbytes,
+                             "hbm_frac": nbytes / (t * 1e-3) / 1e9 / hbm_peak}
+            extra["ops"] = ops
+            del xs, wsh, wsr
+
         # ---- e2e: through the public API from pinned host buffers, H2D + op + D2H per step
         if hasattr(wl, "e2e_setup"):
             h2d, d2h = wl.e2e_setup()

@@ -63,7 +63,9 @@ typedef enum {
     HKS_OP_MODUP = 0,           /* hks_modup */
     HKS_OP_MODDOWN = 1,         /* hks_moddown */
     HKS_OP_KEYSWITCH = 2,       /* hks_keyswitch */
-    HKS_OP_ROTATE_HOISTED = 3   /* hks_rotate_hoisted (count = nrot, not needed for sizing) */
+    HKS_OP_ROTATE_HOISTED = 3,  /* hks_rotate_hoisted (count = nrot, not needed for sizing) */
+    HKS_OP_HMULT = 4,           /* hks_hmult */
+    HKS_OP_RESCALE = 5          /* hks_rescale (count = npoly; 0 at level 0) */
 } hks_op;
 
 #define HKS_MAX_DIGITS 64
@@ -163,6 +165,25 @@ hks_status hks_keyswitch(const hks_ctx *ctx, const uint64_t *c0, const uint64_t 
 hks_status hks_relinearize(const hks_ctx *ctx, const uint64_t *d0, const uint64_t *d1, const uint64_t *d2,
                            uint32_t level, const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws,
                            void *stream);
+
+/* HMult without rescale (Table 1 "HMult"; §3.6.5 HMult fusion; DESIGN.md
+ * reading 16) of ct_a = (a0, a1) and ct_b = (b0, b1) at `level`, all [l+1][N] EVAL canonical:
+ *   d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1 (mod q_i);
+ *   out0 = d0 + ModDown(acc0), out1 = d1 + ModDown(acc1), acc = KIP(ModUp(d2), evk)  (evk = relin key).
+ * Fused: d2 is formed inside the first INTT pass, d0 / d1 inside the ModDown epilogue.  Outputs must
+ * not overlap any input or ws.  ws: hks_workspace_bytes(ctx, HKS_OP_HMULT, level, 0) bytes. */
+hks_status hks_hmult(const hks_ctx *ctx, const uint64_t *a0, const uint64_t *a1, const uint64_t *b0,
+                     const uint64_t *b1, uint32_t level, const uint64_t *evk, uint64_t *out0, uint64_t *out1,
+                     void *ws, void *stream);
+
+/* Rescale of npoly polynomials from level l >= 1 to l - 1 (Table 1 "Rescale after
+ * multiplication"; §3.6.5 "q_l^{-1}(x^(i) - NTT(SwitchModulo(x^(l))))"; DESIGN.md reading
+ * 15: centered SwitchModulo, i.e. the CRT value of the output is round(X / q_l)):
+ *   x   [npoly][l+1][N] EVAL canonical;  out [npoly][l][N] EVAL canonical (polynomial p at p*l*N).
+ *   A ciphertext is npoly = 2 (c0, c1 contiguous).  HKS_EINVAL at level 0, on overlap, NULL.
+ *   ws: hks_workspace_bytes(ctx, HKS_OP_RESCALE, level, npoly) bytes. */
+hks_status hks_rescale(const hks_ctx *ctx, const uint64_t *x, uint32_t npoly, uint32_t level, uint64_t *out,
+                       void *ws, void *stream);
 
 /* EVAL-form automorphism X -> X^galois on nlimbs limbs (prime-independent permutation,
  * SPEC.md:244-252; SURVEY.md reading 15):  out[l][j] = in[l][j'], 2brv(j')+1 = k(2brv(j)+1) mod 2N.

@@ -87,12 +87,14 @@ void add_groups(std::vector<BconvGroup> &out, u32 nsrc, const u16 *src_slot, con
 // ModUp: d [l+1][N] EVAL -> ext slots (j * ne + t) for t outside digit j.  coef: [l+1][N] scratch.
 // rows_pass = false stops after the column pass of the forward NTT (the KeySwitch fuses the row
 // pass with the key inner product).
+// d_b != NULL (HMult): the input is the tensor term d * d_b, computed inside the first INTT pass and
+// also stored (EVAL) to d_side for the key product's own-digit limbs.
 hks_status modup_core(const hks_ctx *c, const u64 *d, u32 level, u64 *ext, u64 *coef, cudaStream_t s,
-                      bool rows_pass = true) {
+                      bool rows_pass = true, const u64 *d_b = nullptr, u64 *d_side = nullptr) {
     const u32 ne = c->ne(level), beta = c->beta(level);
     LimbList L;
     for (u32 i = 0; i <= level; i++) L.push(i, i, i);
-    hks_status st = run_ntt(c, NTT_INV, L, d, coef, c->d_mu_scale + c->mu_scale_off[level], level + 1, s);
+    hks_status st = run_ntt(c, NTT_INV, L, d, coef, c->d_mu_scale + c->mu_scale_off[level], level + 1, s, d_b, d_side);
     if (st != HKS_OK) return st;
     std::vector<BconvGroup> groups;
     LimbList T;
@@ -141,7 +143,8 @@ hks_status ntt_kip_core(const hks_ctx *c, const u64 *ext, const u64 *c1, const u
 // the automorphism gal[p].  ws: y [npoly][K][N] then conv [npoly][l+1][N].  y_rows_done: the inverse
 // row pass of the P limbs already ran inside k_ntt_kip (y holds it).
 hks_status moddown_core(const hks_ctx *c, const u64 *acc, u32 npoly, u32 level, u64 *const *outs,
-                        const u64 *const *adds, const u64 *gal, u64 *ws, cudaStream_t s, bool y_rows_done = false) {
+                        const u64 *const *adds, const u64 *gal, u64 *ws, cudaStream_t s, bool y_rows_done = false,
+                        const u64 *const *tensor = nullptr) {
     const u32 ne = c->ne(level), K = c->np;
     u64 *y = ws, *conv = ws + (size_t)npoly * K * c->n;
     hks_status st = HKS_OK;
@@ -179,7 +182,7 @@ hks_status moddown_core(const hks_ctx *c, const u64 *acc, u32 npoly, u32 level, 
             poly.push_back((uint8_t)p);
         }
     }
-    return run_ntt_moddown(c, M, poly, mo, conv, acc, s);
+    return run_ntt_moddown(c, M, poly, mo, conv, acc, s, tensor);
 }
 
 hks_status kip_core(const hks_ctx *c, const u64 *ext, const u64 *c1, const u64 *evk, u32 level, u64 galois,
@@ -226,6 +229,12 @@ extern "C" size_t hks_workspace_bytes(const hks_ctx *c, hks_op op, uint32_t leve
         case HKS_OP_ROTATE_HOISTED: {
             const size_t rb = std::min<size_t>(count ? count : 1, rot_batch(c, level));
             return (l1 + beta * ne + rb * (2 * ne + 2 * K + 2 * l1)) * lb;
+        }
+        case HKS_OP_HMULT: return (l1 + beta * ne + 2 * ne + 2 * K + 2 * l1 + l1) * lb;
+        case HKS_OP_RESCALE: {
+            if (level == 0) return 0;
+            const size_t np_ = count ? count : 1;
+            return (np_ + np_ * level) * lb;
         }
     }
     return 0;
@@ -385,7 +394,7 @@ extern "C" hks_status hks_moddown(const hks_ctx *c, const uint64_t *acc, uint32_
 
 static hks_status keyswitch_impl(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, const uint64_t *add1,
                                   uint32_t level, const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws,
-                                  void *stream);
+                                  void *stream, const uint64_t *const *tensor = nullptr);
 
 extern "C" hks_status hks_keyswitch(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, uint32_t level,
                                     const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws, void *stream) {
@@ -404,19 +413,20 @@ extern "C" hks_status hks_relinearize(const hks_ctx *c, const uint64_t *d0, cons
 
 static hks_status keyswitch_impl(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, const uint64_t *add1,
                                   uint32_t level, const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws,
-                                  void *stream) {
+                                  void *stream, const uint64_t *const *tensor) {
     hks_status st = check_ctx(c);
     if (st != HKS_OK) return st;
     if (!c1 || !evk || !out0 || !out1 || !ws) HKS_FAIL(HKS_EINVAL, "keyswitch: NULL argument");
     if (level > c->L()) HKS_FAIL(HKS_EINVAL, "keyswitch: level %u > L", level);
     if (c->beta(level) > c->dnum) HKS_FAIL(HKS_EKEY, "keyswitch: key has fewer digits than beta");
     const size_t lb = limb_bytes(c), l1 = level + 1, ne = c->ne(level), beta = c->beta(level);
-    const size_t wsb = hks_workspace_bytes(c, HKS_OP_KEYSWITCH, level, 0);
-    const void *ins[3] = {c0, c1, evk};
-    size_t insz[3] = {l1 * lb, l1 * lb, (size_t)c->dnum * 2 * (c->nq + c->np) * lb};
+    const size_t wsb = hks_workspace_bytes(c, tensor ? HKS_OP_HMULT : HKS_OP_KEYSWITCH, level, 0);
+    const void *ins[6] = {c0, c1, evk, tensor ? tensor[1] : nullptr, tensor ? tensor[2] : nullptr,
+                          tensor ? tensor[3] : nullptr};
+    size_t insz[6] = {l1 * lb, l1 * lb, (size_t)c->dnum * 2 * (c->nq + c->np) * lb, l1 * lb, l1 * lb, l1 * lb};
     void *outs_[3] = {out0, out1, ws};
     size_t outsz[3] = {l1 * lb, l1 * lb, wsb};
-    for (int i = 0; i < 3; i++)
+    for (int i = 0; i < 6; i++)
         for (int o = 0; o < 3; o++)
             if (overlap(ins[i], insz[i], outs_[o], outsz[o])) HKS_FAIL(HKS_EINVAL, "keyswitch: output overlaps an input");
     if (overlap(out0, l1 * lb, out1, l1 * lb) || overlap(out0, l1 * lb, ws, wsb) || overlap(out1, l1 * lb, ws, wsb))
@@ -427,20 +437,59 @@ static hks_status keyswitch_impl(const hks_ctx *c, const uint64_t *c0, const uin
     u64 *ext = coef + l1 * c->n;
     u64 *acc = ext + beta * ne * c->n;
     u64 *md = acc + 2 * ne * c->n;
+    // HMult: d2 = a1 * b1 is formed inside the first INTT pass and kept (EVAL) after the ModDown
+    // workspace for the key product's own-digit limbs
+    u64 *d2 = tensor ? md + (2 * c->np + 2 * l1) * c->n : nullptr;
+    const u64 *kin = tensor ? d2 : c1;
+    const u64 *tb = tensor ? tensor[3] : nullptr;
     const bool fused = beta <= FK_MAXD;
     const bool ymode = fused && beta >= 2 && 2 * c->np <= HKS_MAXB;
     if (fused) {
         // INTT + BConv + NTT column pass, then the fused NTT row pass + key inner product (+ for the P
         // limbs, ModDown's inverse row pass straight into the ModDown workspace)
-        if ((st = modup_core(c, c1, level, ext, coef, s, false)) != HKS_OK) return st;
-        if ((st = ntt_kip_core(c, ext, c1, evk, level, acc, s, ymode ? md : nullptr)) != HKS_OK) return st;
+        if ((st = modup_core(c, c1, level, ext, coef, s, false, tb, d2)) != HKS_OK) return st;
+        if ((st = ntt_kip_core(c, ext, kin, evk, level, acc, s, ymode ? md : nullptr)) != HKS_OK) return st;
     } else {
-        if ((st = modup_core(c, c1, level, ext, coef, s)) != HKS_OK) return st;
-        if ((st = kip_core(c, ext, c1, evk, level, 1, acc, s)) != HKS_OK) return st;
+        if ((st = modup_core(c, c1, level, ext, coef, s, true, tb, d2)) != HKS_OK) return st;
+        if ((st = kip_core(c, ext, kin, evk, level, 1, acc, s)) != HKS_OK) return st;
     }
     u64 *outs[2] = {out0, out1};
     const u64 *adds[2] = {c0, add1};
+    if (tensor) return moddown_core(c, acc, 2, level, outs, nullptr, nullptr, md, s, ymode, tensor);
     return moddown_core(c, acc, 2, level, outs, adds, nullptr, md, s, ymode);
+}
+
+extern "C" hks_status hks_hmult(const hks_ctx *c, const uint64_t *a0, const uint64_t *a1, const uint64_t *b0,
+                                const uint64_t *b1, uint32_t level, const uint64_t *evk, uint64_t *out0,
+                                uint64_t *out1, void *ws, void *stream) {
+    if (!a0 || !a1 || !b0 || !b1) HKS_FAIL(HKS_EINVAL, "hmult: NULL ciphertext half");
+    const uint64_t *tensor[4] = {a0, a1, b0, b1};
+    // the KeySwitch input is d2 = a1 * b1 (first factor a1 passed as c1); a0 and c0 = NULL
+    return keyswitch_impl(c, a0, a1, nullptr, level, evk, out0, out1, ws, stream, tensor);
+}
+
+extern "C" hks_status hks_rescale(const hks_ctx *c, const uint64_t *x, uint32_t npoly, uint32_t level, uint64_t *out,
+                                  void *ws, void *stream) {
+    hks_status st = check_ctx(c);
+    if (st != HKS_OK) return st;
+    if (!x || !out || !ws || npoly == 0) HKS_FAIL(HKS_EINVAL, "rescale: NULL argument / no polynomial");
+    if (level > c->L()) HKS_FAIL(HKS_EINVAL, "rescale: level %u > L", level);
+    if (level == 0) HKS_FAIL(HKS_EINVAL, "rescale: level 0 has no limb to drop");
+    if (npoly > 0xffff / (level + 1)) HKS_FAIL(HKS_EINVAL, "rescale: too many polynomials");
+    const size_t lb = limb_bytes(c), wsb = hks_workspace_bytes(c, HKS_OP_RESCALE, level, npoly);
+    const size_t xb = (size_t)npoly * (level + 1) * lb, ob = (size_t)npoly * level * lb;
+    if (overlap(x, xb, out, ob) || overlap(ws, wsb, out, ob) || overlap(ws, wsb, x, xb))
+        HKS_FAIL(HKS_EINVAL, "rescale: buffers overlap");
+    DevGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    u64 *coef = (u64 *)ws, *buf = coef + (size_t)npoly * c->n;
+    // INTT of every top limb (canonical COEFF), then the fused SwitchModulo / NTT / epilogue passes
+    LimbList L;
+    for (u32 p = 0; p < npoly; p++) L.push(p * (level + 1) + level, p, level);
+    if ((st = run_ntt(c, NTT_INV, L, x, coef, nullptr, 0, s)) != HKS_OK) return st;
+    std::vector<u64 *> outs(npoly);
+    for (u32 p = 0; p < npoly; p++) outs[p] = out + (size_t)p * level * c->n;
+    return run_rescale(c, npoly, level, x, coef, buf, outs.data(), s);
 }
 
 extern "C" hks_status hks_automorph(const hks_ctx *c, const uint64_t *in, uint32_t nlimbs, uint64_t galois,

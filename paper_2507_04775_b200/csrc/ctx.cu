@@ -101,7 +101,8 @@ hks_status upload(T **dptr, const std::vector<T> &h) {
 
 void free_tables(hks_ctx *c) {
     void *ptrs[] = {c->d_pc, c->d_tw_col_fwd, c->d_tw_row_fwd, c->d_tw_col_inv, c->d_tw_row_inv, c->d_ninv,
-                    c->d_mu_scale, c->d_mu_mat, c->d_md_scale, c->d_md_mat, c->d_pinv, c->d_mu_matf, c->d_md_matf, c->d_mu_mats, c->d_md_mats};
+                    c->d_mu_scale, c->d_mu_mat, c->d_md_scale, c->d_md_mat, c->d_pinv, c->d_mu_matf, c->d_md_matf, c->d_mu_mats, c->d_md_mats,
+                    c->d_qmod, c->d_qlinv};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -257,6 +258,17 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
         pinv[i] = sh(inv_mod(P, qi), qi);
     }
 
+    // Rescale constants: q_j mod q_i (centered SwitchModulo from q_j into q_i) and
+    // q_j^-1 mod q_i (Shoup), row j = the dropped limb, [L+1][L+1]; diagonal unused.
+    std::vector<u64> qmod((size_t)num_q * num_q, 0);
+    std::vector<ulonglong2> qlinv((size_t)num_q * num_q, make_ulonglong2(0, 0));
+    for (u32 j = 0; j < num_q; j++)
+        for (u32 i = 0; i < num_q; i++) {
+            if (i == j) continue;
+            qmod[(size_t)j * num_q + i] = q[j] % q[i];
+            qlinv[(size_t)j * num_q + i] = sh(inv_mod(q[j] % q[i], q[i]), q[i]);
+        }
+
     // the same matrices as exact 20-bit limbs in doubles (FP64-pipe part of k_bconv_fp)
     auto limbs20 = [](const std::vector<uint2> &m) {
         std::vector<double> f(m.size() * 3);
@@ -293,6 +305,8 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     UP(d_md_matf, md_matf);
     UP(d_mu_mats, mu_mats);
     UP(d_md_mats, md_mats);
+    UP(d_qmod, qmod);
+    UP(d_qlinv, qlinv);
 #undef UP
     cudaSetDevice(prev);
     if (st != HKS_OK) {

@@ -34,7 +34,10 @@ enum NttEpi : int {
     EPI_LAZY = 0,      // first pass: store lazily reduced values
     EPI_CANON = 1,     // last forward pass: canonical store
     EPI_MODDOWN = 2,   // last forward pass: out = (a - x) * P^-1 [+ b]  (PAPER.md:350 ModDown fusion)
-    EPI_SCALE = 3      // last inverse pass: out = x * s (s = N^-1 or N^-1 * qhat^-1) canonical
+    EPI_SCALE = 3,     // last inverse pass: out = x * s (s = N^-1 or N^-1 * qhat^-1) canonical
+    EPI_TENSOR = 4,    // first inverse pass (rows) of d2 = in * in2, d2 also stored to side (HMult)
+    EPI_MDTENSOR = 5,  // EPI_MODDOWN + tensor terms: role 0 adds a0*b0, role 1 adds a0*b1 + a1*b0
+    EPI_SWITCH = 6     // first forward pass (columns) of centered SwitchModulo(in) from sw_q (Rescale)
 };
 
 struct NttArgs {
@@ -52,6 +55,15 @@ struct NttArgs {
     u64 *outs[NTT_MAXO];
     const u64 *adds[NTT_MAXO];
     u64 ogal[NTT_MAXO];
+    // EPI_TENSOR: second factor and the side output of the product (same slots as in / sin)
+    const u64 *in2;
+    u64 *side;
+    // EPI_MDTENSOR: ciphertext halves (slot = output limb sout), role of output-table entry
+    const u64 *ta0, *ta1, *tb0, *tb1;
+    uint8_t trole[NTT_MAXO];
+    // EPI_SWITCH: source modulus and sw_qmod[prime] = sw_q mod prime
+    u64 sw_q;
+    const u64 *sw_qmod;
     u32 log_n, log_r, log_c;   // N = R * C; R = 2^log_r rows, C = 2^log_c columns (row length)
     u32 tiles;                 // CTAs per limb
     u32 scale_mod;
@@ -187,6 +199,8 @@ struct hks_ctx {
     u32 *d_md_mats = nullptr;           // ModDown matrix: lo30 + hi30 per entry
     double *d_md_matf = nullptr;        // ModDown matrix as 20-bit limbs in doubles
     ulonglong2 *d_pinv = nullptr;       // P^-1 mod q_i  [L+1] (Shoup)
+    u64 *d_qmod = nullptr;              // Rescale: q_j mod q_i  [L+1][L+1] (row j = dropped limb)
+    ulonglong2 *d_qlinv = nullptr;      // Rescale: q_j^-1 mod q_i (Shoup)  [L+1][L+1]
 
     u32 L() const { return nq - 1; }
     u32 beta(u32 level) const { return (level + 1 + alpha - 1) / alpha; }
@@ -235,8 +249,11 @@ struct LimbList {
     }
     size_t size() const { return sin.size(); }
 };
+// in2 != NULL (inverse only): the first pass transforms in * in2 (tensor term) and stores the product
+// to side (same slots as in).
 hks_status run_ntt(const hks_ctx *ctx, NttDir dir, const LimbList &L, const u64 *in, u64 *out,
-                   const ulonglong2 *scale, u32 scale_mod, cudaStream_t s);
+                   const ulonglong2 *scale, u32 scale_mod, cudaStream_t s, const u64 *in2 = nullptr,
+                   u64 *side = nullptr);
 // second (column) pass of the inverse NTT only (the row pass was fused into k_ntt_kip)
 hks_status run_ntt_inv_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in, u64 *out, const ulonglong2 *scale,
                             u32 scale_mod, cudaStream_t s);
@@ -249,8 +266,13 @@ struct MdOut {
     const u64 *add;
     u64 galois;
 };
+// tensor != NULL (HMult): {a0, a1, b0, b1}; polynomial 0 adds a0 b0, polynomial 1 adds a0 b1 + a1 b0.
 hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, const std::vector<uint8_t> &poly,
-                           const std::vector<MdOut> &outs, u64 *buf, const u64 *acc, cudaStream_t s);
+                           const std::vector<MdOut> &outs, u64 *buf, const u64 *acc, cudaStream_t s,
+                           const u64 *const *tensor = nullptr);
+// Rescale of npoly polynomials (top limbs already COEFF in coef slots 0..npoly-1), see ntt.cu.
+hks_status run_rescale(const hks_ctx *ctx, u32 npoly, u32 level, const u64 *x, const u64 *coef, u64 *buf,
+                       u64 *const *outs, cudaStream_t s);
 hks_status launch_bconv(const BconvArgs &a, u32 max_ndst, cudaStream_t s);
 hks_status launch_kip(const KipArgs &a, cudaStream_t s);
 hks_status launch_automorph(const u64 *in, u64 *out, u32 nlimbs, u32 log_n, u64 galois, cudaStream_t s);

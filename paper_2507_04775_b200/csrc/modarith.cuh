@@ -334,6 +334,24 @@ HKS_DEV u64 reduce128(u64 lo, u64 hi, const PrimeConst &c) {
     return csub(r, c.p);
 }
 
+// x * y mod p, canonical, for x, y < 2^60 (one 128-bit product, one reduction)
+HKS_DEV u64 mulmod_full(u64 x, u64 y, const PrimeConst &c) { return reduce128(x * y, __umul64hi(x, y), c); }
+
+// (x0 y0 + x1 y1) mod p, canonical, for operands < 2^60 (128-bit sum < 2^121, one reduction)
+HKS_DEV u64 mul2mod_full(u64 x0, u64 y0, u64 x1, u64 y1, const PrimeConst &c) {
+    const u64 l0 = x0 * y0, l1 = x1 * y1, lo = l0 + l1;
+    const u64 hi = __umul64hi(x0, y0) + __umul64hi(x1, y1) + (lo < l0 ? 1 : 0);
+    return reduce128(lo, hi, c);
+}
+
+// SwitchModulo of t in [0, qs) from modulus qs into p, centered representative (t if 2t < qs, else
+// t - qs): the Rescale prologue (reading 15).  qs_mod_p = qs mod p.
+HKS_DEV u64 switch_centered(u64 t, u64 qs, u64 qs_mod_p, const PrimeConst &c) {
+    u64 r = csub(csub(mod64_lazy(t, c), 2 * c.p), c.p);
+    if (t > (qs >> 1)) r = r >= qs_mod_p ? r - qs_mod_p : r + c.p - qs_mod_p;
+    return r;
+}
+
 HKS_DEV u64 acc_reduce_lazy(const Acc30 &a, const PrimeConst &c) {
     u64 lo, hi;
     acc_to128(a, lo, hi);

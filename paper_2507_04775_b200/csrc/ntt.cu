@@ -29,10 +29,10 @@
 #ifndef HKS_NTT_MINB
 #define HKS_NTT_MINB 4
 #endif
+// One tile (NB sub-transforms of limb b) of a pass.  Round 0 reads global memory (forward and
+// inverse-column passes) or the tile the inverse-row prologue staged in shared memory.
 template <int LOGN, int LOGE, int LOGNB, int LOGC, bool COLS, bool FWD, int EPI>
-__global__ void __launch_bounds__((1 << LOGNB) << (LOGN - LOGE),
-                                  (((1 << LOGNB) << (LOGN - LOGE)) >= 512) ? 2 : HKS_NTT_MINB)
-k_ntt(const __grid_constant__ NttArgs A) {
+__device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u32 tile, u64 *sm) {
     constexpr int n = 1 << LOGN;
     constexpr int E = 1 << LOGE;
     constexpr int NB = 1 << LOGNB;
@@ -42,10 +42,8 @@ k_ntt(const __grid_constant__ NttArgs A) {
     constexpr int NR = (LOGN + LOGE - 1) / LOGE;      // rounds
     constexpr int ROWPAD = n + (n >> LOGE);
     constexpr int LOG_NLIMB = COLS ? (LOGN + LOGC) : 0;   // log2 N for the column pass
-    extern __shared__ __align__(16) u64 sm[];
+    constexpr bool MD = EPI == EPI_MODDOWN || EPI == EPI_MDTENSOR;   // ModDown-style epilogue
 
-    const u32 b = blockIdx.x / A.tiles;
-    const u32 tile = blockIdx.x - b * A.tiles;
     const u32 prime = A.map.prime[b];
     const u32 log_n = COLS ? (u32)LOG_NLIMB : A.log_n;
     const size_t N = (size_t)1 << log_n;
@@ -56,8 +54,8 @@ k_ntt(const __grid_constant__ NttArgs A) {
     // element j of this thread's sub-transform lives at src_sub[j * JS]
     constexpr int JS = COLS ? C : 1;
     const size_t sub_off = COLS ? (size_t)(tile * NB + bsub) : (size_t)(tile * NB + bsub) * n;
-    const u32 ob = EPI == EPI_MODDOWN ? A.map.ob[b] : 0;   // ModDown output-table entry
-    u64 *const out_base = EPI == EPI_MODDOWN ? A.outs[ob] : A.out;
+    const u32 ob = MD ? A.map.ob[b] : 0;   // ModDown output-table entry
+    u64 *const out_base = MD ? A.outs[ob] : A.out;
     const u64 *__restrict__ src = A.in + (size_t)A.map.sin[b] * N + sub_off;
     u64 *__restrict__ dst = out_base + (size_t)A.map.sout[b] * N + sub_off;
     const ulonglong2 *__restrict__ tw =
@@ -72,15 +70,17 @@ k_ntt(const __grid_constant__ NttArgs A) {
     if (EPI == EPI_SCALE) sc = A.scale ? A.scale[b % A.scale_mod] : A.ninv[prime];
     ulonglong2 pinv = make_ulonglong2(0, 0);
     const u64 *ea = nullptr, *eb = nullptr;
-    if (EPI == EPI_MODDOWN) {
+    if (MD) {
         pinv = A.pinv[prime];
         ea = A.ea + (size_t)A.map.sa[b] * N + sub_off;
         const u64 *ebase = A.adds[ob];
-        eb = (ebase && A.map.sb[b] != 0xffff) ? ebase + (size_t)A.map.sb[b] * N : nullptr;
+        eb = (EPI == EPI_MODDOWN && ebase && A.map.sb[b] != 0xffff) ? ebase + (size_t)A.map.sb[b] * N : nullptr;
     }
-    const u64 galois = EPI == EPI_MODDOWN ? A.ogal[ob] : 1;
+    const u64 galois = MD ? A.ogal[ob] : 1;
+    // EPI_SWITCH: the column pass loads the source-modulus COEFF limb and switches it into this prime
+    const u64 sw_m = EPI == EPI_SWITCH ? A.sw_qmod[prime] : 0;
     auto epi = [&](u64 x, int j) -> u64 {
-        if (EPI == EPI_LAZY) return x;
+        if (EPI == EPI_LAZY || EPI == EPI_TENSOR || EPI == EPI_SWITCH) return x;
         if (EPI == EPI_SCALE) return csub(csub(shoup_approx(x, sc.x, sc.y, m.np), m.two_p), m.p);
         if (EPI == EPI_CANON) return canon8(x, m);
         // EPI_MODDOWN: (a - x) * P^-1 [+ b], a canonical, x < 8p + 2^32
@@ -97,13 +97,38 @@ k_ntt(const __grid_constant__ NttArgs A) {
     // of its first round are contiguous, so a direct load would not coalesce); loads are batched.
     if (!FWD && !COLS) {
         const u64 *__restrict__ tsrc = A.in + (size_t)A.map.sin[b] * N + (size_t)tile * NB * n;
-        u64 tmp[E];
+        if (EPI == EPI_TENSOR) {
+            // HMult fusion: the INTT input is the tensor term d2 = in * in2, which the
+            // key product also needs in EVAL form, so it is stored once to side (4 pairs at a time)
+            const u64 *__restrict__ tsrc2 = A.in2 + (size_t)A.map.sin[b] * N + (size_t)tile * NB * n;
+            u64 *__restrict__ tside = A.side + (size_t)A.map.sin[b] * N + (size_t)tile * NB * n;
+            const PrimeConst pcb = A.pc[prime];
+            constexpr int TC = E < 4 ? E : 4;
 #pragma unroll
-        for (int q = 0; q < E; q++) tmp[q] = tsrc[tid + q * NT];
+            for (int q0 = 0; q0 < E; q0 += TC) {
+                u64 x1[TC], x2[TC];
 #pragma unroll
-        for (int q = 0; q < E; q++) {
-            const int idx = tid + q * NT, r = idx >> LOGN, k = idx & (n - 1);
-            sm[r * ROWPAD + k + (k >> LOGE)] = tmp[q];
+                for (int q = 0; q < TC; q++) {
+                    x1[q] = tsrc[tid + (q0 + q) * NT];
+                    x2[q] = tsrc2[tid + (q0 + q) * NT];
+                }
+#pragma unroll
+                for (int q = 0; q < TC; q++) {
+                    const int idx = tid + (q0 + q) * NT, r = idx >> LOGN, k = idx & (n - 1);
+                    const u64 d = mulmod_full(x1[q], x2[q], pcb);
+                    tside[idx] = d;
+                    sm[r * ROWPAD + k + (k >> LOGE)] = d;
+                }
+            }
+        } else {
+            u64 tmp[E];
+#pragma unroll
+            for (int q = 0; q < E; q++) tmp[q] = tsrc[tid + q * NT];
+#pragma unroll
+            for (int q = 0; q < E; q++) {
+                const int idx = tid + q * NT, r = idx >> LOGN, k = idx & (n - 1);
+                sm[r * ROWPAD + k + (k >> LOGE)] = tmp[q];
+            }
         }
         __syncthreads();
     }
@@ -129,7 +154,10 @@ k_ntt(const __grid_constant__ NttArgs A) {
 #pragma unroll
             for (int k = 0; k < Ee; k++) {
                 const int j = base + (k << lstride);
-                v[q * Ee + k] = from_global ? src[(size_t)j * JS] : sm[saddr(j)];
+                if (EPI == EPI_SWITCH && from_global)
+                    v[q * Ee + k] = switch_centered(src[(size_t)j * JS], A.sw_q, sw_m, A.pc[prime]);
+                else
+                    v[q * Ee + k] = from_global ? src[(size_t)j * JS] : sm[saddr(j)];
             }
         }
         // butterflies: twiddle of (stage half-size 2^ltg, element j) is tw[(n + j) >> (ltg + 1)],
@@ -195,14 +223,29 @@ k_ntt(const __grid_constant__ NttArgs A) {
         __syncthreads();
         const size_t tbase = (size_t)tile * NB * n;
         u64 *__restrict__ tdst = out_base + (size_t)A.map.sout[b] * N + tbase;
-        constexpr int CH = E < 8 ? E : 8;   // epilogue chunk: loads of a chunk are issued together
+        constexpr int CHM = EPI == EPI_MDTENSOR ? 2 : 8;
+        constexpr int CH = E < CHM ? E : CHM;   // epilogue chunk: loads of a chunk are issued together
+        const bool role1 = EPI == EPI_MDTENSOR && A.trole[ob] != 0;
+        const size_t tso = (size_t)A.map.sout[b] * N + tbase;   // tensor operand slot = output limb
 #pragma unroll
         for (int q0 = 0; q0 < E; q0 += CH) {
-            u64 av[CH], bv[CH];
-            if (EPI == EPI_MODDOWN) {
+            u64 av[CH], bv[CH], ta[CH], tb[CH], tc[CH], td[CH];
+            if (MD) {
                 const u64 *__restrict__ tea = A.ea + (size_t)A.map.sa[b] * N + tbase;
 #pragma unroll
                 for (int q = 0; q < CH; q++) av[q] = tea[tid + (q0 + q) * NT];
+                if (EPI == EPI_MDTENSOR) {
+#pragma unroll
+                    for (int q = 0; q < CH; q++) {
+                        const size_t o = tso + tid + (q0 + q) * NT;
+                        ta[q] = A.ta0[o];
+                        tb[q] = role1 ? A.tb1[o] : A.tb0[o];
+                        if (role1) {
+                            tc[q] = A.ta1[o];
+                            td[q] = A.tb0[o];
+                        }
+                    }
+                }
                 if (eb) {
 #pragma unroll
                     for (int q = 0; q < CH; q++) {
@@ -217,16 +260,31 @@ k_ntt(const __grid_constant__ NttArgs A) {
                 u64 x = sm[r * ROWPAD + k + (k >> LOGE)];
                 if (EPI == EPI_CANON) {
                     x = canon8(x, m);
-                } else if (EPI == EPI_MODDOWN) {
+                } else if (MD) {
                     u64 rr2 = shoup_approx(av[q] + m.eight_p + m.p - x, pinv.x, pinv.y, m.np);
                     rr2 = csub(csub(rr2, m.two_p), m.p);
                     if (eb) rr2 = csub(rr2 + bv[q], m.p);
+                    if (EPI == EPI_MDTENSOR) {
+                        // HMult: + a0 b0 (role 0) or + a0 b1 + a1 b0 (role 1)
+                        const PrimeConst pcb = A.pc[prime];
+                        const u64 t = role1 ? mul2mod_full(ta[q], tb[q], tc[q], td[q], pcb) : mulmod_full(ta[q], tb[q], pcb);
+                        rr2 = csub(rr2 + t, m.p);
+                    }
                     x = rr2;
                 }
                 tdst[idx] = x;
             }
         }
     }
+}
+
+template <int LOGN, int LOGE, int LOGNB, int LOGC, bool COLS, bool FWD, int EPI>
+__global__ void __launch_bounds__((1 << LOGNB) << (LOGN - LOGE),
+                                  (((1 << LOGNB) << (LOGN - LOGE)) >= 512) ? 2 : HKS_NTT_MINB)
+k_ntt(const __grid_constant__ NttArgs A) {
+    extern __shared__ __align__(16) u64 sm[];
+    const u32 b = blockIdx.x / A.tiles;
+    ntt_tile<LOGN, LOGE, LOGNB, LOGC, COLS, FWD, EPI>(A, b, blockIdx.x - b * A.tiles, sm);
 }
 
 template <int LOGN, int LOGE, int LOGNB, int LOGC, bool COLS, bool FWD, int EPI>
@@ -242,7 +300,7 @@ static hks_status go(NttArgs &a, cudaStream_t s) {
         (void)once;
     }
     a.tiles = COLS ? ((1u << a.log_c) >> LOGNB) : ((1u << a.log_r) >> LOGNB);
-    const int cls = FWD ? (COLS ? K_NTT_FWD_COLS : (EPI == EPI_MODDOWN ? K_NTT_FWD_ROWS_MODDOWN : K_NTT_FWD_ROWS))
+    const int cls = FWD ? (COLS ? K_NTT_FWD_COLS : ((EPI == EPI_MODDOWN || EPI == EPI_MDTENSOR) ? K_NTT_FWD_ROWS_MODDOWN : K_NTT_FWD_ROWS))
                         : (COLS ? K_NTT_INV_COLS : K_NTT_INV_ROWS);
     ProfScope ps(cls, s);
     kern<<<a.nlimbs * a.tiles, threads, smem, s>>>(a);
@@ -251,19 +309,34 @@ static hks_status go(NttArgs &a, cudaStream_t s) {
     double words = 2.0 * a.nlimbs;
     if (EPI == EPI_MODDOWN)
         for (u32 i = 0; i < a.nlimbs; i++) words += (a.adds[a.map.ob[i]] && a.map.sb[i] != 0xffff) ? 2.0 : 1.0;
+    double tmuls = 0;   // tensor products: 4 partial products each
+    if (EPI == EPI_MDTENSOR)
+        for (u32 i = 0; i < a.nlimbs; i++) {
+            const bool r1 = a.trole[a.map.ob[i]] != 0;
+            words += r1 ? 5.0 : 3.0;
+            tmuls += r1 ? 8.0 : 4.0;
+        }
+    if (EPI == EPI_TENSOR) {
+        words += 2.0 * a.nlimbs;   // second factor in, product out
+        tmuls += 4.0 * a.nlimbs;
+    }
     // butterflies of this pass: N/2 per stage, LOGN stages; +1 Shoup per element for SCALE/MODDOWN
     const double nn = (double)(1ull << a.log_n);
     double muls = a.nlimbs * (nn / 2.0) * LOGN * 7.0;
-    if (EPI == EPI_SCALE || EPI == EPI_MODDOWN) muls += a.nlimbs * nn * 7.0;
+    if (EPI == EPI_SCALE || EPI == EPI_MODDOWN || EPI == EPI_MDTENSOR) muls += a.nlimbs * nn * 7.0;
+    muls += tmuls * nn;
     ps.done(words * nn * 8.0, muls);
     return HKS_OK;
 }
 
 template <int LR, int ER, int BR, int LC, int EC, int BC>
 static hks_status dispatch(NttDir dir, bool cols, int epi, NttArgs &a, cudaStream_t s) {
+    if (dir == NTT_FWD && cols && epi == EPI_SWITCH) return go<LR, ER, BR, LC, true, true, EPI_SWITCH>(a, s);
     if (dir == NTT_FWD && cols) return go<LR, ER, BR, LC, true, true, EPI_LAZY>(a, s);
     if (dir == NTT_FWD && epi == EPI_CANON) return go<LC, EC, BC, LC, false, true, EPI_CANON>(a, s);
     if (dir == NTT_FWD && epi == EPI_MODDOWN) return go<LC, EC, BC, LC, false, true, EPI_MODDOWN>(a, s);
+    if (dir == NTT_FWD && epi == EPI_MDTENSOR) return go<LC, EC, BC, LC, false, true, EPI_MDTENSOR>(a, s);
+    if (dir == NTT_INV && !cols && epi == EPI_TENSOR) return go<LC, EC, BC, LC, false, false, EPI_TENSOR>(a, s);
     if (dir == NTT_INV && !cols) return go<LC, EC, BC, LC, false, false, EPI_LAZY>(a, s);
     if (dir == NTT_INV && cols) return go<LR, ER, BR, LC, true, false, EPI_SCALE>(a, s);
     HKS_FAIL(HKS_EINVAL, "ntt: unsupported epilogue %d", epi);
@@ -305,7 +378,8 @@ static void fill_map(NttArgs &a, const LimbList &L, size_t off, u32 cnt, bool se
 }
 
 hks_status run_ntt(const hks_ctx *ctx, NttDir dir, const LimbList &L, const u64 *in, u64 *out,
-                   const ulonglong2 *scale, u32 scale_mod, cudaStream_t s) {
+                   const ulonglong2 *scale, u32 scale_mod, cudaStream_t s, const u64 *in2, u64 *side) {
+    if (in2 && dir != NTT_INV) HKS_FAIL(HKS_EINVAL, "ntt: tensor prologue only on the inverse transform");
     for (size_t off = 0; off < L.size(); off += HKS_MAXB) {
         u32 cnt = (u32)((L.size() - off) < HKS_MAXB ? (L.size() - off) : HKS_MAXB);
         NttArgs a{};
@@ -317,7 +391,9 @@ hks_status run_ntt(const hks_ctx *ctx, NttDir dir, const LimbList &L, const u64 
         a.in = in;
         a.out = out;
         a.tw = dir == NTT_FWD ? ctx->d_tw_col_fwd : ctx->d_tw_row_inv;
-        hks_status st = launch_ntt_pass(ctx, dir, 0, EPI_LAZY, a, s);
+        a.in2 = in2;
+        a.side = side;
+        hks_status st = launch_ntt_pass(ctx, dir, 0, in2 ? EPI_TENSOR : EPI_LAZY, a, s);
         if (st != HKS_OK) return st;
         // pass 1 (in place on out)
         fill_map(a, L, off, cnt, true);
@@ -369,7 +445,8 @@ hks_status run_ntt_inv_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in
 }
 
 hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, const std::vector<uint8_t> &poly,
-                           const std::vector<MdOut> &outs, u64 *buf, const u64 *acc, cudaStream_t s) {
+                           const std::vector<MdOut> &outs, u64 *buf, const u64 *acc, cudaStream_t s,
+                           const u64 *const *tensor) {
     size_t off = 0;
     while (off < L.size()) {
         // one launch: at most HKS_MAXB limbs spanning at most NTT_MAXO polynomials
@@ -413,9 +490,67 @@ hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, const std::vec
         a.in = buf;
         a.ea = acc;
         a.tw = ctx->d_tw_row_fwd;
-        st = launch_ntt_pass(ctx, NTT_FWD, 1, EPI_MODDOWN, a, s);
+        if (tensor) {   // HMult: polynomial p of the pair takes tensor role p
+            a.ta0 = tensor[0];
+            a.ta1 = tensor[1];
+            a.tb0 = tensor[2];
+            a.tb1 = tensor[3];
+            for (u32 k = 0; k < seen.size(); k++) a.trole[k] = seen[k];
+        }
+        st = launch_ntt_pass(ctx, NTT_FWD, 1, tensor ? EPI_MDTENSOR : EPI_MODDOWN, a, s);
         if (st != HKS_OK) return st;
         off = end;
+    }
+    return HKS_OK;
+}
+
+// Rescale ("Rescale fusion"): for npoly polynomials x_p [l+1][N] EVAL whose top limb
+// is already COEFF in coef slot p, out_p[i] = q_l^-1 (x_p[i] - NTT_{q_i}(SwitchModulo(coef_p))) for
+// i < l.  Column pass: SwitchModulo fused into the load, into buf slot p*l + i.  Row pass: NTT and
+// the epilogue (EPI_MODDOWN with q_l^-1 in place of P^-1).
+hks_status run_rescale(const hks_ctx *ctx, u32 npoly, u32 level, const u64 *x, const u64 *coef, u64 *buf,
+                       u64 *const *outs, cudaStream_t s) {
+    const u32 pl = std::max<u32>(1, std::min<u32>(NTT_MAXO, HKS_MAXB / level));   // polys per launch
+    for (u32 p0 = 0; p0 < npoly; p0 += pl) {
+        const u32 np_ = std::min(pl, npoly - p0);
+        NttArgs a{};
+        a.pc = ctx->d_pc;
+        a.ninv = ctx->d_ninv;
+        a.galois = 1;
+        u32 cnt = 0;
+        for (u32 p = 0; p < np_; p++)
+            for (u32 i = 0; i < level; i++, cnt++) {
+                a.map.sin[cnt] = (u16)(p0 + p);
+                a.map.sout[cnt] = (u16)((p0 + p) * level + i);
+                a.map.prime[cnt] = (u16)i;
+            }
+        a.nlimbs = cnt;
+        a.in = coef;
+        a.out = buf;
+        a.tw = ctx->d_tw_col_fwd;
+        a.sw_q = ctx->primes[level];
+        a.sw_qmod = ctx->d_qmod + (size_t)level * ctx->nq;
+        hks_status st = launch_ntt_pass(ctx, NTT_FWD, 0, EPI_SWITCH, a, s);
+        if (st != HKS_OK) return st;
+        cnt = 0;
+        for (u32 p = 0; p < np_; p++) {
+            a.outs[p] = outs[p0 + p];
+            a.adds[p] = nullptr;
+            a.ogal[p] = 1;
+            for (u32 i = 0; i < level; i++, cnt++) {
+                a.map.sin[cnt] = (u16)((p0 + p) * level + i);
+                a.map.sout[cnt] = (u16)i;
+                a.map.sa[cnt] = (u16)((p0 + p) * (level + 1) + i);
+                a.map.sb[cnt] = 0xffff;
+                a.map.ob[cnt] = (uint8_t)p;
+            }
+        }
+        a.in = buf;
+        a.ea = x;
+        a.pinv = ctx->d_qlinv + (size_t)level * ctx->nq;
+        a.tw = ctx->d_tw_row_fwd;
+        st = launch_ntt_pass(ctx, NTT_FWD, 1, EPI_MODDOWN, a, s);
+        if (st != HKS_OK) return st;
     }
     return HKS_OK;
 }

@@ -15,13 +15,14 @@ LIB_PATH = os.environ.get("HKS_LIB_PATH") or os.path.join(_HERE, "libhks.so")   
 HKS_OK = 0
 STATUS = {0: "HKS_OK", 1: "HKS_EINVAL", 2: "HKS_ENOTPRIME", 3: "HKS_ENOTNTT", 4: "HKS_ERANGE", 5: "HKS_EDUP",
           6: "HKS_EKEY", 7: "HKS_EGALOIS", 8: "HKS_ECUDA", 9: "HKS_ENOMEM", 10: "HKS_EDEVICE"}
-OP_MODUP, OP_MODDOWN, OP_KEYSWITCH, OP_ROTATE_HOISTED = 0, 1, 2, 3
+OP_MODUP, OP_MODDOWN, OP_KEYSWITCH, OP_ROTATE_HOISTED, OP_HMULT, OP_RESCALE = 0, 1, 2, 3, 4, 5
 MAX_DIGITS = 64
 
 # every symbol include/hks.h declares (checked by tests/test_capi.py)
 EXPORTS = ("hks_last_error", "hks_ctx_create", "hks_ctx_destroy", "hks_ctx_query", "hks_ctx_psi",
            "hks_workspace_bytes", "hks_ntt_fwd", "hks_ntt_inv", "hks_bconv", "hks_modup",
-           "hks_ksk_inner_product", "hks_moddown", "hks_keyswitch", "hks_relinearize", "hks_automorph",
+           "hks_ksk_inner_product", "hks_moddown", "hks_keyswitch", "hks_relinearize", "hks_hmult", "hks_rescale",
+           "hks_automorph",
            "hks_rotate_hoisted", "hks_rotate_hoisted_batch", "hks_rotate_hoisted_batch_workspace_bytes",
            "hks_launch_count", "hks_prof_enable", "hks_prof_read", "hks_shard_query", "hks_shard_workspace_bytes",
            "hks_shard_ks_modup_in", "hks_shard_ks_inner", "hks_shard_ks_moddown_out")
@@ -82,6 +83,8 @@ def lib() -> ctypes.CDLL:
         L.hks_keyswitch.argtypes = [_vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp]
         L.hks_automorph.argtypes = [_vp, _vp, _u32, _u64, _vp, _vp]
         L.hks_relinearize.argtypes = [_vp, _vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp]
+        L.hks_hmult.argtypes = [_vp, _vp, _vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp]
+        L.hks_rescale.argtypes = [_vp, _vp, _u32, _u32, _vp, _vp, _vp]
         L.hks_rotate_hoisted.argtypes = [_vp, _vp, _vp, _u32, _u32, ctypes.POINTER(_u64), ctypes.POINTER(_vp),
                                          ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp]
         L.hks_launch_count.restype = ctypes.c_uint64
@@ -223,6 +226,15 @@ def keyswitch(ctx: Context, c0, c1, level: int, evk, out0, out1, ws, stream=None
 def relinearize(ctx: Context, d0, d1, d2, level: int, evk, out0, out1, ws, stream=None):
     _check(lib().hks_relinearize(ctx.handle, _ptr(d0), _ptr(d1), _ptr(d2), level, _ptr(evk), _ptr(out0), _ptr(out1),
                                  _ptr(ws), _stream(stream)), "hks_relinearize")
+
+
+def hmult(ctx: Context, a0, a1, b0, b1, level: int, evk, out0, out1, ws, stream=None):
+    _check(lib().hks_hmult(ctx.handle, _ptr(a0), _ptr(a1), _ptr(b0), _ptr(b1), level, _ptr(evk), _ptr(out0),
+                           _ptr(out1), _ptr(ws), _stream(stream)), "hks_hmult")
+
+
+def rescale(ctx: Context, x, npoly: int, level: int, out, ws, stream=None):
+    _check(lib().hks_rescale(ctx.handle, _ptr(x), npoly, level, _ptr(out), _ptr(ws), _stream(stream)), "hks_rescale")
 
 
 def automorph(ctx: Context, x, nlimbs: int, galois: int, out, stream=None):

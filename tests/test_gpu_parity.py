@@ -352,3 +352,110 @@ def test_rotate_hoisted_batch_parity(orc, name, level, nct, rots):
         w0, w1 = o.rotate_hoisted(c0, c1, evks, level, ks)
         for r in range(nr):
             assert (to_host(outs0[i * nr + r]) == w0[r]).all() and (to_host(outs1[i * nr + r]) == w1[r]).all(), (i, r)
+
+
+# ------------------------------------------------------------------ HMult front-end and Rescale (NEXT-1)
+
+def run_hmult(ctx, a0, a1, b0, b1, level, evk_dev):
+    out0, out1 = empty_dev(a0.shape), empty_dev(a0.shape)
+    ws = ctx.workspace(H.OP_HMULT, level)
+    H.hmult(ctx, to_dev(a0), to_dev(a1), to_dev(b0), to_dev(b1), level, evk_dev, out0, out1, ws)
+    return to_host(out0), to_host(out1)
+
+
+@pytest.mark.parametrize("name,levels", [("C1", [2]), ("C1p", [2, 0]), ("T10", [4, 1]), ("T12", [6, 3, 0]),
+                                         ("T16s", [5]), ("T17s", [4, 2])])
+def test_hmult_parity_small(orc, name, levels):
+    """tensor product fused into the first INTT pass (d2) and the ModDown epilogue (d0, d1): bit-exact
+    with the oracle's tensor + relinearisation, and decrypts to m1 * m2 within the KS bound."""
+    cfg, ctx, o = ctxs(orc, name)
+    keys, evk = relin_key(o, name)
+    evk_d = to_dev(evk)
+    g = S.rng(cfg.seed + 41)
+    for level in levels:
+        m1, a0, a1 = encrypt_under(o, g, keys.s_eval, level, 12)
+        m2, b0, b1 = encrypt_under(o, g, keys.s_eval, level, 12)
+        got0, got1 = run_hmult(ctx, a0, a1, b0, b1, level, evk_d)
+        want0, want1 = o.hmult(a0, a1, b0, b1, evk, level)
+        assert (got0 == want0).all() and (got1 == want1).all(), level
+
+
+@pytest.mark.parametrize("level", [29, 19, 9, 0])
+def test_hmult_parity_c2(orc, level):
+    """C2 parameters (N=2^16, L=29, dnum=3) with edge residues, across the digit drops."""
+    cfg, ctx, o = ctxs(orc, "C2")
+    keys, evk = relin_key(o, "C2")
+    g = S.rng(cfg.seed + 200 + level)
+    qs = o.q[: level + 1]
+    a0, b1 = edge_limbs(qs, o.n, g), edge_limbs(qs, o.n, g)
+    a1, b0 = S.uniform_limbs(g, qs, o.n), S.uniform_limbs(g, qs, o.n)
+    got0, got1 = run_hmult(ctx, a0, a1, b0, b1, level, to_dev(evk))
+    want0, want1 = o.hmult(a0, a1, b0, b1, evk, level)
+    assert (got0 == want0).all() and (got1 == want1).all()
+
+
+@pytest.mark.slow
+def test_hmult_parity_c4(orc):
+    cfg, ctx, o = ctxs(orc, "C4")
+    g = S.rng(cfg.seed + 5)
+    nk = o.nq + o.np
+    evk = np.stack([S.uniform_limbs(g, o.primes, o.n) for _ in range(2 * o.dnum)]).reshape(o.dnum, 2, nk, o.n)
+    level = 35
+    a0, a1, b0, b1 = (S.uniform_limbs(g, o.q[: level + 1], o.n) for _ in range(4))
+    got0, got1 = run_hmult(ctx, a0, a1, b0, b1, level, to_dev(evk))
+    want0, want1 = o.hmult(a0, a1, b0, b1, evk, level)
+    assert (got0 == want0).all() and (got1 == want1).all()
+
+
+def run_rescale(ctx, x, npoly, level):
+    out = empty_dev((npoly, level, x.shape[-1]))
+    ws = ctx.workspace(H.OP_RESCALE, level, npoly)
+    H.rescale(ctx, to_dev(np.ascontiguousarray(x)), npoly, level, out, ws)
+    return to_host(out)
+
+
+@pytest.mark.parametrize("name,levels,npoly", [("C1", [2, 1], 2), ("T10", [4, 1], 1), ("T12", [6, 3, 1], 2),
+                                               ("T16s", [5], 3), ("T17s", [4, 1], 2), ("C2", [29, 20, 1], 2),
+                                               ("C4", [35], 2)])
+def test_rescale_parity(orc, name, levels, npoly):
+    """PAPER.md:349 Rescale fusion: SwitchModulo fused into the forward column pass, q_l^-1 (x - .) in
+    the row-pass epilogue; bit-exact with the oracle per polynomial."""
+    cfg, ctx, o = ctxs(orc, name)
+    g = S.rng(cfg.seed + 51)
+    for level in levels:
+        qs = o.q[: level + 1]
+        x = np.stack([edge_limbs(qs, o.n, g) for _ in range(npoly)])
+        got = run_rescale(ctx, x, npoly, level)
+        for p in range(npoly):
+            assert (got[p] == o.rescale(x[p], level)).all(), (level, p)
+
+
+def test_rescale_many_polys_and_errors(orc):
+    """more polynomials than one launch's output table (16), level 0 / overlap rejected."""
+    cfg, ctx, o = ctxs(orc, "T12")
+    g = S.rng(61)
+    level, npoly = 3, 20
+    x = np.stack([S.uniform_limbs(g, o.q[: level + 1], o.n) for _ in range(npoly)])
+    got = run_rescale(ctx, x, npoly, level)
+    for p in (0, 7, 15, 16, 19):
+        assert (got[p] == o.rescale(x[p], level)).all(), p
+    xd = to_dev(x[0])
+    ws = ctx.workspace(H.OP_RESCALE, 1, 1)
+    with pytest.raises(H.HksError) as e:
+        H.rescale(ctx, xd, 1, 0, empty_dev((1, o.n)), ws)            # level 0
+    assert e.value.status == 1
+    with pytest.raises(H.HksError) as e:
+        H.rescale(ctx, xd, 1, level, xd, ws)                         # out overlaps x
+    assert e.value.status == 1
+
+
+def test_hmult_rejects_aliasing(orc):
+    cfg, ctx, o = ctxs(orc, "T12")
+    keys, evk = relin_key(o, "T12")
+    level = 2
+    a = to_dev(S.uniform_limbs(S.rng(1), o.q[: level + 1], o.n))
+    out1 = empty_dev(a.shape)
+    ws = ctx.workspace(H.OP_HMULT, level)
+    with pytest.raises(H.HksError) as e:
+        H.hmult(ctx, a, a, a, a, level, to_dev(evk), a, out1, ws)    # out0 aliases an input
+    assert e.value.status == 1
