@@ -561,12 +561,14 @@ hks_status run_rescale(const hks_ctx *ctx, u32 npoly, u32 level, const u64 *x, c
 // (lazy values).  Phase 2: coalesced sweep over the tile, two coefficients per thread:
 // acc_p = sum_j canon(D_j) * evk_j[p] with the 30-bit-split IMAD.WIDE accumulation (one reduction
 // per output).  D never returns to HBM.
-#ifndef HKS_KIP_MINB
-#define HKS_KIP_MINB 4
-#endif
+// resident CTAs per SM requested from ptxas: an 80-register budget per thread (the kernel's natural
+// size), 1..16 CTAs
+constexpr int kip_minb(int threads) {
+    return (65536 / (80 * threads)) < 1 ? 1 : ((65536 / (80 * threads)) > 16 ? 16 : 65536 / (80 * threads));
+}
 template <int LOGN, int LOGE, int LOGNB, int NTR, int NDIG>
 __global__ void __launch_bounds__(NTR * ((1 << LOGNB) << (LOGN - LOGE)),
-                                  (NTR * ((1 << LOGNB) << (LOGN - LOGE))) >= 384 ? 2 : HKS_KIP_MINB)
+                                  kip_minb(NTR * ((1 << LOGNB) << (LOGN - LOGE))))
 k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
     constexpr int n = 1 << LOGN;
     constexpr int E = 1 << LOGE;
@@ -826,8 +828,8 @@ static hks_status go_kip_d(FusedKipArgs &a, cudaStream_t s) {
 }
 
 #ifndef HKS_KIP_LOGNB
-#define HKS_KIP_LOGNB 2   // 4 rows per CTA: more, smaller CTAs keep the three phases of co-resident CTAs staggered
-#endif
+#define HKS_KIP_LOGNB 1   // 2 rows per CTA: many small CTAs keep the three phases of co-resident CTAs staggered
+#endif                    // (measured: 4 rows 98.7 us, 2 rows 96.5 us per C2 KeySwitch)
 hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s) {
     a.log_n = ctx->log_n;
     a.log_r = ctx->log_r;
