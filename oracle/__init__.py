@@ -78,6 +78,10 @@ def lib():
         L.or_tensor.argtypes = [_vp, _u64p, _u64p, _u64p, _u64p, ctypes.c_uint32, _u64p, _u64p, _u64p]
         L.or_hmult.argtypes = [_vp, _u64p, _u64p, _u64p, _u64p, ctypes.c_uint32, _u64p, _u64p, _u64p]
         L.or_rescale.argtypes = [_vp, _u64p, ctypes.c_uint32, _u64p]
+        _pp = ctypes.POINTER(_u64p)
+        L.or_pt_wsum.argtypes = [_vp, ctypes.c_uint32, _pp, _pp, _pp, ctypes.c_uint32, _u64p, _u64p]
+        L.or_lintrans.argtypes = [_vp, _u64p, _u64p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, _u64p, _pp,
+                                  _u64p, _pp, _pp, _u64p, _u64p]
         L.or_keygen_ks.argtypes = [_vp, _u64p, _u64p, _u64p, _i64p, _u64p]
         L.or_decrypt.argtypes = [_vp, _u64p, _u64p, ctypes.c_uint32, _u64p, _u64p]
         _lib = L
@@ -288,6 +292,30 @@ class Ctx:
         out = np.empty((level, self.n), dtype=np.uint64)
         lib().or_rescale(self._h, _p64(x), level, _p64(out))
         return out
+
+    # ---- BSGS linear transform (oracle.c: or_pt_wsum, or_lintrans)
+    def pt_wsum(self, w, x0, x1, level: int):
+        w, x0, x1 = ([np.ascontiguousarray(v, dtype=np.uint64) for v in arr] for arr in (w, x0, x1))
+        n = len(w)
+        arr = lambda vs: (_u64p * n)(*[_p64(v) for v in vs])
+        out0, out1 = np.empty_like(x0[0]), np.empty_like(x0[0])
+        lib().or_pt_wsum(self._h, n, arr(w), arr(x0), arr(x1), level, _p64(out0), _p64(out1))
+        return out0, out1
+
+    def lintrans(self, c0, c1, level: int, n1: int, n2: int, baby_galois, baby_keys, giant_galois, giant_keys, pts):
+        """pts: n2*n1 diagonals [l+1][N] (index i*n1 + j); baby/giant lists have n1-1 / n2-1 entries."""
+        c0 = np.ascontiguousarray(c0, dtype=np.uint64)
+        c1 = np.ascontiguousarray(c1, dtype=np.uint64)
+        keep = [np.ascontiguousarray(v, dtype=np.uint64) for v in list(baby_keys) + list(giant_keys) + list(pts)]
+        nb, ng = len(baby_keys), len(giant_keys)
+        assert nb == n1 - 1 and ng == n2 - 1 and len(pts) == n1 * n2
+        arr = lambda vs: (_u64p * max(1, len(vs)))(*[_p64(v) for v in vs])
+        bg = np.array(list(baby_galois) + [1], dtype=np.uint64)
+        gg = np.array(list(giant_galois) + [1], dtype=np.uint64)
+        out0, out1 = np.empty_like(c0), np.empty_like(c0)
+        lib().or_lintrans(self._h, _p64(c0), _p64(c1), level, n1, n2, _p64(bg), arr(keep[:nb]), _p64(gg),
+                          arr(keep[nb:nb + ng]), arr(keep[nb + ng:]), _p64(out0), _p64(out1))
+        return out0, out1
 
     # ---- client side (harness only)
     def secret_eval(self, s_coef: np.ndarray) -> np.ndarray:

@@ -553,6 +553,71 @@ void or_rescale(const or_ctx *c, const u64 *x, u32 level, u64 *out) {
     free(s);
 }
 
+/* ---------------------------------------------------------------- BSGS linear transform (NEXT-2) */
+
+/* Fused plaintext-weighted sum of ciphertexts (§3.6.5 "a weighed sum can be reduced
+ * from 4n-2 down to n+1 memory operations"): out_p = sum_j w_j * x_{j,p} (mod q_i), p = 0, 1.
+ * x0[j], x1[j], w[j]: [l+1][N] EVAL. */
+void or_pt_wsum(const or_ctx *c, u32 nterm, const u64 *const *w, const u64 *const *x0, const u64 *const *x1,
+                u32 level, u64 *out0, u64 *out1) {
+    u32 n = c->n;
+    for (u32 i = 0; i <= level; i++) {
+        u64 q = c->m[i];
+        for (u32 k = 0; k < n; k++) {
+            size_t o = (size_t)i * n + k;
+            u64 s0 = 0, s1 = 0;
+            for (u32 j = 0; j < nterm; j++) {
+                s0 = addmod(s0, mulmod(w[j][o], x0[j][o], q), q);
+                s1 = addmod(s1, mulmod(w[j][o], x1[j][o], q), q);
+            }
+            out0[o] = s0;
+            out1[o] = s1;
+        }
+    }
+}
+
+/* Ciphertext x plaintext-matrix product by baby-step giant-step (§3.6.7: "Each
+ * ciphertext-vector times plaintext-matrix multiplication is then performed using a BSGS algorithm,
+ * which reduces the number of required rotations and leverages the hoisted rotation optimization";
+ * no ModDown hoisting; SPEC.md:576-583 homomorphic_linear_transform):
+ *   ct_0 = ct, ct_j = RotHoisted_{bg[j-1]}(ct) for j = 1..n1-1 (one shared ModUp);
+ *   I_i  = sum_j pt[i*n1 + j] * ct_j  (i < n2);
+ *   out  = I_0 + sum_{i>=1} RotHoisted_{gg[i-1]}(I_i)  (one rotation per giant step).
+ * pt[i*n1+j] [l+1][N] EVAL are the (pre-rotated) diagonals; bk[j-1], gk[i-1] the rotation keys. */
+void or_lintrans(const or_ctx *c, const u64 *c0, const u64 *c1, u32 level, u32 n1, u32 n2, const u64 *bg,
+                 const u64 *const *bk, const u64 *gg, const u64 *const *gk, const u64 *const *pt, u64 *out0,
+                 u64 *out1) {
+    size_t sz = (size_t)(level + 1) * c->n;
+    u64 **b0 = (u64 **)malloc(sizeof(u64 *) * n1), **b1 = (u64 **)malloc(sizeof(u64 *) * n1);
+    b0[0] = (u64 *)c0;
+    b1[0] = (u64 *)c1;
+    for (u32 j = 1; j < n1; j++) {
+        b0[j] = (u64 *)malloc(sizeof(u64) * sz);
+        b1[j] = (u64 *)malloc(sizeof(u64) * sz);
+    }
+    if (n1 > 1) or_rotate_hoisted(c, c0, c1, level, n1 - 1, bg, bk, b0 + 1, b1 + 1);
+    u64 *i0 = (u64 *)malloc(sizeof(u64) * sz), *i1 = (u64 *)malloc(sizeof(u64) * sz);
+    u64 *r0 = (u64 *)malloc(sizeof(u64) * sz), *r1 = (u64 *)malloc(sizeof(u64) * sz);
+    u32 *qidx = (u32 *)malloc(sizeof(u32) * (level + 1));
+    for (u32 i = 0; i <= level; i++) qidx[i] = i;
+    for (u32 i = 0; i < n2; i++) {
+        or_pt_wsum(c, n1, pt + (size_t)i * n1, (const u64 *const *)b0, (const u64 *const *)b1, level, i0, i1);
+        if (i == 0) {
+            memcpy(out0, i0, sizeof(u64) * sz);
+            memcpy(out1, i1, sizeof(u64) * sz);
+        } else {
+            or_rotate_hoisted(c, i0, i1, level, 1, gg + (i - 1), gk + (i - 1), &r0, &r1);
+            or_add(c, out0, r0, qidx, level + 1, out0);
+            or_add(c, out1, r1, qidx, level + 1, out1);
+        }
+    }
+    for (u32 j = 1; j < n1; j++) {
+        free(b0[j]);
+        free(b1[j]);
+    }
+    free(b0); free(b1); free(i0); free(i1); free(r0); free(r1); free(qidx);
+}
+
 /* ---------------------------------------------------------------- client side (harness only) */
 
 /* Key-switching key generation (SURVEY.md §8(c) "oracle-side keygen", reading 10):
