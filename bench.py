@@ -73,9 +73,9 @@ def workload_desc(cfg, level):
         return (f"C3: 8 ciphertexts x 8 hoisted rotation KeySwitches (r=1..8, Galois 5^r), {base}, level={level}, "
                 f"keys replicated, ciphertexts sharded over ranks")
     if cfg.name == "C5":
-        return (f"C5: BOOT_SHAPE v1 (SURVEY.md 8(d)): CtS 3x(7 hoisted baby + 7 giant rotations) at l=29..27, "
-                f"conjugation at 26, 12 relin KS + rescale-shaped INTT/NTT at l=26..15, StC 3x14 at l=14..12 "
-                f"= 97 KeySwitches, {base}")
+        return (f"C5: BOOT_SHAPE v2 (DESIGN.md reading 14): CtS 3x(BSGS linear transform n1=n2=8: 7 hoisted baby "
+                f"+ 7 giant rotations, 64 diagonals; Rescale) at l=29..27, conjugation at 26, EvalMod stand-in "
+                f"12x(HMult + Rescale) at l=26..15, StC 3x(BSGS + Rescale) at l=14..12 = 97 KeySwitches, {base}")
     return f"{cfg.name}: one relinearisation KeySwitch per ciphertext, {base}, level={level}, primes<2^{cfg.bits}"
 
 
@@ -340,70 +340,102 @@ class C3Workload:
 
 
 class C5Workload:
-    """C5 = BOOT_SHAPE v1 on one ciphertext per rank (replicas)."""
+    """C5 = BOOT_SHAPE v2 on one ciphertext per rank (replicas): the bootstrapping schedule of
+    SURVEY.md 8(d) built from the real operations (reading 14):
+      CoeffToSlot: 3 BSGS linear transforms (n1 = n2 = 8: 7 hoisted baby + 7 giant rotations, 64
+                   plaintext diagonals, PAPER.md:364) at l = 29, 28, 27, each followed by Rescale;
+      conjugation KS at l = 26;
+      EvalMod stand-in: 12 x (HMult + Rescale) at l = 26 .. 15;
+      SlotToCoeff: 3 BSGS transforms + Rescale at l = 14, 13, 12.
+    97 KeySwitches per sequence (3*14 + 1 + 12 + 3*14)."""
     unit = "sequences/s"
     scaling = "weak"
 
     def __init__(self, H, ctx, cfg, dev, seed, sid):
         import torch
         self.H, self.ctx, self.cfg, self.sid = H, ctx, cfg, sid
-        L = cfg.L
-        bs = [S.galois_rot(r, cfg.log_n) for r in range(1, 8)]              # baby steps 1..7
-        gs = [S.galois_rot(8 * r, cfg.log_n) for r in range(1, 8)]          # giant steps 8..56
-        self.baby, self.giant, self.conj = bs, gs, S.GALOIS_CONJ(cfg.log_n)
+        L, n = cfg.L, cfg.n
+        self.n1 = self.n2 = 8
+        self.baby = [S.galois_rot(r, cfg.log_n) for r in range(1, 8)]
+        self.giant = [S.galois_rot(8 * r, cfg.log_n) for r in range(1, 8)]
+        self.conj = S.GALOIS_CONJ(cfg.log_n)
         keys = make_sets(cfg, L, 16, dev, seed)
         self.kb = [keys[i]["evk"] for i in range(7)]
         self.kg = [keys[7 + i]["evk"] for i in range(7)]
         self.krelin, self.kconj = keys[14]["evk"], keys[15]["evk"]
         for k in keys:
             del k["c0"], k["c1"], k["out0"], k["out1"]
-        ct = make_sets(cfg, L, 1, dev, seed + 3)[0]
-        self.c0, self.c1 = ct["c0"], ct["c1"]
-        shape = self.c0.shape
-        self.o0 = [torch.empty(shape, dtype=torch.int64, device=dev) for _ in range(7)]
-        self.o1 = [torch.empty(shape, dtype=torch.int64, device=dev) for _ in range(7)]
-        self.t0 = torch.empty(shape, dtype=torch.int64, device=dev)
-        self.t1 = torch.empty(shape, dtype=torch.int64, device=dev)
-        self.ws = ctx.workspace(H.OP_ROTATE_HOISTED, L, 7)
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed + 5)
+        q = torch.tensor([int(v) for v in cfg.q], dtype=torch.int64, device=dev).view(-1, 1)
+        # 64 seeded diagonals [L+1][N] (uniform residues), sliced to each stage's level
+        self.pts = [torch.randint(0, 2 ** 62, (L + 1, n), generator=g, device=dev, dtype=torch.int64) % q
+                    for _ in range(self.n1 * self.n2)]
+        ct = make_sets(cfg, L, 2, dev, seed + 3)
+        self.c0, self.c1 = ct[0]["c0"], ct[0]["c1"]
+        self.d0, self.d1 = ct[1]["c0"], ct[1]["c1"]                      # second HMult operand
+        mk = lambda: torch.empty((L + 1, n), dtype=torch.int64, device=dev)
+        self.a0, self.a1 = mk(), mk()
+        self.ws_lt = H.linear_transform_workspace(ctx, L, self.n1)
+        self.ws_ks = ctx.workspace(H.OP_HMULT, L)
+        self.ws_rs = ctx.workspace(H.OP_RESCALE, L, 1)
         self.units = 1
         self.ks_per_seq = 97
 
-    def _stage(self, level):
+    def _rescale(self, x0, x1, level, out0, out1):
+        """Rescale (x0, x1) at level -> (out0, out1) at level - 1, one polynomial per call."""
         H, c, s = self.H, self.ctx, self.sid
-        a0, a1 = self.c0[: level + 1], self.c1[: level + 1]
-        H.rotate_hoisted(c, a0, a1, level, self.baby, self.kb, [o[: level + 1] for o in self.o0],
-                         [o[: level + 1] for o in self.o1], self.ws, s)                    # 7 hoisted baby steps
-        for g in range(7):                                                                 # 7 giant steps
-            H.rotate_hoisted(c, self.o0[g][: level + 1], self.o1[g][: level + 1], level, [self.giant[g]],
-                             [self.kg[g]], [self.t0[: level + 1]], [self.t1[: level + 1]], self.ws, s)
+        H.rescale(c, x0[: level + 1], 1, level, out0[:level], self.ws_rs, s)
+        H.rescale(c, x1[: level + 1], 1, level, out1[:level], self.ws_rs, s)
+
+    def _lt(self, level):
+        H, c, s = self.H, self.ctx, self.sid
+        l1 = level + 1
+        H.linear_transform(c, self.c0[:l1], self.c1[:l1], level, self.n1, self.n2, self.baby, self.kb, self.giant,
+                           self.kg, [p[:l1] for p in self.pts], self.a0[:l1], self.a1[:l1], self.ws_lt, s)
+        self._rescale(self.a0, self.a1, level, self.c0, self.c1)
 
     def step(self, i):
         H, c, s, L = self.H, self.ctx, self.sid, self.cfg.L
         for level in (L, L - 1, L - 2):                                                    # CoeffToSlot
-            self._stage(level)
+            self._lt(level)
         lv = L - 3
         H.rotate_hoisted(c, self.c0[: lv + 1], self.c1[: lv + 1], lv, [self.conj], [self.kconj],
-                         [self.t0[: lv + 1]], [self.t1[: lv + 1]], self.ws, s)             # conjugation
+                         [self.a0[: lv + 1]], [self.a1[: lv + 1]], self.ws_ks, s)        # conjugation
         for level in range(L - 3, L - 15, -1):                                             # EvalMod stand-in
-            H.keyswitch(c, self.c0[: level + 1], self.c1[: level + 1], level, self.krelin, self.t0[: level + 1],
-                        self.t1[: level + 1], self.ws, s)
-            H.ntt_inv(c, self.t0[: level + 1], list(range(level + 1)), s)                    # rescale-shaped
-            H.ntt_fwd(c, self.t0[: level], list(range(level)), s)
+            l1 = level + 1
+            H.hmult(c, self.c0[:l1], self.c1[:l1], self.d0[:l1], self.d1[:l1], level, self.krelin,
+                    self.a0[:l1], self.a1[:l1], self.ws_ks, s)
+            self._rescale(self.a0, self.a1, level, self.c0, self.c1)
         for level in (L - 15, L - 16, L - 17):                                             # SlotToCoeff
-            self._stage(level)
+            self._lt(level)
+
+    def ops(self, timeit):
+        """one BSGS linear transform (n1 = n2 = 8, 14 KeySwitches) at l = L, timed alone"""
+        L, l1 = self.cfg.L, self.cfg.L + 1
+        H, c, s = self.H, self.ctx, self.sid
+        t = timeit(lambda i: H.linear_transform(c, self.c0, self.c1, L, 8, 8, self.baby, self.kb, self.giant, self.kg,
+                                                self.pts, self.a0, self.a1, self.ws_lt, s), 10)
+        return {"linear_transform_bsgs_8x8": {"us": 1e3 * t, "per_s": 1e3 / t, "keyswitch_per_s": 14e3 / t,
+                                              "level": L}}
 
     def alg_bytes(self):
         c = self.cfg
+        ks = lambda l: (4 * (l + 1) + 2 * c.beta(l) * (l + 1 + c.K)) * c.n * 8
+        rs = lambda l: (4 * l + 2) * c.n * 8
+        wsum = lambda l: 8 * (3 * 8 + 2) * (l + 1) * c.n * 8
         tot = 0
-        for l in [c.L, c.L - 1, c.L - 2] * 1 + [c.L - 15, c.L - 16, c.L - 17]:
-            tot += 14 * (4 * (l + 1) + 2 * c.beta(l) * (l + 1 + c.K)) * c.n * 8
+        for l in [c.L, c.L - 1, c.L - 2, c.L - 15, c.L - 16, c.L - 17]:
+            tot += 14 * ks(l) + wsum(l) + rs(l)
+        tot += ks(c.L - 3)
         for l in range(c.L - 3, c.L - 15, -1):
-            tot += (4 * (l + 1) + 2 * c.beta(l) * (l + 1 + c.K) + 4 * (l + 1)) * c.n * 8
+            tot += ks(l) + 4 * (l + 1) * c.n * 8 + rs(l)
         return tot
 
     def l2_note(self):
         c = self.cfg
-        return f"16 keys ({16 * 2 * c.dnum * (c.L + 1 + c.K) * c.n * 8 / 1e9:.2f} GB) >> 126 MB L2"
+        return (f"16 keys ({16 * 2 * c.dnum * (c.L + 1 + c.K) * c.n * 8 / 1e9:.2f} GB) + 64 diagonals "
+                f"({64 * (c.L + 1) * c.n * 8 / 1e9:.2f} GB) >> 126 MB L2")
 
 
 def torch_empty_pinned_like(t):
@@ -585,6 +617,20 @@ def main():
                              "hbm_frac": nbytes / (t * 1e-3) / 1e9 / hbm_peak}
             extra["ops"] = ops
             del xs, wsh, wsr
+
+        if hasattr(wl, "ops"):
+            def timeit(fn, it):
+                for i in range(2):
+                    fn(i)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for i in range(it):
+                    fn(i)
+                e1.record(stream)
+                e1.synchronize()
+                return e0.elapsed_time(e1) / it
+            extra["ops"] = wl.ops(timeit)
 
         # ---- e2e: through the public API from pinned host buffers, H2D + op + D2H per step
         if hasattr(wl, "e2e_setup"):

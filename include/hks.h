@@ -185,6 +185,30 @@ hks_status hks_hmult(const hks_ctx *ctx, const uint64_t *a0, const uint64_t *a1,
 hks_status hks_rescale(const hks_ctx *ctx, const uint64_t *x, uint32_t npoly, uint32_t level, uint64_t *out,
                        void *ws, void *stream);
 
+/* Fused plaintext-weighted sum of ciphertexts (§3.6.5 "a weighed sum can be reduced from
+ * 4n-2 down to n+1 memory operations"):  out_p = sum_{j<nterm} w[j] * x_p[j]  (mod q_i), p = 0, 1.
+ *   w[j], x0[j], x1[j]: host arrays of nterm device pointers, each [l+1][N] EVAL canonical (w[j] a
+ *   plaintext, (x0[j], x1[j]) a ciphertext); out0, out1 [l+1][N] EVAL canonical, must not overlap any
+ *   term.  One 128-bit accumulation and one reduction per output (16 terms per pass). */
+hks_status hks_pt_weighted_sum(const hks_ctx *ctx, uint32_t nterm, const uint64_t *const *w,
+                               const uint64_t *const *x0, const uint64_t *const *x1, uint32_t level,
+                               uint64_t *out0, uint64_t *out1, void *stream);
+
+/* Ciphertext x plaintext-matrix product by baby-step giant-step (§3.6.7: "performed using
+ * a BSGS algorithm ... leverages the hoisted rotation optimization"; no ModDown hoisting):
+ *   ct_0 = (c0, c1);  ct_j = RotHoisted(ct, baby_galois[j-1], baby_evk[j-1]), j = 1..n1-1 (one ModUp);
+ *   I_i = sum_j pt[i*n1 + j] * ct_j   (hks_pt_weighted_sum);
+ *   out = I_0 + sum_{i=1..n2-1} RotHoisted(I_i, giant_galois[i-1], giant_evk[i-1]).
+ *   pt: host array of n1*n2 device pointers to the (pre-rotated) diagonals [l+1][N] EVAL; galois / evk:
+ *   host arrays (n1-1 and n2-1 entries).  out0/out1 [l+1][N] must not overlap the inputs or ws.
+ *   ws: hks_linear_transform_workspace_bytes(ctx, level, n1) bytes. */
+hks_status hks_linear_transform(const hks_ctx *ctx, const uint64_t *c0, const uint64_t *c1, uint32_t level,
+                                uint32_t n1, uint32_t n2, const uint64_t *baby_galois,
+                                const uint64_t *const *baby_evk, const uint64_t *giant_galois,
+                                const uint64_t *const *giant_evk, const uint64_t *const *pt, uint64_t *out0,
+                                uint64_t *out1, void *ws, void *stream);
+size_t hks_linear_transform_workspace_bytes(const hks_ctx *ctx, uint32_t level, uint32_t n1);
+
 /* EVAL-form automorphism X -> X^galois on nlimbs limbs (prime-independent permutation,
  * SPEC.md:244-252; SURVEY.md reading 15):  out[l][j] = in[l][j'], 2brv(j')+1 = k(2brv(j)+1) mod 2N.
  * in != out required. */

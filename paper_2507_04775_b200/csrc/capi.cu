@@ -622,3 +622,115 @@ extern "C" size_t hks_rotate_hoisted_batch_workspace_bytes(const hks_ctx *c, uin
     const size_t lb = limb_bytes(c), l1 = level + 1, ne = c->ne(level), K = c->np, beta = c->beta(level);
     return (l1 + nct * (beta * ne + 2 * ne) + nct * (2 * K + 2 * l1)) * lb;
 }
+
+// ------------------------------------------------------------------------------------------------
+// BSGS linear transform
+
+namespace {
+// chunks of WS_MAXT terms; chunks after the first accumulate into out
+hks_status wsum_core(const hks_ctx *c, u32 nterm, const uint64_t *const *w, const uint64_t *const *x0,
+                     const uint64_t *const *x1, u32 level, u64 *out0, u64 *out1, cudaStream_t s) {
+    for (u32 j0 = 0; j0 < nterm; j0 += WS_MAXT) {
+        WsumArgs a{};
+        a.nterm = std::min<u32>(WS_MAXT, nterm - j0);
+        for (u32 j = 0; j < a.nterm; j++) {
+            a.w[j] = w[j0 + j];
+            a.x0[j] = x0[j0 + j];
+            a.x1[j] = x1[j0 + j];
+        }
+        a.out0 = out0;
+        a.out1 = out1;
+        a.pc = c->d_pc;
+        a.nlimbs = level + 1;
+        a.log_n = c->log_n;
+        a.accumulate = j0 > 0;
+        hks_status st = launch_pt_wsum(a, s);
+        if (st != HKS_OK) return st;
+    }
+    return HKS_OK;
+}
+}  // namespace
+
+extern "C" hks_status hks_pt_weighted_sum(const hks_ctx *c, uint32_t nterm, const uint64_t *const *w,
+                                          const uint64_t *const *x0, const uint64_t *const *x1, uint32_t level,
+                                          uint64_t *out0, uint64_t *out1, void *stream) {
+    hks_status st = check_ctx(c);
+    if (st != HKS_OK) return st;
+    if (!w || !x0 || !x1 || !out0 || !out1 || nterm == 0) HKS_FAIL(HKS_EINVAL, "pt_weighted_sum: NULL argument / no term");
+    if (level > c->L()) HKS_FAIL(HKS_EINVAL, "pt_weighted_sum: level %u > L", level);
+    const size_t sz = (level + 1) * limb_bytes(c);
+    if (overlap(out0, sz, out1, sz)) HKS_FAIL(HKS_EINVAL, "pt_weighted_sum: outputs overlap");
+    for (u32 j = 0; j < nterm; j++) {
+        if (!w[j] || !x0[j] || !x1[j]) HKS_FAIL(HKS_EINVAL, "pt_weighted_sum: NULL term %u", j);
+        const void *ins[3] = {w[j], x0[j], x1[j]};
+        for (const void *p : ins)
+            if (overlap(p, sz, out0, sz) || overlap(p, sz, out1, sz))
+                HKS_FAIL(HKS_EINVAL, "pt_weighted_sum: an output overlaps term %u", j);
+    }
+    DevGuard g(c->device);
+    return wsum_core(c, nterm, w, x0, x1, level, out0, out1, (cudaStream_t)stream);
+}
+
+extern "C" size_t hks_linear_transform_workspace_bytes(const hks_ctx *c, uint32_t level, uint32_t n1) {
+    if (!c || level > c->L() || n1 == 0) return 0;
+    const size_t lb = limb_bytes(c), l1 = level + 1;
+    const size_t rot = std::max(hks_workspace_bytes(c, HKS_OP_ROTATE_HOISTED, level, n1 > 1 ? n1 - 1 : 1),
+                                hks_workspace_bytes(c, HKS_OP_ROTATE_HOISTED, level, 1));
+    return (2 * (size_t)(n1 - 1) + 4) * l1 * lb + rot;   // baby ciphertexts, inner, rotated inner, rotations
+}
+
+extern "C" hks_status hks_linear_transform(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, uint32_t level,
+                                           uint32_t n1, uint32_t n2, const uint64_t *baby_galois,
+                                           const uint64_t *const *baby_evk, const uint64_t *giant_galois,
+                                           const uint64_t *const *giant_evk, const uint64_t *const *pt,
+                                           uint64_t *out0, uint64_t *out1, void *ws, void *stream) {
+    hks_status st = check_ctx(c);
+    if (st != HKS_OK) return st;
+    if (!c0 || !c1 || !pt || !out0 || !out1 || !ws) HKS_FAIL(HKS_EINVAL, "linear_transform: NULL argument");
+    if (n1 == 0 || n2 == 0 || n1 > 1024 || n2 > 1024) HKS_FAIL(HKS_EINVAL, "linear_transform: n1, n2 must be in [1, 1024]");
+    if (level > c->L()) HKS_FAIL(HKS_EINVAL, "linear_transform: level %u > L", level);
+    if ((n1 > 1 && (!baby_galois || !baby_evk)) || (n2 > 1 && (!giant_galois || !giant_evk)))
+        HKS_FAIL(HKS_EINVAL, "linear_transform: missing rotation keys");
+    for (u32 k = 0; k + 1 < n2; k++)
+        if ((st = check_galois(c, giant_galois[k])) != HKS_OK) return st;
+    for (u32 k = 0; k < n1 * n2; k++)
+        if (!pt[k]) HKS_FAIL(HKS_EINVAL, "linear_transform: NULL diagonal %u", k);
+    const size_t lb = limb_bytes(c), l1 = level + 1, sz = l1 * lb;
+    const size_t wsb = hks_linear_transform_workspace_bytes(c, level, n1);
+    if (overlap(out0, sz, c0, sz) || overlap(out0, sz, c1, sz) || overlap(out1, sz, c0, sz) ||
+        overlap(out1, sz, c1, sz) || overlap(out0, sz, out1, sz) || overlap(out0, sz, ws, wsb) ||
+        overlap(out1, sz, ws, wsb))
+        HKS_FAIL(HKS_EINVAL, "linear_transform: outputs overlap an input or ws");
+    cudaStream_t s = (cudaStream_t)stream;
+    DevGuard g(c->device);
+    u64 *base = (u64 *)ws;
+    const size_t lw = l1 * c->n;   // words per polynomial
+    // ciphertext j (j = 0: the input; j >= 1: baby rotation j) halves
+    std::vector<const u64 *> x0(n1), x1(n1);
+    std::vector<u64 *> b0(n1), b1(n1);
+    x0[0] = c0;
+    x1[0] = c1;
+    for (u32 j = 1; j < n1; j++) {
+        b0[j] = base + (2 * (size_t)(j - 1)) * lw;
+        b1[j] = b0[j] + lw;
+        x0[j] = b0[j];
+        x1[j] = b1[j];
+    }
+    u64 *i0 = base + 2 * (size_t)(n1 - 1) * lw, *i1 = i0 + lw, *r0 = i1 + lw, *r1 = r0 + lw, *rws = r1 + lw;
+    // baby steps: one ModUp shared by the n1 - 1 rotations (hoisted)
+    if (n1 > 1 && (st = hks_rotate_hoisted(c, c0, c1, level, n1 - 1, baby_galois, baby_evk, b0.data() + 1,
+                                           b1.data() + 1, rws, stream)) != HKS_OK)
+        return st;
+    // giant steps: I_i = sum_j pt[i n1 + j] ct_j (fused weighted sum), out += Rot_{g_i}(I_i)
+    for (u32 i = 0; i < n2; i++) {
+        u64 *t0 = i == 0 ? out0 : i0, *t1 = i == 0 ? out1 : i1;
+        if ((st = wsum_core(c, n1, pt + (size_t)i * n1, x0.data(), x1.data(), level, t0, t1, s)) != HKS_OK) return st;
+        if (i == 0) continue;
+        u64 *o0 = r0, *o1 = r1;
+        if ((st = hks_rotate_hoisted(c, i0, i1, level, 1, giant_galois + (i - 1), giant_evk + (i - 1), &o0, &o1, rws,
+                                     stream)) != HKS_OK)
+            return st;
+        if ((st = launch_add_ct(r0, r1, out0, out1, level + 1, c->log_n, c->d_pc, s)) != HKS_OK) return st;
+    }
+    return HKS_OK;
+}

@@ -163,6 +163,24 @@ struct FusedKipArgs {
 
 hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s);
 
+// ----------------------------------------------------------------------------------------------
+// Fused plaintext-weighted sum of ciphertexts ("weighed sum ... 4n-2 down to n+1 memory
+// operations"): out_p[t] = (accumulate ? out_p[t] : 0) + sum_j w_j[t] * x_{j,p}[t] (mod q_t), limbs
+// t = 0..nlimbs-1 of the chain, one 128-bit 30-bit-split accumulation and one reduction per output.
+#define WS_MAXT 16
+struct WsumArgs {
+    const u64 *w[WS_MAXT];
+    const u64 *x0[WS_MAXT];
+    const u64 *x1[WS_MAXT];
+    u64 *out0, *out1;
+    const PrimeConst *pc;
+    u32 nterm, nlimbs, log_n, accumulate;
+};
+hks_status launch_pt_wsum(const WsumArgs &a, cudaStream_t s);
+// out_p += r_p (mod q_t) for p = 0, 1 over nlimbs chain limbs (BSGS giant-step accumulation)
+hks_status launch_add_ct(const u64 *r0, const u64 *r1, u64 *out0, u64 *out1, u32 nlimbs, u32 log_n,
+                         const PrimeConst *pc, cudaStream_t s);
+
 // One output limb of the fused row pass + key product: its prime, key slot, acc slot, and per digit j
 // the source slot (ext pass-1 output, or FK_DIRECT | c1 slot for the own-digit limb).
 struct KipItem {
@@ -213,7 +231,7 @@ struct hks_ctx {
 // ----------------------------------------------------------------------------------------------
 // diagnostics (prof.cu): launch counter + optional per-launch event pair tagged with a kernel class
 enum KCls { K_NTT_FWD_COLS = 0, K_NTT_FWD_ROWS, K_NTT_FWD_ROWS_MODDOWN, K_NTT_INV_ROWS, K_NTT_INV_COLS, K_BCONV,
-            K_KIP, K_AUTOMORPH, K_NTT_ROWS_KIP, K_NCLS };
+            K_KIP, K_AUTOMORPH, K_NTT_ROWS_KIP, K_WSUM, K_ADD, K_NCLS };
 struct ProfScope {
     int cls;
     cudaStream_t s;

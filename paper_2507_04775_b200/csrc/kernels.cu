@@ -466,3 +466,83 @@ hks_status launch_automorph(const u64 *in, u64 *out, u32 nlimbs, u32 log_n, u64 
     ps.done(2.0 * nlimbs * (double)N * 8.0);
     return HKS_OK;
 }
+
+// ------------------------------------------------------------------------------------------------
+// Fused plaintext-weighted sum (BSGS inner products): each thread owns two
+// coefficients of one limb for both ciphertext halves; every weight word is loaded once and used
+// for both halves.
+__global__ void __launch_bounds__(256) k_pt_wsum(const __grid_constant__ WsumArgs A) {
+    const size_t N = (size_t)1 << A.log_n;
+    const u32 t = blockIdx.y;
+    const size_t x = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    if (x >= N) return;
+    const size_t o = (size_t)t * N + x;
+    const PrimeConst pc = A.pc[t];
+    Acc30 a0[2], a1[2];
+    acc_zero(a0[0]); acc_zero(a0[1]);
+    acc_zero(a1[0]); acc_zero(a1[1]);
+    if (A.accumulate) {   // the running value enters as one more term of weight 1
+        const ulonglong2 v0 = *reinterpret_cast<const ulonglong2 *>(A.out0 + o);
+        const ulonglong2 v1 = *reinterpret_cast<const ulonglong2 *>(A.out1 + o);
+        u32 l, h;
+        split30(v0.x, l, h); a0[0].s0 = l; a0[0].s1a = h;
+        split30(v0.y, l, h); a0[1].s0 = l; a0[1].s1a = h;
+        split30(v1.x, l, h); a1[0].s0 = l; a1[0].s1a = h;
+        split30(v1.y, l, h); a1[1].s0 = l; a1[1].s1a = h;
+    }
+    for (u32 j = 0; j < A.nterm; j++) {
+        const ulonglong2 w = *reinterpret_cast<const ulonglong2 *>(A.w[j] + o);
+        const ulonglong2 p = *reinterpret_cast<const ulonglong2 *>(A.x0[j] + o);
+        const ulonglong2 q = *reinterpret_cast<const ulonglong2 *>(A.x1[j] + o);
+        u32 wl, wh, yl, yh;
+        split30(w.x, wl, wh);
+        split30(p.x, yl, yh); acc_mac(a0[0], yl, yh, wl, wh);
+        split30(q.x, yl, yh); acc_mac(a1[0], yl, yh, wl, wh);
+        split30(w.y, wl, wh);
+        split30(p.y, yl, yh); acc_mac(a0[1], yl, yh, wl, wh);
+        split30(q.y, yl, yh); acc_mac(a1[1], yl, yh, wl, wh);
+    }
+    *reinterpret_cast<ulonglong2 *>(A.out0 + o) = make_ulonglong2(acc_reduce(a0[0], pc), acc_reduce(a0[1], pc));
+    *reinterpret_cast<ulonglong2 *>(A.out1 + o) = make_ulonglong2(acc_reduce(a1[0], pc), acc_reduce(a1[1], pc));
+}
+
+hks_status launch_pt_wsum(const WsumArgs &a, cudaStream_t s) {
+    const u32 threads = 256;
+    const size_t N = (size_t)1 << a.log_n;
+    dim3 grid((u32)((N / 2 + threads - 1) / threads), a.nlimbs);
+    ProfScope ps(K_WSUM, s);
+    k_pt_wsum<<<grid, threads, 0, s>>>(a);
+    HKS_CHECK_LAUNCH();
+    ps.done((3.0 * a.nterm + 2.0 + (a.accumulate ? 2.0 : 0.0)) * a.nlimbs * (double)N * 8.0,
+            (double)a.nterm * 2.0 * a.nlimbs * (double)N * 4.0);
+    return HKS_OK;
+}
+
+__global__ void __launch_bounds__(256) k_add_ct(const u64 *__restrict__ r0, const u64 *__restrict__ r1,
+                                                u64 *__restrict__ out0, u64 *__restrict__ out1, u32 log_n,
+                                                const PrimeConst *__restrict__ pcs) {
+    const size_t N = (size_t)1 << log_n;
+    const u32 t = blockIdx.y;
+    const size_t x = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    if (x >= N) return;
+    const size_t o = (size_t)t * N + x;
+    const u64 p = pcs[t].p;
+    const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(r0 + o), b = *reinterpret_cast<const ulonglong2 *>(r1 + o);
+    ulonglong2 u = *reinterpret_cast<const ulonglong2 *>(out0 + o), v = *reinterpret_cast<const ulonglong2 *>(out1 + o);
+    u.x = csub(u.x + a.x, p); u.y = csub(u.y + a.y, p);
+    v.x = csub(v.x + b.x, p); v.y = csub(v.y + b.y, p);
+    *reinterpret_cast<ulonglong2 *>(out0 + o) = u;
+    *reinterpret_cast<ulonglong2 *>(out1 + o) = v;
+}
+
+hks_status launch_add_ct(const u64 *r0, const u64 *r1, u64 *out0, u64 *out1, u32 nlimbs, u32 log_n,
+                         const PrimeConst *pc, cudaStream_t s) {
+    const u32 threads = 256;
+    const size_t N = (size_t)1 << log_n;
+    dim3 grid((u32)((N / 2 + threads - 1) / threads), nlimbs);
+    ProfScope ps(K_ADD, s);
+    k_add_ct<<<grid, threads, 0, s>>>(r0, r1, out0, out1, log_n, pc);
+    HKS_CHECK_LAUNCH();
+    ps.done(6.0 * nlimbs * (double)N * 8.0, 0.0);
+    return HKS_OK;
+}

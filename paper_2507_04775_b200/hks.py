@@ -22,6 +22,7 @@ MAX_DIGITS = 64
 EXPORTS = ("hks_last_error", "hks_ctx_create", "hks_ctx_destroy", "hks_ctx_query", "hks_ctx_psi",
            "hks_workspace_bytes", "hks_ntt_fwd", "hks_ntt_inv", "hks_bconv", "hks_modup",
            "hks_ksk_inner_product", "hks_moddown", "hks_keyswitch", "hks_relinearize", "hks_hmult", "hks_rescale",
+           "hks_pt_weighted_sum", "hks_linear_transform", "hks_linear_transform_workspace_bytes",
            "hks_automorph",
            "hks_rotate_hoisted", "hks_rotate_hoisted_batch", "hks_rotate_hoisted_batch_workspace_bytes",
            "hks_launch_count", "hks_prof_enable", "hks_prof_read", "hks_shard_query", "hks_shard_workspace_bytes",
@@ -85,6 +86,12 @@ def lib() -> ctypes.CDLL:
         L.hks_relinearize.argtypes = [_vp, _vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp]
         L.hks_hmult.argtypes = [_vp, _vp, _vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp]
         L.hks_rescale.argtypes = [_vp, _vp, _u32, _u32, _vp, _vp, _vp]
+        _vpp = ctypes.POINTER(_vp)
+        L.hks_pt_weighted_sum.argtypes = [_vp, _u32, _vpp, _vpp, _vpp, _u32, _vp, _vp, _vp]
+        L.hks_linear_transform.argtypes = [_vp, _vp, _vp, _u32, _u32, _u32, ctypes.POINTER(_u64), _vpp,
+                                           ctypes.POINTER(_u64), _vpp, _vpp, _vp, _vp, _vp, _vp]
+        L.hks_linear_transform_workspace_bytes.restype = ctypes.c_size_t
+        L.hks_linear_transform_workspace_bytes.argtypes = [_vp, _u32, _u32]
         L.hks_rotate_hoisted.argtypes = [_vp, _vp, _vp, _u32, _u32, ctypes.POINTER(_u64), ctypes.POINTER(_vp),
                                          ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp]
         L.hks_launch_count.restype = ctypes.c_uint64
@@ -235,6 +242,29 @@ def hmult(ctx: Context, a0, a1, b0, b1, level: int, evk, out0, out1, ws, stream=
 
 def rescale(ctx: Context, x, npoly: int, level: int, out, ws, stream=None):
     _check(lib().hks_rescale(ctx.handle, _ptr(x), npoly, level, _ptr(out), _ptr(ws), _stream(stream)), "hks_rescale")
+
+
+def pt_weighted_sum(ctx: Context, w, x0, x1, level: int, out0, out1, stream=None):
+    n = len(w)
+    arr = lambda vs: (_vp * n)(*[_ptr(v) for v in vs])
+    _check(lib().hks_pt_weighted_sum(ctx.handle, n, arr(w), arr(x0), arr(x1), level, _ptr(out0), _ptr(out1),
+                                     _stream(stream)), "hks_pt_weighted_sum")
+
+
+def linear_transform_workspace(ctx: Context, level: int, n1: int):
+    import torch
+    nbytes = int(lib().hks_linear_transform_workspace_bytes(ctx.handle, level, n1))
+    return torch.empty(max(nbytes // 8, 1), dtype=torch.uint64, device=f"cuda:{ctx.device}")
+
+
+def linear_transform(ctx: Context, c0, c1, level: int, n1: int, n2: int, baby_galois, baby_evks, giant_galois,
+                     giant_evks, pts, out0, out1, ws, stream=None):
+    """pts: n1*n2 diagonals (index i*n1 + j); baby lists n1-1 entries, giant lists n2-1 entries."""
+    arr = lambda vs: (_vp * max(1, len(vs)))(*[_ptr(v) for v in vs])
+    gal = lambda vs: (_u64 * max(1, len(vs)))(*[int(v) for v in vs])
+    _check(lib().hks_linear_transform(ctx.handle, _ptr(c0), _ptr(c1), level, n1, n2, gal(baby_galois), arr(baby_evks),
+                                      gal(giant_galois), arr(giant_evks), arr(pts), _ptr(out0), _ptr(out1), _ptr(ws),
+                                      _stream(stream)), "hks_linear_transform")
 
 
 def automorph(ctx: Context, x, nlimbs: int, galois: int, out, stream=None):

@@ -459,3 +459,42 @@ def test_hmult_rejects_aliasing(orc):
     with pytest.raises(H.HksError) as e:
         H.hmult(ctx, a, a, a, a, level, to_dev(evk), a, out1, ws)    # out0 aliases an input
     assert e.value.status == 1
+
+
+# ------------------------------------------------------------------ BSGS linear transform (NEXT-2)
+
+@pytest.mark.parametrize("name,level,nterm", [("T12", 6, 5), ("T12", 3, 21), ("C2", 29, 8)])
+def test_pt_weighted_sum_parity(orc, name, level, nterm):
+    """fused weighted sum, incl. > 16 terms (second pass accumulates into the outputs)."""
+    cfg, ctx, o = ctxs(orc, name)
+    g = S.rng(cfg.seed + 71 + nterm)
+    qs = o.q[: level + 1]
+    w = [edge_limbs(qs, o.n, g) for _ in range(nterm)]
+    x0 = [S.uniform_limbs(g, qs, o.n) for _ in range(nterm)]
+    x1 = [edge_limbs(qs, o.n, g) for _ in range(nterm)]
+    out0, out1 = empty_dev(x0[0].shape), empty_dev(x0[0].shape)
+    H.pt_weighted_sum(ctx, [to_dev(v) for v in w], [to_dev(v) for v in x0], [to_dev(v) for v in x1], level, out0, out1)
+    w0, w1 = o.pt_wsum(w, x0, x1, level)
+    assert (to_host(out0) == w0).all() and (to_host(out1) == w1).all()
+
+
+@pytest.mark.parametrize("name,level,n1,n2", [("T12", 6, 3, 3), ("T12", 4, 4, 1), ("T12", 5, 1, 3), ("T12", 2, 1, 1),
+                                              ("C2", 29, 4, 4)])
+def test_linear_transform_parity(orc, name, level, n1, n2):
+    """BSGS: hoisted baby rotations, fused weighted sums, one rotation per giant step; bit-exact."""
+    cfg, ctx, o = ctxs(orc, name)
+    keys = Keys(o, cfg.seed + 81)
+    g = S.rng(cfg.seed + 82)
+    bgal = [S.galois_rot(j, cfg.log_n) for j in range(1, n1)]
+    ggal = [S.galois_rot(i * n1, cfg.log_n) for i in range(1, n2)]
+    bk = [keys.rot(k) for k in bgal]
+    gk = [keys.rot(k) for k in ggal]
+    qs = o.q[: level + 1]
+    c0, c1 = S.uniform_limbs(g, qs, o.n), edge_limbs(qs, o.n, g)
+    pts = [S.uniform_limbs(g, qs, o.n) for _ in range(n1 * n2)]
+    out0, out1 = empty_dev(c0.shape), empty_dev(c0.shape)
+    ws = H.linear_transform_workspace(ctx, level, n1)
+    H.linear_transform(ctx, to_dev(c0), to_dev(c1), level, n1, n2, bgal, [to_dev(k) for k in bk], ggal,
+                       [to_dev(k) for k in gk], [to_dev(p) for p in pts], out0, out1, ws)
+    w0, w1 = o.lintrans(c0, c1, level, n1, n2, bgal, bk, ggal, gk, pts)
+    assert (to_host(out0) == w0).all() and (to_host(out1) == w1).all()
