@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/hks.h"
@@ -241,6 +242,30 @@ struct ProfScope {
     // product; 7 wide-equivalents per Shoup butterfly: 3 for the quotient, 2 + 4/2 for the remainder)
     void done(double algorithmic_bytes, double algorithmic_muls = 0);
 };
+
+// ----------------------------------------------------------------------------------------------
+// Programmatic dependent launch (sm_90+): every kernel lets its stream successor launch as soon as all
+// of its CTAs are running (pdl_trigger) and waits for its predecessor's completion and memory
+// (pdl_wait) before touching anything the predecessor wrote, so a kernel's launch, CTA rasterisation
+// and constant-table prologue overlap the previous kernel's tail.  HKS_PDL=0 disables the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t hks_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ----------------------------------------------------------------------------------------------
 // error plumbing

@@ -30,6 +30,8 @@ static bool getenv_fp_enabled() {
 #define BC_TCH 10
 template <int NSRC, bool PRESCALE, bool LAZY, int CPT>
 __global__ void __launch_bounds__(256, CPT == 1 ? 5 : 3) k_bconv(const __grid_constant__ BconvArgs A) {
+    pdl_trigger();
+    pdl_wait();
     const BconvGroup &G = A.g[blockIdx.y];
     const u32 u0 = blockIdx.z * BC_TCH;
     if (u0 >= G.ndst) return;
@@ -94,6 +96,7 @@ __global__ void __launch_bounds__(256, CPT == 1 ? 5 : 3) k_bconv(const __grid_co
 // Karatsuba variant (3 IMAD.WIDE per MAC instead of 4), one coefficient per thread, NSRC <= 12.
 template <int NSRC, bool LAZY>
 __global__ void __launch_bounds__(256, 3) k_bconv_kara(const __grid_constant__ BconvArgs A) {
+    pdl_trigger();
     const BconvGroup &G = A.g[blockIdx.y];
     const u32 u0 = blockIdx.z * BC_TCH;
     if (u0 >= G.ndst) return;
@@ -107,6 +110,7 @@ __global__ void __launch_bounds__(256, 3) k_bconv_kara(const __grid_constant__ B
     }
     for (u32 u = threadIdx.x; u < nt; u += blockDim.x) spc[u] = A.pc[G.dst_prime[u0 + u]];
     __syncthreads();
+    pdl_wait();   // ctx tables above are immutable; the inputs below come from the predecessor
 
     const size_t N = (size_t)1 << A.log_n;
     const size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -142,9 +146,9 @@ static void bconv_kara_go(const BconvArgs &a, cudaStream_t s) {
     dim3 grid((u32)((N + threads - 1) / threads), a.ngroups, (maxdst + BC_TCH - 1) / BC_TCH);
     ProfScope ps(K_BCONV, s);
     if (a.lazy_out)
-        k_bconv_kara<NSRC, true><<<grid, threads, 0, s>>>(a);
+        (void)hks_launch(k_bconv_kara<NSRC, true>, grid, dim3(threads), 0, s, a);
     else
-        k_bconv_kara<NSRC, false><<<grid, threads, 0, s>>>(a);
+        (void)hks_launch(k_bconv_kara<NSRC, false>, grid, dim3(threads), 0, s, a);
     double words = 0, macs = 0;
     for (u32 g = 0; g < a.ngroups; g++) {
         words += a.g[g].nsrc + a.g[g].ndst;
@@ -168,6 +172,7 @@ static bool getenv_kara_enabled() {
 // is the same integer X = sum_i y_i [qhat_i]_t, so the output is bit-identical to k_bconv.
 template <int NSRC, int NFP, bool LAZY>
 __global__ void __launch_bounds__(256) k_bconv_fp(const __grid_constant__ BconvArgs A) {
+    pdl_trigger();
     constexpr int NINT = NSRC - NFP;
     const BconvGroup &G = A.g[blockIdx.y];
     const u32 u0 = blockIdx.z * BC_TCH;
@@ -190,6 +195,7 @@ __global__ void __launch_bounds__(256) k_bconv_fp(const __grid_constant__ BconvA
     }
     for (u32 u = threadIdx.x; u < nt; u += blockDim.x) spc[u] = A.pc[G.dst_prime[u0 + u]];
     __syncthreads();
+    pdl_wait();   // ctx tables above are immutable; the inputs below come from the predecessor
 
     const size_t N = (size_t)1 << A.log_n;
     const size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -242,9 +248,9 @@ static void bconv_fp_go(const BconvArgs &a, cudaStream_t s) {
     dim3 grid((u32)((N + threads - 1) / threads), a.ngroups, (maxdst + BC_TCH - 1) / BC_TCH);
     ProfScope ps(K_BCONV, s);
     if (a.lazy_out)
-        k_bconv_fp<NSRC, NFP, true><<<grid, threads, 0, s>>>(a);
+        (void)hks_launch(k_bconv_fp<NSRC, NFP, true>, grid, dim3(threads), 0, s, a);
     else
-        k_bconv_fp<NSRC, NFP, false><<<grid, threads, 0, s>>>(a);
+        (void)hks_launch(k_bconv_fp<NSRC, NFP, false>, grid, dim3(threads), 0, s, a);
     double words = 0, macs = 0;
     for (u32 g = 0; g < a.ngroups; g++) {
         words += a.g[g].nsrc + a.g[g].ndst;
@@ -266,11 +272,11 @@ static void bconv_go(const BconvArgs &a, cudaStream_t s) {
     dim3 grid((u32)((N / CPT + threads - 1) / threads), a.ngroups, (maxdst + BC_TCH - 1) / BC_TCH);
     ProfScope ps(K_BCONV, s);
     if (a.prescale)
-        k_bconv<NSRC, true, false, CPT><<<grid, threads, 0, s>>>(a);
+        (void)hks_launch(k_bconv<NSRC, true, false, CPT>, grid, dim3(threads), 0, s, a);
     else if (a.lazy_out)
-        k_bconv<NSRC, false, true, CPT><<<grid, threads, 0, s>>>(a);
+        (void)hks_launch(k_bconv<NSRC, false, true, CPT>, grid, dim3(threads), 0, s, a);
     else
-        k_bconv<NSRC, false, false, CPT><<<grid, threads, 0, s>>>(a);
+        (void)hks_launch(k_bconv<NSRC, false, false, CPT>, grid, dim3(threads), 0, s, a);
     double words = 0, macs = 0;
     for (u32 g = 0; g < a.ngroups; g++) {
         words += a.g[g].nsrc + a.g[g].ndst;
@@ -323,6 +329,8 @@ hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
 // with D_j optionally read through the EVAL automorphism (hoisted rotation, reading 14).
 // grid.x: coefficient blocks, grid.y: extended limb t.
 __global__ void __launch_bounds__(256) k_kip(const __grid_constant__ KipArgs A) {
+    pdl_trigger();
+    pdl_wait();
     const size_t N = (size_t)1 << A.log_n;
     const u32 t = blockIdx.y;
     const size_t x0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
@@ -373,7 +381,7 @@ hks_status launch_kip(const KipArgs &a, cudaStream_t s) {
     const size_t N = (size_t)1 << a.log_n;
     dim3 grid((u32)((N / 2 + threads - 1) / threads), a.ne);
     ProfScope ps(K_KIP, s);
-    k_kip<<<grid, threads, 0, s>>>(a);
+    (void)hks_launch(k_kip, grid, dim3(threads), 0, s, a);
     HKS_CHECK_LAUNCH();
     ps.done((3.0 * a.beta + 2.0) * a.ne * (double)N * 8.0,    // D_j + (b_j, a_j) read, acc0/acc1 written
             (double)a.ne * a.beta * 2.0 * (double)N * 4.0);
@@ -383,6 +391,8 @@ hks_status launch_kip(const KipArgs &a, cudaStream_t s) {
 // Multi-ciphertext key inner product: the key words of (t, x) are loaded once and reused for all nct
 // ciphertexts of the batch (amortising the dominant key stream, SURVEY.md §7 "key streaming").
 __global__ void __launch_bounds__(256) k_kip_multi(const __grid_constant__ KipMultiArgs A) {
+    pdl_trigger();
+    pdl_wait();
     const size_t N = (size_t)1 << A.log_n;
     const u32 t = blockIdx.y;
     const size_t x0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
@@ -436,7 +446,7 @@ hks_status launch_kip_multi(const KipMultiArgs &a, cudaStream_t s) {
     const size_t N = (size_t)1 << a.log_n;
     dim3 grid((u32)((N / 2 + threads - 1) / threads), a.ne);
     ProfScope ps(K_KIP, s);
-    k_kip_multi<<<grid, threads, 0, s>>>(a);
+    (void)hks_launch(k_kip_multi, grid, dim3(threads), 0, s, a);
     HKS_CHECK_LAUNCH();
     ps.done((2.0 * a.beta + a.nct * (a.beta + 2.0)) * a.ne * (double)N * 8.0,
             (double)a.nct * a.ne * a.beta * 2.0 * (double)N * 4.0);
@@ -449,6 +459,8 @@ hks_status launch_kip_multi(const KipMultiArgs &a, cudaStream_t s) {
 // inside one 256-byte segment.
 __global__ void __launch_bounds__(256) k_automorph(const u64 *__restrict__ in, u64 *__restrict__ out,
                                                   u32 log_n, u64 galois) {
+    pdl_trigger();
+    pdl_wait();
     const size_t N = (size_t)1 << log_n;
     const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
     const size_t l = blockIdx.y;
@@ -461,7 +473,7 @@ hks_status launch_automorph(const u64 *in, u64 *out, u32 nlimbs, u32 log_n, u64 
     const size_t N = (size_t)1 << log_n;
     dim3 grid((u32)((N + threads - 1) / threads), nlimbs);
     ProfScope ps(K_AUTOMORPH, s);
-    k_automorph<<<grid, threads, 0, s>>>(in, out, log_n, galois);
+    (void)hks_launch(k_automorph, grid, dim3(threads), 0, s, in, out, log_n, galois);
     HKS_CHECK_LAUNCH();
     ps.done(2.0 * nlimbs * (double)N * 8.0);
     return HKS_OK;
@@ -472,6 +484,8 @@ hks_status launch_automorph(const u64 *in, u64 *out, u32 nlimbs, u32 log_n, u64 
 // coefficients of one limb for both ciphertext halves; every weight word is loaded once and used
 // for both halves.
 __global__ void __launch_bounds__(256) k_pt_wsum(const __grid_constant__ WsumArgs A) {
+    pdl_trigger();
+    pdl_wait();
     const size_t N = (size_t)1 << A.log_n;
     const u32 t = blockIdx.y;
     const size_t x = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
@@ -511,7 +525,7 @@ hks_status launch_pt_wsum(const WsumArgs &a, cudaStream_t s) {
     const size_t N = (size_t)1 << a.log_n;
     dim3 grid((u32)((N / 2 + threads - 1) / threads), a.nlimbs);
     ProfScope ps(K_WSUM, s);
-    k_pt_wsum<<<grid, threads, 0, s>>>(a);
+    (void)hks_launch(k_pt_wsum, grid, dim3(threads), 0, s, a);
     HKS_CHECK_LAUNCH();
     ps.done((3.0 * a.nterm + 2.0 + (a.accumulate ? 2.0 : 0.0)) * a.nlimbs * (double)N * 8.0,
             (double)a.nterm * 2.0 * a.nlimbs * (double)N * 4.0);
@@ -521,6 +535,8 @@ hks_status launch_pt_wsum(const WsumArgs &a, cudaStream_t s) {
 __global__ void __launch_bounds__(256) k_add_ct(const u64 *__restrict__ r0, const u64 *__restrict__ r1,
                                                 u64 *__restrict__ out0, u64 *__restrict__ out1, u32 log_n,
                                                 const PrimeConst *__restrict__ pcs) {
+    pdl_trigger();
+    pdl_wait();
     const size_t N = (size_t)1 << log_n;
     const u32 t = blockIdx.y;
     const size_t x = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
@@ -541,7 +557,7 @@ hks_status launch_add_ct(const u64 *r0, const u64 *r1, u64 *out0, u64 *out1, u32
     const size_t N = (size_t)1 << log_n;
     dim3 grid((u32)((N / 2 + threads - 1) / threads), nlimbs);
     ProfScope ps(K_ADD, s);
-    k_add_ct<<<grid, threads, 0, s>>>(r0, r1, out0, out1, log_n, pc);
+    (void)hks_launch(k_add_ct, grid, dim3(threads), 0, s, r0, r1, out0, out1, log_n, pc);
     HKS_CHECK_LAUNCH();
     ps.done(6.0 * nlimbs * (double)N * 8.0, 0.0);
     return HKS_OK;

@@ -283,6 +283,8 @@ __global__ void __launch_bounds__((1 << LOGNB) << (LOGN - LOGE),
                                   (((1 << LOGNB) << (LOGN - LOGE)) >= 512) ? 2 : HKS_NTT_MINB)
 k_ntt(const __grid_constant__ NttArgs A) {
     extern __shared__ __align__(16) u64 sm[];
+    pdl_trigger();
+    pdl_wait();
     const u32 b = blockIdx.x / A.tiles;
     ntt_tile<LOGN, LOGE, LOGNB, LOGC, COLS, FWD, EPI>(A, b, blockIdx.x - b * A.tiles, sm);
 }
@@ -303,7 +305,7 @@ static hks_status go(NttArgs &a, cudaStream_t s) {
     const int cls = FWD ? (COLS ? K_NTT_FWD_COLS : ((EPI == EPI_MODDOWN || EPI == EPI_MDTENSOR) ? K_NTT_FWD_ROWS_MODDOWN : K_NTT_FWD_ROWS))
                         : (COLS ? K_NTT_INV_COLS : K_NTT_INV_ROWS);
     ProfScope ps(cls, s);
-    kern<<<a.nlimbs * a.tiles, threads, smem, s>>>(a);
+    (void)hks_launch(kern, dim3(a.nlimbs * a.tiles), dim3(threads), smem, s, a);
     HKS_CHECK_LAUNCH();
     // algorithmic bytes: each limb read once and written once (+ ModDown operands acc, c0)
     double words = 2.0 * a.nlimbs;
@@ -570,6 +572,8 @@ template <int LOGN, int LOGE, int LOGNB, int NTR, int NDIG>
 __global__ void __launch_bounds__(NTR * ((1 << LOGNB) << (LOGN - LOGE)),
                                   kip_minb(NTR * ((1 << LOGNB) << (LOGN - LOGE))))
 k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
+    pdl_trigger();
+    pdl_wait();
     constexpr int n = 1 << LOGN;
     constexpr int E = 1 << LOGE;
     constexpr int NB = 1 << LOGNB;
@@ -804,7 +808,7 @@ static hks_status go_kip(FusedKipArgs &a, cudaStream_t s) {
     }
     a.tiles = (1u << a.log_r) >> LOGNB;
     ProfScope ps(K_NTT_ROWS_KIP, s);
-    kern<<<a.nu * a.tiles, threads, smem, s>>>(a);
+    (void)hks_launch(kern, dim3(a.nu * a.tiles), dim3(threads), smem, s, a);
     HKS_CHECK_LAUNCH();
     // algorithmic words: D read once (pass-1 output or c1), key 2 limbs per (u, j), acc 2 limbs per u
     const double nn = (double)(1ull << a.log_n);

@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // prof.cu -- launch counter and optional per-kernel CUDA-event timer (include/hks.h diagnostics).
 #include <string.h>
 
@@ -94,4 +95,12 @@ extern "C" int hks_prof_read(hks_prof_entry *out, int max) {
         k++;
     }
     return k;
+}
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("HKS_PDL");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
 }
