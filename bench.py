@@ -630,9 +630,23 @@ def main():
             def rs(i):
                 H.rescale(ctx, xs[i % len(xs)], 2, level, rout, wsr, sid)
 
+            # throughput mode: 8 ciphertexts relinearised with ONE key per call (key words read once
+            # for the batch; hks_rotate_hoisted_batch with Galois element 1 = KeySwitch)
+            NBT = 8
+            bc0 = [sets[i % len(sets)]["c0"] for i in range(NBT)]
+            bc1 = [sets[i % len(sets)]["c1"] for i in range(NBT)]
+            bo0 = [torch.empty_like(bc0[0]) for _ in range(NBT)]
+            bo1 = [torch.empty_like(bc0[0]) for _ in range(NBT)]
+            wsb = H.rotate_hoisted_batch_workspace(ctx, NBT, level)
+
+            def kb(i):
+                H.rotate_hoisted_batch(ctx, bc0, bc1, level, [1], [sets[i % len(sets)]["evk"]], bo0, bo1, wsb, sid)
+
             for name, fn, it, nbytes in (
                     ("hmult", hm, 50, (6 * (level + 1) + 2 * cfg.beta(level) * (level + 1 + cfg.K)) * cfg.n * 8),
-                    ("rescale", rs, 200, (2 * (level + 1) + 2 * level) * cfg.n * 8)):
+                    ("rescale", rs, 200, (2 * (level + 1) + 2 * level) * cfg.n * 8),
+                    ("keyswitch_batch8_shared_key", kb, 20,
+                     (NBT * 4 * (level + 1) + 2 * cfg.beta(level) * (level + 1 + cfg.K)) * cfg.n * 8)):
                 for i in range(3):
                     fn(i)
                 torch.cuda.synchronize()
@@ -645,8 +659,9 @@ def main():
                 t = e0.elapsed_time(e1) / it
                 ops[name] = {"us": 1e3 * t, "per_s": 1e3 / t, "alg_bytes": nbytes,
                              "hbm_frac": nbytes / (t * 1e-3) / 1e9 / hbm_peak}
+            ops["keyswitch_batch8_shared_key"]["keyswitch_per_s"] = NBT * ops["keyswitch_batch8_shared_key"]["per_s"]
             extra["ops"] = ops
-            del xs, wsh, wsr
+            del xs, wsh, wsr, wsb, bo0, bo1
 
         if hasattr(wl, "ops"):
             def timeit(fn, it):

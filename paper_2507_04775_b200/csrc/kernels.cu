@@ -27,7 +27,10 @@ static bool getenv_fp_enabled() {
 // grid.x: coefficient blocks (2 coefficients / thread), grid.y: group (digit or polynomial),
 // grid.z: chunk of BC_TCH targets.  LAZY: outputs in [0, 8t) for a consumer that accepts the lazy
 // range (the forward NTT); otherwise canonical.
-#define BC_TCH 10
+#ifndef HKS_BC_TCH
+#define HKS_BC_TCH 10
+#endif
+#define BC_TCH HKS_BC_TCH
 template <int NSRC, bool PRESCALE, bool LAZY, int CPT>
 __global__ void __launch_bounds__(256, CPT == 1 ? 5 : 3) k_bconv(const __grid_constant__ BconvArgs A) {
     pdl_trigger();

@@ -498,3 +498,22 @@ def test_linear_transform_parity(orc, name, level, n1, n2):
                        [to_dev(k) for k in gk], [to_dev(p) for p in pts], out0, out1, ws)
     w0, w1 = o.lintrans(c0, c1, level, n1, n2, bgal, bk, ggal, gk, pts)
     assert (to_host(out0) == w0).all() and (to_host(out1) == w1).all()
+
+
+def test_keyswitch_batch_shared_key_parity(orc):
+    """a batch of ciphertexts relinearised with one key = hks_rotate_hoisted_batch with Galois 1 (the
+    identity): each output is bit-exactly the oracle's single-ciphertext KeySwitch."""
+    cfg, ctx, o = ctxs(orc, "C2")
+    keys, evk = relin_key(o, "C2")
+    level, nct = 29, 3
+    g = S.rng(91)
+    c0s = [S.uniform_limbs(g, o.q[: level + 1], o.n) for _ in range(nct)]
+    c1s = [edge_limbs(o.q[: level + 1], o.n, g) for _ in range(nct)]
+    outs0 = [empty_dev(c0s[0].shape) for _ in range(nct)]
+    outs1 = [empty_dev(c0s[0].shape) for _ in range(nct)]
+    ws = H.rotate_hoisted_batch_workspace(ctx, nct, level)
+    H.rotate_hoisted_batch(ctx, [to_dev(c) for c in c0s], [to_dev(c) for c in c1s], level, [1], [to_dev(evk)],
+                           outs0, outs1, ws)
+    for i in range(nct):
+        w0, w1 = o.keyswitch(c0s[i], c1s[i], evk, level)
+        assert (to_host(outs0[i]) == w0).all() and (to_host(outs1[i]) == w1).all(), i
