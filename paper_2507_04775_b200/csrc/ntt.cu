@@ -347,15 +347,34 @@ static hks_status dispatch(NttDir dir, bool cols, int epi, NttArgs &a, cudaStrea
 // Per ring size: sub-transform shapes (log length, log elements per thread, log sub-transforms per
 // CTA) of the column pass (length R) and the row pass (length C).  Batches too small to fill two
 // waves of 256-thread CTAs use radix-8 rounds (E = 8, twice the warps per tile) at N = 2^16 / 2^17.
+// N = 2^16 pass shapes (log length, log elements per thread, log sub-transforms per CTA) x (cols, rows);
+// experiment presets selected with -DHKS_D16_BIG_SEL / -DHKS_D16_SMALL_SEL (nvcc splits -D values at commas)
+#if defined(HKS_D16_BIG_SEL) && HKS_D16_BIG_SEL == 1
+#define HKS_D16_BIG 8, 5, 4, 8, 5, 4
+#elif defined(HKS_D16_BIG_SEL) && HKS_D16_BIG_SEL == 2
+#define HKS_D16_BIG 8, 4, 3, 8, 4, 3
+#else
+#define HKS_D16_BIG 8, 4, 4, 8, 4, 4     // large batches: radix-16 rounds, 16 sub-transforms per CTA
+#endif
+#if defined(HKS_D16_SMALL_SEL) && HKS_D16_SMALL_SEL == 1
+#define HKS_D16_SMALL 8, 4, 3, 8, 4, 3
+#elif defined(HKS_D16_SMALL_SEL) && HKS_D16_SMALL_SEL == 2
+#define HKS_D16_SMALL 8, 3, 3, 8, 3, 3
+#else
+#define HKS_D16_SMALL 8, 3, 4, 8, 3, 4   // small batches: radix-8 rounds (twice the warps per tile)
+#endif
+#ifndef HKS_SMALL_LIMIT
+#define HKS_SMALL_LIMIT (2u * 148u * 4u)
+#endif
 hks_status launch_ntt_pass(const hks_ctx *ctx, NttDir dir, int pass, int epi, NttArgs &a, cudaStream_t s) {
     a.log_n = ctx->log_n;
     a.log_r = ctx->log_r;
     a.log_c = ctx->log_c;
     const bool cols = (dir == NTT_FWD) ? (pass == 0) : (pass == 1);
-    const bool small = a.nlimbs * 16u < 2u * 148u * 4u;
+    const bool small = a.nlimbs * 16u < HKS_SMALL_LIMIT;
     switch (ctx->log_n) {
         case 17: return small ? dispatch<9, 3, 3, 8, 3, 4>(dir, cols, epi, a, s) : dispatch<9, 4, 3, 8, 4, 4>(dir, cols, epi, a, s);
-        case 16: return small ? dispatch<8, 3, 4, 8, 3, 4>(dir, cols, epi, a, s) : dispatch<8, 4, 4, 8, 4, 4>(dir, cols, epi, a, s);
+        case 16: return small ? dispatch<HKS_D16_SMALL>(dir, cols, epi, a, s) : dispatch<HKS_D16_BIG>(dir, cols, epi, a, s);
         case 15: return dispatch<8, 4, 4, 7, 4, 4>(dir, cols, epi, a, s);
         case 14: return dispatch<7, 4, 4, 7, 4, 4>(dir, cols, epi, a, s);
         case 13: return dispatch<7, 4, 4, 6, 3, 4>(dir, cols, epi, a, s);
