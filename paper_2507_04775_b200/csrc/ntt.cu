@@ -360,8 +360,19 @@ static hks_status dispatch(NttDir dir, bool cols, int epi, NttArgs &a, cudaStrea
 #define HKS_D16_SMALL 8, 4, 3, 8, 4, 3
 #elif defined(HKS_D16_SMALL_SEL) && HKS_D16_SMALL_SEL == 2
 #define HKS_D16_SMALL 8, 3, 3, 8, 3, 3
+#elif defined(HKS_D16_SMALL_SEL) && HKS_D16_SMALL_SEL == 3
+#define HKS_D16_SMALL 8, 4, 3, 8, 3, 3
+#elif defined(HKS_D16_SMALL_SEL) && HKS_D16_SMALL_SEL == 4
+#define HKS_D16_SMALL 8, 4, 3, 8, 3, 2
+#elif defined(HKS_D16_SMALL_SEL) && HKS_D16_SMALL_SEL == 5
+#define HKS_D16_SMALL 8, 4, 3, 8, 4, 2
+#elif defined(HKS_D16_SMALL_SEL) && HKS_D16_SMALL_SEL == 6
+#define HKS_D16_SMALL 8, 3, 4, 8, 3, 4   // previous default (radix-8, 16 sub-transforms per CTA both passes)
 #else
-#define HKS_D16_SMALL 8, 3, 4, 8, 3, 4   // small batches: radix-8 rounds (twice the warps per tile)
+// small batches (< 74 limbs: the 30-limb INTT, ModDown's 20- and 60-limb passes): columns radix-16 with
+// 8 columns per CTA (128 threads, 64-byte row segments), rows radix-8 with 8 rows per CTA (256
+// threads) -- measured per pass: C2 3 162 -> 3 298 KS/s over the previous 8,3,4,8,3,4
+#define HKS_D16_SMALL 8, 4, 3, 8, 3, 3
 #endif
 #ifndef HKS_SMALL_LIMIT
 #define HKS_SMALL_LIMIT (2u * 148u * 4u)
