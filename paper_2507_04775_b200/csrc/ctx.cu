@@ -81,6 +81,20 @@ u64 shoup_of(u64 w, u64 m) { return (u64)(((u128)w << 64) / m); }
 
 ulonglong2 sh(u64 w, u64 m) { return make_ulonglong2(w, shoup_of(w, m)); }
 
+// Byte-column words of a base-conversion matrix entry v = [qhat]_t (tensor-pipe BConv, k_bconv_mma):
+// m_a = 2^(8a) v mod t for a = 0..7, and word c (c = 0..7) holds byte c of m_a in its byte a.  Then
+// for any y = sum_a y_a 2^(8a):  sum_a y_a m_a = sum_c 2^(8c) sum_a y_a byte_c(m_a) == y v (mod t).
+void push_bytecols(std::vector<u64> &out, u64 v, u64 t) {
+    u64 m[8];
+    m[0] = v % t;
+    for (int a = 1; a < 8; a++) m[a] = (u64)(((u128)m[a - 1] << 8) % t);
+    for (int c = 0; c < 8; c++) {
+        u64 w = 0;
+        for (int a = 0; a < 8; a++) w |= ((m[a] >> (8 * c)) & 0xffull) << (8 * a);
+        out.push_back(w);
+    }
+}
+
 uint2 split(u64 v) { return make_uint2((u32)(v & 0x3fffffffu), (u32)(v >> 30)); }
 
 u32 bitrev(u32 x, u32 bits) {
@@ -101,7 +115,7 @@ hks_status upload(T **dptr, const std::vector<T> &h) {
 
 void free_tables(hks_ctx *c) {
     void *ptrs[] = {c->d_pc, c->d_tw_col_fwd, c->d_tw_row_fwd, c->d_tw_col_inv, c->d_tw_row_inv, c->d_ninv,
-                    c->d_mu_scale, c->d_mu_mat, c->d_md_scale, c->d_md_mat, c->d_pinv, c->d_mu_matf, c->d_md_matf, c->d_mu_mats, c->d_md_mats,
+                    c->d_mu_scale, c->d_mu_mat, c->d_md_scale, c->d_md_mat, c->d_pinv, c->d_mu_matf, c->d_md_matf, c->d_mu_mats, c->d_md_mats, c->d_mu_matb, c->d_md_matb,
                     c->d_qmod, c->d_qlinv};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -212,6 +226,7 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     // digit's active limbs, matrix [qhat_{j,i}]_t for targets t in (Q_l \ digit j) u P.
     std::vector<ulonglong2> mu_scale;
     std::vector<uint2> mu_mat;
+    std::vector<u64> mu_matb;
     c->mu_scale_off.resize(num_q);
     c->mu_mat_off.assign((size_t)num_q * dnum, 0);
     for (u32 lv = 0; lv <= L; lv++) {
@@ -234,12 +249,14 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
                     for (u32 k = lo; k < hi; k++)
                         if (k != i) h = mul_mod(h, primes[k] % m, m);
                     mu_mat.push_back(split(h));
+                    push_bytecols(mu_matb, h, m);
                 }
         }
     }
     // ModDown constants: scale N^-1 [phat_k]^-1 mod p_k, matrix [phat_k]_{q_i} [K][L+1], P^-1 mod q_i.
     std::vector<ulonglong2> md_scale(num_p), pinv(num_q);
     std::vector<uint2> md_mat((size_t)num_p * num_q);
+    std::vector<u64> md_matb((size_t)num_p * num_q * 8);
     for (u32 k = 0; k < num_p; k++) {
         u64 m = p[k], h = 1;
         for (u32 o = 0; o < num_p; o++)
@@ -250,6 +267,9 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
             for (u32 o = 0; o < num_p; o++)
                 if (o != k) hv = mul_mod(hv, p[o] % qi, qi);
             md_mat[(size_t)k * num_q + i] = split(hv);
+            std::vector<u64> w;
+            push_bytecols(w, hv, qi);
+            std::copy(w.begin(), w.end(), md_matb.begin() + ((size_t)k * num_q + i) * 8);
         }
     }
     for (u32 i = 0; i < num_q; i++) {
@@ -304,6 +324,8 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     UP(d_mu_matf, mu_matf);
     UP(d_md_matf, md_matf);
     UP(d_mu_mats, mu_mats);
+    UP(d_mu_matb, mu_matb);
+    UP(d_md_matb, md_matb);
     UP(d_md_mats, md_mats);
     UP(d_qmod, qmod);
     UP(d_qlinv, qlinv);

@@ -83,6 +83,8 @@ struct BconvGroup {
     const uint2 *mat;          // [nsrc][mat_stride] (lo30, hi30) of [qhat_i]_t, column u = target u
     const double *matf;        // same entries as three exact 20-bit limbs [nsrc][mat_stride][3] (FP64 path) or NULL
     const u32 *mats;           // (lo30 + hi30) of each entry [nsrc][mat_stride] (Karatsuba path) or NULL
+    const u64 *matb;           // byte-column words [nsrc][mat_stride][8] (tensor-pipe path, k_bconv_mma) or NULL:
+                               // word c of entry (i, u) has byte a = byte c of (2^(8a) [qhat_i]_t mod t)
     u16 src_slot[BC_MAXSRC];
     u16 src_prime[BC_MAXSRC];
     u64 pre_w[BC_MAXSRC];      // optional prescale y_i = x_i * pre_w (Shoup) -- generic hks_bconv
@@ -217,6 +219,8 @@ struct hks_ctx {
     u32 *d_mu_mats = nullptr;           // ModUp matrices: lo30 + hi30 per entry (Karatsuba middle term)
     u32 *d_md_mats = nullptr;           // ModDown matrix: lo30 + hi30 per entry
     double *d_md_matf = nullptr;        // ModDown matrix as 20-bit limbs in doubles
+    u64 *d_mu_matb = nullptr;           // ModUp matrices as byte-column words, 8 per entry (k_bconv_mma)
+    u64 *d_md_matb = nullptr;           // ModDown matrix as byte-column words, 8 per entry
     ulonglong2 *d_pinv = nullptr;       // P^-1 mod q_i  [L+1] (Shoup)
     u64 *d_qmod = nullptr;              // Rescale: q_j mod q_i  [L+1][L+1] (row j = dropped limb)
     ulonglong2 *d_qlinv = nullptr;      // Rescale: q_j^-1 mod q_i (Shoup)  [L+1][L+1]

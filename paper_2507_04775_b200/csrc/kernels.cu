@@ -160,6 +160,146 @@ static void bconv_kara_go(const BconvArgs &a, cudaStream_t s) {
     ps.done(words * (double)N * 8.0, macs * (double)N * 4.0);
 }
 
+// ------------------------------------------------------------------------------------------------
+// Base conversion on the tensor pipe.  Eq. 1 is, across the N coefficients, a dense contraction
+// OUT[t][x] = sum_i M[i][t] Y[i][x] with a constant matrix.  Splitting y_i into bytes y_{i,a} and
+// folding the byte weight into the matrix, m_{i,t,a} = 2^(8a) M[i][t] mod t, gives an exact integer
+// identity   X'_t(x) = sum_c 2^(8c) S_{t,c}(x),  S_{t,c}(x) = sum_{i,a} y_{i,a}(x) byte_c(m_{i,t,a}),
+// with X' == sum_i y_i M[i][t] (mod t): a u8 x u8 GEMM of K = 8 NSRC and 8 byte columns per target,
+// computed with warp-level IMMA (m16n8k32 / m16n8k16, s32 accumulators: S < 128 * 255^2 < 2^23), and
+// one 80-bit reduction per output ("reduced only before being written back").  The
+// output is congruent to the Eq. 1 value, so canonical outputs are identical to k_bconv's and lazy
+// ones ([0, 6t)) differ only inside the forward NTT's accepted input range.
+//
+// K order (chosen so a thread's A bytes are whole words): k-step s covers sources 4s..4s+3; lane
+// (g, q) holds bytes 0-3 / 4-7 of y_{4s+q}[x0+g] in a0 / a2 and of y_{4s+q}[x0+g+8] in a1 / a3.  A
+// trailing k16 step takes 1-2 sources: lane q holds half (q & 1) of y_{4s + q/2}.  Columns: in n-tile
+// j, column 2q+e is (target 4gb+q, byte column c = 2j+e), so after the 4 n-tiles lane (g, q) holds all
+// eight S_{t,c} of target 4gb+q for coefficients x0+g and x0+g+8 (no shuffles).
+#ifndef HKS_MMA_TCH
+#define HKS_MMA_TCH 32
+#endif
+#ifndef HKS_MMA_TPW
+#define HKS_MMA_TPW 2
+#endif
+#define MMA_TCH HKS_MMA_TCH
+template <int NSRC, int TPW, bool LAZY>
+__global__ void __launch_bounds__(256, 2) k_bconv_mma(const __grid_constant__ BconvArgs A) {
+    pdl_trigger();
+    constexpr int KS32 = NSRC / 4 + (NSRC % 4 == 3 ? 1 : 0);   // k32 steps (the last one may be padded)
+    constexpr bool K16 = (NSRC % 4 == 1 || NSRC % 4 == 2);    // trailing k16 step
+    constexpr int NS = KS32 + (K16 ? 1 : 0);
+    constexpr int NG = MMA_TCH / 4;                            // target groups (4 targets) per CTA
+    const BconvGroup &G = A.g[blockIdx.y];
+    const u32 u0 = blockIdx.z * MMA_TCH;
+    if (u0 >= G.ndst) return;
+    const u32 nt = min((u32)MMA_TCH, G.ndst - u0);
+    const u32 ngr = (nt + 3) / 4;
+    // B fragments, laid out [group][k-step][n-tile j][qq][g]: a warp's 32 lanes read 32 consecutive words
+    __shared__ u64 sB[NG * NS * 128];
+    __shared__ PrimeConst spc[MMA_TCH];
+    for (u32 idx = threadIdx.x; idx < ngr * NS * 128; idx += blockDim.x) {
+        const u32 g8 = idx & 7, qq = (idx >> 3) & 3, j = (idx >> 5) & 3, s = (idx >> 7) % NS, gb = (idx >> 7) / NS;
+        const u32 u = gb * 4 + (g8 >> 1), c = 2 * j + (g8 & 1), i = 4 * s + qq;
+        sB[idx] = (u < nt && i < (u32)NSRC) ? G.matb[((size_t)i * G.mat_stride + u0 + u) * 8 + c] : 0;
+    }
+    for (u32 u = threadIdx.x; u < nt; u += blockDim.x) spc[u] = A.pc[G.dst_prime[u0 + u]];
+    __syncthreads();
+    pdl_wait();   // ctx tables above are immutable; the inputs below come from the predecessor
+
+    const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, q = lane & 3;
+    const size_t N = (size_t)1 << A.log_n;
+    const size_t xw = ((size_t)blockIdx.x * 8 + warp) * (16 * TPW);
+    if (xw >= N) return;
+    u32 af[TPW][NS][4];
+#pragma unroll
+    for (int s = 0; s < NS; s++) {
+        const bool k16 = K16 && s == KS32;
+        const u32 i = k16 ? 4 * s + (q >> 1) : 4 * s + q;
+        const u64 *src = i < (u32)NSRC ? A.in + (size_t)G.src_slot[i] * N + xw : nullptr;
+#pragma unroll
+        for (int t = 0; t < TPW; t++) {
+            const u64 v0 = src ? src[16 * t + g] : 0, v1 = src ? src[16 * t + g + 8] : 0;
+            if (k16) {
+                af[t][s][0] = (q & 1) ? (u32)(v0 >> 32) : (u32)v0;
+                af[t][s][1] = (q & 1) ? (u32)(v1 >> 32) : (u32)v1;
+                af[t][s][2] = af[t][s][3] = 0;
+            } else {
+                af[t][s][0] = (u32)v0;
+                af[t][s][1] = (u32)v1;
+                af[t][s][2] = (u32)(v0 >> 32);
+                af[t][s][3] = (u32)(v1 >> 32);
+            }
+        }
+    }
+    for (u32 gb = 0; gb < ngr; gb++) {
+        int acc[TPW][4][4];
+#pragma unroll
+        for (int t = 0; t < TPW; t++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) acc[t][j][0] = acc[t][j][1] = acc[t][j][2] = acc[t][j][3] = 0;
+        const u64 *sb = sB + gb * NS * 128;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+#pragma unroll
+            for (int s = 0; s < NS; s++) {
+                if (K16 && s == KS32) {
+                    const u64 w = sb[s * 128 + j * 32 + (q >> 1) * 8 + g];
+                    const u32 b0 = (q & 1) ? (u32)(w >> 32) : (u32)w;
+#pragma unroll
+                    for (int t = 0; t < TPW; t++) mma_u8_k16(acc[t][j], af[t][s][0], af[t][s][1], b0);
+                } else {
+                    const u64 w = sb[s * 128 + j * 32 + q * 8 + g];
+#pragma unroll
+                    for (int t = 0; t < TPW; t++) mma_u8_k32(acc[t][j], af[t][s], (u32)w, (u32)(w >> 32));
+                }
+            }
+        }
+        const u32 u = gb * 4 + q;
+        if (u < nt) {
+            const PrimeConst pc = spc[u];
+            u64 *dst = A.out + (size_t)G.dst_slot[u0 + u] * N + xw;
+#pragma unroll
+            for (int t = 0; t < TPW; t++)
+#pragma unroll
+                for (int h = 0; h < 2; h++)
+                    dst[16 * t + g + 8 * h] =
+                        bytesum_reduce<LAZY>(acc[t][0][2 * h], acc[t][0][2 * h + 1], acc[t][1][2 * h], acc[t][1][2 * h + 1],
+                                             acc[t][2][2 * h], acc[t][2][2 * h + 1], acc[t][3][2 * h],
+                                             acc[t][3][2 * h + 1], pc);
+        }
+    }
+}
+
+template <int NSRC>
+static void bconv_mma_go(const BconvArgs &a, cudaStream_t s) {
+    constexpr int TPW = HKS_MMA_TPW;
+    const size_t N = (size_t)1 << a.log_n;
+    u32 maxdst = 0;
+    for (u32 g = 0; g < a.ngroups; g++) maxdst = max(maxdst, a.g[g].ndst);
+    dim3 grid((u32)(N / (8 * 16 * TPW)), a.ngroups, (maxdst + MMA_TCH - 1) / MMA_TCH);
+    ProfScope ps(K_BCONV, s);
+    if (a.lazy_out)
+        (void)hks_launch(k_bconv_mma<NSRC, TPW, true>, grid, dim3(256), 0, s, a);
+    else
+        (void)hks_launch(k_bconv_mma<NSRC, TPW, false>, grid, dim3(256), 0, s, a);
+    double words = 0, macs = 0;
+    for (u32 g = 0; g < a.ngroups; g++) {
+        words += a.g[g].nsrc + a.g[g].ndst;
+        macs += (double)a.g[g].nsrc * a.g[g].ndst;
+    }
+    ps.done(words * (double)N * 8.0, macs * (double)N * 4.0);
+}
+
+// HKS_BCONV_MMA=0 selects the integer-pipe kernels (results identical).
+static bool getenv_mma_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("HKS_BCONV_MMA");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 static bool getenv_kara_enabled() {
     static const bool on = [] {
         const char *e = getenv("HKS_BCONV_KARA");
@@ -290,6 +430,14 @@ static void bconv_go(const BconvArgs &a, cudaStream_t s) {
 
 hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
     // all groups of one launch share nsrc (the caller groups them so)
+    if (!a.prescale && a.g[0].matb && a.log_n >= 8 && getenv_mma_enabled()) {
+        switch (a.g[0].nsrc) {
+#define CM(NS) case NS: bconv_mma_go<NS>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            CM(1) CM(2) CM(3) CM(4) CM(5) CM(6) CM(7) CM(8) CM(9) CM(10) CM(11) CM(12) CM(13) CM(14) CM(15) CM(16)
+#undef CM
+            default: break;
+        }
+    }
     if (!a.prescale && a.g[0].matf && getenv_fp_enabled()) {
         // FP64-pipe share chosen so both pipes carry similar work: 16 NINT + 56 ~ 18 NFP + 10 cycles
         switch (a.g[0].nsrc) {

@@ -352,6 +352,48 @@ HKS_DEV u64 switch_centered(u64 t, u64 qs, u64 qs_mod_p, const PrimeConst &c) {
     return r;
 }
 
+// ---- base conversion on the tensor pipe (k_bconv_mma): byte-split products -------------------
+// Legacy warp-level integer MMA (SASS IMMA): D(16x8, s32) += A(16xK, u8, row) * B(Kx8, u8, col).
+HKS_DEV void mma_u8_k32(int (&d)[4], const u32 (&a)[4], u32 b0, u32 b1) {
+    asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+HKS_DEV void mma_u8_k16(int (&d)[4], u32 a0, u32 a1, u32 b0) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                 : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+                 : "r"(a0), "r"(a1), "r"(b0));
+}
+
+// y * w mod p in [0, 2p) for a 32-bit multiplier y (exact Shoup quotient from two 32-bit products).
+HKS_DEV u64 shoup_u32(u32 y, u64 w, u64 wp, u64 np) {
+    const u32 t1 = __umulhi(y, (u32)wp);
+    const u32 q = (u32)(((u64)y * (u32)(wp >> 32) + t1) >> 32);
+    const u64 r = (u64)y * (u32)w + (u64)q * (u32)np;
+    const u32 rh = (u32)(r >> 32) + y * (u32)(w >> 32) + q * (u32)(np >> 32);
+    return ((u64)rh << 32) | (u32)r;
+}
+
+// X' = sum_c S_c 2^(8c) (S_c < 2^23, c = 0..7, so X' < 2^80) reduced modulo p: [0, 6p) lazily,
+// else canonical.  X' = T01 + T23 2^16 + T45 2^32 + T67 2^48 with T_{c,c+1} = S_c + S_{c+1} 2^8 < 2^32.
+template <bool LAZY>
+HKS_DEV u64 bytesum_reduce(int s0, int s1, int s2, int s3, int s4, int s5, int s6, int s7, const PrimeConst &c) {
+    const u32 t01 = (u32)s0 + ((u32)s1 << 8), t23 = (u32)s2 + ((u32)s3 << 8);
+    const u32 t45 = (u32)s4 + ((u32)s5 << 8), t67 = (u32)s6 + ((u32)s7 << 8);
+    u64 lo = (u64)t01 + ((u64)t23 << 16) + ((u64)t45 << 32);   // < 2^64
+    const u64 add = (u64)t67 << 48;
+    lo += add;
+    const u32 hi = (t67 >> 16) + (lo < add ? 1u : 0u);
+    u64 r = mod64_lazy(lo, c) + shoup_u32(hi, c.r64, c.r64p, 0 - c.p);   // [0, 4p) + [0, 2p)
+    if (!LAZY) {
+        r = csub(r, 4 * c.p);
+        r = csub(r, 2 * c.p);
+        r = csub(r, c.p);
+    }
+    return r;
+}
+
 HKS_DEV u64 acc_reduce_lazy(const Acc30 &a, const PrimeConst &c) {
     u64 lo, hi;
     acc_to128(a, lo, hi);
