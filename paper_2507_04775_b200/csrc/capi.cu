@@ -54,6 +54,7 @@ hks_status run_bconv_groups(const hks_ctx *c, std::vector<BconvGroup> &groups, c
         a.log_n = c->log_n;
         a.prescale = 0;
         a.lazy_out = 1;   // internal conversions feed the forward NTT, which takes [0, 8p + 2^32)
+        a.big = c->all_big ? 1 : 0;
         u32 ns = groups[i].nsrc, k = 0;
         while (i < groups.size() && k < BC_MAXG && groups[i].nsrc == ns) a.g[k++] = groups[i++];
         a.ngroups = k;

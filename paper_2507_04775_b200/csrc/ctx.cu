@@ -203,7 +203,9 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     for (u32 i = 0; i < nm; i++) {
         u64 m = primes[i];
         u64 r64 = (u64)(((u128)1 << 64) % m);
-        pc[i] = PrimeConst{m, r64, shoup_of(r64, m), (u64)(~0ull / m)};
+        const u64 r48 = (u64)(((u128)1 << 48) % m);
+        pc[i] = PrimeConst{m, r64, shoup_of(r64, m), (u64)(~0ull / m), r48, shoup_of(r48, m)};
+        if (m >> 32 == 0) c->all_big = false;
         ninv[i] = sh(inv_mod(n % m, m), m);
     }
     // one_p = floor(2^64 / m) = floor((2^64 - 1) / m) since m does not divide 2^64.

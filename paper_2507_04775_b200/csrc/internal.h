@@ -101,6 +101,8 @@ struct BconvArgs {
     u32 ngroups;
     u32 prescale;              // 1: apply pre_w (inputs raw COEFF), 0: inputs are canonical y_i
     u32 lazy_out;              // 1: outputs in [0, 8t) (consumer: forward NTT), 0: canonical
+    u32 big;                   // 1: every prime > 2^32 (required by the tensor-pipe kernel k_bconv_mma)
+    u32 cw;                    // k_bconv_mma: coefficients per CTA (set by the launcher)
     BconvGroup g[BC_MAXG];
 };
 
@@ -200,6 +202,7 @@ hks_status run_ntt_kip(const hks_ctx *ctx, const std::vector<KipItem> &items, u3
 struct hks_ctx {
     u32 log_n, n, log_r, log_c, nq, np, dnum, alpha;
     int device;
+    bool all_big = true;        // every prime > 2^32
     std::vector<u64> primes, psi;
 
     // host mirrors of the small tables (offsets into the device arrays)

@@ -171,118 +171,175 @@ static void bconv_kara_go(const BconvArgs &a, cudaStream_t s) {
 // output is congruent to the Eq. 1 value, so canonical outputs are identical to k_bconv's and lazy
 // ones ([0, 6t)) differ only inside the forward NTT's accepted input range.
 //
-// K order (chosen so a thread's A bytes are whole words): k-step s covers sources 4s..4s+3; lane
-// (g, q) holds bytes 0-3 / 4-7 of y_{4s+q}[x0+g] in a0 / a2 and of y_{4s+q}[x0+g+8] in a1 / a3.  A
-// trailing k16 step takes 1-2 sources: lane q holds half (q & 1) of y_{4s + q/2}.  Columns: in n-tile
-// j, column 2q+e is (target 4gb+q, byte column c = 2j+e), so after the 4 n-tiles lane (g, q) holds all
-// eight S_{t,c} of target 4gb+q for coefficients x0+g and x0+g+8 (no shuffles).
+// Operands: A = the byte-column matrix (M = 16 rows = 8 targets x 2 byte columns per m-tile, from
+// shared memory), B = the input bytes (N = 8 coefficients per n-tile, straight from the limbs), so a
+// lane's B fragment of a k32 step is one whole word: lane (g, q) holds y_{4s+q}[x0+g] (bytes 0-3 in b0,
+// 4-7 in b1) -- k-step s covers sources 4s..4s+3; a trailing k16 step takes 1-2 sources, lane q holding
+// half (q & 1) of y_{4s + q/2}.  Row g (g + 8) of m-tile i is (target g of the warp's block, byte column
+// c = 2i (2i + 1)), so after the 4 m-tiles lane (g, q) holds all eight S_{t,c} of target g for the
+// coefficients x0 + 2q and x0 + 2q + 1: no shuffles, one 16-byte store per lane and n-tile.
 #ifndef HKS_MMA_TCH
 #define HKS_MMA_TCH 32
 #endif
-#ifndef HKS_MMA_TPW
-#define HKS_MMA_TPW 2
+#ifndef HKS_MMA_CW
+#define HKS_MMA_CW 128
+#endif
+#ifndef HKS_MMA_MINB
+#define HKS_MMA_MINB 2
+#endif
+#ifndef HKS_MMA_NPI
+#define HKS_MMA_NPI 2
 #endif
 #define MMA_TCH HKS_MMA_TCH
-template <int NSRC, int TPW, bool LAZY>
-__global__ void __launch_bounds__(256, 2) k_bconv_mma(const __grid_constant__ BconvArgs A) {
+#define MMA_CW HKS_MMA_CW
+#define NPI HKS_MMA_NPI
+template <int NSRC, bool LAZY>
+__global__ void __launch_bounds__(256, HKS_MMA_MINB) k_bconv_mma(const __grid_constant__ BconvArgs A) {
     pdl_trigger();
     constexpr int KS32 = NSRC / 4 + (NSRC % 4 == 3 ? 1 : 0);   // k32 steps (the last one may be padded)
     constexpr bool K16 = (NSRC % 4 == 1 || NSRC % 4 == 2);    // trailing k16 step
     constexpr int NS = KS32 + (K16 ? 1 : 0);
-    constexpr int NG = MMA_TCH / 4;                            // target groups (4 targets) per CTA
+    constexpr int NB = MMA_TCH / 8;                            // target blocks (8 targets) per CTA
     const BconvGroup &G = A.g[blockIdx.y];
     const u32 u0 = blockIdx.z * MMA_TCH;
     if (u0 >= G.ndst) return;
     const u32 nt = min((u32)MMA_TCH, G.ndst - u0);
-    const u32 ngr = (nt + 3) / 4;
-    // B fragments, laid out [group][k-step][n-tile j][qq][g]: a warp's 32 lanes read 32 consecutive words
-    __shared__ u64 sB[NG * NS * 128];
+    const u32 nblk = (nt + 7) / 8;
+    // A fragments [block][m-tile i][k-step s][lane] as uint4 (a0, a1, a2, a3)
+    __shared__ uint4 sA[NB * 4 * NS * 32];
+    __shared__ uint2 sA16[K16 ? NB * 4 * 32 : 1];   // k16-step fragments (a0, a1), lane-contiguous
     __shared__ PrimeConst spc[MMA_TCH];
-    for (u32 idx = threadIdx.x; idx < ngr * NS * 128; idx += blockDim.x) {
-        const u32 g8 = idx & 7, qq = (idx >> 3) & 3, j = (idx >> 5) & 3, s = (idx >> 7) % NS, gb = (idx >> 7) / NS;
-        const u32 u = gb * 4 + (g8 >> 1), c = 2 * j + (g8 & 1), i = 4 * s + qq;
-        sB[idx] = (u < nt && i < (u32)NSRC) ? G.matb[((size_t)i * G.mat_stride + u0 + u) * 8 + c] : 0;
+    {
+        // all table loads of a thread are issued before its shared-memory stores (one L2 round trip)
+        constexpr int PER = (NB * 4 * NS * 32 + 255) / 256;
+        const u32 ne = nblk * 4 * NS * 32;
+        ulonglong2 w[PER];
+#pragma unroll
+        for (int r = 0; r < PER; r++) {
+            const u32 idx = threadIdx.x + 256 * r;
+            const u32 ln = idx & 31, s = (idx >> 5) % NS, mi = (idx >> 5) / NS % 4, tb = (idx >> 5) / NS / 4;
+            const u32 g = ln >> 2, q = ln & 3, u = tb * 8 + g;
+            const u32 i = (K16 && (int)s == KS32) ? 4 * s + (q >> 1) : 4 * s + q;
+            w[r] = make_ulonglong2(0, 0);
+            if (idx < ne && u < nt && i < (u32)NSRC)
+                w[r] = __ldg(reinterpret_cast<const ulonglong2 *>(G.matb + ((size_t)i * G.mat_stride + u0 + u) * 8 + 2 * mi));
+        }
+#pragma unroll
+        for (int r = 0; r < PER; r++) {
+            const u32 idx = threadIdx.x + 256 * r;
+            if (idx >= ne) break;
+            const u32 ln = idx & 31, s = (idx >> 5) % NS, mi = (idx >> 5) / NS % 4, tb = (idx >> 5) / NS / 4;
+            const u32 q = ln & 3;
+            if (K16 && (int)s == KS32) {
+                const u32 sh = (q & 1) * 32;
+                sA16[(tb * 4 + mi) * 32 + ln] = make_uint2((u32)(w[r].x >> sh), (u32)(w[r].y >> sh));
+            } else {
+                sA[idx] = make_uint4((u32)w[r].x, (u32)w[r].y, (u32)(w[r].x >> 32), (u32)(w[r].y >> 32));
+            }
+        }
     }
     for (u32 u = threadIdx.x; u < nt; u += blockDim.x) spc[u] = A.pc[G.dst_prime[u0 + u]];
     __syncthreads();
     pdl_wait();   // ctx tables above are immutable; the inputs below come from the predecessor
 
     const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, q = lane & 3;
+    const u32 nparts = 8 / nblk, tb = warp % nblk, part = warp / nblk;
+    if (part >= nparts) return;
+    const u32 u = tb * 8 + g;
+    const bool active = u < nt;
+    const PrimeConst pc = spc[active ? u : 0];
     const size_t N = (size_t)1 << A.log_n;
-    const size_t xw = ((size_t)blockIdx.x * 8 + warp) * (16 * TPW);
-    if (xw >= N) return;
-    u32 af[TPW][NS][4];
+    u64 *dst = A.out + (size_t)G.dst_slot[u0 + (active ? u : 0)] * N;
+    const uint4 *fa = sA + tb * 4 * NS * 32 + lane;
+    const uint2 *fa16 = sA16 + (K16 ? tb * 4 * 32 + lane : 0);
+    const u64 *src[NS];
 #pragma unroll
     for (int s = 0; s < NS; s++) {
-        const bool k16 = K16 && s == KS32;
-        const u32 i = k16 ? 4 * s + (q >> 1) : 4 * s + q;
-        const u64 *src = i < (u32)NSRC ? A.in + (size_t)G.src_slot[i] * N + xw : nullptr;
-#pragma unroll
-        for (int t = 0; t < TPW; t++) {
-            const u64 v0 = src ? src[16 * t + g] : 0, v1 = src ? src[16 * t + g + 8] : 0;
-            if (k16) {
-                af[t][s][0] = (q & 1) ? (u32)(v0 >> 32) : (u32)v0;
-                af[t][s][1] = (q & 1) ? (u32)(v1 >> 32) : (u32)v1;
-                af[t][s][2] = af[t][s][3] = 0;
-            } else {
-                af[t][s][0] = (u32)v0;
-                af[t][s][1] = (u32)v1;
-                af[t][s][2] = (u32)(v0 >> 32);
-                af[t][s][3] = (u32)(v1 >> 32);
-            }
-        }
+        const u32 i = (K16 && s == KS32) ? 4 * s + (q >> 1) : 4 * s + q;
+        src[s] = i < (u32)NSRC ? A.in + (size_t)G.src_slot[i] * N + g : nullptr;
     }
-    for (u32 gb = 0; gb < ngr; gb++) {
-        int acc[TPW][4][4];
+    const size_t xbeg = (size_t)blockIdx.x * A.cw, xend = xbeg + A.cw, xstep = 8 * NPI * nparts;
+    // NPI n-tiles (8 NPI coefficients) per iteration: 4 NPI independent accumulator chains; the next
+    // iteration's input words are requested before this one's MMAs (register double buffer)
+    u64 ynx[NPI][NS];
 #pragma unroll
-        for (int t = 0; t < TPW; t++)
+    for (int s = 0; s < NS; s++)
 #pragma unroll
-            for (int j = 0; j < 4; j++) acc[t][j][0] = acc[t][j][1] = acc[t][j][2] = acc[t][j][3] = 0;
-        const u64 *sb = sB + gb * NS * 128;
+        for (int n = 0; n < NPI; n++) ynx[n][s] = src[s] ? __ldg(src[s] + xbeg + 8 * NPI * part + 8 * n) : 0;
+    for (size_t x0 = xbeg + 8 * NPI * part; x0 < xend; x0 += xstep) {
+        u64 yb[NPI][NS];
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
+        for (int s = 0; s < NS; s++)
 #pragma unroll
-            for (int s = 0; s < NS; s++) {
+            for (int n = 0; n < NPI; n++) yb[n][s] = ynx[n][s];
+        if (x0 + xstep < xend) {
+#pragma unroll
+            for (int s = 0; s < NS; s++)
+#pragma unroll
+                for (int n = 0; n < NPI; n++) ynx[n][s] = src[s] ? __ldg(src[s] + x0 + xstep + 8 * n) : 0;
+        }
+        int acc[NPI][4][4];
+#pragma unroll
+        for (int n = 0; n < NPI; n++)
+#pragma unroll
+            for (int mi = 0; mi < 4; mi++) acc[n][mi][0] = acc[n][mi][1] = acc[n][mi][2] = acc[n][mi][3] = 0;
+#pragma unroll
+        for (int s = 0; s < NS; s++) {
+#pragma unroll
+            for (int mi = 0; mi < 4; mi++) {
                 if (K16 && s == KS32) {
-                    const u64 w = sb[s * 128 + j * 32 + (q >> 1) * 8 + g];
-                    const u32 b0 = (q & 1) ? (u32)(w >> 32) : (u32)w;
+                    const uint2 a = fa16[mi * 32];
 #pragma unroll
-                    for (int t = 0; t < TPW; t++) mma_u8_k16(acc[t][j], af[t][s][0], af[t][s][1], b0);
+                    for (int n = 0; n < NPI; n++) {
+                        const u32 b = (q & 1) ? (u32)(yb[n][s] >> 32) : (u32)yb[n][s];
+                        mma_u8_k16(acc[n][mi], a.x, a.y, b);
+                    }
                 } else {
-                    const u64 w = sb[s * 128 + j * 32 + q * 8 + g];
+                    const uint4 a = fa[(mi * NS + s) * 32];
+                    const u32 af[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
-                    for (int t = 0; t < TPW; t++) mma_u8_k32(acc[t][j], af[t][s], (u32)w, (u32)(w >> 32));
+                    for (int n = 0; n < NPI; n++) mma_u8_k32(acc[n][mi], af, (u32)yb[n][s], (u32)(yb[n][s] >> 32));
                 }
             }
         }
-        const u32 u = gb * 4 + q;
-        if (u < nt) {
-            const PrimeConst pc = spc[u];
-            u64 *dst = A.out + (size_t)G.dst_slot[u0 + u] * N + xw;
+        if (active) {
 #pragma unroll
-            for (int t = 0; t < TPW; t++)
+            for (int n = 0; n < NPI; n++) {
+                u64 o[2];
 #pragma unroll
-                for (int h = 0; h < 2; h++)
-                    dst[16 * t + g + 8 * h] =
-                        bytesum_reduce<LAZY>(acc[t][0][2 * h], acc[t][0][2 * h + 1], acc[t][1][2 * h], acc[t][1][2 * h + 1],
-                                             acc[t][2][2 * h], acc[t][2][2 * h + 1], acc[t][3][2 * h],
-                                             acc[t][3][2 * h + 1], pc);
+                for (int e = 0; e < 2; e++)
+                    o[e] = bytesum_reduce<LAZY>(acc[n][0][e], acc[n][0][2 + e], acc[n][1][e], acc[n][1][2 + e],
+                                                acc[n][2][e], acc[n][2][2 + e], acc[n][3][e], acc[n][3][2 + e], pc);
+                *reinterpret_cast<ulonglong2 *>(dst + x0 + 8 * n + 2 * q) = make_ulonglong2(o[0], o[1]);
+            }
         }
     }
 }
 
 template <int NSRC>
 static void bconv_mma_go(const BconvArgs &a, cudaStream_t s) {
-    constexpr int TPW = HKS_MMA_TPW;
     const size_t N = (size_t)1 << a.log_n;
     u32 maxdst = 0;
     for (u32 g = 0; g < a.ngroups; g++) maxdst = max(maxdst, a.g[g].ndst);
-    dim3 grid((u32)(N / (8 * 16 * TPW)), a.ngroups, (maxdst + MMA_TCH - 1) / MMA_TCH);
+    // one wave: every CTA stages its matrix fragments before griddepcontrol.wait, i.e. while the
+    // predecessor is still running (MMA_SLOTS resident CTAs per SM); CW = coefficients per CTA
+    const u32 nz = (maxdst + MMA_TCH - 1) / MMA_TCH;
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    size_t cw = MMA_CW;
+    while (cw < N && (N / cw) * a.ngroups * nz > (size_t)nsm * HKS_MMA_MINB) cw *= 2;
+    BconvArgs b = a;
+    b.cw = (u32)cw;
+    dim3 grid((u32)(N / cw), a.ngroups, nz);
     ProfScope ps(K_BCONV, s);
     if (a.lazy_out)
-        (void)hks_launch(k_bconv_mma<NSRC, TPW, true>, grid, dim3(256), 0, s, a);
+        (void)hks_launch(k_bconv_mma<NSRC, true>, grid, dim3(256), 0, s, b);
     else
-        (void)hks_launch(k_bconv_mma<NSRC, TPW, false>, grid, dim3(256), 0, s, a);
+        (void)hks_launch(k_bconv_mma<NSRC, false>, grid, dim3(256), 0, s, b);
     double words = 0, macs = 0;
     for (u32 g = 0; g < a.ngroups; g++) {
         words += a.g[g].nsrc + a.g[g].ndst;
@@ -430,7 +487,7 @@ static void bconv_go(const BconvArgs &a, cudaStream_t s) {
 
 hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
     // all groups of one launch share nsrc (the caller groups them so)
-    if (!a.prescale && a.g[0].matb && a.log_n >= 8 && getenv_mma_enabled()) {
+    if (!a.prescale && a.big && a.g[0].matb && ((size_t)1 << a.log_n) >= MMA_CW && getenv_mma_enabled()) {
         switch (a.g[0].nsrc) {
 #define CM(NS) case NS: bconv_mma_go<NS>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
             CM(1) CM(2) CM(3) CM(4) CM(5) CM(6) CM(7) CM(8) CM(9) CM(10) CM(11) CM(12) CM(13) CM(14) CM(15) CM(16)

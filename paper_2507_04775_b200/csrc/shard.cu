@@ -68,6 +68,7 @@ hks_status bconv_groups(const hks_ctx *c, std::vector<BconvGroup> &groups, const
         a.pc = c->d_pc;
         a.log_n = c->log_n;
         a.lazy_out = 1;
+        a.big = c->all_big ? 1 : 0;
         u32 ns = groups[i].nsrc, k = 0;
         while (i < groups.size() && k < BC_MAXG && groups[i].nsrc == ns) a.g[k++] = groups[i++];
         a.ngroups = k;
