@@ -348,7 +348,259 @@ static void bconv_mma_go(const BconvArgs &a, cudaStream_t s) {
     ps.done(words * (double)N * 8.0, macs * (double)N * 4.0);
 }
 
-// HKS_BCONV_MMA=0 selects the integer-pipe kernels (results identical).
+// ------------------------------------------------------------------------------------------------
+// The same byte-split contraction on the 5th-generation tensor cores (tcgen05, accumulators in TMEM).
+//   D[m][8t + c] (s32, TMEM lane m, column 8t + c) = sum_k A[m][k] B[8t + c][k]
+//   A = input tile: 128 coefficients x K bytes (source i, byte a) -- K-major, no swizzle: core
+//       matrices of 8 rows x 16 bytes, the 16 bytes of row m / chunk kc being y_{2kc}[x_m], y_{2kc+1}[x_m]
+//   B = byte-column matrix: row 8t + c, chunk kc = matb words (2kc, t, c), (2kc + 1, t, c)
+// so TMEM lane m holds, in 8 consecutive columns, the eight S_{t,c} of coefficient m and target t:
+// one tcgen05.ld (32x32b.x8) per output.  Persistent CTAs (one per SM, 512 TMEM columns = two
+// accumulators), warp roles:
+//   warps 0-7  epilogue: TMEM -> registers -> bytesum_reduce -> coalesced stores (warp w: lanes
+//              32 (w % 4) .. +31, targets t = w / 4 (mod 2))
+//   warps 8-11 producers: cp.async of the next tiles' input words into TC_SA shared stages; thread
+//              256 issues the tcgen05.mma of a tile (K / 32 instructions) and commits to mbarriers.
+#ifndef HKS_TC_SA
+#define HKS_TC_SA 4
+#endif
+#define TC_SA HKS_TC_SA
+#define TC_THREADS 384
+
+__device__ __forceinline__ u32 smem_u32(const void *p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u32 a, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(u32 a, u32 parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "W%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W%=;\n\t}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(u32 a) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void tc_commit(u32 mbar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// no-swizzle K-major smem matrix descriptor (version 1): start, LBO = K-chunk stride, SBO = 8-row stride
+__device__ __forceinline__ u64 tc_desc(u32 saddr, u32 lbo, u32 sbo) {
+    return (u64)((saddr >> 4) & 0x3fff) | ((u64)((lbo >> 4) & 0x3fff) << 16) | ((u64)((sbo >> 4) & 0x3fff) << 32) |
+           (1ull << 46);
+}
+__device__ __forceinline__ void tc_mma_i8(u32 dtmem, u64 adesc, u64 bdesc, u32 idesc, u32 accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tc_ld8(u32 taddr, u32 (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cp_async8(u32 saddr, const void *g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr), "l"(g) : "memory");
+}
+
+template <int NSRC, bool LAZY>
+__global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constant__ BconvArgs A) {
+    pdl_trigger();
+    constexpr int KPAD = 32 * ((NSRC + 3) / 4);   // bytes of K (whole K = 32 MMA steps)
+    constexpr int NCH = KPAD / 16;                // 16-byte K chunks
+    constexpr u32 SBO = NCH * 128;                // 8-row group stride
+    constexpr u32 ATILE = 128 * KPAD;             // bytes per input stage
+    const BconvGroup &G = A.g[blockIdx.y];
+    const u32 tch = A.cw;                         // targets per z-chunk (even, <= 32)
+    const u32 u0 = blockIdx.z * tch;
+    if (u0 >= G.ndst) return;
+    const u32 nt = min(tch, G.ndst - u0);
+    const u32 ncol = 8 * ((nt + 1) & ~1u);        // MMA N (multiple of 16, <= 256)
+    const size_t N = (size_t)1 << A.log_n;
+    const u32 ntiles_all = (u32)(N >> 7);
+    const u32 ntile = blockIdx.x < ntiles_all ? (ntiles_all - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+    extern __shared__ __align__(1024) uint8_t tsm[];
+    uint8_t *sB = tsm;                                   // 256 x KPAD
+    uint8_t *sA = tsm + 256 * KPAD;                      // TC_SA x ATILE
+    __shared__ __align__(8) u64 bar_done[2], bar_empty[2], bar_free[TC_SA];
+    __shared__ u32 tmem_base_s;
+    __shared__ PrimeConst spc[32];
+    const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    // ---- prologue (before griddepcontrol.wait: ctx tables only) ----
+    for (u32 idx = tid; idx < 256 * NCH; idx += TC_THREADS) {
+        const u32 n = idx / NCH, kc = idx - n * NCH, t = n >> 3, c = n & 7;
+        u64 w0 = 0, w1 = 0;
+        if (t < nt) {
+            if (2 * kc < (u32)NSRC) w0 = __ldg(G.matb + ((size_t)(2 * kc) * G.mat_stride + u0 + t) * 8 + c);
+            if (2 * kc + 1 < (u32)NSRC) w1 = __ldg(G.matb + ((size_t)(2 * kc + 1) * G.mat_stride + u0 + t) * 8 + c);
+        }
+        *reinterpret_cast<ulonglong2 *>(sB + (n >> 3) * SBO + kc * 128 + (n & 7) * 16) = make_ulonglong2(w0, w1);
+    }
+    for (u32 t = tid; t < nt; t += TC_THREADS) spc[t] = A.pc[G.dst_prime[u0 + t]];
+    if (tid == 0) {
+        for (int b = 0; b < 2; b++) {
+            mbar_init(smem_u32(&bar_done[b]), 1);
+            mbar_init(smem_u32(&bar_empty[b]), 8);
+        }
+        for (int s = 0; s < TC_SA; s++) mbar_init(smem_u32(&bar_free[s]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_s)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // sB visible to the tensor core
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const u32 tmem = tmem_base_s;
+    pdl_wait();
+
+    if (warp >= 8) {
+        // ---------------- producers + MMA issuer ----------------
+        const u32 ptid = tid - 256;               // 0..127: coefficient row m of the tile
+        const u32 m = ptid;
+        const u32 soff = (m >> 3) * SBO + (m & 7) * 16;
+        const u64 *srcp[NSRC];
+#pragma unroll
+        for (int i = 0; i < NSRC; i++) srcp[i] = A.in + (size_t)G.src_slot[i] * N + m;
+        auto load_tile = [&](u32 j) {
+            const u32 st = j % TC_SA;
+            const size_t x0 = (size_t)(blockIdx.x + j * gridDim.x) << 7;
+            const u32 base = smem_u32(sA + st * ATILE) + soff;
+#pragma unroll
+            for (int i = 0; i < NSRC; i++) cp_async8(base + (i >> 1) * 128 + (i & 1) * 8, srcp[i] + x0);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        const u32 idesc = (2u << 4) | ((ncol >> 3) << 17) | ((128u >> 4) << 24);   // s32 += u8 x u8, K-major
+        for (u32 j = 0; j + 1 < TC_SA; j++) {   // TC_SA - 1 groups in flight (empty ones past the end)
+            if (j < ntile) load_tile(j);
+            else asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        for (u32 j = 0; j < ntile; j++) {
+            const u32 jn = j + TC_SA - 1;
+            if (jn < ntile) {
+                if (jn >= TC_SA) mbar_wait(smem_u32(&bar_free[jn % TC_SA]), (jn / TC_SA - 1) & 1);
+                load_tile(jn);
+            } else {
+                asm volatile("cp.async.commit_group;" ::: "memory");   // keep the group count uniform
+            }
+            asm volatile("cp.async.wait_group %0;" ::"n"(TC_SA - 1) : "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (ptid == 0) {
+                const u32 b = j & 1;
+                if (j >= 2) mbar_wait(smem_u32(&bar_empty[b]), ((j >> 1) - 1) & 1);
+                tc_fence_after();
+                const u32 abase = smem_u32(sA + (j % TC_SA) * ATILE), bbase = smem_u32(sB);
+#pragma unroll
+                for (int s = 0; s < KPAD / 32; s++)
+                    tc_mma_i8(tmem + b * 256, tc_desc(abase + s * 256, 128, SBO), tc_desc(bbase + s * 256, 128, SBO),
+                              idesc, s > 0 ? 1u : 0u);
+                tc_commit(smem_u32(&bar_free[j % TC_SA]));
+                tc_commit(smem_u32(&bar_done[b]));
+            }
+        }
+    } else {
+        // ---------------- epilogue ----------------
+        const u32 q = warp & 3, h = warp >> 2;
+        const u32 lrow = q * 32 + lane;           // TMEM lane = coefficient row of the tile
+        for (u32 j = 0; j < ntile; j++) {
+            const u32 b = j & 1;
+            mbar_wait(smem_u32(&bar_done[b]), (j >> 1) & 1);
+            tc_fence_after();
+            const size_t x = ((size_t)(blockIdx.x + j * gridDim.x) << 7) + lrow;
+            const u32 tbase = tmem + b * 256 + ((q * 32) << 16);
+            for (u32 t = h; t < nt; t += 4) {
+                u32 v[8], w[8];
+                const bool two = t + 2 < nt;
+                tc_ld8(tbase + t * 8, v);
+                if (two) tc_ld8(tbase + (t + 2) * 8, w);
+                tc_wait_ld();
+                const PrimeConst pc = spc[t];
+                A.out[(size_t)G.dst_slot[u0 + t] * N + x] =
+                    bytesum_reduce<LAZY>(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], pc);
+                if (two) {
+                    const PrimeConst pc2 = spc[t + 2];
+                    A.out[(size_t)G.dst_slot[u0 + t + 2] * N + x] =
+                        bytesum_reduce<LAZY>(w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], pc2);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bar_empty[b]));
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+template <int NSRC>
+static hks_status bconv_tc_go(const BconvArgs &a, cudaStream_t s) {
+    constexpr int KPAD = 32 * ((NSRC + 3) / 4);
+    const size_t smem = 256 * KPAD + TC_SA * 128 * KPAD;
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_bconv_tc<NSRC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_bconv_tc<NSRC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    const size_t N = (size_t)1 << a.log_n;
+    u32 maxdst = 0;
+    for (u32 g = 0; g < a.ngroups; g++) maxdst = max(maxdst, a.g[g].ndst);
+    const u32 nz = (maxdst + 31) / 32;
+    u32 tch = (maxdst + nz - 1) / nz;
+    tch = (tch + 1) & ~1u;
+    BconvArgs b = a;
+    b.cw = tch;
+    // one CTA per SM (512 TMEM columns each): split the SMs over (group, target chunk) pairs
+    const u32 pairs = a.ngroups * nz;
+    u32 gx = std::max<u32>(1, (u32)nsm / pairs);
+    gx = std::min<u32>(gx, (u32)(N >> 7));
+    ProfScope ps(K_BCONV, s);
+    cudaError_t e;
+    if (a.lazy_out)
+        e = hks_launch(k_bconv_tc<NSRC, true>, dim3(gx, a.ngroups, nz), dim3(TC_THREADS), smem, s, b);
+    else
+        e = hks_launch(k_bconv_tc<NSRC, false>, dim3(gx, a.ngroups, nz), dim3(TC_THREADS), smem, s, b);
+    double words = 0, macs = 0;
+    for (u32 g = 0; g < a.ngroups; g++) {
+        words += a.g[g].nsrc + a.g[g].ndst;
+        macs += (double)a.g[g].nsrc * a.g[g].ndst;
+    }
+    ps.done(words * (double)N * 8.0, macs * (double)N * 4.0);
+    if (e != cudaSuccess) HKS_FAIL(HKS_ECUDA, "k_bconv_tc launch: %s", cudaGetErrorString(e));
+    return HKS_OK;
+}
+
+// HKS_BCONV_TC=0 selects the warp-level IMMA kernel, HKS_BCONV_MMA=0 the integer-pipe kernels
+// (results identical).
+static bool getenv_tc_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("HKS_BCONV_TC");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 static bool getenv_mma_enabled() {
     static const bool on = [] {
         const char *e = getenv("HKS_BCONV_MMA");
@@ -487,14 +739,6 @@ static void bconv_go(const BconvArgs &a, cudaStream_t s) {
 
 hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
     // all groups of one launch share nsrc (the caller groups them so)
-    if (!a.prescale && a.big && a.g[0].matb && ((size_t)1 << a.log_n) >= MMA_CW && getenv_mma_enabled()) {
-        switch (a.g[0].nsrc) {
-#define CM(NS) case NS: bconv_mma_go<NS>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
-            CM(1) CM(2) CM(3) CM(4) CM(5) CM(6) CM(7) CM(8) CM(9) CM(10) CM(11) CM(12) CM(13) CM(14) CM(15) CM(16)
-#undef CM
-            default: break;
-        }
-    }
     if (!a.prescale && a.g[0].matf && getenv_fp_enabled()) {
         // FP64-pipe share chosen so both pipes carry similar work: 16 NINT + 56 ~ 18 NFP + 10 cycles
         switch (a.g[0].nsrc) {
@@ -509,6 +753,22 @@ hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
             case 14: bconv_fp_go<14, 8>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
             case 15: bconv_fp_go<15, 8>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
             case 16: bconv_fp_go<16, 9>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            default: break;
+        }
+    }
+    if (!a.prescale && a.big && a.g[0].matb && getenv_mma_enabled() && getenv_tc_enabled()) {
+        switch (a.g[0].nsrc) {
+#define CT(NS) case NS: return bconv_tc_go<NS>(a, s);
+            CT(1) CT(2) CT(3) CT(4) CT(5) CT(6) CT(7) CT(8) CT(9) CT(10) CT(11) CT(12) CT(13) CT(14) CT(15) CT(16)
+#undef CT
+            default: break;
+        }
+    }
+    if (!a.prescale && a.big && a.g[0].matb && ((size_t)1 << a.log_n) >= MMA_CW && getenv_mma_enabled()) {
+        switch (a.g[0].nsrc) {
+#define CM(NS) case NS: bconv_mma_go<NS>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
+            CM(1) CM(2) CM(3) CM(4) CM(5) CM(6) CM(7) CM(8) CM(9) CM(10) CM(11) CM(12) CM(13) CM(14) CM(15) CM(16)
+#undef CM
             default: break;
         }
     }

@@ -316,8 +316,12 @@ def test_relinearize_parity(orc, name, level):
     assert max(abs(v) for v in diff) <= ks_bound(o, level, keys.B_e, keys.h)
 
 
-def test_bconv_fp64_path_identical(orc):
-    """The FP64-assisted conversion (HKS_BCONV_FP=1) must produce the same KeySwitch bits."""
+@pytest.mark.parametrize("env", [{"HKS_BCONV_FP": "1"}, {"HKS_BCONV_TC": "0"}, {"HKS_BCONV_MMA": "0"},
+                                 {"HKS_BCONV_MMA": "0", "HKS_BCONV_KARA": "0"}],
+                         ids=["fp64", "imma", "int-kara", "int-plain"])
+def test_bconv_alternate_paths_identical(orc, env):
+    """Every base-conversion kernel (tcgen05 default; warp IMMA, integer Karatsuba / plain, FP64-assisted
+    behind switches) must produce the same KeySwitch bits as the oracle."""
     import subprocess, sys, os
     code = ("import sys; sys.path.insert(0, 'tests'); sys.path.insert(0, '.');"
             "import numpy as np, hks_synth as S, oracle; from helpers import *;"
@@ -327,8 +331,7 @@ def test_bconv_fp64_path_identical(orc):
             "c0=S.uniform_limbs(g,o.q,o.n); c1=S.uniform_limbs(g,o.q,o.n); a,b=empty_dev(c0.shape),empty_dev(c0.shape);"
             "H.keyswitch(ctx,to_dev(c0),to_dev(c1),29,to_dev(evk),a,b,ctx.workspace(H.OP_KEYSWITCH,29));"
             "w0,w1=o.keyswitch(c0,c1,evk,29); assert (to_host(a)==w0).all() and (to_host(b)==w1).all(); print('ok')")
-    env = dict(os.environ, HKS_BCONV_FP="1")
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True, timeout=600,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
