@@ -67,7 +67,7 @@ hks_status run_bconv_groups(const hks_ctx *c, std::vector<BconvGroup> &groups, c
 // groups converting src slots -> dst slots with a row-major matrix [nsrc][stride]; targets chunked by 64
 void add_groups(std::vector<BconvGroup> &out, u32 nsrc, const u16 *src_slot, const uint2 *mat, u32 stride,
                 const std::vector<u16> &dst_slot, const std::vector<u16> &dst_prime, const double *matf = nullptr,
-                const u32 *mats = nullptr, const u64 *matb = nullptr) {
+                const u32 *mats = nullptr, const u64 *matb = nullptr, const u64 *mimg = nullptr) {
     for (size_t u0 = 0; u0 < dst_slot.size(); u0 += BC_MAXDST) {
         BconvGroup g{};
         g.nsrc = nsrc;
@@ -77,6 +77,7 @@ void add_groups(std::vector<BconvGroup> &out, u32 nsrc, const u16 *src_slot, con
         g.matf = matf ? matf + 3 * u0 : nullptr;
         g.mats = mats ? mats + u0 : nullptr;
         g.matb = matb ? matb + 8 * u0 : nullptr;
+        g.mimg = mimg ? mimg + (size_t)bconv_img_words(nsrc) * u0 : nullptr;
         for (u32 i = 0; i < nsrc; i++) g.src_slot[i] = src_slot[i];
         for (u32 u = 0; u < g.ndst; u++) {
             g.dst_slot[u] = dst_slot[u0 + u];
@@ -113,7 +114,7 @@ hks_status modup_core(const hks_ctx *c, const u64 *d, u32 level, u64 *ext, u64 *
         }
         const size_t off = c->mu_mat_off[(size_t)level * c->dnum + j];
         add_groups(groups, hi - lo, src, c->d_mu_mat + off, (u32)ds.size(), ds, dp, c->d_mu_matf + 3 * off,
-                   c->d_mu_mats + off, c->d_mu_matb + 8 * off);
+                   c->d_mu_mats + off, c->d_mu_matb + 8 * off, c->d_mu_img + c->mu_img_off[(size_t)level * c->dnum + j]);
     }
     st = run_bconv_groups(c, groups, coef, ext, s);
     if (st != HKS_OK) return st;
@@ -170,7 +171,7 @@ hks_status moddown_core(const hks_ctx *c, const u64 *acc, u32 npoly, u32 level, 
         for (u32 k = 0; k < K; k++) src[k] = (u16)(p * K + k);
         std::vector<u16> ds(level + 1);
         for (u32 i = 0; i <= level; i++) ds[i] = (u16)(p * (level + 1) + i);
-        add_groups(groups, K, src, c->d_md_mat, c->nq, ds, dp, c->d_md_matf, c->d_md_mats, c->d_md_matb);
+        add_groups(groups, K, src, c->d_md_mat, c->nq, ds, dp, c->d_md_matf, c->d_md_mats, c->d_md_matb, c->d_md_img);
     }
     st = run_bconv_groups(c, groups, y, conv, s);
     if (st != HKS_OK) return st;

@@ -115,7 +115,7 @@ hks_status upload(T **dptr, const std::vector<T> &h) {
 
 void free_tables(hks_ctx *c) {
     void *ptrs[] = {c->d_pc, c->d_tw_col_fwd, c->d_tw_row_fwd, c->d_tw_col_inv, c->d_tw_row_inv, c->d_ninv,
-                    c->d_mu_scale, c->d_mu_mat, c->d_md_scale, c->d_md_mat, c->d_pinv, c->d_mu_matf, c->d_md_matf, c->d_mu_mats, c->d_md_mats, c->d_mu_matb, c->d_md_matb,
+                    c->d_mu_scale, c->d_mu_mat, c->d_md_scale, c->d_md_mat, c->d_pinv, c->d_mu_matf, c->d_md_matf, c->d_mu_mats, c->d_md_mats, c->d_mu_matb, c->d_md_matb, c->d_mu_img, c->d_md_img,
                     c->d_qmod, c->d_qlinv};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -203,9 +203,9 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     for (u32 i = 0; i < nm; i++) {
         u64 m = primes[i];
         u64 r64 = (u64)(((u128)1 << 64) % m);
-        const u64 r48 = (u64)(((u128)1 << 48) % m);
-        pc[i] = PrimeConst{m, r64, shoup_of(r64, m), (u64)(~0ull / m), r48, shoup_of(r48, m)};
-        if (m >> 32 == 0) c->all_big = false;
+        const u128 mu80 = ((u128)1 << 80) / m;   // used only when every prime > 2^49 (then < 2^31)
+        pc[i] = PrimeConst{m, r64, shoup_of(r64, m), (u64)(~0ull / m), mu80 >> 64 ? 0 : (u64)mu80};
+        if (m >> 49 == 0) c->all_big = false;   // the byte-sum reduction needs p > 2^49
         ninv[i] = sh(inv_mod(n % m, m), m);
     }
     // one_p = floor(2^64 / m) = floor((2^64 - 1) / m) since m does not divide 2^64.
@@ -310,6 +310,28 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     };
     std::vector<u32> mu_mats = sums(mu_mat), md_mats = sums(md_mat);
 
+    // k_bconv_tc B-operand images (internal.h bconv_img_words): image word (t, kc, c, h) = matb word
+    // (2kc + h, t, c), zero past the sources
+    auto image = [](const u64 *matb, u32 nsrc, u32 ntg, std::vector<u64> &out) {
+        const u32 nch = bconv_img_words(nsrc) / 16;
+        for (u32 t = 0; t < ntg; t++)
+            for (u32 kc = 0; kc < nch; kc++)
+                for (u32 cc = 0; cc < 8; cc++)
+                    for (u32 hh = 0; hh < 2; hh++) {
+                        const u32 i = 2 * kc + hh;
+                        out.push_back(i < nsrc ? matb[((size_t)i * ntg + t) * 8 + cc] : 0);
+                    }
+    };
+    std::vector<u64> mu_img, md_img;
+    c->mu_img_off.assign((size_t)num_q * dnum, 0);
+    for (u32 lv = 0; lv <= L; lv++)
+        for (u32 j = 0; j < c->beta(lv); j++) {
+            const u32 lo = c->digit_lo(j), hi = c->digit_hi(lv, j), ntg = c->ne(lv) - (hi - lo);
+            c->mu_img_off[(size_t)lv * dnum + j] = mu_img.size();
+            image(mu_matb.data() + 8 * c->mu_mat_off[(size_t)lv * dnum + j], hi - lo, ntg, mu_img);
+        }
+    image(md_matb.data(), num_p, num_q, md_img);
+
     hks_status st = HKS_OK;
 #define UP(dst, src) if (st == HKS_OK) st = upload(&c->dst, src)
     UP(d_pc, pc);
@@ -328,6 +350,8 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     UP(d_mu_mats, mu_mats);
     UP(d_mu_matb, mu_matb);
     UP(d_md_matb, md_matb);
+    UP(d_mu_img, mu_img);
+    UP(d_md_img, md_img);
     UP(d_md_mats, md_mats);
     UP(d_qmod, qmod);
     UP(d_qlinv, qlinv);

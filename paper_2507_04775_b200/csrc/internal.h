@@ -83,6 +83,8 @@ struct BconvGroup {
     const uint2 *mat;          // [nsrc][mat_stride] (lo30, hi30) of [qhat_i]_t, column u = target u
     const double *matf;        // same entries as three exact 20-bit limbs [nsrc][mat_stride][3] (FP64 path) or NULL
     const u32 *mats;           // (lo30 + hi30) of each entry [nsrc][mat_stride] (Karatsuba path) or NULL
+    const u64 *mimg;           // k_bconv_tc: shared-memory image of the B operand from this group's first target
+                               // on (bconv_img_words(nsrc) words per target; see ctx.cu) or NULL
     const u64 *matb;           // byte-column words [nsrc][mat_stride][8] (tensor-pipe path, k_bconv_mma) or NULL:
                                // word c of entry (i, u) has byte a = byte c of (2^(8a) [qhat_i]_t mod t)
     u16 src_slot[BC_MAXSRC];
@@ -93,6 +95,10 @@ struct BconvGroup {
     u16 dst_prime[BC_MAXDST];
 };
 
+// k_bconv_tc B operand: per target, NCH = 2 ceil(nsrc / 4) K-chunks of 8 rows (byte columns c) x 16
+// bytes (words (2kc, t, c), (2kc + 1, t, c)), i.e. the canonical no-swizzle K-major UMMA layout
+__host__ __device__ constexpr u32 bconv_img_words(u32 nsrc) { return 2 * ((nsrc + 3) / 4) * 16; }
+
 struct BconvArgs {
     const u64 *in;
     u64 *out;
@@ -101,7 +107,7 @@ struct BconvArgs {
     u32 ngroups;
     u32 prescale;              // 1: apply pre_w (inputs raw COEFF), 0: inputs are canonical y_i
     u32 lazy_out;              // 1: outputs in [0, 8t) (consumer: forward NTT), 0: canonical
-    u32 big;                   // 1: every prime > 2^32 (required by the tensor-pipe kernel k_bconv_mma)
+    u32 big;                   // 1: every prime > 2^49 (required by the tensor-pipe kernels k_bconv_tc / _mma)
     u32 cw;                    // k_bconv_mma: coefficients per CTA (set by the launcher)
     BconvGroup g[BC_MAXG];
 };
@@ -202,7 +208,7 @@ hks_status run_ntt_kip(const hks_ctx *ctx, const std::vector<KipItem> &items, u3
 struct hks_ctx {
     u32 log_n, n, log_r, log_c, nq, np, dnum, alpha;
     int device;
-    bool all_big = true;        // every prime > 2^32
+    bool all_big = true;        // every prime > 2^49 (tensor-pipe base conversion)
     std::vector<u64> primes, psi;
 
     // host mirrors of the small tables (offsets into the device arrays)
@@ -224,6 +230,9 @@ struct hks_ctx {
     double *d_md_matf = nullptr;        // ModDown matrix as 20-bit limbs in doubles
     u64 *d_mu_matb = nullptr;           // ModUp matrices as byte-column words, 8 per entry (k_bconv_mma)
     u64 *d_md_matb = nullptr;           // ModDown matrix as byte-column words, 8 per entry
+    std::vector<size_t> mu_img_off;     // [(L+1) * dnum]: word offset of the (level, digit) B image in d_mu_img
+    u64 *d_mu_img = nullptr;            // ModUp matrices as k_bconv_tc B-operand images (per target contiguous)
+    u64 *d_md_img = nullptr;            // ModDown matrix as a k_bconv_tc B-operand image
     ulonglong2 *d_pinv = nullptr;       // P^-1 mod q_i  [L+1] (Shoup)
     u64 *d_qmod = nullptr;              // Rescale: q_j mod q_i  [L+1][L+1] (row j = dropped limb)
     ulonglong2 *d_qlinv = nullptr;      // Rescale: q_j^-1 mod q_i (Shoup)  [L+1][L+1]

@@ -357,15 +357,19 @@ static void bconv_mma_go(const BconvArgs &a, cudaStream_t s) {
 // so TMEM lane m holds, in 8 consecutive columns, the eight S_{t,c} of coefficient m and target t:
 // one tcgen05.ld (32x32b.x8) per output.  Persistent CTAs (one per SM, 512 TMEM columns = two
 // accumulators), warp roles:
-//   warps 0-7  epilogue: TMEM -> registers -> bytesum_reduce -> coalesced stores (warp w: lanes
-//              32 (w % 4) .. +31, targets t = w / 4 (mod 2))
-//   warps 8-11 producers: cp.async of the next tiles' input words into TC_SA shared stages; thread
-//              256 issues the tcgen05.mma of a tile (K / 32 instructions) and commits to mbarriers.
+//   warps 0 .. TC_EPW-1  epilogue: TMEM -> registers -> bytesum_reduce -> coalesced stores (warp w:
+//              lanes 32 (w % 4) .. +31, targets t = w / 4 (mod TC_EPW / 4), four targets in flight)
+//   next 4 warps producers: cp.async of the next tiles' input words into TC_SA shared stages; their
+//              first thread issues the tcgen05.mma of a tile (K / 32 instructions) and commits.
 #ifndef HKS_TC_SA
 #define HKS_TC_SA 4
 #endif
+#ifndef HKS_TC_EPW
+#define HKS_TC_EPW 16
+#endif
 #define TC_SA HKS_TC_SA
-#define TC_THREADS 384
+#define TC_EPW HKS_TC_EPW                  // epilogue warps (multiple of 4)
+#define TC_THREADS ((TC_EPW + 4) * 32)
 
 __device__ __forceinline__ u32 smem_u32(const void *p) { return (u32)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(u32 a, u32 count) {
@@ -435,24 +439,38 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constan
     uint8_t *sA = tsm + 256 * KPAD;                      // TC_SA x ATILE
     __shared__ __align__(8) u64 bar_done[2], bar_empty[2], bar_free[TC_SA];
     __shared__ u32 tmem_base_s;
-    __shared__ PrimeConst spc[32];
+    __shared__ ulonglong2 sred[32];                // per target: (2^64 - p, floor(2^80 / p))
+    __shared__ u64 *sdst[32];                       // per target: output limb
     const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     // ---- prologue (before griddepcontrol.wait: ctx tables only) ----
-    for (u32 idx = tid; idx < 256 * NCH; idx += TC_THREADS) {
-        const u32 n = idx / NCH, kc = idx - n * NCH, t = n >> 3, c = n & 7;
-        u64 w0 = 0, w1 = 0;
-        if (t < nt) {
-            if (2 * kc < (u32)NSRC) w0 = __ldg(G.matb + ((size_t)(2 * kc) * G.mat_stride + u0 + t) * 8 + c);
-            if (2 * kc + 1 < (u32)NSRC) w1 = __ldg(G.matb + ((size_t)(2 * kc + 1) * G.mat_stride + u0 + t) * 8 + c);
+    {
+        // B operand: the group's precomputed image (nt targets x SBO bytes, contiguous) plus zero rows for
+        // the padding target of an odd nt; 16-byte loads all issued before the stores
+        const uint4 *img = reinterpret_cast<const uint4 *>(G.mimg + (size_t)bconv_img_words(NSRC) * u0);
+        const u32 nimg = nt * (SBO / 16), ntot = (ncol / 8) * (SBO / 16);
+        constexpr int PER = (32 * (SBO / 16) + TC_THREADS - 1) / TC_THREADS;
+        uint4 w[PER];
+#pragma unroll
+        for (int r = 0; r < PER; r++) {
+            const u32 idx = tid + r * TC_THREADS;
+            w[r] = idx < nimg ? __ldg(img + idx) : make_uint4(0, 0, 0, 0);
         }
-        *reinterpret_cast<ulonglong2 *>(sB + (n >> 3) * SBO + kc * 128 + (n & 7) * 16) = make_ulonglong2(w0, w1);
+#pragma unroll
+        for (int r = 0; r < PER; r++) {
+            const u32 idx = tid + r * TC_THREADS;
+            if (idx < ntot) reinterpret_cast<uint4 *>(sB)[idx] = w[r];
+        }
     }
-    for (u32 t = tid; t < nt; t += TC_THREADS) spc[t] = A.pc[G.dst_prime[u0 + t]];
+    for (u32 t = tid; t < nt; t += TC_THREADS) {
+        const PrimeConst pc = A.pc[G.dst_prime[u0 + t]];
+        sred[t] = make_ulonglong2(0 - pc.p, pc.mu80);
+        sdst[t] = A.out + (size_t)G.dst_slot[u0 + t] * N;
+    }
     if (tid == 0) {
         for (int b = 0; b < 2; b++) {
             mbar_init(smem_u32(&bar_done[b]), 1);
-            mbar_init(smem_u32(&bar_empty[b]), 8);
+            mbar_init(smem_u32(&bar_empty[b]), TC_EPW);
         }
         for (int s = 0; s < TC_SA; s++) mbar_init(smem_u32(&bar_free[s]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -468,9 +486,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constan
     const u32 tmem = tmem_base_s;
     pdl_wait();
 
-    if (warp >= 8) {
+    if (warp >= TC_EPW) {
         // ---------------- producers + MMA issuer ----------------
-        const u32 ptid = tid - 256;               // 0..127: coefficient row m of the tile
+        const u32 ptid = tid - TC_EPW * 32;       // 0..127: coefficient row m of the tile
         const u32 m = ptid;
         const u32 soff = (m >> 3) * SBO + (m & 7) * 16;
         const u64 *srcp[NSRC];
@@ -515,6 +533,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constan
         }
     } else {
         // ---------------- epilogue ----------------
+        constexpr u32 NH = TC_EPW / 4;           // warps sharing a TMEM lane quarter
         const u32 q = warp & 3, h = warp >> 2;
         const u32 lrow = q * 32 + lane;           // TMEM lane = coefficient row of the tile
         for (u32 j = 0; j < ntile; j++) {
@@ -523,19 +542,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constan
             tc_fence_after();
             const size_t x = ((size_t)(blockIdx.x + j * gridDim.x) << 7) + lrow;
             const u32 tbase = tmem + b * 256 + ((q * 32) << 16);
-            for (u32 t = h; t < nt; t += 4) {
-                u32 v[8], w[8];
-                const bool two = t + 2 < nt;
-                tc_ld8(tbase + t * 8, v);
-                if (two) tc_ld8(tbase + (t + 2) * 8, w);
+            for (u32 t0 = h; t0 < nt; t0 += 4 * NH) {
+                u32 v[4][8];
+#pragma unroll
+                for (int k = 0; k < 4; k++)
+                    if (t0 + k * NH < nt) tc_ld8(tbase + (t0 + k * NH) * 8, v[k]);
                 tc_wait_ld();
-                const PrimeConst pc = spc[t];
-                A.out[(size_t)G.dst_slot[u0 + t] * N + x] =
-                    bytesum_reduce<LAZY>(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], pc);
-                if (two) {
-                    const PrimeConst pc2 = spc[t + 2];
-                    A.out[(size_t)G.dst_slot[u0 + t + 2] * N + x] =
-                        bytesum_reduce<LAZY>(w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], pc2);
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const u32 t = t0 + k * NH;
+                    if (t < nt) {
+                        const ulonglong2 c = sred[t];
+                        sdst[t][x] = bytesum_reduce_c<LAZY>(v[k], c.x, (u32)c.y);
+                    }
                 }
             }
             tc_fence_before();
@@ -756,7 +775,7 @@ hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
             default: break;
         }
     }
-    if (!a.prescale && a.big && a.g[0].matb && getenv_mma_enabled() && getenv_tc_enabled()) {
+    if (!a.prescale && a.big && a.g[0].mimg && getenv_mma_enabled() && getenv_tc_enabled()) {
         switch (a.g[0].nsrc) {
 #define CT(NS) case NS: return bconv_tc_go<NS>(a, s);
             CT(1) CT(2) CT(3) CT(4) CT(5) CT(6) CT(7) CT(8) CT(9) CT(10) CT(11) CT(12) CT(13) CT(14) CT(15) CT(16)

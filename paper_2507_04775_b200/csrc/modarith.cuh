@@ -35,8 +35,7 @@ struct PrimeConst {
     u64 r64;     // 2^64 mod p
     u64 r64p;    // Shoup companion of r64
     u64 one_p;   // floor(2^64 / p): Shoup companion of 1
-    u64 r48;     // 2^48 mod p (tensor-pipe base conversion epilogue)
-    u64 r48p;    // Shoup companion of r48
+    u64 mu80;    // floor(2^80 / p) (< 2^32 for p > 2^48): byte-sum reduction of the tensor-pipe BConv
 };
 
 // 128-bit accumulator of 30-bit-split products:  X = s2*2^60 + (s1a + s1b)*2^30 + s0.
@@ -377,57 +376,52 @@ HKS_DEV u64 shoup_u32(u32 y, u64 w, u64 wp, u64 np) {
     return ((u64)rh << 32) | (u32)r;
 }
 
-// X' = sum_c S_c 2^(8c) (S_c < 2^23, c = 0..7) reduced modulo p > 2^32: [0, 6p) lazily, else
-// canonical.  X' = A + B 2^48 with A = T01 + T23 2^16 + T45 2^32 < 2^64 and B = T67 < 2^32, where
-// T_{c,c+1} = S_c + S_{c+1} 2^8;  X' == (A mod p) + B [2^48]_p: one 64-bit and one 32x60-bit Shoup step.
+// X' = sum_c S_c 2^(8c) (S_c < 2^23, c = 0..7, so X' < 2^80) reduced modulo p, 2^49 < p < 2^60:
+// [0, 3p) lazily, else canonical.  X' = a + T67 2^48 with a = T01 + T23 2^16 + T45 2^32 < 2^64 and
+// T_{c,c+1} = S_c + S_{c+1} 2^8 < 2^32.  Quotient estimate q = floor((X' >> 48) mu / 2^32) with
+// mu = floor(2^80 / p): q <= X'/p < q + 3 (truncations cost < 1 + 2^48/p), so X' - q p < 3p is
+// exact in 64-bit arithmetic.  14 instructions.
 template <bool LAZY>
-HKS_DEV u64 bytesum_reduce(u32 s0, u32 s1, u32 s2, u32 s3, u32 s4, u32 s5, u32 s6, u32 s7, const PrimeConst &c) {
+HKS_DEV u64 bytesum_reduce_c(u32 s0, u32 s1, u32 s2, u32 s3, u32 s4, u32 s5, u32 s6, u32 s7, u64 np, u32 mu) {
     u64 r;
-    // 19 instructions: 4 byte-pair merges, the 64-bit A, its approximate quotient (one_p < 2^32) and
-    // A - q p, the exact Shoup product B [2^48]_p, one 64-bit add.
     asm("{\n\t"
-        ".reg .u32 t01, t23, t45, t67, x, al, ah, q, t1, q2, rl, rh, w0, w1, n0, n1, f0, f1, o0;\n\t"
-        ".reg .u64 qq, rr, aa, r2;\n\t"
+        ".reg .u32 t01, t23, t45, t67, x, al, ah, top, q, rl, rh, n0, n1;\n\t"
+        ".reg .u64 w, aa, rr;\n\t"
         "mad.lo.u32 t01, %2, 256, %1;\n\t"
         "mad.lo.u32 t23, %4, 256, %3;\n\t"
         "mad.lo.u32 t45, %6, 256, %5;\n\t"
         "mad.lo.u32 t67, %8, 256, %7;\n\t"
-        "shl.b32 x, t23, 16;\n\t"
-        "add.cc.u32 al, t01, x;\n\t"
-        "shr.u32 x, t23, 16;\n\t"
-        "addc.u32 ah, t45, x;\n\t"
-        "mov.b64 {n0, n1}, %9;\n\t"          // 2^64 - p
-        "cvt.u32.u64 o0, %10;\n\t"           // one_p (< 2^32)
-        "mul.hi.u32 q, ah, o0;\n\t"
+        "mul.wide.u32 w, t23, 65536;\n\t"
+        "mov.b64 {al, ah}, w;\n\t"
+        "add.cc.u32 al, al, t01;\n\t"
+        "addc.u32 ah, ah, t45;\n\t"                 // a = (al, ah)
+        "shr.u32 x, ah, 16;\n\t"
+        "add.u32 top, x, t67;\n\t"                  // X' >> 48
+        "mad.lo.u32 ah, t67, 65536, ah;\n\t"        // X' mod 2^64
+        "mul.hi.u32 q, top, %10;\n\t"
+        "mov.b64 {n0, n1}, %9;\n\t"                 // 2^64 - p
         "mov.b64 aa, {al, ah};\n\t"
         "mad.wide.u32 rr, q, n0, aa;\n\t"
         "mov.b64 {rl, rh}, rr;\n\t"
         "mad.lo.u32 rh, q, n1, rh;\n\t"
-        "mov.b64 {w0, w1}, %11;\n\t"         // r48
-        "mov.b64 {f0, f1}, %12;\n\t"         // r48'
-        "mul.hi.u32 t1, t67, f0;\n\t"
-        "cvt.u64.u32 qq, t1;\n\t"
-        "mad.wide.u32 qq, t67, f1, qq;\n\t"
-        "mov.b64 {x, q2}, qq;\n\t"
-        "mul.wide.u32 r2, t67, w0;\n\t"
-        "mad.wide.u32 r2, q2, n0, r2;\n\t"
-        "mov.b64 {x, t1}, r2;\n\t"
-        "mad.lo.u32 t1, t67, w1, t1;\n\t"
-        "mad.lo.u32 t1, q2, n1, t1;\n\t"
-        "cvt.u32.u64 x, r2;\n\t"
-        "add.cc.u32 rl, rl, x;\n\t"
-        "addc.u32 rh, rh, t1;\n\t"
         "mov.b64 %0, {rl, rh};\n\t"
         "}"
         : "=l"(r)
-        : "r"(s0), "r"(s1), "r"(s2), "r"(s3), "r"(s4), "r"(s5), "r"(s6), "r"(s7), "l"(0 - c.p), "l"(c.one_p),
-          "l"(c.r48), "l"(c.r48p));
+        : "r"(s0), "r"(s1), "r"(s2), "r"(s3), "r"(s4), "r"(s5), "r"(s6), "r"(s7), "l"(np), "r"(mu));
     if (!LAZY) {
-        r = csub(r, 4 * c.p);
-        r = csub(r, 2 * c.p);
-        r = csub(r, c.p);
+        const u64 p = 0 - np;
+        r = csub(r, 2 * p);
+        r = csub(r, p);
     }
     return r;
+}
+template <bool LAZY>
+HKS_DEV u64 bytesum_reduce(u32 s0, u32 s1, u32 s2, u32 s3, u32 s4, u32 s5, u32 s6, u32 s7, const PrimeConst &c) {
+    return bytesum_reduce_c<LAZY>(s0, s1, s2, s3, s4, s5, s6, s7, 0 - c.p, (u32)c.mu80);
+}
+template <bool LAZY>
+HKS_DEV u64 bytesum_reduce_c(const u32 (&v)[8], u64 np, u32 mu) {
+    return bytesum_reduce_c<LAZY>(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], np, mu);
 }
 
 HKS_DEV u64 acc_reduce_lazy(const Acc30 &a, const PrimeConst &c) {

@@ -79,7 +79,7 @@ hks_status bconv_groups(const hks_ctx *c, std::vector<BconvGroup> &groups, const
 }
 
 void push_group(std::vector<BconvGroup> &out, u32 nsrc, const u16 *src_slot, const uint2 *mat, u32 stride,
-                const std::vector<u16> &ds, const std::vector<u16> &dp, const double *matf, const u32 *mats, const u64 *matb) {
+                const std::vector<u16> &ds, const std::vector<u16> &dp, const double *matf, const u32 *mats, const u64 *matb, const u64 *mimg) {
     for (size_t u0 = 0; u0 < ds.size(); u0 += BC_MAXDST) {
         BconvGroup g{};
         g.nsrc = nsrc;
@@ -89,6 +89,7 @@ void push_group(std::vector<BconvGroup> &out, u32 nsrc, const u16 *src_slot, con
         g.matf = matf ? matf + 3 * u0 : nullptr;
         g.mats = mats ? mats + u0 : nullptr;
         g.matb = matb ? matb + 8 * u0 : nullptr;
+        g.mimg = mimg ? mimg + (size_t)bconv_img_words(nsrc) * u0 : nullptr;
         for (u32 i = 0; i < nsrc; i++) g.src_slot[i] = src_slot[i];
         for (u32 u = 0; u < g.ndst; u++) { g.dst_slot[u] = ds[u0 + u]; g.dst_prime[u] = dp[u0 + u]; }
         out.push_back(g);
@@ -168,13 +169,15 @@ extern "C" hks_status hks_shard_ks_inner(const hks_ctx *c, uint32_t level, uint3
         const double *matf = c->d_mu_matf + 3 * moff;
         const u32 *mats = c->d_mu_mats + moff;
         const u64 *matb = c->d_mu_matb + 8 * moff;
+        const u64 *mimg = c->d_mu_img + c->mu_img_off[(size_t)level * c->dnum + j];
+        const u32 imgw = bconv_img_words(hi - lo);
         const u32 ntg = ne - (hi - lo);
         // contiguous runs of column positions
         std::vector<u16> ds, dp;
         int run_col = -1;
         auto flush = [&]() {
             if (!ds.empty()) push_group(groups, hi - lo, src, mat + run_col, ntg, ds, dp, matf + 3 * run_col, mats + run_col,
-                                         matb + 8 * run_col);
+                                         matb + 8 * run_col, mimg + (size_t)imgw * run_col);
             ds.clear(); dp.clear(); run_col = -1;
         };
         int prev_col = -2;
@@ -238,7 +241,7 @@ extern "C" hks_status hks_shard_ks_moddown_out(const hks_ctx *c, uint32_t level,
         std::vector<u16> ds(P.nq_act), dp(P.nq_act);
         for (u32 li = 0; li < P.nq_act; li++) { ds[li] = (u16)(p * P.nq_act + li); dp[li] = (u16)(P.q_lo + li); }
         push_group(groups, K, src, c->d_md_mat + P.q_lo, c->nq, ds, dp, c->d_md_matf + 3 * P.q_lo, c->d_md_mats + P.q_lo,
-                   c->d_md_matb + 8 * P.q_lo);
+                   c->d_md_matb + 8 * P.q_lo, c->d_md_img + (size_t)bconv_img_words(K) * P.q_lo);
     }
     if ((st = bconv_groups(c, groups, ypall, conv, s)) != HKS_OK) return st;
     LimbList M;
