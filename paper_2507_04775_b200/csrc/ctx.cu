@@ -115,7 +115,7 @@ hks_status upload(T **dptr, const std::vector<T> &h) {
 
 void free_tables(hks_ctx *c) {
     void *ptrs[] = {c->d_pc, c->d_tw_col_fwd, c->d_tw_row_fwd, c->d_tw_col_inv, c->d_tw_row_inv, c->d_ninv,
-                    c->d_mu_scale, c->d_mu_mat, c->d_md_scale, c->d_md_mat, c->d_pinv, c->d_mu_matf, c->d_md_matf, c->d_mu_mats, c->d_md_mats, c->d_mu_matb, c->d_md_matb, c->d_mu_img, c->d_md_img,
+                    c->d_mu_scale, c->d_mu_mat, c->d_md_scale, c->d_md_mat, c->d_pinv, c->d_mu_matf, c->d_md_matf, c->d_mu_mats, c->d_md_mats, c->d_mu_matb, c->d_md_matb, c->d_mu_img, c->d_md_img, c->d_ntt_img_fwd, c->d_ntt_img_inv,
                     c->d_qmod, c->d_qlinv};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -323,6 +323,60 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
                     }
     };
     std::vector<u64> mu_img, md_img;
+    // column-pass matrices for the tensor-core NTT (log N = 16 only; R = C = 256): the butterfly stages of
+    // the pass (the same twiddles as k_ntt) applied to unit vectors, so the two 16-point rounds compose to
+    // exactly the column pass's linear map
+    std::vector<u64> ntt_img_fwd, ntt_img_inv;
+    if (log_n == 16) {
+        ntt_img_fwd.reserve((size_t)nm * 17 * NTT16_IMG);
+        ntt_img_inv.reserve((size_t)nm * 17 * NTT16_IMG);
+        for (u32 pi = 0; pi < nm; pi++) {
+            const u64 m = primes[pi];
+            const ulonglong2 *twf = &tcf[(size_t)pi * R], *twi = &tci[(size_t)pi * R];
+            // stages [s_first, s_last] of the 256-row column transform on a unit vector at row `row`
+            auto run = [&](bool fwd, int s_from, int s_to, u32 row, std::vector<u64> &v) {
+                v.assign(R, 0);
+                v[row] = 1;
+                const int step = fwd ? 1 : -1;
+                for (int st = s_from;; st += step) {
+                    const u32 mm = 1u << st, t = R >> (st + 1);
+                    for (u32 i = 0; i < mm; i++) {
+                        const u64 w = fwd ? twf[mm + i].x : twi[mm + i].x;
+                        for (u32 jj = i * 2 * t; jj < i * 2 * t + t; jj++) {
+                            const u64 X = v[jj], Y = v[jj + t];
+                            if (fwd) {
+                                const u64 wy = mul_mod(Y, w, m);
+                                v[jj] = (X + wy) % m;
+                                v[jj + t] = (X + m - wy) % m;
+                            } else {
+                                v[jj] = (X + Y) % m;
+                                v[jj + t] = mul_mod((X + m - Y) % m, w, m);
+                            }
+                        }
+                    }
+                    if (st == s_to) break;
+                }
+            };
+            // matrix W[k'][k] of rows {base + str k} -> {base + str k'} as an image (targets k', sources k)
+            auto emit = [&](bool fwd, int s_from, int s_to, u32 base, u32 str, std::vector<u64> &out) {
+                std::vector<u64> words((size_t)16 * 16 * 8);   // matb layout [k][k'][c]
+                std::vector<u64> v, w8;
+                for (u32 k = 0; k < 16; k++) {
+                    run(fwd, s_from, s_to, base + str * k, v);
+                    for (u32 kk = 0; kk < 16; kk++) {
+                        w8.clear();
+                        push_bytecols(w8, v[base + str * kk], m);
+                        std::copy(w8.begin(), w8.end(), words.begin() + ((size_t)k * 16 + kk) * 8);
+                    }
+                }
+                image(words.data(), 16, 16, out);
+            };
+            emit(true, 0, 3, 0, 16, ntt_img_fwd);
+            for (u32 b = 0; b < 16; b++) emit(true, 4, 7, 16 * b, 1, ntt_img_fwd);
+            for (u32 b = 0; b < 16; b++) emit(false, 7, 4, 16 * b, 1, ntt_img_inv);
+            emit(false, 3, 0, 0, 16, ntt_img_inv);
+        }
+    }
     c->mu_img_off.assign((size_t)num_q * dnum, 0);
     for (u32 lv = 0; lv <= L; lv++)
         for (u32 j = 0; j < c->beta(lv); j++) {
@@ -352,6 +406,8 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     UP(d_md_matb, md_matb);
     UP(d_mu_img, mu_img);
     UP(d_md_img, md_img);
+    UP(d_ntt_img_fwd, ntt_img_fwd);
+    UP(d_ntt_img_inv, ntt_img_inv);
     UP(d_md_mats, md_mats);
     UP(d_qmod, qmod);
     UP(d_qlinv, qlinv);

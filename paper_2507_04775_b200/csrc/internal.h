@@ -99,6 +99,8 @@ struct BconvGroup {
 // bytes (words (2kc, t, c), (2kc + 1, t, c)), i.e. the canonical no-swizzle K-major UMMA layout
 __host__ __device__ constexpr u32 bconv_img_words(u32 nsrc) { return 2 * ((nsrc + 3) / 4) * 16; }
 
+#define NTT16_IMG 2048   // words per 16 x 16 column-pass matrix image (bconv_img_words(16) * 16 targets)
+
 struct BconvArgs {
     const u64 *in;
     u64 *out;
@@ -233,6 +235,10 @@ struct hks_ctx {
     std::vector<size_t> mu_img_off;     // [(L+1) * dnum]: word offset of the (level, digit) B image in d_mu_img
     u64 *d_mu_img = nullptr;            // ModUp matrices as k_bconv_tc B-operand images (per target contiguous)
     u64 *d_md_img = nullptr;            // ModDown matrix as a k_bconv_tc B-operand image
+    // k_ntt16_tc (log N = 16): per prime 17 B-operand images (NTT16_IMG words each) of the 16 x 16 matrices
+    // of the column pass -- forward: [0] stages 0-3 on a stride-16 class, [1 + b] stages 4-7 on rows
+    // 16b..16b+15; inverse: [b] GS stages 7-4 on block b, [16] GS stages 3-0 on a class
+    u64 *d_ntt_img_fwd = nullptr, *d_ntt_img_inv = nullptr;
     ulonglong2 *d_pinv = nullptr;       // P^-1 mod q_i  [L+1] (Shoup)
     u64 *d_qmod = nullptr;              // Rescale: q_j mod q_i  [L+1][L+1] (row j = dropped limb)
     ulonglong2 *d_qlinv = nullptr;      // Rescale: q_j^-1 mod q_i (Shoup)  [L+1][L+1]
@@ -333,5 +339,9 @@ hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, const std::vec
 hks_status run_rescale(const hks_ctx *ctx, u32 npoly, u32 level, const u64 *x, const u64 *coef, u64 *buf,
                        u64 *const *outs, cudaStream_t s);
 hks_status launch_bconv(const BconvArgs &a, u32 max_ndst, cudaStream_t s);
+// column pass of the log N = 16 NTT on the tensor cores (kernels.cu k_ntt16_tc): forward EPI_LAZY or
+// inverse EPI_SCALE, same limb map / scale semantics as launch_ntt_pass
+hks_status launch_ntt_cols_tc(const hks_ctx *ctx, NttDir dir, int epi, const NttArgs &a, cudaStream_t s);
+bool ntt_tc_enabled();
 hks_status launch_kip(const KipArgs &a, cudaStream_t s);
 hks_status launch_automorph(const u64 *in, u64 *out, u32 nlimbs, u32 log_n, u64 galois, cudaStream_t s);

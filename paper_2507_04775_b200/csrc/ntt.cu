@@ -382,6 +382,9 @@ hks_status launch_ntt_pass(const hks_ctx *ctx, NttDir dir, int pass, int epi, Nt
     a.log_r = ctx->log_r;
     a.log_c = ctx->log_c;
     const bool cols = (dir == NTT_FWD) ? (pass == 0) : (pass == 1);
+    if (cols && ctx->log_n == 16 && ctx->all_big && ctx->d_ntt_img_fwd && ntt_tc_enabled() &&
+        ((dir == NTT_FWD && epi == EPI_LAZY) || (dir == NTT_INV && epi == EPI_SCALE)))
+        return launch_ntt_cols_tc(ctx, dir, epi, a, s);
     const bool small = a.nlimbs * 16u < HKS_SMALL_LIMIT;
     switch (ctx->log_n) {
         case 17: return small ? dispatch<9, 3, 3, 8, 3, 4>(dir, cols, epi, a, s) : dispatch<9, 4, 3, 8, 4, 4>(dir, cols, epi, a, s);
