@@ -317,11 +317,12 @@ def test_relinearize_parity(orc, name, level):
 
 
 @pytest.mark.parametrize("env", [{"HKS_BCONV_FP": "1"}, {"HKS_BCONV_TC": "0"}, {"HKS_BCONV_MMA": "0"},
-                                 {"HKS_BCONV_MMA": "0", "HKS_BCONV_KARA": "0"}],
-                         ids=["fp64", "imma", "int-kara", "int-plain"])
+                                 {"HKS_BCONV_MMA": "0", "HKS_BCONV_KARA": "0"}, {"HKS_NTT_TC": "1"}],
+                         ids=["fp64", "imma", "int-kara", "int-plain", "ntt-tensor-cols"])
 def test_bconv_alternate_paths_identical(orc, env):
     """Every base-conversion kernel (tcgen05 default; warp IMMA, integer Karatsuba / plain, FP64-assisted
-    behind switches) must produce the same KeySwitch bits as the oracle."""
+    behind switches) and the tensor-core NTT column pass (opt-in) must produce the same KeySwitch bits as
+    the oracle."""
     import subprocess, sys, os
     code = ("import sys; sys.path.insert(0, 'tests'); sys.path.insert(0, '.');"
             "import numpy as np, hks_synth as S, oracle; from helpers import *;"
