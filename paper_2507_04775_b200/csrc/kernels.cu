@@ -1,11 +1,12 @@
-// kernels.cu -- base conversion (Eq. 1), evaluation-key inner product, EVAL automorphism.
+// kernels.cu -- base conversion (Eq. 1), evaluation-key inner product, EVAL automorphism, and the
+// tensor-core column pass of the NTT (opt-in).
 //
-// All three are cross-limb, same-coefficient passes (§3.6.1 dependency classes):
-// a thread owns two consecutive coefficients (16-byte vector loads/stores along the limb) and
-// loops over limbs.  They are integer-bound, not dense contractions, so no tensor cores: every
-// 60x60-bit product is four IMAD.WIDE.U32 on 30-bit halves accumulated carry-free in 64-bit
-// registers, reduced once per output (the paper's "128-bit accumulation, one reduction per
-// output").
+// All are cross-limb, same-coefficient passes (§3.6.1 dependency classes).  The base
+// conversion is, across the N coefficients, a dense contraction with a constant matrix, and runs on the
+// tcgen05 tensor cores through an exact byte-split identity (k_bconv_tc); the warp-level
+// IMMA and the integer-pipe kernels (30-bit-split IMAD.WIDE MACs, "128-bit accumulation, one reduction
+// per output") remain behind switches and are tested for identical bits.  The key inner
+// product is element-wise (no shared operand) and stays on the integer pipe.
 #include <stdlib.h>
 
 #include "internal.h"
