@@ -45,6 +45,10 @@ def parse():
     ap.add_argument("--quick", action="store_true", help="skip e2e / NTT / profile legs (for ncu runs)")
     ap.add_argument("--no-graph", action="store_true",
                     help="time direct C-ABI calls instead of CUDA-graph replays of the same calls")
+    ap.add_argument("--shard", default="auto", choices=["auto", "none", "nccl", "peer"],
+                    help="C4 limb sharding: nccl = two NCCL all-gathers per KeySwitch; peer = the exchanges fused "
+                         "into the base conversions over NVLink symmetric memory; none = one KeySwitch per GPU; "
+                         "auto = nccl for C4 under torchrun, else none")
     return ap.parse_args()
 
 
@@ -296,6 +300,69 @@ class KSWorkload:
         return self.s_in, self.s_out
 
 
+class C4ShardWorkload:
+    """C4 (BASELINE.json configs[3]): ONE KeySwitch per step with the RNS limbs sharded over the ranks
+    (SURVEY.md §8(e) item 2).  mode "nccl": shard.ShardedKeySwitch, two all_gather_into_tensor per
+    KeySwitch; mode "peer": shard.PeerShardedKeySwitch, base conversions read the peers' limbs over NVLink
+    (symmetric memory), no all-gather.  At world 1 the exchange degenerates to the rank's own buffer."""
+    unit = "KeySwitch/s"
+    scaling = "strong"
+    graphable = False      # collectives / symmetric-memory barriers: timed as direct calls
+
+    def __init__(self, H, ctx, cfg, level, nsets, dev, seed, sid, world, rank, mode):
+        import torch
+        from paper_2507_04775_b200 import shard
+        self.H, self.ctx, self.cfg, self.level, self.sid, self.mode = H, ctx, cfg, level, sid, mode
+        self.world, self.rank = world, rank
+        self.units = 1
+        self.nsets = nsets
+        if mode == "peer":
+            if world > 1:
+                self.ks = shard.PeerShardedKeySwitch(ctx, level, world, rank, dev)
+            else:
+                s0 = H.shard_query(ctx, level, 1, 0)
+                ys = [torch.zeros((s0.q_pad, cfg.n), dtype=torch.int64, device=dev)]
+                yps = [torch.zeros((2 * s0.p_pad, cfg.n), dtype=torch.int64, device=dev)]
+                self.ks = shard.PeerShardedKeySwitch(ctx, level, 1, 0, dev, sim_ysend=ys, sim_ypsend=yps)
+        else:
+            self.ks = shard.ShardedKeySwitch(ctx, level, world, rank, dev,
+                                             gather_fn=None if world > 1 else (lambda o, i: o.copy_(i)))
+        info = self.ks.info
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        n = cfg.n
+        q_own = list(cfg.q[info.q_lo:info.q_lo + info.nq_act])
+        key_pr = list(cfg.q[info.q_lo:info.q_hi]) + list(cfg.p[info.p_lo:info.p_hi])
+
+        def limbs(pr):
+            t = torch.empty((len(pr), n), dtype=torch.int64, device=dev)
+            for i, q in enumerate(pr):
+                t[i] = torch.randint(0, int(q), (n,), generator=g, device=dev, dtype=torch.int64)
+            return t
+
+        self.sets = []
+        for _ in range(nsets):
+            c0, c1 = limbs(q_own), limbs(q_own)
+            evk = torch.stack([limbs(key_pr) for _ in range(2 * cfg.dnum)]).reshape(cfg.dnum, 2, len(key_pr), n)
+            self.sets.append({"c0": c0, "c1": c1, "evk": evk, "out0": torch.empty_like(c0),
+                              "out1": torch.empty_like(c1)})
+
+    def step(self, i):
+        import torch
+        s = self.sets[i % len(self.sets)]
+        self.ks(s["c0"], s["c1"], s["evk"], s["out0"], s["out1"], self.sid)
+
+    def alg_bytes(self):
+        c, l = self.cfg, self.level
+        return (4 * (l + 1) + 2 * c.beta(l) * (l + 1 + c.K)) * c.n * 8
+
+    def l2_note(self):
+        c, l = self.cfg, self.level
+        mb = self.nsets * (2 * c.dnum * (c.L + 1 + c.K) + 2 * (l + 1)) * c.n * 8 / 1e6 / self.world
+        return (f"{self.nsets} rotating (ct, key) sets, {mb:.0f} MB per rank; limbs sharded over {self.world} "
+                f"rank(s), exchange: {'NCCL all-gathers' if self.mode == 'nccl' else 'peer loads in BConv'}")
+
+
 class C3Workload:
     """C3: 8 ciphertexts x 8 hoisted rotations, ciphertexts sharded over ranks (keys replicated)."""
     unit = "rotation-KeySwitch/s"
@@ -481,7 +548,12 @@ def main():
     stream = torch.cuda.current_stream()
     sid = stream.cuda_stream
     seed = cfg.seed * 1000 + rank
-    if cfg.name == "C3":
+    shard_mode = args.shard if args.shard != "auto" else ("nccl" if cfg.name == "C4" and world > 1 else "none")
+    if shard_mode != "none" and cfg.name != "C4":
+        raise SystemExit("--shard nccl|peer applies to --config C4 (limb sharding)")
+    if shard_mode != "none":
+        wl = C4ShardWorkload(H, ctx, cfg, level, args.sets, dev, seed, sid, world, rank, shard_mode)
+    elif cfg.name == "C3":
         wl = C3Workload(H, ctx, cfg, level, world, rank, dev, seed, sid)
     elif cfg.name == "C5":
         wl = C5Workload(H, ctx, cfg, dev, seed, sid)
@@ -497,7 +569,7 @@ def main():
     # replay (gpu_launches counts the kernels the timed region executes either way)
     period = len(wl.sets) if hasattr(wl, "sets") else 1
     graphs, glaunch = [], []
-    if not args.no_graph:
+    if not args.no_graph and getattr(wl, "graphable", True):
         for i in range(period):
             g = torch.cuda.CUDAGraph()
             sid0 = wl.sid
@@ -703,7 +775,9 @@ def main():
                 "scaling": wl.scaling, "vs_baseline": None, "dtype": "u64", "data": "synthetic",
                 "config": {"workload": workload_desc(cfg, level), "N": cfg.n, "L": cfg.L, "K": cfg.K,
                            "dnum": cfg.dnum, "level": level,
-                           "parallelism": f"{'replicas' if cfg.name == 'C5' else 'ciphertexts sharded'} over {world} GPU(s)",
+                           "parallelism": (f"RNS limbs sharded over {world} GPU(s) ({shard_mode})"
+                                           if shard_mode != "none" else
+                                           f"{'replicas' if cfg.name == 'C5' else 'ciphertexts sharded'} over {world} GPU(s)"),
                            "l2": wl.l2_note()},
                 "gpu_launches": launches, "clocks": clk.summary(),
                 "launch_mode": (f"CUDA graph replay of the C-ABI calls ({glaunch[0]} kernels per step)" if graphs

@@ -291,6 +291,26 @@ hks_status hks_shard_ks_moddown_out(const hks_ctx *ctx, uint32_t level, uint32_t
                                     const uint64_t *ypall, const uint64_t *acc_loc, const uint64_t *c0_loc,
                                     uint64_t *out0_loc, uint64_t *out1_loc, void *ws, void *stream);
 
+/* Peer-memory variants of phases B and C (the collective fused into the base
+ * conversion over NVLink).  Instead of an all-gathered buffer, the caller passes a HOST array of `world`
+ * device pointers: rank r's ysend ([q_pad][N]) resp. ypsend ([2][p_pad][N]) as mapped into this rank's
+ * address space (its own buffer for r == rank; a peer mapping -- CUDA IPC / symmetric memory over
+ * NVLink -- for the others; plain device pointers when several simulated ranks share one GPU).  The
+ * base-conversion kernel loads every source limb directly from its owner, so no all-gather runs and
+ * each rank reads only the limbs its targets need.  Same outputs as the all-gather phases, bit for bit.
+ * Ordering is the caller's: every rank's phase A (resp. B) must be complete and visible before any rank
+ * starts phase B (resp. C), and no rank may overwrite its ysend / ypsend until all peers finished
+ * reading it (e.g. a symmetric-memory barrier on the stream).  Errors: HKS_EINVAL for a NULL table or
+ * entry, plus those of the all-gather phases. */
+hks_status hks_shard_ks_inner_peer(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
+                                   const uint64_t *const *ysend_ranks, const uint64_t *c1_loc,
+                                   const uint64_t *evk_loc, uint64_t *acc_loc, uint64_t *ypsend, void *ws,
+                                   void *stream);
+hks_status hks_shard_ks_moddown_out_peer(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
+                                         const uint64_t *const *ypsend_ranks, const uint64_t *acc_loc,
+                                         const uint64_t *c0_loc, uint64_t *out0_loc, uint64_t *out1_loc, void *ws,
+                                         void *stream);
+
 #ifdef __cplusplus
 }
 #endif

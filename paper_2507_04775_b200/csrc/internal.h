@@ -88,6 +88,8 @@ struct BconvGroup {
     const u64 *matb;           // byte-column words [nsrc][mat_stride][8] (tensor-pipe path, k_bconv_mma) or NULL:
                                // word c of entry (i, u) has byte a = byte c of (2^(8a) [qhat_i]_t mod t)
     u16 src_slot[BC_MAXSRC];
+    const u64 *srcp[BC_MAXSRC];   // non-NULL: absolute address of source i (e.g. a peer GPU's limb over
+                                  // NVLink, limb-sharded KeySwitch); NULL: in + src_slot[i] * N
     u16 src_prime[BC_MAXSRC];
     u64 pre_w[BC_MAXSRC];      // optional prescale y_i = x_i * pre_w (Shoup) -- generic hks_bconv
     u64 pre_wp[BC_MAXSRC];

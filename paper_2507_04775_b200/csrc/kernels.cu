@@ -11,6 +11,11 @@
 
 #include "internal.h"
 
+// source limb i of a base-conversion group: an absolute (possibly peer-mapped) address, or a slot of A.in
+__device__ __forceinline__ const u64 *bc_src(const BconvArgs &A, const BconvGroup &G, int i, size_t N) {
+    return G.srcp[i] ? G.srcp[i] : A.in + (size_t)G.src_slot[i] * N;
+}
+
 // HKS_BCONV_FP=1 enables the FP64-assisted base conversion (results are identical).  Off by default:
 // on B200 it measured slower (60 vs 52 us for the C2 ModUp conversion) because the 128-bit
 // recombination of the five FP64 limb sums makes it issue-bound (+48 % instructions); see DESIGN.md.
@@ -57,11 +62,11 @@ __global__ void __launch_bounds__(256, CPT == 1 ? 5 : 3) k_bconv(const __grid_co
     for (int i = 0; i < NSRC; i++) {
         u64 v[CPT];
         if (CPT == 2) {
-            const ulonglong2 t = *reinterpret_cast<const ulonglong2 *>(A.in + (size_t)G.src_slot[i] * N + x0);
+            const ulonglong2 t = *reinterpret_cast<const ulonglong2 *>(bc_src(A, G, i, N) + x0);
             v[0] = t.x;
             v[CPT - 1] = t.y;
         } else {
-            v[0] = A.in[(size_t)G.src_slot[i] * N + x0];
+            v[0] = bc_src(A, G, i, N)[x0];
         }
 #pragma unroll
         for (int c = 0; c < CPT; c++) {
@@ -121,7 +126,7 @@ __global__ void __launch_bounds__(256, 3) k_bconv_kara(const __grid_constant__ B
     if (x >= N) return;
     u32 yl[NSRC], yh[NSRC];
 #pragma unroll
-    for (int i = 0; i < NSRC; i++) split30(A.in[(size_t)G.src_slot[i] * N + x], yl[i], yh[i]);
+    for (int i = 0; i < NSRC; i++) split30(bc_src(A, G, i, N)[x], yl[i], yh[i]);
     // two targets per iteration: their independent MAC/reduction chains interleave
     for (u32 u = 0; u < nt; u += 2) {
         const u32 v = (u + 1 < nt) ? u + 1 : u;
@@ -257,7 +262,7 @@ __global__ void __launch_bounds__(256, HKS_MMA_MINB) k_bconv_mma(const __grid_co
 #pragma unroll
     for (int s = 0; s < NS; s++) {
         const u32 i = (K16 && s == KS32) ? 4 * s + (q >> 1) : 4 * s + q;
-        src[s] = i < (u32)NSRC ? A.in + (size_t)G.src_slot[i] * N + g : nullptr;
+        src[s] = i < (u32)NSRC ? bc_src(A, G, i, N) + g : nullptr;
     }
     const size_t xbeg = (size_t)blockIdx.x * A.cw, xend = xbeg + A.cw, xstep = 8 * NPI * nparts;
     // NPI n-tiles (8 NPI coefficients) per iteration: 4 NPI independent accumulator chains; the next
@@ -494,7 +499,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constan
         const u32 soff = (m >> 3) * SBO + (m & 7) * 16;
         const u64 *srcp[NSRC];
 #pragma unroll
-        for (int i = 0; i < NSRC; i++) srcp[i] = A.in + (size_t)G.src_slot[i] * N + m;
+        for (int i = 0; i < NSRC; i++) srcp[i] = bc_src(A, G, i, N) + m;
         auto load_tile = [&](u32 j) {
             const u32 st = j % TC_SA;
             const size_t x0 = (size_t)(blockIdx.x + j * gridDim.x) << 7;
@@ -886,7 +891,7 @@ __global__ void __launch_bounds__(256) k_bconv_fp(const __grid_constant__ BconvA
     double Y[NFP][3];
 #pragma unroll
     for (int i = 0; i < NSRC; i++) {
-        const u64 v = A.in[(size_t)G.src_slot[i] * N + x];
+        const u64 v = bc_src(A, G, i, N)[x];
         if (i < NINT)
             split30(v, yl[i], yh[i]);
         else

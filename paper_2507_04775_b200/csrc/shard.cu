@@ -79,7 +79,8 @@ hks_status bconv_groups(const hks_ctx *c, std::vector<BconvGroup> &groups, const
 }
 
 void push_group(std::vector<BconvGroup> &out, u32 nsrc, const u16 *src_slot, const uint2 *mat, u32 stride,
-                const std::vector<u16> &ds, const std::vector<u16> &dp, const double *matf, const u32 *mats, const u64 *matb, const u64 *mimg) {
+                const std::vector<u16> &ds, const std::vector<u16> &dp, const double *matf, const u32 *mats, const u64 *matb, const u64 *mimg,
+                const u64 *const *srcp = nullptr) {
     for (size_t u0 = 0; u0 < ds.size(); u0 += BC_MAXDST) {
         BconvGroup g{};
         g.nsrc = nsrc;
@@ -90,7 +91,10 @@ void push_group(std::vector<BconvGroup> &out, u32 nsrc, const u16 *src_slot, con
         g.mats = mats ? mats + u0 : nullptr;
         g.matb = matb ? matb + 8 * u0 : nullptr;
         g.mimg = mimg ? mimg + (size_t)bconv_img_words(nsrc) * u0 : nullptr;
-        for (u32 i = 0; i < nsrc; i++) g.src_slot[i] = src_slot[i];
+        for (u32 i = 0; i < nsrc; i++) {
+            g.src_slot[i] = src_slot[i];
+            g.srcp[i] = srcp ? srcp[i] : nullptr;
+        }
         for (u32 u = 0; u < g.ndst; u++) { g.dst_slot[u] = ds[u0 + u]; g.dst_prime[u] = dp[u0 + u]; }
         out.push_back(g);
     }
@@ -136,14 +140,19 @@ extern "C" hks_status hks_shard_ks_modup_in(const hks_ctx *c, uint32_t level, ui
 
 // Phase B: D_j for owned limbs from the gathered y, fused NTT + key inner product, then
 // ypsend[p][kk] = INTT(acc_p[owned P_kk]) * N^-1 [phat_k]^-1.
-extern "C" hks_status hks_shard_ks_inner(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
-                                        const uint64_t *yall, const uint64_t *c1_loc, const uint64_t *evk_loc,
-                                        uint64_t *acc_loc, uint64_t *ypsend, void *ws, void *stream) {
+// yall != NULL: sources are slots of the all-gathered buffer; else peers[r] is rank r's ysend (a local or
+// peer-mapped device address) and the base conversion reads every source limb straight from its owner.
+static hks_status shard_inner(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank, const uint64_t *yall,
+                              const uint64_t *const *peers, const uint64_t *c1_loc, const uint64_t *evk_loc,
+                              uint64_t *acc_loc, uint64_t *ypsend, void *ws, void *stream) {
     Plan P;
     hks_status st = make_plan(c, level, world, rank, P);
     if (st != HKS_OK || (st = dev_ctx(c)) != HKS_OK) return st;
-    if (!yall || !evk_loc || !acc_loc || !ypsend || !ws || (P.nq_act && !c1_loc))
+    if ((!yall && !peers) || !evk_loc || !acc_loc || !ypsend || !ws || (P.nq_act && !c1_loc))
         HKS_FAIL(HKS_EINVAL, "shard_ks_inner: NULL buffer");
+    if (peers)
+        for (u32 r = 0; r < world; r++)
+            if (!peers[r]) HKS_FAIL(HKS_EINVAL, "shard_ks_inner_peer: NULL buffer of rank %u", r);
     const u32 beta = c->beta(level), ne = c->ne(level);
     if (beta > FK_MAXD) HKS_FAIL(HKS_EINVAL, "shard_ks_inner: beta %u > %d", beta, FK_MAXD);
     DevGuard g(c->device);
@@ -160,9 +169,11 @@ extern "C" hks_status hks_shard_ks_inner(const hks_ctx *c, uint32_t level, uint3
     for (u32 j = 0; j < beta; j++) {
         const u32 lo = c->digit_lo(j), hi = c->digit_hi(level, j);
         u16 src[BC_MAXSRC];
+        const u64 *srcp[BC_MAXSRC];
         for (u32 i = lo; i < hi; i++) {
             const u32 r = P.q_owner(i);
             src[i - lo] = (u16)(r * P.q_pad + (i - P.qlo_r[r]));
+            srcp[i - lo] = peers ? peers[r] + (size_t)(i - P.qlo_r[r]) * c->n : nullptr;
         }
         const size_t moff = c->mu_mat_off[(size_t)level * c->dnum + j];
         const uint2 *mat = c->d_mu_mat + moff;
@@ -177,7 +188,7 @@ extern "C" hks_status hks_shard_ks_inner(const hks_ctx *c, uint32_t level, uint3
         int run_col = -1;
         auto flush = [&]() {
             if (!ds.empty()) push_group(groups, hi - lo, src, mat + run_col, ntg, ds, dp, matf + 3 * run_col, mats + run_col,
-                                         matb + 8 * run_col, mimg + (size_t)imgw * run_col);
+                                         matb + 8 * run_col, mimg + (size_t)imgw * run_col, srcp);
             ds.clear(); dp.clear(); run_col = -1;
         };
         int prev_col = -2;
@@ -193,7 +204,7 @@ extern "C" hks_status hks_shard_ks_inner(const hks_ctx *c, uint32_t level, uint3
         }
         flush();
     }
-    if ((st = bconv_groups(c, groups, yall, ext, s)) != HKS_OK) return st;
+    if ((st = bconv_groups(c, groups, yall ? yall : ext, ext, s)) != HKS_OK) return st;
     if (T.size() && (st = run_ntt_fwd_cols(c, T, ext, ext, s)) != HKS_OK) return st;
     std::vector<KipItem> items(own_t.size());
     for (u32 u = 0; u < own_t.size(); u++) {
@@ -219,14 +230,18 @@ extern "C" hks_status hks_shard_ks_inner(const hks_ctx *c, uint32_t level, uint3
 }
 
 // Phase C: conv_p = BConv_{P -> owned chain}(ypall_p); out_p = (acc_p - NTT(conv_p)) P^-1 (+ c0 on p = 0).
-extern "C" hks_status hks_shard_ks_moddown_out(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
-                                              const uint64_t *ypall, const uint64_t *acc_loc, const uint64_t *c0_loc,
-                                              uint64_t *out0_loc, uint64_t *out1_loc, void *ws, void *stream) {
+static hks_status shard_moddown(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank, const uint64_t *ypall,
+                                const uint64_t *const *peers, const uint64_t *acc_loc, const uint64_t *c0_loc,
+                                uint64_t *out0_loc, uint64_t *out1_loc, void *ws, void *stream) {
     Plan P;
     hks_status st = make_plan(c, level, world, rank, P);
     if (st != HKS_OK || (st = dev_ctx(c)) != HKS_OK) return st;
     if (P.nq_act == 0) return HKS_OK;
-    if (!ypall || !acc_loc || !out0_loc || !out1_loc || !ws) HKS_FAIL(HKS_EINVAL, "shard_ks_moddown_out: NULL buffer");
+    if ((!ypall && !peers) || !acc_loc || !out0_loc || !out1_loc || !ws)
+        HKS_FAIL(HKS_EINVAL, "shard_ks_moddown_out: NULL buffer");
+    if (peers)
+        for (u32 r = 0; r < world; r++)
+            if (!peers[r]) HKS_FAIL(HKS_EINVAL, "shard_ks_moddown_out_peer: NULL buffer of rank %u", r);
     DevGuard g(c->device);
     cudaStream_t s = (cudaStream_t)stream;
     const u32 beta = c->beta(level), K = c->np;
@@ -234,16 +249,18 @@ extern "C" hks_status hks_shard_ks_moddown_out(const hks_ctx *c, uint32_t level,
     std::vector<BconvGroup> groups;
     for (u32 p = 0; p < 2; p++) {
         u16 src[BC_MAXSRC];
+        const u64 *srcp[BC_MAXSRC];
         for (u32 k = 0; k < K; k++) {
             const u32 r = P.p_owner(k);
             src[k] = (u16)(r * 2 * P.p_pad + p * P.p_pad + (k - P.plo_r[r]));
+            srcp[k] = peers ? peers[r] + (size_t)(p * P.p_pad + (k - P.plo_r[r])) * c->n : nullptr;
         }
         std::vector<u16> ds(P.nq_act), dp(P.nq_act);
         for (u32 li = 0; li < P.nq_act; li++) { ds[li] = (u16)(p * P.nq_act + li); dp[li] = (u16)(P.q_lo + li); }
         push_group(groups, K, src, c->d_md_mat + P.q_lo, c->nq, ds, dp, c->d_md_matf + 3 * P.q_lo, c->d_md_mats + P.q_lo,
-                   c->d_md_matb + 8 * P.q_lo, c->d_md_img + (size_t)bconv_img_words(K) * P.q_lo);
+                   c->d_md_matb + 8 * P.q_lo, c->d_md_img + (size_t)bconv_img_words(K) * P.q_lo, srcp);
     }
-    if ((st = bconv_groups(c, groups, ypall, conv, s)) != HKS_OK) return st;
+    if ((st = bconv_groups(c, groups, ypall ? ypall : conv, conv, s)) != HKS_OK) return st;
     LimbList M;
     std::vector<uint8_t> poly;
     for (u32 p = 0; p < 2; p++)
@@ -254,4 +271,35 @@ extern "C" hks_status hks_shard_ks_moddown_out(const hks_ctx *c, uint32_t level,
     std::vector<MdOut> mo = {MdOut{out0_loc, c0_loc, 1}, MdOut{out1_loc, nullptr, 1}};
     if ((st = run_ntt_moddown(c, M, poly, mo, conv, acc_loc, s)) != HKS_OK) return st;
     return HKS_OK;
+}
+
+extern "C" hks_status hks_shard_ks_inner(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
+                                        const uint64_t *yall, const uint64_t *c1_loc, const uint64_t *evk_loc,
+                                        uint64_t *acc_loc, uint64_t *ypsend, void *ws, void *stream) {
+    if (!yall) HKS_FAIL(HKS_EINVAL, "shard_ks_inner: NULL yall");
+    return shard_inner(c, level, world, rank, yall, nullptr, c1_loc, evk_loc, acc_loc, ypsend, ws, stream);
+}
+
+extern "C" hks_status hks_shard_ks_inner_peer(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
+                                             const uint64_t *const *ysend_ranks, const uint64_t *c1_loc,
+                                             const uint64_t *evk_loc, uint64_t *acc_loc, uint64_t *ypsend, void *ws,
+                                             void *stream) {
+    if (!ysend_ranks) HKS_FAIL(HKS_EINVAL, "shard_ks_inner_peer: NULL rank table");
+    return shard_inner(c, level, world, rank, nullptr, ysend_ranks, c1_loc, evk_loc, acc_loc, ypsend, ws, stream);
+}
+
+extern "C" hks_status hks_shard_ks_moddown_out(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
+                                              const uint64_t *ypall, const uint64_t *acc_loc, const uint64_t *c0_loc,
+                                              uint64_t *out0_loc, uint64_t *out1_loc, void *ws, void *stream) {
+    if (!ypall) HKS_FAIL(HKS_EINVAL, "shard_ks_moddown_out: NULL ypall");
+    return shard_moddown(c, level, world, rank, ypall, nullptr, acc_loc, c0_loc, out0_loc, out1_loc, ws, stream);
+}
+
+extern "C" hks_status hks_shard_ks_moddown_out_peer(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
+                                                   const uint64_t *const *ypsend_ranks, const uint64_t *acc_loc,
+                                                   const uint64_t *c0_loc, uint64_t *out0_loc, uint64_t *out1_loc,
+                                                   void *ws, void *stream) {
+    if (!ypsend_ranks) HKS_FAIL(HKS_EINVAL, "shard_ks_moddown_out_peer: NULL rank table");
+    return shard_moddown(c, level, world, rank, nullptr, ypsend_ranks, acc_loc, c0_loc, out0_loc, out1_loc, ws,
+                         stream);
 }

@@ -26,7 +26,8 @@ EXPORTS = ("hks_last_error", "hks_ctx_create", "hks_ctx_destroy", "hks_ctx_query
            "hks_automorph",
            "hks_rotate_hoisted", "hks_rotate_hoisted_batch", "hks_rotate_hoisted_batch_workspace_bytes",
            "hks_launch_count", "hks_prof_enable", "hks_prof_read", "hks_shard_query", "hks_shard_workspace_bytes",
-           "hks_shard_ks_modup_in", "hks_shard_ks_inner", "hks_shard_ks_moddown_out")
+           "hks_shard_ks_modup_in", "hks_shard_ks_inner", "hks_shard_ks_moddown_out", "hks_shard_ks_inner_peer",
+           "hks_shard_ks_moddown_out_peer")
 
 
 class HksError(RuntimeError):
@@ -109,6 +110,10 @@ def lib() -> ctypes.CDLL:
         L.hks_shard_ks_modup_in.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp]
         L.hks_shard_ks_inner.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         L.hks_shard_ks_moddown_out.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.hks_shard_ks_inner_peer.argtypes = [_vp, _u32, _u32, _u32, ctypes.POINTER(_vp), _vp, _vp, _vp, _vp, _vp,
+                                              _vp]
+        L.hks_shard_ks_moddown_out_peer.argtypes = [_vp, _u32, _u32, _u32, ctypes.POINTER(_vp), _vp, _vp, _vp, _vp,
+                                                    _vp, _vp]
         for f in EXPORTS[1:]:
             if f not in ("hks_ctx_destroy", "hks_workspace_bytes", "hks_launch_count", "hks_shard_workspace_bytes",
                          "hks_rotate_hoisted_batch_workspace_bytes"):
@@ -337,6 +342,28 @@ def shard_ks_modup_in(ctx: Context, level, world, rank, c1_loc, ysend, stream=No
 def shard_ks_inner(ctx: Context, level, world, rank, yall, c1_loc, evk_loc, acc_loc, ypsend, ws, stream=None):
     _check(lib().hks_shard_ks_inner(ctx.handle, level, world, rank, _ptr(yall), _ptr(c1_loc), _ptr(evk_loc),
                                     _ptr(acc_loc), _ptr(ypsend), _ptr(ws), _stream(stream)), "hks_shard_ks_inner")
+
+
+def _ptr_table(ptrs):
+    """HOST array of device addresses (ints or tensors) for the *_peer phases."""
+    vals = [p if isinstance(p, int) else _ptr(p) for p in ptrs]
+    return (_vp * len(vals))(*vals)
+
+
+def shard_ks_inner_peer(ctx: Context, level, world, rank, ysend_ranks, c1_loc, evk_loc, acc_loc, ypsend, ws,
+                        stream=None):
+    """Phase B reading every rank's ysend through `ysend_ranks` (addresses valid on this GPU: own buffer,
+    peer mappings over NVLink, or simulated ranks' buffers on one device) -- no all-gather."""
+    _check(lib().hks_shard_ks_inner_peer(ctx.handle, level, world, rank, _ptr_table(ysend_ranks), _ptr(c1_loc),
+                                         _ptr(evk_loc), _ptr(acc_loc), _ptr(ypsend), _ptr(ws), _stream(stream)),
+           "hks_shard_ks_inner_peer")
+
+
+def shard_ks_moddown_out_peer(ctx: Context, level, world, rank, ypsend_ranks, acc_loc, c0_loc, out0_loc, out1_loc,
+                              ws, stream=None):
+    _check(lib().hks_shard_ks_moddown_out_peer(ctx.handle, level, world, rank, _ptr_table(ypsend_ranks),
+                                               _ptr(acc_loc), _ptr(c0_loc), _ptr(out0_loc), _ptr(out1_loc),
+                                               _ptr(ws), _stream(stream)), "hks_shard_ks_moddown_out_peer")
 
 
 def shard_ks_moddown_out(ctx: Context, level, world, rank, ypall, acc_loc, c0_loc, out0_loc, out1_loc, ws,

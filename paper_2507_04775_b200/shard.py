@@ -83,6 +83,65 @@ class ShardedKeySwitch:
         self.phase_c(c0_loc, out0_loc, out1_loc, stream)
 
 
+class PeerShardedKeySwitch:
+    """Limb-sharded KeySwitch with both exchanges fused into the base conversions:
+    ysend / ypsend live in symmetric memory (torch.distributed._symmetric_memory, NVLink peer mappings),
+    and phases B and C hand libhks the table of every rank's buffer address, so the BConv kernel loads
+    each source limb straight from its owner -- no all-gather, no gathered copy, and each rank reads only
+    the limbs its targets need.  Device-side barriers on the stream order the phases across ranks.
+
+    Simulated ranks (tests, one GPU): pass `sim_ysend` / `sim_ypsend`, the lists of every rank's buffers;
+    the caller then runs phase A of all ranks before phase B of any, and so on."""
+
+    def __init__(self, ctx, level: int, world: int, rank: int, device, group=None, sim_ysend=None, sim_ypsend=None):
+        import torch
+        self.ctx, self.level, self.world, self.rank = ctx, level, world, rank
+        self.info = H.shard_query(ctx, level, world, rank)
+        s, n = self.info, ctx.n
+        self.sim = sim_ysend is not None
+        if self.sim:
+            self.ysend, self.ypsend = sim_ysend[rank], sim_ypsend[rank]
+            self.yptrs = [t.data_ptr() for t in sim_ysend]
+            self.ypptrs = [t.data_ptr() for t in sim_ypsend]
+        else:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm
+            grp = group or dist.group.WORLD
+            self.ysend = symm.empty((s.q_pad, n), dtype=torch.int64, device=device)
+            self.ypsend = symm.empty((2 * s.p_pad, n), dtype=torch.int64, device=device)
+            self._hy = symm.rendezvous(self.ysend, grp)
+            self._hyp = symm.rendezvous(self.ypsend, grp)
+            self.yptrs = list(self._hy.buffer_ptrs)
+            self.ypptrs = list(self._hyp.buffer_ptrs)
+        self.acc = torch.empty((2 * (s.nq_act + s.p_hi - s.p_lo), n), dtype=torch.int64, device=device)
+        self.ws = torch.empty((max(H.shard_workspace_bytes(ctx, level, world, rank) // 8, 1),), dtype=torch.int64,
+                              device=device)
+
+    def barrier(self):
+        """Stream-ordered barrier across ranks (no-op for simulated ranks)."""
+        if not self.sim:
+            self._hy.barrier(channel=0)
+
+    def phase_a(self, c1_loc, stream=None):
+        H.shard_ks_modup_in(self.ctx, self.level, self.world, self.rank, c1_loc, self.ysend, stream)
+
+    def phase_b(self, c1_loc, evk_loc, stream=None):
+        H.shard_ks_inner_peer(self.ctx, self.level, self.world, self.rank, self.yptrs, c1_loc, evk_loc, self.acc,
+                              self.ypsend, self.ws, stream)
+
+    def phase_c(self, c0_loc, out0_loc, out1_loc, stream=None):
+        H.shard_ks_moddown_out_peer(self.ctx, self.level, self.world, self.rank, self.ypptrs, self.acc, c0_loc,
+                                    out0_loc, out1_loc, self.ws, stream)
+
+    def __call__(self, c0_loc, c1_loc, evk_loc, out0_loc, out1_loc, stream=None):
+        self.phase_a(c1_loc, stream)
+        self.barrier()          # every ysend written before any rank reads it
+        self.phase_b(c1_loc, evk_loc, stream)
+        self.barrier()          # every ypsend written (and every ysend read) before phase C / the next call
+        self.phase_c(c0_loc, out0_loc, out1_loc, stream)
+        self.barrier()          # every ypsend read before the next call overwrites it
+
+
 def slice_key(evk_full, info, num_q: int):
     """A rank's owned key limbs [dnum][2][nkey][N] from a full key [dnum][2][L+1+K][N]: owned chain
     limbs then owned special limbs (the evk_loc layout of include/hks.h)."""

@@ -121,3 +121,59 @@ def test_sharded_keyswitch_matches_unsharded(name, level, world):
     got1 = torch.cat([l[4] for l in loc])
     torch.cuda.synchronize()
     assert torch.equal(got0, ref0) and torch.equal(got1, ref1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,level,world", [("T12", 6, 2), ("T12", 4, 3), ("C2", 29, 4), ("C4", 35, 8),
+                                              ("C4", 35, 2), ("C4", 17, 4)])
+def test_peer_sharded_keyswitch_matches_unsharded(name, level, world):
+    """NEXT-3: phases B and C read the other ranks' limbs through a pointer table (here: simulated ranks'
+    buffers on one GPU) inside the base conversion; bit-identical to hks_keyswitch."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    dev = "cuda:0"
+    cfg = S.config(name)
+    ctx = H.Context.from_config(cfg, 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(cfg.seed + 1)
+    n = cfg.n
+    primes = list(cfg.q) + list(cfg.p)
+
+    def limbs(pr):
+        return torch.stack([torch.randint(0, int(p), (n,), generator=g, device=dev, dtype=torch.int64) for p in pr])
+
+    c0, c1 = limbs(cfg.q[: level + 1]), limbs(cfg.q[: level + 1])
+    evk = torch.stack([limbs(primes) for _ in range(2 * cfg.dnum)]).reshape(cfg.dnum, 2, len(primes), n)
+    ref0, ref1 = torch.empty_like(c0), torch.empty_like(c1)
+    H.keyswitch(ctx, c0, c1, level, evk, ref0, ref1, ctx.workspace(H.OP_KEYSWITCH, level))
+
+    infos = [H.shard_query(ctx, level, world, r) for r in range(world)]
+    ys = [torch.full((s.q_pad, n), -1, dtype=torch.int64, device=dev) for s in infos]
+    yps = [torch.full((2 * s.p_pad, n), -1, dtype=torch.int64, device=dev) for s in infos]
+    ranks = [shard.PeerShardedKeySwitch(ctx, level, world, r, dev, sim_ysend=ys, sim_ypsend=yps)
+             for r in range(world)]
+    loc = []
+    for ks in ranks:
+        s = ks.info
+        c0l, c1l = c0[s.q_lo:s.q_lo + s.nq_act].contiguous(), c1[s.q_lo:s.q_lo + s.nq_act].contiguous()
+        loc.append((c0l, c1l, shard.slice_key(evk, s, len(cfg.q)), torch.empty_like(c0l), torch.empty_like(c1l)))
+        ks.phase_a(c1l)
+    for r, ks in enumerate(ranks):
+        ks.phase_b(loc[r][1], loc[r][2])
+    for r, ks in enumerate(ranks):
+        c0l, _, _, o0, o1 = loc[r]
+        ks.phase_c(c0l, o0, o1)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat([l[3] for l in loc]), ref0) and torch.equal(torch.cat([l[4] for l in loc]), ref1)
+
+
+@pytest.mark.gpu
+def test_peer_phase_rejects_null_table():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = S.config("T12")
+    ctx = H.Context.from_config(cfg, 0)
+    s = H.shard_query(ctx, 4, 2, 0)
+    z = torch.zeros((8, cfg.n), dtype=torch.int64, device="cuda:0")
+    with pytest.raises(H.HksError):
+        H.shard_ks_inner_peer(ctx, 4, 2, 0, [z.data_ptr(), 0], z, z, z, z, z)
