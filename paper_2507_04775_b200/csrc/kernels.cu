@@ -627,7 +627,13 @@ static hks_status bconv_tc_go(const BconvArgs &a, cudaStream_t s) {
 // pass's (same linear map mod p), lazily reduced to [0, 3p) except the final inverse round, which
 // applies the EPI_SCALE factor and canonicalises.  Tiles: 128 vectors (consecutive columns c) of one
 // (limb, class / block); persistent CTAs (two per SM: 256 TMEM columns each).
-#define NT_SA 3
+#ifndef HKS_NT_SA
+#define HKS_NT_SA 3
+#endif
+#ifndef HKS_NT_CPS
+#define HKS_NT_CPS 2       // CTAs per SM
+#endif
+#define NT_SA HKS_NT_SA
 #define NT_EPW 8
 #define NT_THREADS ((NT_EPW + 4) * 32)
 struct Ntt16Args {
@@ -643,7 +649,7 @@ struct Ntt16Args {
 };
 
 template <bool FINAL>
-__global__ void __launch_bounds__(NT_THREADS, 2) k_ntt16_tc(const __grid_constant__ Ntt16Args A) {
+__global__ void __launch_bounds__(NT_THREADS, HKS_NT_CPS) k_ntt16_tc(const __grid_constant__ Ntt16Args A) {
     pdl_trigger();
     constexpr u32 SBO = 1024;                 // 8 K-chunks x 128 bytes per 8-row group
     constexpr u32 STAGE = 2 * 16384;          // A tile (128 x 128 bytes) + B image (128 x 128 bytes)
@@ -801,7 +807,7 @@ hks_status launch_ntt_cols_tc(const hks_ctx *ctx, NttDir dir, int epi, const Ntt
     a.scale_mod = na.scale_mod ? na.scale_mod : 1;
     a.fwd = dir == NTT_FWD;
     a.map = na.map;
-    const u32 grid = std::min<u32>(a.nlimbs * 32, 2 * (u32)nsm);
+    const u32 grid = std::min<u32>(a.nlimbs * 32, HKS_NT_CPS * (u32)nsm);
     for (u32 r = 0; r < 2; r++) {
         a.round = r;
         const bool final = dir == NTT_INV && r == 1;

@@ -22,6 +22,10 @@
 
 #include "internal.h"
 
+#ifndef HKS_KIP_TMA
+#define HKS_KIP_TMA 0     // 1: key rows prefetched into shared memory with 1D bulk copies (measured slower)
+#endif
+
 // One pass over a limb batch.  LOGN = log2 of the sub-transform length n; LOGE = log2 of the
 // elements a thread holds (radix-2^LOGE rounds); LOGNB = log2 of the sub-transforms per CTA;
 // LOGC = log2 of the row length C (the column stride).  COLS: sub-transforms are columns (stride C);
@@ -606,7 +610,6 @@ __global__ void __launch_bounds__(NTR * ((1 << LOGNB) << (LOGN - LOGE)),
                                   kip_minb(NTR * ((1 << LOGNB) << (LOGN - LOGE))))
 k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
     pdl_trigger();
-    pdl_wait();
     constexpr int n = 1 << LOGN;
     constexpr int E = 1 << LOGE;
     constexpr int NB = 1 << LOGNB;
@@ -626,6 +629,36 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
     const NttMod m = make_nttmod(pc.p);
     const int tid = threadIdx.x;
     const size_t tbase = (size_t)tile * NB * n;
+    const size_t kst = (size_t)A.nkey * N;
+    const u64 *__restrict__ kbase = A.evk + (size_t)A.map.kslot[u] * N + tbase;
+#if HKS_KIP_TMA
+    // The key rows of this CTA (2 NDIG contiguous runs of NB n words) stream into shared memory with 1D
+    // bulk copies issued before griddepcontrol.wait -- the key is a caller input that no kernel of the
+    // chain writes -- so the dominant HBM stream overlaps the predecessor's tail and this CTA's row pass.
+    u64 *skey = sm + NTR * BUF;
+    __shared__ __align__(8) u64 kbar;
+    if (tid == 0) {
+        const u32 bar = (u32)__cvta_generic_to_shared(&kbar);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        constexpr u32 bytes = (u32)(NB * n * 8);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * NDIG * bytes)
+                     : "memory");
+#pragma unroll
+        for (int i = 0; i < NDIG; i++) {
+            const u32 j = A.map.dig[u][i];
+#pragma unroll
+            for (int pp = 0; pp < 2; pp++) {
+                const u32 dst = (u32)__cvta_generic_to_shared(skey + (size_t)(2 * i + pp) * NB * n);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                    "l"(kbase + (size_t)(2 * j + pp) * kst), "r"(bytes), "r"(bar)
+                    : "memory");
+            }
+        }
+    }
+#endif
+    pdl_wait();
 
     // phase 1: thread group i runs the row pass of term i (< NTR) into shared buffer i, concurrently
     {
@@ -694,8 +727,13 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
 
     // phase 2: acc_p = sum_i canon(D_i) * evk_{dig(i)}[p], two coefficients per thread per step; the
     // loads of all terms are issued before the multiply-accumulates.
-    const size_t kst = (size_t)A.nkey * N;
-    const u64 *__restrict__ kbase = A.evk + (size_t)A.map.kslot[u] * N + tbase;
+#if HKS_KIP_TMA
+    {
+        const u32 bar = (u32)__cvta_generic_to_shared(&kbar);
+        asm volatile("{\n\t.reg .pred p;\n\tKW%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra KW%=;\n\t}" ::"r"(bar)
+                     : "memory");
+    }
+#endif
     const u32 as = A.map.aslot[u];
     const u32 ys = A.map.yslot[u];
     const bool ymode = ys != 0xffff && NTR >= 2;      // uniform per CTA
@@ -705,8 +743,14 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
 #pragma unroll
         for (int i = 0; i < NDIG; i++) {
             const u32 j = A.map.dig[u][i];
+#if HKS_KIP_TMA
+            (void)j;
+            kb[i] = *reinterpret_cast<const ulonglong2 *>(skey + (size_t)(2 * i) * NB * n + idx);
+            ka[i] = *reinterpret_cast<const ulonglong2 *>(skey + (size_t)(2 * i + 1) * NB * n + idx);
+#else
             kb[i] = *reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j) * kst + idx);
             ka[i] = *reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j + 1) * kst + idx);
+#endif
             if (i >= (int)A.map.ntr[u]) {
                 dv[i] = *reinterpret_cast<const ulonglong2 *>(A.c1 + (size_t)(A.map.dsrc[u][i] & 0x7fff) * N + tbase + idx);
             } else {
@@ -830,7 +874,8 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
 template <int LOGN, int LOGE, int LOGNB, int NTR, int NDIG>
 static hks_status go_kip(FusedKipArgs &a, cudaStream_t s) {
     constexpr int threads = NTR * ((1 << LOGNB) << (LOGN - LOGE));
-    constexpr size_t smem = (size_t)NTR * ((1 << LOGN) + ((1 << LOGN) >> LOGE)) * (1 << LOGNB) * sizeof(u64);
+    constexpr size_t smem = (size_t)NTR * ((1 << LOGN) + ((1 << LOGN) >> LOGE)) * (1 << LOGNB) * sizeof(u64) +
+                            (HKS_KIP_TMA ? (size_t)2 * NDIG * (1 << LOGN) * (1 << LOGNB) * sizeof(u64) : 0);
     auto kern = k_ntt_kip<LOGN, LOGE, LOGNB, NTR, NDIG>;
     if (smem > 48 * 1024) {
         static bool once = [&] {
