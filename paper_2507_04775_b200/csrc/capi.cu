@@ -316,6 +316,53 @@ extern "C" hks_status hks_bconv(const hks_ctx *c, const uint64_t *x, const uint3
     }
     DevGuard g(c->device);
     cudaStream_t s = (cudaStream_t)stream;
+    if (c->all_big && bconv_tc_enabled()) {
+        // tensor-core path (the hot path's kernel): y_i = [x_i qhat_i^-1]_{q_i} into a temporary, then
+        // k_bconv_tc with this call's byte-column words and B-operand image
+        std::vector<u64> matb, img, w(nsrc), wp(nsrc), pp(nsrc);
+        matb.reserve((size_t)nsrc * ndst * 8);
+        for (u32 i = 0; i < nsrc; i++) {
+            w[i] = proto.pre_w[i];
+            wp[i] = proto.pre_wp[i];
+            pp[i] = c->primes[src_idx[i]];
+            for (u32 u = 0; u < ndst; u++) {
+                const uint2 m2 = mat[(size_t)i * ndst + u];
+                push_bytecols(matb, (u64)m2.x | ((u64)m2.y << 30), c->primes[dst_idx[u]]);
+            }
+        }
+        bconv_image(matb.data(), nsrc, ndst, img);
+        u64 *dy = nullptr, *dmb = nullptr, *dimg = nullptr;
+        HKS_CUDA(cudaMallocAsync((void **)&dy, (size_t)nsrc * c->n * 8, s));
+        HKS_CUDA(cudaMallocAsync((void **)&dmb, matb.size() * 8, s));
+        HKS_CUDA(cudaMallocAsync((void **)&dimg, img.size() * 8, s));
+        HKS_CUDA(cudaMemcpyAsync(dmb, matb.data(), matb.size() * 8, cudaMemcpyHostToDevice, s));
+        HKS_CUDA(cudaMemcpyAsync(dimg, img.data(), img.size() * 8, cudaMemcpyHostToDevice, s));
+        st = launch_limb_scale(x, dy, nsrc, w.data(), wp.data(), pp.data(), c->log_n, s);
+        for (u32 u0 = 0; st == HKS_OK && u0 < ndst; u0 += BC_MAXDST) {
+            BconvArgs a{};
+            a.in = dy;
+            a.out = out;
+            a.pc = c->d_pc;
+            a.log_n = c->log_n;
+            a.big = 1;
+            a.ngroups = 1;
+            a.g[0] = proto;
+            a.g[0].nsrc = nsrc;
+            a.g[0].ndst = std::min<u32>(BC_MAXDST, ndst - u0);
+            a.g[0].mat_stride = ndst;
+            a.g[0].matb = dmb + 8 * (size_t)u0;
+            a.g[0].mimg = dimg + (size_t)bconv_img_words(nsrc) * u0;
+            for (u32 u = 0; u < a.g[0].ndst; u++) {
+                a.g[0].dst_slot[u] = (u16)(u0 + u);
+                a.g[0].dst_prime[u] = (u16)dst_idx[u0 + u];
+            }
+            st = launch_bconv(a, BC_MAXDST, s);
+        }
+        cudaFreeAsync(dy, s);
+        cudaFreeAsync(dmb, s);
+        cudaFreeAsync(dimg, s);
+        return st;
+    }
     uint2 *dmat = nullptr;
     HKS_CUDA(cudaMallocAsync((void **)&dmat, mat.size() * sizeof(uint2), s));
     HKS_CUDA(cudaMemcpyAsync(dmat, mat.data(), mat.size() * sizeof(uint2), cudaMemcpyHostToDevice, s));

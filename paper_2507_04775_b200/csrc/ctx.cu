@@ -81,20 +81,6 @@ u64 shoup_of(u64 w, u64 m) { return (u64)(((u128)w << 64) / m); }
 
 ulonglong2 sh(u64 w, u64 m) { return make_ulonglong2(w, shoup_of(w, m)); }
 
-// Byte-column words of a base-conversion matrix entry v = [qhat]_t (tensor-pipe BConv, k_bconv_mma):
-// m_a = 2^(8a) v mod t for a = 0..7, and word c (c = 0..7) holds byte c of m_a in its byte a.  Then
-// for any y = sum_a y_a 2^(8a):  sum_a y_a m_a = sum_c 2^(8c) sum_a y_a byte_c(m_a) == y v (mod t).
-void push_bytecols(std::vector<u64> &out, u64 v, u64 t) {
-    u64 m[8];
-    m[0] = v % t;
-    for (int a = 1; a < 8; a++) m[a] = (u64)(((u128)m[a - 1] << 8) % t);
-    for (int c = 0; c < 8; c++) {
-        u64 w = 0;
-        for (int a = 0; a < 8; a++) w |= ((m[a] >> (8 * c)) & 0xffull) << (8 * a);
-        out.push_back(w);
-    }
-}
-
 uint2 split(u64 v) { return make_uint2((u32)(v & 0x3fffffffu), (u32)(v >> 30)); }
 
 u32 bitrev(u32 x, u32 bits) {
@@ -140,6 +126,34 @@ void twiddles(u64 m, u64 root, u32 log_n, u32 log_r, u32 log_c, ulonglong2 *col,
 }
 
 }  // namespace
+
+// Byte-column words of a base-conversion matrix entry v = [qhat]_t (tensor-pipe BConv, k_bconv_mma):
+// m_a = 2^(8a) v mod t for a = 0..7, and word c (c = 0..7) holds byte c of m_a in its byte a.  Then
+// for any y = sum_a y_a 2^(8a):  sum_a y_a m_a = sum_c 2^(8c) sum_a y_a byte_c(m_a) == y v (mod t).
+void push_bytecols(std::vector<u64> &out, u64 v, u64 t) {
+    u64 m[8];
+    m[0] = v % t;
+    for (int a = 1; a < 8; a++) m[a] = (u64)(((u128)m[a - 1] << 8) % t);
+    for (int c = 0; c < 8; c++) {
+        u64 w = 0;
+        for (int a = 0; a < 8; a++) w |= ((m[a] >> (8 * c)) & 0xffull) << (8 * a);
+        out.push_back(w);
+    }
+}
+
+
+// B-operand image of k_bconv_tc (internal.h bconv_img_words) from byte-column words [nsrc][ntg][8]:
+// image word (t, kc, c, h) = word (2kc + h, t, c), zero past the sources.
+void bconv_image(const u64 *matb, u32 nsrc, u32 ntg, std::vector<u64> &out) {
+    const u32 nch = bconv_img_words(nsrc) / 16;
+    for (u32 t = 0; t < ntg; t++)
+        for (u32 kc = 0; kc < nch; kc++)
+            for (u32 cc = 0; cc < 8; cc++)
+                for (u32 hh = 0; hh < 2; hh++) {
+                    const u32 i = 2 * kc + hh;
+                    out.push_back(i < nsrc ? matb[((size_t)i * ntg + t) * 8 + cc] : 0);
+                }
+}
 
 extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t num_q, const uint64_t *p,
                                      uint32_t num_p, uint32_t dnum, int device, hks_ctx **out) {
@@ -312,16 +326,7 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
 
     // k_bconv_tc B-operand images (internal.h bconv_img_words): image word (t, kc, c, h) = matb word
     // (2kc + h, t, c), zero past the sources
-    auto image = [](const u64 *matb, u32 nsrc, u32 ntg, std::vector<u64> &out) {
-        const u32 nch = bconv_img_words(nsrc) / 16;
-        for (u32 t = 0; t < ntg; t++)
-            for (u32 kc = 0; kc < nch; kc++)
-                for (u32 cc = 0; cc < 8; cc++)
-                    for (u32 hh = 0; hh < 2; hh++) {
-                        const u32 i = 2 * kc + hh;
-                        out.push_back(i < nsrc ? matb[((size_t)i * ntg + t) * 8 + cc] : 0);
-                    }
-    };
+    auto image = bconv_image;
     std::vector<u64> mu_img, md_img;
     // column-pass matrices for the tensor-core NTT (log N = 16 only; R = C = 256): the butterfly stages of
     // the pass (the same twiddles as k_ntt) applied to unit vectors, so the two 16-point rounds compose to

@@ -103,6 +103,11 @@ __host__ __device__ constexpr u32 bconv_img_words(u32 nsrc) { return 2 * ((nsrc 
 
 #define NTT16_IMG 2048   // words per 16 x 16 column-pass matrix image (bconv_img_words(16) * 16 targets)
 
+// host helpers (ctx.cu): the byte-column words of a matrix entry v = [qhat]_t (8 words, word c holding
+// byte c of 2^(8a) v mod t in its byte a) and the k_bconv_tc image of a [nsrc][ntg][8] word table
+void push_bytecols(std::vector<u64> &out, u64 v, u64 t);
+void bconv_image(const u64 *matb, u32 nsrc, u32 ntg, std::vector<u64> &out);
+
 struct BconvArgs {
     const u64 *in;
     u64 *out;
@@ -345,5 +350,9 @@ hks_status launch_bconv(const BconvArgs &a, u32 max_ndst, cudaStream_t s);
 // inverse EPI_SCALE, same limb map / scale semantics as launch_ntt_pass
 hks_status launch_ntt_cols_tc(const hks_ctx *ctx, NttDir dir, int epi, const NttArgs &a, cudaStream_t s);
 bool ntt_tc_enabled();
+bool bconv_tc_enabled();
+// out[i] = in[i] * w_i mod p_i (canonical) for n <= 16 limbs (hks_bconv's y_i = x_i [qhat_i]^-1)
+hks_status launch_limb_scale(const u64 *in, u64 *out, u32 nl, const u64 *w, const u64 *wp, const u64 *p, u32 log_n,
+                             cudaStream_t s);
 hks_status launch_kip(const KipArgs &a, cudaStream_t s);
 hks_status launch_automorph(const u64 *in, u64 *out, u32 nlimbs, u32 log_n, u64 galois, cudaStream_t s);

@@ -842,12 +842,52 @@ bool ntt_tc_enabled() {
     return on;
 }
 
+bool bconv_tc_enabled();
+
 static bool getenv_mma_enabled() {
     static const bool on = [] {
         const char *e = getenv("HKS_BCONV_MMA");
         return !(e && e[0] == '0');
     }();
     return on;
+}
+
+bool bconv_tc_enabled() { return getenv_mma_enabled() && getenv_tc_enabled(); }
+
+struct ScaleArgs {
+    const u64 *in;
+    u64 *out;
+    u64 w[BC_MAXSRC], wp[BC_MAXSRC], p[BC_MAXSRC];
+    u32 log_n;
+};
+__global__ void __launch_bounds__(256) k_limb_scale(const __grid_constant__ ScaleArgs A) {
+    pdl_trigger();
+    pdl_wait();
+    const size_t N = (size_t)1 << A.log_n;
+    const u32 i = blockIdx.y;
+    const size_t x = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    if (x >= N) return;
+    const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(A.in + i * N + x);
+    *reinterpret_cast<ulonglong2 *>(A.out + i * N + x) =
+        make_ulonglong2(shoup(v.x, A.w[i], A.wp[i], A.p[i]), shoup(v.y, A.w[i], A.wp[i], A.p[i]));
+}
+
+hks_status launch_limb_scale(const u64 *in, u64 *out, u32 nl, const u64 *w, const u64 *wp, const u64 *p, u32 log_n,
+                             cudaStream_t s) {
+    if (nl < 1 || nl > BC_MAXSRC) HKS_FAIL(HKS_EINVAL, "limb_scale: %u limbs", nl);
+    ScaleArgs a{};
+    a.in = in;
+    a.out = out;
+    a.log_n = log_n;
+    for (u32 i = 0; i < nl; i++) {
+        a.w[i] = w[i];
+        a.wp[i] = wp[i];
+        a.p[i] = p[i];
+    }
+    const size_t N = (size_t)1 << log_n;
+    (void)hks_launch(k_limb_scale, dim3((u32)(N / 2 / 256), nl), dim3(256), 0, s, a);
+    HKS_CHECK_LAUNCH();
+    return HKS_OK;
 }
 
 static bool getenv_kara_enabled() {

@@ -94,7 +94,10 @@ def test_ntt_large_batch(orc):
 @pytest.mark.parametrize("name,src,dst", [("T12", [0, 1, 2], [3, 4, 5, 6, 7, 8, 9]),
                                           ("C2", list(range(10)), list(range(10, 40))),
                                           ("C2", list(range(30, 40)), list(range(30))),
-                                          ("T12", [5], [0, 1, 9])])
+                                          ("T12", [5], [0, 1, 9]),
+                                          ("C4", list(range(36, 45)), list(range(36))),
+                                          ("C4", [7], list(range(7)) + list(range(8, 45))),
+                                          ("C1", [0, 1, 2], [3])])
 def test_bconv_parity(orc, name, src, dst):
     cfg, ctx, o = ctxs(orc, name)
     g = S.rng(420)
