@@ -1137,14 +1137,17 @@ hks_status launch_kip(const KipArgs &a, cudaStream_t s) {
     return HKS_OK;
 }
 
-// Multi-ciphertext key inner product: the key words of (t, x) are loaded once and reused for all nct
-// ciphertexts of the batch (amortising the dominant key stream, SURVEY.md §7 "key streaming").
+// Multi-ciphertext key inner product: the nct ciphertexts of a batch share one key, whose words are read
+// from HBM once per batch (amortising the dominant key stream, SURVEY.md §7 "key streaming").
 __global__ void __launch_bounds__(256) k_kip_multi(const __grid_constant__ KipMultiArgs A) {
+    // one (ciphertext, coefficient block) per CTA; the nct CTAs sharing a key block are adjacent in
+    // launch order (ciphertext fastest), so the key words come from HBM once and from L2 for the others
     pdl_trigger();
     pdl_wait();
     const size_t N = (size_t)1 << A.log_n;
     const u32 t = blockIdx.y;
-    const size_t x0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    const u32 c = blockIdx.x % A.nct, xb = blockIdx.x / A.nct;
+    const size_t x0 = ((size_t)xb * blockDim.x + threadIdx.x) * 2;
     if (x0 >= N) return;
     const u32 prime = t <= A.level ? t : A.nq + (t - A.level - 1);
     const PrimeConst pc = A.pc[prime];
@@ -1155,45 +1158,45 @@ __global__ void __launch_bounds__(256) k_kip_multi(const __grid_constant__ KipMu
     }
     constexpr int MAXD = 4;
     ulonglong2 kb[MAXD], ka[MAXD];
+    u64 d0[MAXD], d1[MAXD];
 #pragma unroll
     for (int j = 0; j < MAXD; j++) {
         if (j < (int)A.beta) {
             kb[j] = *reinterpret_cast<const ulonglong2 *>(A.evk + (((size_t)j * 2 + 0) * A.nk + prime) * N + x0);
             ka[j] = *reinterpret_cast<const ulonglong2 *>(A.evk + (((size_t)j * 2 + 1) * A.nk + prime) * N + x0);
-        }
-    }
-    for (u32 c = 0; c < A.nct; c++) {
-        Acc30 a0[2], a1[2];
-        acc_zero(a0[0]); acc_zero(a0[1]); acc_zero(a1[0]); acc_zero(a1[1]);
-#pragma unroll
-        for (int j = 0; j < MAXD; j++) {
-            if (j >= (int)A.beta) break;
             const bool own = A.c1[c] && t <= A.level && t / A.alpha == (u32)j;
             const u64 *D = own ? A.c1[c] + (size_t)t * N : A.ext[c] + ((size_t)j * A.ne + t) * N;
-            const u64 d0 = D[s0], d1 = D[s1];
-            u32 dl, dh, ml, mh;
-            split30(d0, dl, dh);
-            split30(kb[j].x, ml, mh); acc_mac(a0[0], dl, dh, ml, mh);
-            split30(ka[j].x, ml, mh); acc_mac(a1[0], dl, dh, ml, mh);
-            split30(d1, dl, dh);
-            split30(kb[j].y, ml, mh); acc_mac(a0[1], dl, dh, ml, mh);
-            split30(ka[j].y, ml, mh); acc_mac(a1[1], dl, dh, ml, mh);
+            d0[j] = D[s0];
+            d1[j] = D[s1];
         }
-        ulonglong2 o0, o1;
-        o0.x = acc_reduce(a0[0], pc);
-        o0.y = acc_reduce(a0[1], pc);
-        o1.x = acc_reduce(a1[0], pc);
-        o1.y = acc_reduce(a1[1], pc);
-        *reinterpret_cast<ulonglong2 *>(A.acc[c] + (size_t)t * N + x0) = o0;
-        *reinterpret_cast<ulonglong2 *>(A.acc[c] + ((size_t)A.ne + t) * N + x0) = o1;
     }
+    Acc30 a0[2], a1[2];
+    acc_zero(a0[0]); acc_zero(a0[1]); acc_zero(a1[0]); acc_zero(a1[1]);
+#pragma unroll
+    for (int j = 0; j < MAXD; j++) {
+        if (j >= (int)A.beta) break;
+        u32 dl, dh, ml, mh;
+        split30(d0[j], dl, dh);
+        split30(kb[j].x, ml, mh); acc_mac(a0[0], dl, dh, ml, mh);
+        split30(ka[j].x, ml, mh); acc_mac(a1[0], dl, dh, ml, mh);
+        split30(d1[j], dl, dh);
+        split30(kb[j].y, ml, mh); acc_mac(a0[1], dl, dh, ml, mh);
+        split30(ka[j].y, ml, mh); acc_mac(a1[1], dl, dh, ml, mh);
+    }
+    ulonglong2 o0, o1;
+    o0.x = acc_reduce(a0[0], pc);
+    o0.y = acc_reduce(a0[1], pc);
+    o1.x = acc_reduce(a1[0], pc);
+    o1.y = acc_reduce(a1[1], pc);
+    *reinterpret_cast<ulonglong2 *>(A.acc[c] + (size_t)t * N + x0) = o0;
+    *reinterpret_cast<ulonglong2 *>(A.acc[c] + ((size_t)A.ne + t) * N + x0) = o1;
 }
 
 hks_status launch_kip_multi(const KipMultiArgs &a, cudaStream_t s) {
     if (a.beta > 4 || a.nct > KIP_MAXCT) HKS_FAIL(HKS_EINVAL, "kip_multi: beta %u / nct %u", a.beta, a.nct);
     const u32 threads = 256;
     const size_t N = (size_t)1 << a.log_n;
-    dim3 grid((u32)((N / 2 + threads - 1) / threads), a.ne);
+    dim3 grid((u32)((N / 2 + threads - 1) / threads) * a.nct, a.ne);
     ProfScope ps(K_KIP, s);
     (void)hks_launch(k_kip_multi, grid, dim3(threads), 0, s, a);
     HKS_CHECK_LAUNCH();
