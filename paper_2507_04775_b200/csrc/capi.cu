@@ -316,7 +316,7 @@ extern "C" hks_status hks_bconv(const hks_ctx *c, const uint64_t *x, const uint3
     }
     DevGuard g(c->device);
     cudaStream_t s = (cudaStream_t)stream;
-    if (c->all_big && bconv_tc_enabled()) {
+    if (c->all_big && bconv_tc_enabled() && bconv_tc_large(c->log_n, 1)) {
         // tensor-core path (the hot path's kernel): y_i = [x_i qhat_i^-1]_{q_i} into a temporary, then
         // k_bconv_tc with this call's byte-column words and B-operand image
         std::vector<u64> matb, img, w(nsrc), wp(nsrc), pp(nsrc);

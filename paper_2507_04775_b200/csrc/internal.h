@@ -351,6 +351,7 @@ hks_status launch_bconv(const BconvArgs &a, u32 max_ndst, cudaStream_t s);
 hks_status launch_ntt_cols_tc(const hks_ctx *ctx, NttDir dir, int epi, const NttArgs &a, cudaStream_t s);
 bool ntt_tc_enabled();
 bool bconv_tc_enabled();
+bool bconv_tc_large(u32 log_n, u32 ngroups);
 // out[i] = in[i] * w_i mod p_i (canonical) for n <= 16 limbs (hks_bconv's y_i = x_i [qhat_i]^-1)
 hks_status launch_limb_scale(const u64 *in, u64 *out, u32 nl, const u64 *w, const u64 *wp, const u64 *p, u32 log_n,
                              cudaStream_t s);

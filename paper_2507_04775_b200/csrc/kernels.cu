@@ -843,6 +843,7 @@ bool ntt_tc_enabled() {
 }
 
 bool bconv_tc_enabled();
+bool bconv_tc_large(u32 log_n, u32 ngroups);
 
 static bool getenv_mma_enabled() {
     static const bool on = [] {
@@ -853,6 +854,17 @@ static bool getenv_mma_enabled() {
 }
 
 bool bconv_tc_enabled() { return getenv_mma_enabled() && getenv_tc_enabled(); }
+
+// enough 128-coefficient tiles to give every SM one (otherwise the tensor kernels' fixed prologue loses)
+bool bconv_tc_large(u32 log_n, u32 ngroups) {
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return (((size_t)1 << log_n) >> 7) * ngroups >= (size_t)nsm;
+}
 
 struct ScaleArgs {
     const u64 *in;
@@ -1037,7 +1049,10 @@ hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
             default: break;
         }
     }
-    if (!a.prescale && a.big && a.g[0].mimg && getenv_mma_enabled() && getenv_tc_enabled()) {
+    // the tensor-core kernels pay a fixed prologue (TMEM allocation, matrix image, barriers): small
+    // conversions (fewer 128-coefficient tiles than SMs, e.g. N = 2^12) stay on the integer pipe
+    const bool large = bconv_tc_large(a.log_n, a.ngroups);
+    if (!a.prescale && a.big && large && a.g[0].mimg && getenv_mma_enabled() && getenv_tc_enabled()) {
         switch (a.g[0].nsrc) {
 #define CT(NS) case NS: return bconv_tc_go<NS>(a, s);
             CT(1) CT(2) CT(3) CT(4) CT(5) CT(6) CT(7) CT(8) CT(9) CT(10) CT(11) CT(12) CT(13) CT(14) CT(15) CT(16)
@@ -1045,7 +1060,7 @@ hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
             default: break;
         }
     }
-    if (!a.prescale && a.big && a.g[0].matb && ((size_t)1 << a.log_n) >= MMA_CW && getenv_mma_enabled()) {
+    if (!a.prescale && a.big && large && a.g[0].matb && getenv_mma_enabled()) {
         switch (a.g[0].nsrc) {
 #define CM(NS) case NS: bconv_mma_go<NS>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
             CM(1) CM(2) CM(3) CM(4) CM(5) CM(6) CM(7) CM(8) CM(9) CM(10) CM(11) CM(12) CM(13) CM(14) CM(15) CM(16)
