@@ -932,9 +932,19 @@ hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s) {
     HKS_FAIL(HKS_EINVAL, "ntt_kip: unsupported log_n %u", ctx->log_n);
 }
 
-hks_status run_ntt_kip(const hks_ctx *ctx, const std::vector<KipItem> &items, u32 ndig, const u64 *ext,
+hks_status run_ntt_kip(const hks_ctx *ctx, const std::vector<KipItem> &items_in, u32 ndig, const u64 *ext,
                        const u64 *c1, const u64 *evk, u64 *acc, u32 nkey, u32 acc_stride, cudaStream_t s,
                        u64 *y, u32 ystride) {
+    // heaviest limbs first (more transformed terms; special limbs also run ModDown's inverse row pass), so
+    // the grid's tail is made of light CTAs (measured at C2: the special limbs last formed a ~20 us tail)
+    std::vector<KipItem> items(items_in);
+    auto weight = [&](const KipItem &it) {
+        u32 w = (y && it.yslot != 0xffff) ? 2 : 0;
+        for (u32 j = 0; j < ndig; j++) w += (it.src[j] & FK_DIRECT) ? 0 : 1;
+        return w;
+    };
+    std::stable_sort(items.begin(), items.end(),
+                     [&](const KipItem &a, const KipItem &b) { return weight(a) > weight(b); });
     for (size_t u0 = 0; u0 < items.size(); u0 += FK_MAXU) {
         FusedKipArgs a{};
         a.ext = ext;
