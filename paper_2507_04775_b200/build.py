@@ -11,8 +11,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libhks.so")
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["ctx.cu", "ntt.cu", "kernels.cu", "capi.cu", "prof.cu", "shard.cu"]
-HEADERS = ["internal.h", "modarith.cuh", os.path.join("..", "..", "include", "hks.h")]
+SOURCES = ["ctx.cu", "ntt.cu", "ntt_tc.cu", "kernels.cu", "capi.cu", "prof.cu", "shard.cu"]
+HEADERS = ["internal.h", "modarith.cuh", "tc.cuh", os.path.join("..", "..", "include", "hks.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

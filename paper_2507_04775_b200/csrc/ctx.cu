@@ -328,17 +328,21 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     // (2kc + h, t, c), zero past the sources
     auto image = bconv_image;
     std::vector<u64> mu_img, md_img;
-    // column-pass matrices for the tensor-core NTT (log N = 16 only; R = C = 256): the butterfly stages of
-    // the pass (the same twiddles as k_ntt) applied to unit vectors, so the two 16-point rounds compose to
-    // exactly the column pass's linear map
+    // Column-pass tables of the tensor-core NTT (log N = 16 only; R = C = 256; ntt_tc.cu).  The butterfly
+    // stages of the pass (the same twiddles as k_ntt) are applied to unit vectors, giving the 16 x 16
+    // matrices of its two rounds: forward = W_A (stages 0-3, any stride-16 class) then W_B[b] (stages 4-7,
+    // block b) = W_B[0] diag(d_b); inverse = W'_B[b] (GS stages 7-4) = diag(f_b) W'_B[0] then W'_A (GS
+    // stages 3-0).  Per prime and direction: image of round 1 (W_A / W'_B[0]), image of round 2
+    // (W_B[0] / W'_A), and the twist between the rounds as Shoup pairs tw[v][o] for round-1 vector class v
+    // and output o (forward d_o[v], inverse f_v[o]).
     std::vector<u64> ntt_img_fwd, ntt_img_inv;
     if (log_n == 16) {
-        ntt_img_fwd.reserve((size_t)nm * 17 * NTT16_IMG);
-        ntt_img_inv.reserve((size_t)nm * 17 * NTT16_IMG);
+        ntt_img_fwd.reserve((size_t)nm * NTT16_TAB);
+        ntt_img_inv.reserve((size_t)nm * NTT16_TAB);
         for (u32 pi = 0; pi < nm; pi++) {
             const u64 m = primes[pi];
             const ulonglong2 *twf = &tcf[(size_t)pi * R], *twi = &tci[(size_t)pi * R];
-            // stages [s_first, s_last] of the 256-row column transform on a unit vector at row `row`
+            // stages s_from .. s_to of the 256-row column transform on a unit vector at `row`
             auto run = [&](bool fwd, int s_from, int s_to, u32 row, std::vector<u64> &v) {
                 v.assign(R, 0);
                 v[row] = 1;
@@ -362,24 +366,45 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
                     if (st == s_to) break;
                 }
             };
-            // matrix W[k'][k] of rows {base + str k} -> {base + str k'} as an image (targets k', sources k)
-            auto emit = [&](bool fwd, int s_from, int s_to, u32 base, u32 str, std::vector<u64> &out) {
-                std::vector<u64> words((size_t)16 * 16 * 8);   // matb layout [k][k'][c]
-                std::vector<u64> v, w8;
+            // W[k'][k]: rows {base + str k} -> {base + str k'}
+            auto matrix = [&](bool fwd, int s_from, int s_to, u32 base, u32 str) {
+                std::vector<u64> W(256), v;
                 for (u32 k = 0; k < 16; k++) {
                     run(fwd, s_from, s_to, base + str * k, v);
+                    for (u32 kk = 0; kk < 16; kk++) W[kk * 16 + k] = v[base + str * kk];
+                }
+                return W;
+            };
+            auto emit_image = [&](const std::vector<u64> &W, std::vector<u64> &out) {
+                std::vector<u64> words((size_t)16 * 16 * 8), w8;   // matb layout [k][k'][c]
+                for (u32 k = 0; k < 16; k++)
                     for (u32 kk = 0; kk < 16; kk++) {
                         w8.clear();
-                        push_bytecols(w8, v[base + str * kk], m);
+                        push_bytecols(w8, W[kk * 16 + k], m);
                         std::copy(w8.begin(), w8.end(), words.begin() + ((size_t)k * 16 + kk) * 8);
                     }
-                }
                 image(words.data(), 16, 16, out);
             };
-            emit(true, 0, 3, 0, 16, ntt_img_fwd);
-            for (u32 b = 0; b < 16; b++) emit(true, 4, 7, 16 * b, 1, ntt_img_fwd);
-            for (u32 b = 0; b < 16; b++) emit(false, 7, 4, 16 * b, 1, ntt_img_inv);
-            emit(false, 3, 0, 0, 16, ntt_img_inv);
+            for (int dir = 0; dir < 2; dir++) {
+                const bool fwd = dir == 0;
+                std::vector<u64> &out = fwd ? ntt_img_fwd : ntt_img_inv;
+                const std::vector<u64> W1 = fwd ? matrix(true, 0, 3, 0, 16) : matrix(false, 7, 4, 0, 1);
+                const std::vector<u64> W2 = fwd ? matrix(true, 4, 7, 0, 1) : matrix(false, 3, 0, 0, 16);
+                emit_image(W1, out);
+                emit_image(W2, out);
+                std::vector<std::vector<u64>> Wb(16);
+                for (u32 b = 0; b < 16; b++) Wb[b] = fwd ? matrix(true, 4, 7, 16 * b, 1) : matrix(false, 7, 4, 16 * b, 1);
+                for (u32 v = 0; v < 16; v++)
+                    for (u32 o = 0; o < 16; o++) {
+                        // forward: column v of W_B[o] over column v of W_B[0]; inverse: row o of W'_B[v]
+                        // over row o of W'_B[0] (entries are products of roots of unity, never 0)
+                        const u64 num = fwd ? Wb[o][0 * 16 + v] : Wb[v][o * 16 + 0];
+                        const u64 den = fwd ? W2[0 * 16 + v] : W1[o * 16 + 0];
+                        const u64 tw = mul_mod(num, inv_mod(den, m), m);
+                        out.push_back(tw);
+                        out.push_back(shoup_of(tw, m));
+                    }
+            }
         }
     }
     c->mu_img_off.assign((size_t)num_q * dnum, 0);

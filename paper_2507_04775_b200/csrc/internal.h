@@ -102,6 +102,7 @@ struct BconvGroup {
 __host__ __device__ constexpr u32 bconv_img_words(u32 nsrc) { return 2 * ((nsrc + 3) / 4) * 16; }
 
 #define NTT16_IMG 2048   // words per 16 x 16 column-pass matrix image (bconv_img_words(16) * 16 targets)
+#define NTT16_TAB (2 * NTT16_IMG + 512)   // per prime: round-1 image, round-2 image, twist (w, w')[16][16]
 
 // host helpers (ctx.cu): the byte-column words of a matrix entry v = [qhat]_t (8 words, word c holding
 // byte c of 2^(8a) v mod t in its byte a) and the k_bconv_tc image of a [nsrc][ntg][8] word table
@@ -242,9 +243,8 @@ struct hks_ctx {
     std::vector<size_t> mu_img_off;     // [(L+1) * dnum]: word offset of the (level, digit) B image in d_mu_img
     u64 *d_mu_img = nullptr;            // ModUp matrices as k_bconv_tc B-operand images (per target contiguous)
     u64 *d_md_img = nullptr;            // ModDown matrix as a k_bconv_tc B-operand image
-    // k_ntt16_tc (log N = 16): per prime 17 B-operand images (NTT16_IMG words each) of the 16 x 16 matrices
-    // of the column pass -- forward: [0] stages 0-3 on a stride-16 class, [1 + b] stages 4-7 on rows
-    // 16b..16b+15; inverse: [b] GS stages 7-4 on block b, [16] GS stages 3-0 on a class
+    // k_ntt_cols_tc (log N = 16): per prime NTT16_TAB words -- the B-operand images of the two 16-point
+    // rounds of the column pass and the twist between them (ctx.cu, ntt_tc.cu)
     u64 *d_ntt_img_fwd = nullptr, *d_ntt_img_inv = nullptr;
     ulonglong2 *d_pinv = nullptr;       // P^-1 mod q_i  [L+1] (Shoup)
     u64 *d_qmod = nullptr;              // Rescale: q_j mod q_i  [L+1][L+1] (row j = dropped limb)

@@ -10,6 +10,7 @@
 #include <stdlib.h>
 
 #include "internal.h"
+#include "tc.cuh"
 
 // source limb i of a base-conversion group: an absolute (possibly peer-mapped) address, or a slot of A.in
 __device__ __forceinline__ const u64 *bc_src(const BconvArgs &A, const BconvGroup &G, int i, size_t N) {
@@ -377,52 +378,6 @@ static void bconv_mma_go(const BconvArgs &a, cudaStream_t s) {
 #define TC_EPW HKS_TC_EPW                  // epilogue warps (multiple of 4)
 #define TC_THREADS ((TC_EPW + 4) * 32)
 
-__device__ __forceinline__ u32 smem_u32(const void *p) { return (u32)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(u32 a, u32 count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
-}
-__device__ __forceinline__ void mbar_wait(u32 a, u32 parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "W%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra W%=;\n\t}" ::"r"(a),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(u32 a) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void tc_commit(u32 mbar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
-                 : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-// no-swizzle K-major smem matrix descriptor (version 1): start, LBO = K-chunk stride, SBO = 8-row stride
-__device__ __forceinline__ u64 tc_desc(u32 saddr, u32 lbo, u32 sbo) {
-    return (u64)((saddr >> 4) & 0x3fff) | ((u64)((lbo >> 4) & 0x3fff) << 16) | ((u64)((sbo >> 4) & 0x3fff) << 32) |
-           (1ull << 46);
-}
-__device__ __forceinline__ void tc_mma_i8(u32 dtmem, u64 adesc, u64 bdesc, u32 idesc, u32 accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void tc_ld8(u32 taddr, u32 (&v)[8]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                 : "r"(taddr)
-                 : "memory");
-}
-__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void cp_async8(u32 saddr, const void *g) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr), "l"(g) : "memory");
-}
-
 template <int NSRC, bool LAZY>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constant__ BconvArgs A) {
     pdl_trigger();
@@ -613,212 +568,6 @@ static hks_status bconv_tc_go(const BconvArgs &a, cudaStream_t s) {
     }
     ps.done(words * (double)N * 8.0, macs * (double)N * 4.0);
     if (e != cudaSuccess) HKS_FAIL(HKS_ECUDA, "k_bconv_tc launch: %s", cudaGetErrorString(e));
-    return HKS_OK;
-}
-
-// ------------------------------------------------------------------------------------------------
-// Column pass of the N = 2^16 NTT on the tensor cores.  The pass (8 butterfly stages on
-// each 256-row column) is the product of two rounds of 16-point transforms: forward = [stages 0-3 on the
-// stride-16 classes {r0 + 16k}, one matrix] then [stages 4-7 on the blocks {16b + k}, one matrix per b];
-// inverse = [GS stages 7-4 per block b] then [GS stages 3-0 per class].  Each round is, per limb, a
-// (4096 vectors x 16) x (16 x 16) product mod p, done with the byte-split identity of k_bconv_tc: A =
-// the vector's 16 words (K = 128 bytes), B = the matrix image (N = 16 outputs x 8 byte columns), D in
-// TMEM, one tcgen05.ld + 14-instruction reduction per output.  Outputs are congruent to the butterfly
-// pass's (same linear map mod p), lazily reduced to [0, 3p) except the final inverse round, which
-// applies the EPI_SCALE factor and canonicalises.  Tiles: 128 vectors (consecutive columns c) of one
-// (limb, class / block); persistent CTAs (two per SM: 256 TMEM columns each).
-#ifndef HKS_NT_SA
-#define HKS_NT_SA 3
-#endif
-#ifndef HKS_NT_CPS
-#define HKS_NT_CPS 2       // CTAs per SM
-#endif
-#define NT_SA HKS_NT_SA
-#define NT_EPW 8
-#define NT_THREADS ((NT_EPW + 4) * 32)
-struct Ntt16Args {
-    const u64 *in;
-    u64 *out;
-    const u64 *img;             // [prime][17][NTT16_IMG]
-    const ulonglong2 *scale;    // final inverse round: scale[b % scale_mod] or, if NULL, ninv[prime]
-    const ulonglong2 *ninv;
-    const PrimeConst *pc;
-    u32 log_n, nlimbs, scale_mod;
-    u32 fwd, round;             // round 0 reads in (slot sin), round 1 works in place on out (slot sout)
-    LimbMap map;
-};
-
-template <bool FINAL>
-__global__ void __launch_bounds__(NT_THREADS, HKS_NT_CPS) k_ntt16_tc(const __grid_constant__ Ntt16Args A) {
-    pdl_trigger();
-    constexpr u32 SBO = 1024;                 // 8 K-chunks x 128 bytes per 8-row group
-    constexpr u32 STAGE = 2 * 16384;          // A tile (128 x 128 bytes) + B image (128 x 128 bytes)
-    const size_t N = (size_t)1 << A.log_n;
-    const u32 ntiles_all = A.nlimbs * 32;
-    const u32 ntile = blockIdx.x < ntiles_all ? (ntiles_all - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const bool strided = (A.fwd != 0) == (A.round == 0);   // class round (stride 16 rows) vs block round
-    extern __shared__ __align__(1024) uint8_t nsm[];
-    __shared__ __align__(8) u64 bar_done[2], bar_empty[2], bar_free[NT_SA];
-    __shared__ u32 tmem_base_s;
-    const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // tile -> limb b, class / block cl, half h: vectors c = 128 h + m; element k at base + m + str k
-    auto tile_geo = [&](u32 tile, u32 &b, u32 &cl, size_t &base, size_t &str) {
-        b = tile >> 5;
-        cl = (tile >> 1) & 15;
-        const u32 h = tile & 1;
-        base = (strided ? (size_t)cl * 256 : (size_t)cl * 16 * 256) + 128 * h;
-        str = strided ? 16 * 256 : 256;
-    };
-    if (tid == 0) {
-        for (int b = 0; b < 2; b++) {
-            mbar_init(smem_u32(&bar_done[b]), 1);
-            mbar_init(smem_u32(&bar_empty[b]), NT_EPW);
-        }
-        for (int s = 0; s < NT_SA; s++) mbar_init(smem_u32(&bar_free[s]), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base_s)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const u32 tmem = tmem_base_s;
-    pdl_wait();
-
-    if (warp >= NT_EPW) {
-        // ---------------- producers + MMA issuer ----------------
-        const u32 m = tid - NT_EPW * 32;      // vector (row of the A tile)
-        const u32 soff = (m >> 3) * SBO + (m & 7) * 16;
-        auto load_tile = [&](u32 j) {
-            const u32 tile = blockIdx.x + j * gridDim.x;
-            u32 b, cl;
-            size_t base, str;
-            tile_geo(tile, b, cl, base, str);
-            const u64 *src = (A.round == 0 ? A.in + (size_t)A.map.sin[b] * N : A.out + (size_t)A.map.sout[b] * N) + base + m;
-            const u32 sa = smem_u32(nsm + (j % NT_SA) * STAGE);
-#pragma unroll
-            for (int k = 0; k < 16; k++) cp_async8(sa + soff + (k >> 1) * 128 + (k & 1) * 8, src + str * k);
-            const u32 im = A.fwd ? (A.round == 0 ? 0 : 1 + cl) : (A.round == 0 ? cl : 16);
-            const uint8_t *img = reinterpret_cast<const uint8_t *>(A.img + ((size_t)A.map.prime[b] * 17 + im) * NTT16_IMG);
-#pragma unroll
-            for (int r = 0; r < 8; r++) {
-                const u32 off = (r * 128 + m) * 16;
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16384 + off), "l"(img + off) : "memory");
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        };
-        const u32 idesc = (2u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);   // M = N = 128, s32 += u8 x u8
-        for (u32 j = 0; j + 1 < NT_SA; j++) {
-            if (j < ntile) load_tile(j);
-            else asm volatile("cp.async.commit_group;" ::: "memory");
-        }
-        for (u32 j = 0; j < ntile; j++) {
-            const u32 jn = j + NT_SA - 1;
-            if (jn < ntile) {
-                if (jn >= NT_SA) mbar_wait(smem_u32(&bar_free[jn % NT_SA]), (jn / NT_SA - 1) & 1);
-                load_tile(jn);
-            } else {
-                asm volatile("cp.async.commit_group;" ::: "memory");
-            }
-            asm volatile("cp.async.wait_group %0;" ::"n"(NT_SA - 1) : "memory");
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (m == 0) {
-                const u32 b = j & 1;
-                if (j >= 2) mbar_wait(smem_u32(&bar_empty[b]), ((j >> 1) - 1) & 1);
-                tc_fence_after();
-                const u32 abase = smem_u32(nsm + (j % NT_SA) * STAGE), bbase = abase + 16384;
-#pragma unroll
-                for (int s = 0; s < 4; s++)
-                    tc_mma_i8(tmem + b * 128, tc_desc(abase + s * 256, 128, SBO), tc_desc(bbase + s * 256, 128, SBO),
-                              idesc, s > 0 ? 1u : 0u);
-                tc_commit(smem_u32(&bar_free[j % NT_SA]));
-                tc_commit(smem_u32(&bar_done[b]));
-            }
-        }
-    } else {
-        // ---------------- epilogue: outputs k' = h, h + 2, ..., four TMEM loads in flight ----------------
-        const u32 q = warp & 3, h = warp >> 2;
-        const u32 mrow = q * 32 + lane;
-        for (u32 j = 0; j < ntile; j++) {
-            const u32 tb = j & 1;
-            const u32 tile = blockIdx.x + j * gridDim.x;
-            u32 b, cl;
-            size_t base, str;
-            tile_geo(tile, b, cl, base, str);
-            const PrimeConst pc = A.pc[A.map.prime[b]];
-            const u64 np = 0 - pc.p;
-            const u32 mu = (u32)pc.mu80;
-            ulonglong2 sc = make_ulonglong2(0, 0);
-            if (FINAL) sc = A.scale ? A.scale[b % A.scale_mod] : A.ninv[A.map.prime[b]];
-            u64 *dst = A.out + (size_t)A.map.sout[b] * N + base + mrow;
-            mbar_wait(smem_u32(&bar_done[tb]), (j >> 1) & 1);
-            tc_fence_after();
-            const u32 tbase = tmem + tb * 128 + ((q * 32) << 16);
-#pragma unroll
-            for (u32 k0 = 0; k0 < 16; k0 += 8) {
-                u32 v[4][8];
-#pragma unroll
-                for (int k = 0; k < 4; k++) tc_ld8(tbase + (h + k0 + 2 * k) * 8, v[k]);
-                tc_wait_ld();
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const u32 kk = h + k0 + 2 * k;
-                    u64 r = bytesum_reduce_c<true>(v[k], np, mu);
-                    if (FINAL) r = csub(csub(shoup_approx(r, sc.x, sc.y, np), 2 * pc.p), pc.p);
-                    dst[str * kk] = r;
-                }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&bar_empty[tb]));
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
-    }
-}
-
-// Column pass through the tensor cores: two launches (rounds), the second in place on out.
-hks_status launch_ntt_cols_tc(const hks_ctx *ctx, NttDir dir, int epi, const NttArgs &na, cudaStream_t s) {
-    constexpr size_t smem = (size_t)NT_SA * 2 * 16384;
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_ntt16_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_ntt16_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }
-    Ntt16Args a;
-    a.in = na.in;
-    a.out = na.out;
-    a.img = dir == NTT_FWD ? ctx->d_ntt_img_fwd : ctx->d_ntt_img_inv;
-    a.scale = na.scale;
-    a.ninv = ctx->d_ninv;
-    a.pc = ctx->d_pc;
-    a.log_n = ctx->log_n;
-    a.nlimbs = na.nlimbs;
-    a.scale_mod = na.scale_mod ? na.scale_mod : 1;
-    a.fwd = dir == NTT_FWD;
-    a.map = na.map;
-    const u32 grid = std::min<u32>(a.nlimbs * 32, HKS_NT_CPS * (u32)nsm);
-    for (u32 r = 0; r < 2; r++) {
-        a.round = r;
-        const bool final = dir == NTT_INV && r == 1;
-        (void)epi;
-        ProfScope ps(dir == NTT_FWD ? K_NTT_FWD_COLS : K_NTT_INV_COLS, s);
-        const cudaError_t e = final ? hks_launch(k_ntt16_tc<true>, dim3(grid), dim3(NT_THREADS), smem, s, a)
-                                    : hks_launch(k_ntt16_tc<false>, dim3(grid), dim3(NT_THREADS), smem, s, a);
-        const double nn = (double)((size_t)1 << a.log_n);
-        ps.done(2.0 * a.nlimbs * nn * 8.0, a.nlimbs * (nn / 2.0) * 4 * 7.0);
-        if (e != cudaSuccess) HKS_FAIL(HKS_ECUDA, "k_ntt16_tc launch: %s", cudaGetErrorString(e));
-    }
     return HKS_OK;
 }
 

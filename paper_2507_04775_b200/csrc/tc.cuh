@@ -1,0 +1,51 @@
+// tc.cuh -- tcgen05 / TMEM / mbarrier / cp.async helpers shared by the tensor-core kernels
+// (k_bconv_tc in kernels.cu, k_ntt_cols_tc in ntt_tc.cu).  sm_100a only.
+#pragma once
+#include "internal.h"
+
+__device__ __forceinline__ u32 smem_u32(const void *p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u32 a, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(u32 a, u32 parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "W%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W%=;\n\t}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(u32 a) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void tc_commit(u32 mbar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// no-swizzle K-major smem matrix descriptor (version 1): start, LBO = K-chunk stride, SBO = 8-row stride
+__device__ __forceinline__ u64 tc_desc(u32 saddr, u32 lbo, u32 sbo) {
+    return (u64)((saddr >> 4) & 0x3fff) | ((u64)((lbo >> 4) & 0x3fff) << 16) | ((u64)((sbo >> 4) & 0x3fff) << 32) |
+           (1ull << 46);
+}
+__device__ __forceinline__ void tc_mma_i8(u32 dtmem, u64 adesc, u64 bdesc, u32 idesc, u32 accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tc_ld8(u32 taddr, u32 (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cp_async8(u32 saddr, const void *g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr), "l"(g) : "memory");
+}
+

@@ -6,7 +6,7 @@ name=$1; shift
 out=/root/repo/tools/exp/$name
 mkdir -p $out
 cd /root/repo/paper_2507_04775_b200/csrc
-for f in ctx ntt kernels capi prof shard; do
+for f in ctx ntt ntt_tc kernels capi prof shard; do
   /usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC \
     --expt-relaxed-constexpr "$@" -c $f.cu -o $out/$f.o &
 done
