@@ -524,3 +524,46 @@ def test_keyswitch_batch_shared_key_parity(orc):
     for i in range(nct):
         w0, w1 = o.keyswitch(c0s[i], c1s[i], evk, level)
         assert (to_host(outs0[i]) == w0).all() and (to_host(outs1[i]) == w1).all(), i
+
+
+def test_keyswitch_after_cross_stream_copy(orc):
+    """Programmatic dependent launch must not let a KeySwitch start before a cross-stream dependency
+    (an H2D copy ordered by an event) completes: the e2e pipeline and any caller rely on it."""
+    import torch
+    cfg, ctx, o = ctxs(orc, "C2")
+    dev = "cuda:0"
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+    n, level = cfg.n, 29
+    prim = list(cfg.q) + list(cfg.p)
+
+    def limbs(pr):
+        return torch.stack([torch.randint(0, int(p), (n,), generator=g, device=dev, dtype=torch.int64) for p in pr])
+
+    evk = torch.stack([limbs(prim) for _ in range(2 * cfg.dnum)]).reshape(cfg.dnum, 2, len(prim), n)
+    cts = [(limbs(cfg.q), limbs(cfg.q)) for _ in range(3)]
+    ws = ctx.workspace(H.OP_KEYSWITCH, level)
+    refs = []
+    for c0, c1 in cts:
+        r0, r1 = torch.empty_like(c0), torch.empty_like(c1)
+        H.keyswitch(ctx, c0, c1, level, evk, r0, r1, ws)
+        refs.append((r0, r1))
+    host = [(c0.cpu().pin_memory(), c1.cpu().pin_memory()) for c0, c1 in cts]
+    d0, d1 = torch.empty_like(cts[0][0]), torch.empty_like(cts[0][1])
+    s_cmp, s_cpy = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    outs = [(torch.empty_like(d0), torch.empty_like(d1)) for _ in range(9)]
+    e_done, e_in = torch.cuda.Event(), torch.cuda.Event()
+    torch.cuda.synchronize()
+    for i in range(9):
+        k = i % 3
+        with torch.cuda.stream(s_cpy):
+            s_cpy.wait_event(e_done)                # previous KeySwitch has read d0, d1
+            d0.copy_(host[k][0], non_blocking=True)
+            d1.copy_(host[k][1], non_blocking=True)
+            e_in.record(s_cpy)
+        s_cmp.wait_event(e_in)
+        H.keyswitch(ctx, d0, d1, level, evk, outs[i][0], outs[i][1], ws, s_cmp.cuda_stream)
+        e_done.record(s_cmp)
+    torch.cuda.synchronize()
+    for i in range(9):
+        assert torch.equal(outs[i][0], refs[i % 3][0]) and torch.equal(outs[i][1], refs[i % 3][1]), i
