@@ -602,8 +602,13 @@ hks_status run_rescale(const hks_ctx *ctx, u32 npoly, u32 level, const u64 *x, c
 // per output).  D never returns to HBM.
 // resident CTAs per SM requested from ptxas: an 80-register budget per thread (the kernel's natural
 // size), 1..16 CTAs
+#ifndef HKS_KIP_REGS
+#define HKS_KIP_REGS 80   // register budget per thread of the fused row pass + key product
+#endif
 constexpr int kip_minb(int threads) {
-    return (65536 / (80 * threads)) < 1 ? 1 : ((65536 / (80 * threads)) > 16 ? 16 : 65536 / (80 * threads));
+    return (65536 / (HKS_KIP_REGS * threads)) < 1
+               ? 1
+               : ((65536 / (HKS_KIP_REGS * threads)) > 16 ? 16 : 65536 / (HKS_KIP_REGS * threads));
 }
 template <int LOGN, int LOGE, int LOGNB, int NTR, int NDIG>
 __global__ void __launch_bounds__(NTR * ((1 << LOGNB) << (LOGN - LOGE)),
