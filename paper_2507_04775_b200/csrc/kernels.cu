@@ -903,55 +903,65 @@ hks_status launch_kip(const KipArgs &a, cudaStream_t s) {
 
 // Multi-ciphertext key inner product: the nct ciphertexts of a batch share one key, whose words are read
 // from HBM once per batch (amortising the dominant key stream, SURVEY.md §7 "key streaming").
+template <int BETA>
 __global__ void __launch_bounds__(256) k_kip_multi(const __grid_constant__ KipMultiArgs A) {
     // one (ciphertext, coefficient block) per CTA; the nct CTAs sharing a key block are adjacent in
-    // launch order (ciphertext fastest), so the key words come from HBM once and from L2 for the others
+    // launch order (ciphertext fastest), so the key words come from HBM once and from L2 for the others.
+    // Karatsuba products (3 IMAD.WIDE each), the digit count a template parameter (straight-line code).
     pdl_trigger();
     pdl_wait();
     const size_t N = (size_t)1 << A.log_n;
     const u32 t = blockIdx.y;
-    const u32 c = blockIdx.x % A.nct, xb = blockIdx.x / A.nct;
+    const u32 xb = blockIdx.x / A.nct, c = blockIdx.x - xb * A.nct;
     const size_t x0 = ((size_t)xb * blockDim.x + threadIdx.x) * 2;
     if (x0 >= N) return;
     const u32 prime = t <= A.level ? t : A.nq + (t - A.level - 1);
-    const PrimeConst pc = A.pc[prime];
+    const u32 jown = (A.c1[c] && t <= A.level) ? t / A.alpha : 0xffffffffu;
     u32 s0 = (u32)x0, s1 = (u32)x0 + 1;
     if (A.galois != 1) {
         s0 = automorph_src((u32)x0, A.log_n, A.galois);
         s1 = automorph_src((u32)x0 + 1, A.log_n, A.galois);
     }
-    constexpr int MAXD = 4;
-    ulonglong2 kb[MAXD], ka[MAXD];
-    u64 d0[MAXD], d1[MAXD];
+    ulonglong2 kb[BETA], ka[BETA];
+    u64 d0[BETA], d1[BETA];
 #pragma unroll
-    for (int j = 0; j < MAXD; j++) {
-        if (j < (int)A.beta) {
-            kb[j] = *reinterpret_cast<const ulonglong2 *>(A.evk + (((size_t)j * 2 + 0) * A.nk + prime) * N + x0);
-            ka[j] = *reinterpret_cast<const ulonglong2 *>(A.evk + (((size_t)j * 2 + 1) * A.nk + prime) * N + x0);
-            const bool own = A.c1[c] && t <= A.level && t / A.alpha == (u32)j;
-            const u64 *D = own ? A.c1[c] + (size_t)t * N : A.ext[c] + ((size_t)j * A.ne + t) * N;
-            d0[j] = D[s0];
-            d1[j] = D[s1];
-        }
+    for (int j = 0; j < BETA; j++) {
+        kb[j] = *reinterpret_cast<const ulonglong2 *>(A.evk + (((size_t)j * 2 + 0) * A.nk + prime) * N + x0);
+        ka[j] = *reinterpret_cast<const ulonglong2 *>(A.evk + (((size_t)j * 2 + 1) * A.nk + prime) * N + x0);
+        const u64 *D = (u32)j == jown ? A.c1[c] + (size_t)t * N : A.ext[c] + ((size_t)j * A.ne + t) * N;
+        d0[j] = D[s0];
+        d1[j] = D[s1];
     }
-    Acc30 a0[2], a1[2];
-    acc_zero(a0[0]); acc_zero(a0[1]); acc_zero(a1[0]); acc_zero(a1[1]);
+    AccK a0[2], a1[2];
 #pragma unroll
-    for (int j = 0; j < MAXD; j++) {
-        if (j >= (int)A.beta) break;
+    for (int j = 0; j < BETA; j++) {
         u32 dl, dh, ml, mh;
+#define KP(J, DV, KW, ACC)                                                                        \
+        {                                                                                         \
+            split30(KW, ml, mh);                                                                  \
+            acck_mac<J>(ACC, dl, dh, ds, ml, mh, ml + mh);                                        \
+        }
         split30(d0[j], dl, dh);
-        split30(kb[j].x, ml, mh); acc_mac(a0[0], dl, dh, ml, mh);
-        split30(ka[j].x, ml, mh); acc_mac(a1[0], dl, dh, ml, mh);
+        u32 ds = dl + dh;
+        if (j == 0) { KP(0, d0, kb[0].x, a0[0]) KP(0, d0, ka[0].x, a1[0]) }
+        if (j == 1) { KP(1, d0, kb[1].x, a0[0]) KP(1, d0, ka[1].x, a1[0]) }
+        if (j == 2) { KP(2, d0, kb[2].x, a0[0]) KP(2, d0, ka[2].x, a1[0]) }
+        if (j == 3) { KP(3, d0, kb[3].x, a0[0]) KP(3, d0, ka[3].x, a1[0]) }
         split30(d1[j], dl, dh);
-        split30(kb[j].y, ml, mh); acc_mac(a0[1], dl, dh, ml, mh);
-        split30(ka[j].y, ml, mh); acc_mac(a1[1], dl, dh, ml, mh);
+        ds = dl + dh;
+        if (j == 0) { KP(0, d1, kb[0].y, a0[1]) KP(0, d1, ka[0].y, a1[1]) }
+        if (j == 1) { KP(1, d1, kb[1].y, a0[1]) KP(1, d1, ka[1].y, a1[1]) }
+        if (j == 2) { KP(2, d1, kb[2].y, a0[1]) KP(2, d1, ka[2].y, a1[1]) }
+        if (j == 3) { KP(3, d1, kb[3].y, a0[1]) KP(3, d1, ka[3].y, a1[1]) }
+#undef KP
     }
+    const PrimeConst pc = A.pc[prime];
+    u64 lo, hi;
     ulonglong2 o0, o1;
-    o0.x = acc_reduce(a0[0], pc);
-    o0.y = acc_reduce(a0[1], pc);
-    o1.x = acc_reduce(a1[0], pc);
-    o1.y = acc_reduce(a1[1], pc);
+    acck_to128(a0[0], BETA, lo, hi); o0.x = reduce128(lo, hi, pc);
+    acck_to128(a0[1], BETA, lo, hi); o0.y = reduce128(lo, hi, pc);
+    acck_to128(a1[0], BETA, lo, hi); o1.x = reduce128(lo, hi, pc);
+    acck_to128(a1[1], BETA, lo, hi); o1.y = reduce128(lo, hi, pc);
     *reinterpret_cast<ulonglong2 *>(A.acc[c] + (size_t)t * N + x0) = o0;
     *reinterpret_cast<ulonglong2 *>(A.acc[c] + ((size_t)A.ne + t) * N + x0) = o1;
 }
@@ -962,7 +972,12 @@ hks_status launch_kip_multi(const KipMultiArgs &a, cudaStream_t s) {
     const size_t N = (size_t)1 << a.log_n;
     dim3 grid((u32)((N / 2 + threads - 1) / threads) * a.nct, a.ne);
     ProfScope ps(K_KIP, s);
-    (void)hks_launch(k_kip_multi, grid, dim3(threads), 0, s, a);
+    switch (a.beta) {
+        case 1: (void)hks_launch(k_kip_multi<1>, grid, dim3(threads), 0, s, a); break;
+        case 2: (void)hks_launch(k_kip_multi<2>, grid, dim3(threads), 0, s, a); break;
+        case 3: (void)hks_launch(k_kip_multi<3>, grid, dim3(threads), 0, s, a); break;
+        default: (void)hks_launch(k_kip_multi<4>, grid, dim3(threads), 0, s, a); break;
+    }
     HKS_CHECK_LAUNCH();
     ps.done((2.0 * a.beta + a.nct * (a.beta + 2.0)) * a.ne * (double)N * 8.0,
             (double)a.nct * a.ne * a.beta * 2.0 * (double)N * 4.0);
