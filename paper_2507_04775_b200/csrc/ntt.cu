@@ -764,6 +764,35 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
                 dv[i].y = canon8(smj[1], m);
             }
         }
+#if HKS_KIP_KARA
+        // Karatsuba products (3 IMAD.WIDE each): D split once per term, shared by the two key words
+        AccK a0[2], a1[2];
+#pragma unroll
+        for (int i = 0; i < NDIG; i++) {
+            u32 dl, dh, ml, mh;
+#define KKP(I)                                                                                    \
+            if (i == I) {                                                                         \
+                split30(dv[I].x, dl, dh);                                                         \
+                u32 ds = dl + dh;                                                                 \
+                split30(kb[I].x, ml, mh); acck_mac<I>(a0[0], dl, dh, ds, ml, mh, ml + mh);        \
+                split30(ka[I].x, ml, mh); acck_mac<I>(a1[0], dl, dh, ds, ml, mh, ml + mh);        \
+                split30(dv[I].y, dl, dh);                                                         \
+                ds = dl + dh;                                                                     \
+                split30(kb[I].y, ml, mh); acck_mac<I>(a0[1], dl, dh, ds, ml, mh, ml + mh);        \
+                split30(ka[I].y, ml, mh); acck_mac<I>(a1[1], dl, dh, ds, ml, mh, ml + mh);        \
+            }
+            KKP(0) KKP(1) KKP(2) KKP(3)
+#undef KKP
+        }
+        ulonglong2 o0, o1;
+        {
+            u64 lo, hi;
+            acck_to128(a0[0], NDIG, lo, hi); o0.x = reduce128(lo, hi, pc);
+            acck_to128(a0[1], NDIG, lo, hi); o0.y = reduce128(lo, hi, pc);
+            acck_to128(a1[0], NDIG, lo, hi); o1.x = reduce128(lo, hi, pc);
+            acck_to128(a1[1], NDIG, lo, hi); o1.y = reduce128(lo, hi, pc);
+        }
+#else
         Acc30 a0[2], a1[2];
 #pragma unroll
         for (int i = 0; i < NDIG; i++) {
@@ -784,6 +813,7 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
         o0.y = acc_reduce(a0[1], pc);
         o1.x = acc_reduce(a1[0], pc);
         o1.y = acc_reduce(a1[1], pc);
+#endif
         if (ymode) {
             // each thread overwrites only the positions it read its D values from: no race
             u64 *s0 = sm + r * ROWPAD + k + (k >> LOGE);
@@ -914,6 +944,9 @@ static hks_status go_kip_d(FusedKipArgs &a, cudaStream_t s) {
     HKS_FAIL(HKS_EINVAL, "ntt_kip: %u transformed of %u digits", a.ntr, a.ndig);
 }
 
+#ifndef HKS_KIP_KARA
+#define HKS_KIP_KARA 1    // Karatsuba products in the key inner product of the fused row pass
+#endif
 #ifndef HKS_KIP_LOGE
 #define HKS_KIP_LOGE 4    // radix-2^LOGE rounds of the fused row pass at log N = 16
 #endif
