@@ -841,7 +841,8 @@ hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
 //   acc0[t] = sum_j D_j[t] * b_j[t],  acc1[t] = sum_j D_j[t] * a_j[t]   (mod t)
 // with D_j optionally read through the EVAL automorphism (hoisted rotation, reading 14).
 // grid.x: coefficient blocks, grid.y: extended limb t.
-__global__ void __launch_bounds__(256) k_kip(const __grid_constant__ KipArgs A) {
+// any digit count (runtime loop, 30-bit-split MACs: up to 16 digits)
+__global__ void __launch_bounds__(256) k_kip_any(const __grid_constant__ KipArgs A) {
     pdl_trigger();
     pdl_wait();
     const size_t N = (size_t)1 << A.log_n;
@@ -889,12 +890,79 @@ __global__ void __launch_bounds__(256) k_kip(const __grid_constant__ KipArgs A) 
     *reinterpret_cast<ulonglong2 *>(A.acc + ((size_t)A.ne + t) * N + x0) = o1;
 }
 
+template <int BETA>
+__global__ void __launch_bounds__(256) k_kip(const __grid_constant__ KipArgs A) {
+    pdl_trigger();
+    pdl_wait();
+    const size_t N = (size_t)1 << A.log_n;
+    const u32 t = blockIdx.y;
+    const size_t x0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    if (x0 >= N) return;
+    const u32 prime = t <= A.level ? t : A.nq + (t - A.level - 1);   // key limb index == prime index
+    const u32 jown = (A.c1 && t <= A.level) ? t / A.alpha : 0xffffffffu;
+    u32 s0 = 0, s1 = 1;
+    if (A.galois != 1) {
+        s0 = automorph_src((u32)x0, A.log_n, A.galois);
+        s1 = automorph_src((u32)x0 + 1, A.log_n, A.galois);
+    }
+    ulonglong2 kb[BETA], ka[BETA];
+    u64 d0[BETA], d1[BETA];
+#pragma unroll
+    for (int j = 0; j < BETA; j++) {
+        const u64 *D = (u32)j == jown ? A.c1 + (size_t)t * N : A.ext + ((size_t)j * A.ne + t) * N;
+        if (A.galois == 1) {
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(D + x0);
+            d0[j] = v.x;
+            d1[j] = v.y;
+        } else {
+            d0[j] = D[s0];
+            d1[j] = D[s1];
+        }
+        kb[j] = *reinterpret_cast<const ulonglong2 *>(A.evk + (((size_t)j * 2 + 0) * A.nk + prime) * N + x0);
+        ka[j] = *reinterpret_cast<const ulonglong2 *>(A.evk + (((size_t)j * 2 + 1) * A.nk + prime) * N + x0);
+    }
+    // Karatsuba products (3 IMAD.WIDE each); D split once per term, shared by the two key words
+    AccK a0[2], a1[2];
+#pragma unroll
+    for (int j = 0; j < BETA; j++) {
+        u32 dl, dh, ml, mh;
+#define KKP(J)                                                                                    \
+        if (j == J) {                                                                             \
+            split30(d0[J], dl, dh);                                                               \
+            u32 ds = dl + dh;                                                                     \
+            split30(kb[J].x, ml, mh); acck_mac<J>(a0[0], dl, dh, ds, ml, mh, ml + mh);            \
+            split30(ka[J].x, ml, mh); acck_mac<J>(a1[0], dl, dh, ds, ml, mh, ml + mh);            \
+            split30(d1[J], dl, dh);                                                               \
+            ds = dl + dh;                                                                         \
+            split30(kb[J].y, ml, mh); acck_mac<J>(a0[1], dl, dh, ds, ml, mh, ml + mh);            \
+            split30(ka[J].y, ml, mh); acck_mac<J>(a1[1], dl, dh, ds, ml, mh, ml + mh);            \
+        }
+        KKP(0) KKP(1) KKP(2) KKP(3)
+#undef KKP
+    }
+    const PrimeConst pc = A.pc[prime];
+    u64 lo, hi;
+    ulonglong2 o0, o1;
+    acck_to128(a0[0], BETA, lo, hi); o0.x = reduce128(lo, hi, pc);
+    acck_to128(a0[1], BETA, lo, hi); o0.y = reduce128(lo, hi, pc);
+    acck_to128(a1[0], BETA, lo, hi); o1.x = reduce128(lo, hi, pc);
+    acck_to128(a1[1], BETA, lo, hi); o1.y = reduce128(lo, hi, pc);
+    *reinterpret_cast<ulonglong2 *>(A.acc + (size_t)t * N + x0) = o0;
+    *reinterpret_cast<ulonglong2 *>(A.acc + ((size_t)A.ne + t) * N + x0) = o1;
+}
+
 hks_status launch_kip(const KipArgs &a, cudaStream_t s) {
     const u32 threads = 256;
     const size_t N = (size_t)1 << a.log_n;
     dim3 grid((u32)((N / 2 + threads - 1) / threads), a.ne);
     ProfScope ps(K_KIP, s);
-    (void)hks_launch(k_kip, grid, dim3(threads), 0, s, a);
+    switch (a.beta) {
+        case 1: (void)hks_launch(k_kip<1>, grid, dim3(threads), 0, s, a); break;
+        case 2: (void)hks_launch(k_kip<2>, grid, dim3(threads), 0, s, a); break;
+        case 3: (void)hks_launch(k_kip<3>, grid, dim3(threads), 0, s, a); break;
+        case 4: (void)hks_launch(k_kip<4>, grid, dim3(threads), 0, s, a); break;
+        default: (void)hks_launch(k_kip_any, grid, dim3(threads), 0, s, a); break;
+    }
     HKS_CHECK_LAUNCH();
     ps.done((3.0 * a.beta + 2.0) * a.ne * (double)N * 8.0,    // D_j + (b_j, a_j) read, acc0/acc1 written
             (double)a.ne * a.beta * 2.0 * (double)N * 4.0);
