@@ -346,7 +346,7 @@ hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, const std::vec
 hks_status run_rescale(const hks_ctx *ctx, u32 npoly, u32 level, const u64 *x, const u64 *coef, u64 *buf,
                        u64 *const *outs, cudaStream_t s);
 hks_status launch_bconv(const BconvArgs &a, u32 max_ndst, cudaStream_t s);
-// column pass of the log N = 16 NTT on the tensor cores (kernels.cu k_ntt16_tc): forward EPI_LAZY or
+// column pass of the log N = 16 NTT on the tensor cores (ntt_tc.cu k_ntt_cols_tc): forward EPI_LAZY or
 // inverse EPI_SCALE, same limb map / scale semantics as launch_ntt_pass
 hks_status launch_ntt_cols_tc(const hks_ctx *ctx, NttDir dir, int epi, const NttArgs &a, cudaStream_t s);
 bool ntt_tc_enabled();
