@@ -97,7 +97,10 @@ def test_ntt_large_batch(orc):
                                           ("T12", [5], [0, 1, 9]),
                                           ("C4", list(range(36, 45)), list(range(36))),
                                           ("C4", [7], list(range(7)) + list(range(8, 45))),
-                                          ("C1", [0, 1, 2], [3])])
+                                          ("C1", [0, 1, 2], [3]),
+                                          ("C2", list(range(10)), list(range(10, 39))),
+                                          ("C2", [3, 17, 25], [0, 1, 2, 39, 38, 37, 10]),
+                                          ("C4", list(range(16)), list(range(16, 45)))])
 def test_bconv_parity(orc, name, src, dst):
     cfg, ctx, o = ctxs(orc, name)
     g = S.rng(420)
@@ -198,7 +201,7 @@ def test_keyswitch_parity_small(orc, name, levels):
         assert err <= ks_bound(o, level, keys.B_e, keys.h)
 
 
-@pytest.mark.parametrize("level", [29, 20, 19, 9, 0])
+@pytest.mark.parametrize("level", [29, 27, 20, 19, 11, 9, 0])
 def test_keyswitch_parity_c2(orc, level):
     """BASELINE.json configs[1]: N=2^16, L=29, dnum=3, 60-bit primes; level sweep across digit drops."""
     cfg, ctx, o = ctxs(orc, "C2")
