@@ -211,7 +211,7 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     cudaGetDevice(&prev);
     if (cudaSetDevice(device) != cudaSuccess) { delete c; HKS_FAIL(HKS_EDEVICE, "ctx_create: cudaSetDevice(%d) failed", device); }
 
-    const u32 R = 1u << c->log_r, C = 1u << c->log_c, L = num_q - 1;
+    const u32 R = 1u << c->log_r, L = num_q - 1;
     std::vector<PrimeConst> pc(nm);
     std::vector<ulonglong2> ninv(nm);
     for (u32 i = 0; i < nm; i++) {
