@@ -369,7 +369,7 @@ static void bconv_mma_go(const BconvArgs &a, cudaStream_t s) {
 //   next 4 warps producers: cp.async of the next tiles' input words into TC_SA shared stages; their
 //              first thread issues the tcgen05.mma of a tile (K / 32 instructions) and commits.
 #ifndef HKS_TC_SA
-#define HKS_TC_SA 4
+#define HKS_TC_SA 2
 #endif
 #ifndef HKS_TC_EPW
 #define HKS_TC_EPW 16
