@@ -32,16 +32,17 @@ struct NttColsArgs {
     LimbMap map;
 };
 
-// Shared memory (dynamic, 1024-aligned): [0, 64K) vector operands -- round 1: M-tile mt (classes
-// 4mt..4mt+3 x 32 columns) at mt * 16K, K-major, SBO 1024; round 2: two K halves (elements 0-7 / 8-15)
-// at 0 / 32K, M-tile mt2 at mt2 * 8K, SBO 512 -- [64K, 80K) round-1 image, [80K, 96K) round-2 image,
-// [96K, 100K) twist.
+// Shared memory (dynamic, 1024-aligned): two 32 KB tile buffers (the next tile is loaded into one while
+// the current one is processed in the other), [64K, 80K) round-1 image, [80K, 96K) round-2 image,
+// [96K, 100K) twist.  A tile = (limb, 16 columns): 256 vectors per round = two 128-row M-tiles, K-major,
+// SBO 1024.  Round 1: vector V = (class V / 16, column V % 16); its outputs are twisted into round 2's
+// operands in place of the consumed round-1 operands (round-2 vector v2 = output index, element =
+// round-1 class).  CTAs take contiguous tile ranges so a CTA rarely changes prime (tables reloaded then).
 template <bool FWD>
 __global__ void __launch_bounds__(NC_THREADS, 2) k_ntt_cols_tc(const __grid_constant__ NttColsArgs A) {
     pdl_trigger();
     constexpr u32 N = 1u << 16;
     extern __shared__ __align__(1024) uint8_t csm[];
-    uint8_t *sv = csm;
     uint8_t *simg1 = csm + 65536, *simg2 = csm + 81920;
     const ulonglong2 *stw = reinterpret_cast<const ulonglong2 *>(csm + 98304);
     __shared__ __align__(8) u64 mbar;
@@ -62,62 +63,66 @@ __global__ void __launch_bounds__(NC_THREADS, 2) k_ntt_cols_tc(const __grid_cons
     pdl_wait();
 
     const u32 idesc = (2u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);   // M = N = 128, s32 += u8 x u8
-    const u32 sv_a = smem_u32(sv), img1_a = smem_u32(simg1), img2_a = smem_u32(simg2);
-    u32 phase = 0;
-    u32 cur_prime = 0xffffffffu;
+    const u32 buf_a = smem_u32(csm), img1_a = smem_u32(simg1), img2_a = smem_u32(simg2);
+    u32 phase = 0, cur_prime = 0xffffffffu;
     // round-1 / round-2 row of element k of vector class v:  strided v + 16k, blocked 16v + k
     auto row1 = [](u32 v, u32 k) { return FWD ? v + 16 * k : 16 * v + k; };
     auto row2 = [](u32 v, u32 k) { return FWD ? 16 * v + k : v + 16 * k; };
-
-    const u32 ntile = A.nlimbs * 8;
-    for (u32 tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
-        const u32 b = tile >> 3, c0 = (tile & 7) * 32;
-        const u32 prime = A.map.prime[b];
+    const u32 ntile = A.nlimbs * 16;
+    const u32 per = (ntile + gridDim.x - 1) / gridDim.x;
+    const u32 t_beg = blockIdx.x * per, t_end = min(ntile, t_beg + per);
+    // this thread's two round-1 vectors: V = tid, tid + 256 ... (256 vectors: M-tile V >> 7)
+    auto load_tile = [&](u32 tile, u32 buf) {
+        const u32 b = tile >> 4, c0 = (tile & 15) * 16;
         const u64 *src = A.in + (size_t)A.map.sin[b] * N + c0;
-        u64 *dst = A.out + (size_t)A.map.sout[b] * N + c0;
-        // ---- load: the tile's 8192 words into the round-1 operand layout (+ the prime's tables)
+        const u32 V = tid, mt = V >> 7, m = V & 127, cls = V >> 4, c = V & 15;
+        const u32 base = buf_a + buf * 32768 + mt * 16384 + (m >> 3) * 1024 + (m & 7) * 16;
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const u32 V = tid + 256 * h;                  // vector: class V / 32, column V % 32
-            const u32 mt = V >> 7, m = V & 127, cls = V >> 5, c = V & 31;
-            const u32 base = sv_a + mt * 16384 + (m >> 3) * 1024 + (m & 7) * 16;
-#pragma unroll
-            for (int k = 0; k < 16; k++) cp_async8(base + (k >> 1) * 128 + (k & 1) * 8, src + (size_t)row1(cls, k) * 256 + c);
-        }
-        if (prime != cur_prime) {
+        for (int k = 0; k < 16; k++) cp_async8(base + (k >> 1) * 128 + (k & 1) * 8, src + (size_t)row1(cls, k) * 256 + c);
+    };
+    if (t_beg < t_end) load_tile(t_beg, 0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (u32 tile = t_beg, it = 0; tile < t_end; tile++, it++) {
+        const u32 buf = it & 1;
+        const u32 b = tile >> 4, c0 = (tile & 15) * 16;
+        const u32 prime = A.map.prime[b];
+        if (prime != cur_prime) {   // tables of this prime (rare: contiguous tile ranges)
+            __syncthreads();
             const uint8_t *t = reinterpret_cast<const uint8_t *>(A.tab + (size_t)prime * NTT16_TAB);
             for (u32 o = tid * 16; o < 36864; o += NC_THREADS * 16)
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(img1_a + o), "l"(t + o) : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
             cur_prime = prime;
         }
-        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+        if (tile + 1 < t_end) load_tile(tile + 1, buf ^ 1);   // next tile in flight during this one
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 1;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
 
         const PrimeConst pc = A.pc[prime];
         const u64 np = 0 - pc.p;
         const u32 mu = (u32)pc.mu80;
-        const u32 q = warp & 3, mtl = warp >> 2;          // TMEM lane quarter, M-tile of the pair
-        // ---- round 1: two M-tile pairs; outputs twisted into round 2's operand layout
-        for (u32 pr = 0; pr < 2; pr++) {
-            if (tid == 0) {
-                tc_fence_after();
-#pragma unroll
-                for (int t = 0; t < 2; t++)
-#pragma unroll
-                    for (int s = 0; s < 4; s++)
-                        tc_mma_i8(tmem + t * 128, tc_desc(sv_a + (2 * pr + t) * 16384 + s * 256, 128, 1024),
-                                  tc_desc(img1_a + s * 256, 128, 1024), idesc, s > 0 ? 1u : 0u);
-                tc_commit(smem_u32(&mbar));
-            }
-            mbar_wait(smem_u32(&mbar), phase);
-            phase ^= 1;
+        const u32 q = warp & 3, mtl = warp >> 2;          // TMEM lane quarter, M-tile
+        const u32 sv_a = buf_a + buf * 32768;
+        const u32 tb = tmem + mtl * 128 + ((q * 32) << 16);
+        // ---- round 1
+        if (tid == 0) {
             tc_fence_after();
-            const u32 v1 = 4 * (2 * pr + mtl) + q, c = lane;   // this thread's round-1 vector
-            const u32 tb = tmem + mtl * 128 + ((q * 32) << 16);
-            // round-2 operand: vector v2 = o (M-tile o / 4, row (o % 4) 32 + c), element v1
-            const u32 half = v1 >> 3, kk = v1 & 7;
-            const u32 w2 = sv_a + half * 32768 + (c >> 3) * 512 + (kk >> 1) * 128 + (c & 7) * 16 + (kk & 1) * 8;
+#pragma unroll
+            for (int t = 0; t < 2; t++)
+#pragma unroll
+                for (int s = 0; s < 4; s++)
+                    tc_mma_i8(tmem + t * 128, tc_desc(sv_a + t * 16384 + s * 256, 128, 1024),
+                              tc_desc(img1_a + s * 256, 128, 1024), idesc, s > 0 ? 1u : 0u);
+            tc_commit(smem_u32(&mbar));
+        }
+        mbar_wait(smem_u32(&mbar), phase);
+        phase ^= 1;
+        tc_fence_after();
+        {
+            const u32 m = 32 * q + lane, v1 = 8 * mtl + (m >> 4), c = m & 15;   // this thread's round-1 vector
+            // round-2 operand: vector o (M-tile o / 8, row (o % 8) 16 + c), element v1
+            const u32 w2 = sv_a + ((c & 8) ? 1024 : 0) + (v1 >> 1) * 128 + (c & 7) * 16 + (v1 & 1) * 8;
 #pragma unroll
             for (u32 o0 = 0; o0 < 16; o0 += 4) {
                 u32 v[4][8];
@@ -130,34 +135,33 @@ __global__ void __launch_bounds__(NC_THREADS, 2) k_ntt_cols_tc(const __grid_cons
                     const u64 r = bytesum_reduce_c<true>(v[k], np, mu);   // [0, 3p)
                     const ulonglong2 tw = stw[v1 * 16 + o];
                     const u64 y = shoup_approx(r, tw.x, tw.y, np);        // [0, 4p)
-                    const u32 a = w2 + (o >> 2) * 8192 + (o & 3) * 2048;
+                    const u32 a = w2 + (o >> 3) * 16384 + (o & 7) * 2048;
                     asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(y) : "memory");
                 }
             }
-            tc_fence_before();
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncthreads();
         }
-        // ---- round 2: two M-tile pairs; outputs to global
-        ulonglong2 sc = make_ulonglong2(0, 0);
-        if (!FWD) sc = A.scale ? A.scale[b % A.scale_mod] : A.ninv[prime];
-        for (u32 pr = 0; pr < 2; pr++) {
-            if (tid == 0) {
-                tc_fence_after();
-#pragma unroll
-                for (int t = 0; t < 2; t++)
-#pragma unroll
-                    for (int s = 0; s < 4; s++)
-                        tc_mma_i8(tmem + t * 128,
-                                  tc_desc(sv_a + (s >> 1) * 32768 + (2 * pr + t) * 8192 + (s & 1) * 256, 128, 512),
-                                  tc_desc(img2_a + s * 256, 128, 1024), idesc, s > 0 ? 1u : 0u);
-                tc_commit(smem_u32(&mbar));
-            }
-            mbar_wait(smem_u32(&mbar), phase);
-            phase ^= 1;
+        tc_fence_before();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        // ---- round 2
+        if (tid == 0) {
             tc_fence_after();
-            const u32 v2 = 4 * (2 * pr + mtl) + q, c = lane;
-            const u32 tb = tmem + mtl * 128 + ((q * 32) << 16);
+#pragma unroll
+            for (int t = 0; t < 2; t++)
+#pragma unroll
+                for (int s = 0; s < 4; s++)
+                    tc_mma_i8(tmem + t * 128, tc_desc(sv_a + t * 16384 + s * 256, 128, 1024),
+                              tc_desc(img2_a + s * 256, 128, 1024), idesc, s > 0 ? 1u : 0u);
+            tc_commit(smem_u32(&mbar));
+        }
+        mbar_wait(smem_u32(&mbar), phase);
+        phase ^= 1;
+        tc_fence_after();
+        {
+            ulonglong2 sc = make_ulonglong2(0, 0);
+            if (!FWD) sc = A.scale ? A.scale[b % A.scale_mod] : A.ninv[prime];
+            const u32 m = 32 * q + lane, v2 = 8 * mtl + (m >> 4), c = m & 15;
+            u64 *dst = A.out + (size_t)A.map.sout[b] * N + c0 + c;
 #pragma unroll
             for (u32 o0 = 0; o0 < 16; o0 += 4) {
                 u32 v[4][8];
@@ -169,13 +173,14 @@ __global__ void __launch_bounds__(NC_THREADS, 2) k_ntt_cols_tc(const __grid_cons
                     const u32 o = o0 + k;
                     u64 r = bytesum_reduce_c<true>(v[k], np, mu);
                     if (!FWD) r = csub(csub(shoup_approx(r, sc.x, sc.y, np), 2 * pc.p), pc.p);
-                    dst[(size_t)row2(v2, o) * 256 + c] = r;
+                    dst[(size_t)row2(v2, o) * 256] = r;
                 }
             }
-            tc_fence_before();
-            __syncthreads();
         }
+        tc_fence_before();
+        __syncthreads();
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {
@@ -204,7 +209,7 @@ hks_status launch_ntt_cols_tc(const hks_ctx *ctx, NttDir dir, int /*epi*/, const
     a.nlimbs = na.nlimbs;
     a.scale_mod = na.scale_mod ? na.scale_mod : 1;
     a.map = na.map;
-    const u32 grid = std::min<u32>(a.nlimbs * 8, 2 * (u32)nsm);
+    const u32 grid = std::min<u32>(a.nlimbs * 16, 2 * (u32)nsm);
     ProfScope ps(dir == NTT_FWD ? K_NTT_FWD_COLS : K_NTT_INV_COLS, s);
     const cudaError_t e = dir == NTT_FWD
                               ? hks_launch(k_ntt_cols_tc<true>, dim3(grid), dim3(NC_THREADS), smem, s, a)
