@@ -493,7 +493,7 @@ static hks_status keyswitch_impl(const hks_ctx *c, const uint64_t *c0, const uin
     const u64 *kin = tensor ? d2 : c1;
     const u64 *tb = tensor ? tensor[3] : nullptr;
     const bool fused = beta <= FK_MAXD;
-    const bool ymode = fused && beta >= 2 && 2 * c->np <= HKS_MAXB;
+    const bool ymode = fused && 2 * c->np <= HKS_MAXB;   // beta = 1: the launch gets a second thread group
     if (fused) {
         // INTT + BConv + NTT column pass, then the fused NTT row pass + key inner product (+ for the P
         // limbs, ModDown's inverse row pass straight into the ModDown workspace)

@@ -938,7 +938,7 @@ static hks_status go_kip(FusedKipArgs &a, cudaStream_t s) {
 template <int LOGN, int LOGE, int LOGNB>
 static hks_status go_kip_d(FusedKipArgs &a, cudaStream_t s) {
 #define KC(T, D) if (a.ntr == T && a.ndig == D) return go_kip<LOGN, LOGE, LOGNB, T, D>(a, s);
-    KC(1, 1) KC(1, 2) KC(2, 2) KC(2, 3) KC(3, 3) KC(3, 4) KC(4, 4)
+    KC(1, 1) KC(2, 1) KC(1, 2) KC(2, 2) KC(2, 3) KC(3, 3) KC(3, 4) KC(4, 4)
 #undef KC
     if (a.ntr == 0) { a.ntr = 1; return go_kip_d<LOGN, LOGE, LOGNB>(a, s); }   // all-direct launch
     HKS_FAIL(HKS_EINVAL, "ntt_kip: %u transformed of %u digits", a.ntr, a.ndig);
@@ -957,7 +957,7 @@ hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s) {
     a.log_n = ctx->log_n;
     a.log_r = ctx->log_r;
     a.log_c = ctx->log_c;
-    if (a.ndig > FK_MAXD || a.nu > FK_MAXU || a.ntr > a.ndig)
+    if (a.ndig > FK_MAXD || a.nu > FK_MAXU || a.ntr > (a.ndig > 2 ? a.ndig : 2))
         HKS_FAIL(HKS_EINVAL, "ntt_kip: %u digits (%u transformed) / %u limbs per launch", a.ndig, a.ntr, a.nu);
     switch (ctx->log_n) {
         case 17: return go_kip_d<8, 4, HKS_KIP_LOGNB>(a, s);
@@ -1021,6 +1021,10 @@ hks_status run_ntt_kip(const hks_ctx *ctx, const std::vector<KipItem> &items_in,
             a.map.ntr[uu] = (u8)ntr;
             a.ntr = std::max(a.ntr, ntr);
         }
+        // ModDown's inverse row pass (y mode) needs two thread groups, one per accumulator
+        bool anyy = false;
+        for (u32 uu = 0; uu < a.nu; uu++) anyy |= a.map.yslot[uu] != 0xffff;
+        if (anyy && a.ntr < 2) a.ntr = 2;
         hks_status st = launch_ntt_kip(ctx, a, s);
         if (st != HKS_OK) return st;
     }
