@@ -972,7 +972,7 @@ hks_status launch_kip(const KipArgs &a, cudaStream_t s) {
 // Multi-ciphertext key inner product: the nct ciphertexts of a batch share one key, whose words are read
 // from HBM once per batch (amortising the dominant key stream, SURVEY.md §7 "key streaming").
 template <int BETA>
-__global__ void __launch_bounds__(256) k_kip_multi(const __grid_constant__ KipMultiArgs A) {
+__global__ void __launch_bounds__(512) k_kip_multi(const __grid_constant__ KipMultiArgs A) {
     // one (ciphertext, coefficient block) per CTA; the nct CTAs sharing a key block are adjacent in
     // launch order (ciphertext fastest), so the key words come from HBM once and from L2 for the others.
     // Karatsuba products (3 IMAD.WIDE each), the digit count a template parameter (straight-line code).
@@ -1036,7 +1036,10 @@ __global__ void __launch_bounds__(256) k_kip_multi(const __grid_constant__ KipMu
 
 hks_status launch_kip_multi(const KipMultiArgs &a, cudaStream_t s) {
     if (a.beta > 4 || a.nct > KIP_MAXCT) HKS_FAIL(HKS_EINVAL, "kip_multi: beta %u / nct %u", a.beta, a.nct);
-    const u32 threads = 256;
+#ifndef HKS_KIPM_THREADS
+#define HKS_KIPM_THREADS 128   // measured: C3 7 649 (256) -> 7 720 rot-KS/s
+#endif
+    const u32 threads = HKS_KIPM_THREADS;
     const size_t N = (size_t)1 << a.log_n;
     dim3 grid((u32)((N / 2 + threads - 1) / threads) * a.nct, a.ne);
     ProfScope ps(K_KIP, s);
