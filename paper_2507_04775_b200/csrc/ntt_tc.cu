@@ -19,7 +19,12 @@
 #include "internal.h"
 #include "tc.cuh"
 
-#define NC_THREADS 256
+#ifndef HKS_NTC_SPLIT
+#define HKS_NTC_SPLIT 1   // warps per TMEM lane quarter and M-tile (each takes 16 / SPLIT of the outputs)
+#endif
+#define NC_THREADS (256 * HKS_NTC_SPLIT)
+#define NC_OUT (16 / HKS_NTC_SPLIT)
+#define NC_ILP (NC_OUT < 4 ? NC_OUT : 4)
 
 struct NttColsArgs {
     const u64 *in;
@@ -65,20 +70,24 @@ __global__ void __launch_bounds__(NC_THREADS, 2) k_ntt_cols_tc(const __grid_cons
     const u32 idesc = (2u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);   // M = N = 128, s32 += u8 x u8
     const u32 buf_a = smem_u32(csm), img1_a = smem_u32(simg1), img2_a = smem_u32(simg2);
     u32 phase = 0, cur_prime = 0xffffffffu;
+    PrimeConst pc{};
     // round-1 / round-2 row of element k of vector class v:  strided v + 16k, blocked 16v + k
     auto row1 = [](u32 v, u32 k) { return FWD ? v + 16 * k : 16 * v + k; };
     auto row2 = [](u32 v, u32 k) { return FWD ? 16 * v + k : v + 16 * k; };
     const u32 ntile = A.nlimbs * 16;
-    const u32 per = (ntile + gridDim.x - 1) / gridDim.x;
-    const u32 t_beg = blockIdx.x * per, t_end = min(ntile, t_beg + per);
+    const u32 t_beg = (u32)((u64)blockIdx.x * ntile / gridDim.x);        // balanced contiguous ranges
+    const u32 t_end = (u32)((u64)(blockIdx.x + 1) * ntile / gridDim.x);
     // this thread's two round-1 vectors: V = tid, tid + 256 ... (256 vectors: M-tile V >> 7)
     auto load_tile = [&](u32 tile, u32 buf) {
         const u32 b = tile >> 4, c0 = (tile & 15) * 16;
         const u64 *src = A.in + (size_t)A.map.sin[b] * N + c0;
-        const u32 V = tid, mt = V >> 7, m = V & 127, cls = V >> 4, c = V & 15;
+        const u32 V = tid & 255, mt = V >> 7, m = V & 127, cls = V >> 4, c = V & 15;
         const u32 base = buf_a + buf * 32768 + mt * 16384 + (m >> 3) * 1024 + (m & 7) * 16;
 #pragma unroll
-        for (int k = 0; k < 16; k++) cp_async8(base + (k >> 1) * 128 + (k & 1) * 8, src + (size_t)row1(cls, k) * 256 + c);
+        for (int kk = 0; kk < NC_OUT; kk++) {
+            const int k = (tid >> 8) * NC_OUT + kk;
+            cp_async8(base + (k >> 1) * 128 + (k & 1) * 8, src + (size_t)row1(cls, k) * 256 + c);
+        }
     };
     if (t_beg < t_end) load_tile(t_beg, 0);
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -93,16 +102,16 @@ __global__ void __launch_bounds__(NC_THREADS, 2) k_ntt_cols_tc(const __grid_cons
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(img1_a + o), "l"(t + o) : "memory");
             asm volatile("cp.async.commit_group;" ::: "memory");
             cur_prime = prime;
+            pc = A.pc[prime];
         }
         if (tile + 1 < t_end) load_tile(tile + 1, buf ^ 1);   // next tile in flight during this one
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 1;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
 
-        const PrimeConst pc = A.pc[prime];
         const u64 np = 0 - pc.p;
         const u32 mu = (u32)pc.mu80;
-        const u32 q = warp & 3, mtl = warp >> 2;          // TMEM lane quarter, M-tile
+        const u32 q = warp & 3, mtl = (warp >> 2) & 1, ob = (warp >> 3) * NC_OUT;   // lane quarter, M-tile, outputs
         const u32 sv_a = buf_a + buf * 32768;
         const u32 tb = tmem + mtl * 128 + ((q * 32) << 16);
         // ---- round 1
@@ -124,13 +133,13 @@ __global__ void __launch_bounds__(NC_THREADS, 2) k_ntt_cols_tc(const __grid_cons
             // round-2 operand: vector o (M-tile o / 8, row (o % 8) 16 + c), element v1
             const u32 w2 = sv_a + ((c & 8) ? 1024 : 0) + (v1 >> 1) * 128 + (c & 7) * 16 + (v1 & 1) * 8;
 #pragma unroll
-            for (u32 o0 = 0; o0 < 16; o0 += 4) {
-                u32 v[4][8];
+            for (u32 o0 = ob; o0 < ob + NC_OUT; o0 += NC_ILP) {
+                u32 v[NC_ILP][8];
 #pragma unroll
-                for (int k = 0; k < 4; k++) tc_ld8(tb + (o0 + k) * 8, v[k]);
+                for (int k = 0; k < NC_ILP; k++) tc_ld8(tb + (o0 + k) * 8, v[k]);
                 tc_wait_ld();
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
+                for (int k = 0; k < NC_ILP; k++) {
                     const u32 o = o0 + k;
                     const u64 r = bytesum_reduce_c<true>(v[k], np, mu);   // [0, 3p)
                     const ulonglong2 tw = stw[v1 * 16 + o];
@@ -163,13 +172,13 @@ __global__ void __launch_bounds__(NC_THREADS, 2) k_ntt_cols_tc(const __grid_cons
             const u32 m = 32 * q + lane, v2 = 8 * mtl + (m >> 4), c = m & 15;
             u64 *dst = A.out + (size_t)A.map.sout[b] * N + c0 + c;
 #pragma unroll
-            for (u32 o0 = 0; o0 < 16; o0 += 4) {
-                u32 v[4][8];
+            for (u32 o0 = ob; o0 < ob + NC_OUT; o0 += NC_ILP) {
+                u32 v[NC_ILP][8];
 #pragma unroll
-                for (int k = 0; k < 4; k++) tc_ld8(tb + (o0 + k) * 8, v[k]);
+                for (int k = 0; k < NC_ILP; k++) tc_ld8(tb + (o0 + k) * 8, v[k]);
                 tc_wait_ld();
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
+                for (int k = 0; k < NC_ILP; k++) {
                     const u32 o = o0 + k;
                     u64 r = bytesum_reduce_c<true>(v[k], np, mu);
                     if (!FWD) r = csub(csub(shoup_approx(r, sc.x, sc.y, np), 2 * pc.p), pc.p);
