@@ -528,10 +528,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HKS_BENCH_BACKEND=gloo: several ranks sharing the visible GPUs (a check of the multi-rank logic --
+    # sharding, barriers, max over ranks, one line from rank 0 -- on a one-GPU box; never a bench number)
+    backend = os.environ.get("HKS_BENCH_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(dev))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(dev))
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
