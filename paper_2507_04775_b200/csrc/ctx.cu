@@ -10,6 +10,8 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <mutex>
+#include <set>
 #include <thread>
 
 #include "internal.h"
@@ -489,4 +491,26 @@ extern "C" hks_status hks_ctx_psi(const hks_ctx *c, uint32_t prime_idx, uint64_t
     if (prime_idx >= c->primes.size()) HKS_FAIL(HKS_EINVAL, "ctx_psi: prime index %u out of range", prime_idx);
     *psi = c->psi[prime_idx];
     return HKS_OK;
+}
+
+void hks_func_smem(const void *fn, size_t smem) {
+    static std::mutex mu;
+    static std::set<std::pair<int, const void *>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.insert({dev, fn}).second) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+int hks_num_sms() {
+    static int nsm[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!nsm[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        nsm[dev] = v > 0 ? v : 148;
+    }
+    return nsm[dev];
 }

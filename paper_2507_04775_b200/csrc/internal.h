@@ -280,6 +280,11 @@ struct ProfScope {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 bool pdl_enabled();
+// Per-(device, kernel) one-time setup, thread-safe: cudaFuncSetAttribute acts on the current device only,
+// so a process with contexts on several devices raises each kernel's dynamic shared-memory limit once per
+// device.  hks_num_sms: SM count of the current device (cached per device).
+void hks_func_smem(const void *fn, size_t smem);
+int hks_num_sms();
 template <typename... KArgs, typename... Args>
 inline cudaError_t hks_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args &&...args) {

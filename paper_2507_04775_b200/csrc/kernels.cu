@@ -331,12 +331,7 @@ static void bconv_mma_go(const BconvArgs &a, cudaStream_t s) {
     // one wave: every CTA stages its matrix fragments before griddepcontrol.wait, i.e. while the
     // predecessor is still running (MMA_SLOTS resident CTAs per SM); CW = coefficients per CTA
     const u32 nz = (maxdst + MMA_TCH - 1) / MMA_TCH;
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int nsm = hks_num_sms();
     size_t cw = MMA_CW;
     while (cw < N && (N / cw) * a.ngroups * nz > (size_t)nsm * HKS_MMA_MINB) cw *= 2;
     BconvArgs b = a;
@@ -535,14 +530,9 @@ template <int NSRC>
 static hks_status bconv_tc_go(const BconvArgs &a, cudaStream_t s) {
     constexpr int KPAD = 32 * ((NSRC + 3) / 4);
     const size_t smem = 256 * KPAD + TC_SA * 128 * KPAD;
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_bconv_tc<NSRC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_bconv_tc<NSRC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }
+    const int nsm = hks_num_sms();
+    hks_func_smem((const void *)k_bconv_tc<NSRC, true>, smem);
+    hks_func_smem((const void *)k_bconv_tc<NSRC, false>, smem);
     const size_t N = (size_t)1 << a.log_n;
     u32 maxdst = 0;
     for (u32 g = 0; g < a.ngroups; g++) maxdst = max(maxdst, a.g[g].ndst);
@@ -606,12 +596,7 @@ bool bconv_tc_enabled() { return getenv_mma_enabled() && getenv_tc_enabled(); }
 
 // enough 128-coefficient tiles to give every SM one (otherwise the tensor kernels' fixed prologue loses)
 bool bconv_tc_large(u32 log_n, u32 ngroups) {
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int nsm = hks_num_sms();
     return (((size_t)1 << log_n) >> 7) * ngroups >= (size_t)nsm;
 }
 

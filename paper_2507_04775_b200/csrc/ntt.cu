@@ -299,11 +299,7 @@ static hks_status go(NttArgs &a, cudaStream_t s) {
     constexpr size_t smem = (size_t)((1 << LOGN) + ((1 << LOGN) >> LOGE)) * (1 << LOGNB) * sizeof(u64);
     auto kern = k_ntt<LOGN, LOGE, LOGNB, LOGC, COLS, FWD, EPI>;
     if (smem > 48 * 1024) {
-        static bool once = [&] {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            return true;
-        }();
-        (void)once;
+        hks_func_smem((const void *)kern, smem);
     }
     a.tiles = COLS ? ((1u << a.log_c) >> LOGNB) : ((1u << a.log_r) >> LOGNB);
     const int cls = FWD ? (COLS ? K_NTT_FWD_COLS : ((EPI == EPI_MODDOWN || EPI == EPI_MDTENSOR) ? K_NTT_FWD_ROWS_MODDOWN : K_NTT_FWD_ROWS))
@@ -913,11 +909,7 @@ static hks_status go_kip(FusedKipArgs &a, cudaStream_t s) {
                             (HKS_KIP_TMA ? (size_t)2 * NDIG * (1 << LOGN) * (1 << LOGNB) * sizeof(u64) : 0);
     auto kern = k_ntt_kip<LOGN, LOGE, LOGNB, NTR, NDIG>;
     if (smem > 48 * 1024) {
-        static bool once = [&] {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            return true;
-        }();
-        (void)once;
+        hks_func_smem((const void *)kern, smem);
     }
     a.tiles = (1u << a.log_r) >> LOGNB;
     ProfScope ps(K_NTT_ROWS_KIP, s);

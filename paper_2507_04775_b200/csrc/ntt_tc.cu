@@ -200,14 +200,9 @@ __global__ void __launch_bounds__(NC_THREADS, 2) k_ntt_cols_tc(const __grid_cons
 
 hks_status launch_ntt_cols_tc(const hks_ctx *ctx, NttDir dir, int /*epi*/, const NttArgs &na, cudaStream_t s) {
     constexpr size_t smem = 98304 + 4096;
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_ntt_cols_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_ntt_cols_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }
+    const int nsm = hks_num_sms();
+    hks_func_smem((const void *)k_ntt_cols_tc<true>, smem);
+    hks_func_smem((const void *)k_ntt_cols_tc<false>, smem);
     NttColsArgs a;
     a.in = na.in;
     a.out = na.out;
