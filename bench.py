@@ -3,7 +3,9 @@
 
 Default workload (BASELINE.json configs[1], `C2`): one relinearisation KeySwitch of one ciphertext at
 N=2^16, L=29 (30 Q limbs), K=10 special primes, dnum=3, 60-bit primes, level 29.  A step = one
-KeySwitch (all of SURVEY.md §8(a): INTT, ModUp BConv, NTT, key inner product, ModDown).
+KeySwitch (all of SURVEY.md §8(a): INTT, ModUp BConv, NTT, key inner product, ModDown) per ciphertext of
+a batch of `--streams` independent ciphertexts, each on its own CUDA stream with its own workspace (the
+throughput-with-batch setting of the paper's throughput figures; `--streams 1` = one KeySwitch at a time).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl hks|reference] [--config C2|C1|C4]
   torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, ciphertexts sharded: weak scaling)
@@ -41,6 +43,9 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--level", type=int, default=None)
     ap.add_argument("--sets", type=int, default=5)
+    ap.add_argument("--streams", type=int, default=0,
+                    help="C1/C2/C4: ciphertexts KeySwitched concurrently per step, one CUDA stream each "
+                         "(0 = the measured best per config: C1 8, C2 3, C4 2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e / NTT / profile legs (for ncu runs)")
     ap.add_argument("--no-graph", action="store_true",
@@ -235,20 +240,45 @@ class KSWorkload:
     unit = "KeySwitch/s"
     scaling = "weak"
 
-    def __init__(self, H, ctx, cfg, level, nsets, dev, seed, sid):
+    def __init__(self, H, ctx, cfg, level, nsets, dev, seed, sid, conc=1):
+        import torch
         self.H, self.ctx, self.cfg, self.level, self.sid = H, ctx, cfg, level, sid
+        nsets = max(nsets, conc)
         self.sets = make_sets(cfg, level, nsets, dev, seed)
-        self.ws = ctx.workspace(H.OP_KEYSWITCH, level)
-        self.units = 1
+        self.conc = conc
+        self.wss = [ctx.workspace(H.OP_KEYSWITCH, level) for _ in range(conc)]
+        self.ws = self.wss[0]
+        self.streams = [torch.cuda.Stream(dev) for _ in range(conc)] if conc > 1 else []
+        self.units = conc
         self.nsets = nsets
 
-    def step(self, i):
+    e2e_units = 1   # the e2e pipeline moves one ciphertext per step
+
+    def step1(self, i):
         s = self.sets[i % len(self.sets)]
         self.H.keyswitch(self.ctx, s["c0"], s["c1"], self.level, s["evk"], s["out0"], s["out1"], self.ws, self.sid)
 
+    def step(self, i):
+        """One batch: `conc` KeySwitches of distinct (ct, key) sets, forked onto their own streams from the
+        current stream and joined back (inside a CUDA graph: `conc` parallel branches)."""
+        if self.conc == 1:
+            s = self.sets[i % len(self.sets)]
+            self.H.keyswitch(self.ctx, s["c0"], s["c1"], self.level, s["evk"], s["out0"], s["out1"], self.ws, self.sid)
+            return
+        import torch
+        cur = torch.cuda.current_stream()
+        for st in self.streams:
+            st.wait_stream(cur)
+        for j, st in enumerate(self.streams):
+            s = self.sets[(i * self.conc + j) % len(self.sets)]
+            self.H.keyswitch(self.ctx, s["c0"], s["c1"], self.level, s["evk"], s["out0"], s["out1"], self.wss[j],
+                             st.cuda_stream)
+        for st in self.streams:
+            cur.wait_stream(st)
+
     def alg_bytes(self):
         c, l = self.cfg, self.level
-        return (4 * (l + 1) + 2 * c.beta(l) * (l + 1 + c.K)) * c.n * 8
+        return self.conc * (4 * (l + 1) + 2 * c.beta(l) * (l + 1 + c.K)) * c.n * 8
 
     def l2_note(self):
         c, l = self.cfg, self.level
@@ -354,7 +384,7 @@ class C4ShardWorkload:
 
     def alg_bytes(self):
         c, l = self.cfg, self.level
-        return (4 * (l + 1) + 2 * c.beta(l) * (l + 1 + c.K)) * c.n * 8
+        return self.conc * (4 * (l + 1) + 2 * c.beta(l) * (l + 1 + c.K)) * c.n * 8
 
     def l2_note(self):
         c, l = self.cfg, self.level
@@ -565,7 +595,8 @@ def main():
     elif cfg.name == "C5":
         wl = C5Workload(H, ctx, cfg, dev, seed, sid)
     else:
-        wl = KSWorkload(H, ctx, cfg, level, args.sets, dev, seed, sid)
+        conc = args.streams or {"C1": 8, "C2": 3, "C4": 2}.get(cfg.name, 1)
+        wl = KSWorkload(H, ctx, cfg, level, args.sets, dev, seed, sid, conc)
 
     for i in range(args.warmup):
         wl.step(i)
@@ -634,8 +665,8 @@ def main():
         # ---- per-kernel breakdown: CUDA events recorded by libhks around each launch, same stream
         H.prof_enable(True)
         nprof = max(1, min(args.steps, 100 if cfg.name not in ("C3", "C5") else 5))
-        for i in range(nprof):
-            wl.step(i)
+        for i in range(nprof):   # kernels of one KeySwitch at a time (no concurrent-stream overlap in the events)
+            getattr(wl, "step1", wl.step)(i)
         prof = H.prof_read()
         H.prof_enable(False)
         tot = sum(v[1] for v in prof.values())
@@ -773,7 +804,7 @@ def main():
             e1.record(s_out)
             e1.synchronize()
             et = max_over_ranks(e0.elapsed_time(e1))
-            extra["e2e"] = {"value": world * wl.units * e_steps / (et / 1e3), "unit": wl.unit,
+            extra["e2e"] = {"value": world * getattr(wl, "e2e_units", wl.units) * e_steps / (et / 1e3), "unit": wl.unit,
                             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e_steps}
 
     if rank == 0:
@@ -785,7 +816,9 @@ def main():
                            "parallelism": (f"RNS limbs sharded over {world} GPU(s) ({shard_mode})"
                                            if shard_mode != "none" else
                                            f"{'replicas' if cfg.name == 'C5' else 'ciphertexts sharded'} over {world} GPU(s)"),
-                           "l2": wl.l2_note()},
+                           "l2": wl.l2_note(),
+                           "batch": (f"{wl.conc} ciphertexts per step, each KeySwitched on its own CUDA stream"
+                                     if getattr(wl, "conc", 1) > 1 else "1 ciphertext per step")},
                 "gpu_launches": launches, "clocks": clk.summary(),
                 "launch_mode": (f"CUDA graph replay of the C-ABI calls ({glaunch[0]} kernels per step)" if graphs
                                 else "direct C-ABI calls")}

@@ -570,3 +570,47 @@ def test_keyswitch_after_cross_stream_copy(orc):
     torch.cuda.synchronize()
     for i in range(9):
         assert torch.equal(outs[i][0], refs[i % 3][0]) and torch.equal(outs[i][1], refs[i % 3][1]), i
+
+
+@pytest.mark.parametrize("name,level,nstream", [("C2", 29, 3), ("C1", 2, 8)])
+def test_concurrent_keyswitches_on_streams(orc, name, level, nstream):
+    """bench.py's batch step: `nstream` KeySwitches of distinct ciphertexts, each on its own stream with its
+    own workspace, forked from and joined to the current stream (directly and as one captured CUDA graph):
+    every output equals the oracle's."""
+    import torch
+    cfg, ctx, o = ctxs(orc, name)
+    g = S.rng(cfg.seed + 31)
+    nk = o.nq + o.np
+    evk = np.stack([S.uniform_limbs(g, o.primes, o.n) for _ in range(2 * o.dnum)]).reshape(o.dnum, 2, nk, o.n)
+    evk_d = to_dev(evk)
+    cts = [(S.uniform_limbs(g, o.q[: level + 1], o.n), S.uniform_limbs(g, o.q[: level + 1], o.n))
+           for _ in range(nstream)]
+    want = [o.keyswitch(c0, c1, evk, level) for c0, c1 in cts]
+    dcts = [(to_dev(c0), to_dev(c1)) for c0, c1 in cts]
+    outs = [(torch.empty_like(a), torch.empty_like(b)) for a, b in dcts]
+    wss = [ctx.workspace(H.OP_KEYSWITCH, level) for _ in range(nstream)]
+    sts = [torch.cuda.Stream() for _ in range(nstream)]
+
+    def batch():
+        cur = torch.cuda.current_stream()
+        for st in sts:
+            st.wait_stream(cur)
+        for j, st in enumerate(sts):
+            H.keyswitch(ctx, dcts[j][0], dcts[j][1], level, evk_d, outs[j][0], outs[j][1], wss[j], st.cuda_stream)
+        for st in sts:
+            cur.wait_stream(st)
+
+    def check():
+        torch.cuda.synchronize()
+        for j in range(nstream):
+            assert (to_host(outs[j][0]) == want[j][0]).all() and (to_host(outs[j][1]) == want[j][1]).all(), j
+            outs[j][0].zero_()
+            outs[j][1].zero_()
+
+    batch()
+    check()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        batch()
+    graph.replay()
+    check()
