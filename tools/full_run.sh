@@ -11,5 +11,5 @@ done
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"^k_" --csv --log-file $out/launches_${tag}.csv \
   python bench.py --quick --steps 20 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"^k_" --launch-skip 90 --launch-count 9 \
-  -o $out/prof_${tag} -f python bench.py --quick --steps 12 --warmup 3 --sets 2 --no-cpu-baseline > /dev/null 2>&1
+  -o $out/prof_${tag} -f python bench.py --quick --streams 1 --steps 12 --warmup 3 --sets 2 --no-cpu-baseline > /dev/null 2>&1
 ls -la $out | grep $tag
