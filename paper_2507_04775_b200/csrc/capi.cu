@@ -726,7 +726,9 @@ extern "C" size_t hks_linear_transform_workspace_bytes(const hks_ctx *c, uint32_
     const size_t lb = limb_bytes(c), l1 = level + 1;
     const size_t rot = std::max(hks_workspace_bytes(c, HKS_OP_ROTATE_HOISTED, level, n1 > 1 ? n1 - 1 : 1),
                                 hks_workspace_bytes(c, HKS_OP_ROTATE_HOISTED, level, 1));
-    return (2 * (size_t)(n1 - 1) + 4) * l1 * lb + rot;   // baby ciphertexts, inner, rotated inner, rotations
+    const size_t rot1 = hks_workspace_bytes(c, HKS_OP_ROTATE_HOISTED, level, 1);
+    // baby ciphertexts, inner, rotated inner, rotations; per side branch: inner, rotated, accumulator, rotation
+    return (2 * (size_t)(n1 - 1) + 4) * l1 * lb + rot + hks_ctx::NSIDE * (6 * l1 * lb + rot1);
 }
 
 extern "C" hks_status hks_linear_transform(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, uint32_t level,
@@ -766,21 +768,54 @@ extern "C" hks_status hks_linear_transform(const hks_ctx *c, const uint64_t *c0,
         x0[j] = b0[j];
         x1[j] = b1[j];
     }
-    u64 *i0 = base + 2 * (size_t)(n1 - 1) * lw, *i1 = i0 + lw, *r0 = i1 + lw, *r1 = r0 + lw, *rws = r1 + lw;
+    const size_t rotb = hks_workspace_bytes(c, HKS_OP_ROTATE_HOISTED, level, n1 > 1 ? n1 - 1 : 1);
+    const size_t rot = std::max(rotb, hks_workspace_bytes(c, HKS_OP_ROTATE_HOISTED, level, 1));
+    const size_t rot1w = hks_workspace_bytes(c, HKS_OP_ROTATE_HOISTED, level, 1) / 8;
+    // branch 0 = the caller's stream (accumulates into out), branch b >= 1 = side stream b - 1 (own inner,
+    // rotated and accumulator buffers and rotation workspace, summed into out after the join)
+    struct Branch { u64 *i0, *i1, *r0, *r1, *a0, *a1, *rws; cudaStream_t s; bool first; };
+    Branch br[1 + hks_ctx::NSIDE];
+    {
+        u64 *at = base + 2 * (size_t)(n1 - 1) * lw;
+        br[0] = {at, at + lw, at + 2 * lw, at + 3 * lw, out0, out1, at + 4 * lw, s, false};
+        at += 4 * lw + rot / 8;
+        for (int b = 1; b <= hks_ctx::NSIDE; b++) {
+            br[b] = {at, at + lw, at + 2 * lw, at + 3 * lw, at + 4 * lw, at + 5 * lw, at + 6 * lw, c->side[b - 1], true};
+            at += 6 * lw + rot1w;
+        }
+    }
     // baby steps: one ModUp shared by the n1 - 1 rotations (hoisted)
     if (n1 > 1 && (st = hks_rotate_hoisted(c, c0, c1, level, n1 - 1, baby_galois, baby_evk, b0.data() + 1,
-                                           b1.data() + 1, rws, stream)) != HKS_OK)
+                                           b1.data() + 1, br[0].rws, stream)) != HKS_OK)
         return st;
-    // giant steps: I_i = sum_j pt[i n1 + j] ct_j (fused weighted sum), out += Rot_{g_i}(I_i)
-    for (u32 i = 0; i < n2; i++) {
-        u64 *t0 = i == 0 ? out0 : i0, *t1 = i == 0 ? out1 : i1;
-        if ((st = wsum_core(c, n1, pt + (size_t)i * n1, x0.data(), x1.data(), level, t0, t1, s)) != HKS_OK) return st;
-        if (i == 0) continue;
-        u64 *o0 = r0, *o1 = r1;
-        if ((st = hks_rotate_hoisted(c, i0, i1, level, 1, giant_galois + (i - 1), giant_evk + (i - 1), &o0, &o1, rws,
-                                     stream)) != HKS_OK)
+    // giant steps: I_i = sum_j pt[i n1 + j] ct_j (fused weighted sum), out += Rot_{g_i}(I_i).  The giant
+    // steps are independent: with more than two of them, steps i = 1, 2, ... go round-robin to the caller's
+    // stream and the side streams (modular sums are exact, so the order of the additions does not matter)
+    if ((st = wsum_core(c, n1, pt, x0.data(), x1.data(), level, out0, out1, s)) != HKS_OK) return st;
+    const int nb = (n2 > 2 && c->side[0]) ? std::min<int>(1 + hks_ctx::NSIDE, (int)n2 - 1) : 1;
+    std::unique_lock<std::mutex> lk(c->side_mu, std::defer_lock);
+    if (nb > 1) {
+        lk.lock();
+        if (cudaEventRecord(c->ev_fork, s) != cudaSuccess) HKS_FAIL(HKS_ECUDA, "linear_transform: event record");
+        for (int b = 1; b < nb; b++)
+            if (cudaStreamWaitEvent(br[b].s, c->ev_fork, 0) != cudaSuccess) HKS_FAIL(HKS_ECUDA, "linear_transform: wait");
+    }
+    for (u32 i = 1; i < n2; i++) {
+        Branch &B = br[(i - 1) % nb];
+        if ((st = wsum_core(c, n1, pt + (size_t)i * n1, x0.data(), x1.data(), level, B.i0, B.i1, B.s)) != HKS_OK)
             return st;
-        if ((st = launch_add_ct(r0, r1, out0, out1, level + 1, c->log_n, c->d_pc, s)) != HKS_OK) return st;
+        u64 *o0 = B.first ? B.a0 : B.r0, *o1 = B.first ? B.a1 : B.r1;
+        if ((st = hks_rotate_hoisted(c, B.i0, B.i1, level, 1, giant_galois + (i - 1), giant_evk + (i - 1), &o0, &o1,
+                                     B.rws, B.s)) != HKS_OK)
+            return st;
+        if (!B.first && (st = launch_add_ct(B.r0, B.r1, B.a0, B.a1, level + 1, c->log_n, c->d_pc, B.s)) != HKS_OK)
+            return st;
+        B.first = false;
+    }
+    for (int b = 1; b < nb; b++) {
+        if (cudaEventRecord(c->ev_join[b - 1], br[b].s) != cudaSuccess || cudaStreamWaitEvent(s, c->ev_join[b - 1], 0) != cudaSuccess)
+            HKS_FAIL(HKS_ECUDA, "linear_transform: join");
+        if ((st = launch_add_ct(br[b].a0, br[b].a1, out0, out1, level + 1, c->log_n, c->d_pc, s)) != HKS_OK) return st;
     }
     return HKS_OK;
 }

@@ -107,6 +107,11 @@ void free_tables(hks_ctx *c) {
                     c->d_qmod, c->d_qlinv};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    for (int i = 0; i < hks_ctx::NSIDE; i++) {
+        if (c->side[i]) cudaStreamDestroy(c->side[i]);
+        if (c->ev_join[i]) cudaEventDestroy(c->ev_join[i]);
+    }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
 }
 
 // Twiddle tables of one prime.  psi_brv[k] = psi^brv_logN(k) ("precomputing the
@@ -444,6 +449,12 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     UP(d_qmod, qmod);
     UP(d_qlinv, qlinv);
 #undef UP
+    for (int i = 0; i < hks_ctx::NSIDE && st == HKS_OK; i++) {
+        if (cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming) != cudaSuccess)
+            st = HKS_ECUDA;
+    }
+    if (st == HKS_OK && cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess) st = HKS_ECUDA;
     cudaSetDevice(prev);
     if (st != HKS_OK) {
         free_tables(c);

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
@@ -249,6 +250,14 @@ struct hks_ctx {
     ulonglong2 *d_pinv = nullptr;       // P^-1 mod q_i  [L+1] (Shoup)
     u64 *d_qmod = nullptr;              // Rescale: q_j mod q_i  [L+1][L+1] (row j = dropped limb)
     ulonglong2 *d_qlinv = nullptr;      // Rescale: q_j^-1 mod q_i (Shoup)  [L+1][L+1]
+
+    // side streams for independent branches inside one call (the giant steps of hks_linear_transform):
+    // created with the context, forked from / joined to the caller's stream with the events below; the
+    // mutex serialises concurrent callers' enqueue phases (a wait binds the event's latest record)
+    static constexpr int NSIDE = 2;
+    cudaStream_t side[NSIDE] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join[NSIDE] = {};
+    mutable std::mutex side_mu;
 
     u32 L() const { return nq - 1; }
     u32 beta(u32 level) const { return (level + 1 + alpha - 1) / alpha; }

@@ -488,10 +488,15 @@ def test_pt_weighted_sum_parity(orc, name, level, nterm):
     assert (to_host(out0) == w0).all() and (to_host(out1) == w1).all()
 
 
-@pytest.mark.parametrize("name,level,n1,n2", [("T12", 6, 3, 3), ("T12", 4, 4, 1), ("T12", 5, 1, 3), ("T12", 2, 1, 1),
-                                              ("C2", 29, 4, 4)])
-def test_linear_transform_parity(orc, name, level, n1, n2):
-    """BSGS: hoisted baby rotations, fused weighted sums, one rotation per giant step; bit-exact."""
+@pytest.mark.parametrize("name,level,n1,n2,graph", [("T12", 6, 3, 3, False), ("T12", 4, 4, 1, False),
+                                                    ("T12", 5, 1, 3, False), ("T12", 2, 1, 1, False),
+                                                    ("T12", 6, 2, 8, False), ("T12", 3, 3, 5, True),
+                                                    ("T12", 6, 2, 8, True), ("C2", 29, 4, 4, False)])
+def test_linear_transform_parity(orc, name, level, n1, n2, graph):
+    """BSGS: hoisted baby rotations, fused weighted sums, one rotation per giant step; bit-exact.  n2 > 2:
+    the giant steps run round-robin on the caller's stream and the context's side streams (n2 = 8: every
+    branch takes several steps); `graph`: the call captured into a CUDA graph (fork / join inside the
+    capture) and replayed."""
     cfg, ctx, o = ctxs(orc, name)
     keys = Keys(o, cfg.seed + 81)
     g = S.rng(cfg.seed + 82)
@@ -504,8 +509,17 @@ def test_linear_transform_parity(orc, name, level, n1, n2):
     pts = [S.uniform_limbs(g, qs, o.n) for _ in range(n1 * n2)]
     out0, out1 = empty_dev(c0.shape), empty_dev(c0.shape)
     ws = H.linear_transform_workspace(ctx, level, n1)
-    H.linear_transform(ctx, to_dev(c0), to_dev(c1), level, n1, n2, bgal, [to_dev(k) for k in bk], ggal,
-                       [to_dev(k) for k in gk], [to_dev(p) for p in pts], out0, out1, ws)
+    args = (ctx, to_dev(c0), to_dev(c1), level, n1, n2, bgal, [to_dev(k) for k in bk], ggal,
+            [to_dev(k) for k in gk], [to_dev(p) for p in pts], out0, out1, ws)
+    if graph:
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            H.linear_transform(*args, torch.cuda.current_stream().cuda_stream)
+        gr.replay()
+        torch.cuda.synchronize()
+    else:
+        H.linear_transform(*args)
     w0, w1 = o.lintrans(c0, c1, level, n1, n2, bgal, bk, ggal, gk, pts)
     assert (to_host(out0) == w0).all() and (to_host(out1) == w1).all()
 
