@@ -230,7 +230,9 @@ hks_status hks_rotate_hoisted(const hks_ctx *ctx, const uint64_t *c0, const uint
 /* Hoisted rotations of nct <= 8 ciphertexts sharing the same nrot rotation keys (SURVEY.md §7 "key
  * streaming": the key product loads every key word once for the whole batch).  c0[i], c1[i]:
  * ciphertext i [l+1][N] EVAL; out0/out1[i * nrot + r] receive rotation r of ciphertext i (as in
- * hks_rotate_hoisted).  beta(level) <= 4.  ws: hks_rotate_hoisted_batch_workspace_bytes(ctx, nct, level). */
+ * hks_rotate_hoisted).  beta(level) <= 4.  ws: hks_rotate_hoisted_batch_workspace_bytes(ctx, nct, level).
+ * Stream semantics: after the ModUps the nrot rotations are spread round-robin over `stream` and the
+ * context's two side streams (event fork / join), so the call stays ordered on `stream` and is graph-capturable. */
 hks_status hks_rotate_hoisted_batch(const hks_ctx *ctx, uint32_t nct, const uint64_t *const *c0,
                                     const uint64_t *const *c1, uint32_t level, uint32_t nrot,
                                     const uint64_t *galois, const uint64_t *const *evk, uint64_t *const *out0,

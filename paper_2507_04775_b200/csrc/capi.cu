@@ -628,14 +628,30 @@ extern "C" hks_status hks_rotate_hoisted_batch(const hks_ctx *c, uint32_t nct, c
     u64 *exts = coef + l1 * N;                          // [nct][beta][ne]
     u64 *accs = exts + (size_t)nct * beta * ne * N;     // [nct][2][ne]
     u64 *md = accs + (size_t)nct * 2 * ne * N;          // ModDown workspace for 2 nct polynomials
+    const size_t accw = (size_t)nct * 2 * ne * N, mdw = (size_t)nct * (2 * K + 2 * l1) * N;
     for (u32 i = 0; i < nct; i++)
         if ((st = modup_core(c, c1[i], level, exts + (size_t)i * beta * ne * N, coef, s)) != HKS_OK) return st;
+    // the rotations are independent after the ModUps: round-robin over the caller's stream and the
+    // context's side streams, each branch with its own accumulators and ModDown workspace
+    const int nb = (nrot > 1 && c->side[0]) ? std::min<int>(1 + hks_ctx::NSIDE, (int)nrot) : 1;
+    std::unique_lock<std::mutex> lk(c->side_mu, std::defer_lock);
+    if (nb > 1) {
+        lk.lock();
+        if (cudaEventRecord(c->ev_fork, s) != cudaSuccess) HKS_FAIL(HKS_ECUDA, "rotate_hoisted_batch: event record");
+        for (int b = 1; b < nb; b++)
+            if (cudaStreamWaitEvent(c->side[b - 1], c->ev_fork, 0) != cudaSuccess)
+                HKS_FAIL(HKS_ECUDA, "rotate_hoisted_batch: wait");
+    }
     for (u32 r = 0; r < nrot; r++) {
+        const int b = (int)(r % (u32)nb);
+        const cudaStream_t bs = b == 0 ? s : c->side[b - 1];
+        u64 *baccs = b == 0 ? accs : md + mdw + (size_t)(b - 1) * (accw + mdw);
+        u64 *bmd = b == 0 ? md : baccs + accw;
         KipMultiArgs a{};
         for (u32 i = 0; i < nct; i++) {
             a.ext[i] = exts + (size_t)i * beta * ne * N;
             a.c1[i] = c1[i];
-            a.acc[i] = accs + (size_t)i * 2 * ne * N;
+            a.acc[i] = baccs + (size_t)i * 2 * ne * N;
         }
         a.evk = evk[r];
         a.pc = c->d_pc;
@@ -649,7 +665,7 @@ extern "C" hks_status hks_rotate_hoisted_batch(const hks_ctx *c, uint32_t nct, c
         a.nk = c->nq + c->np;
         a.beta = beta;
         a.alpha = c->alpha;
-        if ((st = launch_kip_multi(a, s)) != HKS_OK) return st;
+        if ((st = launch_kip_multi(a, bs)) != HKS_OK) return st;
         std::vector<u64 *> outs(2 * nct);
         std::vector<const u64 *> adds(2 * nct);
         std::vector<u64> gal(2 * nct);
@@ -661,16 +677,21 @@ extern "C" hks_status hks_rotate_hoisted_batch(const hks_ctx *c, uint32_t nct, c
             gal[2 * i] = galois[r];
             gal[2 * i + 1] = 1;
         }
-        if ((st = moddown_core(c, accs, 2 * nct, level, outs.data(), adds.data(), gal.data(), md, s)) != HKS_OK) return st;
+        if ((st = moddown_core(c, baccs, 2 * nct, level, outs.data(), adds.data(), gal.data(), bmd, bs)) != HKS_OK)
+            return st;
     }
-    (void)K;
+    for (int b = 1; b < nb; b++)
+        if (cudaEventRecord(c->ev_join[b - 1], c->side[b - 1]) != cudaSuccess ||
+            cudaStreamWaitEvent(s, c->ev_join[b - 1], 0) != cudaSuccess)
+            HKS_FAIL(HKS_ECUDA, "rotate_hoisted_batch: join");
     return HKS_OK;
 }
 
 extern "C" size_t hks_rotate_hoisted_batch_workspace_bytes(const hks_ctx *c, uint32_t nct, uint32_t level) {
     if (!c || level > c->L() || nct == 0) return 0;
     const size_t lb = limb_bytes(c), l1 = level + 1, ne = c->ne(level), K = c->np, beta = c->beta(level);
-    return (l1 + nct * (beta * ne + 2 * ne) + nct * (2 * K + 2 * l1)) * lb;
+    // coef, ModUp outputs, then per branch (caller's stream + side streams) accumulators and ModDown workspace
+    return (l1 + nct * beta * ne + (1 + hks_ctx::NSIDE) * (nct * 2 * ne + nct * (2 * K + 2 * l1))) * lb;
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -343,9 +343,13 @@ def test_bconv_alternate_paths_identical(orc, env):
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("name,level,nct,rots", [("T12", 6, 3, [1, 2, 5]), ("C2", 29, 2, [1, 3, 8])])
-def test_rotate_hoisted_batch_parity(orc, name, level, nct, rots):
-    """Several ciphertexts sharing rotation keys (C3 shape): each output bit-equal to the hoisted oracle."""
+@pytest.mark.parametrize("name,level,nct,rots,graph", [("T12", 6, 3, [1, 2, 5], False), ("C2", 29, 2, [1, 3, 8], False),
+                                                     ("T12", 5, 2, [1, 2, 3, 4, 5, 6, 7], False),
+                                                     ("T12", 4, 3, [1, 3, 5, 7, 9], True)])
+def test_rotate_hoisted_batch_parity(orc, name, level, nct, rots, graph):
+    """Several ciphertexts sharing rotation keys (C3 shape): each output bit-equal to the hoisted oracle.
+    The rotations run round-robin on the caller's stream and the context's side streams (7 rotations:
+    several per branch); `graph`: captured into a CUDA graph and replayed."""
     cfg, ctx, o = ctxs(orc, name)
     keys = Keys(o, cfg.seed + 13)
     ks = [S.galois_rot(r, cfg.log_n) for r in rots]
@@ -356,8 +360,17 @@ def test_rotate_hoisted_batch_parity(orc, name, level, nct, rots):
     outs0 = [empty_dev(cts[0][0].shape) for _ in range(nct * nr)]
     outs1 = [empty_dev(cts[0][0].shape) for _ in range(nct * nr)]
     ws = H.rotate_hoisted_batch_workspace(ctx, nct, level)
-    H.rotate_hoisted_batch(ctx, [to_dev(c[0]) for c in cts], [to_dev(c[1]) for c in cts], level, ks,
-                           [to_dev(e) for e in evks], outs0, outs1, ws)
+    args = (ctx, [to_dev(c[0]) for c in cts], [to_dev(c[1]) for c in cts], level, ks, [to_dev(e) for e in evks],
+            outs0, outs1, ws)
+    if graph:
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            H.rotate_hoisted_batch(*args, torch.cuda.current_stream().cuda_stream)
+        gr.replay()
+        torch.cuda.synchronize()
+    else:
+        H.rotate_hoisted_batch(*args)
     for i, (c0, c1) in enumerate(cts):
         w0, w1 = o.rotate_hoisted(c0, c1, evks, level, ks)
         for r in range(nr):
