@@ -641,3 +641,46 @@ def test_concurrent_keyswitches_on_streams(orc, name, level, nstream):
         batch()
     graph.replay()
     check()
+
+
+def test_linear_transform_two_host_threads(orc):
+    """Two host threads run BSGS transforms on one context concurrently (own streams and workspaces): the
+    context's side streams are shared under its mutex, and both results equal the oracle's."""
+    import threading
+    cfg, ctx, o = ctxs(orc, "T12")
+    keys = Keys(o, cfg.seed + 91)
+    level, n1, n2 = 5, 2, 6
+    bgal = [S.galois_rot(j, cfg.log_n) for j in range(1, n1)]
+    ggal = [S.galois_rot(i * n1, cfg.log_n) for i in range(1, n2)]
+    bk, gk = [keys.rot(k) for k in bgal], [keys.rot(k) for k in ggal]
+    bkd, gkd = [to_dev(k) for k in bk], [to_dev(k) for k in gk]
+    qs = o.q[: level + 1]
+    jobs = []
+    for t in range(2):
+        g = S.rng(cfg.seed + 92 + t)
+        c0, c1 = S.uniform_limbs(g, qs, o.n), S.uniform_limbs(g, qs, o.n)
+        pts = [S.uniform_limbs(g, qs, o.n) for _ in range(n1 * n2)]
+        jobs.append(dict(c0=c0, c1=c1, pts=pts, d0=to_dev(c0), d1=to_dev(c1), dp=[to_dev(p) for p in pts],
+                         out0=empty_dev(c0.shape), out1=empty_dev(c0.shape),
+                         ws=H.linear_transform_workspace(ctx, level, n1), st=torch.cuda.Stream()))
+    torch.cuda.synchronize()
+    errs = []
+
+    def work(j):
+        try:
+            for _ in range(5):
+                H.linear_transform(ctx, j["d0"], j["d1"], level, n1, n2, bgal, bkd, ggal, gkd, j["dp"], j["out0"],
+                                   j["out1"], j["ws"], j["st"].cuda_stream)
+        except Exception as e:   # pragma: no cover - reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(j,)) for j in jobs]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errs, errs
+    for j in jobs:
+        w0, w1 = o.lintrans(j["c0"], j["c1"], level, n1, n2, bgal, bk, ggal, gk, j["pts"])
+        assert (to_host(j["out0"]) == w0).all() and (to_host(j["out1"]) == w1).all()
