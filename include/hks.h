@@ -221,7 +221,9 @@ hks_status hks_automorph(const hks_ctx *ctx, const uint64_t *in, uint32_t nlimbs
 /* Hoisted rotations (§3.6.6): one ModUp of c1 shared by nrot rotations.
  *   galois[r], evk[r], out0[r], out1[r]: host arrays of length nrot (device pointers inside).
  *   out0[r] = pi_k(c0) + ModDown(acc0_r), out1[r] = ModDown(acc1_r), acc_r = KIP(ext, evk[r], k_r).
- *   ws   hks_workspace_bytes(ctx, HKS_OP_ROTATE_HOISTED, level, nrot) bytes. */
+ *   ws   hks_workspace_bytes(ctx, HKS_OP_ROTATE_HOISTED, level, nrot) bytes.
+ *   Stream semantics: with nrot > 1 the rotations after the shared ModUp are split over `stream` and the
+ *   context's two side streams (event fork / join); the call stays ordered on `stream`, graph-capturable. */
 hks_status hks_rotate_hoisted(const hks_ctx *ctx, const uint64_t *c0, const uint64_t *c1, uint32_t level,
                               uint32_t nrot, const uint64_t *galois, const uint64_t *const *evk,
                               uint64_t *const *out0, uint64_t *const *out1, void *ws, void *stream);

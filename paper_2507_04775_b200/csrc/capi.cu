@@ -210,6 +210,12 @@ hks_status kip_core(const hks_ctx *c, const u64 *ext, const u64 *c1, const u64 *
 
 // rotations whose ModDowns are batched together: 2 RB polynomials must fit the 16-entry output
 // table of one ModDown epilogue launch and the K-limb INTT batches (HKS_MAXB limbs).
+// branches of hks_rotate_hoisted: the rotations after the shared ModUp split over the caller's stream and
+// the context's side streams (one branch for a single rotation or a host-only context)
+size_t rot_branches(const hks_ctx *c, u32 nrot) {
+    return (nrot > 1 && c->side[0]) ? std::min<size_t>(1 + hks_ctx::NSIDE, nrot) : 1;
+}
+
 size_t rot_batch(const hks_ctx *c, u32 level) {
     (void)level;
     return std::max<size_t>(1, std::min<size_t>(NTT_MAXO / 2, HKS_MAXB / (2 * c->np)));
@@ -230,8 +236,9 @@ extern "C" size_t hks_workspace_bytes(const hks_ctx *c, hks_op op, uint32_t leve
         case HKS_OP_MODDOWN: return (K + l1) * lb;
         case HKS_OP_KEYSWITCH: return (l1 + beta * ne + 2 * ne + 2 * K + 2 * l1) * lb;
         case HKS_OP_ROTATE_HOISTED: {
-            const size_t rb = std::min<size_t>(count ? count : 1, rot_batch(c, level));
-            return (l1 + beta * ne + rb * (2 * ne + 2 * K + 2 * l1)) * lb;
+            const size_t nr = count ? count : 1, nb = rot_branches(c, (u32)nr);
+            const size_t rb = std::min<size_t>((nr + nb - 1) / nb, rot_batch(c, level));
+            return (l1 + beta * ne + nb * rb * (2 * ne + 2 * K + 2 * l1)) * lb;
         }
         case HKS_OP_HMULT: return (l1 + beta * ne + 2 * ne + 2 * K + 2 * l1 + l1) * lb;
         case HKS_OP_RESCALE: {
@@ -577,28 +584,49 @@ extern "C" hks_status hks_rotate_hoisted(const hks_ctx *c, const uint64_t *c0, c
     u64 *coef = (u64 *)ws;
     u64 *ext = coef + l1 * c->n;
     if ((st = modup_core(c, c1, level, ext, coef, s)) != HKS_OK) return st;
-    // rotations in groups of RB: RB key products (each with its automorphism gather) into RB
+    // the rotations split into nb contiguous ranges, one per branch (caller's stream, side streams); a
+    // branch takes its range in groups of RB: RB key products (each with its automorphism gather) into RB
     // accumulator pairs, then ONE ModDown over the 2 RB polynomials (large batches per launch)
-    const u32 RB = (u32)std::min<size_t>(nrot, rot_batch(c, level));
-    u64 *acc = ext + beta * ne * c->n;
-    u64 *md = acc + (size_t)RB * 2 * ne * c->n;
-    for (u32 r0 = 0; r0 < nrot; r0 += RB) {
-        const u32 nr = std::min(RB, nrot - r0);
-        std::vector<u64 *> outs(2 * nr);
-        std::vector<const u64 *> adds(2 * nr);
-        std::vector<u64> gal(2 * nr);
-        for (u32 r = 0; r < nr; r++) {
-            if ((st = kip_core(c, ext, c1, evk[r0 + r], level, galois[r0 + r], acc + (size_t)r * 2 * ne * c->n, s)) != HKS_OK)
-                return st;
-            outs[2 * r] = out0[r0 + r];
-            outs[2 * r + 1] = out1[r0 + r];
-            adds[2 * r] = c0;
-            adds[2 * r + 1] = nullptr;
-            gal[2 * r] = galois[r0 + r];
-            gal[2 * r + 1] = 1;
-        }
-        if ((st = moddown_core(c, acc, 2 * nr, level, outs.data(), adds.data(), gal.data(), md, s)) != HKS_OK) return st;
+    const u32 nb = (u32)rot_branches(c, nrot);
+    const u32 per = (nrot + nb - 1) / nb;
+    const u32 RB = (u32)std::min<size_t>(per, rot_batch(c, level));
+    const size_t bw = (size_t)RB * (2 * ne + 2 * c->np + 2 * l1) * c->n;   // words per branch
+    std::unique_lock<std::recursive_mutex> lk(c->side_mu, std::defer_lock);
+    if (nb > 1) {
+        lk.lock();
+        if (cudaEventRecord(c->ev_fork, s) != cudaSuccess) HKS_FAIL(HKS_ECUDA, "rotate_hoisted: event record");
+        for (u32 b = 1; b < nb; b++)
+            if (cudaStreamWaitEvent(c->side[b - 1], c->ev_fork, 0) != cudaSuccess) HKS_FAIL(HKS_ECUDA, "rotate_hoisted: wait");
     }
+    for (u32 b = 0; b < nb; b++) {
+        const cudaStream_t bs = b == 0 ? s : c->side[b - 1];
+        u64 *acc = ext + beta * ne * c->n + b * bw;
+        u64 *md = acc + (size_t)RB * 2 * ne * c->n;
+        const u32 rend = std::min(nrot, (b + 1) * per);
+        for (u32 r0 = b * per; r0 < rend; r0 += RB) {
+            const u32 nr = std::min(RB, rend - r0);
+            std::vector<u64 *> outs(2 * nr);
+            std::vector<const u64 *> adds(2 * nr);
+            std::vector<u64> gal(2 * nr);
+            for (u32 r = 0; r < nr; r++) {
+                if ((st = kip_core(c, ext, c1, evk[r0 + r], level, galois[r0 + r], acc + (size_t)r * 2 * ne * c->n, bs)) !=
+                    HKS_OK)
+                    return st;
+                outs[2 * r] = out0[r0 + r];
+                outs[2 * r + 1] = out1[r0 + r];
+                adds[2 * r] = c0;
+                adds[2 * r + 1] = nullptr;
+                gal[2 * r] = galois[r0 + r];
+                gal[2 * r + 1] = 1;
+            }
+            if ((st = moddown_core(c, acc, 2 * nr, level, outs.data(), adds.data(), gal.data(), md, bs)) != HKS_OK)
+                return st;
+        }
+    }
+    for (u32 b = 1; b < nb; b++)
+        if (cudaEventRecord(c->ev_join[b - 1], c->side[b - 1]) != cudaSuccess ||
+            cudaStreamWaitEvent(s, c->ev_join[b - 1], 0) != cudaSuccess)
+            HKS_FAIL(HKS_ECUDA, "rotate_hoisted: join");
     return HKS_OK;
 }
 
@@ -634,7 +662,7 @@ extern "C" hks_status hks_rotate_hoisted_batch(const hks_ctx *c, uint32_t nct, c
     // the rotations are independent after the ModUps: round-robin over the caller's stream and the
     // context's side streams, each branch with its own accumulators and ModDown workspace
     const int nb = (nrot > 1 && c->side[0]) ? std::min<int>(1 + hks_ctx::NSIDE, (int)nrot) : 1;
-    std::unique_lock<std::mutex> lk(c->side_mu, std::defer_lock);
+    std::unique_lock<std::recursive_mutex> lk(c->side_mu, std::defer_lock);
     if (nb > 1) {
         lk.lock();
         if (cudaEventRecord(c->ev_fork, s) != cudaSuccess) HKS_FAIL(HKS_ECUDA, "rotate_hoisted_batch: event record");
@@ -814,7 +842,7 @@ extern "C" hks_status hks_linear_transform(const hks_ctx *c, const uint64_t *c0,
     // stream and the side streams (modular sums are exact, so the order of the additions does not matter)
     if ((st = wsum_core(c, n1, pt, x0.data(), x1.data(), level, out0, out1, s)) != HKS_OK) return st;
     const int nb = (n2 > 2 && c->side[0]) ? std::min<int>(1 + hks_ctx::NSIDE, (int)n2 - 1) : 1;
-    std::unique_lock<std::mutex> lk(c->side_mu, std::defer_lock);
+    std::unique_lock<std::recursive_mutex> lk(c->side_mu, std::defer_lock);
     if (nb > 1) {
         lk.lock();
         if (cudaEventRecord(c->ev_fork, s) != cudaSuccess) HKS_FAIL(HKS_ECUDA, "linear_transform: event record");

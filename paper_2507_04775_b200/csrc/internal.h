@@ -257,7 +257,7 @@ struct hks_ctx {
     static constexpr int NSIDE = 2;
     cudaStream_t side[NSIDE] = {};
     cudaEvent_t ev_fork = nullptr, ev_join[NSIDE] = {};
-    mutable std::mutex side_mu;
+    mutable std::recursive_mutex side_mu;
 
     u32 L() const { return nq - 1; }
     u32 beta(u32 level) const { return (level + 1 + alpha - 1) / alpha; }
