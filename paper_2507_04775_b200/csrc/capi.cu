@@ -587,7 +587,8 @@ extern "C" hks_status hks_rotate_hoisted(const hks_ctx *c, const uint64_t *c0, c
     // the rotations split into nb contiguous ranges, one per branch (caller's stream, side streams); a
     // branch takes its range in groups of RB: RB key products (each with its automorphism gather) into RB
     // accumulator pairs, then ONE ModDown over the 2 RB polynomials (large batches per launch)
-    const u32 nb = (u32)rot_branches(c, nrot);
+    // (one branch while profiling; the workspace, sized for rot_branches, holds the single-branch layout too)
+    const u32 nb = prof_active() ? 1u : (u32)rot_branches(c, nrot);
     const u32 per = (nrot + nb - 1) / nb;
     const u32 RB = (u32)std::min<size_t>(per, rot_batch(c, level));
     const size_t bw = (size_t)RB * (2 * ne + 2 * c->np + 2 * l1) * c->n;   // words per branch
@@ -661,7 +662,7 @@ extern "C" hks_status hks_rotate_hoisted_batch(const hks_ctx *c, uint32_t nct, c
         if ((st = modup_core(c, c1[i], level, exts + (size_t)i * beta * ne * N, coef, s)) != HKS_OK) return st;
     // the rotations are independent after the ModUps: round-robin over the caller's stream and the
     // context's side streams, each branch with its own accumulators and ModDown workspace
-    const int nb = (nrot > 1 && c->side[0]) ? std::min<int>(1 + hks_ctx::NSIDE, (int)nrot) : 1;
+    const int nb = (nrot > 1 && c->side[0] && !prof_active()) ? std::min<int>(1 + hks_ctx::NSIDE, (int)nrot) : 1;
     std::unique_lock<std::recursive_mutex> lk(c->side_mu, std::defer_lock);
     if (nb > 1) {
         lk.lock();
@@ -841,7 +842,7 @@ extern "C" hks_status hks_linear_transform(const hks_ctx *c, const uint64_t *c0,
     // steps are independent: with more than two of them, steps i = 1, 2, ... go round-robin to the caller's
     // stream and the side streams (modular sums are exact, so the order of the additions does not matter)
     if ((st = wsum_core(c, n1, pt, x0.data(), x1.data(), level, out0, out1, s)) != HKS_OK) return st;
-    const int nb = (n2 > 2 && c->side[0]) ? std::min<int>(1 + hks_ctx::NSIDE, (int)n2 - 1) : 1;
+    const int nb = (n2 > 2 && c->side[0] && !prof_active()) ? std::min<int>(1 + hks_ctx::NSIDE, (int)n2 - 1) : 1;
     std::unique_lock<std::recursive_mutex> lk(c->side_mu, std::defer_lock);
     if (nb > 1) {
         lk.lock();

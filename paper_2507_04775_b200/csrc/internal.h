@@ -294,6 +294,9 @@ bool pdl_enabled();
 // device.  hks_num_sms: SM count of the current device (cached per device).
 void hks_func_smem(const void *fn, size_t smem);
 int hks_num_sms();
+// per-kernel profiling on (hks_prof_enable): calls with independent branches then keep them on the caller's
+// stream, so each launch's event pair times that kernel alone rather than its overlap with a sibling
+bool prof_active();
 template <typename... KArgs, typename... Args>
 inline cudaError_t hks_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args &&...args) {

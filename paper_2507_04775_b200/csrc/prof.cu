@@ -54,6 +54,8 @@ void ProfScope::done(double bytes, double muls) {
 
 extern "C" uint64_t hks_launch_count(void) { return g_launches.load(); }
 
+bool prof_active() { return g_on.load(std::memory_order_relaxed) != 0; }
+
 extern "C" hks_status hks_prof_enable(int on) {
     g_on.store(on ? 1 : 0);
     return HKS_OK;

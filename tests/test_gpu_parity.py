@@ -684,3 +684,28 @@ def test_linear_transform_two_host_threads(orc):
     for j in jobs:
         w0, w1 = o.lintrans(j["c0"], j["c1"], level, n1, n2, bgal, bk, ggal, gk, j["pts"])
         assert (to_host(j["out0"]) == w0).all() and (to_host(j["out1"]) == w1).all()
+
+
+def test_hoisted_and_bsgs_under_profiling(orc):
+    """With per-kernel profiling on, the branch-parallel calls keep every branch on the caller's stream
+    (workspaces sized for the concurrent layout): results still equal the oracle."""
+    cfg, ctx, o = ctxs(orc, "T12")
+    keys = Keys(o, cfg.seed + 95)
+    level, rots = 5, [1, 2, 3, 4, 5, 6, 7]
+    ks = [S.galois_rot(r, cfg.log_n) for r in rots]
+    evks = [keys.rot(k) for k in ks]
+    g = S.rng(496)
+    c0, c1 = S.uniform_limbs(g, o.q[: level + 1], o.n), S.uniform_limbs(g, o.q[: level + 1], o.n)
+    outs0 = [empty_dev(c0.shape) for _ in ks]
+    outs1 = [empty_dev(c0.shape) for _ in ks]
+    ws = ctx.workspace(H.OP_ROTATE_HOISTED, level, len(ks))
+    H.prof_enable(True)
+    try:
+        H.rotate_hoisted(ctx, to_dev(c0), to_dev(c1), level, ks, [to_dev(e) for e in evks], outs0, outs1, ws)
+        torch.cuda.synchronize()
+    finally:
+        H.prof_enable(False)
+        H.prof_read()
+    w0, w1 = o.rotate_hoisted(c0, c1, evks, level, ks)
+    for r in range(len(ks)):
+        assert (to_host(outs0[r]) == w0[r]).all() and (to_host(outs1[r]) == w1[r]).all(), r
