@@ -203,7 +203,7 @@ hks_status hks_pt_weighted_sum(const hks_ctx *ctx, uint32_t nterm, const uint64_
  *   host arrays (n1-1 and n2-1 entries).  out0/out1 [l+1][N] must not overlap the inputs or ws.
  *   ws: hks_linear_transform_workspace_bytes(ctx, level, n1) bytes.
  *   Stream semantics: with n2 > 2 the independent giant steps are spread round-robin over `stream` and
- *   the context's two side streams (forked from `stream` by an event, joined back before the last
+ *   the context's three side streams (forked from `stream` by an event, joined back before the last
  *   accumulation), so the whole call stays ordered on `stream` and can be captured into a CUDA graph. */
 hks_status hks_linear_transform(const hks_ctx *ctx, const uint64_t *c0, const uint64_t *c1, uint32_t level,
                                 uint32_t n1, uint32_t n2, const uint64_t *baby_galois,
