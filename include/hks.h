@@ -223,7 +223,7 @@ hks_status hks_automorph(const hks_ctx *ctx, const uint64_t *in, uint32_t nlimbs
  *   out0[r] = pi_k(c0) + ModDown(acc0_r), out1[r] = ModDown(acc1_r), acc_r = KIP(ext, evk[r], k_r).
  *   ws   hks_workspace_bytes(ctx, HKS_OP_ROTATE_HOISTED, level, nrot) bytes.
  *   Stream semantics: with nrot > 1 the rotations after the shared ModUp are split over `stream` and the
- *   context's two side streams (event fork / join); the call stays ordered on `stream`, graph-capturable. */
+ *   context's three side streams (event fork / join); the call stays ordered on `stream`, graph-capturable. */
 hks_status hks_rotate_hoisted(const hks_ctx *ctx, const uint64_t *c0, const uint64_t *c1, uint32_t level,
                               uint32_t nrot, const uint64_t *galois, const uint64_t *const *evk,
                               uint64_t *const *out0, uint64_t *const *out1, void *ws, void *stream);
@@ -234,7 +234,7 @@ hks_status hks_rotate_hoisted(const hks_ctx *ctx, const uint64_t *c0, const uint
  * ciphertext i [l+1][N] EVAL; out0/out1[i * nrot + r] receive rotation r of ciphertext i (as in
  * hks_rotate_hoisted).  beta(level) <= 4.  ws: hks_rotate_hoisted_batch_workspace_bytes(ctx, nct, level).
  * Stream semantics: after the ModUps the nrot rotations are spread round-robin over `stream` and the
- * context's two side streams (event fork / join), so the call stays ordered on `stream` and is graph-capturable. */
+ * context's three side streams (event fork / join), so the call stays ordered on `stream` and is graph-capturable. */
 hks_status hks_rotate_hoisted_batch(const hks_ctx *ctx, uint32_t nct, const uint64_t *const *c0,
                                     const uint64_t *const *c1, uint32_t level, uint32_t nrot,
                                     const uint64_t *galois, const uint64_t *const *evk, uint64_t *const *out0,
