@@ -817,8 +817,9 @@ def main():
                                            if shard_mode != "none" else
                                            f"{'replicas' if cfg.name == 'C5' else 'ciphertexts sharded'} over {world} GPU(s)"),
                            "l2": wl.l2_note(),
-                           "batch": (f"{wl.conc} ciphertexts per step, each KeySwitched on its own CUDA stream"
-                                     if getattr(wl, "conc", 1) > 1 else "1 ciphertext per step")},
+                           **({"batch": (f"{wl.conc} ciphertexts per step, each KeySwitched on its own CUDA stream"
+                                         if wl.conc > 1 else "1 ciphertext per step")}
+                              if isinstance(wl, KSWorkload) else {})},
                 "gpu_launches": launches, "clocks": clk.summary(),
                 "launch_mode": (f"CUDA graph replay of the C-ABI calls ({glaunch[0]} kernels per step)" if graphs
                                 else "direct C-ABI calls")}
