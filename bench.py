@@ -12,7 +12,8 @@ throughput-with-batch setting of the paper's throughput figures; `--streams 1` =
 
 Timing: W untimed steps, then K steps between barrier + synchronize, CUDA events on the launch
 stream, max over ranks.  L2: every step uses the next of `--sets` distinct (ciphertext, key) sets
-(total > 4x the 126 MB L2), so nothing is L2-resident from the previous step.
+(total > 4x the device's L2, read from cudaDevAttrL2CacheSize), so nothing is L2-resident from the
+previous step.
 Inputs are seeded synthetic residues (timing is data-independent; bit-exactness with real keys is
 the job of tests/test_gpu_parity.py).  `--impl reference` times the CPU oracle (oracle/) instead.
 """
@@ -50,6 +51,9 @@ def parse():
     ap.add_argument("--quick", action="store_true", help="skip e2e / NTT / profile legs (for ncu runs)")
     ap.add_argument("--no-graph", action="store_true",
                     help="time direct C-ABI calls instead of CUDA-graph replays of the same calls")
+    ap.add_argument("--dump", default=None,
+                    help="directory: after the timed region every rank saves one step's inputs and outputs (.npy) "
+                         "for an offline oracle check (tests/test_multirank.py)")
     ap.add_argument("--shard", default="auto", choices=["auto", "none", "nccl", "peer"],
                     help="C4 limb sharding: nccl = two NCCL all-gathers per KeySwitch; peer = the exchanges fused "
                          "into the base conversions over NVLink symmetric memory; none = one KeySwitch per GPU; "
@@ -64,6 +68,24 @@ def peaks():
             d = json.load(f)
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def tensor_peak():
+    """Dense u8 tensor-core ops/s: the measured bf16 burst rate (MEASURED_PEAKS.json) x 2, the nominal int8 /
+    bf16 ratio of B200_PROFILING.md; fallback: the nominal 4.5 POPS."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return 2e12 * float(d["bf16_tflops"]), "measured bf16 x 2 (MEASURED_PEAKS.json bf16_tflops)"
+    return 4.5e15, "nominal int8 dense"
+
+
+L2_BYTES = 126 * 1024 * 1024   # replaced in main() by the device's cudaDevAttrL2CacheSize
+
+
+def l2_str():
+    return f"{L2_BYTES / 2**20:.0f} MiB L2"
 
 
 def mul_peak():
@@ -200,14 +222,37 @@ def oracle_ks_timer(cfg, level, seed):
     return one
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def cpu_baseline(cfg, level, budget_s=20.0):
+    """The oracle as it stands on the host: all cores (OpenMP over limbs / coefficients), then one KeySwitch
+    single-threaded (SURVEY.md §8(d) oracle timing)."""
+    import oracle
     one = oracle_ks_timer(cfg, level, 7)
     ts = [one()]
     while sum(ts) < budget_s * 0.5 and len(ts) < 10:
         ts.append(one())
+    prev = oracle.set_num_threads(1)
+    try:
+        t1 = one()
+    finally:
+        oracle.set_num_threads(prev)
     return {"value": len(ts) / sum(ts), "unit": "KeySwitch/s", "cores": cpu_cores(), "kind": "oracle",
-            "sample": f"{len(ts)} full KeySwitches of {cfg.name} at level {level} (oracle/oracle.c, %-on-u128, "
-                      f"OpenMP over limbs), {sum(ts):.1f} s"}
+            "cpu_model": cpu_model(),
+            "single_thread": {"value": 1.0 / t1, "unit": "KeySwitch/s", "cores": 1, "seconds": t1},
+            "sample": f"{len(ts)} full KeySwitches of {cfg.name} at level {level} on {cpu_cores()} threads "
+                      f"(oracle/oracle.c, %-on-u128, OpenMP over limbs), {sum(ts):.1f} s; then 1 KeySwitch on 1 "
+                      f"thread, {t1:.1f} s"}
 
 
 def run_reference(args, cfg, level):
@@ -282,8 +327,16 @@ class KSWorkload:
 
     def l2_note(self):
         c, l = self.cfg, self.level
-        mb = self.nsets * (2 * c.dnum * (c.L + 1 + c.K) + 2 * (l + 1)) * c.n * 8 / 1e6
-        return f"{self.nsets} rotating (ct, key) sets, {mb:.0f} MB > 4x 126 MB L2"
+        b = self.nsets * (2 * c.dnum * (c.L + 1 + c.K) + 2 * (l + 1)) * c.n * 8
+        rel = ">" if b > 4 * L2_BYTES else "<="
+        return f"{self.nsets} rotating (ct, key) sets, {b / 2**20:.0f} MiB {rel} 4x the {l2_str()}"
+
+    def dump(self, d, rank):
+        s = self.sets[0]
+        self.step1(0)
+        import torch
+        torch.cuda.synchronize()
+        save_npy(d, rank, level=self.level, c0=s["c0"], c1=s["c1"], evk=s["evk"], out0=s["out0"], out1=s["out1"])
 
     # e2e: every step copies its ciphertext (c0, c1) H2D from pinned host memory, runs the KeySwitch
     # and copies (out0, out1) D2H.  Three streams pipeline step i's H2D, step i-1's KeySwitch and
@@ -383,14 +436,24 @@ class C4ShardWorkload:
         self.ks(s["c0"], s["c1"], s["evk"], s["out0"], s["out1"], self.sid)
 
     def alg_bytes(self):
+        """one sharded KeySwitch per step: this rank's share of its algorithmic bytes"""
         c, l = self.cfg, self.level
-        return self.conc * (4 * (l + 1) + 2 * c.beta(l) * (l + 1 + c.K)) * c.n * 8
+        return (4 * (l + 1) + 2 * c.beta(l) * (l + 1 + c.K)) * c.n * 8 / self.world
 
     def l2_note(self):
         c, l = self.cfg, self.level
-        mb = self.nsets * (2 * c.dnum * (c.L + 1 + c.K) + 2 * (l + 1)) * c.n * 8 / 1e6 / self.world
-        return (f"{self.nsets} rotating (ct, key) sets, {mb:.0f} MB per rank; limbs sharded over {self.world} "
-                f"rank(s), exchange: {'NCCL all-gathers' if self.mode == 'nccl' else 'peer loads in BConv'}")
+        b = self.nsets * (2 * c.dnum * (c.L + 1 + c.K) + 2 * (l + 1)) * c.n * 8 / self.world
+        return (f"{self.nsets} rotating (ct, key) sets, {b / 2**20:.0f} MiB per rank ({l2_str()}); limbs sharded over "
+                f"{self.world} rank(s), exchange: {'NCCL all-gathers' if self.mode == 'nccl' else 'peer loads in BConv'}")
+
+    def dump(self, d, rank):
+        import torch
+        s = self.sets[0]
+        self.step(0)
+        torch.cuda.synchronize()
+        i = self.ks.info
+        save_npy(d, rank, level=self.level, world=self.world, q_lo=i.q_lo, q_hi=i.q_hi, p_lo=i.p_lo, p_hi=i.p_hi,
+                 nq_act=i.nq_act, c0=s["c0"], c1=s["c1"], evk=s["evk"], out0=s["out0"], out1=s["out1"])
 
 
 class C3Workload:
@@ -435,7 +498,17 @@ class C3Workload:
 
     def l2_note(self):
         c = self.cfg
-        return f"8 rotation keys ({8 * 2 * c.dnum * (c.L + 1 + c.K) * c.n * 8 / 1e6:.0f} MB) > 4x 126 MB L2"
+        return f"8 rotation keys ({8 * 2 * c.dnum * (c.L + 1 + c.K) * c.n * 8 / 2**20:.0f} MiB) > 4x the {l2_str()}"
+
+    def dump(self, d, rank):
+        """ciphertext 0 of this rank with rotations 0 and nrot - 1 (their keys and outputs)"""
+        import torch
+        self.step(0)
+        torch.cuda.synchronize()
+        r = [0, self.nrot - 1]
+        save_npy(d, rank, level=self.level, galois=[self.galois[k] for k in r], c0=self.c0s[0], c1=self.c1s[0],
+                 evk=torch.stack([self.evks[k] for k in r]), out0=torch.stack([self.out0[0][k] for k in r]),
+                 out1=torch.stack([self.out1[0][k] for k in r]))
 
 
 class C5Workload:
@@ -534,7 +607,22 @@ class C5Workload:
     def l2_note(self):
         c = self.cfg
         return (f"16 keys ({16 * 2 * c.dnum * (c.L + 1 + c.K) * c.n * 8 / 1e9:.2f} GB) + 64 diagonals "
-                f"({64 * (c.L + 1) * c.n * 8 / 1e9:.2f} GB) >> 126 MB L2")
+                f"({64 * (c.L + 1) * c.n * 8 / 1e9:.2f} GB) >> the {l2_str()}")
+
+
+def save_npy(d, rank, **kw):
+    """one rank's dump: tensors as uint64 .npy, scalars / lists in meta.json (bench.py --dump)"""
+    import numpy as np
+    out = os.path.join(d, f"rank{rank}")
+    os.makedirs(out, exist_ok=True)
+    meta = {}
+    for k, v in kw.items():
+        if hasattr(v, "cpu"):
+            np.save(os.path.join(out, k + ".npy"), v.cpu().numpy().view(np.uint64))
+        else:
+            meta[k] = v
+    with open(os.path.join(out, "meta.json"), "w") as f:
+        json.dump(meta, f)
 
 
 def torch_empty_pinned_like(t):
@@ -555,6 +643,7 @@ def main():
     import torch.distributed as dist
     from paper_2507_04775_b200 import hks as H
 
+    global L2_BYTES
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -564,6 +653,7 @@ def main():
     local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
+    L2_BYTES = int(getattr(torch.cuda.get_device_properties(local), "L2_cache_size", L2_BYTES)) or L2_BYTES
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device(dev))
@@ -662,6 +752,34 @@ def main():
         q = lambda f: per[min(nd - 1, int(f * nd))]
         extra["step_ms"] = {"p10": q(0.1), "median": q(0.5), "p90": q(0.9), "steps": nd}
 
+        # ---- configs[1] as stated: ONE ciphertext per step (no concurrent batch), same sets, graphs, timing
+        if isinstance(wl, KSWorkload) and wl.conc > 1:
+            g1 = []
+            if graphs:
+                for i in range(len(wl.sets)):
+                    g = torch.cuda.CUDAGraph()
+                    ws0 = wl.ws
+                    with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                        s_ = wl.sets[i]
+                        H.keyswitch(ctx, s_["c0"], s_["c1"], level, s_["evk"], s_["out0"], s_["out1"], ws0,
+                                    torch.cuda.current_stream().cuda_stream)
+                    g1.append(g)
+            run1 = (lambda i: g1[i % len(g1)].replay()) if g1 else wl.step1
+            for i in range(max(3, args.warmup)):
+                run1(i)
+            torch.cuda.synchronize()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(args.steps):
+                run1(i)
+            e1.record(stream)
+            e1.synchronize()
+            t1 = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+            extra["single_ciphertext"] = {"value": world / (t1 * 1e-3), "unit": wl.unit, "ms_per_keyswitch": t1,
+                                          "note": "one KeySwitch per step on one stream (BASELINE configs[1] as "
+                                                  "stated); `value` batches --streams ciphertexts per step"}
+
         # ---- per-kernel breakdown: CUDA events recorded by libhks around each launch, same stream
         H.prof_enable(True)
         nprof = max(1, min(args.steps, 100 if cfg.name not in ("C3", "C5") else 5))
@@ -699,6 +817,26 @@ def main():
         alg = wl.alg_bytes()
         extra["step_hbm"] = {"alg_bytes": alg, "achieved_gbs": alg / (ms / args.steps * 1e-3) / 1e9,
                              "frac": alg / (ms / args.steps * 1e-3) / 1e9 / hbm_peak}
+        # ---- step-level roofline: max(T_HBM, T_INT, T_tensor) / T_measured for the unit the
+        # profile pass ran (one KeySwitch for C1/C2/C4, one step otherwise); the pipes overlap, so the bound is
+        # the largest of the three
+        per_ks = isinstance(wl, KSWorkload)
+        t_unit = (ms / args.steps) * 1e-3 / (wl.conc if per_ks else 1)
+        b_unit = alg / (wl.conc if per_ks else 1)
+        m_unit = sum(v[3] for v in prof.values()) / nprof
+        tc_ops = 0.0
+        if per_ks and prof.get("bconv", (0, 0, 0, 1))[3] == 0:      # conversions ran on the tensor cores
+            c_, l_ = cfg, level
+            macs = sum((min((j + 1) * c_.alpha, l_ + 1) - j * c_.alpha) * (l_ + 1 + c_.K - (min((j + 1) * c_.alpha, l_ + 1) - j * c_.alpha))
+                       for j in range(c_.beta(l_))) + 2 * c_.K * (l_ + 1)
+            tc_ops = 2.0 * 64 * macs * c_.n          # u8 products: 8 bytes x 8 byte columns per 60-bit MAC
+        tpk, tpk_src = tensor_peak()
+        tb = {"hbm": b_unit / (hbm_peak * 1e9), "int": m_unit / mpeak, "tensor": tc_ops / tpk}
+        bound = max(tb, key=tb.get)
+        extra["step_roofline"] = {"unit": "KeySwitch" if per_ks else "step", "t_measured_us": 1e6 * t_unit,
+                                  "t_hbm_us": 1e6 * tb["hbm"], "t_int_us": 1e6 * tb["int"],
+                                  "t_tensor_us": 1e6 * tb["tensor"], "bound": bound, "frac": tb[bound] / t_unit,
+                                  "peaks": {"hbm": peak_src, "int": mpeak_src, "tensor": tpk_src}}
 
         # ---- NTT limbs/s: the ModUp NTT batch (beta(l+1+K) - (l+1) limbs), 4 buffers > L2
         beta = cfg.beta(level)
@@ -807,6 +945,8 @@ def main():
             extra["e2e"] = {"value": world * getattr(wl, "e2e_units", wl.units) * e_steps / (et / 1e3), "unit": wl.unit,
                             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e_steps}
 
+    if args.dump and hasattr(wl, "dump"):
+        wl.dump(args.dump, rank)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": wl.unit, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,

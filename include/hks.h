@@ -20,7 +20,11 @@
  *             Extended limb order at level l: Q_0..Q_l, P_0..P_{K-1}.  Key limb index of P_k is
  *             L+1+k.  Digit j = chain limbs [j*alpha, min((j+1)*alpha, l+1)), alpha =
  *             ceil((L+1)/dnum), beta(l) = ceil((l+1)/alpha) (§2.1).
- *   Keys      evk layout [dnum][2][L+1+K][N]: evk[j][0] = b_j, evk[j][1] = a_j, EVAL.
+ *   Keys      evk layout [evk_digits][2][L+1+K][N]: evk[j][0] = b_j, evk[j][1] = a_j, EVAL.  Every call
+ *             that reads a key takes the key's digit count `evk_digits`: the call needs the first
+ *             beta(level) digits, so a key generated with fewer digits than the context's dnum is
+ *             usable at the levels it covers.  evk_digits < beta(level) or > dnum -> HKS_EKEY
+ *             ("ksk digit count < beta"), checked before any launch.
  *   Streams   Every compute call is enqueued on `stream` (a cudaStream_t passed as void*; NULL =
  *             legacy default stream).  Argument errors return synchronously before any launch;
  *             launch failures return HKS_ECUDA; asynchronous device faults surface on the
@@ -51,7 +55,7 @@ typedef enum {
     HKS_ENOTNTT = 3,    /* a modulus is not 1 mod 2N */
     HKS_ERANGE = 4,     /* modulus >= 2^60, log_n outside [10, 17], dnum outside [1, L+1] */
     HKS_EDUP = 5,       /* a modulus appears twice in q || p */
-    HKS_EKEY = 6,       /* evaluation key has fewer digits than beta(level) */
+    HKS_EKEY = 6,       /* evk_digits < beta(level) or > the context's dnum */
     HKS_EGALOIS = 7,    /* Galois element even or >= 2N */
     HKS_ECUDA = 8,      /* a CUDA runtime call or kernel launch failed */
     HKS_ENOMEM = 9,     /* device table allocation failed at context creation */
@@ -63,7 +67,9 @@ typedef enum {
     HKS_OP_MODUP = 0,           /* hks_modup */
     HKS_OP_MODDOWN = 1,         /* hks_moddown */
     HKS_OP_KEYSWITCH = 2,       /* hks_keyswitch */
-    HKS_OP_ROTATE_HOISTED = 3,  /* hks_rotate_hoisted (count = nrot, not needed for sizing) */
+    HKS_OP_ROTATE_HOISTED = 3,  /* hks_rotate_hoisted: count = the largest nrot of any call that will use
+                                   the buffer (the layout has one accumulator region per concurrent
+                                   branch); count = 0 returns the worst case over every nrot */
     HKS_OP_HMULT = 4,           /* hks_hmult */
     HKS_OP_RESCALE = 5          /* hks_rescale (count = npoly; 0 at level 0) */
 } hks_op;
@@ -121,9 +127,13 @@ hks_status hks_ntt_inv(const hks_ctx *ctx, uint64_t *x, const uint32_t *prime_id
  *   out_t = [ sum_i [x_i * qhat_i^-1]_{q_i} * [qhat_i]_t ]_t ,  qhat_i = prod_{m in src, m != i} m
  *   x       [nsrc][N] COEFF, limb i modulo prime src_idx[i];  out [ndst][N] COEFF.
  *   src_idx / dst_idx are host arrays of prime indices; nsrc <= 16, ndst <= 128, src and dst
- *   disjoint.  The result is the unique Eq. 1 value with canonical y_i (SURVEY.md reading 16). */
+ *   disjoint.  The result is the unique Eq. 1 value with canonical y_i (SURVEY.md reading 16).
+ *   ws      hks_bconv_workspace_bytes(ctx, nsrc, ndst) bytes of device memory: the call derives this
+ *           (src, dst) pair's Eq. 1 constants on the device into ws (no allocation, no host->device
+ *           copy, graph-capturable), scales y_i = [x_i qhat_i^-1]_{q_i} into ws, then converts. */
 hks_status hks_bconv(const hks_ctx *ctx, const uint64_t *x, const uint32_t *src_idx, uint32_t nsrc,
-                     const uint32_t *dst_idx, uint32_t ndst, uint64_t *out, void *stream);
+                     const uint32_t *dst_idx, uint32_t ndst, uint64_t *out, void *ws, void *stream);
+size_t hks_bconv_workspace_bytes(const hks_ctx *ctx, uint32_t nsrc, uint32_t ndst);
 
 /* ModUp (§3.6.3): digit decomposition + BConv + NTT.
  *   d    [l+1][N] EVAL at `level` = l.
@@ -135,12 +145,12 @@ hks_status hks_modup(const hks_ctx *ctx, const uint64_t *d, uint32_t level, uint
 
 /* Evaluation-key inner product (§3.6.5 dot-product fusion):
  *   acc[0][t] = sum_{j<beta} D_j[t] * b_j[key(t)],  acc[1][t] = sum_j D_j[t] * a_j[key(t)]  (mod t)
- *   ext     [beta][l+1+K][N] EVAL (hks_modup output).  evk [dnum][2][L+1+K][N], dnum >= beta.
+ *   ext     [beta][l+1+K][N] EVAL (hks_modup output).  evk [evk_digits][2][L+1+K][N].
  *   galois  1 for none; otherwise odd k < 2N and D_j is replaced by its automorphism pi_k
  *           (EVAL permutation, hoisted order; SURVEY.md readings 14-15).
  *   acc     [2][l+1+K][N] EVAL. */
 hks_status hks_ksk_inner_product(const hks_ctx *ctx, const uint64_t *ext, const uint64_t *evk,
-                                 uint32_t level, uint64_t galois, uint64_t *acc, void *stream);
+                                 uint32_t evk_digits, uint32_t level, uint64_t galois, uint64_t *acc, void *stream);
 
 /* ModDown (§3.6.5 "P^-1(x - NTT(x'))"):
  *   acc [l+1+K][N] EVAL -> out [l+1][N] EVAL,
@@ -153,17 +163,19 @@ hks_status hks_moddown(const hks_ctx *ctx, const uint64_t *acc, uint32_t level, 
  *   out0 = c0 + ModDown(acc0), out1 = ModDown(acc1), acc = KIP(ModUp(c1), evk).
  *   Relinearisation of (d0, d1, d2): call with (c0, c1) = (0-or-d0, d2) and add d1 to out1.
  *   c0 may be NULL (then out0 = ModDown(acc0)).  c0, c1, out0, out1: [l+1][N] EVAL.
- *   evk [dnum][2][L+1+K][N]; dnum (the key's digit count) >= beta(level) is implied by the ctx.
+ *   evk [evk_digits][2][L+1+K][N], beta(level) <= evk_digits <= dnum (else HKS_EKEY).
  *   ws   hks_workspace_bytes(ctx, HKS_OP_KEYSWITCH, level, 0) bytes. */
 hks_status hks_keyswitch(const hks_ctx *ctx, const uint64_t *c0, const uint64_t *c1, uint32_t level,
-                         const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws, void *stream);
+                         const uint64_t *evk, uint32_t evk_digits, uint64_t *out0, uint64_t *out1, void *ws,
+                         void *stream);
 
 /* Relinearisation of a tensor-product ciphertext (d0, d1, d2) at `level` (HMult's KeySwitch,
  * PAPER.md:75 Table 1 HMult, PAPER.md:351 HMult fusion):  out0 = d0 + ModDown(acc0),
  * out1 = d1 + ModDown(acc1), acc = KIP(ModUp(d2), evk).  Both additions are fused in the ModDown
  * epilogue.  d0 may be NULL (treated as 0); d1 must not be NULL.  Layouts and ws as hks_keyswitch. */
 hks_status hks_relinearize(const hks_ctx *ctx, const uint64_t *d0, const uint64_t *d1, const uint64_t *d2,
-                           uint32_t level, const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws,
+                           uint32_t level, const uint64_t *evk, uint32_t evk_digits, uint64_t *out0, uint64_t *out1,
+                           void *ws,
                            void *stream);
 
 /* HMult without rescale (Table 1 "HMult"; §3.6.5 HMult fusion; DESIGN.md
@@ -173,7 +185,8 @@ hks_status hks_relinearize(const hks_ctx *ctx, const uint64_t *d0, const uint64_
  * Fused: d2 is formed inside the first INTT pass, d0 / d1 inside the ModDown epilogue.  Outputs must
  * not overlap any input or ws.  ws: hks_workspace_bytes(ctx, HKS_OP_HMULT, level, 0) bytes. */
 hks_status hks_hmult(const hks_ctx *ctx, const uint64_t *a0, const uint64_t *a1, const uint64_t *b0,
-                     const uint64_t *b1, uint32_t level, const uint64_t *evk, uint64_t *out0, uint64_t *out1,
+                     const uint64_t *b1, uint32_t level, const uint64_t *evk, uint32_t evk_digits, uint64_t *out0,
+                     uint64_t *out1,
                      void *ws, void *stream);
 
 /* Rescale of npoly polynomials from level l >= 1 to l - 1 (Table 1 "Rescale after
@@ -208,7 +221,8 @@ hks_status hks_pt_weighted_sum(const hks_ctx *ctx, uint32_t nterm, const uint64_
 hks_status hks_linear_transform(const hks_ctx *ctx, const uint64_t *c0, const uint64_t *c1, uint32_t level,
                                 uint32_t n1, uint32_t n2, const uint64_t *baby_galois,
                                 const uint64_t *const *baby_evk, const uint64_t *giant_galois,
-                                const uint64_t *const *giant_evk, const uint64_t *const *pt, uint64_t *out0,
+                                const uint64_t *const *giant_evk, uint32_t evk_digits, const uint64_t *const *pt,
+                                uint64_t *out0,
                                 uint64_t *out1, void *ws, void *stream);
 size_t hks_linear_transform_workspace_bytes(const hks_ctx *ctx, uint32_t level, uint32_t n1);
 
@@ -225,7 +239,7 @@ hks_status hks_automorph(const hks_ctx *ctx, const uint64_t *in, uint32_t nlimbs
  *   Stream semantics: with nrot > 1 the rotations after the shared ModUp are split over `stream` and the
  *   context's three side streams (event fork / join); the call stays ordered on `stream`, graph-capturable. */
 hks_status hks_rotate_hoisted(const hks_ctx *ctx, const uint64_t *c0, const uint64_t *c1, uint32_t level,
-                              uint32_t nrot, const uint64_t *galois, const uint64_t *const *evk,
+                              uint32_t nrot, const uint64_t *galois, const uint64_t *const *evk, uint32_t evk_digits,
                               uint64_t *const *out0, uint64_t *const *out1, void *ws, void *stream);
 
 
@@ -237,7 +251,8 @@ hks_status hks_rotate_hoisted(const hks_ctx *ctx, const uint64_t *c0, const uint
  * context's three side streams (event fork / join), so the call stays ordered on `stream` and is graph-capturable. */
 hks_status hks_rotate_hoisted_batch(const hks_ctx *ctx, uint32_t nct, const uint64_t *const *c0,
                                     const uint64_t *const *c1, uint32_t level, uint32_t nrot,
-                                    const uint64_t *galois, const uint64_t *const *evk, uint64_t *const *out0,
+                                    const uint64_t *galois, const uint64_t *const *evk, uint32_t evk_digits,
+                                    uint64_t *const *out0,
                                     uint64_t *const *out1, void *ws, void *stream);
 size_t hks_rotate_hoisted_batch_workspace_bytes(const hks_ctx *ctx, uint32_t nct, uint32_t level);
 
@@ -276,7 +291,7 @@ int hks_prof_read(hks_prof_entry *out, int max);
  *   C  hks_shard_ks_moddown_out : BConv P -> owned chain limbs + NTT + (acc - .) P^-1 (+ c0)
  * The result is bit-identical to hks_keyswitch restricted to the owned limbs.
  * Local layouts: c0_loc, c1_loc, out0_loc, out1_loc [nq_act][N] (owned chain limbs <= level, in
- * order); evk_loc [dnum][2][nkey][N] (owned chain limbs of the full chain, then owned special limbs);
+ * order); evk_loc [evk_digits][2][nkey][N] (owned chain limbs of the full chain, then owned special limbs);
  * acc_loc [2][nq_act + (p_hi - p_lo)][N]. */
 typedef struct hks_shard_info {
     uint32_t world, rank, level;
@@ -292,7 +307,7 @@ size_t hks_shard_workspace_bytes(const hks_ctx *ctx, uint32_t level, uint32_t wo
 hks_status hks_shard_ks_modup_in(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
                                  const uint64_t *c1_loc, uint64_t *ysend, void *stream);
 hks_status hks_shard_ks_inner(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
-                              const uint64_t *yall, const uint64_t *c1_loc, const uint64_t *evk_loc,
+                              const uint64_t *yall, const uint64_t *c1_loc, const uint64_t *evk_loc, uint32_t evk_digits,
                               uint64_t *acc_loc, uint64_t *ypsend, void *ws, void *stream);
 hks_status hks_shard_ks_moddown_out(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
                                     const uint64_t *ypall, const uint64_t *acc_loc, const uint64_t *c0_loc,
@@ -311,7 +326,7 @@ hks_status hks_shard_ks_moddown_out(const hks_ctx *ctx, uint32_t level, uint32_t
  * entry, plus those of the all-gather phases. */
 hks_status hks_shard_ks_inner_peer(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
                                    const uint64_t *const *ysend_ranks, const uint64_t *c1_loc,
-                                   const uint64_t *evk_loc, uint64_t *acc_loc, uint64_t *ypsend, void *ws,
+                                   const uint64_t *evk_loc, uint32_t evk_digits, uint64_t *acc_loc, uint64_t *ypsend, void *ws,
                                    void *stream);
 hks_status hks_shard_ks_moddown_out_peer(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
                                          const uint64_t *const *ypsend_ranks, const uint64_t *acc_loc,

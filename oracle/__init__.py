@@ -103,6 +103,16 @@ def _p32(seq) -> tuple:
     return arr, arr.ctypes.data_as(_u32p)
 
 
+def set_num_threads(n: int) -> int:
+    """OpenMP threads of the oracle's parallel loops (independent limbs / coefficients); returns the previous
+    count.  Timing only (bench.py cpu_baseline single-thread leg): results do not depend on it."""
+    L = lib()
+    L.omp_get_max_threads.restype = ctypes.c_int
+    prev = int(L.omp_get_max_threads())
+    L.omp_set_num_threads(ctypes.c_int(int(n)))
+    return prev
+
+
 def is_prime(n: int) -> bool:
     return bool(lib().or_is_prime(n))
 

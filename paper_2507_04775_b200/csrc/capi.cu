@@ -52,7 +52,6 @@ hks_status run_bconv_groups(const hks_ctx *c, std::vector<BconvGroup> &groups, c
         a.out = out;
         a.pc = c->d_pc;
         a.log_n = c->log_n;
-        a.prescale = 0;
         a.lazy_out = 1;   // internal conversions feed the forward NTT, which takes [0, 8p + 2^32)
         a.big = c->all_big ? 1 : 0;
         u32 ns = groups[i].nsrc, k = 0;
@@ -74,7 +73,7 @@ void add_groups(std::vector<BconvGroup> &out, u32 nsrc, const u16 *src_slot, con
         g.ndst = (u32)std::min<size_t>(BC_MAXDST, dst_slot.size() - u0);
         g.mat_stride = stride;
         g.mat = mat + u0;
-        g.matf = matf ? matf + 3 * u0 : nullptr;
+        g.matf = matf ? matf + 3 * u0 : nullptr;   // NULL unless HKS_EXPERIMENTAL uploaded the table
         g.mats = mats ? mats + u0 : nullptr;
         g.matb = matb ? matb + 8 * u0 : nullptr;
         g.mimg = mimg ? mimg + (size_t)bconv_img_words(nsrc) * u0 : nullptr;
@@ -113,8 +112,8 @@ hks_status modup_core(const hks_ctx *c, const u64 *d, u32 level, u64 *ext, u64 *
             T.push(j * ne + t, j * ne + t, c->ext_prime(level, t));
         }
         const size_t off = c->mu_mat_off[(size_t)level * c->dnum + j];
-        add_groups(groups, hi - lo, src, c->d_mu_mat + off, (u32)ds.size(), ds, dp, c->d_mu_matf + 3 * off,
-                   c->d_mu_mats + off, c->d_mu_matb + 8 * off, c->d_mu_img + c->mu_img_off[(size_t)level * c->dnum + j]);
+        add_groups(groups, hi - lo, src, c->d_mu_mat + off, (u32)ds.size(), ds, dp, tab_at(c->d_mu_matf, 3 * off),
+                   c->d_mu_mats + off, tab_at(c->d_mu_matb, 8 * off), c->d_mu_img + c->mu_img_off[(size_t)level * c->dnum + j]);
     }
     st = run_bconv_groups(c, groups, coef, ext, s);
     if (st != HKS_OK) return st;
@@ -221,6 +220,52 @@ size_t rot_batch(const hks_ctx *c, u32 level) {
     return std::max<size_t>(1, std::min<size_t>(NTT_MAXO / 2, HKS_MAXB / (2 * c->np)));
 }
 
+// the key's digit count (include/hks.h "Keys"): a call at `level` reads digits 0..beta(level)-1
+hks_status check_evk(const hks_ctx *c, u32 evk_digits, u32 level, const char *where) {
+    if (evk_digits < c->beta(level) || evk_digits > c->dnum)
+        HKS_FAIL(HKS_EKEY, "%s: key has %u digits; level %u needs %u (context dnum %u)", where, evk_digits, level,
+                 c->beta(level), c->dnum);
+    return HKS_OK;
+}
+size_t evk_bytes(const hks_ctx *c, u32 evk_digits) { return (size_t)evk_digits * 2 * (c->nq + c->np) * limb_bytes(c); }
+
+// Fork / join of the context's side streams around the independent branches of one call.  join() -- also
+// run by the destructor when a branch returns an error -- records every forked side stream's join event and
+// makes the caller's stream wait on it, so work already enqueued on a side stream stays ordered before
+// whatever the caller enqueues next, and a stream capture ends joined.
+struct SideFork {
+    const hks_ctx *c;
+    cudaStream_t s;
+    int nb = 1;
+    bool joined = true;
+    std::unique_lock<std::recursive_mutex> lk;
+    SideFork(const hks_ctx *c_, cudaStream_t s_) : c(c_), s(s_), lk(c_->side_mu, std::defer_lock) {}
+    cudaStream_t stream(int b) const { return b == 0 ? s : c->side[b - 1]; }
+    hks_status fork(int n, const char *where) {
+        if (n <= 1) return HKS_OK;
+        lk.lock();
+        if (cudaEventRecord(c->ev_fork, s) != cudaSuccess) HKS_FAIL(HKS_ECUDA, "%s: fork event record", where);
+        joined = false;
+        for (nb = 1; nb < n; nb++)
+            if (cudaStreamWaitEvent(c->side[nb - 1], c->ev_fork, 0) != cudaSuccess) HKS_FAIL(HKS_ECUDA, "%s: fork wait", where);
+        return HKS_OK;
+    }
+    bool join_quiet() {
+        if (joined) return true;
+        joined = true;
+        bool ok = true;
+        for (int b = 1; b < nb; b++)
+            ok &= cudaEventRecord(c->ev_join[b - 1], c->side[b - 1]) == cudaSuccess &&
+                  cudaStreamWaitEvent(s, c->ev_join[b - 1], 0) == cudaSuccess;
+        return ok;
+    }
+    hks_status join(const char *where) {
+        if (!join_quiet()) HKS_FAIL(HKS_ECUDA, "%s: join", where);
+        return HKS_OK;
+    }
+    ~SideFork() { (void)join_quiet(); }
+};
+
 hks_status check_galois(const hks_ctx *c, u64 g) {
     if ((g & 1) == 0 || g >= 2 * (u64)c->n) HKS_FAIL(HKS_EGALOIS, "galois element %llu must be odd and < 2N", (unsigned long long)g);
     return HKS_OK;
@@ -236,7 +281,9 @@ extern "C" size_t hks_workspace_bytes(const hks_ctx *c, hks_op op, uint32_t leve
         case HKS_OP_MODDOWN: return (K + l1) * lb;
         case HKS_OP_KEYSWITCH: return (l1 + beta * ne + 2 * ne + 2 * K + 2 * l1) * lb;
         case HKS_OP_ROTATE_HOISTED: {
-            const size_t nr = count ? count : 1, nb = rot_branches(c, (u32)nr);
+            // count = 0: the worst case over every nrot (all branches, full rotation batches)
+            const size_t nr = count ? count : (size_t)(1 + hks_ctx::NSIDE) * rot_batch(c, level);
+            const size_t nb = rot_branches(c, (u32)nr);
             const size_t rb = std::min<size_t>((nr + nb - 1) / nb, rot_batch(c, level));
             return (l1 + beta * ne + nb * rb * (2 * ne + 2 * K + 2 * l1)) * lb;
         }
@@ -280,121 +327,88 @@ extern "C" hks_status hks_ntt_inv(const hks_ctx *c, uint64_t *x, const uint32_t 
     return run_ntt(c, NTT_INV, L, x, x, nullptr, 0, (cudaStream_t)stream);
 }
 
+namespace {
+// hks_bconv workspace (words): y [nsrc][N] | w, wp [2 * 16] | mat uint2 [nsrc][ndst] | img [ndst][img(nsrc)],
+// every region 128-byte aligned
+struct BconvWs {
+    size_t y, w, mat, img, total;
+    BconvWs(const hks_ctx *c, u32 nsrc, u32 ndst) {
+        auto up = [](size_t x) { return (x + 15) & ~(size_t)15; };
+        y = 0;
+        w = up((size_t)nsrc * c->n);
+        mat = w + up(2 * BC_MAXSRC);
+        img = mat + up((size_t)nsrc * ndst);
+        total = img + up((size_t)ndst * bconv_img_words(nsrc));
+    }
+};
+}  // namespace
+
+extern "C" size_t hks_bconv_workspace_bytes(const hks_ctx *c, uint32_t nsrc, uint32_t ndst) {
+    if (!c || nsrc < 1 || nsrc > BC_MAXSRC || ndst < 1 || ndst > 2 * BC_MAXDST) return 0;
+    return BconvWs(c, nsrc, ndst).total * sizeof(u64);
+}
+
 extern "C" hks_status hks_bconv(const hks_ctx *c, const uint64_t *x, const uint32_t *src_idx, uint32_t nsrc,
-                                const uint32_t *dst_idx, uint32_t ndst, uint64_t *out, void *stream) {
+                                const uint32_t *dst_idx, uint32_t ndst, uint64_t *out, void *ws, void *stream) {
     hks_status st = check_ctx(c);
     if (st != HKS_OK) return st;
-    if (!x || !out || !src_idx || !dst_idx) HKS_FAIL(HKS_EINVAL, "bconv: NULL argument");
+    if (!x || !out || !src_idx || !dst_idx || !ws) HKS_FAIL(HKS_EINVAL, "bconv: NULL argument");
     if (nsrc < 1 || nsrc > BC_MAXSRC || ndst < 1 || ndst > 2 * BC_MAXDST)
         HKS_FAIL(HKS_EINVAL, "bconv: nsrc must be in [1,%d], ndst in [1,%d]", BC_MAXSRC, 2 * BC_MAXDST);
     const size_t lb = limb_bytes(c);
-    if (overlap(x, nsrc * lb, out, ndst * lb)) HKS_FAIL(HKS_EINVAL, "bconv: out overlaps x");
+    const BconvWs L(c, nsrc, ndst);
+    if (overlap(x, nsrc * lb, out, ndst * lb) || overlap(ws, L.total * 8, out, ndst * lb) ||
+        overlap(ws, L.total * 8, x, nsrc * lb))
+        HKS_FAIL(HKS_EINVAL, "bconv: buffers overlap");
     const u32 nm = (u32)c->primes.size();
+    u64 sp[BC_MAXSRC], dp[2 * BC_MAXDST];
     for (u32 i = 0; i < nsrc; i++) {
         if (src_idx[i] >= nm) HKS_FAIL(HKS_EINVAL, "bconv: src prime index out of range");
         for (u32 k = 0; k < i; k++)
             if (src_idx[k] == src_idx[i]) HKS_FAIL(HKS_EINVAL, "bconv: repeated source prime");
+        sp[i] = c->primes[src_idx[i]];
     }
     for (u32 u = 0; u < ndst; u++) {
         if (dst_idx[u] >= nm) HKS_FAIL(HKS_EINVAL, "bconv: dst prime index out of range");
         for (u32 i = 0; i < nsrc; i++)
             if (src_idx[i] == dst_idx[u]) HKS_FAIL(HKS_EINVAL, "bconv: source and target bases overlap");
-    }
-    typedef unsigned __int128 u128;
-    auto mm = [](u64 a, u64 b, u64 m) { return (u64)((u128)a * b % m); };
-    auto pw = [&](u64 a, u64 e, u64 m) { u64 r = 1; a %= m; for (; e; e >>= 1, a = mm(a, a, m)) if (e & 1) r = mm(r, a, m); return r; };
-    std::vector<uint2> mat((size_t)nsrc * ndst);
-    BconvGroup proto{};
-    for (u32 i = 0; i < nsrc; i++) {
-        u64 qi = c->primes[src_idx[i]], h = 1;
-        for (u32 k = 0; k < nsrc; k++)
-            if (k != i) h = mm(h, c->primes[src_idx[k]] % qi, qi);
-        u64 w = pw(h, qi - 2, qi);
-        proto.pre_w[i] = w;
-        proto.pre_wp[i] = (u64)(((u128)w << 64) / qi);
-        proto.src_slot[i] = (u16)i;
-        proto.src_prime[i] = (u16)src_idx[i];
-        for (u32 u = 0; u < ndst; u++) {
-            u64 t = c->primes[dst_idx[u]], v = 1;
-            for (u32 k = 0; k < nsrc; k++)
-                if (k != i) v = mm(v, c->primes[src_idx[k]] % t, t);
-            mat[(size_t)i * ndst + u] = make_uint2((u32)(v & 0x3fffffffu), (u32)(v >> 30));
-        }
+        dp[u] = c->primes[dst_idx[u]];
     }
     DevGuard g(c->device);
     cudaStream_t s = (cudaStream_t)stream;
-    if (c->all_big && bconv_tc_enabled() && bconv_tc_large(c->log_n, 1)) {
-        // tensor-core path (the hot path's kernel): y_i = [x_i qhat_i^-1]_{q_i} into a temporary, then
-        // k_bconv_tc with this call's byte-column words and B-operand image
-        std::vector<u64> matb, img, w(nsrc), wp(nsrc), pp(nsrc);
-        matb.reserve((size_t)nsrc * ndst * 8);
-        for (u32 i = 0; i < nsrc; i++) {
-            w[i] = proto.pre_w[i];
-            wp[i] = proto.pre_wp[i];
-            pp[i] = c->primes[src_idx[i]];
-            for (u32 u = 0; u < ndst; u++) {
-                const uint2 m2 = mat[(size_t)i * ndst + u];
-                push_bytecols(matb, (u64)m2.x | ((u64)m2.y << 30), c->primes[dst_idx[u]]);
-            }
-        }
-        bconv_image(matb.data(), nsrc, ndst, img);
-        u64 *dy = nullptr, *dmb = nullptr, *dimg = nullptr;
-        HKS_CUDA(cudaMallocAsync((void **)&dy, (size_t)nsrc * c->n * 8, s));
-        HKS_CUDA(cudaMallocAsync((void **)&dmb, matb.size() * 8, s));
-        HKS_CUDA(cudaMallocAsync((void **)&dimg, img.size() * 8, s));
-        HKS_CUDA(cudaMemcpyAsync(dmb, matb.data(), matb.size() * 8, cudaMemcpyHostToDevice, s));
-        HKS_CUDA(cudaMemcpyAsync(dimg, img.data(), img.size() * 8, cudaMemcpyHostToDevice, s));
-        st = launch_limb_scale(x, dy, nsrc, w.data(), wp.data(), pp.data(), c->log_n, s);
-        for (u32 u0 = 0; st == HKS_OK && u0 < ndst; u0 += BC_MAXDST) {
-            BconvArgs a{};
-            a.in = dy;
-            a.out = out;
-            a.pc = c->d_pc;
-            a.log_n = c->log_n;
-            a.big = 1;
-            a.ngroups = 1;
-            a.g[0] = proto;
-            a.g[0].nsrc = nsrc;
-            a.g[0].ndst = std::min<u32>(BC_MAXDST, ndst - u0);
-            a.g[0].mat_stride = ndst;
-            a.g[0].matb = dmb + 8 * (size_t)u0;
-            a.g[0].mimg = dimg + (size_t)bconv_img_words(nsrc) * u0;
-            for (u32 u = 0; u < a.g[0].ndst; u++) {
-                a.g[0].dst_slot[u] = (u16)(u0 + u);
-                a.g[0].dst_prime[u] = (u16)dst_idx[u0 + u];
-            }
-            st = launch_bconv(a, BC_MAXDST, s);
-        }
-        cudaFreeAsync(dy, s);
-        cudaFreeAsync(dmb, s);
-        cudaFreeAsync(dimg, s);
-        return st;
-    }
-    uint2 *dmat = nullptr;
-    HKS_CUDA(cudaMallocAsync((void **)&dmat, mat.size() * sizeof(uint2), s));
-    HKS_CUDA(cudaMemcpyAsync(dmat, mat.data(), mat.size() * sizeof(uint2), cudaMemcpyHostToDevice, s));
+    u64 *w64 = (u64 *)ws;
+    u64 *y = w64 + L.y, *w = w64 + L.w, *img = w64 + L.img;
+    uint2 *mat = reinterpret_cast<uint2 *>(w64 + L.mat);
+    // constants (device), y_i = [x_i qhat_i^-1]_{q_i} (canonical, reading 16), then the conversion kernel the
+    // hot path uses for this shape (tcgen05 for large rings with primes > 2^49, else the integer pipe)
+    if ((st = launch_bconv_prep(sp, nsrc, dp, ndst, w, mat, img, s)) != HKS_OK) return st;
+    if ((st = launch_limb_scale(x, y, nsrc, w, sp, c->log_n, s)) != HKS_OK) return st;
     for (u32 u0 = 0; u0 < ndst; u0 += BC_MAXDST) {
         BconvArgs a{};
-        a.in = x;
+        a.in = y;
         a.out = out;
         a.pc = c->d_pc;
         a.log_n = c->log_n;
-        a.prescale = 1;
+        a.lazy_out = 0;
+        a.big = c->all_big ? 1 : 0;
         a.ngroups = 1;
-        a.g[0] = proto;
-        a.g[0].nsrc = nsrc;
-        a.g[0].ndst = std::min<u32>(BC_MAXDST, ndst - u0);
-        a.g[0].mat = dmat + u0;
-        a.g[0].mat_stride = ndst;
-        for (u32 u = 0; u < a.g[0].ndst; u++) {
-            a.g[0].dst_slot[u] = (u16)(u0 + u);
-            a.g[0].dst_prime[u] = (u16)dst_idx[u0 + u];
+        BconvGroup &G = a.g[0];
+        G.nsrc = nsrc;
+        G.ndst = std::min<u32>(BC_MAXDST, ndst - u0);
+        G.mat_stride = ndst;
+        G.mat = mat + u0;
+        G.mimg = img + (size_t)bconv_img_words(nsrc) * u0;
+        for (u32 i = 0; i < nsrc; i++) {
+            G.src_slot[i] = (u16)i;
+            G.src_prime[i] = (u16)src_idx[i];
         }
-        st = launch_bconv(a, BC_MAXDST, s);
-        if (st != HKS_OK) break;
+        for (u32 u = 0; u < G.ndst; u++) {
+            G.dst_slot[u] = (u16)(u0 + u);
+            G.dst_prime[u] = (u16)dst_idx[u0 + u];
+        }
+        if ((st = launch_bconv(a, BC_MAXDST, s)) != HKS_OK) return st;
     }
-    cudaFreeAsync(dmat, s);
-    return st;
+    return HKS_OK;
 }
 
 extern "C" hks_status hks_modup(const hks_ctx *c, const uint64_t *d, uint32_t level, uint64_t *ext, void *ws,
@@ -420,15 +434,16 @@ extern "C" hks_status hks_modup(const hks_ctx *c, const uint64_t *d, uint32_t le
 }
 
 extern "C" hks_status hks_ksk_inner_product(const hks_ctx *c, const uint64_t *ext, const uint64_t *evk,
-                                            uint32_t level, uint64_t galois, uint64_t *acc, void *stream) {
+                                            uint32_t evk_digits, uint32_t level, uint64_t galois, uint64_t *acc,
+                                            void *stream) {
     hks_status st = check_ctx(c);
     if (st != HKS_OK) return st;
     if (!ext || !evk || !acc) HKS_FAIL(HKS_EINVAL, "ksk_inner_product: NULL argument");
     if (level > c->L()) HKS_FAIL(HKS_EINVAL, "ksk_inner_product: level %u > L", level);
     if (galois != 1 && (st = check_galois(c, galois)) != HKS_OK) return st;
+    if ((st = check_evk(c, evk_digits, level, "ksk_inner_product")) != HKS_OK) return st;
     const size_t lb = limb_bytes(c), ne = c->ne(level);
-    if (overlap(ext, c->beta(level) * ne * lb, acc, 2 * ne * lb) ||
-        overlap(evk, (size_t)c->dnum * 2 * (c->nq + c->np) * lb, acc, 2 * ne * lb))
+    if (overlap(ext, c->beta(level) * ne * lb, acc, 2 * ne * lb) || overlap(evk, evk_bytes(c, evk_digits), acc, 2 * ne * lb))
         HKS_FAIL(HKS_EINVAL, "ksk_inner_product: acc overlaps an input");
     DevGuard g(c->device);
     return kip_core(c, ext, nullptr, evk, level, galois, acc, (cudaStream_t)stream);
@@ -450,37 +465,38 @@ extern "C" hks_status hks_moddown(const hks_ctx *c, const uint64_t *acc, uint32_
 }
 
 static hks_status keyswitch_impl(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, const uint64_t *add1,
-                                  uint32_t level, const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws,
-                                  void *stream, const uint64_t *const *tensor = nullptr);
+                                  uint32_t level, const uint64_t *evk, uint32_t evk_digits, uint64_t *out0,
+                                  uint64_t *out1, void *ws, void *stream, const uint64_t *const *tensor = nullptr);
 
 extern "C" hks_status hks_keyswitch(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, uint32_t level,
-                                    const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws, void *stream) {
-    return keyswitch_impl(c, c0, c1, nullptr, level, evk, out0, out1, ws, stream);
+                                    const uint64_t *evk, uint32_t evk_digits, uint64_t *out0, uint64_t *out1, void *ws,
+                                    void *stream) {
+    return keyswitch_impl(c, c0, c1, nullptr, level, evk, evk_digits, out0, out1, ws, stream);
 }
 
 extern "C" hks_status hks_relinearize(const hks_ctx *c, const uint64_t *d0, const uint64_t *d1, const uint64_t *d2,
-                                      uint32_t level, const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws,
-                                      void *stream) {
+                                      uint32_t level, const uint64_t *evk, uint32_t evk_digits, uint64_t *out0,
+                                      uint64_t *out1, void *ws, void *stream) {
     if (!d1) HKS_FAIL(HKS_EINVAL, "relinearize: NULL d1");
     if (c && level <= c->L() && (overlap(d1, (level + 1) * limb_bytes(c), out0, (level + 1) * limb_bytes(c)) ||
                                  overlap(d1, (level + 1) * limb_bytes(c), out1, (level + 1) * limb_bytes(c))))
         HKS_FAIL(HKS_EINVAL, "relinearize: d1 overlaps an output");
-    return keyswitch_impl(c, d0, d2, d1, level, evk, out0, out1, ws, stream);
+    return keyswitch_impl(c, d0, d2, d1, level, evk, evk_digits, out0, out1, ws, stream);
 }
 
 static hks_status keyswitch_impl(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, const uint64_t *add1,
-                                  uint32_t level, const uint64_t *evk, uint64_t *out0, uint64_t *out1, void *ws,
-                                  void *stream, const uint64_t *const *tensor) {
+                                  uint32_t level, const uint64_t *evk, uint32_t evk_digits, uint64_t *out0,
+                                  uint64_t *out1, void *ws, void *stream, const uint64_t *const *tensor) {
     hks_status st = check_ctx(c);
     if (st != HKS_OK) return st;
     if (!c1 || !evk || !out0 || !out1 || !ws) HKS_FAIL(HKS_EINVAL, "keyswitch: NULL argument");
     if (level > c->L()) HKS_FAIL(HKS_EINVAL, "keyswitch: level %u > L", level);
-    if (c->beta(level) > c->dnum) HKS_FAIL(HKS_EKEY, "keyswitch: key has fewer digits than beta");
+    if ((st = check_evk(c, evk_digits, level, "keyswitch")) != HKS_OK) return st;
     const size_t lb = limb_bytes(c), l1 = level + 1, ne = c->ne(level), beta = c->beta(level);
     const size_t wsb = hks_workspace_bytes(c, tensor ? HKS_OP_HMULT : HKS_OP_KEYSWITCH, level, 0);
     const void *ins[6] = {c0, c1, evk, tensor ? tensor[1] : nullptr, tensor ? tensor[2] : nullptr,
                           tensor ? tensor[3] : nullptr};
-    size_t insz[6] = {l1 * lb, l1 * lb, (size_t)c->dnum * 2 * (c->nq + c->np) * lb, l1 * lb, l1 * lb, l1 * lb};
+    size_t insz[6] = {l1 * lb, l1 * lb, evk_bytes(c, evk_digits), l1 * lb, l1 * lb, l1 * lb};
     void *outs_[3] = {out0, out1, ws};
     size_t outsz[3] = {l1 * lb, l1 * lb, wsb};
     for (int i = 0; i < 6; i++)
@@ -517,12 +533,12 @@ static hks_status keyswitch_impl(const hks_ctx *c, const uint64_t *c0, const uin
 }
 
 extern "C" hks_status hks_hmult(const hks_ctx *c, const uint64_t *a0, const uint64_t *a1, const uint64_t *b0,
-                                const uint64_t *b1, uint32_t level, const uint64_t *evk, uint64_t *out0,
-                                uint64_t *out1, void *ws, void *stream) {
+                                const uint64_t *b1, uint32_t level, const uint64_t *evk, uint32_t evk_digits,
+                                uint64_t *out0, uint64_t *out1, void *ws, void *stream) {
     if (!a0 || !a1 || !b0 || !b1) HKS_FAIL(HKS_EINVAL, "hmult: NULL ciphertext half");
     const uint64_t *tensor[4] = {a0, a1, b0, b1};
     // the KeySwitch input is d2 = a1 * b1 (first factor a1 passed as c1); a0 and c0 = NULL
-    return keyswitch_impl(c, a0, a1, nullptr, level, evk, out0, out1, ws, stream, tensor);
+    return keyswitch_impl(c, a0, a1, nullptr, level, evk, evk_digits, out0, out1, ws, stream, tensor);
 }
 
 extern "C" hks_status hks_rescale(const hks_ctx *c, const uint64_t *x, uint32_t npoly, uint32_t level, uint64_t *out,
@@ -562,12 +578,14 @@ extern "C" hks_status hks_automorph(const hks_ctx *c, const uint64_t *in, uint32
 
 extern "C" hks_status hks_rotate_hoisted(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, uint32_t level,
                                          uint32_t nrot, const uint64_t *galois, const uint64_t *const *evk,
-                                         uint64_t *const *out0, uint64_t *const *out1, void *ws, void *stream) {
+                                         uint32_t evk_digits, uint64_t *const *out0, uint64_t *const *out1, void *ws,
+                                         void *stream) {
     hks_status st = check_ctx(c);
     if (st != HKS_OK) return st;
     if (!c0 || !c1 || !ws || (nrot && (!galois || !evk || !out0 || !out1))) HKS_FAIL(HKS_EINVAL, "rotate_hoisted: NULL argument");
     if (level > c->L()) HKS_FAIL(HKS_EINVAL, "rotate_hoisted: level %u > L", level);
     if (nrot == 0) return HKS_OK;
+    if ((st = check_evk(c, evk_digits, level, "rotate_hoisted")) != HKS_OK) return st;
     const size_t lb = limb_bytes(c), l1 = level + 1, ne = c->ne(level), beta = c->beta(level);
     const size_t wsb = hks_workspace_bytes(c, HKS_OP_ROTATE_HOISTED, level, nrot);
     for (u32 r = 0; r < nrot; r++) {
@@ -592,15 +610,10 @@ extern "C" hks_status hks_rotate_hoisted(const hks_ctx *c, const uint64_t *c0, c
     const u32 per = (nrot + nb - 1) / nb;
     const u32 RB = (u32)std::min<size_t>(per, rot_batch(c, level));
     const size_t bw = (size_t)RB * (2 * ne + 2 * c->np + 2 * l1) * c->n;   // words per branch
-    std::unique_lock<std::recursive_mutex> lk(c->side_mu, std::defer_lock);
-    if (nb > 1) {
-        lk.lock();
-        if (cudaEventRecord(c->ev_fork, s) != cudaSuccess) HKS_FAIL(HKS_ECUDA, "rotate_hoisted: event record");
-        for (u32 b = 1; b < nb; b++)
-            if (cudaStreamWaitEvent(c->side[b - 1], c->ev_fork, 0) != cudaSuccess) HKS_FAIL(HKS_ECUDA, "rotate_hoisted: wait");
-    }
+    SideFork fk(c, s);
+    if ((st = fk.fork((int)nb, "rotate_hoisted")) != HKS_OK) return st;
     for (u32 b = 0; b < nb; b++) {
-        const cudaStream_t bs = b == 0 ? s : c->side[b - 1];
+        const cudaStream_t bs = fk.stream((int)b);
         u64 *acc = ext + beta * ne * c->n + b * bw;
         u64 *md = acc + (size_t)RB * 2 * ne * c->n;
         const u32 rend = std::min(nrot, (b + 1) * per);
@@ -624,16 +637,12 @@ extern "C" hks_status hks_rotate_hoisted(const hks_ctx *c, const uint64_t *c0, c
                 return st;
         }
     }
-    for (u32 b = 1; b < nb; b++)
-        if (cudaEventRecord(c->ev_join[b - 1], c->side[b - 1]) != cudaSuccess ||
-            cudaStreamWaitEvent(s, c->ev_join[b - 1], 0) != cudaSuccess)
-            HKS_FAIL(HKS_ECUDA, "rotate_hoisted: join");
-    return HKS_OK;
+    return fk.join("rotate_hoisted");
 }
 
 extern "C" hks_status hks_rotate_hoisted_batch(const hks_ctx *c, uint32_t nct, const uint64_t *const *c0,
                                                const uint64_t *const *c1, uint32_t level, uint32_t nrot,
-                                               const uint64_t *galois, const uint64_t *const *evk,
+                                               const uint64_t *galois, const uint64_t *const *evk, uint32_t evk_digits,
                                                uint64_t *const *out0, uint64_t *const *out1, void *ws, void *stream) {
     hks_status st = check_ctx(c);
     if (st != HKS_OK) return st;
@@ -643,6 +652,9 @@ extern "C" hks_status hks_rotate_hoisted_batch(const hks_ctx *c, uint32_t nct, c
     if (nct > KIP_MAXCT) HKS_FAIL(HKS_EINVAL, "rotate_hoisted_batch: at most %d ciphertexts per call", KIP_MAXCT);
     const u32 beta = c->beta(level);
     if (beta > 4) HKS_FAIL(HKS_EINVAL, "rotate_hoisted_batch: beta %u > 4", beta);
+    if ((st = check_evk(c, evk_digits, level, "rotate_hoisted_batch")) != HKS_OK) return st;
+    for (u32 r = 0; r < nrot; r++)
+        if (!evk[r]) HKS_FAIL(HKS_EINVAL, "rotate_hoisted_batch: NULL key %u", r);
     for (u32 r = 0; r < nrot; r++)
         if ((st = check_galois(c, galois[r])) != HKS_OK) return st;
     for (u32 i = 0; i < nct * nrot; i++)
@@ -663,17 +675,11 @@ extern "C" hks_status hks_rotate_hoisted_batch(const hks_ctx *c, uint32_t nct, c
     // the rotations are independent after the ModUps: round-robin over the caller's stream and the
     // context's side streams, each branch with its own accumulators and ModDown workspace
     const int nb = (nrot > 1 && c->side[0] && !prof_active()) ? std::min<int>(1 + hks_ctx::NSIDE, (int)nrot) : 1;
-    std::unique_lock<std::recursive_mutex> lk(c->side_mu, std::defer_lock);
-    if (nb > 1) {
-        lk.lock();
-        if (cudaEventRecord(c->ev_fork, s) != cudaSuccess) HKS_FAIL(HKS_ECUDA, "rotate_hoisted_batch: event record");
-        for (int b = 1; b < nb; b++)
-            if (cudaStreamWaitEvent(c->side[b - 1], c->ev_fork, 0) != cudaSuccess)
-                HKS_FAIL(HKS_ECUDA, "rotate_hoisted_batch: wait");
-    }
+    SideFork fk(c, s);
+    if ((st = fk.fork(nb, "rotate_hoisted_batch")) != HKS_OK) return st;
     for (u32 r = 0; r < nrot; r++) {
         const int b = (int)(r % (u32)nb);
-        const cudaStream_t bs = b == 0 ? s : c->side[b - 1];
+        const cudaStream_t bs = fk.stream(b);
         u64 *baccs = b == 0 ? accs : md + mdw + (size_t)(b - 1) * (accw + mdw);
         u64 *bmd = b == 0 ? md : baccs + accw;
         KipMultiArgs a{};
@@ -709,11 +715,7 @@ extern "C" hks_status hks_rotate_hoisted_batch(const hks_ctx *c, uint32_t nct, c
         if ((st = moddown_core(c, baccs, 2 * nct, level, outs.data(), adds.data(), gal.data(), bmd, bs)) != HKS_OK)
             return st;
     }
-    for (int b = 1; b < nb; b++)
-        if (cudaEventRecord(c->ev_join[b - 1], c->side[b - 1]) != cudaSuccess ||
-            cudaStreamWaitEvent(s, c->ev_join[b - 1], 0) != cudaSuccess)
-            HKS_FAIL(HKS_ECUDA, "rotate_hoisted_batch: join");
-    return HKS_OK;
+    return fk.join("rotate_hoisted_batch");
 }
 
 extern "C" size_t hks_rotate_hoisted_batch_workspace_bytes(const hks_ctx *c, uint32_t nct, uint32_t level) {
@@ -784,8 +786,9 @@ extern "C" size_t hks_linear_transform_workspace_bytes(const hks_ctx *c, uint32_
 extern "C" hks_status hks_linear_transform(const hks_ctx *c, const uint64_t *c0, const uint64_t *c1, uint32_t level,
                                            uint32_t n1, uint32_t n2, const uint64_t *baby_galois,
                                            const uint64_t *const *baby_evk, const uint64_t *giant_galois,
-                                           const uint64_t *const *giant_evk, const uint64_t *const *pt,
-                                           uint64_t *out0, uint64_t *out1, void *ws, void *stream) {
+                                           const uint64_t *const *giant_evk, uint32_t evk_digits,
+                                           const uint64_t *const *pt, uint64_t *out0, uint64_t *out1, void *ws,
+                                           void *stream) {
     hks_status st = check_ctx(c);
     if (st != HKS_OK) return st;
     if (!c0 || !c1 || !pt || !out0 || !out1 || !ws) HKS_FAIL(HKS_EINVAL, "linear_transform: NULL argument");
@@ -795,6 +798,7 @@ extern "C" hks_status hks_linear_transform(const hks_ctx *c, const uint64_t *c0,
         HKS_FAIL(HKS_EINVAL, "linear_transform: missing rotation keys");
     for (u32 k = 0; k + 1 < n2; k++)
         if ((st = check_galois(c, giant_galois[k])) != HKS_OK) return st;
+    if ((n1 > 1 || n2 > 1) && (st = check_evk(c, evk_digits, level, "linear_transform")) != HKS_OK) return st;
     for (u32 k = 0; k < n1 * n2; k++)
         if (!pt[k]) HKS_FAIL(HKS_EINVAL, "linear_transform: NULL diagonal %u", k);
     const size_t lb = limb_bytes(c), l1 = level + 1, sz = l1 * lb;
@@ -835,7 +839,7 @@ extern "C" hks_status hks_linear_transform(const hks_ctx *c, const uint64_t *c0,
         }
     }
     // baby steps: one ModUp shared by the n1 - 1 rotations (hoisted)
-    if (n1 > 1 && (st = hks_rotate_hoisted(c, c0, c1, level, n1 - 1, baby_galois, baby_evk, b0.data() + 1,
+    if (n1 > 1 && (st = hks_rotate_hoisted(c, c0, c1, level, n1 - 1, baby_galois, baby_evk, evk_digits, b0.data() + 1,
                                            b1.data() + 1, br[0].rws, stream)) != HKS_OK)
         return st;
     // giant steps: I_i = sum_j pt[i n1 + j] ct_j (fused weighted sum), out += Rot_{g_i}(I_i).  The giant
@@ -843,29 +847,22 @@ extern "C" hks_status hks_linear_transform(const hks_ctx *c, const uint64_t *c0,
     // stream and the side streams (modular sums are exact, so the order of the additions does not matter)
     if ((st = wsum_core(c, n1, pt, x0.data(), x1.data(), level, out0, out1, s)) != HKS_OK) return st;
     const int nb = (n2 > 2 && c->side[0] && !prof_active()) ? std::min<int>(1 + hks_ctx::NSIDE, (int)n2 - 1) : 1;
-    std::unique_lock<std::recursive_mutex> lk(c->side_mu, std::defer_lock);
-    if (nb > 1) {
-        lk.lock();
-        if (cudaEventRecord(c->ev_fork, s) != cudaSuccess) HKS_FAIL(HKS_ECUDA, "linear_transform: event record");
-        for (int b = 1; b < nb; b++)
-            if (cudaStreamWaitEvent(br[b].s, c->ev_fork, 0) != cudaSuccess) HKS_FAIL(HKS_ECUDA, "linear_transform: wait");
-    }
+    SideFork fk(c, s);
+    if ((st = fk.fork(nb, "linear_transform")) != HKS_OK) return st;
     for (u32 i = 1; i < n2; i++) {
         Branch &B = br[(i - 1) % nb];
         if ((st = wsum_core(c, n1, pt + (size_t)i * n1, x0.data(), x1.data(), level, B.i0, B.i1, B.s)) != HKS_OK)
             return st;
         u64 *o0 = B.first ? B.a0 : B.r0, *o1 = B.first ? B.a1 : B.r1;
-        if ((st = hks_rotate_hoisted(c, B.i0, B.i1, level, 1, giant_galois + (i - 1), giant_evk + (i - 1), &o0, &o1,
-                                     B.rws, B.s)) != HKS_OK)
+        if ((st = hks_rotate_hoisted(c, B.i0, B.i1, level, 1, giant_galois + (i - 1), giant_evk + (i - 1), evk_digits,
+                                     &o0, &o1, B.rws, B.s)) != HKS_OK)
             return st;
         if (!B.first && (st = launch_add_ct(B.r0, B.r1, B.a0, B.a1, level + 1, c->log_n, c->d_pc, B.s)) != HKS_OK)
             return st;
         B.first = false;
     }
-    for (int b = 1; b < nb; b++) {
-        if (cudaEventRecord(c->ev_join[b - 1], br[b].s) != cudaSuccess || cudaStreamWaitEvent(s, c->ev_join[b - 1], 0) != cudaSuccess)
-            HKS_FAIL(HKS_ECUDA, "linear_transform: join");
+    if ((st = fk.join("linear_transform")) != HKS_OK) return st;
+    for (int b = 1; b < nb; b++)
         if ((st = launch_add_ct(br[b].a0, br[b].a1, out0, out1, level + 1, c->log_n, c->d_pc, s)) != HKS_OK) return st;
-    }
     return HKS_OK;
 }

@@ -14,6 +14,8 @@
 #include <set>
 #include <thread>
 
+#include <atomic>
+
 #include "internal.h"
 
 typedef unsigned __int128 u128;
@@ -343,7 +345,7 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     // (W_B[0] / W'_A), and the twist between the rounds as Shoup pairs tw[v][o] for round-1 vector class v
     // and output o (forward d_o[v], inverse f_v[o]).
     std::vector<u64> ntt_img_fwd, ntt_img_inv;
-    if (log_n == 16) {
+    if (HKS_EXPERIMENTAL && log_n == 16) {
         ntt_img_fwd.reserve((size_t)nm * NTT16_TAB);
         ntt_img_inv.reserve((size_t)nm * NTT16_TAB);
         for (u32 pi = 0; pi < nm; pi++) {
@@ -436,11 +438,13 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     UP(d_md_scale, md_scale);
     UP(d_md_mat, md_mat);
     UP(d_pinv, pinv);
-    UP(d_mu_matf, mu_matf);
-    UP(d_md_matf, md_matf);
+    if (HKS_EXPERIMENTAL) {   // tables of the FP64-assisted and warp-IMMA base conversions
+        UP(d_mu_matf, mu_matf);
+        UP(d_md_matf, md_matf);
+        UP(d_mu_matb, mu_matb);
+        UP(d_md_matb, md_matb);
+    }
     UP(d_mu_mats, mu_mats);
-    UP(d_mu_matb, mu_matb);
-    UP(d_md_matb, md_matb);
     UP(d_mu_img, mu_img);
     UP(d_md_img, md_img);
     UP(d_ntt_img_fwd, ntt_img_fwd);
@@ -514,14 +518,17 @@ void hks_func_smem(const void *fn, size_t smem) {
 }
 
 int hks_num_sms() {
-    static int nsm[64] = {};
+    // relaxed atomics: concurrent first calls from several host threads may both query the attribute,
+    // and both store the same value
+    static std::atomic<int> nsm[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) dev = 0;
-    if (!nsm[dev]) {
-        int v = 0;
+    int v = nsm[dev].load(std::memory_order_relaxed);
+    if (!v) {
         cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        nsm[dev] = v > 0 ? v : 148;
+        if (v <= 0) v = 148;
+        nsm[dev].store(v, std::memory_order_relaxed);
     }
-    return nsm[dev];
+    return v;
 }

@@ -11,6 +11,10 @@
 #include "../../include/hks.h"
 #include "modarith.cuh"
 
+#ifndef HKS_EXPERIMENTAL
+#define HKS_EXPERIMENTAL 0   // 1: also build the measured-and-rejected kernel variants and
+#endif                       //    their environment switches (tools/build_variant.sh); never the product
+
 typedef uint16_t u16;
 typedef uint8_t u8;
 
@@ -92,8 +96,6 @@ struct BconvGroup {
     const u64 *srcp[BC_MAXSRC];   // non-NULL: absolute address of source i (e.g. a peer GPU's limb over
                                   // NVLink, limb-sharded KeySwitch); NULL: in + src_slot[i] * N
     u16 src_prime[BC_MAXSRC];
-    u64 pre_w[BC_MAXSRC];      // optional prescale y_i = x_i * pre_w (Shoup) -- generic hks_bconv
-    u64 pre_wp[BC_MAXSRC];
     u16 dst_slot[BC_MAXDST];
     u16 dst_prime[BC_MAXDST];
 };
@@ -104,6 +106,10 @@ __host__ __device__ constexpr u32 bconv_img_words(u32 nsrc) { return 2 * ((nsrc 
 
 #define NTT16_IMG 2048   // words per 16 x 16 column-pass matrix image (bconv_img_words(16) * 16 targets)
 #define NTT16_TAB (2 * NTT16_IMG + 512)   // per prime: round-1 image, round-2 image, twist (w, w')[16][16]
+
+// base + off, or NULL for an absent (not uploaded) table
+template <typename T>
+inline T *tab_at(T *base, size_t off) { return base ? base + off : nullptr; }
 
 // host helpers (ctx.cu): the byte-column words of a matrix entry v = [qhat]_t (8 words, word c holding
 // byte c of 2^(8a) v mod t in its byte a) and the k_bconv_tc image of a [nsrc][ntg][8] word table
@@ -116,7 +122,6 @@ struct BconvArgs {
     const PrimeConst *pc;
     u32 log_n;
     u32 ngroups;
-    u32 prescale;              // 1: apply pre_w (inputs raw COEFF), 0: inputs are canonical y_i
     u32 lazy_out;              // 1: outputs in [0, 8t) (consumer: forward NTT), 0: canonical
     u32 big;                   // 1: every prime > 2^49 (required by the tensor-pipe kernels k_bconv_tc / _mma)
     u32 cw;                    // k_bconv_mma: coefficients per CTA (set by the launcher)
@@ -373,7 +378,12 @@ bool ntt_tc_enabled();
 bool bconv_tc_enabled();
 bool bconv_tc_large(u32 log_n, u32 ngroups);
 // out[i] = in[i] * w_i mod p_i (canonical) for n <= 16 limbs (hks_bconv's y_i = x_i [qhat_i]^-1)
-hks_status launch_limb_scale(const u64 *in, u64 *out, u32 nl, const u64 *w, const u64 *wp, const u64 *p, u32 log_n,
+// dw (device): w[0..nl) then the Shoup companions wp[0..nl); p (host): the limbs' primes
+hks_status launch_limb_scale(const u64 *in, u64 *out, u32 nl, const u64 *dw, const u64 *p, u32 log_n, cudaStream_t s);
+// hks_bconv's Eq. 1 constants for one (src, dst) pair, derived on the device (kernels.cu k_bconv_prep):
+// w = [qhat_i^-1]_{q_i} and Shoup companions (2 nsrc words), mat [nsrc][ndst] (lo30, hi30) of [qhat_i]_t,
+// the k_bconv_tc B image img [ndst][bconv_img_words(nsrc)]
+hks_status launch_bconv_prep(const u64 *src, u32 nsrc, const u64 *dst, u32 ndst, u64 *w, uint2 *mat, u64 *img,
                              cudaStream_t s);
 hks_status launch_kip(const KipArgs &a, cudaStream_t s);
 hks_status launch_automorph(const u64 *in, u64 *out, u32 nlimbs, u32 log_n, u64 galois, cudaStream_t s);

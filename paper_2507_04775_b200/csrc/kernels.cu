@@ -17,17 +17,6 @@ __device__ __forceinline__ const u64 *bc_src(const BconvArgs &A, const BconvGrou
     return G.srcp[i] ? G.srcp[i] : A.in + (size_t)G.src_slot[i] * N;
 }
 
-// HKS_BCONV_FP=1 enables the FP64-assisted base conversion (results are identical).  Off by default:
-// on B200 it measured slower (60 vs 52 us for the C2 ModUp conversion) because the 128-bit
-// recombination of the five FP64 limb sums makes it issue-bound (+48 % instructions); see DESIGN.md.
-static bool getenv_fp_enabled() {
-    static const bool on = [] {
-        const char *e = getenv("HKS_BCONV_FP");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
 // ------------------------------------------------------------------------------------------------
 // Base conversion (§3.6.3, eq:conv):  out_t = [ sum_i y_i [qhat_i]_t ]_t.
 // grid.x: coefficient blocks (2 coefficients / thread), grid.y: group (digit or polynomial).
@@ -38,8 +27,8 @@ static bool getenv_fp_enabled() {
 #define HKS_BC_TCH 10
 #endif
 #define BC_TCH HKS_BC_TCH
-template <int NSRC, bool PRESCALE, bool LAZY, int CPT>
-__global__ void __launch_bounds__(256, CPT == 1 ? 5 : 3) k_bconv(const __grid_constant__ BconvArgs A) {
+template <int NSRC, bool LAZY, int CPT>
+__global__ void __launch_bounds__(256, (CPT == 1 && NSRC <= 10) ? 5 : 3) k_bconv(const __grid_constant__ BconvArgs A) {
     pdl_trigger();
     pdl_wait();
     const BconvGroup &G = A.g[blockIdx.y];
@@ -70,13 +59,7 @@ __global__ void __launch_bounds__(256, CPT == 1 ? 5 : 3) k_bconv(const __grid_co
             v[0] = bc_src(A, G, i, N)[x0];
         }
 #pragma unroll
-        for (int c = 0; c < CPT; c++) {
-            if (PRESCALE) {
-                const u64 p = A.pc[G.src_prime[i]].p;
-                v[c] = shoup(v[c], G.pre_w[i], G.pre_wp[i], p);
-            }
-            split30(v[c], yl[i][c], yh[i][c]);
-        }
+        for (int c = 0; c < CPT; c++) split30(v[c], yl[i][c], yh[i][c]);
     }
     for (u32 u = 0; u < nt; u++) {
         Acc30 a[CPT];
@@ -103,7 +86,7 @@ __global__ void __launch_bounds__(256, CPT == 1 ? 5 : 3) k_bconv(const __grid_co
     }
 }
 
-// Karatsuba variant (3 IMAD.WIDE per MAC instead of 4), one coefficient per thread, NSRC <= 12.
+// Karatsuba variant (3 IMAD.WIDE per MAC instead of 4), one coefficient per thread, NSRC <= 11.
 template <int NSRC, bool LAZY>
 __global__ void __launch_bounds__(256, 3) k_bconv_kara(const __grid_constant__ BconvArgs A) {
     pdl_trigger();
@@ -167,6 +150,7 @@ static void bconv_kara_go(const BconvArgs &a, cudaStream_t s) {
     ps.done(words * (double)N * 8.0, macs * (double)N * 4.0);
 }
 
+#if HKS_EXPERIMENTAL
 // ------------------------------------------------------------------------------------------------
 // Base conversion on the tensor pipe.  Eq. 1 is, across the N coefficients, a dense contraction
 // OUT[t][x] = sum_i M[i][t] Y[i][x] with a constant matrix.  Splitting y_i into bytes y_{i,a} and
@@ -350,6 +334,8 @@ static void bconv_mma_go(const BconvArgs &a, cudaStream_t s) {
     (void)macs;   // the contraction runs on the tensor pipe (IMMA): no integer-pipe products to count
     ps.done(words * (double)N * 8.0, 0.0);
 }
+
+#endif  // HKS_EXPERIMENTAL
 
 // ------------------------------------------------------------------------------------------------
 // The same byte-split contraction on the 5th-generation tensor cores (tcgen05, accumulators in TMEM).
@@ -563,39 +549,6 @@ static hks_status bconv_tc_go(const BconvArgs &a, cudaStream_t s) {
     return HKS_OK;
 }
 
-// HKS_BCONV_TC=0 selects the warp-level IMMA kernel, HKS_BCONV_MMA=0 the integer-pipe kernels
-// (results identical).
-static bool getenv_tc_enabled() {
-    static const bool on = [] {
-        const char *e = getenv("HKS_BCONV_TC");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
-// HKS_NTT_TC=1 moves the log N = 16 column passes onto the tensor cores (results identical).  Off by
-// default: measured slower than the butterfly passes (C2 3963 vs 4097 KS/s).
-bool ntt_tc_enabled() {
-    static const bool on = [] {
-        const char *e = getenv("HKS_NTT_TC");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
-bool bconv_tc_enabled();
-bool bconv_tc_large(u32 log_n, u32 ngroups);
-
-static bool getenv_mma_enabled() {
-    static const bool on = [] {
-        const char *e = getenv("HKS_BCONV_MMA");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
-bool bconv_tc_enabled() { return getenv_mma_enabled() && getenv_tc_enabled(); }
-
 // enough 128-coefficient tiles to give every SM one (otherwise the tensor kernels' fixed prologue loses)
 bool bconv_tc_large(u32 log_n, u32 ngroups) {
     const int nsm = hks_num_sms();
@@ -605,8 +558,9 @@ bool bconv_tc_large(u32 log_n, u32 ngroups) {
 struct ScaleArgs {
     const u64 *in;
     u64 *out;
-    u64 w[BC_MAXSRC], wp[BC_MAXSRC], p[BC_MAXSRC];
-    u32 log_n;
+    const u64 *w;          // device: w[0..nl), then the Shoup companions
+    u64 p[BC_MAXSRC];
+    u32 nl, log_n;
 };
 __global__ void __launch_bounds__(256) k_limb_scale(const __grid_constant__ ScaleArgs A) {
     pdl_trigger();
@@ -615,37 +569,129 @@ __global__ void __launch_bounds__(256) k_limb_scale(const __grid_constant__ Scal
     const u32 i = blockIdx.y;
     const size_t x = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
     if (x >= N) return;
+    const u64 w = A.w[i], wp = A.w[A.nl + i];
     const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(A.in + i * N + x);
-    *reinterpret_cast<ulonglong2 *>(A.out + i * N + x) =
-        make_ulonglong2(shoup(v.x, A.w[i], A.wp[i], A.p[i]), shoup(v.y, A.w[i], A.wp[i], A.p[i]));
+    *reinterpret_cast<ulonglong2 *>(A.out + i * N + x) = make_ulonglong2(shoup(v.x, w, wp, A.p[i]), shoup(v.y, w, wp, A.p[i]));
 }
 
-hks_status launch_limb_scale(const u64 *in, u64 *out, u32 nl, const u64 *w, const u64 *wp, const u64 *p, u32 log_n,
-                             cudaStream_t s) {
+hks_status launch_limb_scale(const u64 *in, u64 *out, u32 nl, const u64 *dw, const u64 *p, u32 log_n, cudaStream_t s) {
     if (nl < 1 || nl > BC_MAXSRC) HKS_FAIL(HKS_EINVAL, "limb_scale: %u limbs", nl);
     ScaleArgs a{};
     a.in = in;
     a.out = out;
+    a.w = dw;
+    a.nl = nl;
     a.log_n = log_n;
-    for (u32 i = 0; i < nl; i++) {
-        a.w[i] = w[i];
-        a.wp[i] = wp[i];
-        a.p[i] = p[i];
-    }
+    for (u32 i = 0; i < nl; i++) a.p[i] = p[i];
     const size_t N = (size_t)1 << log_n;
     (void)hks_launch(k_limb_scale, dim3((u32)(N / 2 / 256), nl), dim3(256), 0, s, a);
     HKS_CHECK_LAUNCH();
     return HKS_OK;
 }
 
-static bool getenv_kara_enabled() {
-    static const bool on = [] {
-        const char *e = getenv("HKS_BCONV_KARA");
-        return !(e && e[0] == '0');
-    }();
-    return on;
+// hks_bconv's constants for an arbitrary (src, dst) prime pair (Eq. 1, §3.6.3), built on
+// the device so that the generic entry point needs no host->device copy (graph-capturable):
+//   thread (i, u), i < 4 ceil(nsrc / 4):  v = [qhat_i]_{t_u} = prod_{k != i} q_k mod t_u -> mat (30-bit
+//       halves) and the 8 byte-column words of v (word c holds byte c of 2^(8a) v mod t in byte a) placed
+//       in the k_bconv_tc B image (zero rows for i >= nsrc);
+//   thread i < nsrc:  w_i = [qhat_i^-1]_{q_i} = h^(q_i - 2), h = prod_{k != i} q_k mod q_i, and
+//       floor(w_i 2^64 / q_i).
+// Host-only work stays with the caller: the primes travel in the parameter block.
+struct BconvPrepArgs {
+    u64 src[BC_MAXSRC];
+    u64 dst[2 * BC_MAXDST];
+    u32 nsrc, ndst;
+    u64 *w;
+    uint2 *mat;
+    u64 *img;
+};
+__device__ __forceinline__ u64 prep_mulmod(u64 a, u64 b, u64 m) {
+    return (u64)((unsigned __int128)a * b % m);
+}
+__global__ void __launch_bounds__(256) k_bconv_prep(const __grid_constant__ BconvPrepArgs A) {
+    pdl_trigger();
+    pdl_wait();   // the workspace may still be read by the previous call's conversion
+    const u32 nrow = 4 * ((A.nsrc + 3) / 4);
+    const u32 nent = nrow * A.ndst;
+    const u32 iw = bconv_img_words(A.nsrc);
+    for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < nent + A.nsrc; e += gridDim.x * blockDim.x) {
+        if (e < nent) {
+            const u32 i = e / A.ndst, u = e - i * A.ndst;
+            const u64 t = A.dst[u];
+            u64 v = 0;
+            if (i < A.nsrc) {
+                v = 1;
+                for (u32 k = 0; k < A.nsrc; k++)
+                    if (k != i) v = prep_mulmod(v, A.src[k] % t, t);
+                A.mat[(size_t)i * A.ndst + u] = make_uint2((u32)(v & 0x3fffffffu), (u32)(v >> 30));
+            }
+            u64 m[8];
+            m[0] = v;
+            for (int a = 1; a < 8; a++) m[a] = prep_mulmod(m[a - 1], 256, t);
+            // image word (u, kc, c, h) with source i = 2 kc + h
+            u64 *dst = A.img + (size_t)u * iw + (size_t)(i >> 1) * 16 + (i & 1);
+            for (int c = 0; c < 8; c++) {
+                u64 wd = 0;
+                for (int a = 0; a < 8; a++) wd |= ((m[a] >> (8 * c)) & 0xffull) << (8 * a);
+                dst[2 * c] = wd;
+            }
+        } else {
+            const u32 i = e - nent;
+            const u64 q = A.src[i];
+            u64 h = 1;
+            for (u32 k = 0; k < A.nsrc; k++)
+                if (k != i) h = prep_mulmod(h, A.src[k] % q, q);
+            u64 w = 1, b = h;
+            for (u64 ex = q - 2; ex; ex >>= 1, b = prep_mulmod(b, b, q))
+                if (ex & 1) w = prep_mulmod(w, b, q);
+            A.w[i] = w;
+            A.w[A.nsrc + i] = (u64)(((unsigned __int128)w << 64) / q);
+        }
+    }
 }
 
+hks_status launch_bconv_prep(const u64 *src, u32 nsrc, const u64 *dst, u32 ndst, u64 *w, uint2 *mat, u64 *img,
+                             cudaStream_t s) {
+    if (nsrc < 1 || nsrc > BC_MAXSRC || ndst < 1 || ndst > 2 * BC_MAXDST) HKS_FAIL(HKS_EINVAL, "bconv_prep: sizes");
+    BconvPrepArgs a{};
+    for (u32 i = 0; i < nsrc; i++) a.src[i] = src[i];
+    for (u32 u = 0; u < ndst; u++) a.dst[u] = dst[u];
+    a.nsrc = nsrc;
+    a.ndst = ndst;
+    a.w = w;
+    a.mat = mat;
+    a.img = img;
+    const u32 n = 4 * ((nsrc + 3) / 4) * ndst + nsrc;
+    (void)hks_launch(k_bconv_prep, dim3((n + 255) / 256), dim3(256), 0, s, a);
+    HKS_CHECK_LAUNCH();
+    return HKS_OK;
+}
+
+#if HKS_EXPERIMENTAL
+// Experimental build only (-DHKS_EXPERIMENTAL=1, tools/build_variant.sh): HKS_BCONV_TC=0 selects the
+// warp-level IMMA kernel, HKS_BCONV_MMA=0 the integer-pipe kernels, HKS_BCONV_KARA=0 the plain integer
+// kernel, HKS_BCONV_FP=1 the FP64-assisted one (slower: 60 vs 52 us for the C2 ModUp conversion, the
+// 128-bit recombination of the FP64 limb sums makes it issue-bound), HKS_NTT_TC=1 the tensor-core NTT
+// column pass (results identical; tests/test_gpu_parity.py::test_bconv_alternate_paths_identical).  The
+// product library has one path per op and reads no environment switch.
+static bool env_flag(const char *name, bool dflt) {
+    const char *e = getenv(name);
+    return e ? e[0] == '1' : dflt;
+}
+static bool getenv_tc_enabled() { static const bool on = env_flag("HKS_BCONV_TC", true); return on; }
+static bool getenv_mma_enabled() { static const bool on = env_flag("HKS_BCONV_MMA", true); return on; }
+static bool getenv_kara_enabled() { static const bool on = env_flag("HKS_BCONV_KARA", true); return on; }
+static bool getenv_fp_enabled() { static const bool on = env_flag("HKS_BCONV_FP", false); return on; }
+bool ntt_tc_enabled() { static const bool on = env_flag("HKS_NTT_TC", false); return on; }
+#else
+static bool getenv_tc_enabled() { return true; }
+static bool getenv_mma_enabled() { return true; }
+static bool getenv_kara_enabled() { return true; }
+bool ntt_tc_enabled() { return false; }
+#endif
+bool bconv_tc_enabled() { return getenv_mma_enabled() && getenv_tc_enabled(); }
+
+#if HKS_EXPERIMENTAL
 // FP64-assisted variant (B200: the FP64 pipe runs 64 DFMA/clk/SM and is otherwise idle here):
 // sources [0, NSRC - NFP) accumulate on the integer pipe (4 IMAD.WIDE per MAC), sources
 // [NSRC - NFP, NSRC) on the FP64 pipe (9 exact DFMA per MAC on 20-bit limbs), one coefficient per
@@ -740,6 +786,8 @@ static void bconv_fp_go(const BconvArgs &a, cudaStream_t s) {
     ps.done(words * (double)N * 8.0, macs * (double)N * 4.0);
 }
 
+#endif  // HKS_EXPERIMENTAL
+
 #ifndef HKS_BCONV_CPT
 #define HKS_BCONV_CPT 1
 #endif
@@ -752,12 +800,10 @@ static void bconv_go(const BconvArgs &a, cudaStream_t s) {
     for (u32 g = 0; g < a.ngroups; g++) maxdst = max(maxdst, a.g[g].ndst);
     dim3 grid((u32)((N / CPT + threads - 1) / threads), a.ngroups, (maxdst + BC_TCH - 1) / BC_TCH);
     ProfScope ps(K_BCONV, s);
-    if (a.prescale)
-        (void)hks_launch(k_bconv<NSRC, true, false, CPT>, grid, dim3(threads), 0, s, a);
-    else if (a.lazy_out)
-        (void)hks_launch(k_bconv<NSRC, false, true, CPT>, grid, dim3(threads), 0, s, a);
+    if (a.lazy_out)
+        (void)hks_launch(k_bconv<NSRC, true, CPT>, grid, dim3(threads), 0, s, a);
     else
-        (void)hks_launch(k_bconv<NSRC, false, false, CPT>, grid, dim3(threads), 0, s, a);
+        (void)hks_launch(k_bconv<NSRC, false, CPT>, grid, dim3(threads), 0, s, a);
     double words = 0, macs = 0;
     for (u32 g = 0; g < a.ngroups; g++) {
         words += a.g[g].nsrc + a.g[g].ndst;
@@ -768,7 +814,8 @@ static void bconv_go(const BconvArgs &a, cudaStream_t s) {
 
 hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
     // all groups of one launch share nsrc (the caller groups them so)
-    if (!a.prescale && a.g[0].matf && getenv_fp_enabled()) {
+#if HKS_EXPERIMENTAL
+    if (a.g[0].matf && getenv_fp_enabled()) {
         // FP64-pipe share chosen so both pipes carry similar work: 16 NINT + 56 ~ 18 NFP + 10 cycles
         switch (a.g[0].nsrc) {
             case 6: bconv_fp_go<6, 3>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
@@ -785,10 +832,11 @@ hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
             default: break;
         }
     }
+#endif
     // the tensor-core kernels pay a fixed prologue (TMEM allocation, matrix image, barriers): small
     // conversions (fewer 128-coefficient tiles than SMs, e.g. N = 2^12) stay on the integer pipe
     const bool large = bconv_tc_large(a.log_n, a.ngroups);
-    if (!a.prescale && a.big && large && a.g[0].mimg && getenv_mma_enabled() && getenv_tc_enabled()) {
+    if (a.big && large && a.g[0].mimg && getenv_mma_enabled() && getenv_tc_enabled()) {
         switch (a.g[0].nsrc) {
 #define CT(NS) case NS: return bconv_tc_go<NS>(a, s);
             CT(1) CT(2) CT(3) CT(4) CT(5) CT(6) CT(7) CT(8) CT(9) CT(10) CT(11) CT(12) CT(13) CT(14) CT(15) CT(16)
@@ -796,7 +844,8 @@ hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
             default: break;
         }
     }
-    if (!a.prescale && a.big && large && a.g[0].matb && getenv_mma_enabled()) {
+#if HKS_EXPERIMENTAL
+    if (a.big && large && a.g[0].matb && getenv_mma_enabled() && !getenv_tc_enabled()) {
         switch (a.g[0].nsrc) {
 #define CM(NS) case NS: bconv_mma_go<NS>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
             CM(1) CM(2) CM(3) CM(4) CM(5) CM(6) CM(7) CM(8) CM(9) CM(10) CM(11) CM(12) CM(13) CM(14) CM(15) CM(16)
@@ -804,10 +853,11 @@ hks_status launch_bconv(const BconvArgs &a, u32 /*max_ndst*/, cudaStream_t s) {
             default: break;
         }
     }
-    if (!a.prescale && a.g[0].mats && getenv_kara_enabled()) {
+#endif
+    if (a.g[0].mats && getenv_kara_enabled()) {
         switch (a.g[0].nsrc) {
 #define CK(NS) case NS: bconv_kara_go<NS>(a, s); HKS_CHECK_LAUNCH(); return HKS_OK;
-            CK(2) CK(3) CK(4) CK(5) CK(6) CK(7) CK(8) CK(9) CK(10) CK(11) CK(12)
+            CK(2) CK(3) CK(4) CK(5) CK(6) CK(7) CK(8) CK(9) CK(10) CK(11)   // 12: spills at 3 CTAs / SM
 #undef CK
             default: break;
         }

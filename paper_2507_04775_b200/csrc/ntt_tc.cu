@@ -19,6 +19,8 @@
 #include "internal.h"
 #include "tc.cuh"
 
+#if HKS_EXPERIMENTAL
+
 #ifndef HKS_NTC_SPLIT
 #define HKS_NTC_SPLIT 1   // warps per TMEM lane quarter and M-tile (each takes 16 / SPLIT of the outputs)
 #endif
@@ -223,3 +225,8 @@ hks_status launch_ntt_cols_tc(const hks_ctx *ctx, NttDir dir, int /*epi*/, const
     if (e != cudaSuccess) HKS_FAIL(HKS_ECUDA, "k_ntt_cols_tc launch: %s", cudaGetErrorString(e));
     return HKS_OK;
 }
+#else
+hks_status launch_ntt_cols_tc(const hks_ctx *, NttDir, int, const NttArgs &, cudaStream_t) {
+    HKS_FAIL(HKS_EINVAL, "tensor-core NTT column pass: experimental build only (HKS_EXPERIMENTAL=1)");
+}
+#endif  // HKS_EXPERIMENTAL

@@ -87,7 +87,7 @@ void push_group(std::vector<BconvGroup> &out, u32 nsrc, const u16 *src_slot, con
         g.ndst = (u32)std::min<size_t>(BC_MAXDST, ds.size() - u0);
         g.mat_stride = stride;
         g.mat = mat + u0;
-        g.matf = matf ? matf + 3 * u0 : nullptr;
+        g.matf = matf ? matf + 3 * u0 : nullptr;   // NULL unless HKS_EXPERIMENTAL uploaded the table
         g.mats = mats ? mats + u0 : nullptr;
         g.matb = matb ? matb + 8 * u0 : nullptr;
         g.mimg = mimg ? mimg + (size_t)bconv_img_words(nsrc) * u0 : nullptr;
@@ -144,7 +144,7 @@ extern "C" hks_status hks_shard_ks_modup_in(const hks_ctx *c, uint32_t level, ui
 // peer-mapped device address) and the base conversion reads every source limb straight from its owner.
 static hks_status shard_inner(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank, const uint64_t *yall,
                               const uint64_t *const *peers, const uint64_t *c1_loc, const uint64_t *evk_loc,
-                              uint64_t *acc_loc, uint64_t *ypsend, void *ws, void *stream) {
+                              uint32_t evk_digits, uint64_t *acc_loc, uint64_t *ypsend, void *ws, void *stream) {
     Plan P;
     hks_status st = make_plan(c, level, world, rank, P);
     if (st != HKS_OK || (st = dev_ctx(c)) != HKS_OK) return st;
@@ -155,6 +155,9 @@ static hks_status shard_inner(const hks_ctx *c, uint32_t level, uint32_t world, 
             if (!peers[r]) HKS_FAIL(HKS_EINVAL, "shard_ks_inner_peer: NULL buffer of rank %u", r);
     const u32 beta = c->beta(level), ne = c->ne(level);
     if (beta > FK_MAXD) HKS_FAIL(HKS_EINVAL, "shard_ks_inner: beta %u > %d", beta, FK_MAXD);
+    if (evk_digits < beta || evk_digits > c->dnum)
+        HKS_FAIL(HKS_EKEY, "shard_ks_inner: key has %u digits; level %u needs %u (context dnum %u)", evk_digits, level,
+                 beta, c->dnum);
     DevGuard g(c->device);
     cudaStream_t s = (cudaStream_t)stream;
     u64 *ext = (u64 *)ws;
@@ -177,9 +180,9 @@ static hks_status shard_inner(const hks_ctx *c, uint32_t level, uint32_t world, 
         }
         const size_t moff = c->mu_mat_off[(size_t)level * c->dnum + j];
         const uint2 *mat = c->d_mu_mat + moff;
-        const double *matf = c->d_mu_matf + 3 * moff;
+        const double *matf = tab_at(c->d_mu_matf, 3 * moff);
         const u32 *mats = c->d_mu_mats + moff;
-        const u64 *matb = c->d_mu_matb + 8 * moff;
+        const u64 *matb = tab_at(c->d_mu_matb, 8 * moff);
         const u64 *mimg = c->d_mu_img + c->mu_img_off[(size_t)level * c->dnum + j];
         const u32 imgw = bconv_img_words(hi - lo);
         const u32 ntg = ne - (hi - lo);
@@ -187,8 +190,8 @@ static hks_status shard_inner(const hks_ctx *c, uint32_t level, uint32_t world, 
         std::vector<u16> ds, dp;
         int run_col = -1;
         auto flush = [&]() {
-            if (!ds.empty()) push_group(groups, hi - lo, src, mat + run_col, ntg, ds, dp, matf + 3 * run_col, mats + run_col,
-                                         matb + 8 * run_col, mimg + (size_t)imgw * run_col, srcp);
+            if (!ds.empty()) push_group(groups, hi - lo, src, mat + run_col, ntg, ds, dp, tab_at(matf, 3 * run_col), mats + run_col,
+                                         tab_at(matb, 8 * run_col), mimg + (size_t)imgw * run_col, srcp);
             ds.clear(); dp.clear(); run_col = -1;
         };
         int prev_col = -2;
@@ -257,8 +260,8 @@ static hks_status shard_moddown(const hks_ctx *c, uint32_t level, uint32_t world
         }
         std::vector<u16> ds(P.nq_act), dp(P.nq_act);
         for (u32 li = 0; li < P.nq_act; li++) { ds[li] = (u16)(p * P.nq_act + li); dp[li] = (u16)(P.q_lo + li); }
-        push_group(groups, K, src, c->d_md_mat + P.q_lo, c->nq, ds, dp, c->d_md_matf + 3 * P.q_lo, c->d_md_mats + P.q_lo,
-                   c->d_md_matb + 8 * P.q_lo, c->d_md_img + (size_t)bconv_img_words(K) * P.q_lo, srcp);
+        push_group(groups, K, src, c->d_md_mat + P.q_lo, c->nq, ds, dp, tab_at(c->d_md_matf, 3 * P.q_lo), c->d_md_mats + P.q_lo,
+                   tab_at(c->d_md_matb, 8 * P.q_lo), c->d_md_img + (size_t)bconv_img_words(K) * P.q_lo, srcp);
     }
     if ((st = bconv_groups(c, groups, ypall ? ypall : conv, conv, s)) != HKS_OK) return st;
     LimbList M;
@@ -275,17 +278,19 @@ static hks_status shard_moddown(const hks_ctx *c, uint32_t level, uint32_t world
 
 extern "C" hks_status hks_shard_ks_inner(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
                                         const uint64_t *yall, const uint64_t *c1_loc, const uint64_t *evk_loc,
-                                        uint64_t *acc_loc, uint64_t *ypsend, void *ws, void *stream) {
+                                        uint32_t evk_digits, uint64_t *acc_loc, uint64_t *ypsend, void *ws,
+                                        void *stream) {
     if (!yall) HKS_FAIL(HKS_EINVAL, "shard_ks_inner: NULL yall");
-    return shard_inner(c, level, world, rank, yall, nullptr, c1_loc, evk_loc, acc_loc, ypsend, ws, stream);
+    return shard_inner(c, level, world, rank, yall, nullptr, c1_loc, evk_loc, evk_digits, acc_loc, ypsend, ws, stream);
 }
 
 extern "C" hks_status hks_shard_ks_inner_peer(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
                                              const uint64_t *const *ysend_ranks, const uint64_t *c1_loc,
-                                             const uint64_t *evk_loc, uint64_t *acc_loc, uint64_t *ypsend, void *ws,
-                                             void *stream) {
+                                             const uint64_t *evk_loc, uint32_t evk_digits, uint64_t *acc_loc,
+                                             uint64_t *ypsend, void *ws, void *stream) {
     if (!ysend_ranks) HKS_FAIL(HKS_EINVAL, "shard_ks_inner_peer: NULL rank table");
-    return shard_inner(c, level, world, rank, nullptr, ysend_ranks, c1_loc, evk_loc, acc_loc, ypsend, ws, stream);
+    return shard_inner(c, level, world, rank, nullptr, ysend_ranks, c1_loc, evk_loc, evk_digits, acc_loc, ypsend, ws,
+                       stream);
 }
 
 extern "C" hks_status hks_shard_ks_moddown_out(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,

@@ -20,7 +20,7 @@ MAX_DIGITS = 64
 
 # every symbol include/hks.h declares (checked by tests/test_capi.py)
 EXPORTS = ("hks_last_error", "hks_ctx_create", "hks_ctx_destroy", "hks_ctx_query", "hks_ctx_psi",
-           "hks_workspace_bytes", "hks_ntt_fwd", "hks_ntt_inv", "hks_bconv", "hks_modup",
+           "hks_workspace_bytes", "hks_ntt_fwd", "hks_ntt_inv", "hks_bconv", "hks_bconv_workspace_bytes", "hks_modup",
            "hks_ksk_inner_product", "hks_moddown", "hks_keyswitch", "hks_relinearize", "hks_hmult", "hks_rescale",
            "hks_pt_weighted_sum", "hks_linear_transform", "hks_linear_transform_workspace_bytes",
            "hks_automorph",
@@ -78,29 +78,31 @@ def lib() -> ctypes.CDLL:
         L.hks_workspace_bytes.restype = ctypes.c_size_t
         for f in ("hks_ntt_fwd", "hks_ntt_inv"):
             getattr(L, f).argtypes = [_vp, _vp, ctypes.POINTER(_u32), _u32, _vp]
-        L.hks_bconv.argtypes = [_vp, _vp, ctypes.POINTER(_u32), _u32, ctypes.POINTER(_u32), _u32, _vp, _vp]
+        L.hks_bconv.argtypes = [_vp, _vp, ctypes.POINTER(_u32), _u32, ctypes.POINTER(_u32), _u32, _vp, _vp, _vp]
+        L.hks_bconv_workspace_bytes.argtypes = [_vp, _u32, _u32]
+        L.hks_bconv_workspace_bytes.restype = ctypes.c_size_t
         L.hks_modup.argtypes = [_vp, _vp, _u32, _vp, _vp, _vp]
-        L.hks_ksk_inner_product.argtypes = [_vp, _vp, _vp, _u32, _u64, _vp, _vp]
+        L.hks_ksk_inner_product.argtypes = [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp]
         L.hks_moddown.argtypes = [_vp, _vp, _u32, _vp, _vp, _vp]
-        L.hks_keyswitch.argtypes = [_vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp]
+        L.hks_keyswitch.argtypes = [_vp, _vp, _vp, _u32, _vp, _u32, _vp, _vp, _vp, _vp]
         L.hks_automorph.argtypes = [_vp, _vp, _u32, _u64, _vp, _vp]
-        L.hks_relinearize.argtypes = [_vp, _vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp]
-        L.hks_hmult.argtypes = [_vp, _vp, _vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp]
+        L.hks_relinearize.argtypes = [_vp, _vp, _vp, _vp, _u32, _vp, _u32, _vp, _vp, _vp, _vp]
+        L.hks_hmult.argtypes = [_vp, _vp, _vp, _vp, _vp, _u32, _vp, _u32, _vp, _vp, _vp, _vp]
         L.hks_rescale.argtypes = [_vp, _vp, _u32, _u32, _vp, _vp, _vp]
         _vpp = ctypes.POINTER(_vp)
         L.hks_pt_weighted_sum.argtypes = [_vp, _u32, _vpp, _vpp, _vpp, _u32, _vp, _vp, _vp]
         L.hks_linear_transform.argtypes = [_vp, _vp, _vp, _u32, _u32, _u32, ctypes.POINTER(_u64), _vpp,
-                                           ctypes.POINTER(_u64), _vpp, _vpp, _vp, _vp, _vp, _vp]
+                                           ctypes.POINTER(_u64), _vpp, _u32, _vpp, _vp, _vp, _vp, _vp]
         L.hks_linear_transform_workspace_bytes.restype = ctypes.c_size_t
         L.hks_linear_transform_workspace_bytes.argtypes = [_vp, _u32, _u32]
-        L.hks_rotate_hoisted.argtypes = [_vp, _vp, _vp, _u32, _u32, ctypes.POINTER(_u64), ctypes.POINTER(_vp),
+        L.hks_rotate_hoisted.argtypes = [_vp, _vp, _vp, _u32, _u32, ctypes.POINTER(_u64), ctypes.POINTER(_vp), _u32,
                                          ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp]
         L.hks_launch_count.restype = ctypes.c_uint64
         L.hks_launch_count.argtypes = []
         L.hks_prof_enable.argtypes = [ctypes.c_int]
         L.hks_prof_read.argtypes = [ctypes.POINTER(ProfEntry), ctypes.c_int]
         L.hks_rotate_hoisted_batch.argtypes = [_vp, _u32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _u32, _u32,
-                                               ctypes.POINTER(_u64), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                               ctypes.POINTER(_u64), ctypes.POINTER(_vp), _u32, ctypes.POINTER(_vp),
                                                ctypes.POINTER(_vp), _vp, _vp]
         L.hks_rotate_hoisted_batch_workspace_bytes.argtypes = [_vp, _u32, _u32]
         L.hks_rotate_hoisted_batch_workspace_bytes.restype = ctypes.c_size_t
@@ -108,15 +110,16 @@ def lib() -> ctypes.CDLL:
         L.hks_shard_workspace_bytes.argtypes = [_vp, _u32, _u32, _u32]
         L.hks_shard_workspace_bytes.restype = ctypes.c_size_t
         L.hks_shard_ks_modup_in.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp]
-        L.hks_shard_ks_inner.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.hks_shard_ks_inner.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp]
         L.hks_shard_ks_moddown_out.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
-        L.hks_shard_ks_inner_peer.argtypes = [_vp, _u32, _u32, _u32, ctypes.POINTER(_vp), _vp, _vp, _vp, _vp, _vp,
-                                              _vp]
+        L.hks_shard_ks_inner_peer.argtypes = [_vp, _u32, _u32, _u32, ctypes.POINTER(_vp), _vp, _vp, _u32, _vp, _vp,
+                                              _vp, _vp]
         L.hks_shard_ks_moddown_out_peer.argtypes = [_vp, _u32, _u32, _u32, ctypes.POINTER(_vp), _vp, _vp, _vp, _vp,
                                                     _vp, _vp]
         for f in EXPORTS[1:]:
             if f not in ("hks_ctx_destroy", "hks_workspace_bytes", "hks_launch_count", "hks_shard_workspace_bytes",
-                         "hks_rotate_hoisted_batch_workspace_bytes"):
+                         "hks_rotate_hoisted_batch_workspace_bytes", "hks_bconv_workspace_bytes",
+                         "hks_linear_transform_workspace_bytes"):
                 getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -138,6 +141,15 @@ def _ptr(t) -> int:
     if isinstance(t, int):
         return t
     return t.data_ptr()
+
+
+def evk_digits(ctx, evk) -> int:
+    """Digit count of a key passed to libhks: the leading dimension of a [digits][2][L+1+K][N] tensor, or
+    of the first of a list of keys; a raw address carries none, so the context's dnum is assumed."""
+    if isinstance(evk, (list, tuple)):
+        return min((evk_digits(ctx, e) for e in evk), default=ctx.dnum)
+    shape = getattr(evk, "shape", None)
+    return int(shape[0]) if shape is not None and len(shape) == 4 else ctx.dnum
 
 
 def _stream(stream):
@@ -212,9 +224,18 @@ def ntt_inv(ctx: Context, x, prime_idx: Sequence[int], stream=None):
     _check(lib().hks_ntt_inv(ctx.handle, _ptr(x), _u32arr(prime_idx), len(prime_idx), _stream(stream)), "hks_ntt_inv")
 
 
-def bconv(ctx: Context, x, src_idx: Sequence[int], dst_idx: Sequence[int], out, stream=None):
+def bconv_workspace(ctx: Context, nsrc: int, ndst: int):
+    import torch
+    nbytes = int(lib().hks_bconv_workspace_bytes(ctx.handle, nsrc, ndst))
+    return torch.empty(max(nbytes // 8, 1), dtype=torch.uint64, device=f"cuda:{ctx.device}")
+
+
+def bconv(ctx: Context, x, src_idx: Sequence[int], dst_idx: Sequence[int], out, ws=None, stream=None):
+    """ws: bconv_workspace(ctx, len(src_idx), len(dst_idx)) (allocated here when None)."""
+    if ws is None:
+        ws = bconv_workspace(ctx, len(src_idx), len(dst_idx))
     _check(lib().hks_bconv(ctx.handle, _ptr(x), _u32arr(src_idx), len(src_idx), _u32arr(dst_idx), len(dst_idx),
-                           _ptr(out), _stream(stream)), "hks_bconv")
+                           _ptr(out), _ptr(ws), _stream(stream)), "hks_bconv")
 
 
 def modup(ctx: Context, d, level: int, ext, ws, stream=None):
@@ -222,7 +243,8 @@ def modup(ctx: Context, d, level: int, ext, ws, stream=None):
 
 
 def ksk_inner_product(ctx: Context, ext, evk, level: int, galois: int, acc, stream=None):
-    _check(lib().hks_ksk_inner_product(ctx.handle, _ptr(ext), _ptr(evk), level, galois, _ptr(acc), _stream(stream)),
+    _check(lib().hks_ksk_inner_product(ctx.handle, _ptr(ext), _ptr(evk), evk_digits(ctx, evk), level, galois, _ptr(acc),
+                                       _stream(stream)),
            "hks_ksk_inner_product")
 
 
@@ -231,18 +253,18 @@ def moddown(ctx: Context, acc, level: int, out, ws, stream=None):
 
 
 def keyswitch(ctx: Context, c0, c1, level: int, evk, out0, out1, ws, stream=None):
-    _check(lib().hks_keyswitch(ctx.handle, _ptr(c0), _ptr(c1), level, _ptr(evk), _ptr(out0), _ptr(out1), _ptr(ws),
-                               _stream(stream)), "hks_keyswitch")
+    _check(lib().hks_keyswitch(ctx.handle, _ptr(c0), _ptr(c1), level, _ptr(evk), evk_digits(ctx, evk), _ptr(out0),
+                               _ptr(out1), _ptr(ws), _stream(stream)), "hks_keyswitch")
 
 
 def relinearize(ctx: Context, d0, d1, d2, level: int, evk, out0, out1, ws, stream=None):
-    _check(lib().hks_relinearize(ctx.handle, _ptr(d0), _ptr(d1), _ptr(d2), level, _ptr(evk), _ptr(out0), _ptr(out1),
-                                 _ptr(ws), _stream(stream)), "hks_relinearize")
+    _check(lib().hks_relinearize(ctx.handle, _ptr(d0), _ptr(d1), _ptr(d2), level, _ptr(evk), evk_digits(ctx, evk),
+                                 _ptr(out0), _ptr(out1), _ptr(ws), _stream(stream)), "hks_relinearize")
 
 
 def hmult(ctx: Context, a0, a1, b0, b1, level: int, evk, out0, out1, ws, stream=None):
-    _check(lib().hks_hmult(ctx.handle, _ptr(a0), _ptr(a1), _ptr(b0), _ptr(b1), level, _ptr(evk), _ptr(out0),
-                           _ptr(out1), _ptr(ws), _stream(stream)), "hks_hmult")
+    _check(lib().hks_hmult(ctx.handle, _ptr(a0), _ptr(a1), _ptr(b0), _ptr(b1), level, _ptr(evk), evk_digits(ctx, evk),
+                           _ptr(out0), _ptr(out1), _ptr(ws), _stream(stream)), "hks_hmult")
 
 
 def rescale(ctx: Context, x, npoly: int, level: int, out, ws, stream=None):
@@ -268,8 +290,8 @@ def linear_transform(ctx: Context, c0, c1, level: int, n1: int, n2: int, baby_ga
     arr = lambda vs: (_vp * max(1, len(vs)))(*[_ptr(v) for v in vs])
     gal = lambda vs: (_u64 * max(1, len(vs)))(*[int(v) for v in vs])
     _check(lib().hks_linear_transform(ctx.handle, _ptr(c0), _ptr(c1), level, n1, n2, gal(baby_galois), arr(baby_evks),
-                                      gal(giant_galois), arr(giant_evks), arr(pts), _ptr(out0), _ptr(out1), _ptr(ws),
-                                      _stream(stream)), "hks_linear_transform")
+                                      gal(giant_galois), arr(giant_evks), evk_digits(ctx, list(baby_evks) + list(giant_evks)),
+                                      arr(pts), _ptr(out0), _ptr(out1), _ptr(ws), _stream(stream)), "hks_linear_transform")
 
 
 def automorph(ctx: Context, x, nlimbs: int, galois: int, out, stream=None):
@@ -282,8 +304,8 @@ def rotate_hoisted(ctx: Context, c0, c1, level: int, galois: Sequence[int], evks
     ek = (_vp * n)(*[_ptr(e) for e in evks])
     o0 = (_vp * n)(*[_ptr(o) for o in outs0])
     o1 = (_vp * n)(*[_ptr(o) for o in outs1])
-    _check(lib().hks_rotate_hoisted(ctx.handle, _ptr(c0), _ptr(c1), level, n, g, ek, o0, o1, _ptr(ws),
-                                    _stream(stream)), "hks_rotate_hoisted")
+    _check(lib().hks_rotate_hoisted(ctx.handle, _ptr(c0), _ptr(c1), level, n, g, ek, evk_digits(ctx, list(evks)), o0, o1,
+                                    _ptr(ws), _stream(stream)), "hks_rotate_hoisted")
 
 
 def launch_count() -> int:
@@ -313,7 +335,8 @@ def rotate_hoisted_batch(ctx: Context, c0s, c1s, level: int, galois: Sequence[in
     ek = (_vp * n)(*[_ptr(e) for e in evks])
     o0 = (_vp * (nct * n))(*[_ptr(o) for o in outs0])
     o1 = (_vp * (nct * n))(*[_ptr(o) for o in outs1])
-    _check(lib().hks_rotate_hoisted_batch(ctx.handle, nct, a0, a1, level, n, g, ek, o0, o1, _ptr(ws), _stream(stream)),
+    _check(lib().hks_rotate_hoisted_batch(ctx.handle, nct, a0, a1, level, n, g, ek, evk_digits(ctx, list(evks)), o0, o1,
+                                          _ptr(ws), _stream(stream)),
            "hks_rotate_hoisted_batch")
 
 
@@ -341,7 +364,8 @@ def shard_ks_modup_in(ctx: Context, level, world, rank, c1_loc, ysend, stream=No
 
 def shard_ks_inner(ctx: Context, level, world, rank, yall, c1_loc, evk_loc, acc_loc, ypsend, ws, stream=None):
     _check(lib().hks_shard_ks_inner(ctx.handle, level, world, rank, _ptr(yall), _ptr(c1_loc), _ptr(evk_loc),
-                                    _ptr(acc_loc), _ptr(ypsend), _ptr(ws), _stream(stream)), "hks_shard_ks_inner")
+                                    evk_digits(ctx, evk_loc), _ptr(acc_loc), _ptr(ypsend), _ptr(ws), _stream(stream)),
+           "hks_shard_ks_inner")
 
 
 def _ptr_table(ptrs):
@@ -355,7 +379,8 @@ def shard_ks_inner_peer(ctx: Context, level, world, rank, ysend_ranks, c1_loc, e
     """Phase B reading every rank's ysend through `ysend_ranks` (addresses valid on this GPU: own buffer,
     peer mappings over NVLink, or simulated ranks' buffers on one device) -- no all-gather."""
     _check(lib().hks_shard_ks_inner_peer(ctx.handle, level, world, rank, _ptr_table(ysend_ranks), _ptr(c1_loc),
-                                         _ptr(evk_loc), _ptr(acc_loc), _ptr(ypsend), _ptr(ws), _stream(stream)),
+                                         _ptr(evk_loc), evk_digits(ctx, evk_loc), _ptr(acc_loc), _ptr(ypsend), _ptr(ws),
+                                         _stream(stream)),
            "hks_shard_ks_inner_peer")
 
 

@@ -79,3 +79,27 @@ def test_host_ctx_refuses_compute():
     with pytest.raises(H.HksError) as e:
         H.ntt_fwd(ctx, 0x1000, [0], stream=0)
     assert e.value.status == 10
+
+
+def test_rotate_hoisted_workspace_count_zero_is_worst_case():
+    """include/hks.h HKS_OP_ROTATE_HOISTED: count = 0 sizes for every nrot (the layout grows with nrot)."""
+    for name, levels in (("C2", (29, 9)), ("T12", (6, 0))):
+        cfg = S.config(name)
+        ctx = H.Context.from_config(cfg, device=-1)
+        for level in levels:
+            worst = ctx.workspace_bytes(H.OP_ROTATE_HOISTED, level, 0)
+            sizes = [ctx.workspace_bytes(H.OP_ROTATE_HOISTED, level, n) for n in range(1, 65)]
+            assert all(a <= b for a, b in zip(sizes, sizes[1:]))          # monotone in nrot
+            assert max(sizes) <= worst
+
+
+def test_bconv_workspace_bytes():
+    cfg = S.config("C2")
+    ctx = H.Context.from_config(cfg, device=-1)
+    lb = cfg.n * 8
+    for nsrc, ndst in ((1, 1), (10, 30), (16, 128), (3, 7)):
+        b = int(H.lib().hks_bconv_workspace_bytes(ctx.handle, nsrc, ndst))
+        assert b >= nsrc * lb + (2 * 16 + nsrc * ndst + ndst * 32 * ((nsrc + 3) // 4)) * 8
+        assert b % 128 == 0
+    assert int(H.lib().hks_bconv_workspace_bytes(ctx.handle, 17, 4)) == 0      # nsrc > 16
+    assert int(H.lib().hks_bconv_workspace_bytes(ctx.handle, 4, 129)) == 0     # ndst > 128

@@ -184,7 +184,7 @@ def run_ks(ctx, c0, c1, level, evk_dev):
 
 
 @pytest.mark.parametrize("name,levels", [("C1", [2]), ("C1p", [2, 1, 0]), ("T10", [4, 2]),
-                                         ("T12", [6, 5, 3, 0]), ("T16s", [5, 1]), ("T17s", [4])])
+                                         ("T12", [6, 5, 4, 3, 0]), ("T16s", [5, 1]), ("T17s", [4])])
 def test_keyswitch_parity_small(orc, name, levels):
     cfg, ctx, o = ctxs(orc, name)
     keys, evk = relin_key(o, name)
@@ -199,6 +199,52 @@ def test_keyswitch_parity_small(orc, name, levels):
         dec = o.crt_centered(o.decrypt_coeff(got0, got1, keys.s_eval, level), level)
         err = max(abs(a - int(b)) for a, b in zip(dec, m))
         assert err <= ks_bound(o, level, keys.B_e, keys.h)
+
+
+def test_evk_digit_count(orc):
+    """include/hks.h "Keys" / SPEC.md:482: a key with fewer digits than beta(level) is refused with HKS_EKEY
+    before any launch; the same key is usable (bit-exact) at a level it covers."""
+    cfg, ctx, o = ctxs(orc, "C2")
+    keys, evk = relin_key(o, "C2")
+    g = S.rng(cfg.seed + 77)
+    short = to_dev(np.ascontiguousarray(evk[:2]))          # 2 of 3 digits: covers levels <= 19
+    level = 29
+    c0, c1 = (S.uniform_limbs(g, o.q[: level + 1], o.n) for _ in range(2))
+    out0, out1 = empty_dev(c0.shape), empty_dev(c0.shape)
+    ws = ctx.workspace(H.OP_KEYSWITCH, level)
+    with pytest.raises(H.HksError) as ei:
+        H.keyswitch(ctx, to_dev(c0), to_dev(c1), level, short, out0, out1, ws)
+    assert ei.value.status == 6
+    with pytest.raises(H.HksError) as ei:
+        H.hmult(ctx, to_dev(c0), to_dev(c1), to_dev(c0), to_dev(c1), level, short, out0, out1,
+                ctx.workspace(H.OP_HMULT, level))
+    assert ei.value.status == 6
+    level = 19
+    c0, c1 = c0[: level + 1], c1[: level + 1]
+    got0, got1 = run_ks(ctx, c0, c1, level, short)
+    want0, want1 = o.keyswitch(c0, c1, evk, level)
+    assert (got0 == want0).all() and (got1 == want1).all()
+
+
+def test_bconv_graph_capture(orc):
+    """hks_bconv derives its constants on the device into the caller's workspace: no allocation and no host
+    copy inside the call, so it can be captured into a CUDA graph; the replays are bit-exact."""
+    cfg, ctx, o = ctxs(orc, "C2")
+    src, dst = [3, 17, 25, 31], [0, 1, 2, 39, 38, 37, 10]
+    g = S.rng(421)
+    xs = [edge_limbs([o.primes[i] for i in src], o.n, g) for _ in range(2)]
+    x = to_dev(xs[0])
+    out = empty_dev((len(dst), o.n))
+    ws = H.bconv_workspace(ctx, len(src), len(dst))
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        H.bconv(ctx, x, src, dst, out, ws, torch.cuda.current_stream().cuda_stream)
+    for xv in xs:
+        x.copy_(to_dev(xv))
+        gr.replay()
+        torch.cuda.synchronize()
+        assert (to_host(out) == o.bconv(xv, src, dst)).all()
 
 
 @pytest.mark.parametrize("level", [29, 27, 20, 19, 11, 9, 0])
@@ -322,14 +368,30 @@ def test_relinearize_parity(orc, name, level):
     assert max(abs(v) for v in diff) <= ks_bound(o, level, keys.B_e, keys.h)
 
 
+@pytest.fixture(scope="module")
+def experimental_lib():
+    """libhks built with -DHKS_EXPERIMENTAL=1 into tools/exp/experimental (built once, ~1 min)."""
+    import os, subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = os.path.join(root, "tools", "exp", "experimental", "libhks.so")
+    csrc = os.path.join(root, "paper_2507_04775_b200", "csrc")
+    newest = max(os.path.getmtime(os.path.join(csrc, f)) for f in os.listdir(csrc))
+    if not os.path.exists(out) or os.path.getmtime(out) < newest:
+        subprocess.run(["bash", os.path.join(root, "tools", "build_variant.sh"), "experimental", "-DHKS_EXPERIMENTAL=1"],
+                       check=True, capture_output=True, timeout=1200)
+    return out
+
+
 @pytest.mark.parametrize("env", [{"HKS_BCONV_FP": "1"}, {"HKS_BCONV_TC": "0"}, {"HKS_BCONV_MMA": "0"},
                                  {"HKS_BCONV_MMA": "0", "HKS_BCONV_KARA": "0"}, {"HKS_NTT_TC": "1"}],
                          ids=["fp64", "imma", "int-kara", "int-plain", "ntt-tensor-cols"])
-def test_bconv_alternate_paths_identical(orc, env):
-    """Every base-conversion kernel (tcgen05 default; warp IMMA, integer Karatsuba / plain, FP64-assisted
-    behind switches) and the tensor-core NTT column pass (opt-in) must produce the same KeySwitch bits as
-    the oracle."""
+def test_bconv_alternate_paths_identical(orc, env, experimental_lib):
+    """Every base-conversion kernel (tcgen05 default; warp IMMA, integer Karatsuba / plain, FP64-assisted) and
+    the tensor-core NTT column pass must produce the same KeySwitch bits as the oracle.  The alternatives are
+    measured-and-rejected designs: they exist only in the experimental build
+    (-DHKS_EXPERIMENTAL=1, tools/build_variant.sh), selected there by environment switches."""
     import subprocess, sys, os
+    env = dict(env, HKS_LIB_PATH=experimental_lib)
     code = ("import sys; sys.path.insert(0, 'tests'); sys.path.insert(0, '.');"
             "import numpy as np, hks_synth as S, oracle; from helpers import *;"
             "from paper_2507_04775_b200 import hks as H;"

@@ -2,8 +2,9 @@
 
 CPU (gloo, world_size 2): the ownership plan is a partition, and the all-gather layout the Python
 orchestrator produces matches the slots libhks reads (q_slot / p_slot).
-GPU: G simulated ranks on one device (all-gather = local concatenation) give results bit-identical
-to the unsharded hks_keyswitch (integer math is order-independent: SURVEY.md §4 item 5)."""
+GPU: G simulated ranks on one device (all-gather = local concatenation) give results bit-identical to the
+CPU oracle's KeySwitch on the same inputs (and hence to the unsharded hks_keyswitch; integer math is
+order-independent: SURVEY.md §4 item 5, "sharded == unsharded" anchored on the oracle, SURVEY.md:703)."""
 import os
 
 import numpy as np
@@ -79,10 +80,22 @@ def test_gloo_allgather_layout(name, level):
 
 
 # ------------------------------------------------------------------ GPU: simulated ranks
+def _oracle_ks(orc, cfg, c0, c1, evk, level):
+    """the CPU oracle's KeySwitch on the device inputs (uint64 views)"""
+    o = orc.Ctx.from_config(cfg)
+    h = lambda t: t.cpu().numpy().view(np.uint64)
+    return o.keyswitch(h(c0), h(c1), h(evk), level)
+
+
+def _equal_oracle(got0, got1, want):
+    h = lambda t: t.cpu().numpy().view(np.uint64)
+    return bool((h(got0) == want[0]).all() and (h(got1) == want[1]).all())
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,level,world", [("T12", 6, 2), ("T12", 4, 3), ("T16s", 5, 2), ("C2", 29, 4),
                                               ("C4", 35, 8), ("C4", 35, 2), ("C4", 17, 4)])
-def test_sharded_keyswitch_matches_unsharded(name, level, world):
+def test_sharded_keyswitch_matches_unsharded(orc, name, level, world):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     dev = "cuda:0"
@@ -120,13 +133,14 @@ def test_sharded_keyswitch_matches_unsharded(name, level, world):
     got0 = torch.cat([l[3] for l in loc])
     got1 = torch.cat([l[4] for l in loc])
     torch.cuda.synchronize()
+    assert _equal_oracle(got0, got1, _oracle_ks(orc, cfg, c0, c1, evk, level))
     assert torch.equal(got0, ref0) and torch.equal(got1, ref1)
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,level,world", [("T12", 6, 2), ("T12", 4, 3), ("C2", 29, 4), ("C4", 35, 8),
                                               ("C4", 35, 2), ("C4", 17, 4)])
-def test_peer_sharded_keyswitch_matches_unsharded(name, level, world):
+def test_peer_sharded_keyswitch_matches_unsharded(orc, name, level, world):
     """NEXT-3: phases B and C read the other ranks' limbs through a pointer table (here: simulated ranks'
     buffers on one GPU) inside the base conversion; bit-identical to hks_keyswitch."""
     if not torch.cuda.is_available():
@@ -164,7 +178,9 @@ def test_peer_sharded_keyswitch_matches_unsharded(name, level, world):
         c0l, _, _, o0, o1 = loc[r]
         ks.phase_c(c0l, o0, o1)
     torch.cuda.synchronize()
-    assert torch.equal(torch.cat([l[3] for l in loc]), ref0) and torch.equal(torch.cat([l[4] for l in loc]), ref1)
+    got0, got1 = torch.cat([l[3] for l in loc]), torch.cat([l[4] for l in loc])
+    assert _equal_oracle(got0, got1, _oracle_ks(orc, cfg, c0, c1, evk, level))
+    assert torch.equal(got0, ref0) and torch.equal(got1, ref1)
 
 
 @pytest.mark.gpu
