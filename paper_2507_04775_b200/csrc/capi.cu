@@ -391,6 +391,7 @@ extern "C" hks_status hks_bconv(const hks_ctx *c, const uint64_t *x, const uint3
         a.log_n = c->log_n;
         a.lazy_out = 0;
         a.big = c->all_big ? 1 : 0;
+        a.fresh_tables = 1;
         a.ngroups = 1;
         BconvGroup &G = a.g[0];
         G.nsrc = nsrc;

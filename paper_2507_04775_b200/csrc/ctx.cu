@@ -345,7 +345,7 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     // (W_B[0] / W'_A), and the twist between the rounds as Shoup pairs tw[v][o] for round-1 vector class v
     // and output o (forward d_o[v], inverse f_v[o]).
     std::vector<u64> ntt_img_fwd, ntt_img_inv;
-    if (HKS_EXPERIMENTAL && log_n == 16) {
+    if (log_n == 16) {
         ntt_img_fwd.reserve((size_t)nm * NTT16_TAB);
         ntt_img_inv.reserve((size_t)nm * NTT16_TAB);
         for (u32 pi = 0; pi < nm; pi++) {

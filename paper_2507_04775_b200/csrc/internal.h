@@ -15,6 +15,10 @@
 #define HKS_EXPERIMENTAL 0   // 1: also build the measured-and-rejected kernel variants and
 #endif                       //    their environment switches (tools/build_variant.sh); never the product
 
+#ifndef HKS_NTT_TC_DEFAULT
+#define HKS_NTT_TC_DEFAULT 0   // log N = 16 column passes on the tensor cores (ntt_tc.cu); 0: butterfly passes
+#endif
+
 typedef uint16_t u16;
 typedef uint8_t u8;
 
@@ -125,6 +129,9 @@ struct BconvArgs {
     u32 lazy_out;              // 1: outputs in [0, 8t) (consumer: forward NTT), 0: canonical
     u32 big;                   // 1: every prime > 2^49 (required by the tensor-pipe kernels k_bconv_tc / _mma)
     u32 cw;                    // k_bconv_mma: coefficients per CTA (set by the launcher)
+    u32 fresh_tables;          // 1: mat / mimg were written by a kernel earlier on this stream (hks_bconv), so
+                               // the tensor-core kernel, which stages them before griddepcontrol.wait, is
+                               // launched without programmatic dependent launch
     BconvGroup g[BC_MAXG];
 };
 
@@ -305,9 +312,11 @@ int hks_num_sms();
 // per-kernel profiling on (hks_prof_enable): calls with independent branches then keep them on the caller's
 // stream, so each launch's event pair times that kernel alone rather than its overlap with a sibling
 bool prof_active();
+// pdl = false: an ordinary stream-ordered launch, for a kernel whose pre-wait prologue reads tables a
+// recent kernel of the same stream wrote (hks_bconv's device-built constants)
 template <typename... KArgs, typename... Args>
-inline cudaError_t hks_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                              Args &&...args) {
+inline cudaError_t hks_launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                  cudaStream_t s, Args &&...args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -315,10 +324,15 @@ inline cudaError_t hks_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t hks_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args &&...args) {
+    return hks_launch_pdl(pdl_enabled(), kernel, grid, block, smem, s, std::forward<Args>(args)...);
 }
 
 // ----------------------------------------------------------------------------------------------

@@ -534,10 +534,11 @@ static hks_status bconv_tc_go(const BconvArgs &a, cudaStream_t s) {
     gx = std::min<u32>(gx, (u32)(N >> 7));
     ProfScope ps(K_BCONV, s);
     cudaError_t e;
+    const bool pdl = pdl_enabled() && !a.fresh_tables;
     if (a.lazy_out)
-        e = hks_launch(k_bconv_tc<NSRC, true>, dim3(gx, a.ngroups, nz), dim3(TC_THREADS), smem, s, b);
+        e = hks_launch_pdl(pdl, k_bconv_tc<NSRC, true>, dim3(gx, a.ngroups, nz), dim3(TC_THREADS), smem, s, b);
     else
-        e = hks_launch(k_bconv_tc<NSRC, false>, dim3(gx, a.ngroups, nz), dim3(TC_THREADS), smem, s, b);
+        e = hks_launch_pdl(pdl, k_bconv_tc<NSRC, false>, dim3(gx, a.ngroups, nz), dim3(TC_THREADS), smem, s, b);
     double words = 0, macs = 0;
     for (u32 g = 0; g < a.ngroups; g++) {
         words += a.g[g].nsrc + a.g[g].ndst;
@@ -682,12 +683,12 @@ static bool getenv_tc_enabled() { static const bool on = env_flag("HKS_BCONV_TC"
 static bool getenv_mma_enabled() { static const bool on = env_flag("HKS_BCONV_MMA", true); return on; }
 static bool getenv_kara_enabled() { static const bool on = env_flag("HKS_BCONV_KARA", true); return on; }
 static bool getenv_fp_enabled() { static const bool on = env_flag("HKS_BCONV_FP", false); return on; }
-bool ntt_tc_enabled() { static const bool on = env_flag("HKS_NTT_TC", false); return on; }
+bool ntt_tc_enabled() { static const bool on = env_flag("HKS_NTT_TC", HKS_NTT_TC_DEFAULT != 0); return on; }
 #else
 static bool getenv_tc_enabled() { return true; }
 static bool getenv_mma_enabled() { return true; }
 static bool getenv_kara_enabled() { return true; }
-bool ntt_tc_enabled() { return false; }
+bool ntt_tc_enabled() { return HKS_NTT_TC_DEFAULT != 0; }
 #endif
 bool bconv_tc_enabled() { return getenv_mma_enabled() && getenv_tc_enabled(); }
 
