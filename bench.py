@@ -54,10 +54,11 @@ def parse():
     ap.add_argument("--dump", default=None,
                     help="directory: after the timed region every rank saves one step's inputs and outputs (.npy) "
                          "for an offline oracle check (tests/test_multirank.py)")
-    ap.add_argument("--shard", default="auto", choices=["auto", "none", "nccl", "peer"],
-                    help="C4 limb sharding: nccl = two NCCL all-gathers per KeySwitch; peer = the exchanges fused "
-                         "into the base conversions over NVLink symmetric memory; none = one KeySwitch per GPU; "
-                         "auto = nccl for C4 under torchrun, else none")
+    ap.add_argument("--shard", default="auto", choices=["auto", "none", "nccl", "pipe", "peer"],
+                    help="C4 limb sharding: nccl = two NCCL all-gathers per KeySwitch; pipe = the first exchange as "
+                         "per-digit broadcasts overlapped with the conversions; peer = the exchanges fused into the "
+                         "base conversions over NVLink symmetric memory; none = one KeySwitch per GPU; auto = nccl "
+                         "for C4 under torchrun, else none")
     return ap.parse_args()
 
 
@@ -407,6 +408,10 @@ class C4ShardWorkload:
                 ys = [torch.zeros((s0.q_pad, cfg.n), dtype=torch.int64, device=dev)]
                 yps = [torch.zeros((2 * s0.p_pad, cfg.n), dtype=torch.int64, device=dev)]
                 self.ks = shard.PeerShardedKeySwitch(ctx, level, 1, 0, dev, sim_ysend=ys, sim_ypsend=yps)
+        elif mode == "pipe":
+            self.ks = shard.PipelinedShardedKeySwitch(ctx, level, world, rank, dev,
+                                                      deliver_fn=None if world > 1 else (lambda j, runs, yall: None),
+                                                      gather_fn=None if world > 1 else (lambda o, i: o.copy_(i)))
         else:
             self.ks = shard.ShardedKeySwitch(ctx, level, world, rank, dev,
                                              gather_fn=None if world > 1 else (lambda o, i: o.copy_(i)))
@@ -444,7 +449,9 @@ class C4ShardWorkload:
         c, l = self.cfg, self.level
         b = self.nsets * (2 * c.dnum * (c.L + 1 + c.K) + 2 * (l + 1)) * c.n * 8 / self.world
         return (f"{self.nsets} rotating (ct, key) sets, {b / 2**20:.0f} MiB per rank ({l2_str()}); limbs sharded over "
-                f"{self.world} rank(s), exchange: {'NCCL all-gathers' if self.mode == 'nccl' else 'peer loads in BConv'}")
+                f"{self.world} rank(s), exchange: " + {"nccl": "NCCL all-gathers", "pipe": "per-digit broadcasts "
+                                                        "overlapped with BConv + all-gather",
+                                                        "peer": "peer loads in BConv"}[self.mode])
 
     def dump(self, d, rank):
         import torch

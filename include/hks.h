@@ -313,6 +313,18 @@ hks_status hks_shard_ks_moddown_out(const hks_ctx *ctx, uint32_t level, uint32_t
                                     const uint64_t *ypall, const uint64_t *acc_loc, const uint64_t *c0_loc,
                                     uint64_t *out0_loc, uint64_t *out1_loc, void *ws, void *stream);
 
+/* Pipelined phase B (SURVEY.md §8(f) NEXT-3 "per-digit pipelined all-gather overlapped with BConv"): the
+ * same work and result as hks_shard_ks_inner, but the base conversion of digit j is enqueued only after
+ * `stream` waits on digit_ready[j] -- a HOST array of beta(level) cudaEvent_t handles (as void*; an entry may
+ * be NULL for a digit already delivered) -- so the caller can deliver yall digit by digit (e.g. one NCCL
+ * broadcast per (digit, owner) segment, shard.PipelinedShardedKeySwitch) and the conversion of digit j overlaps
+ * the transfer of digit j + 1.  yall is read only at the slots of each digit's limbs, in the layout of
+ * hks_shard_ks_inner (rank r's limbs at [r * q_pad, r * q_pad + q_hi - q_lo)). */
+hks_status hks_shard_ks_inner_pipelined(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
+                                        const uint64_t *yall, const void *const *digit_ready, const uint64_t *c1_loc,
+                                        const uint64_t *evk_loc, uint32_t evk_digits, uint64_t *acc_loc,
+                                        uint64_t *ypsend, void *ws, void *stream);
+
 /* Peer-memory variants of phases B and C (the collective fused into the base
  * conversion over NVLink).  Instead of an all-gathered buffer, the caller passes a HOST array of `world`
  * device pointers: rank r's ysend ([q_pad][N]) resp. ypsend ([2][p_pad][N]) as mapped into this rank's

@@ -104,7 +104,7 @@ hks_status upload(T **dptr, const std::vector<T> &h) {
 }
 
 void free_tables(hks_ctx *c) {
-    void *ptrs[] = {c->d_pc, c->d_tw_col_fwd, c->d_tw_row_fwd, c->d_tw_col_inv, c->d_tw_row_inv, c->d_ninv,
+    void *ptrs[] = {c->d_pc, c->d_tw_all, c->d_ninv,
                     c->d_mu_scale, c->d_mu_mat, c->d_md_scale, c->d_md_mat, c->d_pinv, c->d_mu_matf, c->d_md_matf, c->d_mu_mats, c->d_md_mats, c->d_mu_matb, c->d_md_matb, c->d_mu_img, c->d_md_img, c->d_ntt_img_fwd, c->d_ntt_img_inv,
                     c->d_qmod, c->d_qlinv};
     for (void *p : ptrs)
@@ -429,10 +429,35 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
 #define UP(dst, src) if (st == HKS_OK) st = upload(&c->dst, src)
     UP(d_pc, pc);
     UP(d_ninv, ninv);
-    UP(d_tw_col_fwd, tcf);
-    UP(d_tw_row_fwd, trf);
-    UP(d_tw_col_inv, tci);
-    UP(d_tw_row_inv, tri);
+    {
+        // the four twiddle tables in one allocation, so that one L2 access-policy window covers them
+        std::vector<ulonglong2> all;
+        all.reserve(tcf.size() + trf.size() + tci.size() + tri.size());
+        for (const auto *v : {&tcf, &trf, &tci, &tri}) all.insert(all.end(), v->begin(), v->end());
+        UP(d_tw_all, all);
+        if (st == HKS_OK) {
+            c->d_tw_col_fwd = c->d_tw_all;
+            c->d_tw_row_fwd = c->d_tw_col_fwd + tcf.size();
+            c->d_tw_col_inv = c->d_tw_row_fwd + trf.size();
+            c->d_tw_row_inv = c->d_tw_col_inv + tci.size();
+            const size_t bytes = all.size() * sizeof(ulonglong2);
+            int maxp = 0, maxw = 0;
+            if (HKS_TW_PERSIST && cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device) == cudaSuccess &&
+                cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, device) == cudaSuccess && maxp > 0 &&
+                maxw > 0) {
+                size_t cur = 0;
+                cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+                if (cur < (size_t)maxp) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp);
+                cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+                c->tw_win.base_ptr = c->d_tw_all;
+                c->tw_win.num_bytes = std::min(bytes, (size_t)maxw);
+                c->tw_win.hitRatio = (float)std::min(1.0, (double)cur / (double)c->tw_win.num_bytes);
+                c->tw_win.hitProp = cudaAccessPropertyPersisting;
+                c->tw_win.missProp = cudaAccessPropertyStreaming;
+                cudaGetLastError();
+            }
+        }
+    }
     UP(d_mu_scale, mu_scale);
     UP(d_mu_mat, mu_mat);
     UP(d_md_scale, md_scale);

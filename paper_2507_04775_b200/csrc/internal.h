@@ -15,6 +15,12 @@
 #define HKS_EXPERIMENTAL 0   // 1: also build the measured-and-rejected kernel variants and
 #endif                       //    their environment switches (tools/build_variant.sh); never the product
 
+#ifndef HKS_TW_PERSIST
+#define HKS_TW_PERSIST 0       // 1: L2 access-policy window (persisting) over the twiddle tables
+#endif
+#ifndef HKS_KEY_STREAM
+#define HKS_KEY_STREAM 0       // 1: key words loaded with the streaming (evict-first) cache hint
+#endif
 #ifndef HKS_NTT_TC_DEFAULT
 #define HKS_NTT_TC_DEFAULT 0   // log N = 16 column passes on the tensor cores (ntt_tc.cu); 0: butterfly passes
 #endif
@@ -240,8 +246,12 @@ struct hks_ctx {
 
     // device tables (owned)
     PrimeConst *d_pc = nullptr;
-    ulonglong2 *d_tw_col_fwd = nullptr, *d_tw_row_fwd = nullptr;
+    ulonglong2 *d_tw_col_fwd = nullptr, *d_tw_row_fwd = nullptr;   // all four inside d_tw_all (one allocation)
     ulonglong2 *d_tw_col_inv = nullptr, *d_tw_row_inv = nullptr;
+    ulonglong2 *d_tw_all = nullptr;
+    // L2 access-policy window over d_tw_all (num_bytes = 0: none): the NTT kernels' twiddle reads persist in
+    // L2 while the key stream passes through (HKS_TW_PERSIST)
+    cudaAccessPolicyWindow tw_win = {};
     ulonglong2 *d_ninv = nullptr;
     ulonglong2 *d_mu_scale = nullptr;   // ModUp: N^-1 * qhat_{j,i}^-1 mod q_i per (level, i)
     uint2 *d_mu_mat = nullptr;          // ModUp: [qhat_{j,i}]_t split, per (level, digit)
@@ -314,20 +324,31 @@ int hks_num_sms();
 bool prof_active();
 // pdl = false: an ordinary stream-ordered launch, for a kernel whose pre-wait prologue reads tables a
 // recent kernel of the same stream wrote (hks_bconv's device-built constants)
+// win != NULL with num_bytes > 0: the launch carries that L2 access-policy window
 template <typename... KArgs, typename... Args>
-inline cudaError_t hks_launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                                  cudaStream_t s, Args &&...args) {
+inline cudaError_t hks_launch_ex(bool pdl, const cudaAccessPolicyWindow *win, void (*kernel)(KArgs...), dim3 grid,
+                                 dim3 block, size_t smem, cudaStream_t s, Args &&...args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
-    cfg.attrs = at;
     cfg.numAttrs = 1;
+    if (win && win->num_bytes) {
+        at[1].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[1].val.accessPolicyWindow = *win;
+        cfg.numAttrs = 2;
+    }
+    cfg.attrs = at;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t hks_launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                  cudaStream_t s, Args &&...args) {
+    return hks_launch_ex(pdl, nullptr, kernel, grid, block, smem, s, std::forward<Args>(args)...);
 }
 template <typename... KArgs, typename... Args>
 inline cudaError_t hks_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -22,6 +22,21 @@
 
 #include "internal.h"
 
+// L2 window of the context whose NTT pass is being launched (set by launch_ntt_pass / launch_ntt_kip on the
+// calling thread; launches are synchronous host code)
+static thread_local const cudaAccessPolicyWindow *t_win = nullptr;
+
+#ifndef HKS_NTT_TC_MINLIMBS
+#define HKS_NTT_TC_MINLIMBS 0   // smallest column-pass batch sent to the tensor cores
+#endif
+#ifndef HKS_NTT_TC_INV
+#define HKS_NTT_TC_INV 1        // inverse column passes on the tensor cores too
+#endif
+
+#ifndef HKS_NTT_INVCOLS_MINB
+#define HKS_NTT_INVCOLS_MINB HKS_NTT_MINB   // resident CTAs requested for the inverse column pass (scale epilogue)
+#endif
+
 #ifndef HKS_KIP_TMA
 #define HKS_KIP_TMA 0     // 1: key rows prefetched into shared memory with 1D bulk copies (measured slower)
 #endif
@@ -284,7 +299,8 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
 
 template <int LOGN, int LOGE, int LOGNB, int LOGC, bool COLS, bool FWD, int EPI>
 __global__ void __launch_bounds__((1 << LOGNB) << (LOGN - LOGE),
-                                  (((1 << LOGNB) << (LOGN - LOGE)) >= 512) ? 2 : HKS_NTT_MINB)
+                                  (((1 << LOGNB) << (LOGN - LOGE)) >= 512) ? 2
+                                  : (COLS && !FWD) ? HKS_NTT_INVCOLS_MINB : HKS_NTT_MINB)
 k_ntt(const __grid_constant__ NttArgs A) {
     extern __shared__ __align__(16) u64 sm[];
     pdl_trigger();
@@ -305,7 +321,7 @@ static hks_status go(NttArgs &a, cudaStream_t s) {
     const int cls = FWD ? (COLS ? K_NTT_FWD_COLS : ((EPI == EPI_MODDOWN || EPI == EPI_MDTENSOR) ? K_NTT_FWD_ROWS_MODDOWN : K_NTT_FWD_ROWS))
                         : (COLS ? K_NTT_INV_COLS : K_NTT_INV_ROWS);
     ProfScope ps(cls, s);
-    (void)hks_launch(kern, dim3(a.nlimbs * a.tiles), dim3(threads), smem, s, a);
+    (void)hks_launch_ex(pdl_enabled(), t_win, kern, dim3(a.nlimbs * a.tiles), dim3(threads), smem, s, a);
     HKS_CHECK_LAUNCH();
     // algorithmic bytes: each limb read once and written once (+ ModDown operands acc, c0)
     double words = 2.0 * a.nlimbs;
@@ -378,12 +394,14 @@ static hks_status dispatch(NttDir dir, bool cols, int epi, NttArgs &a, cudaStrea
 #define HKS_SMALL_LIMIT (2u * 148u * 4u)
 #endif
 hks_status launch_ntt_pass(const hks_ctx *ctx, NttDir dir, int pass, int epi, NttArgs &a, cudaStream_t s) {
+    t_win = &ctx->tw_win;
     a.log_n = ctx->log_n;
     a.log_r = ctx->log_r;
     a.log_c = ctx->log_c;
     const bool cols = (dir == NTT_FWD) ? (pass == 0) : (pass == 1);
     if (cols && ctx->log_n == 16 && ctx->all_big && ctx->d_ntt_img_fwd && ntt_tc_enabled() &&
-        ((dir == NTT_FWD && epi == EPI_LAZY) || (dir == NTT_INV && epi == EPI_SCALE)))
+        a.nlimbs >= HKS_NTT_TC_MINLIMBS &&
+        ((dir == NTT_FWD && epi == EPI_LAZY) || (HKS_NTT_TC_INV && dir == NTT_INV && epi == EPI_SCALE)))
         return launch_ntt_cols_tc(ctx, dir, epi, a, s);
     const bool small = a.nlimbs * 16u < HKS_SMALL_LIMIT;
     switch (ctx->log_n) {
@@ -749,8 +767,15 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
             kb[i] = *reinterpret_cast<const ulonglong2 *>(skey + (size_t)(2 * i) * NB * n + idx);
             ka[i] = *reinterpret_cast<const ulonglong2 *>(skey + (size_t)(2 * i + 1) * NB * n + idx);
 #else
+#if HKS_KEY_STREAM
+            // each key word is read once per KeySwitch: streaming hint (evict first) keeps it from evicting
+            // the twiddle tables and the ModUp output in L2
+            kb[i] = __ldcs(reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j) * kst + idx));
+            ka[i] = __ldcs(reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j + 1) * kst + idx));
+#else
             kb[i] = *reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j) * kst + idx);
             ka[i] = *reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j + 1) * kst + idx);
+#endif
 #endif
             if (i >= (int)A.map.ntr[u]) {
                 dv[i] = *reinterpret_cast<const ulonglong2 *>(A.c1 + (size_t)(A.map.dsrc[u][i] & 0x7fff) * N + tbase + idx);
@@ -913,7 +938,7 @@ static hks_status go_kip(FusedKipArgs &a, cudaStream_t s) {
     }
     a.tiles = (1u << a.log_r) >> LOGNB;
     ProfScope ps(K_NTT_ROWS_KIP, s);
-    (void)hks_launch(kern, dim3(a.nu * a.tiles), dim3(threads), smem, s, a);
+    (void)hks_launch_ex(pdl_enabled(), t_win, kern, dim3(a.nu * a.tiles), dim3(threads), smem, s, a);
     HKS_CHECK_LAUNCH();
     // algorithmic words: D read once (pass-1 output or c1), key 2 limbs per (u, j), acc 2 limbs per u
     const double nn = (double)(1ull << a.log_n);
@@ -946,6 +971,7 @@ static hks_status go_kip_d(FusedKipArgs &a, cudaStream_t s) {
 #define HKS_KIP_LOGNB 1   // 2 rows per CTA: many small CTAs keep the three phases of co-resident CTAs staggered
 #endif                    // (measured: 4 rows 98.7 us, 2 rows 96.5 us per C2 KeySwitch)
 hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s) {
+    t_win = &ctx->tw_win;
     a.log_n = ctx->log_n;
     a.log_r = ctx->log_r;
     a.log_c = ctx->log_c;

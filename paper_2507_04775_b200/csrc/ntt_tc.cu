@@ -31,7 +31,9 @@
 
 #define NC_CW 8                 // columns per tile
 #define NC_TPL (256 / NC_CW)    // tiles per limb
+#ifndef NC_S1
 #define NC_S1 4                 // round-1 operand stages
+#endif
 #define NC_S2 2                 // round-2 operand stages
 #define NC_LOADW 3              // loader warps
 #define NC_E1W 8                // round-1 epilogue warps

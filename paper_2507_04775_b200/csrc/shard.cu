@@ -142,9 +142,12 @@ extern "C" hks_status hks_shard_ks_modup_in(const hks_ctx *c, uint32_t level, ui
 // ypsend[p][kk] = INTT(acc_p[owned P_kk]) * N^-1 [phat_k]^-1.
 // yall != NULL: sources are slots of the all-gathered buffer; else peers[r] is rank r's ysend (a local or
 // peer-mapped device address) and the base conversion reads every source limb straight from its owner.
+// digit_ready != NULL (pipelined phase B): the stream waits on digit_ready[j] before the base conversion of
+// digit j, one conversion launch per digit.
 static hks_status shard_inner(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank, const uint64_t *yall,
                               const uint64_t *const *peers, const uint64_t *c1_loc, const uint64_t *evk_loc,
-                              uint32_t evk_digits, uint64_t *acc_loc, uint64_t *ypsend, void *ws, void *stream) {
+                              uint32_t evk_digits, uint64_t *acc_loc, uint64_t *ypsend, void *ws, void *stream,
+                              const void *const *digit_ready = nullptr) {
     Plan P;
     hks_status st = make_plan(c, level, world, rank, P);
     if (st != HKS_OK || (st = dev_ctx(c)) != HKS_OK) return st;
@@ -168,8 +171,10 @@ static hks_status shard_inner(const hks_ctx *c, uint32_t level, uint32_t world, 
     // BConv per digit to the owned targets outside the digit; matrix columns of (level, digit) follow
     // the target order t in [0, ne) \ digit, so owned targets map to column positions.
     std::vector<BconvGroup> groups;
+    std::vector<size_t> gfirst;   // first group of digit j
     LimbList T;
     for (u32 j = 0; j < beta; j++) {
+        gfirst.push_back(groups.size());
         const u32 lo = c->digit_lo(j), hi = c->digit_hi(level, j);
         u16 src[BC_MAXSRC];
         const u64 *srcp[BC_MAXSRC];
@@ -207,7 +212,17 @@ static hks_status shard_inner(const hks_ctx *c, uint32_t level, uint32_t world, 
         }
         flush();
     }
-    if ((st = bconv_groups(c, groups, yall ? yall : ext, ext, s)) != HKS_OK) return st;
+    gfirst.push_back(groups.size());
+    if (!digit_ready) {
+        if ((st = bconv_groups(c, groups, yall ? yall : ext, ext, s)) != HKS_OK) return st;
+    } else {
+        for (u32 j = 0; j < beta; j++) {
+            if (digit_ready[j] && cudaStreamWaitEvent(s, (cudaEvent_t)digit_ready[j], 0) != cudaSuccess)
+                HKS_FAIL(HKS_ECUDA, "shard_ks_inner_pipelined: wait on digit %u", j);
+            std::vector<BconvGroup> gj(groups.begin() + gfirst[j], groups.begin() + gfirst[j + 1]);
+            if (!gj.empty() && (st = bconv_groups(c, gj, yall, ext, s)) != HKS_OK) return st;
+        }
+    }
     if (T.size() && (st = run_ntt_fwd_cols(c, T, ext, ext, s)) != HKS_OK) return st;
     std::vector<KipItem> items(own_t.size());
     for (u32 u = 0; u < own_t.size(); u++) {
@@ -282,6 +297,15 @@ extern "C" hks_status hks_shard_ks_inner(const hks_ctx *c, uint32_t level, uint3
                                         void *stream) {
     if (!yall) HKS_FAIL(HKS_EINVAL, "shard_ks_inner: NULL yall");
     return shard_inner(c, level, world, rank, yall, nullptr, c1_loc, evk_loc, evk_digits, acc_loc, ypsend, ws, stream);
+}
+
+extern "C" hks_status hks_shard_ks_inner_pipelined(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
+                                                  const uint64_t *yall, const void *const *digit_ready,
+                                                  const uint64_t *c1_loc, const uint64_t *evk_loc, uint32_t evk_digits,
+                                                  uint64_t *acc_loc, uint64_t *ypsend, void *ws, void *stream) {
+    if (!yall || !digit_ready) HKS_FAIL(HKS_EINVAL, "shard_ks_inner_pipelined: NULL yall / event table");
+    return shard_inner(c, level, world, rank, yall, nullptr, c1_loc, evk_loc, evk_digits, acc_loc, ypsend, ws, stream,
+                       digit_ready);
 }
 
 extern "C" hks_status hks_shard_ks_inner_peer(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,

@@ -27,6 +27,7 @@ EXPORTS = ("hks_last_error", "hks_ctx_create", "hks_ctx_destroy", "hks_ctx_query
            "hks_rotate_hoisted", "hks_rotate_hoisted_batch", "hks_rotate_hoisted_batch_workspace_bytes",
            "hks_launch_count", "hks_prof_enable", "hks_prof_read", "hks_shard_query", "hks_shard_workspace_bytes",
            "hks_shard_ks_modup_in", "hks_shard_ks_inner", "hks_shard_ks_moddown_out", "hks_shard_ks_inner_peer",
+           "hks_shard_ks_inner_pipelined",
            "hks_shard_ks_moddown_out_peer")
 
 
@@ -112,6 +113,8 @@ def lib() -> ctypes.CDLL:
         L.hks_shard_ks_modup_in.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp]
         L.hks_shard_ks_inner.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp]
         L.hks_shard_ks_moddown_out.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.hks_shard_ks_inner_pipelined.argtypes = [_vp, _u32, _u32, _u32, _vp, ctypes.POINTER(_vp), _vp, _vp, _u32, _vp,
+                                                   _vp, _vp, _vp]
         L.hks_shard_ks_inner_peer.argtypes = [_vp, _u32, _u32, _u32, ctypes.POINTER(_vp), _vp, _vp, _u32, _vp, _vp,
                                               _vp, _vp]
         L.hks_shard_ks_moddown_out_peer.argtypes = [_vp, _u32, _u32, _u32, ctypes.POINTER(_vp), _vp, _vp, _vp, _vp,
@@ -366,6 +369,17 @@ def shard_ks_inner(ctx: Context, level, world, rank, yall, c1_loc, evk_loc, acc_
     _check(lib().hks_shard_ks_inner(ctx.handle, level, world, rank, _ptr(yall), _ptr(c1_loc), _ptr(evk_loc),
                                     evk_digits(ctx, evk_loc), _ptr(acc_loc), _ptr(ypsend), _ptr(ws), _stream(stream)),
            "hks_shard_ks_inner")
+
+
+def shard_ks_inner_pipelined(ctx: Context, level, world, rank, yall, digit_events, c1_loc, evk_loc, acc_loc, ypsend,
+                             ws, stream=None):
+    """Phase B with one base-conversion launch per digit, digit j after `stream` waits on digit_events[j]
+    (torch.cuda.Event, raw cudaEvent_t int, or None)."""
+    ev = [None if e is None else (e if isinstance(e, int) else e.cuda_event) for e in digit_events]
+    arr = (_vp * max(1, len(ev)))(*ev)
+    _check(lib().hks_shard_ks_inner_pipelined(ctx.handle, level, world, rank, _ptr(yall), arr, _ptr(c1_loc),
+                                              _ptr(evk_loc), evk_digits(ctx, evk_loc), _ptr(acc_loc), _ptr(ypsend),
+                                              _ptr(ws), _stream(stream)), "hks_shard_ks_inner_pipelined")
 
 
 def _ptr_table(ptrs):

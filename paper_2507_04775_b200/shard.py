@@ -83,6 +83,95 @@ class ShardedKeySwitch:
         self.phase_c(c0_loc, out0_loc, out1_loc, stream)
 
 
+def digit_segments(ctx, level: int, world: int):
+    """Per digit j of `level`, the (owner rank, first slot, end slot) runs of its chain limbs in the gathered
+    y buffer [world][q_pad][N] (slot of limb i = r * q_pad + i - q_lo(r)): one broadcast per run delivers the
+    digit.  Host logic only (tests/test_shard.py checks it with gloo)."""
+    infos = [H.shard_query(ctx, level, world, r) for r in range(world)]
+    q_pad = infos[0].q_pad
+    q = ctx.query(level)
+    segs = []
+    for j in range(q.beta):
+        lo, hi = q.digit_lo[j], q.digit_hi[j]
+        runs = []
+        for r, s in enumerate(infos):
+            a, b = max(lo, s.q_lo), min(hi, s.q_hi)
+            if a < b:
+                runs.append((r, r * q_pad + a - s.q_lo, r * q_pad + b - s.q_lo))
+        segs.append(runs)
+    return segs
+
+
+class PipelinedShardedKeySwitch:
+    """Limb-sharded KeySwitch with the first exchange delivered digit by digit and overlapped with the base
+    conversions ("per-digit pipelined all-gather"): phase A writes this rank's scaled
+    COEFF limbs straight into its own slots of the gathered buffer; every (digit, owner) run of chain limbs is
+    then broadcast by its owner (NCCL over NVLink; async, on the process group's stream) and an event per digit
+    records its arrival on an auxiliary stream; phase B (hks_shard_ks_inner_pipelined) waits on digit j's event
+    only before digit j's conversion, so the conversion of one digit overlaps the transfer of the next.  No
+    padding: a rank receives exactly the chain limbs it does not own.  The second exchange (P-parts of the
+    accumulators) stays one all_gather_into_tensor.
+
+    `deliver_fn(j, runs, yall)` replaces the broadcasts (simulated ranks on one GPU in the tests): it must enqueue
+    the delivery of digit j on the current stream."""
+
+    def __init__(self, ctx, level: int, world: int, rank: int, device, deliver_fn=None, gather_fn=None):
+        import torch
+        self.ctx, self.level, self.world, self.rank = ctx, level, world, rank
+        self.info = H.shard_query(ctx, level, world, rank)
+        s, n = self.info, ctx.n
+        self.segments = digit_segments(ctx, level, world)
+        self.yall = torch.zeros((world * s.q_pad, n), dtype=torch.int64, device=device)
+        self.ysend = self.yall[rank * s.q_pad:(rank + 1) * s.q_pad]            # phase A output = own slots
+        self.ypsend = torch.zeros((2 * s.p_pad, n), dtype=torch.int64, device=device)
+        self.ypall = torch.empty((world * 2 * s.p_pad, n), dtype=torch.int64, device=device)
+        self.acc = torch.empty((2 * (s.nq_act + s.p_hi - s.p_lo), n), dtype=torch.int64, device=device)
+        self.ws = torch.empty((max(H.shard_workspace_bytes(ctx, level, world, rank) // 8, 1),), dtype=torch.int64,
+                              device=device)
+        self.aux = torch.cuda.Stream(device)
+        self.events = [torch.cuda.Event() for _ in self.segments]
+        self.deliver = deliver_fn
+        self.gather = gather_fn or ShardedKeySwitch._nccl_gather
+
+    def phase_a(self, c1_loc, stream=None):
+        H.shard_ks_modup_in(self.ctx, self.level, self.world, self.rank, c1_loc, self.ysend, stream)
+
+    def deliver_digits(self):
+        """enqueue every digit's delivery; events[j] fires when digit j has arrived"""
+        import torch
+        if self.deliver is not None:
+            cur = torch.cuda.current_stream()
+            self.aux.wait_stream(cur)
+            with torch.cuda.stream(self.aux):
+                for j, runs in enumerate(self.segments):
+                    self.deliver(j, runs, self.yall)
+                    self.events[j].record(self.aux)
+            return
+        import torch.distributed as dist
+        works = [[dist.broadcast(self.yall[lo:hi], src=r, async_op=True) for r, lo, hi in runs]
+                 for runs in self.segments]
+        with torch.cuda.stream(self.aux):
+            for j, ws in enumerate(works):
+                for w in ws:
+                    w.wait()
+                self.events[j].record(self.aux)
+
+    def phase_b(self, c1_loc, evk_loc, stream=None):
+        H.shard_ks_inner_pipelined(self.ctx, self.level, self.world, self.rank, self.yall, self.events, c1_loc, evk_loc,
+                                   self.acc, self.ypsend, self.ws, stream)
+
+    def phase_c(self, c0_loc, out0_loc, out1_loc, stream=None):
+        H.shard_ks_moddown_out(self.ctx, self.level, self.world, self.rank, self.ypall, self.acc, c0_loc, out0_loc,
+                               out1_loc, self.ws, stream)
+
+    def __call__(self, c0_loc, c1_loc, evk_loc, out0_loc, out1_loc, stream=None):
+        self.phase_a(c1_loc, stream)
+        self.deliver_digits()
+        self.phase_b(c1_loc, evk_loc, stream)
+        self.gather(self.ypall, self.ypsend)
+        self.phase_c(c0_loc, out0_loc, out1_loc, stream)
+
+
 class PeerShardedKeySwitch:
     """Limb-sharded KeySwitch with both exchanges fused into the base conversions:
     ysend / ypsend live in symmetric memory (torch.distributed._symmetric_memory, NVLink peer mappings),

@@ -83,3 +83,26 @@ def test_c3_ciphertext_sharded_two_ranks(orc, tmp_path):
         outs0, outs1 = o.rotate_hoisted(a["c0"], a["c1"], [a["evk"][k] for k in range(2)], m["level"], m["galois"])
         for k in range(2):
             assert (a["out0"][k] == outs0[k]).all() and (a["out1"][k] == outs1[k]).all(), (r, k)
+
+
+def test_c4_pipelined_two_ranks(orc, tmp_path):
+    """C4 limb-sharded with the first exchange as per-digit broadcasts pipelined with the conversions
+    (NEXT-3), two ranks: bit-exact with the oracle."""
+    d, line = _run(tmp_path, ["--config", "C4", "--shard", "pipe", "--sets", "1"])
+    assert "per-digit broadcasts" in line["config"]["l2"]
+    cfg = S.config("C4")
+    o = orc.Ctx.from_config(cfg)
+    nq, nk = len(cfg.q), len(cfg.q) + len(cfg.p)
+    parts = [_load(d, r) for r in range(2)]
+    level = parts[0][0]["level"]
+    c0 = np.concatenate([a["c0"] for m, a in parts])
+    c1 = np.concatenate([a["c1"] for m, a in parts])
+    got0 = np.concatenate([a["out0"] for m, a in parts])
+    got1 = np.concatenate([a["out1"] for m, a in parts])
+    evk = np.zeros((cfg.dnum, 2, nk, o.n), dtype=np.uint64)
+    for m, a in parts:
+        nql = m["q_hi"] - m["q_lo"]
+        evk[:, :, m["q_lo"]:m["q_hi"]] = a["evk"][:, :, :nql]
+        evk[:, :, nq + m["p_lo"]:nq + m["p_hi"]] = a["evk"][:, :, nql:]
+    want0, want1 = o.keyswitch(c0, c1, evk, level)
+    assert (got0 == want0).all() and (got1 == want1).all()

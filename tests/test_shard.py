@@ -79,6 +79,48 @@ def test_gloo_allgather_layout(name, level):
     assert all(ok for _, ok in res), res
 
 
+def _gloo_pipe_worker(rank, world, port, name, level, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = S.config(name)
+        ctx = H.Context.from_config(cfg, -1)
+        plan = shard.ShardPlan(ctx, level, world)
+        me = plan.info[rank]
+        segs = shard.digit_segments(ctx, level, world)
+        n = 4
+        yall = torch.full((world * me.q_pad, n), -1, dtype=torch.int64)
+        for li in range(me.nq_act):
+            yall[rank * me.q_pad + li] = me.q_lo + li           # own slots = phase A output (marker: limb index)
+        for runs in segs:                                       # one broadcast per (digit, owner) run
+            for r, lo, hi in runs:
+                dist.broadcast(yall[lo:hi], src=r)
+        ok = all(int(yall[plan.q_slot(i), 0]) == i for i in range(level + 1))
+        info = ctx.query(level)
+        for j, runs in enumerate(segs):                         # the runs of digit j are exactly its limbs
+            got = sorted(int(yall[s_, 0]) for _, lo, hi in runs for s_ in range(lo, hi))
+            ok &= got == list(range(info.digit_lo[j], info.digit_hi[j]))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,level,world", [("C4", 35, 2), ("C4", 20, 2), ("T12", 5, 2)])
+def test_gloo_digit_broadcast_layout(name, level, world):
+    """NEXT-3 pipelined exchange: per-digit broadcasts of the owners' runs fill the gathered buffer exactly as
+    the all-gather does, and each digit's runs cover that digit's limbs."""
+    ctxmp = mp.get_context("spawn")
+    q = ctxmp.Queue()
+    port = 29700 + (os.getpid() % 1000)
+    procs = [ctxmp.Process(target=_gloo_pipe_worker, args=(r, world, port, name, level, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
+
+
 # ------------------------------------------------------------------ GPU: simulated ranks
 def _oracle_ks(orc, cfg, c0, c1, evk, level):
     """the CPU oracle's KeySwitch on the device inputs (uint64 views)"""
@@ -193,3 +235,55 @@ def test_peer_phase_rejects_null_table():
     z = torch.zeros((8, cfg.n), dtype=torch.int64, device="cuda:0")
     with pytest.raises(H.HksError):
         H.shard_ks_inner_peer(ctx, 4, 2, 0, [z.data_ptr(), 0], z, z, z, z, z)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,level,world", [("T12", 6, 2), ("T12", 4, 3), ("C2", 29, 4), ("C4", 35, 8), ("C4", 35, 2),
+                                              ("C4", 17, 4)])
+def test_pipelined_sharded_keyswitch_matches_oracle(orc, name, level, world):
+    """NEXT-3 per-digit pipelined first exchange: each simulated rank receives digit j by copies of the owners'
+    runs on an auxiliary stream, recorded by an event that phase B waits on before digit j's conversion; the
+    outputs equal the CPU oracle's KeySwitch."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    dev = "cuda:0"
+    cfg = S.config(name)
+    ctx = H.Context.from_config(cfg, 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(cfg.seed + 2)
+    n = cfg.n
+    primes = list(cfg.q) + list(cfg.p)
+
+    def limbs(pr):
+        return torch.stack([torch.randint(0, int(p), (n,), generator=g, device=dev, dtype=torch.int64) for p in pr])
+
+    c0, c1 = limbs(cfg.q[: level + 1]), limbs(cfg.q[: level + 1])
+    evk = torch.stack([limbs(primes) for _ in range(2 * cfg.dnum)]).reshape(cfg.dnum, 2, len(primes), n)
+    ranks = []
+
+    def deliver_for(me):
+        def deliver(j, runs, yall):
+            for r, lo, hi in runs:
+                if r != me:
+                    yall[lo:hi].copy_(ranks[r].yall[lo:hi])
+        return deliver
+
+    ranks.extend(shard.PipelinedShardedKeySwitch(ctx, level, world, r, dev, deliver_fn=deliver_for(r),
+                                                 gather_fn=lambda o, i: None) for r in range(world))
+    loc = []
+    for ks in ranks:
+        s = ks.info
+        c0l, c1l = c0[s.q_lo:s.q_lo + s.nq_act].contiguous(), c1[s.q_lo:s.q_lo + s.nq_act].contiguous()
+        loc.append((c0l, c1l, shard.slice_key(evk, s, len(cfg.q)), torch.empty_like(c0l), torch.empty_like(c1l)))
+        ks.phase_a(c1l)
+    for r, ks in enumerate(ranks):
+        ks.deliver_digits()
+        ks.phase_b(loc[r][1], loc[r][2])
+    ypall = torch.cat([ks.ypsend for ks in ranks])
+    for r, ks in enumerate(ranks):
+        ks.ypall.copy_(ypall)
+        c0l, _, _, o0, o1 = loc[r]
+        ks.phase_c(c0l, o0, o1)
+    torch.cuda.synchronize()
+    got0, got1 = torch.cat([l[3] for l in loc]), torch.cat([l[4] for l in loc])
+    assert _equal_oracle(got0, got1, _oracle_ks(orc, cfg, c0, c1, evk, level))
