@@ -54,9 +54,10 @@ def parse():
     ap.add_argument("--dump", default=None,
                     help="directory: after the timed region every rank saves one step's inputs and outputs (.npy) "
                          "for an offline oracle check (tests/test_multirank.py)")
-    ap.add_argument("--shard", default="auto", choices=["auto", "none", "nccl", "pipe", "peer"],
+    ap.add_argument("--shard", default="auto", choices=["auto", "none", "nccl", "pipe", "a2a", "peer"],
                     help="C4 limb sharding: nccl = two NCCL all-gathers per KeySwitch; pipe = the first exchange as "
-                         "per-digit broadcasts overlapped with the conversions; peer = the exchanges fused into the "
+                         "per-digit broadcasts overlapped with the conversions; a2a = coefficient-sharded "
+                         "conversions with four all-to-alls; peer = the exchanges fused into the "
                          "base conversions over NVLink symmetric memory; none = one KeySwitch per GPU; auto = nccl "
                          "for C4 under torchrun, else none")
     return ap.parse_args()
@@ -408,6 +409,15 @@ class C4ShardWorkload:
                 ys = [torch.zeros((s0.q_pad, cfg.n), dtype=torch.int64, device=dev)]
                 yps = [torch.zeros((2 * s0.p_pad, cfg.n), dtype=torch.int64, device=dev)]
                 self.ks = shard.PeerShardedKeySwitch(ctx, level, 1, 0, dev, sim_ysend=ys, sim_ypsend=yps)
+        elif mode == "a2a":
+            def a2a_gloo(out, inp):      # HKS_BENCH_BACKEND=gloo (logic check): exchange through host tensors
+                import torch.distributed as dist
+                o = torch.empty(out.shape, dtype=out.dtype)
+                dist.all_to_all_single(o, inp.cpu())
+                out.copy_(o)
+            fn = (lambda o, i: o.copy_(i)) if world == 1 else (
+                a2a_gloo if os.environ.get("HKS_BENCH_BACKEND", "nccl") != "nccl" else None)
+            self.ks = shard.A2AShardedKeySwitch(ctx, level, world, rank, dev, a2a_fn=fn)
         elif mode == "pipe":
             self.ks = shard.PipelinedShardedKeySwitch(ctx, level, world, rank, dev,
                                                       deliver_fn=None if world > 1 else (lambda j, runs, yall: None),
@@ -451,6 +461,7 @@ class C4ShardWorkload:
         return (f"{self.nsets} rotating (ct, key) sets, {b / 2**20:.0f} MiB per rank ({l2_str()}); limbs sharded over "
                 f"{self.world} rank(s), exchange: " + {"nccl": "NCCL all-gathers", "pipe": "per-digit broadcasts "
                                                         "overlapped with BConv + all-gather",
+                                                        "a2a": "four all-to-alls, coefficient-sharded BConv",
                                                         "peer": "peer loads in BConv"}[self.mode])
 
     def dump(self, d, rank):

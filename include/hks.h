@@ -345,6 +345,52 @@ hks_status hks_shard_ks_moddown_out_peer(const hks_ctx *ctx, uint32_t level, uin
                                          const uint64_t *c0_loc, uint64_t *out0_loc, uint64_t *out1_loc, void *ws,
                                          void *stream);
 
+/* All-to-all coefficient-sharded KeySwitch (SURVEY.md §8(e) "coefficient-sharded BConv", §8(f) NEXT-3;
+ * PAPER.md:219 LimbPartition).  Same limb ownership as the phases above, but the base
+ * conversions work on a coefficient chunk of every limb instead of every coefficient of the owned limbs:
+ * rank k's chunk is rows [k R / G, (k + 1) R / G) of the R x C limb layout (N = R C, G = world, a power of two
+ * <= R), Nc = N / G words per limb.  A buffer "[G][S][Nc]" is coefficient-chunked: chunk k of slot s at
+ * (k S + s) Nc -- the input / output of torch.distributed.all_to_all_single, which sends part k to rank k.
+ * Five local phases around four all-to-alls the caller issues on the same stream:
+ *   1  hks_shard_a2a_modup_in      ysend [G][q_pad][Nc] = chunks of INTT(c1_loc) N^-1 [qhat]^-1
+ *      all-to-all #1               yrecv [G][q_pad][Nc]: rank r's active chain limbs, this rank's chunk
+ *   2  hks_shard_a2a_bconv         extsend [G][beta][n_pad][Nc]: Eq. 1 of every digit on this chunk to every
+ *                                  extended limb outside the digit, part d holding rank d's owned targets
+ *                                  (slot j n_pad + u, u = index in d's list: active chain limbs, then P limbs)
+ *      all-to-all #2               extrecv [G][beta][n_pad][Nc]: chunk r of this rank's converted limbs
+ *   3  hks_shard_a2a_inner         NTT + key inner product -> acc_loc (as hks_shard_ks_inner); ypsend
+ *                                  [G][2][p_pad][Nc] = chunks of INTT(acc_loc[P]) N^-1 [phat]^-1
+ *      all-to-all #3               yprecv [G][2][p_pad][Nc]
+ *   4  hks_shard_a2a_moddown_bconv convsend [G][2][nq_pad][Nc]: Eq. 1 P -> every active chain limb on this chunk,
+ *                                  part d holding rank d's limbs (slot p nq_pad + i - q_lo(d))
+ *      all-to-all #4               convrecv [G][2][nq_pad][Nc]
+ *   5  hks_shard_a2a_moddown_out   out_p = (acc_p - NTT(conv_p)) P^-1 (+ c0) on the owned active chain limbs
+ * Per-rank receive volume: the source chunks of all limbs plus the owned converted limbs, instead of every
+ * chain / special limb whole (all-gather).  Bit-identical to hks_keyswitch on the owned limbs.  Pad slots are
+ * never read.  ws: hks_shard_a2a_workspace_bytes.  Layouts c0/c1/out/evk/acc as the all-gather phases. */
+typedef struct hks_shard_a2a_info {
+    uint32_t chunk_words;   /* Nc = N / world */
+    uint32_t n_pad;         /* max owned extended limbs (active chain + special) over the ranks */
+    uint32_t nq_pad;        /* max owned active chain limbs over the ranks */
+    uint32_t beta;          /* digits at the level */
+} hks_shard_a2a_info;
+
+hks_status hks_shard_a2a_query(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
+                               hks_shard_a2a_info *out);
+size_t hks_shard_a2a_workspace_bytes(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank);
+hks_status hks_shard_a2a_modup_in(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
+                                  const uint64_t *c1_loc, uint64_t *ysend, void *ws, void *stream);
+hks_status hks_shard_a2a_bconv(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
+                               const uint64_t *yrecv, uint64_t *extsend, void *stream);
+hks_status hks_shard_a2a_inner(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
+                               const uint64_t *extrecv, const uint64_t *c1_loc, const uint64_t *evk_loc,
+                               uint32_t evk_digits, uint64_t *acc_loc, uint64_t *ypsend, void *ws, void *stream);
+hks_status hks_shard_a2a_moddown_bconv(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
+                                       const uint64_t *yprecv, uint64_t *convsend, void *stream);
+hks_status hks_shard_a2a_moddown_out(const hks_ctx *ctx, uint32_t level, uint32_t world, uint32_t rank,
+                                     const uint64_t *convrecv, const uint64_t *acc_loc, const uint64_t *c0_loc,
+                                     uint64_t *out0_loc, uint64_t *out1_loc, void *ws, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

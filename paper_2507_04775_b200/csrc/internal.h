@@ -53,8 +53,13 @@ enum NttEpi : int {
     EPI_SCALE = 3,     // last inverse pass: out = x * s (s = N^-1 or N^-1 * qhat^-1) canonical
     EPI_TENSOR = 4,    // first inverse pass (rows) of d2 = in * in2, d2 also stored to side (HMult)
     EPI_MDTENSOR = 5,  // EPI_MODDOWN + tensor terms: role 0 adds a0*b0, role 1 adds a0*b1 + a1*b0
-    EPI_SWITCH = 6     // first forward pass (columns) of centered SwitchModulo(in) from sw_q (Rescale)
+    EPI_SWITCH = 6,    // first forward pass (columns) of centered SwitchModulo(in) from sw_q (Rescale)
+    EPI_LAZY_CIN = 7,  // first forward pass (columns), input in the coefficient-chunked layout (below)
+    EPI_SCALE_COUT = 8 // last inverse pass (columns) as EPI_SCALE, output in the coefficient-chunked layout
 };
+// Coefficient-chunked layout (all-to-all limb sharding, shard.cu): coefficient x = r C + c of slot s lives at
+// (r >> clog) * cstride + s * (C << clog) + (r & (2^clog - 1)) C + c, i.e. chunk k = rows [k 2^clog,
+// (k + 1) 2^clog) of every limb, chunk-major.
 
 struct NttArgs {
     const u64 *in;
@@ -81,6 +86,8 @@ struct NttArgs {
     u64 sw_q;
     const u64 *sw_qmod;
     u32 log_n, log_r, log_c;   // N = R * C; R = 2^log_r rows, C = 2^log_c columns (row length)
+    u32 clog;                  // EPI_LAZY_CIN / EPI_SCALE_COUT: log2 rows per chunk
+    u64 cstride;               //   and words per chunk of the whole buffer
     u32 tiles;                 // CTAs per limb
     u32 scale_mod;
     u32 nlimbs;
@@ -399,9 +406,17 @@ struct MdOut {
     u64 galois;
 };
 // tensor != NULL (HMult): {a0, a1, b0, b1}; polynomial 0 adds a0 b0, polynomial 1 adds a0 b1 + a1 b0.
+// cin != NULL: the column pass reads limb i from the coefficient-chunked buffer cin (slot cin_slot[i], clog,
+// cstride) instead of buf, and writes buf slot L.sin[i].
+struct ChunkIn {
+    const u64 *buf;
+    u32 clog;
+    u64 cstride;
+    std::vector<u16> slot;
+};
 hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, const std::vector<uint8_t> &poly,
                            const std::vector<MdOut> &outs, u64 *buf, const u64 *acc, cudaStream_t s,
-                           const u64 *const *tensor = nullptr);
+                           const u64 *const *tensor = nullptr, const ChunkIn *cin = nullptr);
 // Rescale of npoly polynomials (top limbs already COEFF in coef slots 0..npoly-1), see ntt.cu.
 hks_status run_rescale(const hks_ctx *ctx, u32 npoly, u32 level, const u64 *x, const u64 *coef, u64 *buf,
                        u64 *const *outs, cudaStream_t s);

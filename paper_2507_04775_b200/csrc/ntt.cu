@@ -62,6 +62,7 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
     constexpr int ROWPAD = n + (n >> LOGE);
     constexpr int LOG_NLIMB = COLS ? (LOGN + LOGC) : 0;   // log2 N for the column pass
     constexpr bool MD = EPI == EPI_MODDOWN || EPI == EPI_MDTENSOR;   // ModDown-style epilogue
+    constexpr bool CIN = EPI == EPI_LAZY_CIN, COUT = EPI == EPI_SCALE_COUT;   // chunked column-pass I/O
 
     const u32 prime = A.map.prime[b];
     const u32 log_n = COLS ? (u32)LOG_NLIMB : A.log_n;
@@ -77,6 +78,11 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
     u64 *const out_base = MD ? A.outs[ob] : A.out;
     const u64 *__restrict__ src = A.in + (size_t)A.map.sin[b] * N + sub_off;
     u64 *__restrict__ dst = out_base + (size_t)A.map.sout[b] * N + sub_off;
+    // chunked layout (COLS only: element j = row j of column sub_off): chunk base + row-in-chunk offset
+    const u32 cmask = (1u << A.clog) - 1;
+    const u64 *__restrict__ csrc = A.in + ((size_t)A.map.sin[b] << (A.clog + LOGC)) + sub_off;
+    u64 *__restrict__ cdst = out_base + ((size_t)A.map.sout[b] << (A.clog + LOGC)) + sub_off;
+    auto cidx = [&](int j) -> size_t { return (size_t)((u32)j >> A.clog) * A.cstride + ((size_t)((u32)j & cmask) << LOGC); };
     const ulonglong2 *__restrict__ tw =
         COLS ? A.tw + (size_t)prime * n : A.tw + (((size_t)prime << A.log_r) + tile * NB + bsub) * n;
 
@@ -86,7 +92,7 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
 
     // epilogue constants
     ulonglong2 sc = make_ulonglong2(0, 0);
-    if (EPI == EPI_SCALE) sc = A.scale ? A.scale[b % A.scale_mod] : A.ninv[prime];
+    if (EPI == EPI_SCALE || EPI == EPI_SCALE_COUT) sc = A.scale ? A.scale[b % A.scale_mod] : A.ninv[prime];
     ulonglong2 pinv = make_ulonglong2(0, 0);
     const u64 *ea = nullptr, *eb = nullptr;
     if (MD) {
@@ -99,8 +105,8 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
     // EPI_SWITCH: the column pass loads the source-modulus COEFF limb and switches it into this prime
     const u64 sw_m = EPI == EPI_SWITCH ? A.sw_qmod[prime] : 0;
     auto epi = [&](u64 x, int j) -> u64 {
-        if (EPI == EPI_LAZY || EPI == EPI_TENSOR || EPI == EPI_SWITCH) return x;
-        if (EPI == EPI_SCALE) return csub(csub(shoup_approx(x, sc.x, sc.y, m.np), m.two_p), m.p);
+        if (EPI == EPI_LAZY || EPI == EPI_TENSOR || EPI == EPI_SWITCH || EPI == EPI_LAZY_CIN) return x;
+        if (EPI == EPI_SCALE || EPI == EPI_SCALE_COUT) return csub(csub(shoup_approx(x, sc.x, sc.y, m.np), m.two_p), m.p);
         if (EPI == EPI_CANON) return canon8(x, m);
         // EPI_MODDOWN: (a - x) * P^-1 [+ b], a canonical, x < 8p + 2^32
         u64 r = shoup_approx(ea[(size_t)j * JS] + m.eight_p + m.p - x, pinv.x, pinv.y, m.np);
@@ -175,6 +181,8 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
                 const int j = base + (k << lstride);
                 if (EPI == EPI_SWITCH && from_global)
                     v[q * Ee + k] = switch_centered(src[(size_t)j * JS], A.sw_q, sw_m, A.pc[prime]);
+                else if (CIN && from_global)
+                    v[q * Ee + k] = csrc[cidx(j)];
                 else
                     v[q * Ee + k] = from_global ? src[(size_t)j * JS] : sm[saddr(j)];
             }
@@ -231,7 +239,10 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
 #pragma unroll
                 for (int k = 0; k < Ee; k++) {
                     const int j = base + (k << lstride);
-                    dst[(size_t)j * JS] = epi(v[q * Ee + k], j);
+                    if (COUT)
+                        cdst[cidx(j)] = epi(v[q * Ee + k], j);
+                    else
+                        dst[(size_t)j * JS] = epi(v[q * Ee + k], j);
                 }
             }
         }
@@ -341,7 +352,7 @@ static hks_status go(NttArgs &a, cudaStream_t s) {
     // butterflies of this pass: N/2 per stage, LOGN stages; +1 Shoup per element for SCALE/MODDOWN
     const double nn = (double)(1ull << a.log_n);
     double muls = a.nlimbs * (nn / 2.0) * LOGN * 7.0;
-    if (EPI == EPI_SCALE || EPI == EPI_MODDOWN || EPI == EPI_MDTENSOR) muls += a.nlimbs * nn * 7.0;
+    if (EPI == EPI_SCALE || EPI == EPI_SCALE_COUT || EPI == EPI_MODDOWN || EPI == EPI_MDTENSOR) muls += a.nlimbs * nn * 7.0;
     muls += tmuls * nn;
     ps.done(words * nn * 8.0, muls);
     return HKS_OK;
@@ -350,12 +361,14 @@ static hks_status go(NttArgs &a, cudaStream_t s) {
 template <int LR, int ER, int BR, int LC, int EC, int BC>
 static hks_status dispatch(NttDir dir, bool cols, int epi, NttArgs &a, cudaStream_t s) {
     if (dir == NTT_FWD && cols && epi == EPI_SWITCH) return go<LR, ER, BR, LC, true, true, EPI_SWITCH>(a, s);
+    if (dir == NTT_FWD && cols && epi == EPI_LAZY_CIN) return go<LR, ER, BR, LC, true, true, EPI_LAZY_CIN>(a, s);
     if (dir == NTT_FWD && cols) return go<LR, ER, BR, LC, true, true, EPI_LAZY>(a, s);
     if (dir == NTT_FWD && epi == EPI_CANON) return go<LC, EC, BC, LC, false, true, EPI_CANON>(a, s);
     if (dir == NTT_FWD && epi == EPI_MODDOWN) return go<LC, EC, BC, LC, false, true, EPI_MODDOWN>(a, s);
     if (dir == NTT_FWD && epi == EPI_MDTENSOR) return go<LC, EC, BC, LC, false, true, EPI_MDTENSOR>(a, s);
     if (dir == NTT_INV && !cols && epi == EPI_TENSOR) return go<LC, EC, BC, LC, false, false, EPI_TENSOR>(a, s);
     if (dir == NTT_INV && !cols) return go<LC, EC, BC, LC, false, false, EPI_LAZY>(a, s);
+    if (dir == NTT_INV && cols && epi == EPI_SCALE_COUT) return go<LR, ER, BR, LC, true, false, EPI_SCALE_COUT>(a, s);
     if (dir == NTT_INV && cols) return go<LR, ER, BR, LC, true, false, EPI_SCALE>(a, s);
     HKS_FAIL(HKS_EINVAL, "ntt: unsupported epilogue %d", epi);
 }
@@ -499,7 +512,7 @@ hks_status run_ntt_inv_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in
 
 hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, const std::vector<uint8_t> &poly,
                            const std::vector<MdOut> &outs, u64 *buf, const u64 *acc, cudaStream_t s,
-                           const u64 *const *tensor) {
+                           const u64 *const *tensor, const ChunkIn *cin) {
     size_t off = 0;
     while (off < L.size()) {
         // one launch: at most HKS_MAXB limbs spanning at most NTT_MAXO polynomials
@@ -519,17 +532,23 @@ hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, const std::vec
         a.ninv = ctx->d_ninv;
         a.pinv = ctx->d_pinv;
         a.galois = 1;
-        // pass 0: columns, in place on buf (slots sin)
+        // pass 0: columns, in place on buf (slots sin) -- or from the chunked input
         for (u32 i = 0; i < cnt; i++) {
-            a.map.sin[i] = L.sin[off + i];
+            a.map.sin[i] = cin ? cin->slot[off + i] : L.sin[off + i];
             a.map.sout[i] = L.sin[off + i];
             a.map.prime[i] = L.prime[off + i];
         }
         a.nlimbs = cnt;
-        a.in = buf;
+        a.in = cin ? cin->buf : buf;
         a.out = buf;
         a.tw = ctx->d_tw_col_fwd;
-        hks_status st = launch_ntt_pass(ctx, NTT_FWD, 0, EPI_LAZY, a, s);
+        if (cin) {
+            a.clog = cin->clog;
+            a.cstride = cin->cstride;
+        }
+        hks_status st = launch_ntt_pass(ctx, NTT_FWD, 0, cin ? EPI_LAZY_CIN : EPI_LAZY, a, s);
+        a.clog = 0;
+        a.cstride = 0;
         if (st != HKS_OK) return st;
         // pass 1: rows, buf -> outs[...] with the ModDown epilogue
         fill_map(a, L, off, cnt, false);

@@ -332,3 +332,312 @@ extern "C" hks_status hks_shard_ks_moddown_out_peer(const hks_ctx *c, uint32_t l
     return shard_moddown(c, level, world, rank, nullptr, ypsend_ranks, acc_loc, c0_loc, out0_loc, out1_loc, ws,
                          stream);
 }
+
+// ------------------------------------------------------------------------------------------------
+// All-to-all coefficient-sharded KeySwitch (SURVEY.md §8(e) "coefficient-sharded BConv", §8(f) NEXT-3;
+// include/hks.h).  Same limb ownership as above; the base conversions run on a coefficient chunk of EVERY
+// limb instead of on every coefficient of the owned limbs, so each rank receives its chunk of the sources
+// (all-to-all #1 / #3) and then the converted chunks of its owned targets (all-to-all #2 / #4).  Rank k's
+// chunk = rows [k R / G, (k + 1) R / G) of the R x C limb layout (chunked layout: internal.h).
+namespace {
+struct A2A {
+    u32 G, logG, clog, nc;     // world, log2 world, log2 rows per chunk, words per chunk of a limb
+    u32 n_pad, nq_pad;         // max owned extended / active chain limbs over the ranks
+};
+
+hks_status make_a2a(const hks_ctx *c, const Plan &P, A2A &X) {
+    X.G = P.world;
+    X.logG = 0;
+    while ((1u << X.logG) < X.G) X.logG++;
+    if ((1u << X.logG) != X.G || X.logG > c->log_r) HKS_FAIL(HKS_EINVAL, "shard_a2a: world %u must be a power of two <= R", X.G);
+    X.clog = c->log_r - X.logG;
+    X.nc = c->n >> X.logG;
+    X.n_pad = X.nq_pad = 0;
+    for (u32 r = 0; r < P.world; r++) {
+        const u32 nq = P.qlo_r[r] >= P.level + 1 ? 0 : std::min(P.qhi_r[r], P.level + 1) - P.qlo_r[r];
+        X.nq_pad = std::max(X.nq_pad, nq);
+        X.n_pad = std::max(X.n_pad, nq + (P.phi_r[r] - P.plo_r[r]));
+    }
+    return HKS_OK;
+}
+
+// local index of extended limb t (chain t <= level, or P_{t - level - 1}) in its owner's list (active chain
+// limbs, then special limbs), and the owner
+void ext_owner(const Plan &P, u32 level, u32 t, u32 &owner, u32 &u) {
+    if (t <= level) {
+        owner = P.q_owner(t);
+        u = t - P.qlo_r[owner];
+    } else {
+        const u32 k = t - level - 1;
+        owner = P.p_owner(k);
+        const u32 nq = P.qlo_r[owner] >= level + 1 ? 0 : std::min(P.qhi_r[owner], level + 1) - P.qlo_r[owner];
+        u = nq + (k - P.plo_r[owner]);
+    }
+}
+
+// inverse NTT of L (in -> chunked out): row pass into scratch, column pass with the chunked store
+hks_status intt_chunked(const hks_ctx *c, const LimbList &L, const u64 *in, u64 *scratch, u64 *out, u32 clog,
+                        u64 cstride, const ulonglong2 *scale, u32 scale_mod, cudaStream_t s) {
+    if (L.size() > HKS_MAXB) HKS_FAIL(HKS_EINVAL, "shard_a2a: batch larger than one launch");
+    NttArgs a{};
+    a.pc = c->d_pc;
+    a.ninv = c->d_ninv;
+    a.galois = 1;
+    for (u32 i = 0; i < L.size(); i++) {
+        a.map.sin[i] = L.sin[i];
+        a.map.sout[i] = (u16)i;
+        a.map.prime[i] = L.prime[i];
+    }
+    a.nlimbs = (u32)L.size();
+    a.in = in;
+    a.out = scratch;
+    a.tw = c->d_tw_row_inv;
+    hks_status st = launch_ntt_pass(c, NTT_INV, 0, EPI_LAZY, a, s);
+    if (st != HKS_OK) return st;
+    for (u32 i = 0; i < L.size(); i++) {
+        a.map.sin[i] = (u16)i;
+        a.map.sout[i] = L.sout[i];
+    }
+    a.in = scratch;
+    a.out = out;
+    a.tw = c->d_tw_col_inv;
+    a.scale = scale;
+    a.scale_mod = scale_mod ? scale_mod : 1;
+    a.clog = clog;
+    a.cstride = cstride;
+    return launch_ntt_pass(c, NTT_INV, 1, EPI_SCALE_COUT, a, s);
+}
+}  // namespace
+
+extern "C" hks_status hks_shard_a2a_query(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
+                                          hks_shard_a2a_info *out) {
+    if (!out) HKS_FAIL(HKS_EINVAL, "shard_a2a_query: NULL out");
+    Plan P;
+    A2A X;
+    hks_status st = make_plan(c, level, world, rank, P);
+    if (st != HKS_OK || (st = make_a2a(c, P, X)) != HKS_OK) return st;
+    out->chunk_words = X.nc;
+    out->n_pad = X.n_pad;
+    out->nq_pad = X.nq_pad;
+    out->beta = c->beta(level);
+    return HKS_OK;
+}
+
+extern "C" size_t hks_shard_a2a_workspace_bytes(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank) {
+    Plan P;
+    A2A X;
+    if (make_plan(c, level, world, rank, P) != HKS_OK || make_a2a(c, P, X) != HKS_OK) return 0;
+    // ext [beta][n_own] | conv [2][nq_act] | scratch for the chunked inverse NTTs max(q_pad, 2 np_own)
+    const size_t scratch = std::max<size_t>(P.q_pad, 2 * (size_t)P.np_own);
+    return ((size_t)c->beta(level) * P.n_own + 2 * (size_t)P.nq_act + scratch) * c->n * sizeof(u64);
+}
+
+// #1 in: ysend [G][q_pad][Nc] = chunks of INTT(c1_loc) * N^-1 [qhat]^-1 (owned active chain limbs)
+extern "C" hks_status hks_shard_a2a_modup_in(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
+                                             const uint64_t *c1_loc, uint64_t *ysend, void *ws, void *stream) {
+    Plan P;
+    A2A X;
+    hks_status st = make_plan(c, level, world, rank, P);
+    if (st != HKS_OK || (st = make_a2a(c, P, X)) != HKS_OK || (st = dev_ctx(c)) != HKS_OK) return st;
+    if (P.nq_act == 0) return HKS_OK;
+    if (!c1_loc || !ysend || !ws) HKS_FAIL(HKS_EINVAL, "shard_a2a_modup_in: NULL buffer");
+    DevGuard g(c->device);
+    u64 *scratch = (u64 *)ws + ((size_t)c->beta(level) * P.n_own + 2 * (size_t)P.nq_act) * c->n;
+    LimbList L;
+    for (u32 li = 0; li < P.nq_act; li++) L.push(li, li, P.q_lo + li);
+    return intt_chunked(c, L, c1_loc, scratch, ysend, X.clog, (u64)P.q_pad * X.nc,
+                        c->d_mu_scale + c->mu_scale_off[level] + P.q_lo, P.nq_act, (cudaStream_t)stream);
+}
+
+// #1 out -> #2 in: yrecv [G][q_pad][Nc] (rank r's limbs at r) -> extsend [G][beta][n_pad][Nc]: for every digit
+// j, Eq. 1 on this rank's coefficient chunk to every extended limb outside the digit, placed for its owner
+extern "C" hks_status hks_shard_a2a_bconv(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
+                                          const uint64_t *yrecv, uint64_t *extsend, void *stream) {
+    Plan P;
+    A2A X;
+    hks_status st = make_plan(c, level, world, rank, P);
+    if (st != HKS_OK || (st = make_a2a(c, P, X)) != HKS_OK || (st = dev_ctx(c)) != HKS_OK) return st;
+    if (!yrecv || !extsend) HKS_FAIL(HKS_EINVAL, "shard_a2a_bconv: NULL buffer");
+    const u32 beta = c->beta(level), ne = c->ne(level);
+    if ((size_t)world * beta * X.n_pad > 0xffff) HKS_FAIL(HKS_EINVAL, "shard_a2a_bconv: too many slots");
+    DevGuard g(c->device);
+    std::vector<BconvGroup> groups;
+    for (u32 j = 0; j < beta; j++) {
+        const u32 lo = c->digit_lo(j), hi = c->digit_hi(level, j);
+        u16 src[BC_MAXSRC];
+        for (u32 i = lo; i < hi; i++) {
+            const u32 r = P.q_owner(i);
+            src[i - lo] = (u16)(r * P.q_pad + (i - P.qlo_r[r]));
+        }
+        std::vector<u16> ds, dp;
+        for (u32 t = 0; t < ne; t++) {
+            if (t >= lo && t < hi) continue;
+            u32 d, u;
+            ext_owner(P, level, t, d, u);
+            ds.push_back((u16)(d * beta * X.n_pad + j * X.n_pad + u));
+            dp.push_back((u16)c->ext_prime(level, t));
+        }
+        const size_t moff = c->mu_mat_off[(size_t)level * c->dnum + j];
+        push_group(groups, hi - lo, src, c->d_mu_mat + moff, (u32)ds.size(), ds, dp, tab_at(c->d_mu_matf, 3 * moff),
+                   c->d_mu_mats + moff, tab_at(c->d_mu_matb, 8 * moff),
+                   c->d_mu_img + c->mu_img_off[(size_t)level * c->dnum + j]);
+    }
+    // the conversion kernels address limbs of Nc words: log N of a chunk
+    std::vector<BconvGroup> gs(groups);
+    size_t i = 0;
+    while (i < gs.size()) {
+        BconvArgs a{};
+        a.in = yrecv;
+        a.out = extsend;
+        a.pc = c->d_pc;
+        a.log_n = c->log_n - X.logG;
+        a.lazy_out = 1;
+        a.big = c->all_big ? 1 : 0;
+        u32 ns = gs[i].nsrc, k = 0;
+        while (i < gs.size() && k < BC_MAXG && gs[i].nsrc == ns) a.g[k++] = gs[i++];
+        a.ngroups = k;
+        if ((st = launch_bconv(a, BC_MAXDST, (cudaStream_t)stream)) != HKS_OK) return st;
+    }
+    return HKS_OK;
+}
+
+// #2 out -> #3 in: extrecv [G][beta][n_pad][Nc] (chunk r of the owned extended limbs) -> NTT, key inner product
+// -> acc_loc; ypsend [G][2][p_pad][Nc] = chunks of INTT(acc_loc[P]) * N^-1 [phat]^-1
+extern "C" hks_status hks_shard_a2a_inner(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
+                                          const uint64_t *extrecv, const uint64_t *c1_loc, const uint64_t *evk_loc,
+                                          uint32_t evk_digits, uint64_t *acc_loc, uint64_t *ypsend, void *ws,
+                                          void *stream) {
+    Plan P;
+    A2A X;
+    hks_status st = make_plan(c, level, world, rank, P);
+    if (st != HKS_OK || (st = make_a2a(c, P, X)) != HKS_OK || (st = dev_ctx(c)) != HKS_OK) return st;
+    if (!extrecv || !evk_loc || !acc_loc || !ypsend || !ws || (P.nq_act && !c1_loc))
+        HKS_FAIL(HKS_EINVAL, "shard_a2a_inner: NULL buffer");
+    const u32 beta = c->beta(level);
+    if (beta > FK_MAXD) HKS_FAIL(HKS_EINVAL, "shard_a2a_inner: beta %u > %d", beta, FK_MAXD);
+    if (evk_digits < beta || evk_digits > c->dnum)
+        HKS_FAIL(HKS_EKEY, "shard_a2a_inner: key has %u digits; level %u needs %u (context dnum %u)", evk_digits, level,
+                 beta, c->dnum);
+    DevGuard g(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    u64 *ext = (u64 *)ws;
+    u64 *scratch = ext + ((size_t)beta * P.n_own + 2 * (size_t)P.nq_act) * c->n;
+    std::vector<u32> own_t;
+    for (u32 li = 0; li < P.nq_act; li++) own_t.push_back(P.q_lo + li);
+    for (u32 k = P.p_lo; k < P.p_hi; k++) own_t.push_back(level + 1 + k);
+    // forward column pass of every converted (digit, owned target) limb, from the chunked receive buffer
+    LimbList T;
+    for (u32 j = 0; j < beta; j++) {
+        const u32 lo = c->digit_lo(j), hi = c->digit_hi(level, j);
+        for (u32 u = 0; u < own_t.size(); u++) {
+            const u32 t = own_t[u];
+            if (t >= lo && t < hi) continue;
+            T.push(j * X.n_pad + u, j * P.n_own + u, c->ext_prime(level, t));
+        }
+    }
+    for (size_t off = 0; off < T.size(); off += HKS_MAXB) {
+        const u32 cnt = (u32)std::min<size_t>(HKS_MAXB, T.size() - off);
+        NttArgs a{};
+        a.pc = c->d_pc;
+        a.ninv = c->d_ninv;
+        a.galois = 1;
+        for (u32 i = 0; i < cnt; i++) {
+            a.map.sin[i] = T.sin[off + i];
+            a.map.sout[i] = T.sout[off + i];
+            a.map.prime[i] = T.prime[off + i];
+        }
+        a.nlimbs = cnt;
+        a.in = extrecv;
+        a.out = ext;
+        a.tw = c->d_tw_col_fwd;
+        a.clog = X.clog;
+        a.cstride = (u64)beta * X.n_pad * X.nc;
+        if ((st = launch_ntt_pass(c, NTT_FWD, 0, EPI_LAZY_CIN, a, s)) != HKS_OK) return st;
+    }
+    std::vector<KipItem> items(own_t.size());
+    for (u32 u = 0; u < own_t.size(); u++) {
+        const u32 t = own_t[u];
+        KipItem &it = items[u];
+        it.prime = (u16)c->ext_prime(level, t);
+        it.kslot = (u16)(t <= level ? t - P.q_lo : (P.q_hi - P.q_lo) + (t - level - 1 - P.p_lo));
+        it.aslot = (u16)u;
+        for (u32 j = 0; j < beta; j++) {
+            const bool own = t <= level && t >= c->digit_lo(j) && t < c->digit_hi(level, j);
+            it.src[j] = own ? (u16)(FK_DIRECT | (t - P.q_lo)) : (u16)(j * P.n_own + u);
+        }
+    }
+    if ((st = run_ntt_kip(c, items, beta, ext, c1_loc, evk_loc, acc_loc, P.nkey, P.n_own, s)) != HKS_OK) return st;
+    if (P.np_own) {
+        LimbList L;
+        for (u32 p = 0; p < 2; p++)
+            for (u32 kk = 0; kk < P.np_own; kk++) L.push(p * P.n_own + P.nq_act + kk, p * P.p_pad + kk, c->nq + P.p_lo + kk);
+        if ((st = intt_chunked(c, L, acc_loc, scratch, ypsend, X.clog, (u64)2 * P.p_pad * X.nc, c->d_md_scale + P.p_lo,
+                               P.np_own, s)) != HKS_OK)
+            return st;
+    }
+    return HKS_OK;
+}
+
+// #3 out -> #4 in: yprecv [G][2][p_pad][Nc] -> convsend [G][2][nq_pad][Nc]: Eq. 1 P -> every active chain limb on
+// this rank's chunk, placed for the chain limb's owner
+extern "C" hks_status hks_shard_a2a_moddown_bconv(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
+                                                  const uint64_t *yprecv, uint64_t *convsend, void *stream) {
+    Plan P;
+    A2A X;
+    hks_status st = make_plan(c, level, world, rank, P);
+    if (st != HKS_OK || (st = make_a2a(c, P, X)) != HKS_OK || (st = dev_ctx(c)) != HKS_OK) return st;
+    if (!yprecv || !convsend) HKS_FAIL(HKS_EINVAL, "shard_a2a_moddown_bconv: NULL buffer");
+    const u32 K = c->np;
+    DevGuard g(c->device);
+    std::vector<BconvGroup> groups;
+    for (u32 p = 0; p < 2; p++) {
+        u16 src[BC_MAXSRC];
+        for (u32 k = 0; k < K; k++) {
+            const u32 r = P.p_owner(k);
+            src[k] = (u16)(r * 2 * P.p_pad + p * P.p_pad + (k - P.plo_r[r]));
+        }
+        std::vector<u16> ds(level + 1), dp(level + 1);
+        for (u32 i = 0; i <= level; i++) {
+            const u32 d = P.q_owner(i);
+            ds[i] = (u16)(d * 2 * X.nq_pad + p * X.nq_pad + (i - P.qlo_r[d]));
+            dp[i] = (u16)i;
+        }
+        push_group(groups, K, src, c->d_md_mat, c->nq, ds, dp, c->d_md_matf, c->d_md_mats, c->d_md_matb, c->d_md_img);
+    }
+    BconvArgs a{};
+    a.in = yprecv;
+    a.out = convsend;
+    a.pc = c->d_pc;
+    a.log_n = c->log_n - X.logG;
+    a.lazy_out = 1;
+    a.big = c->all_big ? 1 : 0;
+    for (size_t k = 0; k < groups.size(); k++) a.g[k] = groups[k];
+    a.ngroups = (u32)groups.size();
+    return launch_bconv(a, BC_MAXDST, (cudaStream_t)stream);
+}
+
+// #4 out: convrecv [G][2][nq_pad][Nc] (chunk r of this rank's conv limbs) -> out_p = (acc_p - NTT(conv_p)) P^-1
+// (+ c0 on p = 0) for the owned active chain limbs
+extern "C" hks_status hks_shard_a2a_moddown_out(const hks_ctx *c, uint32_t level, uint32_t world, uint32_t rank,
+                                                const uint64_t *convrecv, const uint64_t *acc_loc, const uint64_t *c0_loc,
+                                                uint64_t *out0_loc, uint64_t *out1_loc, void *ws, void *stream) {
+    Plan P;
+    A2A X;
+    hks_status st = make_plan(c, level, world, rank, P);
+    if (st != HKS_OK || (st = make_a2a(c, P, X)) != HKS_OK || (st = dev_ctx(c)) != HKS_OK) return st;
+    if (P.nq_act == 0) return HKS_OK;
+    if (!convrecv || !acc_loc || !out0_loc || !out1_loc || !ws) HKS_FAIL(HKS_EINVAL, "shard_a2a_moddown_out: NULL buffer");
+    DevGuard g(c->device);
+    u64 *conv = (u64 *)ws + (size_t)c->beta(level) * P.n_own * c->n;
+    LimbList M;
+    std::vector<uint8_t> poly;
+    ChunkIn cin{convrecv, X.clog, (u64)2 * X.nq_pad * X.nc, {}};
+    for (u32 p = 0; p < 2; p++)
+        for (u32 li = 0; li < P.nq_act; li++) {
+            M.push(p * P.nq_act + li, li, P.q_lo + li, p * P.n_own + li, (p == 0 && c0_loc) ? li : 0xffff);
+            poly.push_back((uint8_t)p);
+            cin.slot.push_back((u16)(p * X.nq_pad + li));
+        }
+    std::vector<MdOut> mo = {MdOut{out0_loc, c0_loc, 1}, MdOut{out1_loc, nullptr, 1}};
+    return run_ntt_moddown(c, M, poly, mo, conv, acc_loc, (cudaStream_t)stream, nullptr, &cin);
+}

@@ -27,7 +27,9 @@ EXPORTS = ("hks_last_error", "hks_ctx_create", "hks_ctx_destroy", "hks_ctx_query
            "hks_rotate_hoisted", "hks_rotate_hoisted_batch", "hks_rotate_hoisted_batch_workspace_bytes",
            "hks_launch_count", "hks_prof_enable", "hks_prof_read", "hks_shard_query", "hks_shard_workspace_bytes",
            "hks_shard_ks_modup_in", "hks_shard_ks_inner", "hks_shard_ks_moddown_out", "hks_shard_ks_inner_peer",
-           "hks_shard_ks_inner_pipelined",
+           "hks_shard_ks_inner_pipelined", "hks_shard_a2a_query", "hks_shard_a2a_workspace_bytes",
+           "hks_shard_a2a_modup_in", "hks_shard_a2a_bconv", "hks_shard_a2a_inner", "hks_shard_a2a_moddown_bconv",
+           "hks_shard_a2a_moddown_out",
            "hks_shard_ks_moddown_out_peer")
 
 
@@ -45,6 +47,10 @@ class ProfEntry(ctypes.Structure):
 class ShardInfo(ctypes.Structure):
     _fields_ = [(f, ctypes.c_uint32) for f in ("world", "rank", "level", "q_lo", "q_hi", "p_lo", "p_hi", "nq_act",
                                                 "q_pad", "p_pad", "nkey")]
+
+
+class A2AInfo(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_uint32) for f in ("chunk_words", "n_pad", "nq_pad", "beta")]
 
 
 class Info(ctypes.Structure):
@@ -115,6 +121,14 @@ def lib() -> ctypes.CDLL:
         L.hks_shard_ks_moddown_out.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         L.hks_shard_ks_inner_pipelined.argtypes = [_vp, _u32, _u32, _u32, _vp, ctypes.POINTER(_vp), _vp, _vp, _u32, _vp,
                                                    _vp, _vp, _vp]
+        L.hks_shard_a2a_query.argtypes = [_vp, _u32, _u32, _u32, ctypes.POINTER(A2AInfo)]
+        L.hks_shard_a2a_workspace_bytes.argtypes = [_vp, _u32, _u32, _u32]
+        L.hks_shard_a2a_workspace_bytes.restype = ctypes.c_size_t
+        L.hks_shard_a2a_modup_in.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp, _vp]
+        L.hks_shard_a2a_bconv.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp]
+        L.hks_shard_a2a_inner.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp]
+        L.hks_shard_a2a_moddown_bconv.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp]
+        L.hks_shard_a2a_moddown_out.argtypes = [_vp, _u32, _u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         L.hks_shard_ks_inner_peer.argtypes = [_vp, _u32, _u32, _u32, ctypes.POINTER(_vp), _vp, _vp, _u32, _vp, _vp,
                                               _vp, _vp]
         L.hks_shard_ks_moddown_out_peer.argtypes = [_vp, _u32, _u32, _u32, ctypes.POINTER(_vp), _vp, _vp, _vp, _vp,
@@ -122,6 +136,7 @@ def lib() -> ctypes.CDLL:
         for f in EXPORTS[1:]:
             if f not in ("hks_ctx_destroy", "hks_workspace_bytes", "hks_launch_count", "hks_shard_workspace_bytes",
                          "hks_rotate_hoisted_batch_workspace_bytes", "hks_bconv_workspace_bytes",
+                         "hks_shard_a2a_workspace_bytes",
                          "hks_linear_transform_workspace_bytes"):
                 getattr(L, f).restype = ctypes.c_int
         _lib = L
@@ -410,3 +425,42 @@ def shard_ks_moddown_out(ctx: Context, level, world, rank, ypall, acc_loc, c0_lo
     _check(lib().hks_shard_ks_moddown_out(ctx.handle, level, world, rank, _ptr(ypall), _ptr(acc_loc), _ptr(c0_loc),
                                           _ptr(out0_loc), _ptr(out1_loc), _ptr(ws), _stream(stream)),
            "hks_shard_ks_moddown_out")
+
+
+# ---- all-to-all coefficient-sharded KeySwitch (include/hks.h "All-to-all coefficient-sharded KeySwitch")
+def shard_a2a_query(ctx: Context, level: int, world: int, rank: int) -> A2AInfo:
+    info = A2AInfo()
+    _check(lib().hks_shard_a2a_query(ctx.handle, level, world, rank, ctypes.byref(info)), "hks_shard_a2a_query")
+    return info
+
+
+def shard_a2a_workspace_bytes(ctx: Context, level: int, world: int, rank: int) -> int:
+    return int(lib().hks_shard_a2a_workspace_bytes(ctx.handle, level, world, rank))
+
+
+def shard_a2a_modup_in(ctx: Context, level, world, rank, c1_loc, ysend, ws, stream=None):
+    _check(lib().hks_shard_a2a_modup_in(ctx.handle, level, world, rank, _ptr(c1_loc), _ptr(ysend), _ptr(ws),
+                                        _stream(stream)), "hks_shard_a2a_modup_in")
+
+
+def shard_a2a_bconv(ctx: Context, level, world, rank, yrecv, extsend, stream=None):
+    _check(lib().hks_shard_a2a_bconv(ctx.handle, level, world, rank, _ptr(yrecv), _ptr(extsend), _stream(stream)),
+           "hks_shard_a2a_bconv")
+
+
+def shard_a2a_inner(ctx: Context, level, world, rank, extrecv, c1_loc, evk_loc, acc_loc, ypsend, ws, stream=None):
+    _check(lib().hks_shard_a2a_inner(ctx.handle, level, world, rank, _ptr(extrecv), _ptr(c1_loc), _ptr(evk_loc),
+                                     evk_digits(ctx, evk_loc), _ptr(acc_loc), _ptr(ypsend), _ptr(ws), _stream(stream)),
+           "hks_shard_a2a_inner")
+
+
+def shard_a2a_moddown_bconv(ctx: Context, level, world, rank, yprecv, convsend, stream=None):
+    _check(lib().hks_shard_a2a_moddown_bconv(ctx.handle, level, world, rank, _ptr(yprecv), _ptr(convsend),
+                                             _stream(stream)), "hks_shard_a2a_moddown_bconv")
+
+
+def shard_a2a_moddown_out(ctx: Context, level, world, rank, convrecv, acc_loc, c0_loc, out0_loc, out1_loc, ws,
+                          stream=None):
+    _check(lib().hks_shard_a2a_moddown_out(ctx.handle, level, world, rank, _ptr(convrecv), _ptr(acc_loc),
+                                           _ptr(c0_loc), _ptr(out0_loc), _ptr(out1_loc), _ptr(ws), _stream(stream)),
+           "hks_shard_a2a_moddown_out")

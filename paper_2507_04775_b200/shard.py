@@ -172,6 +172,63 @@ class PipelinedShardedKeySwitch:
         self.phase_c(c0_loc, out0_loc, out1_loc, stream)
 
 
+class A2AShardedKeySwitch:
+    """Limb-sharded KeySwitch with coefficient-sharded base conversions: four
+    all_to_all_single exchanges instead of two all-gathers.  Rank k converts coefficient chunk k (rows
+    [k R / G, (k + 1) R / G)) of every limb, so it receives the chunk of every source limb and then its own
+    converted limbs' chunks -- about 30 instead of 47 MiB per GPU at C4 / G = 8.  The math
+    is in libhks (hks_shard_a2a_*); `a2a_fn(out, inp)` replaces the collective (simulated ranks in tests)."""
+
+    def __init__(self, ctx, level: int, world: int, rank: int, device, a2a_fn=None):
+        import torch
+        self.ctx, self.level, self.world, self.rank = ctx, level, world, rank
+        self.info = H.shard_query(ctx, level, world, rank)
+        x = self.a2a_info = H.shard_a2a_query(ctx, level, world, rank)
+        s, nc, G, n = self.info, x.chunk_words, world, ctx.n
+        mk = lambda rows, cols: torch.zeros((rows, cols), dtype=torch.int64, device=device)
+        self.ysend, self.yrecv = mk(G * s.q_pad, nc), mk(G * s.q_pad, nc)
+        self.extsend, self.extrecv = mk(G * x.beta * x.n_pad, nc), mk(G * x.beta * x.n_pad, nc)
+        self.ypsend, self.yprecv = mk(G * 2 * s.p_pad, nc), mk(G * 2 * s.p_pad, nc)
+        self.convsend, self.convrecv = mk(G * 2 * x.nq_pad, nc), mk(G * 2 * x.nq_pad, nc)
+        self.acc = torch.empty((2 * (s.nq_act + s.p_hi - s.p_lo), n), dtype=torch.int64, device=device)
+        self.ws = torch.empty((max(H.shard_a2a_workspace_bytes(ctx, level, world, rank) // 8, 1),), dtype=torch.int64,
+                              device=device)
+        self.a2a = a2a_fn or self._nccl_a2a
+
+    @staticmethod
+    def _nccl_a2a(out, inp):
+        import torch.distributed as dist
+        dist.all_to_all_single(out, inp)
+
+    def phase1(self, c1_loc, stream=None):
+        H.shard_a2a_modup_in(self.ctx, self.level, self.world, self.rank, c1_loc, self.ysend, self.ws, stream)
+
+    def phase2(self, stream=None):
+        H.shard_a2a_bconv(self.ctx, self.level, self.world, self.rank, self.yrecv, self.extsend, stream)
+
+    def phase3(self, c1_loc, evk_loc, stream=None):
+        H.shard_a2a_inner(self.ctx, self.level, self.world, self.rank, self.extrecv, c1_loc, evk_loc, self.acc,
+                          self.ypsend, self.ws, stream)
+
+    def phase4(self, stream=None):
+        H.shard_a2a_moddown_bconv(self.ctx, self.level, self.world, self.rank, self.yprecv, self.convsend, stream)
+
+    def phase5(self, c0_loc, out0_loc, out1_loc, stream=None):
+        H.shard_a2a_moddown_out(self.ctx, self.level, self.world, self.rank, self.convrecv, self.acc, c0_loc, out0_loc,
+                                out1_loc, self.ws, stream)
+
+    def __call__(self, c0_loc, c1_loc, evk_loc, out0_loc, out1_loc, stream=None):
+        self.phase1(c1_loc, stream)
+        self.a2a(self.yrecv, self.ysend)
+        self.phase2(stream)
+        self.a2a(self.extrecv, self.extsend)
+        self.phase3(c1_loc, evk_loc, stream)
+        self.a2a(self.yprecv, self.ypsend)
+        self.phase4(stream)
+        self.a2a(self.convrecv, self.convsend)
+        self.phase5(c0_loc, out0_loc, out1_loc, stream)
+
+
 class PeerShardedKeySwitch:
     """Limb-sharded KeySwitch with both exchanges fused into the base conversions:
     ysend / ypsend live in symmetric memory (torch.distributed._symmetric_memory, NVLink peer mappings),

@@ -85,11 +85,13 @@ def test_c3_ciphertext_sharded_two_ranks(orc, tmp_path):
             assert (a["out0"][k] == outs0[k]).all() and (a["out1"][k] == outs1[k]).all(), (r, k)
 
 
-def test_c4_pipelined_two_ranks(orc, tmp_path):
-    """C4 limb-sharded with the first exchange as per-digit broadcasts pipelined with the conversions
-    (NEXT-3), two ranks: bit-exact with the oracle."""
-    d, line = _run(tmp_path, ["--config", "C4", "--shard", "pipe", "--sets", "1"])
-    assert "per-digit broadcasts" in line["config"]["l2"]
+@pytest.mark.parametrize("mode,tag", [("pipe", "per-digit broadcasts"), ("a2a", "four all-to-alls")])
+def test_c4_exchange_variants_two_ranks(orc, tmp_path, mode, tag):
+    """C4 limb-sharded with the NEXT-3 exchange variants, two ranks: the first exchange as per-digit broadcasts
+    pipelined with the conversions (pipe), or coefficient-sharded conversions with four all-to-alls (a2a);
+    bit-exact with the oracle."""
+    d, line = _run(tmp_path, ["--config", "C4", "--shard", mode, "--sets", "1"])
+    assert tag in line["config"]["l2"]
     cfg = S.config("C4")
     o = orc.Ctx.from_config(cfg)
     nq, nk = len(cfg.q), len(cfg.q) + len(cfg.p)

@@ -121,6 +121,49 @@ def test_gloo_digit_broadcast_layout(name, level, world):
     assert all(ok for _, ok in res), res
 
 
+def _gloo_a2a_worker(rank, world, port, name, level, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = S.config(name)
+        ctx = H.Context.from_config(cfg, -1)
+        infos = [H.shard_query(ctx, level, world, r) for r in range(world)]
+        me = infos[rank]
+        nc = H.shard_a2a_query(ctx, level, world, rank).chunk_words
+        assert nc * world == cfg.n
+        # chunked send buffer [G][q_pad][Nc]: chunk k of own limb li carries (limb index, chunk k)
+        ysend = torch.full((world * me.q_pad, 2), -1, dtype=torch.int64)
+        for k in range(world):
+            for li in range(me.nq_act):
+                ysend[k * me.q_pad + li] = torch.tensor([me.q_lo + li, k])
+        yrecv = torch.empty_like(ysend)
+        dist.all_to_all_single(yrecv, ysend)
+        # after the exchange: slot r * q_pad + (i - q_lo(r)) holds chain limb i, this rank's chunk
+        ok = True
+        for i in range(level + 1):
+            r = next(r for r, s_ in enumerate(infos) if s_.q_lo <= i < s_.q_hi)
+            ok &= yrecv[r * me.q_pad + i - infos[r].q_lo].tolist() == [i, rank]
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,level,world", [("C4", 35, 2), ("C4", 17, 2), ("T12", 6, 2)])
+def test_gloo_a2a_chunk_layout(name, level, world):
+    """NEXT-3 coefficient-sharded exchange: all_to_all_single of the chunked send buffers gives every rank its
+    chunk of every active chain limb at the all-gather slot positions (include/hks.h, phase 1 -> 2)."""
+    ctxmp = mp.get_context("spawn")
+    q = ctxmp.Queue()
+    port = 29900 + (os.getpid() % 1000)
+    procs = [ctxmp.Process(target=_gloo_a2a_worker, args=(r, world, port, name, level, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
+
+
 # ------------------------------------------------------------------ GPU: simulated ranks
 def _oracle_ks(orc, cfg, c0, c1, evk, level):
     """the CPU oracle's KeySwitch on the device inputs (uint64 views)"""
@@ -284,6 +327,61 @@ def test_pipelined_sharded_keyswitch_matches_oracle(orc, name, level, world):
         ks.ypall.copy_(ypall)
         c0l, _, _, o0, o1 = loc[r]
         ks.phase_c(c0l, o0, o1)
+    torch.cuda.synchronize()
+    got0, got1 = torch.cat([l[3] for l in loc]), torch.cat([l[4] for l in loc])
+    assert _equal_oracle(got0, got1, _oracle_ks(orc, cfg, c0, c1, evk, level))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,level,world", [("T12", 6, 2), ("T12", 4, 4), ("C2", 29, 4), ("C2", 12, 2), ("C4", 35, 8),
+                                              ("C4", 35, 2), ("C4", 17, 4)])
+def test_a2a_sharded_keyswitch_matches_oracle(orc, name, level, world):
+    """NEXT-3 coefficient-sharded base conversions: four all-to-alls (simulated between ranks on one GPU:
+    part k of rank r's send buffer -> part r of rank k's receive buffer); the outputs equal the oracle's."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    dev = "cuda:0"
+    cfg = S.config(name)
+    ctx = H.Context.from_config(cfg, 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(cfg.seed + 3)
+    n = cfg.n
+    primes = list(cfg.q) + list(cfg.p)
+
+    def limbs(pr):
+        return torch.stack([torch.randint(0, int(p), (n,), generator=g, device=dev, dtype=torch.int64) for p in pr])
+
+    c0, c1 = limbs(cfg.q[: level + 1]), limbs(cfg.q[: level + 1])
+    evk = torch.stack([limbs(primes) for _ in range(2 * cfg.dnum)]).reshape(cfg.dnum, 2, len(primes), n)
+    ranks = [shard.A2AShardedKeySwitch(ctx, level, world, r, dev, a2a_fn=lambda o, i: None) for r in range(world)]
+
+    def exchange(name_s, name_r):
+        sends = [getattr(k, name_s) for k in ranks]
+        for kk, k in enumerate(ranks):
+            recv = getattr(k, name_r)
+            part = recv.shape[0] // world
+            for r in range(world):
+                recv[r * part:(r + 1) * part].copy_(sends[r][kk * part:(kk + 1) * part])
+
+    loc = []
+    for ks in ranks:
+        s = ks.info
+        c0l, c1l = c0[s.q_lo:s.q_lo + s.nq_act].contiguous(), c1[s.q_lo:s.q_lo + s.nq_act].contiguous()
+        loc.append((c0l, c1l, shard.slice_key(evk, s, len(cfg.q)), torch.empty_like(c0l), torch.empty_like(c1l)))
+        ks.phase1(c1l)
+    exchange("ysend", "yrecv")
+    for ks in ranks:
+        ks.phase2()
+    exchange("extsend", "extrecv")
+    for r, ks in enumerate(ranks):
+        ks.phase3(loc[r][1], loc[r][2])
+    exchange("ypsend", "yprecv")
+    for ks in ranks:
+        ks.phase4()
+    exchange("convsend", "convrecv")
+    for r, ks in enumerate(ranks):
+        c0l, _, _, o0, o1 = loc[r]
+        ks.phase5(c0l, o0, o1)
     torch.cuda.synchronize()
     got0, got1 = torch.cat([l[3] for l in loc]), torch.cat([l[4] for l in loc])
     assert _equal_oracle(got0, got1, _oracle_ks(orc, cfg, c0, c1, evk, level))
