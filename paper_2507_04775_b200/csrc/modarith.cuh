@@ -380,26 +380,33 @@ HKS_DEV u64 shoup_u32(u32 y, u64 w, u64 wp, u64 np) {
 // [0, 3p) lazily, else canonical.  X' = a + T67 2^48 with a = T01 + T23 2^16 + T45 2^32 < 2^64 and
 // T_{c,c+1} = S_c + S_{c+1} 2^8 < 2^32.  Quotient estimate q = floor((X' >> 48) mu / 2^32) with
 // mu = floor(2^80 / p): q <= X'/p < q + 3 (truncations cost < 1 + 2^48/p), so X' - q p < 3p is
-// exact in 64-bit arithmetic.  14 instructions.
+// exact in 64-bit arithmetic.  The byte combinations are funnel shifts and adds, which ptxas emits as
+// LEA.HI on the ALU pipe (a plain shl + add, or a mad by 256, becomes an IMAD on the FMA-heavy pipe),
+// so that the heavy pipe carries little more than the quotient step: ~12 SASS instructions per output.
 template <bool LAZY>
 HKS_DEV u64 bytesum_reduce_c(u32 s0, u32 s1, u32 s2, u32 s3, u32 s4, u32 s5, u32 s6, u32 s7, u64 np, u32 mu) {
     u64 r;
     asm("{\n\t"
-        ".reg .u32 t01, t23, t45, t67, x, al, ah, top, q, rl, rh, n0, n1;\n\t"
-        ".reg .u64 w, aa, rr;\n\t"
-        "mad.lo.u32 t01, %2, 256, %1;\n\t"
-        "mad.lo.u32 t23, %4, 256, %3;\n\t"
-        "mad.lo.u32 t45, %6, 256, %5;\n\t"
-        "mad.lo.u32 t67, %8, 256, %7;\n\t"
-        "mul.wide.u32 w, t23, 65536;\n\t"
-        "mov.b64 {al, ah}, w;\n\t"
-        "add.cc.u32 al, al, t01;\n\t"
-        "addc.u32 ah, ah, t45;\n\t"                 // a = (al, ah)
+        ".reg .u32 t01, t23, t45, t67, x, y, al, ah, top, q, n0, n1, rl, rh;\n\t"
+        ".reg .u64 aa, rr;\n\t"
+        "shf.l.wrap.b32 x, %2, %2, 8;\n\t"
+        "add.u32 t01, x, %1;\n\t"
+        "shf.l.wrap.b32 x, %4, %4, 8;\n\t"
+        "add.u32 t23, x, %3;\n\t"
+        "shf.l.wrap.b32 x, %6, %6, 8;\n\t"
+        "add.u32 t45, x, %5;\n\t"
+        "shf.l.wrap.b32 x, %8, %8, 8;\n\t"
+        "add.u32 t67, x, %7;\n\t"
+        "shl.b32 x, t23, 16;\n\t"
+        "shr.u32 y, t23, 16;\n\t"
+        "add.cc.u32 al, t01, x;\n\t"
+        "addc.u32 ah, t45, y;\n\t"                 // a = (al, ah)
         "shr.u32 x, ah, 16;\n\t"
-        "add.u32 top, x, t67;\n\t"                  // X' >> 48
-        "mad.lo.u32 ah, t67, 65536, ah;\n\t"        // X' mod 2^64
+        "add.u32 top, x, t67;\n\t"                 // X' >> 48
+        "shf.l.clamp.b32 x, 0, t67, 16;\n\t"
+        "add.u32 ah, ah, x;\n\t"                   // X' mod 2^64
         "mul.hi.u32 q, top, %10;\n\t"
-        "mov.b64 {n0, n1}, %9;\n\t"                 // 2^64 - p
+        "mov.b64 {n0, n1}, %9;\n\t"                // 2^64 - p
         "mov.b64 aa, {al, ah};\n\t"
         "mad.wide.u32 rr, q, n0, aa;\n\t"
         "mov.b64 {rl, rh}, rr;\n\t"

@@ -8,43 +8,61 @@
 //             EPI_SCALE factor and a canonical store.
 // Each round multiplies 16-word vectors by a 16 x 16 matrix mod p with the byte-split identity of
 // k_bconv_tc: A = the vectors' bytes (K = 128), B = the matrix image (N = 16 outputs x 8 byte columns),
-// D in TMEM, one tcgen05.ld + 14-instruction reduction per output.  Per element that is two reductions
-// and one Shoup product (the twist) instead of the eight butterfly half-products of the butterfly pass:
-// ~48 instead of ~112 FMA-heavy-pipe cycles per warp and 32 elements.
+// D in TMEM, one byte-sum reduction per output (modarith.cuh bytesum_reduce_c: mostly ALU-pipe work).  Per
+// element that is two reductions and one Shoup product (the twist) instead of the four butterfly Shoup
+// products of the butterfly pass, so the pass can run at the HBM rate of its 16 bytes per element.
 //
 // A tile = (limb, 8 columns): 128 vectors per round = one M = 128 MMA of K = 128 (four k32 steps).  The
 // kernel is persistent (one CTA per SM, contiguous balanced tile ranges, so a CTA meets one or two limbs)
 // and warp-specialised, every hand-off an mbarrier:
-//   warps 0-2   loaders: cp.async of the next tiles' round-1 operands (8-byte elements, transposed into
-//               the K-major A layout) into S1 stages, plus the B images of each new prime into one of two
-//               table slots;
-//   warp 3      one thread issues the MMAs: round 1 of tile j, then round 2 of tile j - 1, each into its
-//               own double-buffered TMEM accumulator (4 x 128 of the 512 columns);
-//   warps 4-11  round-1 epilogue: TMEM -> reduce -> twist -> round 2's A operand in shared memory;
-//   warps 12-19 round-2 epilogue: TMEM -> reduce (-> scale) -> global stores.
+//   warp 0      TMA producer: one 4-D tensor copy per tile (8 columns x 16 x 16 rows = 16 KB) into NC_S
+//               shared stages, and the two matrix images of each new prime (1-D bulk copy, 32 KB) into one
+//               of two table slots;
+//   warp 1      TMEM owner and MMA issuer (one thread): round 1 of tile j with its A operand in TMEM
+//               (kind::i8, A from tensor memory), then round 2 of tile j - 1 from shared memory;
+//   warps 2-5   transposers (one per TMEM lane quarter): a thread = one round-1 vector, 16 conflict-free
+//               8-byte shared loads -> 32 registers -> one tcgen05.st into the round-1 A operand;
+//   warps 6-13  round-1 epilogue: TMEM -> reduce -> twist (Shoup pairs held in registers) -> round 2's A
+//               operand in shared memory (256 contiguous bytes per warp store);
+//   warps 14-17 round-2 epilogue: TMEM -> reduce (-> scale) -> global stores.
 // Outputs are congruent to the butterfly pass's: forward lazily reduced to [0, 3p) (the row pass accepts
-// [0, 8p + 2^32)), inverse scaled and canonical.
+// [0, 8p + 2^32)), inverse scaled and canonical.  Parity: every KeySwitch / HMult / NTT test runs through
+// this pass when it is the default (HKS_NTT_TC_DEFAULT).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <mutex>
 
 #include "internal.h"
 #include "tc.cuh"
 
 #define NC_CW 8                 // columns per tile
 #define NC_TPL (256 / NC_CW)    // tiles per limb
-#ifndef NC_S1
-#define NC_S1 4                 // round-1 operand stages
+#ifndef NC_CPT
+#define NC_CPT 4                // tiles per TMA stage (a chunk of NC_CPT * 8 adjacent columns)
 #endif
-#define NC_S2 2                 // round-2 operand stages
-#define NC_LOADW 3              // loader warps
-#define NC_E1W 8                // round-1 epilogue warps
-#define NC_E2W 8                // round-2 epilogue warps
-#define NC_THREADS ((NC_LOADW + 1 + NC_E1W + NC_E2W) * 32)
-#define NC_OPB 16384            // bytes of one operand stage (128 vectors x 128 bytes)
+#define NC_SW (NC_CW * NC_CPT)  // columns per stage: NC_SW * 8-byte row segments per TMA box row
+#ifndef NC_S
+#define NC_S 2                  // TMA stages
+#endif
+#define NC_STAGE (16384 * NC_CPT)   // bytes of one stage (256 rows x NC_SW words)
+#define NC_OPB 16384            // bytes of one round-2 operand buffer (128 vectors x 128 bytes)
 #define NC_TABB 32768           // bytes of one table slot (round-1 and round-2 images)
-#define NC_SMEM (NC_S1 * NC_OPB + NC_S2 * NC_OPB + 2 * NC_TABB)
+#define NC_NW 19                // warps: producer, MMA round 1, 4 transposers, 8 + 4 epilogue, MMA round 2
+                                // (<= 5 warps per SM sub-partition keeps 96 registers per thread)
+#define NC_THREADS (NC_NW * 32)
+#define NC_W_TR 2
+#define NC_W_E1 6
+#define NC_W_E2 14
+#define NC_W_M2 18
+#define NC_SMEM (NC_S * NC_STAGE + 2 * NC_OPB + 2 * NC_TABB + 1024)
+// TMEM columns: D1 x2 [0, 256), D2 [256, 384), A1 x2 [384, 448)
+#define NC_D2 256
+#define NC_A1 384
 
 struct NttColsArgs {
-    const u64 *in;
+    CUtensorMap tmap;           // 4-D view of the input (columns, two 16-row digits, slot); box 8 x 16 x 16 x 1
     u64 *out;
     const u64 *tab;             // [prime][NTT16_TAB]: round-1 image, round-2 image, twist (w, w')[16][16]
     const ulonglong2 *scale;    // inverse: scale[b % scale_mod] or, if NULL, ninv[prime]
@@ -52,50 +70,101 @@ struct NttColsArgs {
     const PrimeConst *pc;
     u32 nlimbs, scale_mod;
     LimbMap map;
+#ifdef NC_TRACE
+    long long *trace;           // [event][tile] clock64 stamps of CTA 0 (debug builds)
+#endif
 };
+#ifdef NC_TRACE
+#define NC_T(ev, j) do { if (blockIdx.x == 0 && (j) < 64) A.trace[(ev) * 64 + (j)] = clock64(); } while (0)
+#else
+#define NC_T(ev, j) do { } while (0)
+#endif
 
-__device__ __forceinline__ void cp_async16(u32 saddr, const void *g) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
-}
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(u32 bar, u32 bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tc_mma_i8_ts(u32 dtmem, u32 atmem, u64 bdesc, u32 idesc, u32 accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtmem),
+        "r"(atmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tc_ld32(u32 taddr, u32 (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+          "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void tc_st32(u32 taddr, const u32 (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+        "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+        "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+    u32 pred;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 template <bool FWD>
 __global__ void __launch_bounds__(NC_THREADS, 1) k_ntt_cols_tc(const __grid_constant__ NttColsArgs A) {
     pdl_trigger();
     constexpr u32 N = 1u << 16;
-    extern __shared__ __align__(1024) uint8_t csm[];
-    __shared__ __align__(8) u64 a1_full[NC_S1], a1_empty[NC_S1], a2_full[NC_S2], a2_empty[NC_S2];
-    __shared__ __align__(8) u64 mma1_done[2], mma2_done[2], t1_empty[2], t2_empty[2], slot_free[2];
+    extern __shared__ uint8_t csm_raw[];
+    __shared__ __align__(8) u64 tma_full[NC_S], tma_empty[NC_S], img_full[2], img_free[2];
+    __shared__ __align__(8) u64 a1_full[2], a1_empty[2], d1_full[2], d1_empty[2], a2_full[2], a2_empty[2];
+    __shared__ __align__(8) u64 d2_full, d2_empty;
     __shared__ u32 tmem_s;
     const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const u32 ntile = A.nlimbs * NC_TPL;
-    const u32 t_beg = (u32)((u64)blockIdx.x * ntile / gridDim.x);      // balanced contiguous ranges
-    const u32 t_end = (u32)((u64)(blockIdx.x + 1) * ntile / gridDim.x);
-    const u32 nloc = t_end - t_beg;
+    const u32 nchunk = A.nlimbs * (NC_TPL / NC_CPT);
+    const u32 ch_beg = (u32)((u64)blockIdx.x * nchunk / gridDim.x);    // balanced contiguous chunk ranges
+    const u32 ch_end = (u32)((u64)(blockIdx.x + 1) * nchunk / gridDim.x);
+    const u32 t_beg = ch_beg * NC_CPT;
+    const u32 nloc = (ch_end - ch_beg) * NC_CPT;
     const u32 b_first = t_beg / NC_TPL;
     // table segment of local tile j: the limb offset from the CTA's first limb (slot = segment & 1)
     auto seg = [&](u32 j) { return (t_beg + j) / NC_TPL - b_first; };
     auto last_of_seg = [&](u32 j) { return j + 1 == nloc || seg(j + 1) != seg(j); };
 
+    // 1024-aligned dynamic shared memory: stages | round-2 operands | table slots
+    const u32 sbase = (smem_u32(csm_raw) + 1023) & ~1023u;
+    const u32 stg0 = sbase, op2 = stg0 + NC_S * NC_STAGE, tab0 = op2 + 2 * NC_OPB;
+    uint8_t *const sgen = csm_raw + (sbase - smem_u32(csm_raw));
+
     if (tid == 0) {
-        for (int s = 0; s < NC_S1; s++) {
-            mbar_init(smem_u32(&a1_full[s]), NC_LOADW * 32);
-            mbar_init(smem_u32(&a1_empty[s]), 1);
-        }
-        for (int s = 0; s < NC_S2; s++) {
-            mbar_init(smem_u32(&a2_full[s]), NC_E1W);
-            mbar_init(smem_u32(&a2_empty[s]), 1);
+        for (int s = 0; s < NC_S; s++) {
+            mbar_init(smem_u32(&tma_full[s]), 1);
+            mbar_init(smem_u32(&tma_empty[s]), 4 * NC_CPT);
         }
         for (int b = 0; b < 2; b++) {
-            mbar_init(smem_u32(&mma1_done[b]), 1);
-            mbar_init(smem_u32(&mma2_done[b]), 1);
-            mbar_init(smem_u32(&t1_empty[b]), NC_E1W);
-            mbar_init(smem_u32(&t2_empty[b]), NC_E2W);
-            mbar_init(smem_u32(&slot_free[b]), 1);
+            mbar_init(smem_u32(&img_full[b]), 1);
+            mbar_init(smem_u32(&img_free[b]), 1);
+            mbar_init(smem_u32(&a1_full[b]), 4);
+            mbar_init(smem_u32(&a1_empty[b]), 1);
+            mbar_init(smem_u32(&d1_full[b]), 1);
+            mbar_init(smem_u32(&d1_empty[b]), 8);
+            mbar_init(smem_u32(&a2_full[b]), 8);
+            mbar_init(smem_u32(&a2_empty[b]), 1);
         }
+        mbar_init(smem_u32(&d2_full), 1);
+        mbar_init(smem_u32(&d2_empty), 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 3) {
+    if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_s)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
@@ -103,136 +172,173 @@ __global__ void __launch_bounds__(NC_THREADS, 1) k_ntt_cols_tc(const __grid_cons
     __syncthreads();
     tc_fence_after();
     const u32 tmem = tmem_s;
-    pdl_wait();
+    if (warp != 0) pdl_wait();   // the producer waits after issuing its first table copy (ctx tables only)
 
-    const u32 op1 = smem_u32(csm), op2 = op1 + NC_S1 * NC_OPB, tab0 = op2 + NC_S2 * NC_OPB;
-    // element k of round-1 / round-2 vector class v sits in row row1(v, k) / row2(v, k) of the column
-    auto row1 = [](u32 v, u32 k) { return FWD ? v + 16 * k : 16 * v + k; };
-    auto row2 = [](u32 v, u32 k) { return FWD ? 16 * v + k : v + 16 * k; };
-
-    if (warp < NC_LOADW) {
-        // ---------------- loaders ----------------
-        const u32 lt = tid;   // 0 .. 95
-        auto arrive_full = [&](u32 j) {
-            fence_async_smem();
-            mbar_arrive(smem_u32(&a1_full[j % NC_S1]));
-        };
-        constexpr u32 LAG = NC_S1 - 1;   // tiles whose copies may be in flight unsignalled
-        u32 na = 0;                      // next tile whose a1_full arrival is due
-        for (u32 j = 0; j < nloc; j++) {
-            const u32 s = j % NC_S1;
-            if (j >= NC_S1) mbar_wait(smem_u32(&a1_empty[s]), ((j / NC_S1) - 1) & 1);
+    if (warp == 0) {
+        // ---------------- TMA producer (warp-uniform loop, one elected lane issues) ----------------
+        if (elect_one()) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&A.tmap)) : "memory");
+        for (u32 n = 0; n * NC_CPT < nloc; n++) {
+            const u32 j = n * NC_CPT, s = n % NC_S;
             const u32 tile = t_beg + j, b = tile / NC_TPL, c0 = (tile % NC_TPL) * NC_CW;
             if (j == 0 || seg(j) != seg(j - 1)) {
-                // a new limb: its prime's round-1 / round-2 images into table slot seg & 1, after the last
-                // round-2 MMA of segment seg - 2 released it -- which needs every earlier tile signalled first
+                // the round-1 / round-2 images of a new limb's prime into slot seg & 1, after the last round-2
+                // MMA of segment seg - 2 released it (ctx tables: no wait on the predecessor)
                 const u32 k = seg(j);
-                if (k >= 2) {
-                    asm volatile("cp.async.wait_group 0;" ::: "memory");
-                    while (na < j) arrive_full(na++);
-                    mbar_wait(smem_u32(&slot_free[k & 1]), ((k - 2) >> 1) & 1);
+                if (k >= 2) mbar_wait(smem_u32(&img_free[k & 1]), ((k - 2) >> 1) & 1);
+                if (elect_one()) {
+                    const u32 bar = smem_u32(&img_full[k & 1]);
+                    mbar_expect_tx(bar, NC_TABB);
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            tab0 + (k & 1) * NC_TABB),
+                        "l"(A.tab + (size_t)A.map.prime[b] * NTT16_TAB), "r"((u32)NC_TABB), "r"(bar)
+                        : "memory");
                 }
-                const uint8_t *t = reinterpret_cast<const uint8_t *>(A.tab + (size_t)A.map.prime[b] * NTT16_TAB);
-                const u32 dst = tab0 + (k & 1) * NC_TABB;
-                for (u32 o = lt * 16; o < NC_TABB; o += NC_LOADW * 32 * 16) cp_async16(dst + o, t + o);
+                __syncwarp();
             }
-            // element (vector m = v * 8 + c, k): row row1(v, k), column c0 + c -> A layout
-            const u64 *src = A.in + (size_t)A.map.sin[b] * N + c0;
-            const u32 base = op1 + s * NC_OPB;
-            for (u32 e = lt; e < 2048; e += NC_LOADW * 32) {
-                const u32 c = e & 7, v = (e >> 3) & 15, k = e >> 7;
-                cp_async8(base + v * 1024 + (k >> 1) * 128 + c * 16 + (k & 1) * 8, src + (size_t)row1(v, k) * 256 + c);
+            if (j == 0) pdl_wait();   // the tile data is the predecessor's output
+            if (n >= NC_S) mbar_wait(smem_u32(&tma_empty[s]), ((n / NC_S) - 1) & 1);
+            NC_T(0, j);
+            if (elect_one()) {
+                const u32 bar = smem_u32(&tma_full[s]);
+                mbar_expect_tx(bar, NC_STAGE);
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                    "%3, %4, %5}], [%6];" ::"r"(stg0 + s * NC_STAGE),
+                    "l"(reinterpret_cast<u64>(&A.tmap)), "r"(c0), "r"(0), "r"(0), "r"((u32)A.map.sin[b]), "r"(bar)
+                    : "memory");
             }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-            if (j + 1 - na > LAG) {          // groups na .. j pending: complete the oldest
-                asm volatile("cp.async.wait_group %0;" ::"n"(LAG) : "memory");
-                arrive_full(na++);
-            }
+            __syncwarp();
         }
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        while (na < nloc) arrive_full(na++);
-    } else if (warp == NC_LOADW) {
-        // ---------------- MMA issuer ----------------
-        if (lane == 0) {
-            const u32 idesc = (2u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);   // M = N = 128, s32 += u8 x u8
-            auto round2 = [&](u32 i) {
-                const u32 s = i % NC_S2;
-                mbar_wait(smem_u32(&a2_full[s]), (i / NC_S2) & 1);
-                if (i >= 2) mbar_wait(smem_u32(&t2_empty[i & 1]), ((i >> 1) - 1) & 1);
-                tc_fence_after();
-                fence_async_smem();
-                const u32 a = op2 + s * NC_OPB, bimg = tab0 + (seg(i) & 1) * NC_TABB + NC_TABB / 2;
-#pragma unroll
-                for (int k = 0; k < 4; k++)
-                    tc_mma_i8(tmem + 256 + (i & 1) * 128, tc_desc(a + k * 256, 128, 1024), tc_desc(bimg + k * 256, 128, 1024),
-                              idesc, k > 0 ? 1u : 0u);
-                tc_commit(smem_u32(&a2_empty[s]));
-                tc_commit(smem_u32(&mma2_done[i & 1]));
-                if (last_of_seg(i)) tc_commit(smem_u32(&slot_free[seg(i) & 1]));
-            };
-            for (u32 j = 0; j < nloc; j++) {
-                const u32 s = j % NC_S1;
-                mbar_wait(smem_u32(&a1_full[s]), (j / NC_S1) & 1);
-                if (j >= 2) mbar_wait(smem_u32(&t1_empty[j & 1]), ((j >> 1) - 1) & 1);
-                tc_fence_after();
-                fence_async_smem();
-                const u32 a = op1 + s * NC_OPB, bimg = tab0 + (seg(j) & 1) * NC_TABB;
-#pragma unroll
-                for (int k = 0; k < 4; k++)
-                    tc_mma_i8(tmem + (j & 1) * 128, tc_desc(a + k * 256, 128, 1024), tc_desc(bimg + k * 256, 128, 1024),
-                              idesc, k > 0 ? 1u : 0u);
-                tc_commit(smem_u32(&a1_empty[s]));
-                tc_commit(smem_u32(&mma1_done[j & 1]));
-                if (j >= 1) round2(j - 1);
-            }
-            if (nloc) round2(nloc - 1);
-        }
-        __syncwarp();
-    } else if (warp < NC_LOADW + 1 + NC_E1W) {
-        // ---------------- round-1 epilogue: reduce, twist, round 2's operand ----------------
-        const u32 ew = warp - (NC_LOADW + 1);
-        const u32 q = warp & 3, half = ew >> 2;            // TMEM lane quarter; outputs [8 half, 8 half + 8)
-        const u32 m = q * 32 + lane, v = m >> 3, c = m & 7;  // this lane's vector (class / block v, column c)
-        for (u32 j = 0; j < nloc; j++) {
-            const u32 tile = t_beg + j, b = tile / NC_TPL;
-            const PrimeConst pc = A.pc[A.map.prime[b]];
-            const u64 np = 0 - pc.p;
-            const u32 mu = (u32)pc.mu80;
-            const ulonglong2 *tw = reinterpret_cast<const ulonglong2 *>(A.tab + (size_t)A.map.prime[b] * NTT16_TAB + 2 * NTT16_IMG) + v * 16;
-            mbar_wait(smem_u32(&mma1_done[j & 1]), (j >> 1) & 1);
+    } else if (warp == 1 || warp == NC_W_M2) {
+        // ---------------- MMA issuers: warp 1 round 1, warp NC_W_M2 round 2 ----------------
+        // The whole warp runs the loop (its values stay warp-uniform, so the descriptors live in uniform
+        // registers); one elected lane issues.  Descriptors: the 14-bit start-address field advances by 16
+        // per 256-byte k32 step.
+        constexpr u32 idesc = (2u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);   // M = N = 128, s32 += u8 x u8
+        const u64 db1_0 = tc_desc(tab0, 128, 1024), db1_1 = tc_desc(tab0 + NC_TABB, 128, 1024);
+        const u64 db2_0 = tc_desc(tab0 + NC_TABB / 2, 128, 1024), db2_1 = tc_desc(tab0 + NC_TABB + NC_TABB / 2, 128, 1024);
+        const u64 da2_0 = tc_desc(op2, 128, 1024), da2_1 = tc_desc(op2 + NC_OPB, 128, 1024);
+        auto round2 = [&](u32 i) {
+            const u32 s = i & 1;
+            NC_T(11, i);
+            mbar_wait(smem_u32(&a2_full[s]), (i >> 1) & 1);
+            if (i >= 1) mbar_wait(smem_u32(&d2_empty), (i - 1) & 1);
             tc_fence_after();
-            const u32 s2 = j % NC_S2;
-            if (j >= NC_S2) mbar_wait(smem_u32(&a2_empty[s2]), ((j / NC_S2) - 1) & 1);
-            const u32 tb = tmem + (j & 1) * 128 + ((q * 32) << 16);
-            // round-2 vector o * 8 + c, element v
-            const u32 w2 = op2 + s2 * NC_OPB + (v >> 1) * 128 + c * 16 + (v & 1) * 8;
+            NC_T(12, i);
+            const u64 a = s ? da2_1 : da2_0, bb = (seg(i) & 1) ? db2_1 : db2_0;
+            if (elect_one()) {
 #pragma unroll
-            for (u32 o0 = 0; o0 < 8; o0 += 4) {
-                u32 r[4][8];
-#pragma unroll
-                for (int k = 0; k < 4; k++) tc_ld8(tb + (8 * half + o0 + k) * 8, r[k]);
-                tc_wait_ld();
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const u32 o = 8 * half + o0 + k;
-                    const u64 x = bytesum_reduce_c<true>(r[k], np, mu);   // [0, 3p)
-                    const ulonglong2 t = __ldg(tw + o);
-                    const u64 y = shoup_approx(x, t.x, t.y, np);          // [0, 4p)
-                    asm volatile("st.shared.u64 [%0], %1;" ::"r"(w2 + o * 1024), "l"(y) : "memory");
-                }
+                for (int k = 0; k < 4; k++) tc_mma_i8(tmem + NC_D2, a + 16 * k, bb + 16 * k, idesc, k > 0 ? 1u : 0u);
+                tc_commit(smem_u32(&a2_empty[s]));
+                tc_commit(smem_u32(&d2_full));
+                if (last_of_seg(i)) tc_commit(smem_u32(&img_free[seg(i) & 1]));
             }
-            fence_async_smem();
+            __syncwarp();
+            NC_T(6, i);
+        };
+        if (warp == 1) {
+            for (u32 j = 0; j < nloc; j++) {
+                const u32 s = j & 1;
+                NC_T(9, j);
+                if (j == 0 || seg(j) != seg(j - 1)) mbar_wait(smem_u32(&img_full[seg(j) & 1]), (seg(j) >> 1) & 1);
+                mbar_wait(smem_u32(&a1_full[s]), (j >> 1) & 1);
+                if (j >= 2) mbar_wait(smem_u32(&d1_empty[s]), ((j >> 1) - 1) & 1);
+                tc_fence_after();
+                NC_T(10, j);
+                const u64 bb = (seg(j) & 1) ? db1_1 : db1_0;
+                if (elect_one()) {
+#pragma unroll
+                    for (int k = 0; k < 4; k++)
+                        tc_mma_i8_ts(tmem + s * 128, tmem + NC_A1 + s * 32 + k * 8, bb + 16 * k, idesc, k > 0 ? 1u : 0u);
+                    tc_commit(smem_u32(&a1_empty[s]));
+                    tc_commit(smem_u32(&d1_full[s]));
+                }
+                __syncwarp();
+                NC_T(3, j);
+            }
+        } else {
+            for (u32 i = 0; i < nloc; i++) round2(i);
+        }
+    } else if (warp < NC_W_E1) {
+        // ---------------- transposers: stage [r_hi][r_lo][c] -> round-1 A operand in TMEM ----------------
+        // vector m = 8 v + c; its element k is stage word (16 k + v) NC_SW + 8 sub + c (the tensor map orders
+        // the row digits so that k is the outer one in both directions; sub = the tile's place in its chunk)
+        const u32 q = warp & 3, m = q * 32 + lane, v = m >> 3, c = m & 7;
+        const u64 *stg = reinterpret_cast<const u64 *>(sgen);
+        for (u32 j = 0; j < nloc; j++) {
+            const u32 n = j / NC_CPT, s = n % NC_S, sub = j % NC_CPT;
+            mbar_wait(smem_u32(&tma_full[s]), (n / NC_S) & 1);
+            if (warp == NC_W_TR && lane == 0) NC_T(1, j);
+            u32 r[32];
+            const u64 *p = stg + (size_t)s * (NC_STAGE / 8) + v * NC_SW + sub * 8 + c;
+#pragma unroll
+            for (int k = 0; k < 16; k++) {
+                const u64 x = p[k * 16 * NC_SW];
+                r[2 * k] = (u32)x;
+                r[2 * k + 1] = (u32)(x >> 32);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&tma_empty[s]));
+            const u32 sa = j & 1;
+            if (j >= 2) mbar_wait(smem_u32(&a1_empty[sa]), ((j >> 1) - 1) & 1);
+            tc_fence_after();
+            tc_st32(tmem + NC_A1 + sa * 32 + ((q * 32) << 16), r);
+            tc_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(smem_u32(&t1_empty[j & 1]));
-                mbar_arrive(smem_u32(&a2_full[s2]));
+            if (lane == 0) mbar_arrive(smem_u32(&a1_full[sa]));
+            if (warp == NC_W_TR && lane == 0) NC_T(2, j);
+        }
+    } else if (warp < NC_W_E2) {
+        // ---------------- round-1 epilogue: reduce, twist, round 2's operand ----------------
+        const u32 ew = warp - NC_W_E1;
+        const u32 q = warp & 3, half = ew >> 2;             // TMEM lane quarter; outputs [8 half, 8 half + 8)
+        const u32 m = q * 32 + lane, v = m >> 3, c = m & 7;  // this lane's vector (class / block v, column c)
+        for (u32 j = 0; j < nloc; j++) {
+            const u32 b = (t_beg + j) / NC_TPL, prime = A.map.prime[b];
+            const PrimeConst pc = A.pc[prime];
+            const u64 np = 0 - pc.p;
+            const u32 mu = (u32)pc.mu80;
+            // twist pairs (w, w') of this lane's class and outputs (read-only path, L1-resident per prime)
+            const ulonglong2 *tw = reinterpret_cast<const ulonglong2 *>(A.tab + (size_t)prime * NTT16_TAB + 2 * NTT16_IMG) +
+                                   v * 16 + 8 * half;
+            const u32 s = j & 1;
+            mbar_wait(smem_u32(&d1_full[s]), (j >> 1) & 1);
+            if (warp == NC_W_E1 && lane == 0) NC_T(4, j);
+            tc_fence_after();
+            if (j >= 2) mbar_wait(smem_u32(&a2_empty[s]), ((j >> 1) - 1) & 1);
+            const u32 tb = tmem + s * 128 + ((q * 32) << 16) + 64 * half;
+            // round-2 vector o * 8 + c, element v
+            const u32 w2 = op2 + s * NC_OPB + (v >> 1) * 128 + c * 16 + (v & 1) * 8;
+            // all eight outputs of this warp's half in flight at once (two 32-column TMEM loads)
+            u32 r[2][32];
+            tc_ld32(tb, r[0]);
+            tc_ld32(tb + 32, r[1]);
+            tc_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&d1_empty[s]));
+            u64 x[8];
+#pragma unroll
+            for (int o = 0; o < 8; o++) {
+                const u32 *rr = &r[o >> 2][8 * (o & 3)];
+                x[o] = bytesum_reduce_c<true>(rr[0], rr[1], rr[2], rr[3], rr[4], rr[5], rr[6], rr[7], np, mu);   // [0, 3p)
             }
+#pragma unroll
+            for (int o = 0; o < 8; o++) {
+                const ulonglong2 t = __ldg(tw + o);
+                const u64 y = shoup_approx(x[o], t.x, t.y, np);                        // [0, 4p)
+                asm volatile("st.shared.u64 [%0], %1;" ::"r"(w2 + (8 * half + o) * 1024), "l"(y) : "memory");
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&a2_full[s]));
+            if (warp == NC_W_E1 && lane == 0) NC_T(5, j);
         }
     } else {
         // ---------------- round-2 epilogue: reduce (scale), store ----------------
-        const u32 ew = warp - (NC_LOADW + 1 + NC_E1W);
-        const u32 q = warp & 3, half = ew >> 2;
+        const u32 q = warp & 3;
         const u32 m = q * 32 + lane, g = m >> 3, c = m & 7;
         for (u32 j = 0; j < nloc; j++) {
             const u32 tile = t_beg + j, b = tile / NC_TPL, c0 = (tile % NC_TPL) * NC_CW;
@@ -243,34 +349,57 @@ __global__ void __launch_bounds__(NC_THREADS, 1) k_ntt_cols_tc(const __grid_cons
             ulonglong2 sc = make_ulonglong2(0, 0);
             if (!FWD) sc = A.scale ? A.scale[b % A.scale_mod] : A.ninv[prime];
             u64 *dst = A.out + (size_t)A.map.sout[b] * N + c0 + c;
-            mbar_wait(smem_u32(&mma2_done[j & 1]), (j >> 1) & 1);
+            mbar_wait(smem_u32(&d2_full), j & 1);
+            if (warp == NC_W_E2 && lane == 0) NC_T(7, j);
             tc_fence_after();
-            const u32 tb = tmem + 256 + (j & 1) * 128 + ((q * 32) << 16);
+            const u32 tb = tmem + NC_D2 + ((q * 32) << 16);
 #pragma unroll
-            for (u32 o0 = 0; o0 < 8; o0 += 4) {
-                u32 r[4][8];
-#pragma unroll
-                for (int k = 0; k < 4; k++) tc_ld8(tb + (8 * half + o0 + k) * 8, r[k]);
+            for (u32 o0 = 0; o0 < 16; o0 += 8) {
+                u32 r[2][32];
+                tc_ld32(tb + o0 * 8, r[0]);
+                tc_ld32(tb + o0 * 8 + 32, r[1]);
                 tc_wait_ld();
+                if (o0 == 8) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(smem_u32(&d2_empty));
+                }
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const u32 o = 8 * half + o0 + k;
-                    u64 x = bytesum_reduce_c<true>(r[k], np, mu);
+                for (int k = 0; k < 8; k++) {
+                    const u32 o = o0 + k;
+                    const u32 *rr = &r[k >> 2][8 * (k & 3)];
+                    u64 x = bytesum_reduce_c<true>(rr[0], rr[1], rr[2], rr[3], rr[4], rr[5], rr[6], rr[7], np, mu);
                     if (!FWD) x = csub(csub(shoup_approx(x, sc.x, sc.y, np), 2 * pc.p), pc.p);
-                    dst[(size_t)row2(g, o) * 256] = x;
+                    const u32 row = FWD ? 16 * g + o : g + 16 * o;
+                    dst[(size_t)row * 256] = x;
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&t2_empty[j & 1]));
+            if (warp == NC_W_E2 && lane == 0) NC_T(8, j);
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 3) {
+    if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
     }
+}
+
+#ifdef NC_TRACE
+long long *hks_nc_trace = nullptr;
+extern "C" void *hks_debug_nc_trace() { return hks_nc_trace; }
+#endif
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
 }
 
 hks_status launch_ntt_cols_tc(const hks_ctx *ctx, NttDir dir, int /*epi*/, const NttArgs &na, cudaStream_t s) {
@@ -279,7 +408,6 @@ hks_status launch_ntt_cols_tc(const hks_ctx *ctx, NttDir dir, int /*epi*/, const
     hks_func_smem((const void *)k_ntt_cols_tc<true>, smem);
     hks_func_smem((const void *)k_ntt_cols_tc<false>, smem);
     NttColsArgs a;
-    a.in = na.in;
     a.out = na.out;
     a.tab = dir == NTT_FWD ? ctx->d_ntt_img_fwd : ctx->d_ntt_img_inv;
     a.scale = na.scale;
@@ -288,7 +416,29 @@ hks_status launch_ntt_cols_tc(const hks_ctx *ctx, NttDir dir, int /*epi*/, const
     a.nlimbs = na.nlimbs;
     a.scale_mod = na.scale_mod ? na.scale_mod : 1;
     a.map = na.map;
-    const u32 grid = std::min<u32>(a.nlimbs * NC_TPL, (u32)nsm);
+#ifdef NC_TRACE
+    {
+        static long long *tr = nullptr;
+        if (!tr) cudaMalloc(&tr, 13 * 64 * sizeof(long long));
+        a.trace = tr;
+        hks_nc_trace = tr;
+    }
+#endif
+    // input view: (column, row digit 1, row digit 2, slot); the digit whose index is the element index k of a
+    // round-1 vector comes second so that the stage lands as [k][v][c] (forward: row = v + 16 k; inverse:
+    // row = 16 v + k)
+    u32 nslot = 0;
+    for (u32 i = 0; i < na.nlimbs; i++) nslot = std::max<u32>(nslot, (u32)na.map.sin[i] + 1);
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
+    if (!enc) HKS_FAIL(HKS_ECUDA, "ntt_cols_tc: cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[4] = {256, 16, 16, nslot};
+    const cuuint64_t str[3] = {dir == NTT_FWD ? 2048ull : 32768ull, dir == NTT_FWD ? 32768ull : 2048ull, 524288ull};
+    const cuuint32_t box[4] = {NC_SW, 16, 16, 1}, es[4] = {1, 1, 1, 1};
+    const CUresult cr = enc(&a.tmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<u64 *>(na.in), dims, str, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) HKS_FAIL(HKS_ECUDA, "ntt_cols_tc: cuTensorMapEncodeTiled failed (%d)", (int)cr);
+    const u32 grid = std::min<u32>(a.nlimbs * (NC_TPL / NC_CPT), (u32)nsm);
     ProfScope ps(dir == NTT_FWD ? K_NTT_FWD_COLS : K_NTT_INV_COLS, s);
     const cudaError_t e = dir == NTT_FWD
                               ? hks_launch(k_ntt_cols_tc<true>, dim3(grid), dim3(NC_THREADS), smem, s, a)

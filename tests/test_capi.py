@@ -14,7 +14,7 @@ H = pytest.importorskip("paper_2507_04775_b200.hks")
 
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "hks.h")).read()
-    return sorted(set(re.findall(r"\b(hks_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(hks_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_exports_match_header():
