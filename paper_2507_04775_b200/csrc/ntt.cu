@@ -40,6 +40,15 @@ static thread_local const cudaAccessPolicyWindow *t_win = nullptr;
 #ifndef HKS_KIP_TMA
 #define HKS_KIP_TMA 0     // 1: key rows prefetched into shared memory with 1D bulk copies (measured slower)
 #endif
+#ifndef HKS_KIP_TWS
+#define HKS_KIP_TWS 1     // 1: the CTA's row twiddles staged in shared memory by cp.async issued before griddepcontrol.wait
+#endif
+#ifndef HKS_KIP_PIPE
+#define HKS_KIP_PIPE 0    // 1: key words of the next product step loaded before the current step's products
+#endif
+#ifndef HKS_KIP_L2PF
+#define HKS_KIP_L2PF 0    // 1: the CTA's key rows prefetched into L2 (bulk prefetch) at the start of the row pass
+#endif
 
 // One pass over a limb batch.  LOGN = log2 of the sub-transform length n; LOGE = log2 of the
 // elements a thread holds (radix-2^LOGE rounds); LOGNB = log2 of the sub-transforms per CTA;
@@ -50,8 +59,21 @@ static thread_local const cudaAccessPolicyWindow *t_win = nullptr;
 #endif
 // One tile (NB sub-transforms of limb b) of a pass.  Round 0 reads global memory (forward and
 // inverse-column passes) or the tile the inverse-row prologue staged in shared memory.
+// Row passes whose tile (data + its NB twiddle rows) still fits HKS_NTT_MINB CTAs per SM stage the twiddle rows
+// in shared memory with cp.async issued before griddepcontrol.wait (the per-row tables are context data, 16 bytes
+// per twiddle, mostly HBM-resident behind the key stream: their latency otherwise sits inside the butterfly chains)
+#ifndef HKS_ROW_TWS
+#define HKS_ROW_TWS 0   // 1: measured slower for the stand-alone row passes (8-row tiles, 32 KB per CTA up front)
+#endif
+template <int LOGN, int LOGE, int LOGNB, bool COLS>
+constexpr bool row_tws() {
+    return HKS_ROW_TWS && !COLS &&
+           ((size_t)((1 << LOGN) + ((1 << LOGN) >> LOGE)) * (1 << LOGNB) * 8 + (size_t)(16 << (LOGN + LOGNB))) * HKS_NTT_MINB <=
+               220 * 1024;
+}
+
 template <int LOGN, int LOGE, int LOGNB, int LOGC, bool COLS, bool FWD, int EPI>
-__device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u32 tile, u64 *sm) {
+__device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u32 tile, u64 *sm, const ulonglong2 *tws) {
     constexpr int n = 1 << LOGN;
     constexpr int E = 1 << LOGE;
     constexpr int NB = 1 << LOGNB;
@@ -83,8 +105,8 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
     const u64 *__restrict__ csrc = A.in + ((size_t)A.map.sin[b] << (A.clog + LOGC)) + sub_off;
     u64 *__restrict__ cdst = out_base + ((size_t)A.map.sout[b] << (A.clog + LOGC)) + sub_off;
     auto cidx = [&](int j) -> size_t { return (size_t)((u32)j >> A.clog) * A.cstride + ((size_t)((u32)j & cmask) << LOGC); };
-    const ulonglong2 *__restrict__ tw =
-        COLS ? A.tw + (size_t)prime * n : A.tw + (((size_t)prime << A.log_r) + tile * NB + bsub) * n;
+    const ulonglong2 *tw =
+        COLS ? A.tw + (size_t)prime * n : (tws ? tws + bsub * n : A.tw + (((size_t)prime << A.log_r) + tile * NB + bsub) * n);
 
     auto saddr = [&](int k) -> int {
         return COLS ? (k + (k >> LOGE)) * NB + bsub : bsub * ROWPAD + k + (k >> LOGE);
@@ -208,7 +230,8 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
                     const ulonglong2 w = make_ulonglong2(m.p - 3 - k, 0x123456789abcull + l);   // timing-only experiment
                     (void)twb;
 #else
-                    const ulonglong2 w = __ldg(twb + ((k << lstride) >> sh));
+                    const ulonglong2 w = row_tws<LOGN, LOGE, LOGNB, COLS>() ? twb[(k << lstride) >> sh]   // shared
+                                                                           : __ldg(twb + ((k << lstride) >> sh));
 #endif
                     if (FWD)
                         ct_lazy(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, m);
@@ -308,22 +331,42 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
     }
 }
 
+#ifndef HKS_NTT_MINB128
+#define HKS_NTT_MINB128 0   // > 0: resident CTAs requested for passes with <= 128 threads per CTA (0: as above)
+#endif
 template <int LOGN, int LOGE, int LOGNB, int LOGC, bool COLS, bool FWD, int EPI>
 __global__ void __launch_bounds__((1 << LOGNB) << (LOGN - LOGE),
                                   (((1 << LOGNB) << (LOGN - LOGE)) >= 512) ? 2
+                                  : (HKS_NTT_MINB128 > 0 && ((1 << LOGNB) << (LOGN - LOGE)) <= 128) ? HKS_NTT_MINB128
                                   : (COLS && !FWD) ? HKS_NTT_INVCOLS_MINB : HKS_NTT_MINB)
 k_ntt(const __grid_constant__ NttArgs A) {
     extern __shared__ __align__(16) u64 sm[];
     pdl_trigger();
+    const u32 b = blockIdx.x / A.tiles, tile = blockIdx.x - b * A.tiles;
+    constexpr bool TWS = row_tws<LOGN, LOGE, LOGNB, COLS>();
+    ulonglong2 *tws = nullptr;
+    if (TWS) {
+        constexpr int NT = (1 << LOGNB) << (LOGN - LOGE), NE = 1 << (LOGN + LOGNB);
+        tws = reinterpret_cast<ulonglong2 *>(sm + (size_t)((1 << LOGN) + ((1 << LOGN) >> LOGE)) * (1 << LOGNB));
+        const ulonglong2 *src = A.tw + (((size_t)A.map.prime[b] << A.log_r) + ((size_t)tile << LOGNB)) * (1 << LOGN);
+        for (int e = threadIdx.x; e < NE; e += NT)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((u32)__cvta_generic_to_shared(tws + e)), "l"(src + e)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     pdl_wait();
-    const u32 b = blockIdx.x / A.tiles;
-    ntt_tile<LOGN, LOGE, LOGNB, LOGC, COLS, FWD, EPI>(A, b, blockIdx.x - b * A.tiles, sm);
+    if (TWS) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+    }
+    ntt_tile<LOGN, LOGE, LOGNB, LOGC, COLS, FWD, EPI>(A, b, tile, sm, tws);
 }
 
 template <int LOGN, int LOGE, int LOGNB, int LOGC, bool COLS, bool FWD, int EPI>
 static hks_status go(NttArgs &a, cudaStream_t s) {
     constexpr int threads = (1 << LOGNB) << (LOGN - LOGE);
-    constexpr size_t smem = (size_t)((1 << LOGN) + ((1 << LOGN) >> LOGE)) * (1 << LOGNB) * sizeof(u64);
+    constexpr size_t smem = (size_t)((1 << LOGN) + ((1 << LOGN) >> LOGE)) * (1 << LOGNB) * sizeof(u64) +
+                            (row_tws<LOGN, LOGE, LOGNB, COLS>() ? (size_t)(16 << (LOGN + LOGNB)) : 0);
     auto kern = k_ntt<LOGN, LOGE, LOGNB, LOGC, COLS, FWD, EPI>;
     if (smem > 48 * 1024) {
         hks_func_smem((const void *)kern, smem);
@@ -669,6 +712,20 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
     const size_t tbase = (size_t)tile * NB * n;
     const size_t kst = (size_t)A.nkey * N;
     const u64 *__restrict__ kbase = A.evk + (size_t)A.map.kslot[u] * N + tbase;
+#if HKS_KIP_TWS
+    // the NB twiddle rows of this tile (contiguous in the per-row table) -> shared memory, issued before
+    // griddepcontrol.wait: context tables, so their HBM latency overlaps the predecessor's tail
+    ulonglong2 *stw = reinterpret_cast<ulonglong2 *>(sm + NTR * BUF + (HKS_KIP_TMA ? 2 * NDIG * NB * n : 0));
+    auto stage_tw = [&](const ulonglong2 *g) {
+        const ulonglong2 *src = g + (((size_t)prime << A.log_r) + tile * NB) * n;
+        for (int e = tid; e < NB * n; e += NT)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((u32)__cvta_generic_to_shared(stw + e)),
+                         "l"(src + e)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    stage_tw(A.tw);
+#endif
 #if HKS_KIP_TMA
     // The key rows of this CTA (2 NDIG contiguous runs of NB n words) stream into shared memory with 1D
     // bulk copies issued before griddepcontrol.wait -- the key is a caller input that no kernel of the
@@ -697,13 +754,42 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
     }
 #endif
     pdl_wait();
+#if HKS_KIP_L2PF
+    if (tid == 0)
+        for (int i = 0; i < NDIG; i++)
+            for (int pp = 0; pp < 2; pp++)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kbase + (size_t)(2 * A.map.dig[u][i] + pp) * kst),
+                             "r"((u32)(NB * n * 8))
+                             : "memory");
+#endif
+#if HKS_KIP_TWS
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+#endif
 
+#if HKS_KIP_PIPE
+    ulonglong2 kbn[NDIG], kan[NDIG];
+#if HKS_KIP_PIPE == 2
+    // the first product step's key words are requested before the row pass (the key is a caller input)
+    if (2 * tid < NB * n)
+#pragma unroll
+        for (int i = 0; i < NDIG; i++) {
+            const u32 j = A.map.dig[u][i];
+            kbn[i] = *reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j) * kst + 2 * tid);
+            kan[i] = *reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j + 1) * kst + 2 * tid);
+        }
+#endif
+#endif
     // phase 1: thread group i runs the row pass of term i (< NTR) into shared buffer i, concurrently
     {
         const int i = tid / NTG, gt = tid - i * NTG;
         const int bsub = gt >> (LOGN - LOGE);
         const int tu = gt & (TPS - 1);
+#if HKS_KIP_TWS
+        const ulonglong2 *tw = stw + bsub * n;
+#else
         const ulonglong2 *__restrict__ tw = A.tw + (((size_t)prime << A.log_r) + tile * NB + bsub) * n;
+#endif
         u64 *smj = sm + i * BUF + bsub * ROWPAD;
         const bool work = i < (int)A.map.ntr[u];                   // warp-uniform (groups are whole warps)
         const u64 *__restrict__ src = A.ext + (size_t)(A.map.dsrc[u][i] & 0x7fff) * N + tbase + (size_t)bsub * n;
@@ -741,7 +827,11 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
 #pragma unroll
                     for (int k = 0; k < Ee; k++) {
                         if (k & t) continue;
+#if HKS_KIP_TWS
+                        const ulonglong2 w = twb[(k << lstride) >> sh];
+#else
                         const ulonglong2 w = __ldg(twb + ((k << lstride) >> sh));
+#endif
                         ct_lazy(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, m);
                     }
                 }
@@ -762,6 +852,9 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
         }
     }
     __syncthreads();
+#if HKS_KIP_TWS
+    if (A.map.yslot[u] != 0xffff && NTR >= 2) stage_tw(A.tw_inv);   // phase 3's inverse twiddles, under phase 2
+#endif
 
     // phase 2: acc_p = sum_i canon(D_i) * evk_{dig(i)}[p], two coefficients per thread per step; the
     // loads of all terms are issued before the multiply-accumulates.
@@ -775,13 +868,37 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
     const u32 as = A.map.aslot[u];
     const u32 ys = A.map.yslot[u];
     const bool ymode = ys != 0xffff && NTR >= 2;      // uniform per CTA
-    for (int idx = 2 * tid; idx < NB * n; idx += 2 * NT) {
-        const int r = idx >> LOGN, k = idx & (n - 1);
-        ulonglong2 kb[NDIG], ka[NDIG], dv[NDIG];
+#if HKS_KIP_PIPE
+    // key words of step idx (the dominant HBM stream): loaded one step ahead of the products that use them
+    auto load_keys = [&](int idx, ulonglong2 (&kb)[NDIG], ulonglong2 (&ka)[NDIG]) {
 #pragma unroll
         for (int i = 0; i < NDIG; i++) {
             const u32 j = A.map.dig[u][i];
-#if HKS_KIP_TMA
+            kb[i] = *reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j) * kst + idx);
+            ka[i] = *reinterpret_cast<const ulonglong2 *>(kbase + (size_t)(2 * j + 1) * kst + idx);
+        }
+    };
+#if HKS_KIP_PIPE == 1
+    if (2 * tid < NB * n) load_keys(2 * tid, kbn, kan);
+#endif
+#endif
+    for (int idx = 2 * tid; idx < NB * n; idx += 2 * NT) {
+        const int r = idx >> LOGN, k = idx & (n - 1);
+        ulonglong2 kb[NDIG], ka[NDIG], dv[NDIG];
+#if HKS_KIP_PIPE
+#pragma unroll
+        for (int i = 0; i < NDIG; i++) {
+            kb[i] = kbn[i];
+            ka[i] = kan[i];
+        }
+        if (idx + 2 * NT < NB * n) load_keys(idx + 2 * NT, kbn, kan);
+#endif
+#pragma unroll
+        for (int i = 0; i < NDIG; i++) {
+            const u32 j = A.map.dig[u][i];
+#if HKS_KIP_PIPE
+            (void)j;
+#elif HKS_KIP_TMA
             (void)j;
             kb[i] = *reinterpret_cast<const ulonglong2 *>(skey + (size_t)(2 * i) * NB * n + idx);
             ka[i] = *reinterpret_cast<const ulonglong2 *>(skey + (size_t)(2 * i + 1) * NB * n + idx);
@@ -876,7 +993,13 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
         const bool work = g < 2;
         const int bsub = gt >> (LOGN - LOGE);
         const int tu = gt & (TPS - 1);
+#if HKS_KIP_TWS
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        const ulonglong2 *tw = stw + bsub * n;
+#else
         const ulonglong2 *__restrict__ tw = A.tw_inv + (((size_t)prime << A.log_r) + tile * NB + bsub) * n;
+#endif
         u64 *smj = sm + (work ? g : 0) * BUF + bsub * ROWPAD;
         u64 *__restrict__ dst = A.y + ((size_t)(work ? g : 0) * A.ystride + ys) * N + tbase + (size_t)bsub * n;
         u64 v[E];
@@ -913,7 +1036,11 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
 #pragma unroll
                         for (int k = 0; k < Ee; k++) {
                             if (k & t) continue;
+#if HKS_KIP_TWS
+                            const ulonglong2 w = twb[(k << lstride) >> sh];
+#else
                             const ulonglong2 w = __ldg(twb + ((k << lstride) >> sh));
+#endif
                             gs_lazy(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, m);
                         }
                     }
@@ -950,7 +1077,8 @@ template <int LOGN, int LOGE, int LOGNB, int NTR, int NDIG>
 static hks_status go_kip(FusedKipArgs &a, cudaStream_t s) {
     constexpr int threads = NTR * ((1 << LOGNB) << (LOGN - LOGE));
     constexpr size_t smem = (size_t)NTR * ((1 << LOGN) + ((1 << LOGN) >> LOGE)) * (1 << LOGNB) * sizeof(u64) +
-                            (HKS_KIP_TMA ? (size_t)2 * NDIG * (1 << LOGN) * (1 << LOGNB) * sizeof(u64) : 0);
+                            (HKS_KIP_TMA ? (size_t)2 * NDIG * (1 << LOGN) * (1 << LOGNB) * sizeof(u64) : 0) +
+                            (HKS_KIP_TWS ? (size_t)(1 << LOGN) * (1 << LOGNB) * sizeof(ulonglong2) : 0);
     auto kern = k_ntt_kip<LOGN, LOGE, LOGNB, NTR, NDIG>;
     if (smem > 48 * 1024) {
         hks_func_smem((const void *)kern, smem);
