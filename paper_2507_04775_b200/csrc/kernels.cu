@@ -360,9 +360,21 @@ static void bconv_mma_go(const BconvArgs &a, cudaStream_t s) {
 #define TC_EPW HKS_TC_EPW                  // epilogue warps (multiple of 4)
 #define TC_THREADS ((TC_EPW + 4) * 32)
 
+#ifdef BC_TRACE
+__device__ long long g_bc_trace[6 * 64];   // events 0-4 per tile; event 5: kernel entry, after prologue, after griddepcontrol.wait
+extern "C" void *hks_debug_bc_trace() {
+    void *p = nullptr;
+    cudaGetSymbolAddress(&p, g_bc_trace);
+    return p;
+}
+#define BC_T(ev, j) do { if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64) g_bc_trace[(ev) * 64 + (j)] = clock64(); } while (0)
+#else
+#define BC_T(ev, j) do { } while (0)
+#endif
 template <int NSRC, bool LAZY>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constant__ BconvArgs A) {
     pdl_trigger();
+    if (threadIdx.x == 0) BC_T(5, 0);
     constexpr int KPAD = 32 * ((NSRC + 3) / 4);   // bytes of K (whole K = 32 MMA steps)
     constexpr int NCH = KPAD / 16;                // 16-byte K chunks
     constexpr u32 SBO = NCH * 128;                // 8-row group stride
@@ -387,28 +399,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constan
     const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     // ---- prologue (before griddepcontrol.wait: ctx tables only) ----
+    // B operand: the group's precomputed image (nt targets x SBO bytes, contiguous) by one bulk copy on its own
+    // mbarrier (awaited by the MMA issuer only), plus zero rows for the padding target of an odd nt
+    __shared__ __align__(8) u64 bar_img;
     {
-        // B operand: the group's precomputed image (nt targets x SBO bytes, contiguous) plus zero rows for
-        // the padding target of an odd nt; 16-byte loads all issued before the stores
-        const uint4 *img = reinterpret_cast<const uint4 *>(G.mimg + (size_t)bconv_img_words(NSRC) * u0);
         const u32 nimg = nt * (SBO / 16), ntot = (ncol / 8) * (SBO / 16);
-        constexpr int PER = (32 * (SBO / 16) + TC_THREADS - 1) / TC_THREADS;
-        uint4 w[PER];
-#pragma unroll
-        for (int r = 0; r < PER; r++) {
-            const u32 idx = tid + r * TC_THREADS;
-            w[r] = idx < nimg ? __ldg(img + idx) : make_uint4(0, 0, 0, 0);
+        if (tid == 0) {
+            mbar_init(smem_u32(&bar_img), 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar_img)), "r"(nimg * 16)
+                         : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             smem_u32(sB)),
+                         "l"(G.mimg + (size_t)bconv_img_words(NSRC) * u0), "r"(nimg * 16), "r"(smem_u32(&bar_img))
+                         : "memory");
         }
-#pragma unroll
-        for (int r = 0; r < PER; r++) {
-            const u32 idx = tid + r * TC_THREADS;
-            if (idx < ntot) reinterpret_cast<uint4 *>(sB)[idx] = w[r];
-        }
-    }
-    for (u32 t = tid; t < nt; t += TC_THREADS) {
-        const PrimeConst pc = A.pc[G.dst_prime[u0 + t]];
-        sred[t] = make_ulonglong2(0 - pc.p, pc.mu80);
-        sdst[t] = A.out + (size_t)G.dst_slot[u0 + t] * N;
+        for (u32 idx = nimg + tid; idx < ntot; idx += TC_THREADS) reinterpret_cast<uint4 *>(sB)[idx] = make_uint4(0, 0, 0, 0);
     }
     if (tid == 0) {
         for (int b = 0; b < 2; b++) {
@@ -427,7 +433,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constan
     __syncthreads();
     tc_fence_after();
     const u32 tmem = tmem_base_s;
+    if (threadIdx.x == 0) BC_T(5, 1);
     pdl_wait();
+    if (threadIdx.x == 0) BC_T(5, 2);
 
     if (warp >= TC_EPW) {
         // ---------------- producers + MMA issuer ----------------
@@ -458,11 +466,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constan
             } else {
                 asm volatile("cp.async.commit_group;" ::: "memory");   // keep the group count uniform
             }
+            if (ptid == 0) BC_T(0, j);
             asm volatile("cp.async.wait_group %0;" ::"n"(TC_SA - 1) : "memory");
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (ptid == 0) BC_T(1, j);
             if (ptid == 0) {
                 const u32 b = j & 1;
+                if (j == 0) mbar_wait(smem_u32(&bar_img), 0);
                 if (j >= 2) mbar_wait(smem_u32(&bar_empty[b]), ((j >> 1) - 1) & 1);
                 tc_fence_after();
                 const u32 abase = smem_u32(sA + (j % TC_SA) * ATILE), bbase = smem_u32(sB);
@@ -472,37 +483,63 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constan
                               idesc, s > 0 ? 1u : 0u);
                 tc_commit(smem_u32(&bar_free[j % TC_SA]));
                 tc_commit(smem_u32(&bar_done[b]));
+                BC_T(2, j);
             }
         }
     } else {
         // ---------------- epilogue ----------------
+        // warp (quarter q, h) reduces a contiguous run of up to 8 targets: two 32-column TMEM loads and one
+        // wait per tile (the accumulator is released before the reductions), so that eight independent
+        // reductions are in flight per thread
         constexpr u32 NH = TC_EPW / 4;           // warps sharing a TMEM lane quarter
         const u32 q = warp & 3, h = warp >> 2;
         const u32 lrow = q * 32 + lane;           // TMEM lane = coefficient row of the tile
+        const u32 tpw = (nt + NH - 1) / NH;       // <= 8 (nt <= 32, NH = 4)
+        const u32 tb0 = h * tpw, tcnt = nt > tb0 ? min(tpw, nt - tb0) : 0;
+        // per-target reduction constants and output limbs of this run, written by the run's quarter-0 warp and
+        // shared with the other three lane quarters through a named barrier (ids 2 + h): the global loads
+        // stay off the CTA-wide prologue barrier
+        if (q == 0 && (u32)lane < tcnt) {
+            const u32 t = tb0 + lane;
+            const PrimeConst pc = A.pc[G.dst_prime[u0 + t]];
+            sred[t] = make_ulonglong2(0 - pc.p, pc.mu80);
+            sdst[t] = A.out + (size_t)G.dst_slot[u0 + t] * N;
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + h) : "memory");
         for (u32 j = 0; j < ntile; j++) {
             const u32 b = j & 1;
             mbar_wait(smem_u32(&bar_done[b]), (j >> 1) & 1);
+            if (warp == 0 && lane == 0) BC_T(3, j);
             tc_fence_after();
             const size_t x = ((size_t)(blockIdx.x + j * gridDim.x) << 7) + lrow;
-            const u32 tbase = tmem + b * 256 + ((q * 32) << 16);
-            for (u32 t0 = h; t0 < nt; t0 += 4 * NH) {
-                u32 v[4][8];
-#pragma unroll
-                for (int k = 0; k < 4; k++)
-                    if (t0 + k * NH < nt) tc_ld8(tbase + (t0 + k * NH) * 8, v[k]);
-                tc_wait_ld();
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const u32 t = t0 + k * NH;
-                    if (t < nt) {
-                        const ulonglong2 c = sred[t];
-                        sdst[t][x] = bytesum_reduce_c<LAZY>(v[k], c.x, (u32)c.y);
-                    }
-                }
-            }
+            const u32 tbase = tmem + b * 256 + ((q * 32) << 16) + tb0 * 8;
+            u32 v[2][32];
+            if (tcnt > 0) tc_ld32(tbase, v[0]);
+            if (tcnt > 4) tc_ld32(tbase + 32, v[1]);
+            tc_wait_ld();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&bar_empty[b]));
+            // branch-free over the eight slots (a slot past the run reduces target tb0 again and is not stored),
+            // so that the eight reductions interleave instead of running one predicated block after another
+#pragma unroll
+            for (int hh = 0; hh < 2; hh++) {
+                u64 o[4];
+                u64 *dp[4];
+#pragma unroll
+                for (int kk = 0; kk < 4; kk++) {
+                    const u32 k = 4 * hh + kk;
+                    const u32 t = tb0 + (k < tcnt ? k : 0u);
+                    const ulonglong2 c = sred[t];
+                    const u32 *r = &v[hh][8 * kk];
+                    o[kk] = bytesum_reduce_c<LAZY>(r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7], c.x, (u32)c.y);
+                    dp[kk] = sdst[t] + x;
+                }
+#pragma unroll
+                for (int kk = 0; kk < 4; kk++)
+                    if ((u32)(4 * hh + kk) < tcnt) *dp[kk] = o[kk];
+            }
+            if (warp == 0 && lane == 0) BC_T(4, j);
         }
     }
     tc_fence_before();

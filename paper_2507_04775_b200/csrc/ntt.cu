@@ -43,6 +43,9 @@ static thread_local const cudaAccessPolicyWindow *t_win = nullptr;
 #ifndef HKS_KIP_TWS
 #define HKS_KIP_TWS 1     // 1: the CTA's row twiddles staged in shared memory by cp.async issued before griddepcontrol.wait
 #endif
+#ifndef HKS_KIP_EXTS
+#define HKS_KIP_EXTS 0    // 1: the row pass's input rows staged into its shared buffers by cp.async right after
+#endif                    //    griddepcontrol.wait (one memory latency with the twiddles instead of a second one)
 #ifndef HKS_KIP_PIPE
 #define HKS_KIP_PIPE 0    // 1: key words of the next product step loaded before the current step's products
 #endif
@@ -686,11 +689,25 @@ constexpr int kip_minb(int threads) {
                ? 1
                : ((65536 / (HKS_KIP_REGS * threads)) > 16 ? 16 : 65536 / (HKS_KIP_REGS * threads));
 }
+#ifdef KIP_TRACE
+__device__ long long g_kip_trace[8192 * 6];
+extern "C" void *hks_debug_kip_trace() {
+    void *p = nullptr;
+    cudaGetSymbolAddress(&p, g_kip_trace);
+    return p;
+}
+#define KIP_T(ev) do { if (threadIdx.x == 0 && blockIdx.x < 8192) g_kip_trace[blockIdx.x * 6 + (ev)] = (ev) == 5 ? (long long)smid() : clock64(); } while (0)
+__device__ __forceinline__ unsigned smid() { unsigned r; asm volatile("mov.u32 %0, %%smid;" : "=r"(r)); return r; }
+#else
+#define KIP_T(ev) do { } while (0)
+#endif
 template <int LOGN, int LOGE, int LOGNB, int NTR, int NDIG>
 __global__ void __launch_bounds__(NTR * ((1 << LOGNB) << (LOGN - LOGE)),
                                   kip_minb(NTR * ((1 << LOGNB) << (LOGN - LOGE))))
 k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
     pdl_trigger();
+    KIP_T(0);
+    KIP_T(5);
     constexpr int n = 1 << LOGN;
     constexpr int E = 1 << LOGE;
     constexpr int NB = 1 << LOGNB;
@@ -754,6 +771,18 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
     }
 #endif
     pdl_wait();
+#if HKS_KIP_EXTS
+    {
+        const int nw = (int)A.map.ntr[u] * NB * n;
+        for (int e = tid; e < nw; e += NT) {
+            const int i = e / (NB * n), rem = e - i * (NB * n), bs = rem >> LOGN, jj = rem & (n - 1);
+            const u64 *g = A.ext + (size_t)(A.map.dsrc[u][i] & 0x7fff) * N + tbase + rem;
+            const u32 d = (u32)__cvta_generic_to_shared(sm + i * BUF + bs * ROWPAD + jj + (jj >> LOGE));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(g) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+#endif
 #if HKS_KIP_L2PF
     if (tid == 0)
         for (int i = 0; i < NDIG; i++)
@@ -762,10 +791,11 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
                              "r"((u32)(NB * n * 8))
                              : "memory");
 #endif
-#if HKS_KIP_TWS
+#if HKS_KIP_TWS || HKS_KIP_EXTS
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
 #endif
+    KIP_T(1);
 
 #if HKS_KIP_PIPE
     ulonglong2 kbn[NDIG], kan[NDIG];
@@ -811,7 +841,7 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
 #pragma unroll
                 for (int k = 0; k < Ee; k++) {
                     const int jj = base + (k << lstride);
-                    v[q * Ee + k] = rr == 0 ? src[jj] : smj[jj + (jj >> LOGE)];
+                    v[q * Ee + k] = (rr == 0 && !HKS_KIP_EXTS) ? src[jj] : smj[jj + (jj >> LOGE)];
                 }
             }
 #pragma unroll
@@ -837,7 +867,7 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
                 }
             }
             }
-            if (rr > 0) __syncthreads();
+            if (rr > 0 || HKS_KIP_EXTS) __syncthreads();
             if (work)
 #pragma unroll
             for (int q = 0; q < UPT; q++) {
@@ -852,6 +882,7 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
         }
     }
     __syncthreads();
+    KIP_T(2);
 #if HKS_KIP_TWS
     if (A.map.yslot[u] != 0xffff && NTR >= 2) stage_tw(A.tw_inv);   // phase 3's inverse twiddles, under phase 2
 #endif
@@ -983,6 +1014,8 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
             *reinterpret_cast<ulonglong2 *>(A.acc + ((size_t)A.acc_stride + as) * N + tbase + idx) = o1;
         }
     }
+    KIP_T(3);
+    KIP_T(4);
     if (!ymode) return;
 
     // phase 3 (P limbs): ModDown's first inverse-NTT pass (Gentleman-Sande row stages) on acc_0 / acc_1,
@@ -1071,6 +1104,7 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
             }
         }
     }
+    KIP_T(4);
 }
 
 template <int LOGN, int LOGE, int LOGNB, int NTR, int NDIG>
