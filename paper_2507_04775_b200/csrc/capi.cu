@@ -177,13 +177,17 @@ hks_status moddown_core(const hks_ctx *c, const u64 *acc, u32 npoly, u32 level, 
     LimbList M;
     std::vector<uint8_t> poly;
     std::vector<MdOut> mo(npoly);
-    for (u32 p = 0; p < npoly; p++) {
-        mo[p] = MdOut{outs[p], adds ? adds[p] : nullptr, gal ? gal[p] : 1};
-        for (u32 i = 0; i <= level; i++) {
+    for (u32 p = 0; p < npoly; p++) mo[p] = MdOut{outs[p], adds ? adds[p] : nullptr, gal ? gal[p] : 1};
+    // limb-major when one launch can take every polynomial (NTT_MAXO): the polynomials' limbs of one prime are
+    // adjacent in the launch, so the CTAs that read a prime's per-row twiddle table run together and share it
+    // in L2
+    const bool lm = npoly <= NTT_MAXO;
+    for (u32 a = 0; a < (lm ? level + 1 : npoly); a++)
+        for (u32 b = 0; b < (lm ? npoly : level + 1); b++) {
+            const u32 i = lm ? a : b, p = lm ? b : a;
             M.push(p * (level + 1) + i, i, i, p * ne + i, mo[p].add ? i : 0xffff);
             poly.push_back((uint8_t)p);
         }
-    }
     return run_ntt_moddown(c, M, poly, mo, conv, acc, s, tensor);
 }
 
