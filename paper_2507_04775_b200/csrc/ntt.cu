@@ -46,6 +46,9 @@ static thread_local const cudaAccessPolicyWindow *t_win = nullptr;
 #ifndef HKS_KIP_EXTS
 #define HKS_KIP_EXTS 0    // 1: the row pass's input rows staged into its shared buffers by cp.async right after
 #endif                    //    griddepcontrol.wait (one memory latency with the twiddles instead of a second one)
+#ifndef HKS_KIP_XWARP
+#define HKS_KIP_XWARP 0   // 1: four warps per CTA at three digits (the extra one joins the key product)
+#endif
 #ifndef HKS_KIP_PIPE
 #define HKS_KIP_PIPE 0    // 1: key words of the next product step loaded before the current step's products
 #endif
@@ -690,13 +693,13 @@ constexpr int kip_minb(int threads) {
                : ((65536 / (HKS_KIP_REGS * threads)) > 16 ? 16 : 65536 / (HKS_KIP_REGS * threads));
 }
 #ifdef KIP_TRACE
-__device__ long long g_kip_trace[8192 * 6];
+__device__ long long g_kip_trace[8192 * 12];
 extern "C" void *hks_debug_kip_trace() {
     void *p = nullptr;
     cudaGetSymbolAddress(&p, g_kip_trace);
     return p;
 }
-#define KIP_T(ev) do { if (threadIdx.x == 0 && blockIdx.x < 8192) g_kip_trace[blockIdx.x * 6 + (ev)] = (ev) == 5 ? (long long)smid() : clock64(); } while (0)
+#define KIP_T(ev) do { if (threadIdx.x == 0 && blockIdx.x < 8192) g_kip_trace[blockIdx.x * 12 + (ev)] = (ev) == 5 ? (long long)smid() : clock64(); } while (0)
 __device__ __forceinline__ unsigned smid() { unsigned r; asm volatile("mov.u32 %0, %%smid;" : "=r"(r)); return r; }
 #else
 #define KIP_T(ev) do { } while (0)
@@ -844,6 +847,15 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
                     v[q * Ee + k] = (rr == 0 && !HKS_KIP_EXTS) ? src[jj] : smj[jj + (jj >> LOGE)];
                 }
             }
+#ifdef KIP_TRACE
+            if (threadIdx.x == 0 && blockIdx.x < 8192) {   // first use of the gathered values
+                u64 acc = 0;
+#pragma unroll
+                for (int q = 0; q < E; q++) acc ^= v[q];
+                g_kip_trace[blockIdx.x * 12 + 6 + 3 * rr] = clock64() + (long long)(acc & 1) * 0;
+                asm volatile("" ::"l"(acc));
+            }
+#endif
 #pragma unroll
             for (int q = 0; q < UPT; q++) {
                 const int uid = tu * UPT + q;
@@ -866,8 +878,20 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
                     }
                 }
             }
+#ifdef KIP_TRACE
+            if (threadIdx.x == 0 && blockIdx.x < 8192) {
+                u64 acc = 0;
+#pragma unroll
+                for (int q = 0; q < E; q++) acc ^= v[q];
+                asm volatile("" ::"l"(acc));
+                g_kip_trace[blockIdx.x * 12 + 7 + 3 * rr] = clock64();
+            }
+#endif
             }
             if (rr > 0 || HKS_KIP_EXTS) __syncthreads();
+#ifdef KIP_TRACE
+            if (threadIdx.x == 0 && blockIdx.x < 8192) g_kip_trace[blockIdx.x * 12 + 8 + 3 * rr] = clock64();
+#endif
             if (work)
 #pragma unroll
             for (int q = 0; q < UPT; q++) {
@@ -1137,6 +1161,9 @@ template <int LOGN, int LOGE, int LOGNB>
 static hks_status go_kip_d(FusedKipArgs &a, cudaStream_t s) {
 #define KC(T, D) if (a.ntr == T && a.ndig == D) return go_kip<LOGN, LOGE, LOGNB, T, D>(a, s);
     KC(1, 1) KC(2, 1) KC(1, 2) KC(2, 2) KC(2, 3) KC(3, 3) KC(3, 4) KC(4, 4)
+#if HKS_KIP_XWARP
+    KC(4, 3)
+#endif
 #undef KC
     if (a.ntr == 0) { a.ntr = 1; return go_kip_d<LOGN, LOGE, LOGNB>(a, s); }   // all-direct launch
     HKS_FAIL(HKS_EINVAL, "ntt_kip: %u transformed of %u digits", a.ntr, a.ndig);
@@ -1156,7 +1183,7 @@ hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s) {
     a.log_n = ctx->log_n;
     a.log_r = ctx->log_r;
     a.log_c = ctx->log_c;
-    if (a.ndig > FK_MAXD || a.nu > FK_MAXU || a.ntr > (a.ndig > 2 ? a.ndig : 2))
+    if (a.ndig > FK_MAXD || a.nu > FK_MAXU || a.ntr > (a.ndig > 2 ? a.ndig + HKS_KIP_XWARP : 2))
         HKS_FAIL(HKS_EINVAL, "ntt_kip: %u digits (%u transformed) / %u limbs per launch", a.ndig, a.ntr, a.nu);
     switch (ctx->log_n) {
         case 17: return go_kip_d<8, 4, HKS_KIP_LOGNB>(a, s);
@@ -1224,6 +1251,9 @@ hks_status run_ntt_kip(const hks_ctx *ctx, const std::vector<KipItem> &items_in,
         bool anyy = false;
         for (u32 uu = 0; uu < a.nu; uu++) anyy |= a.map.yslot[uu] != 0xffff;
         if (anyy && a.ntr < 2) a.ntr = 2;
+#if HKS_KIP_XWARP
+        if (a.ntr == 3 && ndig == 3) a.ntr = 4;   // a fourth warp: idle in the row pass, 2 product steps per thread
+#endif
         hks_status st = launch_ntt_kip(ctx, a, s);
         if (st != HKS_OK) return st;
     }
