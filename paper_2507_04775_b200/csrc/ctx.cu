@@ -449,8 +449,10 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
                 cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
                 if (cur < (size_t)maxp) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp);
                 cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-                c->tw_win.base_ptr = c->d_tw_all;
-                c->tw_win.num_bytes = std::min(bytes, (size_t)maxw);
+                // HKS_TW_PERSIST == 2: only the inverse tables (the c1 INTT's per-row table is the 3x re-read)
+                const size_t off = HKS_TW_PERSIST == 2 ? (size_t)(c->d_tw_col_inv - c->d_tw_all) : 0;
+                c->tw_win.base_ptr = c->d_tw_all + off;
+                c->tw_win.num_bytes = std::min(bytes - off * sizeof(ulonglong2), (size_t)maxw);
                 c->tw_win.hitRatio = (float)std::min(1.0, (double)cur / (double)c->tw_win.num_bytes);
                 c->tw_win.hitProp = cudaAccessPropertyPersisting;
                 c->tw_win.missProp = cudaAccessPropertyStreaming;

@@ -188,6 +188,7 @@ struct NttMod {
     u64 p, np;       // p and 2^64 - p
     u64 two_p, four_p, eight_p;
     u32 h4;          // (4p) >> 32: hi-word threshold of the one-instruction range test
+    u64 zh;          // 0, but opaque to ptxas (derived from p): see lazy_add
 };
 
 HKS_DEV NttMod make_nttmod(u64 p) {
@@ -198,8 +199,17 @@ HKS_DEV NttMod make_nttmod(u64 p) {
     m.four_p = 4 * p;
     m.eight_p = 8 * p;
     m.h4 = (u32)((4 * p) >> 32);
+    m.zh = (u64)(u32)(p >> 63) << 32;   // p < 2^60: zero
     return m;
 }
+
+// x + y for the butterflies.  ptxas lowers a two-operand 64-bit add to IADD3 + IMAD.X, and IMAD.X issues
+// on the FMA-heavy pipe of the Shoup products (~1.25 per butterfly).  With OPQ the opaque zero m.zh joins
+// the high word, so the carry-add is a three-input IADD3.X on the ALU pipe, at no extra instruction.
+// Measured per pass: faster for the inverse row pass only (ptxas then re-balances the other
+// passes with IMAD.MOV and select instructions), so the choice is a template parameter of the butterflies.
+template <bool OPQ>
+HKS_DEV u64 lazy_add(u64 x, u64 y, const NttMod &m) { return OPQ ? x + y + m.zh : x + y; }
 
 // Shoup product with an approximate quotient: three 32x32 partial products of y * w' (the
 // low x low one dropped), so q is short by 0..2 and the result is y*w mod p in [0, 4p) for any
@@ -245,8 +255,10 @@ HKS_DEV u64 shoup_approx(u64 y, u64 w, u64 wp, u64 np) {
 }
 
 // x >= 4p (tested on the high word only) ? x - 4p : x.  For x < 8p + 2^32 the result is < 4p + 2^32.
+template <bool OPQ = false>
 HKS_DEV u64 lazy_sub4p(u64 x, const NttMod &m) {
     u64 r = x;
+    if (!OPQ) {
     asm("{\n\t"
         ".reg .pred p;\n\t"
         ".reg .u32 xl, xh, fl, fh;\n\t"
@@ -259,23 +271,43 @@ HKS_DEV u64 lazy_sub4p(u64 x, const NttMod &m) {
         "}"
         : "+l"(r) : "r"(m.h4), "l"(m.four_p));
     return r;
+    }
+    // OPQ: x - 4p with the opaque zero in its high word (see lazy_add): a three-input IADD3.X, not IMAD.X
+    asm("{\n\t"
+        ".reg .pred p;\n\t"
+        ".reg .u32 xl, xh, fl, fh, zl, zh, dl, dh;\n\t"
+        "mov.b64 {xl, xh}, %0;\n\t"
+        "mov.b64 {fl, fh}, %2;\n\t"
+        "mov.b64 {zl, zh}, %3;\n\t"
+        "setp.gt.u32 p, xh, %1;\n\t"
+        "sub.cc.u32 dl, xl, fl;\n\t"
+        "subc.u32 dh, xh, fh;\n\t"
+        "add.u32 dh, dh, zh;\n\t"
+        "selp.b32 xl, dl, xl, p;\n\t"
+        "selp.b32 xh, dh, xh, p;\n\t"
+        "mov.b64 %0, {xl, xh};\n\t"
+        "}"
+        : "+l"(r) : "r"(m.h4), "l"(m.four_p), "l"(m.zh));
+    return r;
 }
 
 // Forward CT butterfly on the lazy range [0, 8p + 2^32):  X' = x + t, Y' = x - t + 4p with
 // x = X reduced below 4p + 2^32 and t = Y*w in [0, 4p).  Both outputs stay in [0, 8p + 2^32).
+template <bool OPQ = false>
 HKS_DEV void ct_lazy(u64 &X, u64 &Y, u64 w, u64 wp, const NttMod &m) {
-    const u64 x = lazy_sub4p(X, m);
+    const u64 x = lazy_sub4p<OPQ>(X, m);
     const u64 t = shoup_approx(Y, w, wp, m.np);
-    X = x + t;
+    X = lazy_add<OPQ>(x, t, m);
     Y = x - t + m.four_p;
 }
 
 // Inverse GS butterfly.  Inputs < 4p + c with c <= 2^(32+s) after s stages (c < 4p for every
 // supported N): X' = X + Y reduced by 4p on the high-word test (< 4p + 2c), Y' = (X - Y + 8p)*w in
 // [0, 4p).
+template <bool OPQ = false>
 HKS_DEV void gs_lazy(u64 &X, u64 &Y, u64 w, u64 wp, const NttMod &m) {
     const u64 x = X, y = Y;
-    X = lazy_sub4p(x + y, m);
+    X = lazy_sub4p<OPQ>(lazy_add<OPQ>(x, y, m), m);
     Y = shoup_approx(x - y + m.eight_p, w, wp, m.np);
 }
 

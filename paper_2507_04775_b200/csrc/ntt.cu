@@ -52,6 +52,9 @@ static thread_local const cudaAccessPolicyWindow *t_win = nullptr;
 #ifndef HKS_KIP_PIPE
 #define HKS_KIP_PIPE 0    // 1: key words of the next product step loaded before the current step's products
 #endif
+#ifndef HKS_KIP_PF
+#define HKS_KIP_PF 0      // 1 / 2: phase 2's key lines prefetched into L1 / L2 at the start of the last row round
+#endif
 #ifndef HKS_KIP_L2PF
 #define HKS_KIP_L2PF 0    // 1: the CTA's key rows prefetched into L2 (bulk prefetch) at the start of the row pass
 #endif
@@ -71,6 +74,15 @@ static thread_local const cudaAccessPolicyWindow *t_win = nullptr;
 #ifndef HKS_ROW_TWS
 #define HKS_ROW_TWS 0   // 1: measured slower for the stand-alone row passes (8-row tiles, 32 KB per CTA up front)
 #endif
+#ifndef HKS_INVROW_OPQ
+#define HKS_INVROW_OPQ 1  // inverse row passes: butterfly carry-adds on the ALU pipe (modarith.cuh lazy_add)
+#endif
+#ifndef HKS_KIP_OPQ
+#define HKS_KIP_OPQ 0     // the same for the fused kernel's ModDown inverse row pass
+#endif
+#ifndef HKS_ROW_WSYNC
+#define HKS_ROW_WSYNC 1   // row passes: a row never straddles a warp, so the exchanges between rounds (and the
+#endif                    // staged tile load / copy-out, mapped warp by warp) need __syncwarp, not CTA barriers
 template <int LOGN, int LOGE, int LOGNB, bool COLS>
 constexpr bool row_tws() {
     return HKS_ROW_TWS && !COLS &&
@@ -117,6 +129,14 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
     auto saddr = [&](int k) -> int {
         return COLS ? (k + (k >> LOGE)) * NB + bsub : bsub * ROWPAD + k + (k >> LOGE);
     };
+    // warp-private rows: thread tid's sub-transform bsub = tid / TPS lies inside tid's warp, so the warp's
+    // rows are the 32 E contiguous tile words [warp * 32 E, (warp + 1) * 32 E)
+    constexpr bool WS = HKS_ROW_WSYNC && !COLS && TPS <= 32 && (NT % 32) == 0 && !row_tws<LOGN, LOGE, LOGNB, COLS>();
+    auto rsync = [&]() {
+        if (WS) __syncwarp(); else __syncthreads();
+    };
+    // tile word handled by this thread in the q-th coalesced sweep of a staged load / copy-out
+    auto tix = [&](int q) -> int { return WS ? ((tid & ~31) * E + (tid & 31) + 32 * q) : (tid + q * NT); };
 
     // epilogue constants
     ulonglong2 sc = make_ulonglong2(0, 0);
@@ -162,12 +182,12 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
                 u64 x1[TC], x2[TC];
 #pragma unroll
                 for (int q = 0; q < TC; q++) {
-                    x1[q] = tsrc[tid + (q0 + q) * NT];
-                    x2[q] = tsrc2[tid + (q0 + q) * NT];
+                    x1[q] = tsrc[tix(q0 + q)];
+                    x2[q] = tsrc2[tix(q0 + q)];
                 }
 #pragma unroll
                 for (int q = 0; q < TC; q++) {
-                    const int idx = tid + (q0 + q) * NT, r = idx >> LOGN, k = idx & (n - 1);
+                    const int idx = tix(q0 + q), r = idx >> LOGN, k = idx & (n - 1);
                     const u64 d = mulmod_full(x1[q], x2[q], pcb);
                     tside[idx] = d;
                     sm[r * ROWPAD + k + (k >> LOGE)] = d;
@@ -176,14 +196,14 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
         } else {
             u64 tmp[E];
 #pragma unroll
-            for (int q = 0; q < E; q++) tmp[q] = tsrc[tid + q * NT];
+            for (int q = 0; q < E; q++) tmp[q] = tsrc[tix(q)];
 #pragma unroll
             for (int q = 0; q < E; q++) {
-                const int idx = tid + q * NT, r = idx >> LOGN, k = idx & (n - 1);
+                const int idx = tix(q), r = idx >> LOGN, k = idx & (n - 1);
                 sm[r * ROWPAD + k + (k >> LOGE)] = tmp[q];
             }
         }
-        __syncthreads();
+        rsync();
     }
 
     u64 v[E];
@@ -197,7 +217,7 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
         const int lBsz = lstride + e;                       // log2 block size
         const bool from_global = (rr == 0) && (FWD || COLS);
         const bool last = (rr == NR - 1);
-        if (rr > 0) __syncthreads();
+        if (rr > 0) rsync();
 
         // gather
 #pragma unroll
@@ -242,14 +262,14 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
                     if (FWD)
                         ct_lazy(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, m);
                     else
-                        gs_lazy(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, m);
+                        gs_lazy<!COLS && HKS_INVROW_OPQ>(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, m);
                 }
             }
         }
         // scatter
         const bool via_smem_out = last && FWD && !COLS;
         if (!last || via_smem_out) {
-            if (rr > 0 || !from_global) __syncthreads();
+            if (rr > 0 || !from_global) rsync();
 #pragma unroll
             for (int q = 0; q < UPT; q++) {
                 const int uid = tu * UPT + q;
@@ -279,7 +299,7 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
     if (FWD && !COLS) {
         // forward ROWS (last forward pass): coalesced copy-out through shared memory, epilogue here.
         // All global operands of the epilogue are loaded first so their latencies overlap.
-        __syncthreads();
+        rsync();
         const size_t tbase = (size_t)tile * NB * n;
         u64 *__restrict__ tdst = out_base + (size_t)A.map.sout[b] * N + tbase;
         constexpr int CHM = EPI == EPI_MDTENSOR ? 2 : 8;
@@ -292,11 +312,11 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
             if (MD) {
                 const u64 *__restrict__ tea = A.ea + (size_t)A.map.sa[b] * N + tbase;
 #pragma unroll
-                for (int q = 0; q < CH; q++) av[q] = tea[tid + (q0 + q) * NT];
+                for (int q = 0; q < CH; q++) av[q] = tea[tix(q0 + q)];
                 if (EPI == EPI_MDTENSOR) {
 #pragma unroll
                     for (int q = 0; q < CH; q++) {
-                        const size_t o = tso + tid + (q0 + q) * NT;
+                        const size_t o = tso + tix(q0 + q);
                         ta[q] = A.ta0[o];
                         tb[q] = role1 ? A.tb1[o] : A.tb0[o];
                         if (role1) {
@@ -308,14 +328,14 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
                 if (eb) {
 #pragma unroll
                     for (int q = 0; q < CH; q++) {
-                        const u32 xg = (u32)(tbase + tid + (q0 + q) * NT);
+                        const u32 xg = (u32)(tbase + tix(q0 + q));
                         bv[q] = eb[galois == 1 ? xg : automorph_src(xg, log_n, galois)];
                     }
                 }
             }
 #pragma unroll
             for (int q = 0; q < CH; q++) {
-                const int idx = tid + (q0 + q) * NT, r = idx >> LOGN, k = idx & (n - 1);
+                const int idx = tix(q0 + q), r = idx >> LOGN, k = idx & (n - 1);
                 u64 x = sm[r * ROWPAD + k + (k >> LOGE)];
                 if (EPI == EPI_CANON) {
                     x = canon8(x, m);
@@ -720,6 +740,12 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
     constexpr int NR = (LOGN + LOGE - 1) / LOGE;
     constexpr int ROWPAD = n + (n >> LOGE);
     constexpr int BUF = NB * ROWPAD;
+    // thread groups are whole warps and rows never straddle a warp: the row rounds of phases 1 and 3
+    // exchange through warp-private shared rows, so __syncwarp orders them (HKS_ROW_WSYNC)
+    constexpr bool KWS = HKS_ROW_WSYNC && (NTG % 32) == 0 && TPS <= 32 && !HKS_KIP_EXTS;
+    auto gsync = [&]() {
+        if (KWS) __syncwarp(); else __syncthreads();
+    };
     extern __shared__ __align__(16) u64 sm[];
 
     const u32 u = blockIdx.x / A.tiles;
@@ -835,7 +861,22 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
             const int UPT = E >> e;
             const int lstride = LOGN - s0 - e;
             const int lBsz = lstride + e;
-            if (rr > 0) __syncthreads();
+#if HKS_KIP_PF
+            if (rr == NR - 1) {
+                // phase 2's key rows (2 NDIG runs of NB n words) requested into L1 (1) / L2 (2) one round
+                // before the product: one 128-byte line per request, spread over the CTA's threads
+                constexpr int LINES = NB * n * 8 / 128;
+                for (int e2 = tid; e2 < 2 * NDIG * LINES; e2 += NT) {
+                    const int run = e2 / LINES, ln = e2 - run * LINES;
+                    const u64 *a = kbase + (size_t)(2 * A.map.dig[u][run >> 1] + (run & 1)) * kst + ln * 16;
+                    if (HKS_KIP_PF == 1)
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+                    else
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+                }
+            }
+#endif
+            if (rr > 0) gsync();
             if (work) {
 #pragma unroll
             for (int q = 0; q < UPT; q++) {
@@ -888,7 +929,7 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
             }
 #endif
             }
-            if (rr > 0 || HKS_KIP_EXTS) __syncthreads();
+            if (rr > 0 || HKS_KIP_EXTS) gsync();
 #ifdef KIP_TRACE
             if (threadIdx.x == 0 && blockIdx.x < 8192) g_kip_trace[blockIdx.x * 12 + 8 + 3 * rr] = clock64();
 #endif
@@ -1069,7 +1110,7 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
             const int lstride = s0;
             const int lBsz = lstride + e;
             const bool last = rr == NR - 1;
-            if (rr > 0) __syncthreads();
+            if (rr > 0) gsync();
             if (work) {
 #pragma unroll
                 for (int q = 0; q < UPT; q++) {
@@ -1098,13 +1139,13 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
 #else
                             const ulonglong2 w = __ldg(twb + ((k << lstride) >> sh));
 #endif
-                            gs_lazy(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, m);
+                            gs_lazy<HKS_KIP_OPQ>(v[q * Ee + k], v[q * Ee + k + t], w.x, w.y, m);
                         }
                     }
                 }
             }
             if (!last) {
-                __syncthreads();
+                gsync();
                 if (work) {
 #pragma unroll
                     for (int q = 0; q < UPT; q++) {
