@@ -66,6 +66,7 @@ struct NttArgs {
     u64 *out;
     const PrimeConst *pc;      // per prime
     const ulonglong2 *tw;      // COLS: [nprimes][R] ; ROWS: [nprimes][R][C]   (w, w') pairs
+    const ulonglong2 *tw2;     // single-pass cluster INTT (k_intt_cl): the column table; tw = the row table
     const ulonglong2 *scale;   // EPI_SCALE: per-limb (w, w') = scale[b % scale_mod]; NULL -> ninv[prime]
     const ulonglong2 *ninv;    // per prime N^-1
     const u64 *ea;             // EPI_MODDOWN operand a base (acc)
@@ -302,7 +303,7 @@ struct hks_ctx {
 // ----------------------------------------------------------------------------------------------
 // diagnostics (prof.cu): launch counter + optional per-launch event pair tagged with a kernel class
 enum KCls { K_NTT_FWD_COLS = 0, K_NTT_FWD_ROWS, K_NTT_FWD_ROWS_MODDOWN, K_NTT_INV_ROWS, K_NTT_INV_COLS, K_BCONV,
-            K_KIP, K_AUTOMORPH, K_NTT_ROWS_KIP, K_WSUM, K_ADD, K_NCLS };
+            K_KIP, K_AUTOMORPH, K_NTT_ROWS_KIP, K_WSUM, K_ADD, K_NTT_INV_FUSED, K_NCLS };
 struct ProfScope {
     int cls;
     cudaStream_t s;

@@ -20,7 +20,7 @@ std::vector<Rec> g_recs;
 std::vector<cudaEvent_t> g_pool;
 const char *g_names[K_NCLS] = {"ntt_fwd_cols", "ntt_fwd_rows", "ntt_fwd_rows_moddown", "ntt_inv_rows",
                                "ntt_inv_cols_scale", "bconv", "kip", "automorph", "ntt_rows_kip", "pt_wsum",
-                               "add_ct"};
+                               "add_ct", "ntt_inv_fused"};
 
 cudaEvent_t get_event() {
     std::lock_guard<std::mutex> l(g_mu);

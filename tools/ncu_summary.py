@@ -29,6 +29,8 @@ def kernel_class(name: str) -> str:
         return "kip"
     if name.startswith("k_automorph"):
         return "automorph"
+    if name.startswith("k_intt_cl"):
+        return "ntt_inv_fused"
     if name.startswith("k_ntt<") or name.startswith("void k_ntt<"):
         args = name[name.index("<") + 1:name.index(">")].split(",")
         cols, fwd, epi = int(args[4]), int(args[5]), int(args[6])
