@@ -54,6 +54,9 @@ static thread_local const cudaAccessPolicyWindow *t_win = nullptr;
 #ifndef HKS_KIP_PIPE
 #define HKS_KIP_PIPE 0    // 1: key words of the next product step loaded before the current step's products
 #endif
+#ifndef HKS_KIP_LATEWAIT
+#define HKS_KIP_LATEWAIT 1   // the staged twiddles are awaited after the row pass's first loads are issued, so the
+#endif                       // two memory latencies overlap instead of following each other
 #ifndef HKS_KIP_PF
 #define HKS_KIP_PF 0      // 1 / 2: phase 2's key lines prefetched into L1 / L2 at the start of the last row round
 #endif
@@ -999,7 +1002,7 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
                              "r"((u32)(NB * n * 8))
                              : "memory");
 #endif
-#if HKS_KIP_TWS || HKS_KIP_EXTS
+#if (HKS_KIP_TWS || HKS_KIP_EXTS) && !(HKS_KIP_LATEWAIT && HKS_KIP_TWS && !HKS_KIP_EXTS)
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
 #endif
@@ -1067,6 +1070,14 @@ k_ntt_kip(const __grid_constant__ FusedKipArgs A) {
                     v[q * Ee + k] = (rr == 0 && !HKS_KIP_EXTS) ? src[jj] : smj[jj + (jj >> LOGE)];
                 }
             }
+#if HKS_KIP_LATEWAIT && HKS_KIP_TWS && !HKS_KIP_EXTS
+            }
+            if (rr == 0) {   // the staged twiddle rows, awaited after the round-0 loads were issued
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                __syncthreads();
+            }
+            if (work) {
+#endif
 #ifdef KIP_TRACE
             if (threadIdx.x == 0 && blockIdx.x < 8192) {   // first use of the gathered values
                 u64 acc = 0;
