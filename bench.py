@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--streams", type=int, default=0,
                     help="C1/C2/C4: ciphertexts KeySwitched concurrently per step, one CUDA stream each "
                          "(0 = the measured best per config: C1 8, C2 3, C4 2)")
+    ap.add_argument("--key", choices=("prepared", "plain"), default="prepared",
+                    help="C1/C2/C4: keys prepared once at load time with hks_evk_prepare (P^-1 on the Q limbs, "
+                         "outside the timed region; bit-identical outputs) or used as generated")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e / NTT / profile legs (for ncu runs)")
     ap.add_argument("--no-graph", action="store_true",
@@ -287,11 +290,17 @@ class KSWorkload:
     unit = "KeySwitch/s"
     scaling = "weak"
 
-    def __init__(self, H, ctx, cfg, level, nsets, dev, seed, sid, conc=1):
+    def __init__(self, H, ctx, cfg, level, nsets, dev, seed, sid, conc=1, key="plain"):
         import torch
         self.H, self.ctx, self.cfg, self.level, self.sid = H, ctx, cfg, level, sid
         nsets = max(nsets, conc)
         self.sets = make_sets(cfg, level, nsets, dev, seed)
+        self.key = key
+        if key == "prepared":   # once per key at load time (include/hks.h hks_evk_prepare); dumps keep the raw key
+            for s in self.sets:
+                s["evk_raw"] = s["evk"]
+                s["evk"] = H.evk_prepare(ctx, s["evk"], out=torch.empty_like(s["evk"]), stream=sid)
+            torch.cuda.synchronize()
         self.conc = conc
         self.wss = [ctx.workspace(H.OP_KEYSWITCH, level) for _ in range(conc)]
         self.ws = self.wss[0]
@@ -338,7 +347,8 @@ class KSWorkload:
         self.step1(0)
         import torch
         torch.cuda.synchronize()
-        save_npy(d, rank, level=self.level, c0=s["c0"], c1=s["c1"], evk=s["evk"], out0=s["out0"], out1=s["out1"])
+        save_npy(d, rank, level=self.level, c0=s["c0"], c1=s["c1"], evk=s.get("evk_raw", s["evk"]), out0=s["out0"],
+                 out1=s["out1"])
 
     # e2e: every step copies its ciphertext (c0, c1) H2D from pinned host memory, runs the KeySwitch
     # and copies (out0, out1) D2H.  Three streams pipeline step i's H2D, step i-1's KeySwitch and
@@ -704,7 +714,7 @@ def main():
         wl = C5Workload(H, ctx, cfg, dev, seed, sid)
     else:
         conc = args.streams or {"C1": 8, "C2": 3, "C4": 2}.get(cfg.name, 1)
-        wl = KSWorkload(H, ctx, cfg, level, args.sets, dev, seed, sid, conc)
+        wl = KSWorkload(H, ctx, cfg, level, args.sets, dev, seed, sid, conc, args.key)
 
     for i in range(args.warmup):
         wl.step(i)
@@ -977,6 +987,9 @@ def main():
                            "l2": wl.l2_note(),
                            **({"batch": (f"{wl.conc} ciphertexts per step, each KeySwitched on its own CUDA stream"
                                          if wl.conc > 1 else "1 ciphertext per step")}
+                              if isinstance(wl, KSWorkload) else {}),
+                           **({"key": ("prepared once at load time (hks_evk_prepare: P^-1 on the Q limbs, folded "
+                                       "into the ModDown conversion)" if wl.key == "prepared" else "as generated")}
                               if isinstance(wl, KSWorkload) else {})},
                 "gpu_launches": launches, "clocks": clk.summary(),
                 "launch_mode": (f"CUDA graph replay of the C-ABI calls ({glaunch[0]} kernels per step)" if graphs

@@ -24,7 +24,8 @@
  *             that reads a key takes the key's digit count `evk_digits`: the call needs the first
  *             beta(level) digits, so a key generated with fewer digits than the context's dnum is
  *             usable at the levels it covers.  evk_digits < beta(level) or > dnum -> HKS_EKEY
- *             ("ksk digit count < beta"), checked before any launch.
+ *             ("ksk digit count < beta"), checked before any launch.  A key from
+ *             hks_evk_prepare is passed with evk_digits | HKS_EVK_PREPARED.
  *   Streams   Every compute call is enqueued on `stream` (a cudaStream_t passed as void*; NULL =
  *             legacy default stream).  Argument errors return synchronously before any launch;
  *             launch failures return HKS_ECUDA; asynchronous device faults surface on the
@@ -158,6 +159,22 @@ hks_status hks_ksk_inner_product(const hks_ctx *ctx, const uint64_t *ext, const 
  *   ws   hks_workspace_bytes(ctx, HKS_OP_MODDOWN, level, 0) bytes. */
 hks_status hks_moddown(const hks_ctx *ctx, const uint64_t *acc, uint32_t level, uint64_t *out, void *ws,
                        void *stream);
+
+/* Key preparation (optional, bit-exact by construction): evk_out = evk_in with every Q limb
+ * (key limb index t <= L, both components of every digit) multiplied by [P^-1]_{q_t}; the P limbs are copied
+ * unscaled.  Because acc = sum_j D_j evk_j is linear in the key, ModDown's (acc_Q - NTT(conv)) P^-1 becomes
+ * acc'_Q - NTT(conv') with the P^-1 folded into the P -> Q conversion matrix (a context table): the
+ * ModDown epilogue loses one modular product per output, and the outputs are identical in every Z_{q_i}.
+ * Done once per key at load time; no Shoup companion is stored (it would double the key stream).
+ *   evk_in, evk_out  [evk_digits][2][L+1+K][N] EVAL, 1 <= evk_digits <= dnum (else HKS_EKEY); evk_out ==
+ *                    evk_in (in place) or disjoint (HKS_EINVAL on partial overlap); caller-owned.
+ * The prepared key is passed to hks_keyswitch, hks_relinearize, hks_hmult, hks_rotate_hoisted,
+ * hks_rotate_hoisted_batch and hks_linear_transform as evk_digits | HKS_EVK_PREPARED.  The step-level
+ * hks_ksk_inner_product rejects it (HKS_EINVAL: hks_moddown would apply P^-1 twice), and so do the
+ * limb-sharded hks_shard_* calls (HKS_EKEY). */
+#define HKS_EVK_PREPARED 0x10000u
+hks_status hks_evk_prepare(const hks_ctx *ctx, const uint64_t *evk_in, uint32_t evk_digits, uint64_t *evk_out,
+                           void *stream);
 
 /* Hybrid KeySwitch of ct = (c0, c1) at `level`:
  *   out0 = c0 + ModDown(acc0), out1 = ModDown(acc1), acc = KIP(ModUp(c1), evk).

@@ -144,9 +144,11 @@ hks_status ntt_kip_core(const hks_ctx *c, const u64 *ext, const u64 *c1, const u
 // ModDown of npoly accumulators (acc poly p at slots p * ne + t) into outs[p], + adds[p] read through
 // the automorphism gal[p].  ws: y [npoly][K][N] then conv [npoly][l+1][N].  y_rows_done: the inverse
 // row pass of the P limbs already ran inside k_ntt_kip (y holds it).
+// prepared: the accumulators come from a key prepared by hks_evk_prepare (Q limbs times P^-1): the conversion
+// uses the P^-1-folded matrix and the epilogue skips its P^-1 product (bit-identical outputs)
 hks_status moddown_core(const hks_ctx *c, const u64 *acc, u32 npoly, u32 level, u64 *const *outs,
                         const u64 *const *adds, const u64 *gal, u64 *ws, cudaStream_t s, bool y_rows_done = false,
-                        const u64 *const *tensor = nullptr) {
+                        const u64 *const *tensor = nullptr, bool prepared = false) {
     const u32 ne = c->ne(level), K = c->np;
     u64 *y = ws, *conv = ws + (size_t)npoly * K * c->n;
     hks_status st = HKS_OK;
@@ -170,7 +172,11 @@ hks_status moddown_core(const hks_ctx *c, const u64 *acc, u32 npoly, u32 level, 
         for (u32 k = 0; k < K; k++) src[k] = (u16)(p * K + k);
         std::vector<u16> ds(level + 1);
         for (u32 i = 0; i <= level; i++) ds[i] = (u16)(p * (level + 1) + i);
-        add_groups(groups, K, src, c->d_md_mat, c->nq, ds, dp, c->d_md_matf, c->d_md_mats, c->d_md_matb, c->d_md_img);
+        if (prepared)
+            add_groups(groups, K, src, c->d_mdp_mat, c->nq, ds, dp, c->d_mdp_matf, c->d_mdp_mats, c->d_mdp_matb,
+                       c->d_mdp_img);
+        else
+            add_groups(groups, K, src, c->d_md_mat, c->nq, ds, dp, c->d_md_matf, c->d_md_mats, c->d_md_matb, c->d_md_img);
     }
     st = run_bconv_groups(c, groups, y, conv, s);
     if (st != HKS_OK) return st;
@@ -188,7 +194,7 @@ hks_status moddown_core(const hks_ctx *c, const u64 *acc, u32 npoly, u32 level, 
             M.push(p * (level + 1) + i, i, i, p * ne + i, mo[p].add ? i : 0xffff);
             poly.push_back((uint8_t)p);
         }
-    return run_ntt_moddown(c, M, poly, mo, conv, acc, s, tensor);
+    return run_ntt_moddown(c, M, poly, mo, conv, acc, s, tensor, nullptr, prepared);
 }
 
 hks_status kip_core(const hks_ctx *c, const u64 *ext, const u64 *c1, const u64 *evk, u32 level, u64 galois,
@@ -225,13 +231,18 @@ size_t rot_batch(const hks_ctx *c, u32 level) {
 }
 
 // the key's digit count (include/hks.h "Keys"): a call at `level` reads digits 0..beta(level)-1
+// HKS_EVK_PREPARED in evk_digits marks a key from hks_evk_prepare
+static bool evk_prepared(u32 evk_digits) { return (evk_digits & HKS_EVK_PREPARED) != 0; }
 hks_status check_evk(const hks_ctx *c, u32 evk_digits, u32 level, const char *where) {
+    evk_digits &= ~HKS_EVK_PREPARED;
     if (evk_digits < c->beta(level) || evk_digits > c->dnum)
         HKS_FAIL(HKS_EKEY, "%s: key has %u digits; level %u needs %u (context dnum %u)", where, evk_digits, level,
                  c->beta(level), c->dnum);
     return HKS_OK;
 }
-size_t evk_bytes(const hks_ctx *c, u32 evk_digits) { return (size_t)evk_digits * 2 * (c->nq + c->np) * limb_bytes(c); }
+size_t evk_bytes(const hks_ctx *c, u32 evk_digits) {
+    return (size_t)(evk_digits & ~HKS_EVK_PREPARED) * 2 * (c->nq + c->np) * limb_bytes(c);
+}
 
 // Fork / join of the context's side streams around the independent branches of one call.  join() -- also
 // run by the destructor when a branch returns an error -- records every forked side stream's join event and
@@ -447,6 +458,8 @@ extern "C" hks_status hks_ksk_inner_product(const hks_ctx *c, const uint64_t *ex
     if (level > c->L()) HKS_FAIL(HKS_EINVAL, "ksk_inner_product: level %u > L", level);
     if (galois != 1 && (st = check_galois(c, galois)) != HKS_OK) return st;
     if ((st = check_evk(c, evk_digits, level, "ksk_inner_product")) != HKS_OK) return st;
+    if (evk_prepared(evk_digits))   // hks_moddown would apply P^-1 a second time
+        HKS_FAIL(HKS_EINVAL, "ksk_inner_product: a prepared key (hks_evk_prepare) is for the fused calls only");
     const size_t lb = limb_bytes(c), ne = c->ne(level);
     if (overlap(ext, c->beta(level) * ne * lb, acc, 2 * ne * lb) || overlap(evk, evk_bytes(c, evk_digits), acc, 2 * ne * lb))
         HKS_FAIL(HKS_EINVAL, "ksk_inner_product: acc overlaps an input");
@@ -533,8 +546,9 @@ static hks_status keyswitch_impl(const hks_ctx *c, const uint64_t *c0, const uin
     }
     u64 *outs[2] = {out0, out1};
     const u64 *adds[2] = {c0, add1};
-    if (tensor) return moddown_core(c, acc, 2, level, outs, nullptr, nullptr, md, s, ymode, tensor);
-    return moddown_core(c, acc, 2, level, outs, adds, nullptr, md, s, ymode);
+    const bool prep = evk_prepared(evk_digits);
+    if (tensor) return moddown_core(c, acc, 2, level, outs, nullptr, nullptr, md, s, ymode, tensor, prep);
+    return moddown_core(c, acc, 2, level, outs, adds, nullptr, md, s, ymode, nullptr, prep);
 }
 
 extern "C" hks_status hks_hmult(const hks_ctx *c, const uint64_t *a0, const uint64_t *a1, const uint64_t *b0,
@@ -568,6 +582,20 @@ extern "C" hks_status hks_rescale(const hks_ctx *c, const uint64_t *x, uint32_t 
     std::vector<u64 *> outs(npoly);
     for (u32 p = 0; p < npoly; p++) outs[p] = out + (size_t)p * level * c->n;
     return run_rescale(c, npoly, level, x, coef, buf, outs.data(), s);
+}
+
+extern "C" hks_status hks_evk_prepare(const hks_ctx *c, const uint64_t *evk_in, uint32_t evk_digits, uint64_t *evk_out,
+                                      void *stream) {
+    hks_status st = check_ctx(c);
+    if (st != HKS_OK) return st;
+    if (!evk_in || !evk_out) HKS_FAIL(HKS_EINVAL, "evk_prepare: NULL key");
+    if (evk_digits & HKS_EVK_PREPARED) HKS_FAIL(HKS_EINVAL, "evk_prepare: the key is already prepared");
+    if (evk_digits == 0 || evk_digits > c->dnum)
+        HKS_FAIL(HKS_EKEY, "evk_prepare: key has %u digits (context dnum %u)", evk_digits, c->dnum);
+    const size_t b = evk_bytes(c, evk_digits);
+    if (evk_in != evk_out && overlap(evk_in, b, evk_out, b)) HKS_FAIL(HKS_EINVAL, "evk_prepare: partial overlap");
+    DevGuard g(c->device);
+    return launch_evk_prepare(c, evk_in, evk_out, evk_digits, (cudaStream_t)stream);
 }
 
 extern "C" hks_status hks_automorph(const hks_ctx *c, const uint64_t *in, uint32_t nlimbs, uint64_t galois,
@@ -638,7 +666,8 @@ extern "C" hks_status hks_rotate_hoisted(const hks_ctx *c, const uint64_t *c0, c
                 gal[2 * r] = galois[r0 + r];
                 gal[2 * r + 1] = 1;
             }
-            if ((st = moddown_core(c, acc, 2 * nr, level, outs.data(), adds.data(), gal.data(), md, bs)) != HKS_OK)
+            if ((st = moddown_core(c, acc, 2 * nr, level, outs.data(), adds.data(), gal.data(), md, bs, false, nullptr,
+                                   evk_prepared(evk_digits))) != HKS_OK)
                 return st;
         }
     }
@@ -717,7 +746,8 @@ extern "C" hks_status hks_rotate_hoisted_batch(const hks_ctx *c, uint32_t nct, c
             gal[2 * i] = galois[r];
             gal[2 * i + 1] = 1;
         }
-        if ((st = moddown_core(c, baccs, 2 * nct, level, outs.data(), adds.data(), gal.data(), bmd, bs)) != HKS_OK)
+        if ((st = moddown_core(c, baccs, 2 * nct, level, outs.data(), adds.data(), gal.data(), bmd, bs, false, nullptr,
+                               evk_prepared(evk_digits))) != HKS_OK)
             return st;
     }
     return fk.join("rotate_hoisted_batch");

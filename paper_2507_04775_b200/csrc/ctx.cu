@@ -106,7 +106,7 @@ hks_status upload(T **dptr, const std::vector<T> &h) {
 void free_tables(hks_ctx *c) {
     void *ptrs[] = {c->d_pc, c->d_tw_all, c->d_ninv,
                     c->d_mu_scale, c->d_mu_mat, c->d_md_scale, c->d_md_mat, c->d_pinv, c->d_mu_matf, c->d_md_matf, c->d_mu_mats, c->d_md_mats, c->d_mu_matb, c->d_md_matb, c->d_mu_img, c->d_md_img, c->d_ntt_img_fwd, c->d_ntt_img_inv,
-                    c->d_qmod, c->d_qlinv};
+                    c->d_qmod, c->d_qlinv, c->d_mdp_mat, c->d_mdp_mats, c->d_mdp_matf, c->d_mdp_matb, c->d_mdp_img};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < hks_ctx::NSIDE; i++) {
@@ -302,6 +302,19 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
         for (u32 k = 0; k < num_p; k++) P = mul_mod(P, p[k] % qi, qi);
         pinv[i] = sh(inv_mod(P, qi), qi);
     }
+    // hks_evk_prepare keys: ModDown matrix entries times P^-1 mod q_i (the epilogue then skips its P^-1 product)
+    std::vector<uint2> mdp_mat(md_mat.size());
+    std::vector<u64> mdp_matb(md_matb.size());
+    for (u32 k = 0; k < num_p; k++)
+        for (u32 i = 0; i < num_q; i++) {
+            const size_t e = (size_t)k * num_q + i;
+            const u64 hv = (u64)md_mat[e].x | ((u64)md_mat[e].y << 30);
+            const u64 hvp = mul_mod(hv, pinv[i].x, q[i]);
+            mdp_mat[e] = split(hvp);
+            std::vector<u64> w;
+            push_bytecols(w, hvp, q[i]);
+            std::copy(w.begin(), w.end(), mdp_matb.begin() + e * 8);
+        }
 
     // Rescale constants: q_j mod q_i (centered SwitchModulo from q_j into q_i) and
     // q_j^-1 mod q_i (Shoup), row j = the dropped limb, [L+1][L+1]; diagonal unused.
@@ -325,18 +338,18 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
         }
         return f;
     };
-    std::vector<double> mu_matf = limbs20(mu_mat), md_matf = limbs20(md_mat);
+    std::vector<double> mu_matf = limbs20(mu_mat), md_matf = limbs20(md_mat), mdp_matf = limbs20(mdp_mat);
     auto sums = [](const std::vector<uint2> &m) {
         std::vector<u32> f(m.size());
         for (size_t i = 0; i < m.size(); i++) f[i] = m[i].x + m[i].y;
         return f;
     };
-    std::vector<u32> mu_mats = sums(mu_mat), md_mats = sums(md_mat);
+    std::vector<u32> mu_mats = sums(mu_mat), md_mats = sums(md_mat), mdp_mats = sums(mdp_mat);
 
     // k_bconv_tc B-operand images (internal.h bconv_img_words): image word (t, kc, c, h) = matb word
     // (2kc + h, t, c), zero past the sources
     auto image = bconv_image;
-    std::vector<u64> mu_img, md_img;
+    std::vector<u64> mu_img, md_img, mdp_img;
     // Column-pass tables of the tensor-core NTT (log N = 16 only; R = C = 256; ntt_tc.cu).  The butterfly
     // stages of the pass (the same twiddles as k_ntt) are applied to unit vectors, giving the 16 x 16
     // matrices of its two rounds: forward = W_A (stages 0-3, any stride-16 class) then W_B[b] (stages 4-7,
@@ -424,6 +437,7 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
             image(mu_matb.data() + 8 * c->mu_mat_off[(size_t)lv * dnum + j], hi - lo, ntg, mu_img);
         }
     image(md_matb.data(), num_p, num_q, md_img);
+    image(mdp_matb.data(), num_p, num_q, mdp_img);
 
     hks_status st = HKS_OK;
 #define UP(dst, src) if (st == HKS_OK) st = upload(&c->dst, src)
@@ -465,11 +479,16 @@ extern "C" hks_status hks_ctx_create(uint32_t log_n, const uint64_t *q, uint32_t
     UP(d_md_scale, md_scale);
     UP(d_md_mat, md_mat);
     UP(d_pinv, pinv);
+    UP(d_mdp_mat, mdp_mat);
+    UP(d_mdp_mats, mdp_mats);
+    UP(d_mdp_img, mdp_img);
     if (HKS_EXPERIMENTAL) {   // tables of the FP64-assisted and warp-IMMA base conversions
         UP(d_mu_matf, mu_matf);
         UP(d_md_matf, md_matf);
         UP(d_mu_matb, mu_matb);
         UP(d_md_matb, md_matb);
+        UP(d_mdp_matf, mdp_matf);
+        UP(d_mdp_matb, mdp_matb);
     }
     UP(d_mu_mats, mu_mats);
     UP(d_mu_img, mu_img);

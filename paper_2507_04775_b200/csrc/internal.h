@@ -278,6 +278,13 @@ struct hks_ctx {
     // rounds of the column pass and the twist between them (ctx.cu, ntt_tc.cu)
     u64 *d_ntt_img_fwd = nullptr, *d_ntt_img_inv = nullptr;
     ulonglong2 *d_pinv = nullptr;       // P^-1 mod q_i  [L+1] (Shoup)
+    // the ModDown matrix with P^-1 folded in, [phat_k P^-1]_{q_i}, for keys from hks_evk_prepare (whose Q limbs
+    // carry the P^-1): the same layouts as d_md_mat / _mats / _matf / _matb / _img
+    uint2 *d_mdp_mat = nullptr;
+    u32 *d_mdp_mats = nullptr;
+    double *d_mdp_matf = nullptr;
+    u64 *d_mdp_matb = nullptr;
+    u64 *d_mdp_img = nullptr;
     u64 *d_qmod = nullptr;              // Rescale: q_j mod q_i  [L+1][L+1] (row j = dropped limb)
     ulonglong2 *d_qlinv = nullptr;      // Rescale: q_j^-1 mod q_i (Shoup)  [L+1][L+1]
 
@@ -417,7 +424,7 @@ struct ChunkIn {
 };
 hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, const std::vector<uint8_t> &poly,
                            const std::vector<MdOut> &outs, u64 *buf, const u64 *acc, cudaStream_t s,
-                           const u64 *const *tensor = nullptr, const ChunkIn *cin = nullptr);
+                           const u64 *const *tensor = nullptr, const ChunkIn *cin = nullptr, bool prepared = false);
 // Rescale of npoly polynomials (top limbs already COEFF in coef slots 0..npoly-1), see ntt.cu.
 hks_status run_rescale(const hks_ctx *ctx, u32 npoly, u32 level, const u64 *x, const u64 *coef, u64 *buf,
                        u64 *const *outs, cudaStream_t s);
@@ -431,6 +438,7 @@ bool bconv_tc_large(u32 log_n, u32 ngroups);
 // out[i] = in[i] * w_i mod p_i (canonical) for n <= 16 limbs (hks_bconv's y_i = x_i [qhat_i]^-1)
 // dw (device): w[0..nl) then the Shoup companions wp[0..nl); p (host): the limbs' primes
 hks_status launch_limb_scale(const u64 *in, u64 *out, u32 nl, const u64 *dw, const u64 *p, u32 log_n, cudaStream_t s);
+hks_status launch_evk_prepare(const hks_ctx *c, const u64 *in, u64 *out, u32 ndig, cudaStream_t s);
 // hks_bconv's Eq. 1 constants for one (src, dst) pair, derived on the device (kernels.cu k_bconv_prep):
 // w = [qhat_i^-1]_{q_i} and Shoup companions (2 nsrc words), mat [nsrc][ndst] (lo30, hi30) of [qhat_i]_t,
 // the k_bconv_tc B image img [ndst][bconv_img_words(nsrc)]

@@ -627,6 +627,48 @@ hks_status launch_limb_scale(const u64 *in, u64 *out, u32 nl, const u64 *dw, con
     return HKS_OK;
 }
 
+// hks_evk_prepare: key limb t < nq (the Q limbs of every digit and both components) times [P^-1]_{q_t}
+// (canonical Shoup product), the P limbs copied; elementwise, so in place is allowed.
+struct EvkPrepArgs {
+    const u64 *in;
+    u64 *out;
+    const ulonglong2 *pinv;    // [nq] (P^-1 mod q_t, Shoup companion)
+    const PrimeConst *pc;
+    u32 nq, nk, log_n;
+};
+__global__ void __launch_bounds__(256) k_evk_prepare(const __grid_constant__ EvkPrepArgs A) {
+    pdl_trigger();
+    pdl_wait();
+    const size_t N = (size_t)1 << A.log_n;
+    const u32 limb = blockIdx.y, t = limb % A.nk;
+    const size_t x = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    if (x >= N) return;
+    const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(A.in + limb * N + x);
+    ulonglong2 r = v;
+    if (t < A.nq) {
+        const ulonglong2 w = A.pinv[t];
+        const u64 p = A.pc[t].p;
+        r = make_ulonglong2(shoup(v.x, w.x, w.y, p), shoup(v.y, w.x, w.y, p));
+    }
+    *reinterpret_cast<ulonglong2 *>(A.out + limb * N + x) = r;
+}
+
+hks_status launch_evk_prepare(const hks_ctx *c, const u64 *in, u64 *out, u32 ndig, cudaStream_t s) {
+    EvkPrepArgs a{};
+    a.in = in;
+    a.out = out;
+    a.pinv = c->d_pinv;
+    a.pc = c->d_pc;
+    a.nq = c->nq;
+    a.nk = c->nq + c->np;
+    a.log_n = c->log_n;
+    const size_t N = (size_t)1 << c->log_n;
+    const u32 bx = (u32)std::max<size_t>(1, N / 2 / 256);
+    (void)hks_launch(k_evk_prepare, dim3(bx, 2 * ndig * a.nk), dim3(256), 0, s, a);
+    HKS_CHECK_LAUNCH();
+    return HKS_OK;
+}
+
 // hks_bconv's constants for an arbitrary (src, dst) prime pair (Eq. 1, §3.6.3), built on
 // the device so that the generic entry point needs no host->device copy (graph-capturable):
 //   thread (i, u), i < 4 ceil(nsrc / 4):  v = [qhat_i]_{t_u} = prod_{k != i} q_k mod t_u -> mat (30-bit

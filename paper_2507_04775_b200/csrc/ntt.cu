@@ -149,12 +149,19 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
     ulonglong2 pinv = make_ulonglong2(0, 0);
     const u64 *ea = nullptr, *eb = nullptr;
     if (MD) {
-        pinv = A.pinv[prime];
+        if (A.pinv) pinv = A.pinv[prime];
         ea = A.ea + (size_t)A.map.sa[b] * N + sub_off;
         const u64 *ebase = A.adds[ob];
         eb = (EPI == EPI_MODDOWN && ebase && A.map.sb[b] != 0xffff) ? ebase + (size_t)A.map.sb[b] * N : nullptr;
     }
     const u64 galois = MD ? A.ogal[ob] : 1;
+    // ModDown core (a - x) P^-1, a canonical, x < 8p + 2^32; A.pinv == NULL: the key was prepared with P^-1 on
+    // its Q limbs and P^-1 folded into the conversion matrix (hks_evk_prepare), so (a - x) is already the value
+    auto md_sub = [&](u64 a, u64 x) -> u64 {
+        const u64 d = a + m.eight_p + m.p - x;   // < 10p
+        if (A.pinv) return csub(csub(shoup_approx(d, pinv.x, pinv.y, m.np), m.two_p), m.p);
+        return csub(csub(csub(csub(d, m.eight_p), m.four_p), m.two_p), m.p);
+    };
     // EPI_SWITCH: the column pass loads the source-modulus COEFF limb and switches it into this prime
     const u64 sw_m = EPI == EPI_SWITCH ? A.sw_qmod[prime] : 0;
     auto epi = [&](u64 x, int j) -> u64 {
@@ -162,8 +169,7 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
         if (EPI == EPI_SCALE || EPI == EPI_SCALE_COUT) return csub(csub(shoup_approx(x, sc.x, sc.y, m.np), m.two_p), m.p);
         if (EPI == EPI_CANON) return canon8(x, m);
         // EPI_MODDOWN: (a - x) * P^-1 [+ b], a canonical, x < 8p + 2^32
-        u64 r = shoup_approx(ea[(size_t)j * JS] + m.eight_p + m.p - x, pinv.x, pinv.y, m.np);
-        r = csub(csub(r, m.two_p), m.p);
+        u64 r = md_sub(ea[(size_t)j * JS], x);
         if (eb) {
             const u32 xg = (u32)(sub_off + (size_t)j * JS);
             r = csub(r + eb[galois == 1 ? xg : automorph_src(xg, log_n, galois)], m.p);
@@ -345,8 +351,7 @@ __device__ __forceinline__ void ntt_tile(const NttArgs &A, const u32 b, const u3
                 if (EPI == EPI_CANON) {
                     x = canon8(x, m);
                 } else if (MD) {
-                    u64 rr2 = shoup_approx(av[q] + m.eight_p + m.p - x, pinv.x, pinv.y, m.np);
-                    rr2 = csub(csub(rr2, m.two_p), m.p);
+                    u64 rr2 = md_sub(av[q], x);
                     if (eb) rr2 = csub(rr2 + bv[q], m.p);
                     if (EPI == EPI_MDTENSOR) {
                         // HMult: + a0 b0 (role 0) or + a0 b1 + a1 b0 (role 1)
@@ -763,7 +768,7 @@ hks_status run_ntt_inv_cols(const hks_ctx *ctx, const LimbList &L, const u64 *in
 
 hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, const std::vector<uint8_t> &poly,
                            const std::vector<MdOut> &outs, u64 *buf, const u64 *acc, cudaStream_t s,
-                           const u64 *const *tensor, const ChunkIn *cin) {
+                           const u64 *const *tensor, const ChunkIn *cin, bool prepared) {
     size_t off = 0;
     while (off < L.size()) {
         // one launch: at most HKS_MAXB limbs spanning at most NTT_MAXO polynomials
@@ -781,7 +786,7 @@ hks_status run_ntt_moddown(const hks_ctx *ctx, const LimbList &L, const std::vec
         NttArgs a{};
         a.pc = ctx->d_pc;
         a.ninv = ctx->d_ninv;
-        a.pinv = ctx->d_pinv;
+        a.pinv = prepared ? nullptr : ctx->d_pinv;
         a.galois = 1;
         // pass 0: columns, in place on buf (slots sin) -- or from the chunked input
         for (u32 i = 0; i < cnt; i++) {

@@ -21,7 +21,7 @@ MAX_DIGITS = 64
 # every symbol include/hks.h declares (checked by tests/test_capi.py)
 EXPORTS = ("hks_last_error", "hks_ctx_create", "hks_ctx_destroy", "hks_ctx_query", "hks_ctx_psi",
            "hks_workspace_bytes", "hks_ntt_fwd", "hks_ntt_inv", "hks_bconv", "hks_bconv_workspace_bytes", "hks_modup",
-           "hks_ksk_inner_product", "hks_moddown", "hks_keyswitch", "hks_relinearize", "hks_hmult", "hks_rescale",
+           "hks_ksk_inner_product", "hks_moddown", "hks_evk_prepare", "hks_keyswitch", "hks_relinearize", "hks_hmult", "hks_rescale",
            "hks_pt_weighted_sum", "hks_linear_transform", "hks_linear_transform_workspace_bytes",
            "hks_automorph",
            "hks_rotate_hoisted", "hks_rotate_hoisted_batch", "hks_rotate_hoisted_batch_workspace_bytes",
@@ -92,6 +92,7 @@ def lib() -> ctypes.CDLL:
         L.hks_ksk_inner_product.argtypes = [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp]
         L.hks_moddown.argtypes = [_vp, _vp, _u32, _vp, _vp, _vp]
         L.hks_keyswitch.argtypes = [_vp, _vp, _vp, _u32, _vp, _u32, _vp, _vp, _vp, _vp]
+        L.hks_evk_prepare.argtypes = [_vp, _vp, _u32, _vp, _vp]
         L.hks_automorph.argtypes = [_vp, _vp, _u32, _u64, _vp, _vp]
         L.hks_relinearize.argtypes = [_vp, _vp, _vp, _vp, _u32, _vp, _u32, _vp, _vp, _vp, _vp]
         L.hks_hmult.argtypes = [_vp, _vp, _vp, _vp, _vp, _u32, _vp, _u32, _vp, _vp, _vp, _vp]
@@ -161,13 +162,41 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
+HKS_EVK_PREPARED = 0x10000   # include/hks.h: evk_digits flag of a key from hks_evk_prepare
+
+
+class PreparedKey:
+    """A key returned by evk_prepare: the device tensor [digits][2][L+1+K][N] and the flag every key-taking call
+    passes with its digit count (HKS_EVK_PREPARED)."""
+
+    def __init__(self, tensor):
+        self.tensor = tensor
+        self.shape = tensor.shape
+
+    def data_ptr(self) -> int:
+        return self.tensor.data_ptr()
+
+
 def evk_digits(ctx, evk) -> int:
     """Digit count of a key passed to libhks: the leading dimension of a [digits][2][L+1+K][N] tensor, or
-    of the first of a list of keys; a raw address carries none, so the context's dnum is assumed."""
+    of the first of a list of keys; a raw address carries none, so the context's dnum is assumed.  A
+    PreparedKey (or a list of them) adds HKS_EVK_PREPARED."""
     if isinstance(evk, (list, tuple)):
+        flags = {isinstance(e, PreparedKey) for e in evk}
+        if len(flags) > 1:
+            raise ValueError("hks: a call takes either prepared keys or plain keys, not both")
         return min((evk_digits(ctx, e) for e in evk), default=ctx.dnum)
     shape = getattr(evk, "shape", None)
-    return int(shape[0]) if shape is not None and len(shape) == 4 else ctx.dnum
+    d = int(shape[0]) if shape is not None and len(shape) == 4 else ctx.dnum
+    return d | HKS_EVK_PREPARED if isinstance(evk, PreparedKey) else d
+
+
+def evk_prepare(ctx: "Context", evk, out=None, stream=None) -> PreparedKey:
+    """hks_evk_prepare: the key's Q limbs times P^-1 (in place when out is None or out is evk)."""
+    dst = evk if out is None else out
+    _check(lib().hks_evk_prepare(ctx.handle, _ptr(evk), evk_digits(ctx, evk), _ptr(dst), _stream(stream)),
+           "hks_evk_prepare")
+    return PreparedKey(dst)
 
 
 def _stream(stream):

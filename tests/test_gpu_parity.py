@@ -771,3 +771,63 @@ def test_hoisted_and_bsgs_under_profiling(orc):
     w0, w1 = o.rotate_hoisted(c0, c1, evks, level, ks)
     for r in range(len(ks)):
         assert (to_host(outs0[r]) == w0[r]).all() and (to_host(outs1[r]) == w1[r]).all(), r
+
+
+# ------------------------------------------------------------------ prepared keys (hks_evk_prepare)
+
+@pytest.mark.parametrize("name,levels", [("C2", [29, 19, 9, 0]), ("T12", [6, 3, 0]), ("C1p", [2, 0]), ("T16s", [5, 1])])
+def test_prepared_key_keyswitch_parity(orc, name, levels):
+    """include/hks.h hks_evk_prepare (optional): a key with P^-1 on its Q limbs and the
+    P^-1-folded ModDown matrix give the oracle's KeySwitch bit for bit -- the oracle is unchanged, so this is
+    the same pin as every KeySwitch parity test (fused path at beta <= 4, and the small configs)."""
+    cfg, ctx, o = ctxs(orc, name)
+    keys, evk = relin_key(o, name)
+    pk = H.evk_prepare(ctx, to_dev(evk), out=empty_dev(evk.shape))
+    prep = to_host(pk.tensor)
+    assert not (prep == evk).all()                         # the Q limbs did change
+    assert (prep[:, :, o.nq:] == evk[:, :, o.nq:]).all()   # the P limbs did not
+    g = S.rng(cfg.seed + 300)
+    for level in levels:
+        c0 = S.uniform_limbs(g, o.q[: level + 1], o.n)
+        c1 = edge_limbs(o.q[: level + 1], o.n, g)
+        got0, got1 = run_ks(ctx, c0, c1, level, pk)
+        want0, want1 = o.keyswitch(c0, c1, evk, level)
+        assert (got0 == want0).all() and (got1 == want1).all(), level
+
+
+def test_prepared_key_hmult_rotations_and_errors(orc):
+    """The prepared key through HMult (tensor terms after the ModDown core), hoisted rotations (batched
+    ModDowns with per-rotation outputs) and the in-place form; the step-level key product and a second
+    preparation refuse it."""
+    cfg, ctx, o = ctxs(orc, "T12")
+    keys, evk = relin_key(o, "T12")
+    level = 5
+    g = S.rng(cfg.seed + 310)
+    qs = o.q[: level + 1]
+    a0, a1, b0, b1 = (S.uniform_limbs(g, qs, o.n) for _ in range(4))
+    pk = H.evk_prepare(ctx, to_dev(evk))                   # in place
+    got0, got1 = run_hmult(ctx, a0, a1, b0, b1, level, pk)
+    want0, want1 = o.hmult(a0, a1, b0, b1, evk, level)
+    assert (got0 == want0).all() and (got1 == want1).all()
+    rk = Keys(o, cfg.seed + 11)
+    ks = [S.galois_rot(r, cfg.log_n) for r in (1, 2, 5)]
+    evks = [rk.rot(k) for k in ks]
+    pks = [H.evk_prepare(ctx, to_dev(e)) for e in evks]
+    m, c0, c1 = encrypt_under(o, g, rk.s_eval, level, 20)
+    outs0 = [empty_dev(c0.shape) for _ in ks]
+    outs1 = [empty_dev(c0.shape) for _ in ks]
+    H.rotate_hoisted(ctx, to_dev(c0), to_dev(c1), level, ks, pks, outs0, outs1,
+                     ctx.workspace(H.OP_ROTATE_HOISTED, level, len(ks)))
+    w0, w1 = o.rotate_hoisted(c0, c1, evks, level, ks)
+    for r in range(len(ks)):
+        assert (to_host(outs0[r]) == w0[r]).all() and (to_host(outs1[r]) == w1[r]).all(), r
+    with pytest.raises(ValueError):
+        H.evk_digits(ctx, [pks[0], to_dev(evks[1])])
+    ext = empty_dev((o.dnum, level + 1 + o.np, o.n))
+    acc = empty_dev((2, level + 1 + o.np, o.n))
+    with pytest.raises(H.HksError) as ei:
+        H.ksk_inner_product(ctx, ext, pk, level, 1, acc)
+    assert ei.value.status == 1
+    with pytest.raises(H.HksError) as ei:
+        H.evk_prepare(ctx, pk)
+    assert ei.value.status == 1
