@@ -85,6 +85,12 @@ static thread_local const cudaAccessPolicyWindow *t_win = nullptr;
 #ifndef HKS_KIP_OPQ
 #define HKS_KIP_OPQ 0     // the same for the fused kernel's ModDown inverse row pass
 #endif
+#ifndef HKS_ROW_L2PF
+#define HKS_ROW_L2PF 3    // row passes bulk-prefetch their tile's twiddle rows into L2 before griddepcontrol.wait:
+#endif                    // 1 inverse, 2 all, 3 forward (ModDown row pass 37.3 -> 35.5 us; the inverse pass loses)
+#ifndef HKS_ROW_L2PF_EPI
+#define HKS_ROW_L2PF_EPI 1   // the ModDown row pass also prefetches its epilogue operands (acc, c0) into L2
+#endif
 #ifndef HKS_ROW_WSYNC
 #define HKS_ROW_WSYNC 1   // row passes: a row never straddles a warp, so the exchanges between rounds (and the
 #endif                    // staged tile load / copy-out, mapped warp by warp) need __syncwarp, not CTA barriers
@@ -380,6 +386,27 @@ k_ntt(const __grid_constant__ NttArgs A) {
     pdl_trigger();
     const u32 b = blockIdx.x / A.tiles, tile = blockIdx.x - b * A.tiles;
     constexpr bool TWS = row_tws<LOGN, LOGE, LOGNB, COLS>();
+#if HKS_ROW_L2PF
+    if (!COLS && !TWS && (HKS_ROW_L2PF == 2 || (HKS_ROW_L2PF == 1 && !FWD) || (HKS_ROW_L2PF == 3 && FWD)) &&
+        threadIdx.x == 0) {
+        // this tile's per-row twiddle tables (context data, contiguous) requested into L2 before griddepcontrol.wait
+        const ulonglong2 *t = A.tw + (((size_t)A.map.prime[b] << A.log_r) + ((size_t)tile << LOGNB)) * (1 << LOGN);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(t), "r"((u32)(16u << (LOGN + LOGNB))) : "memory");
+        if (HKS_ROW_L2PF_EPI && (EPI == EPI_MODDOWN || EPI == EPI_MDTENSOR)) {
+            // the ModDown epilogue's accumulator and c0 rows of this tile: L2 is the coherence point, so a prefetch
+            // is safe even before griddepcontrol.wait (it moves no data into the SM)
+            const size_t N = (size_t)1 << A.log_n, off = ((size_t)tile << LOGNB) << LOGN;
+            const u32 bytes = 8u << (LOGN + LOGNB);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.ea + (size_t)A.map.sa[b] * N + off), "r"(bytes)
+                         : "memory");
+            const u32 ob = A.map.ob[b];
+            if (EPI == EPI_MODDOWN && A.adds[ob] && A.map.sb[b] != 0xffff && A.ogal[ob] == 1)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.adds[ob] + (size_t)A.map.sb[b] * N + off),
+                             "r"(bytes)
+                             : "memory");
+        }
+    }
+#endif
     ulonglong2 *tws = nullptr;
     if (TWS) {
         constexpr int NT = (1 << LOGNB) << (LOGN - LOGE), NE = 1 << (LOGN + LOGNB);
