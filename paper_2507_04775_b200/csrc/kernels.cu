@@ -353,6 +353,9 @@ static void bconv_mma_go(const BconvArgs &a, cudaStream_t s) {
 #ifndef HKS_TC_SA
 #define HKS_TC_SA 2
 #endif
+#ifndef HKS_TC_MAXREG
+#define HKS_TC_MAXREG 0
+#endif
 #ifndef HKS_TC_EPW
 #define HKS_TC_EPW 16
 #endif
@@ -372,7 +375,11 @@ extern "C" void *hks_debug_bc_trace() {
 #define BC_T(ev, j) do { } while (0)
 #endif
 template <int NSRC, bool LAZY>
+#if HKS_TC_MAXREG   // a register cap below the full register file: room for other kernels' CTAs on the SM
+__global__ void __maxnreg__(HKS_TC_MAXREG) k_bconv_tc(const __grid_constant__ BconvArgs A) {
+#else
 __global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constant__ BconvArgs A) {
+#endif
     pdl_trigger();
     if (threadIdx.x == 0) BC_T(5, 0);
     constexpr int KPAD = 32 * ((NSRC + 3) / 4);   // bytes of K (whole K = 32 MMA steps)
@@ -492,9 +499,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constan
         // wait per tile (the accumulator is released before the reductions), so that eight independent
         // reductions are in flight per thread
         constexpr u32 NH = TC_EPW / 4;           // warps sharing a TMEM lane quarter
+        constexpr u32 NCH = ((32 + NH - 1) / NH + 7) / 8;   // 8-target chunks of a run (1 at 16 epilogue warps)
         const u32 q = warp & 3, h = warp >> 2;
         const u32 lrow = q * 32 + lane;           // TMEM lane = coefficient row of the tile
-        const u32 tpw = (nt + NH - 1) / NH;       // <= 8 (nt <= 32, NH = 4)
+        const u32 tpw = (nt + NH - 1) / NH;       // <= 8 NCH (nt <= 32)
         const u32 tb0 = h * tpw, tcnt = nt > tb0 ? min(tpw, nt - tb0) : 0;
         // per-target reduction constants and output limbs of this run, written by the run's quarter-0 warp and
         // shared with the other three lane quarters through a named barrier (ids 2 + h): the global loads
@@ -512,6 +520,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constan
             if (warp == 0 && lane == 0) BC_T(3, j);
             tc_fence_after();
             const size_t x = ((size_t)(blockIdx.x + j * gridDim.x) << 7) + lrow;
+            if (NCH == 1) {
             const u32 tbase = tmem + b * 256 + ((q * 32) << 16) + tb0 * 8;
             u32 v[2][32];
             if (tcnt > 0) tc_ld32(tbase, v[0]);
@@ -538,6 +547,43 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_bconv_tc(const __grid_constan
 #pragma unroll
                 for (int kk = 0; kk < 4; kk++)
                     if ((u32)(4 * hh + kk) < tcnt) *dp[kk] = o[kk];
+            }
+            } else {   // fewer epilogue warps (HKS_TC_EPW < 16): the run is reduced in chunks of eight targets
+#pragma unroll 1
+            for (u32 ch = 0; ch < NCH; ch++) {
+                const u32 cb = tb0 + 8 * ch;   // first target of this chunk
+                const u32 ccnt = tcnt > 8 * ch ? min(8u, tcnt - 8 * ch) : 0u;
+                const u32 tbase = tmem + b * 256 + ((q * 32) << 16) + cb * 8;
+                u32 v[2][32];
+                if (ccnt > 0) tc_ld32(tbase, v[0]);
+                if (ccnt > 4) tc_ld32(tbase + 32, v[1]);
+                tc_wait_ld();
+                if (ch == NCH - 1) {   // the accumulator is released once its last chunk is in registers
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(smem_u32(&bar_empty[b]));
+                }
+                // branch-free over the eight slots (a slot past the run reduces target cb again and is not
+                // stored), so that the eight reductions interleave instead of running one predicated block after
+                // another
+#pragma unroll
+                for (int hh = 0; hh < 2; hh++) {
+                    u64 o[4];
+                    u64 *dp[4];
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++) {
+                        const u32 k = 4 * hh + kk;
+                        const u32 t = min(cb + (k < ccnt ? k : 0u), 31u);
+                        const ulonglong2 c = sred[t];
+                        const u32 *r = &v[hh][8 * kk];
+                        o[kk] = bytesum_reduce_c<LAZY>(r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7], c.x, (u32)c.y);
+                        dp[kk] = sdst[t] + x;
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++)
+                        if ((u32)(4 * hh + kk) < ccnt) *dp[kk] = o[kk];
+                }
+            }
             }
             if (warp == 0 && lane == 0) BC_T(4, j);
         }
