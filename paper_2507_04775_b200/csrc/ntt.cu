@@ -1441,6 +1441,9 @@ static hks_status go_kip_d(FusedKipArgs &a, cudaStream_t s) {
 #ifndef HKS_KIP_LOGNB
 #define HKS_KIP_LOGNB 1   // 2 rows per CTA: many small CTAs keep the three phases of co-resident CTAs staggered
 #endif                    // (measured: 4 rows 98.7 us, 2 rows 96.5 us per C2 KeySwitch)
+#ifndef HKS_KIP_LOGNB16
+#define HKS_KIP_LOGNB16 2 // at N = 2^16, with per-warp row barriers: 4 rows per CTA (the same 86.3 us per launch alone,
+#endif                    // C2 4 938 -> 4 984 KS/s with three concurrent KeySwitches; at N = 2^17 slower: 2 rows kept)
 hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s) {
     t_win = &ctx->tw_win;
     a.log_n = ctx->log_n;
@@ -1450,7 +1453,7 @@ hks_status launch_ntt_kip(const hks_ctx *ctx, FusedKipArgs &a, cudaStream_t s) {
         HKS_FAIL(HKS_EINVAL, "ntt_kip: %u digits (%u transformed) / %u limbs per launch", a.ndig, a.ntr, a.nu);
     switch (ctx->log_n) {
         case 17: return go_kip_d<8, 4, HKS_KIP_LOGNB>(a, s);
-        case 16: return go_kip_d<8, HKS_KIP_LOGE, HKS_KIP_LOGNB>(a, s);
+        case 16: return go_kip_d<8, HKS_KIP_LOGE, HKS_KIP_LOGNB16>(a, s);
         case 15: return go_kip_d<7, 4, 3>(a, s);
         case 14: return go_kip_d<7, 4, 3>(a, s);
         case 13: return go_kip_d<6, 3, 3>(a, s);

@@ -20,7 +20,7 @@ KERNELS = [
     ("_Z5k_nttILi8ELi4ELi3ELi8ELb1ELb0ELi3EEv7NttArgs", "ntt_inv_cols_scale", "INTT column pass + Eq. 1 / ModDown scale"),
     ("_Z10k_bconv_tcILi10ELb1EEv9BconvArgs", "bconv", "ModUp / ModDown base conversion (Eq. 1) on tcgen05"),
     ("_Z5k_nttILi8ELi4ELi4ELi8ELb1ELb1ELi0EEv7NttArgs", "ntt_fwd_cols", "NTT column pass, 90-limb batch (CT, radix-16)"),
-    ("_Z9k_ntt_kipILi8ELi4ELi1ELi3ELi3EEv12FusedKipArgs", "ntt_rows_kip", "NTT row pass + key inner product + ModDown INTT rows"),
+    ("_Z9k_ntt_kipILi8ELi4ELi2ELi3ELi3EEv12FusedKipArgs", "ntt_rows_kip", "NTT row pass + key inner product + ModDown INTT rows"),
     ("_Z5k_nttILi8ELi3ELi3ELi8ELb0ELb1ELi2EEv7NttArgs", "ntt_fwd_rows_moddown", "NTT row pass + (acc - x) P^-1 + c0 epilogue"),
 ]
 OPS = ["UTCIMMA", "LDTM", "UTMALDG", "UBLKCP", "LDGSTS", "IMAD.WIDE.U32", "IMAD.HI.U32", "IMAD", "IMAD.X",
